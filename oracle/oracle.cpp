@@ -1,0 +1,385 @@
+// ============================================================================
+// OmniMoE layer-forward ORACLE -- test infrastructure, NOT the product.
+//
+// Plain, slow, obviously-correct CPU implementation (C++17, fp64) of what the
+// OmniMoE atomic-expert layer forward computes (arXiv 2602.05711, PAPER.md).
+// Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+// --impl reference leg may load this library.  It shares no code, header or
+// constant with the CUDA path (paper_2602_05711_b200/csrc) and includes no
+// CUDA header.
+//
+// Citations: "PAPER:n" = /root/reference/PAPER.md line n (section / equation
+// named alongside); "Q#" = a reading listed in DESIGN.md "Readings".
+//
+// Pins: every function below is pinned by tests/test_oracle_*.py (-m "not gpu")
+// against closed forms, brute force, invariants and SPEC worked examples,
+// EXCEPT absolute layer outputs at paper scale, which the paper never prints:
+// "parity unpinned" for absolute values (P12) -- only the
+// composition of individually pinned steps vouches for them.
+// ============================================================================
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <numeric>
+#include <thread>
+#include <vector>
+
+namespace {
+
+// --------------------------------------------------------------------------
+// Exact key of a grid cell: the exact real s_r[i] + s_c[j] (Eq.S, PAPER:220-224,
+// ranked on raw logits per reading Q8), represented as the TwoSum pair
+// (hi, lo): hi = RN64(s_r + s_c), lo = exact residual.  Lexicographic order on
+// (hi, lo) is the order of the exact reals.  Ties between EXACTLY equal keys
+// go to the smaller flat id n = i*N_c + j (reading Q7).
+// --------------------------------------------------------------------------
+struct Key {
+  double hi, lo;
+  int64_t n;  // flat expert id
+};
+
+inline Key make_key(float sr, float sc, int64_t n) {
+  double a = (double)sr, b = (double)sc;
+  double hi = a + b;
+  double bb = hi - a;
+  double lo = (a - (hi - bb)) + (b - bb);  // Knuth TwoSum: exact residual
+  return Key{hi, lo, n};
+}
+
+// true iff p precedes q in the total order (larger exact key first, then
+// smaller flat id).
+inline bool precedes(const Key& p, const Key& q) {
+  if (p.hi != q.hi) return p.hi > q.hi;
+  if (p.lo != q.lo) return p.lo > q.lo;
+  return p.n < q.n;
+}
+
+inline double silu(double z) { return z / (1.0 + std::exp(-z)); }  // reading Q1
+
+inline double act_fn(double z, int act) { return act == 1 ? z : silu(z); }
+
+template <class F>
+void parallel_for(int64_t n, int nthreads, F f) {
+  if (nthreads <= 1 || n <= 1) {
+    for (int64_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  int64_t chunk = (n + nthreads - 1) / nthreads;
+  for (int t = 0; t < nthreads; ++t) {
+    int64_t b = t * chunk, e = std::min<int64_t>(n, b + chunk);
+    if (b >= e) break;
+    th.emplace_back([=]() { for (int64_t i = b; i < e; ++i) f(i); });
+  }
+  for (auto& t : th) t.join();
+}
+
+// Per-token-head routing result in the order of the total order above.
+struct RouteOut {
+  std::vector<Key> top;  // first min(K+1, N) keys
+};
+
+// O3 brute force (Eq.TopK): score every one of the N grid
+// cells, order all of them, keep the first K+1 (the extra one gives the gap).
+void select_bruteforce(const float* sr, int64_t Nr, const float* sc, int64_t Nc, int64_t K,
+                       std::vector<Key>& out) {
+  std::vector<Key> all;
+  all.reserve(Nr * Nc);
+  for (int64_t i = 0; i < Nr; ++i)
+    for (int64_t j = 0; j < Nc; ++j) all.push_back(make_key(sr[i], sc[j], i * Nc + j));
+  int64_t keep = std::min<int64_t>(K + 1, Nr * Nc);
+  std::partial_sort(all.begin(), all.begin() + keep, all.end(), precedes);
+  out.assign(all.begin(), all.begin() + keep);
+}
+
+// O4 product selection: order rows by (s_r desc, i asc) and columns by
+// (s_c desc, j asc); a cell with 1-based ranks (a, b) has at least a*b - 1
+// predecessors, so only cells with a*b <= K+1 can be among the first K+1
+// (the north star's k x k candidate grid is a
+// superset).  Candidates are ordered exactly like brute force.
+void select_product(const float* sr, int64_t Nr, const float* sc, int64_t Nc, int64_t K,
+                    std::vector<Key>& out) {
+  std::vector<int64_t> ri(Nr), ci(Nc);
+  std::iota(ri.begin(), ri.end(), 0);
+  std::iota(ci.begin(), ci.end(), 0);
+  std::sort(ri.begin(), ri.end(), [&](int64_t p, int64_t q) {
+    return sr[p] != sr[q] ? sr[p] > sr[q] : p < q;
+  });
+  std::sort(ci.begin(), ci.end(), [&](int64_t p, int64_t q) {
+    return sc[p] != sc[q] ? sc[p] > sc[q] : p < q;
+  });
+  int64_t K1 = K + 1;
+  std::vector<Key> cand;
+  for (int64_t a = 1; a <= std::min(K1, Nr); ++a)
+    for (int64_t b = 1; b <= std::min(K1, Nc) && a * b <= K1; ++b) {
+      int64_t i = ri[a - 1], j = ci[b - 1];
+      cand.push_back(make_key(sr[i], sc[j], i * Nc + j));
+    }
+  int64_t keep = std::min<int64_t>(K1, Nr * Nc);
+  std::partial_sort(cand.begin(), cand.begin() + keep, cand.end(), precedes);
+  out.assign(cand.begin(), cand.begin() + keep);
+}
+
+// Paper App. A "Block-wise Merge Selection": partition the N
+// flat ids into blocks of B_sel, score each block on the fly, take its local
+// top by iterative max-reduction, merge into a running global top buffer by
+// insertion.  Kept only as a cross-check of the two selectors above.
+void select_blockmerge(const float* sr, int64_t Nr, const float* sc, int64_t Nc, int64_t K,
+                       int64_t B_sel, std::vector<Key>& out) {
+  int64_t N = Nr * Nc, K1 = std::min<int64_t>(K + 1, N);
+  std::vector<Key> global;  // sorted by precedes, size <= K1
+  for (int64_t b0 = 0; b0 < N; b0 += B_sel) {
+    int64_t b1 = std::min(N, b0 + B_sel);
+    std::vector<Key> blk;
+    for (int64_t n = b0; n < b1; ++n) blk.push_back(make_key(sr[n / Nc], sc[n % Nc], n));
+    std::vector<char> taken(blk.size(), 0);
+    for (int64_t r = 0; r < std::min<int64_t>(K1, (int64_t)blk.size()); ++r) {  // iterative max
+      int64_t best = -1;
+      for (int64_t t = 0; t < (int64_t)blk.size(); ++t)
+        if (!taken[t] && (best < 0 || precedes(blk[t], blk[best]))) best = t;
+      taken[best] = 1;
+      // insertion into the global buffer
+      Key k = blk[best];
+      auto pos = std::upper_bound(global.begin(), global.end(), k, precedes);
+      global.insert(pos, k);
+      if ((int64_t)global.size() > K1) global.pop_back();
+    }
+  }
+  out = global;
+}
+
+}  // namespace
+
+extern "C" {
+
+// O1 canonical logits (Eq.Logits; reading Q9): for each token
+// l, head h and sub-key row r (rows [0,N_r) are W_r's columns, rows
+// [N_r, N_r+N_c) are W_c's), acc = sum_k x[l][k]*sub[h][r][k] accumulated
+// sequentially in double, then rounded to fp32 (round-to-nearest-even).
+void oracle_logits(int64_t L, int64_t d, int64_t h, int64_t R, const double* x, const double* sub,
+                   float* out, int nthreads) {
+  parallel_for(L, nthreads, [&](int64_t l) {
+    for (int64_t hh = 0; hh < h; ++hh)
+      for (int64_t r = 0; r < R; ++r) {
+        const double* xr = x + l * d;
+        const double* sw = sub + (hh * R + r) * d;
+        double acc = 0.0;
+        for (int64_t k = 0; k < d; ++k) acc += xr[k] * sw[k];
+        out[(l * h + hh) * R + r] = (float)acc;
+      }
+  });
+}
+
+// O2-O5 routing for a batch of token-heads (Eq.TopK + Eq.Gate, PAPER:131-139;
+// Eq.S).  logits: [T][N_r + N_c] fp32 (T = L*h token-heads).
+// method: 0 brute force, 1 product, 2 block-merge (B_sel = bsel).
+// Outputs per token-head t (K entries in the total order):
+//   idx[t][k]    flat expert id
+//   gate[t][k]   g_k = exp(kappa_k - kappa_1) / sum_k' exp(kappa_k' - kappa_1)
+//                (softmax over the selected keys only; Q11)
+//   score[t][k]  kappa_k - lse_r - lse_c = p_r[i] + p_c[j] (Eq.LSM + Eq.S; Q8)
+//   key_hi/key_lo[t][k] exact key pair, gap[t] = kappa_K - kappa_{K+1}
+//                (+inf when K == N)
+void oracle_route(int64_t T, int64_t Nr, int64_t Nc, int64_t K, const float* logits, int method,
+                  int64_t bsel, int nthreads, int32_t* idx, double* gate, double* score,
+                  double* key_hi, double* key_lo, double* gap) {
+  int64_t R = Nr + Nc;
+  parallel_for(T, nthreads, [&](int64_t t) {
+    const float* sr = logits + t * R;
+    const float* sc = sr + Nr;
+    std::vector<Key> top;
+    if (method == 0) select_bruteforce(sr, Nr, sc, Nc, K, top);
+    else if (method == 1) select_product(sr, Nr, sc, Nc, K, top);
+    else select_blockmerge(sr, Nr, sc, Nc, K, bsel, top);
+    // log-sum-exp per half (Eq.LSM)
+    auto lse = [](const float* s, int64_t n) {
+      double m = -INFINITY;
+      for (int64_t i = 0; i < n; ++i) m = std::max(m, (double)s[i]);
+      double acc = 0.0;
+      for (int64_t i = 0; i < n; ++i) acc += std::exp((double)s[i] - m);
+      return m + std::log(acc);
+    };
+    double lr = lse(sr, Nr), lc = lse(sc, Nc);
+    double k1 = top[0].hi + top[0].lo;
+    double den = 0.0;
+    for (int64_t k = 0; k < K; ++k) den += std::exp((top[k].hi - k1) + top[k].lo);
+    for (int64_t k = 0; k < K; ++k) {
+      idx[t * K + k] = (int32_t)top[k].n;
+      gate[t * K + k] = std::exp((top[k].hi - k1) + top[k].lo) / den;
+      score[t * K + k] = top[k].hi + top[k].lo - lr - lc;
+      key_hi[t * K + k] = top[k].hi;
+      key_lo[t * K + k] = top[k].lo;
+    }
+    if ((int64_t)top.size() > K)
+      gap[t] = (top[K - 1].hi - top[K].hi) + (top[K - 1].lo - top[K].lo);
+    else
+      gap[t] = INFINITY;
+  });
+}
+
+// O6-O7 Expert-Centric Scheduling with group size B = 1 (
+// reading Q14): tasks t in token-major order (Eq.Tasks) carry
+// (token[t], ids[t], gate[t]); tasks whose expert lies outside the local
+// range [n_begin, n_end) are not part of this plan.  A stable counting sort
+// by expert id (Eq.Sort with keys (q, l), radix-sortable per PAPER:536)
+// gives, for local expert e = id - n_begin:
+//   offsets[e] .. offsets[e+1]   its task segment (tokens ascending)
+//   sorted_token, sorted_gate    tasks in expert-major order
+//   active[0..n_active)          unique active experts ascending (E_active)
+void oracle_schedule(int64_t M, const int32_t* ids, const double* gates, const int32_t* tokens,
+                     int64_t n_begin, int64_t n_end, int32_t* offsets, int32_t* sorted_token,
+                     double* sorted_gate, int32_t* active, int64_t* n_active) {
+  int64_t n_loc = n_end - n_begin;
+  std::vector<int64_t> cnt(n_loc + 1, 0);
+  for (int64_t t = 0; t < M; ++t)
+    if (ids[t] >= n_begin && ids[t] < n_end) cnt[ids[t] - n_begin + 1]++;
+  for (int64_t e = 0; e < n_loc; ++e) cnt[e + 1] += cnt[e];
+  for (int64_t e = 0; e <= n_loc; ++e) offsets[e] = (int32_t)cnt[e];
+  std::vector<int64_t> cursor(cnt.begin(), cnt.end() - 1);
+  for (int64_t t = 0; t < M; ++t) {  // stable: visits tasks in t order
+    if (ids[t] < n_begin || ids[t] >= n_end) continue;
+    int64_t p = cursor[ids[t] - n_begin]++;
+    sorted_token[p] = tokens[t];
+    sorted_gate[p] = gates[t];
+  }
+  int64_t na = 0;
+  for (int64_t e = 0; e < n_loc; ++e)
+    if (offsets[e + 1] > offsets[e]) active[na++] = (int32_t)e;
+  *n_active = na;
+}
+
+// O8 routed branch, token-centric -- the definition (Eq.Assemble,
+// PAPER:182-186; Eq.Atomic): for every token l,
+// y[l] = sum_{head,k} g * sigma(x_l . W[n]) * V[n], dot products summed
+// sequentially in double.  ids index the (possibly compacted) tables W, V.
+void oracle_routed_token_centric(int64_t L, int64_t d, int64_t HK, const double* x,
+                                 const double* W, const double* V, const int32_t* ids,
+                                 const double* gates, int act, double* y, int nthreads) {
+  parallel_for(L, nthreads, [&](int64_t l) {
+    double* yl = y + l * d;
+    for (int64_t c = 0; c < d; ++c) yl[c] = 0.0;
+    for (int64_t k = 0; k < HK; ++k) {
+      int64_t n = ids[l * HK + k];
+      double z = 0.0;
+      for (int64_t c = 0; c < d; ++c) z += x[l * d + c] * W[n * d + c];
+      double a = gates[l * HK + k] * act_fn(z, act);
+      for (int64_t c = 0; c < d; ++c) yl[c] += a * V[n * d + c];
+    }
+  });
+}
+
+// O9 routed branch, expert-centric (Eq.Grouped, with B = 1 so
+// G_q is one-hot): walk the plan expert by expert; each expert's W/V rows are
+// used for its whole token group, results scatter-added into y.
+void oracle_routed_expert_centric(int64_t L, int64_t d, int64_t n_loc, const int32_t* offsets,
+                                  const int32_t* sorted_token, const double* sorted_gate,
+                                  const double* x, const double* W_loc, const double* V_loc,
+                                  int act, double* y) {
+  for (int64_t i = 0; i < L * d; ++i) y[i] = 0.0;
+  for (int64_t e = 0; e < n_loc; ++e) {
+    const double* w = W_loc + e * d;
+    const double* v = V_loc + e * d;
+    for (int64_t p = offsets[e]; p < offsets[e + 1]; ++p) {
+      int64_t l = sorted_token[p];
+      double z = 0.0;
+      for (int64_t c = 0; c < d; ++c) z += x[l * d + c] * w[c];
+      double a = sorted_gate[p] * act_fn(z, act);
+      for (int64_t c = 0; c < d; ++c) y[l * d + c] += a * v[c];
+    }
+  }
+}
+
+// O10 shared dense MLP (form per reading Q2 = SwiGLU
+// without biases): u = x W_gate, v = x W_up, H = silu(u) * v (not rounded),
+// y = H W_down.  w_gu: [2*d_ff][d] (gate rows then up rows), w_down: [d][d_ff].
+void oracle_shared_mlp(int64_t L, int64_t d, int64_t d_ff, const double* x, const double* w_gu,
+                       const double* w_down, double* y, int nthreads) {
+  parallel_for(L, nthreads, [&](int64_t l) {
+    std::vector<double> H(d_ff);
+    const double* xl = x + l * d;
+    for (int64_t f = 0; f < d_ff; ++f) {
+      double u = 0.0, v = 0.0;
+      for (int64_t c = 0; c < d; ++c) {
+        u += xl[c] * w_gu[f * d + c];
+        v += xl[c] * w_gu[(d_ff + f) * d + c];
+      }
+      H[f] = silu(u) * v;
+    }
+    for (int64_t c = 0; c < d; ++c) {
+      double acc = 0.0;
+      for (int64_t f = 0; f < d_ff; ++f) acc += H[f] * w_down[c * d_ff + f];
+      y[l * d + c] = acc;
+    }
+  });
+}
+
+// Whole layer for a batch of tokens (Eq.MoE):
+// canonical logits -> product selection -> gates -> token-centric routed
+// branch (sum over heads) -> + shared MLP.  Used for the CPU baseline timing
+// (bench.py cpu_baseline / --impl reference) and as the layer parity oracle.
+// subkeys: [h][N_r+N_c][d]; W, V: [N][d] (full tables, or compact tables when
+// id_map != nullptr maps flat id -> table row via a sorted list of
+// (id, row) pairs of length n_map).
+void oracle_layer(int64_t L, int64_t d, int64_t Nr, int64_t Nc, int64_t K, int64_t h,
+                  int64_t d_ff, const double* x, const double* subkeys, const double* W,
+                  const double* V, const int64_t* id_map, int64_t n_map, const double* w_gu,
+                  const double* w_down, int act, double* y, int32_t* idx_out, double* gate_out,
+                  int nthreads) {
+  int64_t R = Nr + Nc;
+  parallel_for(L, nthreads, [&](int64_t l) {
+    const double* xl = x + l * d;
+    std::vector<float> lg(R);
+    std::vector<double> yl(d, 0.0);
+    for (int64_t hh = 0; hh < h; ++hh) {
+      for (int64_t r = 0; r < R; ++r) {
+        const double* sw = subkeys + (hh * R + r) * d;
+        double acc = 0.0;
+        for (int64_t k = 0; k < d; ++k) acc += xl[k] * sw[k];
+        lg[r] = (float)acc;
+      }
+      std::vector<Key> top;
+      select_product(lg.data(), Nr, lg.data() + Nr, Nc, K, top);
+      double k1 = top[0].hi + top[0].lo, den = 0.0;
+      for (int64_t k = 0; k < K; ++k) den += std::exp((top[k].hi - k1) + top[k].lo);
+      for (int64_t k = 0; k < K; ++k) {
+        int64_t n = top[k].n;
+        double g = std::exp((top[k].hi - k1) + top[k].lo) / den;
+        if (idx_out) idx_out[(l * h + hh) * K + k] = (int32_t)n;
+        if (gate_out) gate_out[(l * h + hh) * K + k] = g;
+        int64_t row = n;
+        if (id_map) {  // binary search the (id,row) map
+          int64_t lo = 0, hi = n_map - 1;
+          while (lo < hi) {
+            int64_t mid = (lo + hi) / 2;
+            if (id_map[2 * mid] < n) lo = mid + 1; else hi = mid;
+          }
+          row = id_map[2 * lo + 1];
+        }
+        double z = 0.0;
+        for (int64_t c = 0; c < d; ++c) z += xl[c] * W[row * d + c];
+        double a = g * act_fn(z, act);
+        for (int64_t c = 0; c < d; ++c) yl[c] += a * V[row * d + c];
+      }
+    }
+    if (d_ff > 0) {
+      std::vector<double> H(d_ff);
+      for (int64_t f = 0; f < d_ff; ++f) {
+        double u = 0.0, v = 0.0;
+        for (int64_t c = 0; c < d; ++c) {
+          u += xl[c] * w_gu[f * d + c];
+          v += xl[c] * w_gu[(d_ff + f) * d + c];
+        }
+        H[f] = silu(u) * v;
+      }
+      for (int64_t c = 0; c < d; ++c) {
+        double acc = 0.0;
+        for (int64_t f = 0; f < d_ff; ++f) acc += H[f] * w_down[c * d_ff + f];
+        yl[c] += acc;
+      }
+    }
+    for (int64_t c = 0; c < d; ++c) y[l * d + c] = yl[c];
+  });
+}
+
+}  // extern "C"

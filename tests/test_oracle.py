@@ -1,0 +1,320 @@
+"""Pins for the CPU oracle (-m "not gpu").  Each test pins an oracle function to
+something other than itself: closed forms, exact integer / rational arithmetic,
+brute force on tiny inputs, invariants, or SPEC worked examples
+(tests/golden/spec_examples.json, each with its citation).
+"Oracle pins" for which test pins which function."""
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def _exact_topk(sr, sc, K):
+    """Independent brute force with exact rational keys (Python Fractions)."""
+    Nr, Nc = len(sr), len(sc)
+    cells = [(Fraction(float(sr[i])) + Fraction(float(sc[j])), i * Nc + j)
+             for i in range(Nr) for j in range(Nc)]
+    cells.sort(key=lambda t: (-t[0], t[1]))
+    return cells[:K + 1]
+
+
+def _rand_logits(rng, T, Nr, Nc, kind):
+    if kind == "cont":
+        return rng.standard_normal((T, Nr + Nc)).astype(np.float32)
+    if kind == "dyadic":  # heavy exact ties
+        return (rng.integers(-3, 4, (T, Nr + Nc)) / 4.0).astype(np.float32)
+    # rounding-adversarial: near-equal values differing in the last bits
+    base = rng.integers(-2, 3, (T, Nr + Nc)).astype(np.float32)
+    eps = rng.integers(-2, 3, (T, Nr + Nc)).astype(np.float32) * np.float32(2.0 ** -25)
+    return (base + eps).astype(np.float32)
+
+
+# ---- P1: brute force == exact rational brute force (tiny inputs) -----------------
+@pytest.mark.parametrize("kind", ["cont", "dyadic", "adv"])
+def test_bruteforce_matches_exact_rational(kind):
+    rng = np.random.default_rng(7)
+    for _ in range(60):
+        Nr, Nc = int(rng.integers(1, 7)), int(rng.integers(1, 7))
+        K = int(rng.integers(1, Nr * Nc + 1))
+        lg = _rand_logits(rng, 1, Nr, Nc, kind)
+        r = oracle.route(lg, Nr, Nc, K, method=oracle.BRUTE, nthreads=1)
+        ex = _exact_topk(lg[0, :Nr], lg[0, Nr:], K)
+        assert list(r["idx"][0]) == [n for _, n in ex[:K]]
+        if K < Nr * Nc:
+            assert r["gap"][0] == pytest.approx(float(ex[K - 1][0] - ex[K][0]), abs=1e-12)
+
+
+def test_exact_key_minimal_counterexample():
+    """A.4: s_r=[0, 2^-25], s_c=[1], K=1.  fp32-rounded keys tie; exact keys do not."""
+    lg = np.array([[0.0, 2.0 ** -25, 1.0]], dtype=np.float32)
+    for m in (oracle.BRUTE, oracle.PRODUCT):
+        assert oracle.route(lg, 2, 1, 1, method=m)["idx"][0, 0] == 1
+
+
+# ---- P2: product == brute force == block-merge (>= 1000 instances) ---------------
+@pytest.mark.parametrize("kind", ["cont", "dyadic", "adv"])
+def test_product_equals_bruteforce(kind):
+    rng = np.random.default_rng({"cont": 1, "dyadic": 2, "adv": 3}[kind])
+    n = 0
+    for _ in range(400):
+        Nr, Nc = int(rng.integers(1, 12)), int(rng.integers(1, 12))
+        K = int(rng.integers(1, Nr * Nc + 1))
+        lg = _rand_logits(rng, 3, Nr, Nc, kind)
+        b = oracle.route(lg, Nr, Nc, K, method=oracle.BRUTE, nthreads=1)
+        p = oracle.route(lg, Nr, Nc, K, method=oracle.PRODUCT, nthreads=1)
+        m = oracle.route(lg, Nr, Nc, K, method=oracle.BLOCKMERGE, bsel=max(K + 1, 5), nthreads=1)
+        for o in (p, m):
+            np.testing.assert_array_equal(o["idx"], b["idx"])
+            np.testing.assert_array_equal(o["gate"], b["gate"])
+            np.testing.assert_array_equal(o["gap"], b["gap"])
+        n += 3
+    assert n >= 1000
+
+
+def test_product_equals_bruteforce_larger():
+    rng = np.random.default_rng(11)
+    for Nr, Nc, K in [(64, 64, 1), (64, 64, 16), (32, 32, 8), (16, 48, 64), (256, 256, 16)]:
+        lg = rng.standard_normal((4, Nr + Nc)).astype(np.float32)
+        b = oracle.route(lg, Nr, Nc, K, method=oracle.BRUTE)
+        p = oracle.route(lg, Nr, Nc, K, method=oracle.PRODUCT)
+        np.testing.assert_array_equal(p["idx"], b["idx"])
+
+
+# ---- P3: closed forms --------------------------------------------------------------
+def test_k1_is_argmax_pair():
+    rng = np.random.default_rng(5)
+    lg = rng.standard_normal((20, 9 + 13)).astype(np.float32)
+    r = oracle.route(lg, 9, 13, 1)
+    for t in range(20):
+        i, j = int(np.argmax(lg[t, :9])), int(np.argmax(lg[t, 9:]))
+        assert r["idx"][t, 0] == i * 13 + j
+        assert r["gate"][t, 0] == 1.0
+
+
+def test_single_row_reduces_to_column_topk():
+    rng = np.random.default_rng(6)
+    lg = rng.standard_normal((10, 1 + 40)).astype(np.float32)
+    r = oracle.route(lg, 1, 40, 7)
+    for t in range(10):
+        order = sorted(range(40), key=lambda j: (-lg[t, 1 + j], j))[:7]
+        assert list(r["idx"][t]) == order
+
+
+def test_zero_input_uniform():
+    """x = 0 -> all keys 0 -> ids [0..K), gates 1/K (reading Q20)."""
+    x = np.zeros((3, 16))
+    sub = np.random.default_rng(0).standard_normal((1, 8 + 8, 16))
+    lg = oracle.logits(x, sub)
+    r = oracle.route(lg.reshape(3, 16), 8, 8, 5)
+    for t in range(3):
+        assert list(r["idx"][t]) == [0, 1, 2, 3, 4]
+        np.testing.assert_allclose(r["gate"][t], 0.2, rtol=0, atol=1e-15)
+
+
+def test_uniform_tiebreak_golden():
+    g = GOLD["uniform_tiebreak"]
+    lg = np.zeros((1, g["n_rows"] + g["n_cols"]), np.float32)
+    for m in (oracle.BRUTE, oracle.PRODUCT, oracle.BLOCKMERGE):
+        assert list(oracle.route(lg, g["n_rows"], g["n_cols"], g["K"], method=m, bsel=4)["idx"][0]) == g["expected"]
+
+
+def test_gates_two_golden():
+    g = GOLD["gates_two"]
+    lg = np.array([[g["scores"][0], g["scores"][1], 0.0]], dtype=np.float32)
+    r = oracle.route(lg, 2, 1, 2)
+    np.testing.assert_allclose(r["gate"][0], g["expected"], atol=1e-7)  # fp32 logits
+
+
+def test_logsoftmax_golden_via_scores():
+    g = GOLD["logsoftmax_two"]
+    lg = np.array([[g["s"][0], g["s"][1], 0.0]], dtype=np.float32)
+    r = oracle.route(lg, 2, 1, 2)
+    # score = p_r[i] + p_c[j], p_c = log(1) = 0; sorted desc -> [ln 3/4, ln 1/4]
+    np.testing.assert_allclose(r["score"][0], [g["expected"][1], g["expected"][0]], atol=1e-7)
+
+
+# ---- P4: invariants ----------------------------------------------------------------
+def test_shift_invariance_and_normalisation():
+    rng = np.random.default_rng(9)
+    lg = (rng.integers(-64, 64, (50, 12 + 10)) / 16.0).astype(np.float32)
+    r0 = oracle.route(lg, 12, 10, 6)
+    lg2 = lg.copy()
+    lg2[:, :12] += np.float32(0.75)  # dyadic shift: exact in fp32
+    lg2[:, 12:] -= np.float32(2.5)
+    r1 = oracle.route(lg2, 12, 10, 6)
+    np.testing.assert_array_equal(r0["idx"], r1["idx"])
+    np.testing.assert_allclose(r0["gate"], r1["gate"], atol=1e-12)
+    np.testing.assert_allclose(r0["score"], r1["score"], atol=1e-12)  # log-probs absorb shift
+    np.testing.assert_allclose(r0["gate"].sum(1), 1.0, atol=1e-12)
+    for t in range(50):
+        assert len(set(r0["idx"][t])) == 6
+        assert np.all(np.diff(r0["score"][t]) <= 0)
+
+
+# ---- O1 logits pinned by exact integer arithmetic (P6 + normal mode) ---------------
+@pytest.mark.parametrize("mode", [synth.NORMAL, synth.DYADIC])
+def test_logits_exact_integer(mode):
+    d, L, h, R = 64, 5, 2, 24
+    ex = synth.default_exponents(d, 0, mode)
+    xb = synth.gen_bf16_bits(3, synth.TID_X, (L, d), ex[synth.TID_X], mode)
+    sb = synth.gen_bf16_bits(3, synth.TID_SUBKEYS, (h, R, d), ex[synth.TID_SUBKEYS], mode)
+    x, s = synth.bf16_bits_to_f64(xb), synth.bf16_bits_to_f64(sb)
+    out = oracle.logits(x, s)
+    # integers in units of 2^-e: exact int64 dot products, then one rounding to fp32
+    xi = np.rint(np.ldexp(x, ex[synth.TID_X])).astype(np.int64)
+    si = np.rint(np.ldexp(s, ex[synth.TID_SUBKEYS])).astype(np.int64)
+    assert np.array_equal(np.ldexp(xi.astype(np.float64), -ex[synth.TID_X]), x)
+    for l in range(L):
+        for hh in range(h):
+            for r in range(R):
+                acc = int(np.dot(xi[l], si[hh, r]))  # exact (< 2^53)
+                v = float(Fraction(acc, 2 ** (ex[synth.TID_X] + ex[synth.TID_SUBKEYS])))
+                assert out[l, hh, r] == np.float32(v)
+
+
+# ---- P5: schedule + executor identity ----------------------------------------------
+def test_schedule_golden():
+    g = GOLD["schedule_example"]
+    ids = np.array(g["ids"], np.int32).reshape(-1)
+    toks = np.repeat(np.arange(2), 2).astype(np.int32)
+    p = oracle.schedule(ids, np.ones(4), toks, 0, 10)
+    assert list(p["active"]) == g["active"]
+    assert math.ceil(p["n_active"] / g["B"]) == g["n_groups"]
+    assert list(p["sorted_token"]) == g["expected_sorted_token"]
+
+
+def test_schedule_properties():
+    rng = np.random.default_rng(4)
+    L, HK, N = 40, 6, 37
+    ids = rng.integers(0, N, (L, HK)).astype(np.int32)
+    gates = rng.random((L, HK))
+    toks = np.repeat(np.arange(L), HK).astype(np.int32)
+    for (b, e) in [(0, N), (5, 20)]:
+        p = oracle.schedule(ids, gates, toks, b, e)
+        sel = (ids.reshape(-1) >= b) & (ids.reshape(-1) < e)
+        # multiset conservation
+        want = sorted(zip(toks[sel], ids.reshape(-1)[sel] - b, gates.reshape(-1)[sel]))
+        got = []
+        for ee in range(e - b):
+            s, t = p["offsets"][ee], p["offsets"][ee + 1]
+            assert np.all(np.diff(p["sorted_token"][s:t]) >= 0)  # tokens ascend
+            got += [(p["sorted_token"][q], ee, p["sorted_gate"][q]) for q in range(s, t)]
+        assert sorted(got) == want
+        assert list(p["active"]) == [ee for ee in range(e - b) if p["offsets"][ee + 1] > p["offsets"][ee]]
+
+
+@pytest.mark.parametrize("act", [0, 1])
+def test_token_centric_equals_expert_centric(act):
+    rng = np.random.default_rng(12)
+    for L, d, N, HK in [(1, 8, 5, 1), (16, 32, 64, 8), (64, 16, 1024, 8), (30, 24, 7, 7)]:
+        x = rng.standard_normal((L, d))
+        W, V = rng.standard_normal((N, d)), rng.standard_normal((N, d))
+        ids = np.stack([rng.choice(N, HK, replace=(HK > N)) for _ in range(L)]).astype(np.int32)
+        g = rng.random((L, HK))
+        yt = oracle.routed_token_centric(x, W, V, ids, g, act)
+        p = oracle.schedule(ids, g, np.repeat(np.arange(L), HK), 0, N)
+        ye = oracle.routed_expert_centric(x, W, V, p, act)
+        assert np.max(np.abs(yt - ye)) <= 1e-10 * max(1.0, np.max(np.abs(yt)))
+
+
+def test_atomic_expert_golden():
+    g = GOLD["silu_atomic"]
+    y = oracle.routed_token_centric(np.array([g["x"]]), np.array([g["w"]]), np.array([g["v"]]),
+                                    np.array([[0]]), np.array([[1.0]]))
+    np.testing.assert_allclose(y[0], g["expected"], rtol=0, atol=1e-15)
+
+
+def test_orthogonal_input_zero():
+    y = oracle.routed_token_centric(np.array([[1.0, 0.0]]), np.array([[0.0, 3.0]]),
+                                    np.array([[5.0, 7.0]]), np.array([[0]]), np.array([[1.0]]))
+    assert np.all(y == 0.0)
+
+
+# ---- P8: linearity / convexity -----------------------------------------------------
+def test_linearity_in_V_and_convexity():
+    rng = np.random.default_rng(13)
+    L, d, N, HK = 8, 16, 50, 5
+    x = rng.standard_normal((L, d))
+    W, V = rng.standard_normal((N, d)), rng.standard_normal((N, d))
+    ids = np.stack([rng.choice(N, HK, replace=False) for _ in range(L)]).astype(np.int32)
+    g = rng.random((L, HK)); g /= g.sum(1, keepdims=True)
+    y1 = oracle.routed_token_centric(x, W, V, ids, g)
+    for c in (0.0, 2.0, -1.0):
+        assert np.max(np.abs(oracle.routed_token_centric(x, W, c * V, ids, g) - c * y1)) <= 1e-10
+    # all atomic outputs equal u (identity act, z == 1) -> routed == u (gates sum to 1)
+    x1 = np.zeros((L, d)); x1[:, 0] = 1.0
+    W1 = np.zeros((N, d)); W1[:, 0] = 1.0
+    u = rng.standard_normal(d)
+    y = oracle.routed_token_centric(x1, W1, np.tile(u, (N, 1)), ids, g, act=1)
+    np.testing.assert_allclose(y, np.tile(u, (L, 1)), atol=1e-12)
+
+
+# ---- P9: shared MLP --------------------------------------------------------------
+def test_shared_mlp_golden_and_zero():
+    g = GOLD["shared_mlp_hand"]
+    y = oracle.shared_mlp(np.array([g["x"]]), np.array(g["w_gu"]), np.array(g["w_down"]))
+    np.testing.assert_allclose(y[0], g["expected"], rtol=1e-15)
+    rng = np.random.default_rng(1)
+    assert np.all(oracle.shared_mlp(np.zeros((2, 8)), rng.standard_normal((12, 8)),
+                                    rng.standard_normal((8, 6))) == 0.0)
+
+
+def test_shared_mlp_matches_numpy_composition():
+    """Cross-check against the matrix form silu(xWg^T)*(xWu^T) Wd^T (numpy BLAS, fp64)."""
+    rng = np.random.default_rng(2)
+    x, wgu, wd = rng.standard_normal((7, 12)), rng.standard_normal((2 * 5, 12)), rng.standard_normal((12, 5))
+    u, v = x @ wgu[:5].T, x @ wgu[5:].T
+    ref = (u / (1 + np.exp(-u)) * v) @ wd.T
+    np.testing.assert_allclose(oracle.shared_mlp(x, wgu, wd), ref, rtol=1e-12, atol=1e-12)
+
+
+# ---- layer composition -------------------------------------------------------------
+def test_layer_composition_equals_steps():
+    rng = np.random.default_rng(21)
+    L, d, Nr, Nc, K, h, dff = 12, 16, 6, 5, 4, 2, 8
+    x = rng.standard_normal((L, d)).astype(np.float32).astype(np.float64)
+    sub = rng.standard_normal((h, Nr + Nc, d)).astype(np.float32).astype(np.float64)
+    W, V = rng.standard_normal((Nr * Nc, d)), rng.standard_normal((Nr * Nc, d))
+    wgu, wd = rng.standard_normal((2 * dff, d)), rng.standard_normal((d, dff))
+    out = oracle.layer(x, sub, W, V, Nr, Nc, K, wgu, wd)
+    lg = oracle.logits(x, sub)
+    r = oracle.route(lg.reshape(L * h, -1), Nr, Nc, K, method=oracle.BRUTE)
+    np.testing.assert_array_equal(out["idx"].reshape(L * h, K), r["idx"])
+    yr = oracle.routed_token_centric(x, W, V, r["idx"].reshape(L, h * K), r["gate"].reshape(L, h * K))
+    ys = oracle.shared_mlp(x, wgu, wd)
+    np.testing.assert_allclose(out["y"], yr + ys, rtol=1e-12, atol=1e-12)
+    # compact tables through id_map give the same result
+    used = np.unique(out["idx"])
+    idm = np.stack([used, np.arange(len(used))], 1)
+    out2 = oracle.layer(x, sub, W[used], V[used], Nr, Nc, K, wgu, wd, id_map=idm)
+    np.testing.assert_array_equal(out2["y"], out["y"])
+
+
+# ---- P11 generator sanity: |E_active| under near-uniform routing ---------------------
+def test_active_expert_count_uniform_model():
+    d, Nr, Nc, K, L = 64, 32, 32, 8, 256
+    ex = synth.default_exponents(d, 0)
+    x = synth.bf16_bits_to_f64(synth.gen_bf16_bits(0, synth.TID_X, (L, d), ex[synth.TID_X]))
+    s = synth.bf16_bits_to_f64(synth.gen_bf16_bits(0, synth.TID_SUBKEYS, (1, Nr + Nc, d), ex[synth.TID_SUBKEYS]))
+    r = oracle.route(oracle.logits(x, s).reshape(L, -1), Nr, Nc, K)
+    n_act = len(np.unique(r["idx"]))
+    N, M = Nr * Nc, L * K
+    expect = N * (1 - (1 - 1 / N) ** M)
+    assert abs(n_act - expect) / expect < 0.1  # within 0.1% at scale; loose at C1
+
+
+def test_traffic_and_flop_formulas_golden():
+    g = GOLD["traffic_counter"]
+    assert 2 * g["d"] * g["L"] * g["K"] == g["expected"]
+    f = GOLD["router_flops"]
+    assert 2 * f["d"] * f["N"] == f["dense_flops"]
+    rt = math.isqrt(f["N"])
+    assert (2 * f["d"] * f["N"]) / (2 * f["d"] * (rt + rt)) == f["ratio"]
