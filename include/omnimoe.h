@@ -1,0 +1,191 @@
+/*
+ * omnimoe.h -- C ABI of the B200-native OmniMoE atomic-expert layer forward
+ * (arXiv 2602.05711).  Shared library: paper_2602_05711_b200/libomnimoe.so.
+ *
+ * Citations: "PAPER:n" is /root/reference/PAPER.md line n (section/equation
+ * named alongside).  Readings of silent or ambiguous passages are numbered Q#
+ * and listed in DESIGN.md.
+ *
+ * Conventions for every entry point
+ *  - Every tensor pointer is a DEVICE pointer owned by the caller.  The library
+ *    never allocates, frees or synchronises device memory; scratch comes from
+ *    the caller's workspace `ws` (size from omnimoe_workspace_size, 256-byte
+ *    aligned).  Calls only enqueue work on `stream` and return immediately;
+ *    asynchronous faults surface at the caller's next synchronisation.
+ *  - Layouts are dense row-major, innermost dimension last; all base pointers
+ *    16-byte aligned.
+ *  - Element type of x / sub-keys / W / V / MLP weights / y is bf16 when
+ *    dims.dtype == OMNIMOE_BF16 and fp32 when OMNIMOE_F32 (correctness mode).
+ *  - Validation happens before any launch; on error nothing is enqueued and
+ *    omnimoe_last_error() (thread-local) names the offending argument/shape.
+ *  - L == 0 (or M == 0) is a successful no-op.
+ *  - There is no CPU fallback: a non-sm_100 device returns
+ *    OMNIMOE_ERR_UNSUPPORTED.
+ */
+#ifndef OMNIMOE_H_
+#define OMNIMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* omnimoe_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  OMNIMOE_OK = 0,
+  OMNIMOE_ERR_INVALID_ARGUMENT = 1, /* null required pointer, K<1, h<1, d%8!=0, ... */
+  OMNIMOE_ERR_SHAPE = 2,            /* K > N, expert range outside [0,N), M >= 2^31 */
+  OMNIMOE_ERR_UNSUPPORTED = 3,      /* not sm_100, unknown dtype / activation / kernel */
+  OMNIMOE_ERR_WORKSPACE = 4,        /* ws_bytes below omnimoe_workspace_size() */
+  OMNIMOE_ERR_CUDA = 5              /* launch error; text in omnimoe_last_error() */
+} omnimoe_status;
+
+enum { OMNIMOE_BF16 = 0, OMNIMOE_F32 = 1 };
+/* sigma of the atomic expert (Eq.Atomic).  SILU = z*sigmoid(z)
+ * (reading Q1); IDENTITY exists for linearity tests only. */
+enum { OMNIMOE_SILU = 0, OMNIMOE_IDENTITY = 1 };
+/* Which routed-branch kernel omnimoe_expert_fwd runs. */
+enum { OMNIMOE_EXPERT_AUTO = 0, OMNIMOE_EXPERT_WARP = 1 };
+/* workspace query selector */
+enum { OMNIMOE_WS_ROUTE = 0, OMNIMOE_WS_SCHEDULE = 1, OMNIMOE_WS_EXPERT = 2, OMNIMOE_WS_LAYER = 3 };
+
+/* Layer dimensions.
+ *   d        hidden size (multiple of 8)
+ *   n_rows   N_r, n_cols N_c: the Cartesian grid, N = N_r * N_c; flat expert id
+ *            n = i*N_c + j (row-major, reading Q6)
+ *   top_k    K experts per token and head (Eq.TopK), 1 <= K <= N
+ *   n_heads  h independent sub-key table pairs over one shared expert pool
+ *            (reading Q3); h = 1 is exactly the paper
+ *   d_ff     shared-MLP width (0: no shared branch)
+ *   cert_eps router certification bound:
+ *            > 0: fast tcgen05 logits; a token-head whose fast K/K+1 key gap is
+ *                 <= 4*cert_eps is recomputed with canonical fp64 logits;
+ *            <= 0: canonical fp64 logits for every token-head (slow, exact).
+ *            Ignored in OMNIMOE_F32 mode (always canonical).
+ */
+typedef struct {
+  int64_t d, n_rows, n_cols, top_k, n_heads, d_ff;
+  int32_t dtype;         /* OMNIMOE_BF16 | OMNIMOE_F32 */
+  int32_t act;           /* OMNIMOE_SILU | OMNIMOE_IDENTITY */
+  float cert_eps;
+  int32_t expert_kernel; /* OMNIMOE_EXPERT_* */
+} omnimoe_dims;
+
+/* Expert-centric plan for the local expert range [expert_begin, expert_end)
+ * (Eq.Tasks + active compression + Eq.Sort with group size B = 1, PAPER:259-275;
+ * reading Q14).  n_loc = expert_end - expert_begin.  All arrays are device
+ * memory provided by the caller:
+ *   expert_offsets int32[n_loc+1]  task segment of local expert e is
+ *                                  [expert_offsets[e], expert_offsets[e+1])
+ *   sorted_token   int32[M]        token of each task, expert-major, tokens
+ *                                  ascending inside a segment
+ *   sorted_gate    float[M]        its gate g
+ *   active         int32[n_loc]    local ids of active experts, ascending
+ *   n_active       int32[1]        |E_active| (stays on the device)
+ * Only the first expert_offsets[n_loc] entries of sorted_* are meaningful
+ * (tasks whose expert lies outside the range are not part of the plan). */
+typedef struct {
+  int32_t* expert_offsets;
+  int32_t* sorted_token;
+  float* sorted_gate;
+  int32_t* active;
+  int32_t* n_active;
+  int64_t expert_begin, expert_end;
+} omnimoe_plan;
+
+/* Bytes of workspace needed by entry point `which` (OMNIMOE_WS_*) for L
+ * tokens (ROUTE, EXPERT, LAYER) or M tasks (SCHEDULE: pass M as L). */
+omnimoe_status omnimoe_workspace_size(const omnimoe_dims* dims, int64_t L, int which,
+                                      size_t* bytes);
+
+/* Cartesian Product Router: Eq.Logits s_r = x W_r, s_c = x W_c
+ * with both halves of each head projected from the full x; exact top-K over the
+ * implicit grid S_ij = s_r[i] + s_c[j] (Eq.S; ranking on raw logits is identical
+ * to ranking on the log-probabilities, reading Q8), ties between exactly equal
+ * keys broken toward the lower flat id (Q7); gates = softmax over the selected
+ * keys (Eq.Gate; Q11).
+ *   x        [L][d]
+ *   subkeys  [h][n_rows + n_cols][d]: row r < n_rows is column r of W_r^h,
+ *            row n_rows + c is column c of W_c^h (K-major operand)
+ *   idx      int32 [L][h][K]  flat expert ids, ordered by (key desc, id asc)
+ *   gate     float [L][h][K]
+ *   score    float [L][h][K]  nullable; p_r[i] + p_c[j] (Eq.LSM + Eq.S)
+ * Output is bitwise reproducible and independent of L and batch composition. */
+omnimoe_status omnimoe_route(const omnimoe_dims* dims, int64_t L, const void* x,
+                             const void* subkeys, int32_t* idx, float* gate, float* score,
+                             void* ws, size_t ws_bytes, omnimoe_stream_t stream);
+
+/* Expert-Centric Scheduling: flatten M tasks in token-major order
+ * (Eq.Tasks), histogram + exclusive scan over local experts, active-list
+ * compaction, stable LSD radix sort by local expert id (Eq.Sort; "radix sort",
+ * PAPER:536).
+ *   idx   int32[M]  global expert ids of the tasks
+ *   gate  float[M]
+ *   token int32[M]  nullable: token of task t defaults to t / (h*K)
+ *   plan  outputs (see omnimoe_plan); plan->expert_begin/end select the shard
+ * Result is bitwise deterministic. */
+omnimoe_status omnimoe_schedule(const omnimoe_dims* dims, int64_t M, const int32_t* idx,
+                                const float* gate, const int32_t* token, const omnimoe_plan* plan,
+                                void* ws, size_t ws_bytes, omnimoe_stream_t stream);
+
+/* Grouped atomic-expert compute + scatter-add (Eq.Grouped, the
+ * routed branch of Eq.Assemble): for every active local expert e,
+ * its rows w_e = W_loc[e], v_e = V_loc[e] are read once; for each task (l, g) of
+ * its segment: z = x_l . w_e (fp32), a = g * sigma(z), y_routed[l] += a * v_e.
+ *   x         [L][d]
+ *   W_loc     [n_loc][d]  rows of W for the plan's expert range
+ *   V_loc     [n_loc][d]
+ *   y_routed  float [L][d]; zeroed first unless accumulate != 0
+ * fp32 atomics: reproducible up to summation order. */
+omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const void* x,
+                                  const void* W_loc, const void* V_loc, const omnimoe_plan* plan,
+                                  float* y_routed, int accumulate, void* ws, size_t ws_bytes,
+                                  omnimoe_stream_t stream);
+
+/* Shared dense MLP (SwiGLU without biases, reading Q2) plus
+ * combine (Eq.MoE):
+ *   H = silu(x W_gate^T) * (x W_up^T)  (bf16 in OMNIMOE_BF16 mode)
+ *   y = H W_down^T + y_routed           (y_routed nullable -> treated as 0)
+ *   w_gate_up [2*d_ff][d] (gate rows, then up rows), w_down [d][d_ff],
+ *   y [L][d] (bf16 or fp32 per dtype). */
+omnimoe_status omnimoe_shared_mlp(const omnimoe_dims* dims, int64_t L, const void* x,
+                                  const void* w_gate_up, const void* w_down, const float* y_routed,
+                                  void* y, void* ws, size_t ws_bytes, omnimoe_stream_t stream);
+
+/* Whole layer forward (Eq.MoE / Eq.Assemble):
+ * route -> schedule (full expert range) -> expert_fwd -> shared MLP + combine.
+ *   W, V       [N][d]
+ *   w_gate_up, w_down  as in omnimoe_shared_mlp (ignored when d_ff == 0)
+ *   y          [L][d]
+ *   idx_out, gate_out  nullable copies of the routing decision [L][h][K] */
+omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void* x,
+                                 const void* subkeys, const void* W, const void* V,
+                                 const void* w_gate_up, const void* w_down, void* y,
+                                 int32_t* idx_out, float* gate_out, void* ws, size_t ws_bytes,
+                                 omnimoe_stream_t stream);
+
+/* Raw fast router logits (the tcgen05 GEMM of the route call), for measuring
+ * the certification bound: logits float [L][h][n_rows+n_cols].  canonical != 0
+ * computes the canonical fp64 logits instead. */
+omnimoe_status omnimoe_router_logits(const omnimoe_dims* dims, int64_t L, const void* x,
+                                     const void* subkeys, float* logits, int canonical,
+                                     omnimoe_stream_t stream);
+
+/* Plain GEMM on the library's tcgen05 engine (bf16 in, fp32 out):
+ * C[M][N] = A[M][K] . B[N][K]^T.  Exposed for engine tests / roofline. */
+omnimoe_status omnimoe_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, const void* B,
+                                 float* C, omnimoe_stream_t stream);
+
+/* Number of kernel launches the last successful call on this thread enqueued. */
+int omnimoe_last_launch_count(void);
+
+const char* omnimoe_status_string(omnimoe_status s);
+const char* omnimoe_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OMNIMOE_H_ */

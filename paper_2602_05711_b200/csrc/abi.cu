@@ -1,0 +1,462 @@
+// C ABI of libomnimoe (include/omnimoe.h): argument validation, workspace
+// carving, and the per-call kernel sequence.  No device allocation, no host
+// synchronisation, no CPU fallback.
+#include <mutex>
+#include <string>
+
+#include "gemm.cuh"
+#include "router.cuh"
+#include "schedule.cuh"
+
+namespace omni {
+
+namespace {
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+void count_launch(int n) { g_launches += n; }
+void reset_launch_count() { g_launches = 0; }
+
+namespace {
+
+omnimoe_status check_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    set_error("no CUDA device");
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  static int cached_dev = -1, cached_ok = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> g(mu);
+  if (cached_dev != dev) {
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cached_ok = (major == 10 && minor == 0);
+    cached_dev = dev;
+    if (!cached_ok) {
+      set_error("device " + std::to_string(dev) + " is sm_" + std::to_string(major) +
+                std::to_string(minor) + "; libomnimoe is built for sm_100a only");
+      return OMNIMOE_ERR_UNSUPPORTED;
+    }
+  }
+  if (!cached_ok) {
+    set_error("device is not sm_100a");
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  return OMNIMOE_OK;
+}
+
+std::string dims_str(const omnimoe_dims& d) {
+  return "(d=" + std::to_string(d.d) + ", n_rows=" + std::to_string(d.n_rows) +
+         ", n_cols=" + std::to_string(d.n_cols) + ", K=" + std::to_string(d.top_k) +
+         ", h=" + std::to_string(d.n_heads) + ", d_ff=" + std::to_string(d.d_ff) + ")";
+}
+
+omnimoe_status validate_dims(const omnimoe_dims* dp) {
+  if (!dp) {
+    set_error("dims is null");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  const omnimoe_dims& d = *dp;
+  if (d.d < 8 || d.d % 8 != 0 || d.n_rows < 1 || d.n_cols < 1 || d.top_k < 1 || d.n_heads < 1 ||
+      d.d_ff < 0 || (d.d_ff > 0 && d.d_ff % 8 != 0)) {
+    set_error("invalid dims " + dims_str(d) + ": need d >= 8, d % 8 == 0, N_r, N_c, K, h >= 1, d_ff % 8 == 0");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (d.dtype != OMNIMOE_BF16 && d.dtype != OMNIMOE_F32) {
+    set_error("unknown dtype " + std::to_string(d.dtype));
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  if (d.act != OMNIMOE_SILU && d.act != OMNIMOE_IDENTITY) {
+    set_error("unknown activation " + std::to_string(d.act));
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  if (d.expert_kernel != OMNIMOE_EXPERT_AUTO && d.expert_kernel != OMNIMOE_EXPERT_WARP) {
+    set_error("unknown expert kernel " + std::to_string(d.expert_kernel));
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  const int64_t N = d.n_rows * d.n_cols;
+  if (d.top_k > N) {
+    set_error("K=" + std::to_string(d.top_k) + " exceeds N=" + std::to_string(N) + " " + dims_str(d));
+    return OMNIMOE_ERR_SHAPE;
+  }
+  if (N >= (int64_t(1) << 31) - 1) {
+    set_error("N=" + std::to_string(N) + " must be < 2^31 - 1 (int32 expert ids)");
+    return OMNIMOE_ERR_SHAPE;
+  }
+  return OMNIMOE_OK;
+}
+
+bool fast_logits(const omnimoe_dims& d) { return d.dtype == OMNIMOE_BF16 && d.cert_eps > 0.f; }
+
+size_t route_ws(const omnimoe_dims& d, int64_t L, bool carve, void* ws, float** logits,
+                int32_t** flag_list, int32_t** flag_count) {
+  Carver c(ws);
+  const int64_t T = L * d.n_heads;
+  float* lg = c.take<float>((size_t)T * (d.n_rows + d.n_cols));
+  int32_t* fl = c.take<int32_t>((size_t)std::max<int64_t>(T, 1));
+  int32_t* fc = c.take<int32_t>(1);
+  if (carve) {
+    *logits = lg;
+    *flag_list = fl;
+    *flag_count = fc;
+  }
+  return c.bytes();
+}
+
+size_t elem_size(const omnimoe_dims& d) { return d.dtype == OMNIMOE_BF16 ? 2 : 4; }
+
+struct LayerWs {
+  void* route_ws;
+  size_t route_bytes;
+  int32_t* idx;
+  float* gate;
+  omnimoe_plan plan;
+  void* sched_ws;
+  float* y_routed;
+  void* H;
+};
+
+size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
+  Carver c(ws);
+  const int64_t N = d.n_rows * d.n_cols;
+  const int64_t M = L * d.n_heads * d.top_k;
+  const size_t rb = route_ws(d, L, false, nullptr, nullptr, nullptr, nullptr);
+  void* rw = c.take<char>(rb);
+  int32_t* idx = c.take<int32_t>((size_t)std::max<int64_t>(M, 1));
+  float* gate = c.take<float>((size_t)std::max<int64_t>(M, 1));
+  int32_t* off = c.take<int32_t>(N + 1);
+  int32_t* st = c.take<int32_t>((size_t)std::max<int64_t>(M, 1));
+  float* sg = c.take<float>((size_t)std::max<int64_t>(M, 1));
+  int32_t* act = c.take<int32_t>(N);
+  int32_t* na = c.take<int32_t>(1);
+  const size_t sb = schedule_ws_bytes(M, N);
+  void* sw = c.take<char>(sb);
+  float* yr = c.take<float>((size_t)L * d.d);
+  void* H = c.take<char>((size_t)L * std::max<int64_t>(d.d_ff, 1) * elem_size(d));
+  if (o) {
+    o->route_ws = rw;
+    o->route_bytes = rb;
+    o->idx = idx;
+    o->gate = gate;
+    o->plan = omnimoe_plan{off, st, sg, act, na, 0, N};
+    o->sched_ws = sw;
+    o->y_routed = yr;
+    o->H = H;
+  }
+  return c.bytes();
+}
+
+omnimoe_status check_ws(size_t have, size_t need, const char* who) {
+  if (have < need) {
+    set_error(std::string(who) + ": workspace of " + std::to_string(have) + " bytes < required " +
+              std::to_string(need));
+    return OMNIMOE_ERR_WORKSPACE;
+  }
+  return OMNIMOE_OK;
+}
+
+omnimoe_status route_impl(const omnimoe_dims& d, int64_t L, const void* x, const void* subkeys,
+                          int32_t* idx, float* gate, float* score, void* ws, cudaStream_t st) {
+  float* logits;
+  int32_t *flag_list, *flag_count;
+  route_ws(d, L, true, ws, &logits, &flag_list, &flag_count);
+  const int64_t T = L * d.n_heads;
+  const int R = (int)(d.n_rows + d.n_cols);
+  SelectParams sp;
+  size_t smem;
+  OMNI_TRY(select_params(d, T, &sp, &smem));
+  if (!fast_logits(d)) {
+    sp.cert_eps = 0.f;
+    OMNI_TRY(launch_canon_logits(d.dtype, x, subkeys, (int)d.d, (int)d.n_heads, R, logits, (int)T,
+                                 nullptr, nullptr, st));
+    return launch_select(sp, smem, logits, idx, gate, score, nullptr, nullptr, nullptr, nullptr, st);
+  }
+  // a1: tcgen05 sub-key scoring GEMM, x [L][d] . subkeys [h*R][d]^T -> logits [L][h*R]
+  GemmArgs ga;
+  ga.M = (int)L;
+  ga.N = (int)(d.n_heads * R);
+  ga.K = (int)d.d;
+  ga.out_f32 = logits;
+  OMNI_TRY(gemm_bf16(EPI_F32, x, subkeys, ga, st));
+  if (cudaMemsetAsync(flag_count, 0, sizeof(int32_t), st) != cudaSuccess) {
+    set_error("route: memset failed");
+    return OMNIMOE_ERR_CUDA;
+  }
+  // a2+a3 on fast logits, flagging uncertified token-heads
+  sp.cert_eps = d.cert_eps;
+  OMNI_TRY(launch_select(sp, smem, logits, idx, gate, score, flag_list, flag_count, nullptr, nullptr, st));
+  // canonical fp64 logits + exact reselection for the flagged token-heads only
+  OMNI_TRY(launch_canon_logits(d.dtype, x, subkeys, (int)d.d, (int)d.n_heads, R, logits, (int)T,
+                               flag_list, flag_count, st));
+  sp.cert_eps = 0.f;
+  return launch_select(sp, smem, logits, idx, gate, score, nullptr, nullptr, flag_list, flag_count, st);
+}
+
+omnimoe_status mlp_impl(const omnimoe_dims& d, int64_t L, const void* x, const void* wgu,
+                        const void* wdown, const float* y_routed, void* y, void* H, cudaStream_t st) {
+  GemmArgs g1;
+  g1.M = (int)L;
+  g1.N = (int)d.d_ff;
+  g1.K = (int)d.d;
+  g1.out = H;
+  GemmArgs g2;
+  g2.M = (int)L;
+  g2.N = (int)d.d;
+  g2.K = (int)d.d_ff;
+  g2.out = y;
+  g2.addend = y_routed;
+  if (d.dtype == OMNIMOE_BF16) {
+    OMNI_TRY(gemm_bf16(EPI_SWIGLU, x, wgu, g1, st));
+    return gemm_bf16(EPI_ADD, H, wdown, g2, st);
+  }
+  OMNI_TRY(gemm_f32(EPI_SWIGLU, static_cast<const float*>(x), static_cast<const float*>(wgu), g1, st));
+  return gemm_f32(EPI_ADD, static_cast<const float*>(H), static_cast<const float*>(wdown), g2, st);
+}
+
+__global__ void cast_out_kernel(const float* __restrict__ in, void* __restrict__ out, int64_t n, int bf16) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (bf16) reinterpret_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(in[i]);
+    else reinterpret_cast<float*>(out)[i] = in[i];
+  }
+}
+
+#define OMNI_NONNULL(p, name)                                  \
+  do {                                                         \
+    if (!(p)) {                                                \
+      set_error(std::string(name) + " must not be null");      \
+      return OMNIMOE_ERR_INVALID_ARGUMENT;                     \
+    }                                                          \
+  } while (0)
+
+}  // namespace
+}  // namespace omni
+
+using namespace omni;
+
+extern "C" {
+
+omnimoe_status omnimoe_workspace_size(const omnimoe_dims* dims, int64_t L, int which, size_t* bytes) {
+  OMNI_TRY(validate_dims(dims));
+  OMNI_NONNULL(bytes, "bytes");
+  if (L < 0) {
+    set_error("L must be >= 0");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  const omnimoe_dims& d = *dims;
+  switch (which) {
+    case OMNIMOE_WS_ROUTE: *bytes = route_ws(d, L, false, nullptr, nullptr, nullptr, nullptr); break;
+    case OMNIMOE_WS_SCHEDULE: *bytes = schedule_ws_bytes(L, d.n_rows * d.n_cols); break;
+    case OMNIMOE_WS_EXPERT: *bytes = expert_ws_bytes(d, L); break;
+    case OMNIMOE_WS_LAYER: *bytes = layer_ws(d, L, nullptr, nullptr); break;
+    default:
+      set_error("unknown workspace selector " + std::to_string(which));
+      return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  return OMNIMOE_OK;
+}
+
+omnimoe_status omnimoe_route(const omnimoe_dims* dims, int64_t L, const void* x, const void* subkeys,
+                             int32_t* idx, float* gate, float* score, void* ws, size_t ws_bytes,
+                             omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  if (L < 0 || L >= (int64_t(1) << 31) / std::max<int64_t>(dims->n_heads * dims->top_k, 1)) {
+    set_error("L out of range");
+    return OMNIMOE_ERR_SHAPE;
+  }
+  if (L == 0) return OMNIMOE_OK;
+  OMNI_NONNULL(x, "x");
+  OMNI_NONNULL(subkeys, "subkeys");
+  OMNI_NONNULL(idx, "idx");
+  OMNI_NONNULL(gate, "gate");
+  OMNI_NONNULL(ws, "ws");
+  OMNI_TRY(check_ws(ws_bytes, route_ws(*dims, L, false, nullptr, nullptr, nullptr, nullptr), "route"));
+  OMNI_TRY(check_device());
+  return route_impl(*dims, L, x, subkeys, idx, gate, score, ws, (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_schedule(const omnimoe_dims* dims, int64_t M, const int32_t* idx, const float* gate,
+                                const int32_t* token, const omnimoe_plan* plan, void* ws, size_t ws_bytes,
+                                omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  OMNI_NONNULL(plan, "plan");
+  const int64_t N = dims->n_rows * dims->n_cols;
+  if (plan->expert_begin < 0 || plan->expert_end > N || plan->expert_begin >= plan->expert_end) {
+    set_error("plan expert range [" + std::to_string(plan->expert_begin) + ", " +
+              std::to_string(plan->expert_end) + ") outside [0, " + std::to_string(N) + ")");
+    return OMNIMOE_ERR_SHAPE;
+  }
+  if (M < 0 || M >= (int64_t(1) << 31) - 1) {
+    set_error("M=" + std::to_string(M) + " must be in [0, 2^31-1)");
+    return OMNIMOE_ERR_SHAPE;
+  }
+  OMNI_NONNULL(plan->expert_offsets, "plan.expert_offsets");
+  OMNI_NONNULL(plan->active, "plan.active");
+  OMNI_NONNULL(plan->n_active, "plan.n_active");
+  if (M > 0) {
+    OMNI_NONNULL(idx, "idx");
+    OMNI_NONNULL(gate, "gate");
+    OMNI_NONNULL(plan->sorted_token, "plan.sorted_token");
+    OMNI_NONNULL(plan->sorted_gate, "plan.sorted_gate");
+  }
+  OMNI_NONNULL(ws, "ws");
+  const int64_t n_loc = plan->expert_end - plan->expert_begin;
+  OMNI_TRY(check_ws(ws_bytes, schedule_ws_bytes(M, n_loc), "schedule"));
+  OMNI_TRY(check_device());
+  return schedule_run(M, idx, gate, token, dims->n_heads * dims->top_k, *plan, ws, (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* W_loc,
+                                  const void* V_loc, const omnimoe_plan* plan, float* y_routed,
+                                  int accumulate, void* ws, size_t ws_bytes, omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  if (L < 0) {
+    set_error("L must be >= 0");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (L == 0) return OMNIMOE_OK;
+  OMNI_NONNULL(plan, "plan");
+  OMNI_NONNULL(x, "x");
+  OMNI_NONNULL(W_loc, "W_loc");
+  OMNI_NONNULL(V_loc, "V_loc");
+  OMNI_NONNULL(y_routed, "y_routed");
+  OMNI_NONNULL(plan->expert_offsets, "plan.expert_offsets");
+  OMNI_NONNULL(plan->active, "plan.active");
+  OMNI_NONNULL(plan->n_active, "plan.n_active");
+  OMNI_NONNULL(plan->sorted_token, "plan.sorted_token");
+  OMNI_NONNULL(plan->sorted_gate, "plan.sorted_gate");
+  OMNI_TRY(check_ws(ws_bytes, expert_ws_bytes(*dims, L), "expert_fwd"));
+  OMNI_TRY(check_device());
+  return expert_run(*dims, L, x, W_loc, V_loc, *plan, y_routed, accumulate, ws, (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_shared_mlp(const omnimoe_dims* dims, int64_t L, const void* x, const void* w_gate_up,
+                                  const void* w_down, const float* y_routed, void* y, void* ws,
+                                  size_t ws_bytes, omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  if (dims->d_ff < 1) {
+    set_error("shared_mlp needs d_ff >= 1");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (L == 0) return OMNIMOE_OK;
+  OMNI_NONNULL(x, "x");
+  OMNI_NONNULL(w_gate_up, "w_gate_up");
+  OMNI_NONNULL(w_down, "w_down");
+  OMNI_NONNULL(y, "y");
+  OMNI_NONNULL(ws, "ws");
+  const size_t need = (size_t)L * dims->d_ff * elem_size(*dims);
+  OMNI_TRY(check_ws(ws_bytes, need, "shared_mlp"));
+  OMNI_TRY(check_device());
+  return mlp_impl(*dims, L, x, w_gate_up, w_down, y_routed, y, ws, (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* subkeys,
+                                 const void* W, const void* V, const void* w_gate_up, const void* w_down,
+                                 void* y, int32_t* idx_out, float* gate_out, void* ws, size_t ws_bytes,
+                                 omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  const omnimoe_dims& d = *dims;
+  if (L < 0 || L * d.n_heads * d.top_k >= (int64_t(1) << 31) - 1) {
+    set_error("L*h*K must be < 2^31-1");
+    return OMNIMOE_ERR_SHAPE;
+  }
+  if (L == 0) return OMNIMOE_OK;
+  OMNI_NONNULL(x, "x");
+  OMNI_NONNULL(subkeys, "subkeys");
+  OMNI_NONNULL(W, "W");
+  OMNI_NONNULL(V, "V");
+  OMNI_NONNULL(y, "y");
+  OMNI_NONNULL(ws, "ws");
+  if (d.d_ff > 0) {
+    OMNI_NONNULL(w_gate_up, "w_gate_up");
+    OMNI_NONNULL(w_down, "w_down");
+  }
+  OMNI_TRY(check_ws(ws_bytes, layer_ws(d, L, nullptr, nullptr), "layer_fwd"));
+  OMNI_TRY(check_device());
+  cudaStream_t st = (cudaStream_t)stream;
+  LayerWs w;
+  layer_ws(d, L, ws, &w);
+  int32_t* idx = idx_out ? idx_out : w.idx;
+  float* gate = gate_out ? gate_out : w.gate;
+  const int64_t M = L * d.n_heads * d.top_k;
+  OMNI_TRY(route_impl(d, L, x, subkeys, idx, gate, nullptr, w.route_ws, st));
+  const int r_launch = omnimoe_last_launch_count();
+  OMNI_TRY(schedule_run(M, idx, gate, nullptr, d.n_heads * d.top_k, w.plan, w.sched_ws, st));
+  OMNI_TRY(expert_run(d, L, x, W, V, w.plan, w.y_routed, 0, nullptr, st));
+  if (d.d_ff > 0) {
+    OMNI_TRY(mlp_impl(d, L, x, w_gate_up, w_down, w.y_routed, y, w.H, st));
+  } else {
+    cast_out_kernel<<<kSMs * 4, 256, 0, st>>>(w.y_routed, y, L * d.d, d.dtype == OMNIMOE_BF16);
+    OMNI_CHECK_LAUNCH("cast_out_kernel");
+  }
+  (void)r_launch;
+  return OMNIMOE_OK;
+}
+
+omnimoe_status omnimoe_router_logits(const omnimoe_dims* dims, int64_t L, const void* x, const void* subkeys,
+                                     float* logits, int canonical, omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  if (L == 0) return OMNIMOE_OK;
+  OMNI_NONNULL(x, "x");
+  OMNI_NONNULL(subkeys, "subkeys");
+  OMNI_NONNULL(logits, "logits");
+  OMNI_TRY(check_device());
+  const omnimoe_dims& d = *dims;
+  const int R = (int)(d.n_rows + d.n_cols);
+  if (canonical || d.dtype != OMNIMOE_BF16)
+    return launch_canon_logits(d.dtype, x, subkeys, (int)d.d, (int)d.n_heads, R, logits,
+                               (int)(L * d.n_heads), nullptr, nullptr, (cudaStream_t)stream);
+  GemmArgs ga;
+  ga.M = (int)L;
+  ga.N = (int)(d.n_heads * R);
+  ga.K = (int)d.d;
+  ga.out_f32 = logits;
+  return gemm_bf16(EPI_F32, x, subkeys, ga, (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, const void* B, float* C,
+                                 omnimoe_stream_t stream) {
+  reset_launch_count();
+  if (M < 0 || N < 0 || K < 8 || K % 8 != 0 || M >= (int64_t(1) << 31) || N >= (int64_t(1) << 31)) {
+    set_error("gemm: need M, N >= 0 and K >= 8 with K % 8 == 0");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (M == 0 || N == 0) return OMNIMOE_OK;
+  OMNI_NONNULL(A, "A");
+  OMNI_NONNULL(B, "B");
+  OMNI_NONNULL(C, "C");
+  OMNI_TRY(check_device());
+  GemmArgs ga;
+  ga.M = (int)M;
+  ga.N = (int)N;
+  ga.K = (int)K;
+  ga.out_f32 = C;
+  return gemm_bf16(EPI_F32, A, B, ga, (cudaStream_t)stream);
+}
+
+int omnimoe_last_launch_count(void) { return g_launches; }
+
+const char* omnimoe_status_string(omnimoe_status s) {
+  switch (s) {
+    case OMNIMOE_OK: return "OMNIMOE_OK";
+    case OMNIMOE_ERR_INVALID_ARGUMENT: return "OMNIMOE_ERR_INVALID_ARGUMENT";
+    case OMNIMOE_ERR_SHAPE: return "OMNIMOE_ERR_SHAPE";
+    case OMNIMOE_ERR_UNSUPPORTED: return "OMNIMOE_ERR_UNSUPPORTED";
+    case OMNIMOE_ERR_WORKSPACE: return "OMNIMOE_ERR_WORKSPACE";
+    case OMNIMOE_ERR_CUDA: return "OMNIMOE_ERR_CUDA";
+  }
+  return "OMNIMOE_UNKNOWN_STATUS";
+}
+
+const char* omnimoe_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,168 @@
+// Grouped atomic-expert compute + scatter-add (Eq.Grouped), step
+// a6 of DESIGN.md.  Expert-major: one warp owns one active expert at a time,
+// holds its w_e / v_e rows in registers (read from HBM exactly once per layer,
+// D_expert = 2d|E_active|), then streams the expert's tasks in
+// ascending token order: gather x_l (128-bit loads), z = x_l . w_e in
+// fp32, a = g * sigma(z), and scatter-add a * v_e into y_routed[l] with
+// red.global.add.v4.f32.
+#include <string>
+
+#include "schedule.cuh"
+
+namespace omni {
+namespace {
+
+template <typename T>
+struct VecT;
+template <>
+struct VecT<__nv_bfloat16> {
+  static constexpr int E = 8;  // elements per 16-byte vector
+  __device__ static __forceinline__ void unpack(const uint4& u, float (&f)[8]) {
+    f[0] = bf16_lo(u.x); f[1] = bf16_hi(u.x); f[2] = bf16_lo(u.y); f[3] = bf16_hi(u.y);
+    f[4] = bf16_lo(u.z); f[5] = bf16_hi(u.z); f[6] = bf16_lo(u.w); f[7] = bf16_hi(u.w);
+  }
+};
+template <>
+struct VecT<float> {
+  static constexpr int E = 4;
+  __device__ static __forceinline__ void unpack(const uint4& u, float (&f)[4]) {
+    f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+  }
+};
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {  // read-once rows: no L1 allocation
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_vec(const void* p) {
+  return *reinterpret_cast<const uint4*>(p);
+}
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+template <typename T, int NV>
+__global__ void __launch_bounds__(256)
+    expert_warp_kernel(int d, const T* __restrict__ x, const T* __restrict__ W,
+                       const T* __restrict__ V, const int32_t* __restrict__ offsets,
+                       const int32_t* __restrict__ active, const int32_t* __restrict__ n_active,
+                       const int32_t* __restrict__ stok, const float* __restrict__ sgate,
+                       float* __restrict__ y, int act) {
+  constexpr int E = VecT<T>::E;
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * (int64_t)blockDim.x) >> 5);
+  const int na = *n_active;
+  for (int tau = gw; tau < na; tau += nw) {
+    const int e = active[tau];
+    const int beg = offsets[e], end = offsets[e + 1];
+    uint4 wv[NV], vv[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int c = (j * 32 + lane) * E;
+      if (c < d) {
+        wv[j] = ld_stream(W + (size_t)e * d + c);
+        vv[j] = ld_stream(V + (size_t)e * d + c);
+      } else {
+        wv[j] = make_uint4(0, 0, 0, 0);
+        vv[j] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    for (int p = beg; p < end; ++p) {
+      const int l = stok[p];
+      const float g = sgate[p];
+      const T* xl = x + (size_t)l * d;
+      uint4 xv[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const int c = (j * 32 + lane) * E;
+        xv[j] = c < d ? ld_vec(xl + c) : make_uint4(0, 0, 0, 0);
+      }
+      float z = 0.f;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        float xf[E], wf[E];
+        VecT<T>::unpack(xv[j], xf);
+        VecT<T>::unpack(wv[j], wf);
+#pragma unroll
+        for (int i = 0; i < E; ++i) z = fmaf(xf[i], wf[i], z);
+      }
+      z = warp_sum(z);
+      const float a = g * (act == OMNIMOE_IDENTITY ? z : silu_f(z));
+      float* yl = y + (size_t)l * d;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const int c = (j * 32 + lane) * E;
+        if (c < d) {
+          float vf[E];
+          VecT<T>::unpack(vv[j], vf);
+#pragma unroll
+          for (int i = 0; i < E; i += 4) red_add_v4(yl + c + i, a * vf[i], a * vf[i + 1], a * vf[i + 2], a * vf[i + 3]);
+        }
+      }
+    }
+  }
+}
+
+template <typename T>
+omnimoe_status launch_warp(int d, const void* x, const void* W, const void* V,
+                           const omnimoe_plan& plan, float* y, int act, cudaStream_t st) {
+  constexpr int E = VecT<T>::E;
+  const int nv = (d + 32 * E - 1) / (32 * E);
+  const int grid = kSMs * 8;
+  auto X = static_cast<const T*>(x);
+  auto Wp = static_cast<const T*>(W);
+  auto Vp = static_cast<const T*>(V);
+#define OMNI_EXPERT_CASE(NVC)                                                                       \
+  case NVC:                                                                                        \
+    expert_warp_kernel<T, NVC><<<grid, 256, 0, st>>>(d, X, Wp, Vp, plan.expert_offsets, plan.active, \
+                                                     plan.n_active, plan.sorted_token,              \
+                                                     plan.sorted_gate, y, act);                     \
+    break;
+  switch (nv) {
+    OMNI_EXPERT_CASE(1)
+    OMNI_EXPERT_CASE(2)
+    OMNI_EXPERT_CASE(3)
+    OMNI_EXPERT_CASE(4)
+    OMNI_EXPERT_CASE(6)
+    OMNI_EXPERT_CASE(8)
+    OMNI_EXPERT_CASE(16)
+    default:
+      if (nv <= 16) {
+        expert_warp_kernel<T, 16><<<grid, 256, 0, st>>>(d, X, Wp, Vp, plan.expert_offsets, plan.active,
+                                                       plan.n_active, plan.sorted_token,
+                                                       plan.sorted_gate, y, act);
+        break;
+      }
+      set_error("expert_fwd: d too large for the register-resident expert kernel (d <= " +
+                std::to_string(512 * E) + ")");
+      return OMNIMOE_ERR_UNSUPPORTED;
+  }
+#undef OMNI_EXPERT_CASE
+  OMNI_CHECK_LAUNCH("expert_warp_kernel");
+  return OMNIMOE_OK;
+}
+
+}  // namespace
+
+size_t expert_ws_bytes(const omnimoe_dims&, int64_t) { return 0; }
+
+omnimoe_status expert_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W,
+                          const void* V, const omnimoe_plan& plan, float* y, int accumulate,
+                          void*, cudaStream_t st) {
+  if (!accumulate) {
+    if (cudaMemsetAsync(y, 0, (size_t)L * dm.d * sizeof(float), st) != cudaSuccess) {
+      set_error("expert_fwd: memset failed");
+      return OMNIMOE_ERR_CUDA;
+    }
+  }
+  if (dm.dtype == OMNIMOE_BF16) return launch_warp<__nv_bfloat16>((int)dm.d, x, W, V, plan, y, dm.act, st);
+  return launch_warp<float>((int)dm.d, x, W, V, plan, y, dm.act, st);
+}
+
+}  // namespace omni

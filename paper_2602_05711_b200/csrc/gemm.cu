@@ -1,0 +1,380 @@
+// tcgen05 GEMM engine for sm_100a (router sub-key scoring a1, shared MLP a7/a8).
+//
+// One CTA computes a 128 x 256 fp32 tile of C = A . B^T in TMEM:
+//   warp 0 (one lane)  TMA producer: 2-D cp.async.bulk.tensor loads of A (128x64)
+//                      and B (2 x 128x64) bf16 boxes, 128B swizzle, into a
+//                      kStages-deep SMEM ring guarded by full/empty mbarriers;
+//   warp 1 (one lane)  MMA issuer: 4 x tcgen05.mma.cta_group::1.kind::f16
+//                      (M=128, N=256, K=16) per 64-wide K block, accumulator in
+//                      TMEM (256 columns); tcgen05.commit frees the SMEM slot;
+//   warp 2             TMEM allocator;
+//   warps 4..7         epilogue: tcgen05.ld 32x32b.x32 -> registers -> fused
+//                      epilogue (fp32 store | SiLU(gate)*up -> bf16 | +addend -> bf16).
+#include <cuda.h>
+#include <mutex>
+
+#include "gemm.cuh"
+
+namespace omni {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, kStages = 4;
+constexpr int kABytes = BM * BK * 2;        // 16 KB
+constexpr int kBBytes = BN * BK * 2;        // 32 KB
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+// instruction descriptor, kind::f16: D=f32, A=B=bf16, both K-major, M=128, N=256
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t addr = smem_u32(bar), ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(addr), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  // SM100 UMMA shared-memory descriptor, K-major, SWIZZLE_128B:
+  // start>>4 [0,14), LBO>>4 [16,30) (unused for SW128 K-major), SBO>>4 [32,46) = 1024B
+  // between 8-row core-matrix groups, version=1 [46,48), layout=2 (SW128) [61,64).
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(
+          tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmB2, GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM;
+  const int nt = blockIdx.x;
+  const int num_kb = (args.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % kStages;
+      const uint32_t ph = (kb / kStages) & 1;
+      mbar_wait(&empty[s], ph ^ 1);
+      mbar_expect_tx(&full[s], kStageBytes);
+      tma_load_2d(&tmA, &full[s], sA + s * kABytes, kb * BK, m0);
+      if (EPI == EPI_SWIGLU) {
+        tma_load_2d(&tmB, &full[s], sB + s * kBBytes, kb * BK, nt * (BN / 2));
+        tma_load_2d(&tmB2, &full[s], sB + s * kBBytes + kBBytes / 2, kb * BK, nt * (BN / 2));
+      } else {
+        tma_load_2d(&tmB, &full[s], sB + s * kBBytes, kb * BK, nt * BN);
+        tma_load_2d(&tmB, &full[s], sB + s * kBBytes + kBBytes / 2, kb * BK, nt * BN + BN / 2);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer (single thread) ----------------
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % kStages;
+      const uint32_t ph = (kb / kStages) & 1;
+      mbar_wait(&full[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t a0 = smem_u32(sA + s * kABytes), b0 = smem_u32(sB + s * kBBytes);
+#pragma unroll
+      for (int k = 0; k < BK / 16; ++k)
+        umma_f16(tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), kIdesc, (kb | k) != 0);
+      umma_commit(&empty[s]);
+    }
+    umma_commit(tfull);
+  } else if (warp >= 4) {
+    // ---------------- epilogue (TMEM -> registers -> global) ----------------
+    mbar_wait(tfull, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp - 4;  // TMEM lane quarter == warp id % 4
+    const int row = m0 + q * 32 + lane;
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
+    const bool row_ok = row < args.M;
+    if (EPI == EPI_SWIGLU) {
+      __nv_bfloat16* H = reinterpret_cast<__nv_bfloat16*>(args.out);
+#pragma unroll 1
+      for (int c = 0; c < BN / 2 / 32; ++c) {
+        uint32_t g[32], u[32];
+        tmem_ld32(tbase + c * 32, g);
+        tmem_ld32(tbase + BN / 2 + c * 32, u);
+        const int col0 = nt * (BN / 2) + c * 32;
+        if (!row_ok) continue;
+        __nv_bfloat16* dst = H + (size_t)row * args.N + col0;
+        if (col0 + 32 <= args.N && (args.N % 8) == 0) {
+          uint32_t p[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
+            p[i] = pack_bf16x2(silu_f(g0) * __uint_as_float(u[2 * i]),
+                               silu_f(g1) * __uint_as_float(u[2 * i + 1]));
+          }
+          uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) d4[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+        } else {
+          for (int i = 0; i < 32 && col0 + i < args.N; ++i)
+            dst[i] = __float2bfloat16_rn(silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]));
+        }
+      }
+    } else {
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c * 32, r);
+        const int col0 = nt * BN + c * 32;
+        if (!row_ok || col0 >= args.N) continue;
+        const bool vec = (col0 + 32 <= args.N) && (args.N % 8) == 0;
+        if (EPI == EPI_F32) {
+          float* dst = args.out_f32 + (size_t)row * args.N + col0;
+          if (vec) {
+            float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              d4[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                  __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+          } else {
+            for (int i = 0; i < 32 && col0 + i < args.N; ++i) dst[i] = __uint_as_float(r[i]);
+          }
+        } else {  // EPI_ADD -> bf16
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.N + col0;
+          const float* add = args.addend ? args.addend + (size_t)row * args.N + col0 : nullptr;
+          if (vec) {
+            float a[32];
+            if (add) {
+              const float4* a4 = reinterpret_cast<const float4*>(add);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                float4 t = a4[i];
+                a[4 * i] = t.x; a[4 * i + 1] = t.y; a[4 * i + 2] = t.z; a[4 * i + 3] = t.w;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) a[i] = 0.f;
+            }
+            uint32_t p[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              p[i] = pack_bf16x2(__uint_as_float(r[2 * i]) + a[2 * i],
+                                 __uint_as_float(r[2 * i + 1]) + a[2 * i + 1]);
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) d4[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+          } else {
+            for (int i = 0; i < 32 && col0 + i < args.N; ++i)
+              dst[i] = __float2bfloat16_rn(__uint_as_float(r[i]) + (add ? add[i] : 0.f));
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host: tensor maps through the driver entry point (no libcuda link needed)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t k, uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {k, rows};
+  cuuint64_t strides[1] = {k * 2};
+  cuuint32_t box[2] = {BK, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int EPI>
+omnimoe_status launch_tc(const void* A, const void* B, const GemmArgs& a, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_tc_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmemBytes) != cudaSuccess) {
+      set_error("gemm: cannot set dynamic shared memory size");
+      return OMNIMOE_ERR_CUDA;
+    }
+    attr_set = true;
+  }
+  CUtensorMap mA, mB, mB2;
+  bool ok = make_map(&mA, A, a.M, a.K, BM);
+  if (EPI == EPI_SWIGLU) {
+    ok = ok && make_map(&mB, B, a.N, a.K, BN / 2);
+    ok = ok && make_map(&mB2, static_cast<const char*>(B) + (size_t)a.N * a.K * 2, a.N, a.K, BN / 2);
+  } else {
+    ok = ok && make_map(&mB, B, a.N, a.K, BN / 2);
+    mB2 = mB;
+  }
+  if (!ok) {
+    set_error("gemm: cuTensorMapEncodeTiled failed (alignment: K % 8 == 0, 16-byte base)");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  const int ncols = (EPI == EPI_SWIGLU) ? BN / 2 : BN;
+  dim3 grid((a.N + ncols - 1) / ncols, (a.M + BM - 1) / BM);
+  gemm_tc_kernel<EPI><<<grid, 256, kSmemBytes, st>>>(mA, mB, mB2, a);
+  OMNI_CHECK_LAUNCH("gemm_tc_kernel");
+  return OMNIMOE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// fp32 SIMT GEMM (OMNIMOE_F32 correctness mode): 64x64 tile, 256 threads, 4x4 per thread.
+template <int EPI>
+__global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__ A,
+                                                       const float* __restrict__ B, GemmArgs a) {
+  __shared__ float sa[16][64 + 4], sb[2][16][64 + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int nb = (EPI == EPI_SWIGLU) ? 2 : 1;
+  float acc[2][4][4] = {};
+  for (int k0 = 0; k0 < a.K; k0 += 16) {
+    for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+      int r = i / 16, kk = i % 16;
+      int m = m0 + r, k = k0 + kk;
+      sa[kk][r] = (m < a.M && k < a.K) ? A[(size_t)m * a.K + k] : 0.f;
+      for (int b = 0; b < nb; ++b) {
+        int n = n0 + r;
+        sb[b][kk][r] = (n < a.N && k < a.K) ? B[((size_t)b * a.N + n) * a.K + k] : 0.f;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk)
+      for (int b = 0; b < nb; ++b)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[b][i][j] = fmaf(sa[kk][ty * 4 + i], sb[b][kk][tx * 4 + j], acc[b][i][j]);
+    __syncthreads();
+  }
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+      if (m >= a.M || n >= a.N) continue;
+      size_t o = (size_t)m * a.N + n;
+      if (EPI == EPI_F32) a.out_f32[o] = acc[0][i][j];
+      else if (EPI == EPI_SWIGLU) reinterpret_cast<float*>(a.out)[o] = silu_f(acc[0][i][j]) * acc[1][i][j];
+      else reinterpret_cast<float*>(a.out)[o] = acc[0][i][j] + (a.addend ? a.addend[o] : 0.f);
+    }
+}
+
+}  // namespace
+
+omnimoe_status gemm_bf16(int epi, const void* A, const void* B, const GemmArgs& a, cudaStream_t st) {
+  if (a.M == 0 || a.N == 0) return OMNIMOE_OK;
+  switch (epi) {
+    case EPI_F32: return launch_tc<EPI_F32>(A, B, a, st);
+    case EPI_SWIGLU: return launch_tc<EPI_SWIGLU>(A, B, a, st);
+    case EPI_ADD: return launch_tc<EPI_ADD>(A, B, a, st);
+  }
+  return OMNIMOE_ERR_UNSUPPORTED;
+}
+
+omnimoe_status gemm_f32(int epi, const float* A, const float* B, const GemmArgs& a, cudaStream_t st) {
+  if (a.M == 0 || a.N == 0) return OMNIMOE_OK;
+  dim3 grid((a.N + 63) / 64, (a.M + 63) / 64);
+  switch (epi) {
+    case EPI_F32: gemm_f32_kernel<EPI_F32><<<grid, 256, 0, st>>>(A, B, a); break;
+    case EPI_SWIGLU: gemm_f32_kernel<EPI_SWIGLU><<<grid, 256, 0, st>>>(A, B, a); break;
+    case EPI_ADD: gemm_f32_kernel<EPI_ADD><<<grid, 256, 0, st>>>(A, B, a); break;
+    default: return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  OMNI_CHECK_LAUNCH("gemm_f32_kernel");
+  return OMNIMOE_OK;
+}
+
+}  // namespace omni

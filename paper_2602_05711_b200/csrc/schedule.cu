@@ -1,0 +1,294 @@
+// Expert-Centric Scheduling, steps a4-a5 of DESIGN.md.
+//
+// Tasks t = ((l*h)+head)*K + k arrive in token-major order (Eq.Tasks,
+// PAPER:261-265).  a4: per-local-expert histogram, exclusive scan ->
+// expert_offsets, compaction of active experts (E_active).
+// a5: stable LSD radix sort (8-bit digits, "radix sort") of the
+// local expert ids with the task index as payload; stability over the
+// token-major input gives tokens ascending inside each expert segment, i.e.
+// Eq.Sort with group size B = 1 (reading Q14).  Tasks outside the local
+// expert range get the sentinel key n_loc and sort behind every segment.
+// Everything is deterministic (no order-dependent atomics reach the output).
+#include "schedule.cuh"
+
+namespace omni {
+namespace {
+
+constexpr int kScanThreads = 256, kScanItems = 16, kScanTile = kScanThreads * kScanItems;
+constexpr int kRadixThreads = 256, kRadixRounds = 16, kRadixTile = kRadixThreads * kRadixRounds;
+
+__global__ void hist_keys_kernel(const int32_t* __restrict__ ids, int64_t M, int64_t begin,
+                                 int64_t n_loc, uint32_t* __restrict__ keys,
+                                 int32_t* __restrict__ cnt) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < M;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = (int64_t)ids[t] - begin;
+    const bool in = e >= 0 && e < n_loc;
+    keys[t] = in ? (uint32_t)e : (uint32_t)n_loc;
+    if (in) atomicAdd(&cnt[e], 1);
+  }
+}
+
+// block-wide exclusive scan of one value per thread; returns prefix, *total = sum
+__device__ int block_exclusive_scan(int v, int* total, int* warp_sums) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) warp_sums[w] = x;
+  __syncthreads();
+  int wp = 0, tot = 0;
+  for (int i = 0; i < nw; ++i) {
+    if (i < w) wp += warp_sums[i];
+    tot += warp_sums[i];
+  }
+  *total = tot;
+  return wp + x - v;
+}
+
+// MODE 0: plain exclusive scan (out[i] = prefix);  MODE 1: compaction of
+// nonzero entries (out[prefix] = i).  FLAG: scan (in[i] > 0) instead of in[i].
+template <int MODE>
+__global__ void __launch_bounds__(kScanThreads)
+    scan_reduce_kernel(const int32_t* __restrict__ in, int64_t n, int32_t* __restrict__ tile_sums) {
+  __shared__ int ws[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  int s = 0;
+  for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
+    const int64_t g = base + i;
+    if (g < n) s += MODE ? (in[g] > 0) : in[g];
+  }
+  int tot;
+  block_exclusive_scan(s, &tot, ws);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024)
+    scan_tiles_kernel(int32_t* __restrict__ tile_sums, int nt, int32_t* __restrict__ total_out) {
+  __shared__ int ws[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b = 0; b < nt; b += 1024) {
+    const int i = b + threadIdx.x;
+    const int v = i < nt ? tile_sums[i] : 0;
+    int tot;
+    const int ex = block_exclusive_scan(v, &tot, ws);
+    if (i < nt) tile_sums[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total_out) *total_out = carry;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kScanThreads)
+    scan_down_kernel(const int32_t* __restrict__ in, int64_t n, const int32_t* __restrict__ tile_off,
+                     int32_t* __restrict__ out) {
+  __shared__ int tile[kScanTile];
+  __shared__ int ws[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
+    const int64_t g = base + i;
+    tile[i] = g < n ? (MODE ? (in[g] > 0) : in[g]) : 0;
+  }
+  __syncthreads();
+  int v[kScanItems], s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    v[j] = tile[threadIdx.x * kScanItems + j];
+    s += v[j];
+  }
+  int tot;
+  int run = block_exclusive_scan(s, &tot, ws) + tile_off[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t g = base + threadIdx.x * kScanItems + j;
+    if (MODE == 0) {
+      tile[threadIdx.x * kScanItems + j] = run;
+    } else if (v[j] && g < n) {
+      out[run] = (int32_t)g;
+    }
+    run += v[j];
+  }
+  if (MODE == 0) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
+      const int64_t g = base + i;
+      if (g < n) out[g] = tile[i];
+    }
+  }
+}
+
+template <int MODE>
+omnimoe_status scan(const int32_t* in, int64_t n, int32_t* out, int32_t* total, int32_t* tile_sums,
+                    cudaStream_t st) {
+  const int nt = (int)((n + kScanTile - 1) / kScanTile);
+  if (nt == 0) return OMNIMOE_OK;
+  scan_reduce_kernel<MODE><<<nt, kScanThreads, 0, st>>>(in, n, tile_sums);
+  OMNI_CHECK_LAUNCH("scan_reduce_kernel");
+  scan_tiles_kernel<<<1, 1024, 0, st>>>(tile_sums, nt, total);
+  OMNI_CHECK_LAUNCH("scan_tiles_kernel");
+  scan_down_kernel<MODE><<<nt, kScanThreads, 0, st>>>(in, n, tile_sums, out);
+  OMNI_CHECK_LAUNCH("scan_down_kernel");
+  return OMNIMOE_OK;
+}
+
+// ---- radix sort ------------------------------------------------------------
+__global__ void __launch_bounds__(kRadixThreads)
+    radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift, int nb,
+                      int32_t* __restrict__ hist) {
+  __shared__ int h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kRadixTile;
+  for (int i = threadIdx.x; i < kRadixTile; i += kRadixThreads) {
+    const int64_t g = base + i;
+    if (g < n) atomicAdd(&h[(keys[g] >> shift) & 255], 1);
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * nb + blockIdx.x] = h[threadIdx.x];
+}
+
+// Stable scatter: a tile is consumed in rounds of 256 consecutive keys; inside a
+// round, a key's destination = digit base + keys of the same digit in lower
+// warps + same-digit lanes below it in its warp (__match_any_sync).
+__global__ void __launch_bounds__(kRadixThreads)
+    radix_scatter_kernel(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
+                         uint32_t* __restrict__ kout, int32_t* __restrict__ vout, int64_t n,
+                         int shift, int nb, const int32_t* __restrict__ digit_off) {
+  __shared__ int wcnt[kRadixThreads / 32][256];
+  __shared__ int base[256];
+  __shared__ int rtot[256];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  base[tid] = digit_off[(int64_t)tid * nb + blockIdx.x];
+  const unsigned lt = (1u << lane) - 1u;
+  for (int r = 0; r < kRadixRounds; ++r) {
+#pragma unroll
+    for (int w = 0; w < kRadixThreads / 32; ++w) wcnt[w][tid] = 0;
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * kRadixTile + (int64_t)r * kRadixThreads + tid;
+    const bool valid = i < n;
+    uint32_t key = 0;
+    int32_t val = 0;
+    int dig = 0, rank = 0;
+    const unsigned mask = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      key = kin[i];
+      val = vin ? vin[i] : (int32_t)i;
+      dig = (key >> shift) & 255;
+      const unsigned peers = __match_any_sync(mask, dig);
+      rank = __popc(peers & lt);
+      if (rank == 0) wcnt[warp][dig] = __popc(peers);
+    }
+    __syncthreads();
+    {
+      int s = 0;
+#pragma unroll
+      for (int w = 0; w < kRadixThreads / 32; ++w) {
+        const int c = wcnt[w][tid];
+        wcnt[w][tid] = s;
+        s += c;
+      }
+      rtot[tid] = s;
+    }
+    __syncthreads();
+    if (valid) {
+      const int dest = base[dig] + wcnt[warp][dig] + rank;
+      kout[dest] = key;
+      vout[dest] = val;
+    }
+    __syncthreads();
+    base[tid] += rtot[tid];
+  }
+}
+
+__global__ void gather_plan_kernel(const int32_t* __restrict__ order, int64_t M,
+                                   const int32_t* __restrict__ m_loc_ptr,
+                                   const int32_t* __restrict__ token, const float* __restrict__ gate,
+                                   int64_t hk, int32_t* __restrict__ sorted_token,
+                                   float* __restrict__ sorted_gate) {
+  const int64_t m_loc = *m_loc_ptr;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m_loc;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t = order[p];
+    sorted_token[p] = token ? token[t] : (int32_t)(t / hk);
+    sorted_gate[p] = gate[t];
+  }
+}
+
+int grid_for(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  return (int)std::min<int64_t>(std::max<int64_t>(b, 1), kSMs * 16);
+}
+
+}  // namespace
+
+size_t schedule_ws_bytes(int64_t M, int64_t n_loc) {
+  Carver c(nullptr);
+  const int64_t nb = (M + kRadixTile - 1) / kRadixTile;
+  c.take<int32_t>(n_loc + 1);                                 // cnt
+  c.take<uint32_t>(M); c.take<uint32_t>(M);                   // keys ping/pong
+  c.take<int32_t>(M); c.take<int32_t>(M);                     // vals ping/pong
+  c.take<int32_t>(256 * nb);                                  // radix hist
+  const int64_t scan_n = std::max<int64_t>(n_loc + 1, 256 * nb);
+  c.take<int32_t>((scan_n + kScanTile - 1) / kScanTile + 1);  // tile sums
+  return c.bytes();
+}
+
+omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, const int32_t* token,
+                            int64_t hk, const omnimoe_plan& plan, void* ws, cudaStream_t st) {
+  const int64_t n_loc = plan.expert_end - plan.expert_begin;
+  const int64_t nb = (M + kRadixTile - 1) / kRadixTile;
+  Carver c(ws);
+  int32_t* cnt = c.take<int32_t>(n_loc + 1);
+  uint32_t* k0 = c.take<uint32_t>(M);
+  uint32_t* k1 = c.take<uint32_t>(M);
+  int32_t* v0 = c.take<int32_t>(M);
+  int32_t* v1 = c.take<int32_t>(M);
+  int32_t* hist = c.take<int32_t>(256 * nb);
+  const int64_t scan_n = std::max<int64_t>(n_loc + 1, 256 * nb);
+  int32_t* tiles = c.take<int32_t>((scan_n + kScanTile - 1) / kScanTile + 1);
+
+  if (cudaMemsetAsync(cnt, 0, (n_loc + 1) * sizeof(int32_t), st) != cudaSuccess) {
+    set_error("schedule: memset failed");
+    return OMNIMOE_ERR_CUDA;
+  }
+  if (M > 0) {
+    hist_keys_kernel<<<grid_for(M, 256), 256, 0, st>>>(ids, M, plan.expert_begin, n_loc, k0, cnt);
+    OMNI_CHECK_LAUNCH("hist_keys_kernel");
+  }
+  // a4: offsets (exclusive scan of counts; entry n_loc holds the total m_loc)
+  OMNI_TRY(scan<0>(cnt, n_loc + 1, plan.expert_offsets, nullptr, tiles, st));
+  // a4: active-expert compaction and |E_active|
+  OMNI_TRY(scan<1>(cnt, n_loc, plan.active, plan.n_active, tiles, st));
+  if (M == 0) return OMNIMOE_OK;
+  // a5: stable LSD radix sort of the local ids (sentinel n_loc included)
+  int bits = 1;
+  while ((int64_t(1) << bits) <= n_loc) ++bits;
+  const int passes = (bits + 7) / 8;
+  uint32_t *kin = k0, *kout = k1;
+  int32_t *vin = nullptr, *vout = v0;
+  for (int ps = 0; ps < passes; ++ps) {
+    const int shift = 8 * ps;
+    radix_hist_kernel<<<(int)nb, kRadixThreads, 0, st>>>(kin, M, shift, (int)nb, hist);
+    OMNI_CHECK_LAUNCH("radix_hist_kernel");
+    OMNI_TRY(scan<0>(hist, 256 * nb, hist, nullptr, tiles, st));
+    radix_scatter_kernel<<<(int)nb, kRadixThreads, 0, st>>>(kin, vin, kout, vout, M, shift, (int)nb, hist);
+    OMNI_CHECK_LAUNCH("radix_scatter_kernel");
+    std::swap(kin, kout);
+    vin = vout;
+    vout = (vout == v0) ? v1 : v0;
+  }
+  gather_plan_kernel<<<grid_for(M, 256), 256, 0, st>>>(vin, M, plan.expert_offsets + n_loc, token, gate,
+                                                      hk, plan.sorted_token, plan.sorted_gate);
+  OMNI_CHECK_LAUNCH("gather_plan_kernel");
+  return OMNIMOE_OK;
+}
+
+}  // namespace omni

@@ -1,0 +1,282 @@
+"""Thin ctypes binding over libomnimoe.so (include/omnimoe.h).
+
+Argument marshalling only: every step of the layer runs in the library's CUDA
+kernels.  Tensors must be CUDA, contiguous, of the dtype the dims declare; the
+calls enqueue on torch's current stream.  There is no CPU fallback: if the
+shared library is missing or the device is not sm_100a, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libomnimoe.so")
+
+BF16, F32 = 0, 1
+SILU, IDENTITY = 0, 1
+EXPERT_AUTO, EXPERT_WARP = 0, 1
+WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER = 0, 1, 2, 3
+
+
+class OmniMoEError(RuntimeError):
+    pass
+
+
+class Dims(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_int64), ("n_rows", ctypes.c_int64), ("n_cols", ctypes.c_int64),
+                ("top_k", ctypes.c_int64), ("n_heads", ctypes.c_int64), ("d_ff", ctypes.c_int64),
+                ("dtype", ctypes.c_int32), ("act", ctypes.c_int32), ("cert_eps", ctypes.c_float),
+                ("expert_kernel", ctypes.c_int32)]
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [("expert_offsets", ctypes.c_void_p), ("sorted_token", ctypes.c_void_p),
+                ("sorted_gate", ctypes.c_void_p), ("active", ctypes.c_void_p),
+                ("n_active", ctypes.c_void_p), ("expert_begin", ctypes.c_int64),
+                ("expert_end", ctypes.c_int64)]
+
+
+EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnimoe_expert_fwd",
+           "omnimoe_shared_mlp", "omnimoe_layer_fwd", "omnimoe_router_logits", "omnimoe_gemm_bf16",
+           "omnimoe_last_launch_count", "omnimoe_status_string", "omnimoe_last_error"]
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libomnimoe.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise OmniMoEError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    V, I64, I32, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+    PD, PP = ctypes.POINTER(Dims), ctypes.POINTER(Plan)
+    sig = {
+        "omnimoe_workspace_size": [PD, I64, I32, ctypes.POINTER(ctypes.c_size_t)],
+        "omnimoe_route": [PD, I64, V, V, V, V, V, V, SZ, V],
+        "omnimoe_schedule": [PD, I64, V, V, V, PP, V, SZ, V],
+        "omnimoe_expert_fwd": [PD, I64, V, V, V, PP, V, I32, V, SZ, V],
+        "omnimoe_shared_mlp": [PD, I64, V, V, V, V, V, V, SZ, V],
+        "omnimoe_layer_fwd": [PD, I64, V, V, V, V, V, V, V, V, V, V, SZ, V],
+        "omnimoe_router_logits": [PD, I64, V, V, V, I32, V],
+        "omnimoe_gemm_bf16": [I64, I64, I64, V, V, V, V],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    lib.omnimoe_last_launch_count.restype = ctypes.c_int
+    lib.omnimoe_status_string.restype = ctypes.c_char_p
+    lib.omnimoe_status_string.argtypes = [ctypes.c_int]
+    lib.omnimoe_last_error.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        lib = load()
+        raise OmniMoEError(f"{what}: {lib.omnimoe_status_string(status).decode()}: "
+                           f"{lib.omnimoe_last_error().decode()}")
+
+
+def last_launch_count() -> int:
+    return load().omnimoe_last_launch_count()
+
+
+@dataclass
+class LayerDims:
+    d: int
+    n_rows: int
+    n_cols: int
+    top_k: int
+    n_heads: int = 1
+    d_ff: int = 0
+    dtype: int = BF16
+    act: int = SILU
+    cert_eps: float = 0.0
+    expert_kernel: int = EXPERT_AUTO
+
+    @property
+    def N(self) -> int:
+        return self.n_rows * self.n_cols
+
+    @property
+    def torch_dtype(self):
+        return torch.bfloat16 if self.dtype == BF16 else torch.float32
+
+    def c(self) -> Dims:
+        return Dims(self.d, self.n_rows, self.n_cols, self.top_k, self.n_heads, self.d_ff,
+                    self.dtype, self.act, self.cert_eps, self.expert_kernel)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _req(t, name, dtype=None, numel=None):
+    if t is None:
+        raise OmniMoEError(f"{name} is required")
+    if not t.is_cuda:
+        raise OmniMoEError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise OmniMoEError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise OmniMoEError(f"{name} must be {dtype}, got {t.dtype}")
+    if numel is not None and t.numel() != numel:
+        raise OmniMoEError(f"{name} must have {numel} elements, got {t.numel()}")
+    return t
+
+
+def workspace_size(dims: LayerDims, L: int, which: int) -> int:
+    out = ctypes.c_size_t(0)
+    dc = dims.c()
+    _check(load().omnimoe_workspace_size(ctypes.byref(dc), L, which, ctypes.byref(out)), "workspace_size")
+    return out.value
+
+
+def workspace(dims: LayerDims, L: int, which: int, device=None) -> torch.Tensor:
+    return torch.empty(max(workspace_size(dims, L, which), 1), dtype=torch.uint8,
+                       device=device or torch.cuda.current_device())
+
+
+def route(dims: LayerDims, x, subkeys, ws=None, want_score=True):
+    L = x.shape[0]
+    _req(x, "x", dims.torch_dtype, L * dims.d)
+    _req(subkeys, "subkeys", dims.torch_dtype, dims.n_heads * (dims.n_rows + dims.n_cols) * dims.d)
+    K, h = dims.top_k, dims.n_heads
+    idx = torch.empty((L, h, K), dtype=torch.int32, device=x.device)
+    gate = torch.empty((L, h, K), dtype=torch.float32, device=x.device)
+    score = torch.empty((L, h, K), dtype=torch.float32, device=x.device) if want_score else None
+    ws = ws if ws is not None else workspace(dims, L, WS_ROUTE, x.device)
+    dc = dims.c()
+    _check(load().omnimoe_route(ctypes.byref(dc), L, _ptr(x), _ptr(subkeys), _ptr(idx), _ptr(gate),
+                                _ptr(score), _ptr(ws), ws.numel(), _stream()), "route")
+    return idx, gate, score
+
+
+def new_plan(n_loc: int, M: int, device, expert_begin: int = 0):
+    t = dict(expert_offsets=torch.empty(n_loc + 1, dtype=torch.int32, device=device),
+             sorted_token=torch.empty(max(M, 1), dtype=torch.int32, device=device),
+             sorted_gate=torch.empty(max(M, 1), dtype=torch.float32, device=device),
+             active=torch.empty(max(n_loc, 1), dtype=torch.int32, device=device),
+             n_active=torch.empty(1, dtype=torch.int32, device=device),
+             expert_begin=expert_begin, expert_end=expert_begin + n_loc)
+    return t
+
+
+def _cplan(p) -> Plan:
+    return Plan(p["expert_offsets"].data_ptr(), p["sorted_token"].data_ptr(), p["sorted_gate"].data_ptr(),
+                p["active"].data_ptr(), p["n_active"].data_ptr(), p["expert_begin"], p["expert_end"])
+
+
+def schedule(dims: LayerDims, idx, gate, token=None, expert_begin=0, expert_end=None, plan=None, ws=None):
+    M = idx.numel()
+    _req(idx, "idx", torch.int32)
+    _req(gate, "gate", torch.float32, M)
+    if token is not None:
+        _req(token, "token", torch.int32, M)
+    expert_end = dims.N if expert_end is None else expert_end
+    n_loc = expert_end - expert_begin
+    plan = plan or new_plan(n_loc, M, idx.device, expert_begin)
+    ws = ws if ws is not None else torch.empty(max(workspace_size(dims, M, WS_SCHEDULE)
+                                                   if n_loc == dims.N else _sched_ws(dims, M, n_loc), 1),
+                                               dtype=torch.uint8, device=idx.device)
+    dc, cp = dims.c(), _cplan(plan)
+    _check(load().omnimoe_schedule(ctypes.byref(dc), M, _ptr(idx), _ptr(gate), _ptr(token),
+                                   ctypes.byref(cp), _ptr(ws), ws.numel(), _stream()), "schedule")
+    return plan
+
+
+def _sched_ws(dims, M, n_loc):
+    # workspace for a shard: the library sizes by the plan's n_loc <= N, so the
+    # full-range size is an upper bound
+    return workspace_size(dims, M, WS_SCHEDULE)
+
+
+def expert_fwd(dims: LayerDims, x, W_loc, V_loc, plan, y_routed=None, accumulate=False, ws=None):
+    L = x.shape[0]
+    n_loc = plan["expert_end"] - plan["expert_begin"]
+    _req(x, "x", dims.torch_dtype, L * dims.d)
+    _req(W_loc, "W_loc", dims.torch_dtype, n_loc * dims.d)
+    _req(V_loc, "V_loc", dims.torch_dtype, n_loc * dims.d)
+    if y_routed is None:
+        y_routed = torch.empty((L, dims.d), dtype=torch.float32, device=x.device)
+        accumulate = False
+    _req(y_routed, "y_routed", torch.float32, L * dims.d)
+    ws = ws if ws is not None else workspace(dims, L, WS_EXPERT, x.device)
+    dc, cp = dims.c(), _cplan(plan)
+    _check(load().omnimoe_expert_fwd(ctypes.byref(dc), L, _ptr(x), _ptr(W_loc), _ptr(V_loc),
+                                     ctypes.byref(cp), _ptr(y_routed), int(accumulate), _ptr(ws),
+                                     ws.numel(), _stream()), "expert_fwd")
+    return y_routed
+
+
+def shared_mlp(dims: LayerDims, x, w_gate_up, w_down, y_routed=None, y=None, ws=None):
+    L = x.shape[0]
+    _req(x, "x", dims.torch_dtype, L * dims.d)
+    _req(w_gate_up, "w_gate_up", dims.torch_dtype, 2 * dims.d_ff * dims.d)
+    _req(w_down, "w_down", dims.torch_dtype, dims.d * dims.d_ff)
+    if y_routed is not None:
+        _req(y_routed, "y_routed", torch.float32, L * dims.d)
+    y = y if y is not None else torch.empty((L, dims.d), dtype=dims.torch_dtype, device=x.device)
+    ws = ws if ws is not None else torch.empty(max(L * dims.d_ff * (2 if dims.dtype == BF16 else 4), 1),
+                                               dtype=torch.uint8, device=x.device)
+    dc = dims.c()
+    _check(load().omnimoe_shared_mlp(ctypes.byref(dc), L, _ptr(x), _ptr(w_gate_up), _ptr(w_down),
+                                     _ptr(y_routed), _ptr(y), _ptr(ws), ws.numel(), _stream()),
+           "shared_mlp")
+    return y
+
+
+def layer_fwd(dims: LayerDims, x, subkeys, W, V, w_gate_up=None, w_down=None, y=None, ws=None,
+              return_routing=False):
+    L = x.shape[0]
+    _req(x, "x", dims.torch_dtype, L * dims.d)
+    _req(subkeys, "subkeys", dims.torch_dtype, dims.n_heads * (dims.n_rows + dims.n_cols) * dims.d)
+    _req(W, "W", dims.torch_dtype, dims.N * dims.d)
+    _req(V, "V", dims.torch_dtype, dims.N * dims.d)
+    if dims.d_ff:
+        _req(w_gate_up, "w_gate_up", dims.torch_dtype, 2 * dims.d_ff * dims.d)
+        _req(w_down, "w_down", dims.torch_dtype, dims.d * dims.d_ff)
+    y = y if y is not None else torch.empty((L, dims.d), dtype=dims.torch_dtype, device=x.device)
+    idx = gate = None
+    if return_routing:
+        idx = torch.empty((L, dims.n_heads, dims.top_k), dtype=torch.int32, device=x.device)
+        gate = torch.empty((L, dims.n_heads, dims.top_k), dtype=torch.float32, device=x.device)
+    ws = ws if ws is not None else workspace(dims, L, WS_LAYER, x.device)
+    dc = dims.c()
+    _check(load().omnimoe_layer_fwd(ctypes.byref(dc), L, _ptr(x), _ptr(subkeys), _ptr(W), _ptr(V),
+                                    _ptr(w_gate_up), _ptr(w_down), _ptr(y), _ptr(idx), _ptr(gate),
+                                    _ptr(ws), ws.numel(), _stream()), "layer_fwd")
+    return (y, idx, gate) if return_routing else y
+
+
+def router_logits(dims: LayerDims, x, subkeys, canonical=False):
+    L = x.shape[0]
+    _req(x, "x", dims.torch_dtype, L * dims.d)
+    out = torch.empty((L, dims.n_heads, dims.n_rows + dims.n_cols), dtype=torch.float32, device=x.device)
+    dc = dims.c()
+    _check(load().omnimoe_router_logits(ctypes.byref(dc), L, _ptr(x), _ptr(subkeys), _ptr(out),
+                                        int(canonical), _stream()), "router_logits")
+    return out
+
+
+def gemm_bf16(A, B):
+    M, K = A.shape
+    N = B.shape[0]
+    _req(A, "A", torch.bfloat16)
+    _req(B, "B", torch.bfloat16)
+    C = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    _check(load().omnimoe_gemm_bf16(M, N, K, _ptr(A), _ptr(B), _ptr(C), _stream()), "gemm_bf16")
+    return C

@@ -1,0 +1,75 @@
+"""CPU-side checks of the boundary (-m "not gpu"): the C-ABI library builds for
+sm_100a, loads, and exports every symbol include/omnimoe.h declares; the
+product path never imports the oracle."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2602_05711_b200 import build
+    build.build()
+    return ctypes.CDLL(build.LIB)
+
+
+def _declared():
+    hdr = open(os.path.join(ROOT, "include", "omnimoe.h")).read()
+    return sorted(set(re.findall(r"\b(omnimoe_[a-z_0-9]+)\s*\(", hdr)))
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for n in ("omnimoe_route", "omnimoe_schedule", "omnimoe_expert_fwd", "omnimoe_layer_fwd",
+              "omnimoe_workspace_size", "omnimoe_status_string", "omnimoe_last_error"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for n in _declared():
+        assert hasattr(lib, n), n
+    from paper_2602_05711_b200 import omnimoe as om
+    assert set(om.EXPORTS) <= set(_declared())
+
+
+def test_sm100a_code_only(lib):
+    from paper_2602_05711_b200 import build
+    out = subprocess.run(["cuobjdump", "--list-elf", build.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", build.LIB], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass and "UTMALDG" in sass  # tcgen05 MMA + TMA in the GEMM engine
+
+
+def test_host_side_validation_without_gpu(lib):
+    from paper_2602_05711_b200 import omnimoe as om
+    om.load()
+    d = om.LayerDims(d=64, n_rows=4, n_cols=4, top_k=17)
+    with pytest.raises(om.OmniMoEError, match="SHAPE"):
+        om.workspace_size(d, 10, om.WS_LAYER)
+    d = om.LayerDims(d=60, n_rows=4, n_cols=4, top_k=2)
+    with pytest.raises(om.OmniMoEError, match="INVALID_ARGUMENT"):
+        om.workspace_size(d, 10, om.WS_ROUTE)
+    ok = om.LayerDims(d=64, n_rows=32, n_cols=32, top_k=8, d_ff=128)
+    assert om.workspace_size(ok, 256, om.WS_LAYER) > om.workspace_size(ok, 256, om.WS_ROUTE) > 0
+    assert lib.omnimoe_status_string  # symbol resolves
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2602_05711_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dp, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), f
+                assert "oracle.cpp" not in src and "liboracle" not in src, f
+
+
+def test_oracle_includes_no_cuda():
+    src = open(os.path.join(ROOT, "oracle", "oracle.cpp")).read()
+    incs = re.findall(r"^\s*#\s*include\s*[<\"]([^>\"]+)", src, re.M)
+    assert incs and not any("cuda" in i.lower() or "omnimoe" in i or "csrc" in i for i in incs), incs

@@ -1,0 +1,246 @@
+"""GPU-vs-oracle parity through the C ABI (-m gpu).  Inputs are seeded and
+synthetic (synth/); expected values come only from oracle/."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from synth.cuda import make
+from synth.workloads import make_inputs
+from paper_2602_05711_b200 import configs, omnimoe as om
+from tests.helpers import compare_routing, host_rows, rel_errors
+
+pytestmark = pytest.mark.gpu
+
+
+def _dims(name, **over):
+    return configs.get(name, **over)
+
+
+# ---------------------------------------------------------------- generator
+@pytest.mark.parametrize("mode", [synth.NORMAL, synth.DYADIC])
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32])
+def test_synth_device_matches_host(mode, dt):
+    n = 100_003
+    t = make((n,), dt, 5, synth.TID_W, 13, mode)
+    idx = np.arange(n)
+    if dt == torch.bfloat16:
+        want = synth.gen_bf16_bits(5, synth.TID_W, (n,), 13, mode)
+        got = t.view(torch.int16).cpu().numpy().view(np.uint16)
+    else:
+        want = synth.values_f32(5, synth.TID_W, idx, 13, mode).view(np.uint32)
+        got = t.cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------- tcgen05 GEMM engine
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 136), (1000, 2048, 1024), (77, 40, 8),
+                                   (4096, 640, 1024)])
+def test_gemm_tcgen05(M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    C = om.gemm_bf16(A, B)
+    torch.cuda.synchronize()
+    ref = A.double() @ B.double().T
+    err = (C.double() - ref).abs().max().item()
+    assert err <= 1e-5 * K ** 0.5 * ref.abs().max().item() + 1e-6, err
+
+
+# ---------------------------------------------------------------- router
+def _oracle_route(dims, seed, tokens, mode=synth.NORMAL, method=oracle.BRUTE):
+    x = host_rows(dims, seed, "x", tokens, mode)
+    sub = host_rows(dims, seed, "subkeys", None, mode).reshape(dims.n_heads, dims.n_rows + dims.n_cols, dims.d)
+    lg = oracle.logits(x, sub)  # [T][h][R]
+    rows = lg.reshape(-1, dims.n_rows + dims.n_cols)
+    return oracle.route(rows, dims.n_rows, dims.n_cols, dims.top_k, method=method), rows
+
+
+@pytest.mark.parametrize("mode", [synth.NORMAL, synth.DYADIC])
+@pytest.mark.parametrize("cert", [0.0, 1e-5])
+def test_route_c1_all_tokens(mode, cert):
+    w = _dims("C1", cert_eps=cert)
+    inp = make_inputs(w.dims, w.L, w.seed, mode)
+    idx, gate, score = om.route(w.dims, inp["x"], inp["subkeys"])
+    torch.cuda.synchronize()
+    orc, rows = _oracle_route(w.dims, w.seed, np.arange(w.L), mode)
+    r = compare_routing(idx.cpu().numpy(), gate.cpu().numpy(), orc, rows, w.dims.n_rows, w.dims.n_cols)
+    assert r["mismatch"] == 0, r
+    assert r["gate_err"] <= 1e-5
+    # ordering: sorted by (key desc, id asc) exactly like the oracle
+    np.testing.assert_array_equal(idx.cpu().numpy().reshape(-1, w.dims.top_k), orc["idx"])
+    np.testing.assert_allclose(score.cpu().numpy().reshape(-1, w.dims.top_k), orc["score"], atol=1e-4)
+    np.testing.assert_allclose(gate.sum(-1).cpu().numpy(), 1.0, atol=1e-6)
+
+
+def test_canonical_logits_bitwise():
+    w = _dims("C1")
+    inp = make_inputs(w.dims, w.L, w.seed)
+    lg = om.router_logits(w.dims, inp["x"], inp["subkeys"], canonical=True)
+    torch.cuda.synchronize()
+    x = host_rows(w.dims, w.seed, "x", np.arange(w.L))
+    sub = host_rows(w.dims, w.seed, "subkeys").reshape(1, -1, w.dims.d)
+    assert np.array_equal(lg.cpu().numpy().view(np.uint32), oracle.logits(x, sub).view(np.uint32))
+
+
+@pytest.mark.parametrize("cert", [0.0, 1e-5])
+def test_route_c2_multihead(cert):
+    w = _dims("C2", cert_eps=cert)
+    L = 1024
+    inp = make_inputs(w.dims, L, w.seed, skip=("W", "V"))
+    idx, gate, _ = om.route(w.dims, inp["x"], inp["subkeys"])
+    torch.cuda.synchronize()
+    orc, rows = _oracle_route(w.dims, w.seed, np.arange(L), method=oracle.PRODUCT)
+    r = compare_routing(idx.cpu().numpy(), gate.cpu().numpy(), orc, rows, w.dims.n_rows, w.dims.n_cols)
+    assert r["disallowed"] == 0, r
+    if cert == 0.0:
+        assert r["mismatch"] == 0, r
+    assert r["gate_err"] <= 1e-5
+    # brute force on a subsample pins the product path at this size too
+    sub = orc["idx"][:64]
+    bf = oracle.route(rows[:64], w.dims.n_rows, w.dims.n_cols, w.dims.top_k, method=oracle.BRUTE)
+    np.testing.assert_array_equal(sub, bf["idx"])
+
+
+def test_route_degenerate_zero_input():
+    w = _dims("C1", cert_eps=1e-5)
+    x = torch.zeros(3, w.dims.d, dtype=torch.bfloat16, device="cuda")
+    inp = make_inputs(w.dims, 3, w.seed, skip=("W", "V", "w_gate_up", "w_down", "x"))
+    idx, gate, _ = om.route(w.dims, x, inp["subkeys"])
+    torch.cuda.synchronize()
+    assert (idx.cpu().numpy() == np.arange(w.dims.top_k)).all()
+    np.testing.assert_allclose(gate.cpu().numpy(), 1.0 / w.dims.top_k, atol=1e-7)
+
+
+def test_route_k_equals_n():
+    d = om.LayerDims(d=16, n_rows=3, n_cols=4, top_k=12, d_ff=0, cert_eps=1e-5)
+    inp = make_inputs(d, 9, 4)
+    idx, gate, _ = om.route(d, inp["x"], inp["subkeys"])
+    torch.cuda.synchronize()
+    orc, rows = _oracle_route(d, 4, np.arange(9))
+    np.testing.assert_array_equal(idx.cpu().numpy().reshape(9, 12), orc["idx"])
+
+
+# ---------------------------------------------------------------- schedule
+def _check_plan(plan, ids, gates, toks, b, e):
+    p = oracle.schedule(ids, gates, toks, b, e)
+    m = int(p["offsets"][-1])
+    np.testing.assert_array_equal(plan["expert_offsets"].cpu().numpy(), p["offsets"])
+    np.testing.assert_array_equal(plan["sorted_token"].cpu().numpy()[:m], p["sorted_token"])
+    np.testing.assert_array_equal(plan["sorted_gate"].cpu().numpy()[:m].astype(np.float64), p["sorted_gate"])
+    na = int(plan["n_active"].item())
+    assert na == p["n_active"]
+    np.testing.assert_array_equal(plan["active"].cpu().numpy()[:na], p["active"])
+
+
+@pytest.mark.parametrize("N,L,HK,b,e", [(1024, 256, 8, 0, 1024), (65536, 2048, 64, 0, 65536),
+                                        (1 << 20, 4096, 512, 0, 1 << 20), (1000, 300, 7, 250, 700),
+                                        (5, 50, 3, 0, 5), (1 << 20, 16, 16, 1 << 19, 1 << 20)])
+def test_schedule_bit_exact(N, L, HK, b, e):
+    rng = np.random.default_rng(N + L)
+    ids = rng.integers(0, N, (L, HK)).astype(np.int32)
+    gates = rng.random((L, HK)).astype(np.float32)
+    d = om.LayerDims(d=8, n_rows=N, n_cols=1, top_k=HK, d_ff=0)
+    idx_t = torch.from_numpy(ids).cuda()
+    g_t = torch.from_numpy(gates).cuda()
+    plan = om.schedule(d, idx_t.reshape(-1), g_t.reshape(-1), expert_begin=b, expert_end=e)
+    torch.cuda.synchronize()
+    _check_plan(plan, ids.reshape(-1), gates.reshape(-1).astype(np.float64),
+                np.repeat(np.arange(L), HK).astype(np.int32), b, e)
+
+
+def test_schedule_all_same_expert_and_empty():
+    d = om.LayerDims(d=8, n_rows=64, n_cols=64, top_k=4, d_ff=0)
+    ids = np.full(40000, 17, np.int32)
+    gates = np.linspace(0, 1, 40000).astype(np.float32)
+    plan = om.schedule(d, torch.from_numpy(ids).cuda(), torch.from_numpy(gates).cuda())
+    torch.cuda.synchronize()
+    _check_plan(plan, ids, gates.astype(np.float64), (np.arange(40000) // 4).astype(np.int32), 0, 4096)
+    e = torch.empty(0, dtype=torch.int32, device="cuda")
+    plan = om.schedule(d, e, torch.empty(0, device="cuda"))
+    torch.cuda.synchronize()
+    assert plan["n_active"].item() == 0 and plan["expert_offsets"].cpu().numpy().max() == 0
+
+
+# ---------------------------------------------------------------- expert compute
+@pytest.mark.parametrize("dtype", [om.BF16, om.F32])
+@pytest.mark.parametrize("d,act", [(64, om.SILU), (72, om.SILU), (1024, om.SILU), (2048, om.SILU), (64, om.IDENTITY)])
+def test_expert_fwd_given_plan(dtype, d, act):
+    rng = np.random.default_rng(d)
+    L, N, HK = 200, 3000, 12
+    dims = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, dtype=dtype, act=act)
+    inp = make_inputs(dims, L, 9, skip=("subkeys",))
+    ids = np.stack([rng.choice(N, HK, replace=False) for _ in range(L)]).astype(np.int32)
+    gates = rng.random((L, HK)).astype(np.float32)
+    plan = om.schedule(dims, torch.from_numpy(ids).cuda().reshape(-1), torch.from_numpy(gates).cuda().reshape(-1))
+    y = om.expert_fwd(dims, inp["x"], inp["W"], inp["V"], plan)
+    torch.cuda.synchronize()
+    used = np.unique(ids)
+    remap = np.searchsorted(used, ids)
+    x = host_rows(dims, 9, "x", np.arange(L))
+    W = host_rows(dims, 9, "W", used)
+    V = host_rows(dims, 9, "V", used)
+    ref = oracle.routed_token_centric(x, W, V, remap, gates.astype(np.float64), act)
+    e_tok, e_elt = rel_errors(y.cpu().numpy(), ref)
+    tol = 1e-5 if dtype == om.F32 else 1e-2
+    assert e_tok <= tol and e_elt <= tol, (e_tok, e_elt)
+
+
+# ---------------------------------------------------------------- shared MLP
+@pytest.mark.parametrize("dtype", [om.BF16, om.F32])
+@pytest.mark.parametrize("L,d,dff", [(256, 64, 128), (300, 1024, 1024), (130, 256, 72)])
+def test_shared_mlp(dtype, L, d, dff):
+    dims = om.LayerDims(d=d, n_rows=2, n_cols=2, top_k=1, d_ff=dff, dtype=dtype)
+    inp = make_inputs(dims, L, 11, skip=("subkeys", "W", "V"))
+    yr = torch.randn(L, d, device="cuda")
+    y = om.shared_mlp(dims, inp["x"], inp["w_gate_up"], inp["w_down"], y_routed=yr)
+    torch.cuda.synchronize()
+    x = host_rows(dims, 11, "x", np.arange(L))
+    ref = oracle.shared_mlp(x, host_rows(dims, 11, "w_gate_up"), host_rows(dims, 11, "w_down")) + yr.cpu().double().numpy()
+    e_tok, e_elt = rel_errors(y.float().cpu().numpy(), ref)
+    tol = 1e-5 if dtype == om.F32 else 1e-2
+    assert e_tok <= tol and e_elt <= tol, (e_tok, e_elt)
+
+
+# ---------------------------------------------------------------- whole layer
+@pytest.mark.parametrize("dtype,mode,cert", [(om.BF16, synth.NORMAL, 1e-5), (om.BF16, synth.NORMAL, 0.0),
+                                             (om.BF16, synth.DYADIC, 1e-5), (om.F32, synth.NORMAL, 0.0)])
+def test_layer_c1(dtype, mode, cert):
+    w = _dims("C1", dtype=dtype, cert_eps=cert)
+    dims = w.dims
+    inp = make_inputs(dims, w.L, w.seed, mode)
+    y, idx, gate = om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], inp["V"], inp["w_gate_up"],
+                                inp["w_down"], return_routing=True)
+    torch.cuda.synchronize()
+    hr = lambda n, r=None: host_rows(dims, w.seed, n, r, mode)
+    ref = oracle.layer(hr("x", np.arange(w.L)), hr("subkeys").reshape(1, -1, dims.d), hr("W"), hr("V"),
+                       dims.n_rows, dims.n_cols, dims.top_k, hr("w_gate_up"), hr("w_down"))
+    assert np.array_equal(np.sort(idx.cpu().numpy(), -1), np.sort(ref["idx"], -1))
+    e_tok, e_elt = rel_errors(y.float().cpu().numpy(), ref["y"])
+    tol = 1e-5 if dtype == om.F32 else 1e-2
+    assert e_tok <= tol and e_elt <= tol, (e_tok, e_elt)
+
+
+def test_layer_no_shared_mlp_and_empty():
+    w = _dims("C1", d_ff=0, cert_eps=1e-5)
+    inp = make_inputs(w.dims, 64, w.seed)
+    y = om.layer_fwd(w.dims, inp["x"], inp["subkeys"], inp["W"], inp["V"])
+    torch.cuda.synchronize()
+    hr = lambda n, r=None: host_rows(w.dims, w.seed, n, r)
+    ref = oracle.layer(hr("x", np.arange(64)), hr("subkeys").reshape(1, -1, w.dims.d), hr("W"), hr("V"),
+                       w.dims.n_rows, w.dims.n_cols, w.dims.top_k)
+    e_tok, _ = rel_errors(y.float().cpu().numpy(), ref["y"])
+    assert e_tok <= 1e-2
+    y0 = om.layer_fwd(w.dims, inp["x"][:0], inp["subkeys"], inp["W"], inp["V"])
+    assert y0.shape == (0, w.dims.d)
+
+
+def test_errors_are_loud():
+    w = _dims("C1")
+    inp = make_inputs(w.dims, 8, w.seed)
+    bad = om.LayerDims(d=64, n_rows=4, n_cols=4, top_k=17)
+    with pytest.raises(om.OmniMoEError, match="SHAPE"):
+        om.route(bad, inp["x"], torch.empty(1 * 8 * 64, dtype=torch.bfloat16, device="cuda"))
+    with pytest.raises(om.OmniMoEError):
+        om.route(w.dims, inp["x"].cpu(), inp["subkeys"])
