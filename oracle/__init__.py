@@ -35,6 +35,8 @@ def lib():
         build()
         _lib = ctypes.CDLL(_SO)
         _lib.oracle_logits.argtypes = [i64, i64, i64, i64, P, P, P, c_int]
+        _lib.oracle_exact_dot.argtypes = [P, P, i64]
+        _lib.oracle_exact_dot.restype = ctypes.c_float
         _lib.oracle_route.argtypes = [i64, i64, i64, i64, P, c_int, i64, c_int, P, P, P, P, P, P]
         _lib.oracle_schedule.argtypes = [i64, P, P, P, i64, i64, P, P, P, P, P]
         _lib.oracle_routed_token_centric.argtypes = [i64, i64, i64, P, P, P, P, P, c_int, P, c_int]
@@ -60,8 +62,16 @@ def default_threads() -> int:
     return os.cpu_count() or 1
 
 
+def exact_dot(x, w) -> float:
+    """RN32 of the exact real dot product of two fp32-representable vectors (Q9)."""
+    x, w = _f64(x).reshape(-1), _f64(w).reshape(-1)
+    assert x.size == w.size
+    return float(lib().oracle_exact_dot(_p(x), _p(w), x.size))
+
+
 def logits(x, subkeys, nthreads=None):
-    """x: [L][d], subkeys: [h][R][d] (exactly-decoded values) -> fp32 [L][h][R]."""
+    """x: [L][d], subkeys: [h][R][d] (exactly-decoded values) -> fp32 [L][h][R],
+    each the RN32 of the exact dot product (reading Q9)."""
     x, subkeys = _f64(x), _f64(subkeys)
     L, d = x.shape
     h, R, _ = subkeys.shape

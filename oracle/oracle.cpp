@@ -55,6 +55,77 @@ inline bool precedes(const Key& p, const Key& q) {
   return p.n < q.n;
 }
 
+// --------------------------------------------------------------------------
+// Exact dot product of fp32-representable values, rounded ONCE to fp32 with
+// round-to-nearest-even (reading Q9: "scores computed in fp32 from
+// bf16-rounded inputs" = RN32 of the real dot product).  Every input is an
+// integer mantissa m (|m| < 2^24) times 2^e, so every product is an integer
+// (< 2^48) times 2^(e1+e2); the products are summed exactly in a 128-bit
+// integer at the smallest product exponent, then rounded to 24 significant
+// bits.  Inputs that are not fp32 values, or whose product exponents spread
+// beyond the 128-bit accumulator, give NaN (never the case for bf16/fp32
+// tensors of the synthetic generator; tests/test_oracle.py checks the NaN).
+// --------------------------------------------------------------------------
+struct Dyadic {
+  int64_t m;  // odd or zero
+  int e;
+  bool ok;    // false: not an fp32-representable value
+};
+
+inline Dyadic to_dyadic(double v) {
+  if (v == 0.0) return Dyadic{0, 0, true};
+  if (!std::isfinite(v)) return Dyadic{0, 0, false};
+  int ex;
+  double f = std::frexp(v, &ex);                 // v = f * 2^ex, 0.5 <= |f| < 1
+  int64_t m = (int64_t)std::ldexp(f, 53);        // exact: v has <= 53 significant bits
+  int e = ex - 53;
+  while ((m & 1) == 0) { m /= 2; ++e; }
+  return Dyadic{m, e, m < (int64_t(1) << 24) && m > -(int64_t(1) << 24)};
+}
+
+inline float round_int128_to_f32(__int128 S, int e) {  // RN32(S * 2^e)
+  if (S == 0) return 0.0f;
+  const bool neg = S < 0;
+  unsigned __int128 a = neg ? (unsigned __int128)(-S) : (unsigned __int128)S;
+  int msb = 127;
+  while (!((a >> msb) & 1)) --msb;
+  if (msb > 23) {  // keep 24 significant bits, round half to even
+    const int sh = msb - 23;
+    unsigned __int128 q = a >> sh;
+    unsigned __int128 rem = a - (q << sh);
+    unsigned __int128 half = (unsigned __int128)1 << (sh - 1);
+    if (rem > half || (rem == half && (q & 1))) q += 1;
+    a = q;
+    e += sh;
+  }
+  // a < 2^25 now: exact in double; scaling by 2^e is exact for normal fp32 results
+  const double r = std::ldexp((double)(uint64_t)a, e);
+  return (float)(neg ? -r : r);
+}
+
+inline float exact_dot_rn32(const double* x, const double* w, int64_t d) {
+  std::vector<Dyadic> p;
+  p.reserve(d);
+  int emin = 1 << 30;
+  for (int64_t k = 0; k < d; ++k) {
+    Dyadic a = to_dyadic(x[k]), b = to_dyadic(w[k]);
+    if (!a.ok || !b.ok) return NAN;
+    if (a.m == 0 || b.m == 0) continue;
+    Dyadic q{a.m * b.m, a.e + b.e, true};
+    emin = std::min(emin, q.e);
+    p.push_back(q);
+  }
+  __int128 S = 0;
+  for (const Dyadic& q : p) {
+    const int sh = q.e - emin;
+    int bits = 0;
+    for (uint64_t a = (uint64_t)(q.m < 0 ? -q.m : q.m); a; a >>= 1) ++bits;
+    if (bits + sh > 126 - 20) return NAN;  // beyond the 128-bit accumulator (d <= 2^20)
+    S += (__int128)q.m << sh;
+  }
+  return round_int128_to_f32(S, emin);
+}
+
 inline double silu(double z) { return z / (1.0 + std::exp(-z)); }  // reading Q1
 
 inline double act_fn(double z, int act) { return act == 1 ? z : silu(z); }
@@ -153,23 +224,21 @@ void select_blockmerge(const float* sr, int64_t Nr, const float* sc, int64_t Nc,
 
 extern "C" {
 
-// O1 canonical logits (Eq.Logits; reading Q9): for each token
-// l, head h and sub-key row r (rows [0,N_r) are W_r's columns, rows
-// [N_r, N_r+N_c) are W_c's), acc = sum_k x[l][k]*sub[h][r][k] accumulated
-// sequentially in double, then rounded to fp32 (round-to-nearest-even).
+// O1 logits (Eq.Logits; reading Q9): for each token l, head h
+// and sub-key row r (rows [0,N_r) are W_r's columns, rows [N_r, N_r+N_c) are
+// W_c's), s = RN32(sum_k x[l][k]*sub[h][r][k]) -- the fp32 round-to-nearest-
+// even of the EXACT real dot product (exact_dot_rn32 above).
 void oracle_logits(int64_t L, int64_t d, int64_t h, int64_t R, const double* x, const double* sub,
                    float* out, int nthreads) {
   parallel_for(L, nthreads, [&](int64_t l) {
     for (int64_t hh = 0; hh < h; ++hh)
-      for (int64_t r = 0; r < R; ++r) {
-        const double* xr = x + l * d;
-        const double* sw = sub + (hh * R + r) * d;
-        double acc = 0.0;
-        for (int64_t k = 0; k < d; ++k) acc += xr[k] * sw[k];
-        out[(l * h + hh) * R + r] = (float)acc;
-      }
+      for (int64_t r = 0; r < R; ++r)
+        out[(l * h + hh) * R + r] = exact_dot_rn32(x + l * d, sub + (hh * R + r) * d, d);
   });
 }
+
+// Exact dot product rounded once to fp32, exported for the pins.
+float oracle_exact_dot(const double* x, const double* w, int64_t d) { return exact_dot_rn32(x, w, d); }
 
 // O2-O5 routing for a batch of token-heads (Eq.TopK + Eq.Gate, PAPER:131-139;
 // Eq.S).  logits: [T][N_r + N_c] fp32 (T = L*h token-heads).
@@ -315,7 +384,7 @@ void oracle_shared_mlp(int64_t L, int64_t d, int64_t d_ff, const double* x, cons
 }
 
 // Whole layer for a batch of tokens (Eq.MoE):
-// canonical logits -> product selection -> gates -> token-centric routed
+// exact logits (Q9) -> product selection -> gates -> token-centric routed
 // branch (sum over heads) -> + shared MLP.  Used for the CPU baseline timing
 // (bench.py cpu_baseline / --impl reference) and as the layer parity oracle.
 // subkeys: [h][N_r+N_c][d]; W, V: [N][d] (full tables, or compact tables when
@@ -332,12 +401,7 @@ void oracle_layer(int64_t L, int64_t d, int64_t Nr, int64_t Nc, int64_t K, int64
     std::vector<float> lg(R);
     std::vector<double> yl(d, 0.0);
     for (int64_t hh = 0; hh < h; ++hh) {
-      for (int64_t r = 0; r < R; ++r) {
-        const double* sw = subkeys + (hh * R + r) * d;
-        double acc = 0.0;
-        for (int64_t k = 0; k < d; ++k) acc += xl[k] * sw[k];
-        lg[r] = (float)acc;
-      }
+      for (int64_t r = 0; r < R; ++r) lg[r] = exact_dot_rn32(xl, subkeys + (hh * R + r) * d, d);
       std::vector<Key> top;
       select_product(lg.data(), Nr, lg.data() + Nr, Nc, K, top);
       double k1 = top[0].hi + top[0].lo, den = 0.0;

@@ -111,7 +111,7 @@ def test_single_row_reduces_to_column_topk():
 def test_zero_input_uniform():
     """x = 0 -> all keys 0 -> ids [0..K), gates 1/K (reading Q20)."""
     x = np.zeros((3, 16))
-    sub = np.random.default_rng(0).standard_normal((1, 8 + 8, 16))
+    sub = np.random.default_rng(0).standard_normal((1, 8 + 8, 16)).astype(np.float32)
     lg = oracle.logits(x, sub)
     r = oracle.route(lg.reshape(3, 16), 8, 8, 5)
     for t in range(3):
@@ -178,6 +178,61 @@ def test_logits_exact_integer(mode):
                 acc = int(np.dot(xi[l], si[hh, r]))  # exact (< 2^53)
                 v = float(Fraction(acc, 2 ** (ex[synth.TID_X] + ex[synth.TID_SUBKEYS])))
                 assert out[l, hh, r] == np.float32(v)
+
+
+# ---- Q9: logits are RN32 of the exact dot product -----------------------------------
+def _rn32_of_fraction(fr):
+    """Round a rational to the nearest fp32 (ties to even) with Python integers only."""
+    if fr == 0:
+        return 0.0
+    neg, a = fr < 0, abs(fr)
+    e = a.numerator.bit_length() - a.denominator.bit_length() - 24
+    while a / Fraction(2) ** e >= 2 ** 24:
+        e += 1
+    while a / Fraction(2) ** e < 2 ** 23:
+        e -= 1
+    q = a / Fraction(2) ** e
+    n = q.numerator // q.denominator
+    rem = q - n
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and n % 2 == 1):
+        n += 1
+    v = float(np.float32(n * 2.0 ** e))
+    assert Fraction(v) == n * Fraction(2) ** e  # representable: the rounding above was the only one
+    return -v if neg else v
+
+
+def _exact_dot(x, w):
+    return sum((Fraction(float(a)) * Fraction(float(b)) for a, b in zip(x, w)), Fraction(0))
+
+
+def test_exact_dot_random_vs_fractions():
+    rng = np.random.default_rng(31)
+    for trial in range(300):
+        d = int(rng.integers(1, 80))
+        if trial % 3 == 0:  # bf16 values of the generator's kind
+            x = synth.bf16_bits_to_f64(synth.f32_to_bf16_bits(rng.standard_normal(d).astype(np.float32)))
+            w = synth.bf16_bits_to_f64(synth.f32_to_bf16_bits((rng.standard_normal(d) / 8).astype(np.float32)))
+        else:  # fp32 values spanning many binades
+            x = (rng.standard_normal(d) * 2.0 ** rng.integers(-12, 12, d)).astype(np.float32).astype(np.float64)
+            w = (rng.standard_normal(d) * 2.0 ** rng.integers(-12, 12, d)).astype(np.float32).astype(np.float64)
+        assert oracle.exact_dot(x, w) == _rn32_of_fraction(_exact_dot(x, w))
+
+
+def test_exact_dot_double_rounding_cases():
+    """1 + 2^-24 + 2^-60: fp64 accumulation drops 2^-60 and then ties to even (1.0);
+    the exact value lies above the fp32 midpoint, so RN32 gives 1 + 2^-23."""
+    one = np.ones(3)
+    assert oracle.exact_dot([1.0, 2.0 ** -24, 2.0 ** -60], one) == 1.0 + 2.0 ** -23
+    assert oracle.exact_dot([1.0, 2.0 ** -24, -(2.0 ** -60)], one) == 1.0  # just below: down
+    assert oracle.exact_dot([1.0, 2.0 ** -24], [1.0, 1.0]) == 1.0  # exact tie: to even
+    assert oracle.exact_dot([1.0 + 2.0 ** -23, 2.0 ** -24], [1.0, 1.0]) == 1.0 + 2.0 ** -22  # tie: to even (up)
+    assert oracle.exact_dot([3.0, -3.0], [5.0, 5.0]) == 0.0
+    # a cancellation that fp64 sequential summation gets wrong
+    x, w = [2.0 ** 40, 1.0, -(2.0 ** 40)], [1.0, 2.0 ** -30, 1.0]
+    assert oracle.exact_dot(x, w) == 2.0 ** -30
+    # contract: fp32-representable inputs only; anything else is reported as NaN
+    assert np.isnan(oracle.exact_dot([0.1], [1.0]))
+    assert np.isnan(oracle.exact_dot([2.0 ** 100, 2.0 ** -100], [1.0, 1.0]))
 
 
 # ---- P5: schedule + executor identity ----------------------------------------------
