@@ -174,7 +174,6 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cert-eps", type=float, default=None, help="override the config's router bound")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -186,7 +185,7 @@ def main():
     from paper_2602_05711_b200 import build, configs, omnimoe as om
     build.build()
     from synth.workloads import make_inputs
-    w = configs.get(args.config) if args.cert_eps is None else configs.get(args.config, cert_eps=args.cert_eps)
+    w = configs.get(args.config)
     dims = w.dims
     L = w.L
     if ws > 1:
@@ -308,7 +307,7 @@ def main():
         "data": "synthetic",
         "config": {"workload": w.name, "d": dims.d, "n_rows": dims.n_rows, "n_cols": dims.n_cols,
                    "top_k": dims.top_k, "n_heads": dims.n_heads, "d_ff": dims.d_ff, "tokens": L,
-                   "cert_eps": dims.cert_eps, "parallelism": "single-gpu",
+                   "router": "exact (int8 tcgen05 limbs)", "parallelism": "single-gpu",
                    "l2": "flushed (256 MB write) before every timed step"},
         "stage_ms": stage_ms, "n_active": n_active, "tasks": M,
         "step_ms_min_max": [min(step_ms), max(step_ms)],

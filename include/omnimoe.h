@@ -52,26 +52,33 @@ enum { OMNIMOE_EXPERT_AUTO = 0, OMNIMOE_EXPERT_WARP = 1 };
 /* workspace query selector */
 enum { OMNIMOE_WS_ROUTE = 0, OMNIMOE_WS_SCHEDULE = 1, OMNIMOE_WS_EXPERT = 2, OMNIMOE_WS_LAYER = 3 };
 
+/* How omnimoe_route computes the sub-key logits.  Both give the same bits:
+ * logit = RN32(exact dot product x . w) (reading Q9).
+ *   EXACT      tcgen05 kind::i8 products of 3 int8 digits per operand (fast);
+ *              rows whose exponents span > 22 bits fall back to EXACT_F64.
+ *   EXACT_F64  fp64 double-double dot products on CUDA cores (slow reference). */
+enum { OMNIMOE_ROUTER_EXACT = 0, OMNIMOE_ROUTER_EXACT_F64 = 1 };
+
 /* Layer dimensions.
- *   d        hidden size (multiple of 8)
- *   n_rows   N_r, n_cols N_c: the Cartesian grid, N = N_r * N_c; flat expert id
- *            n = i*N_c + j (row-major, reading Q6)
- *   top_k    K experts per token and head (Eq.TopK), 1 <= K <= N
- *   n_heads  h independent sub-key table pairs over one shared expert pool
- *            (reading Q3); h = 1 is exactly the paper
- *   d_ff     shared-MLP width (0: no shared branch)
- *   cert_eps router certification bound:
- *            > 0: fast tcgen05 logits; a token-head whose fast K/K+1 key gap is
- *                 <= 4*cert_eps is recomputed with canonical fp64 logits;
- *            <= 0: canonical fp64 logits for every token-head (slow, exact).
- *            Ignored in OMNIMOE_F32 mode (always canonical).
+ *   d          hidden size (multiple of 8)
+ *   n_rows     N_r, n_cols N_c: the Cartesian grid, N = N_r * N_c; flat expert id
+ *              n = i*N_c + j (row-major, reading Q6)
+ *   top_k      K experts per token and head (Eq.TopK), 1 <= K <= N
+ *   n_heads    h independent sub-key table pairs over one shared expert pool
+ *              (reading Q3); h = 1 is exactly the paper
+ *   d_ff       shared-MLP width (0: no shared branch)
+ *   router     OMNIMOE_ROUTER_* (ignored in OMNIMOE_F32 mode: always EXACT_F64)
+ *   expert_kernel  OMNIMOE_EXPERT_* (a6 kernel choice)
+ *   group_size B of Expert-Centric Scheduling: consecutive active
+ *              experts per group; 1 = expert-major plan; 0 = library choice.
  */
 typedef struct {
   int64_t d, n_rows, n_cols, top_k, n_heads, d_ff;
   int32_t dtype;         /* OMNIMOE_BF16 | OMNIMOE_F32 */
   int32_t act;           /* OMNIMOE_SILU | OMNIMOE_IDENTITY */
-  float cert_eps;
+  int32_t router;        /* OMNIMOE_ROUTER_* */
   int32_t expert_kernel; /* OMNIMOE_EXPERT_* */
+  int64_t group_size;    /* B >= 0 */
 } omnimoe_dims;
 
 /* Expert-centric plan for the local expert range [expert_begin, expert_end)
@@ -102,7 +109,8 @@ omnimoe_status omnimoe_workspace_size(const omnimoe_dims* dims, int64_t L, int w
                                       size_t* bytes);
 
 /* Cartesian Product Router: Eq.Logits s_r = x W_r, s_c = x W_c
- * with both halves of each head projected from the full x; exact top-K over the
+ * with both halves of each head projected from the full x, each logit the fp32
+ * rounding of the exact dot product (Q9); exact top-K over the
  * implicit grid S_ij = s_r[i] + s_c[j] (Eq.S; ranking on raw logits is identical
  * to ranking on the log-probabilities, reading Q8), ties between exactly equal
  * keys broken toward the lower flat id (Q7); gates = softmax over the selected
@@ -167,12 +175,14 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
                                  int32_t* idx_out, float* gate_out, void* ws, size_t ws_bytes,
                                  omnimoe_stream_t stream);
 
-/* Raw fast router logits (the tcgen05 GEMM of the route call), for measuring
- * the certification bound: logits float [L][h][n_rows+n_cols].  canonical != 0
- * computes the canonical fp64 logits instead. */
+/* The sub-key logits of the route call, for measurement and parity:
+ * logits float [L][h][n_rows+n_cols].  method 0: the route path (dims.router);
+ * 1: exact fp64 double-double kernel; 2: bf16 tcgen05 GEMM with fp32
+ * accumulation (NOT exact -- only to measure what exactness costs).
+ * ws: at least omnimoe_workspace_size(OMNIMOE_WS_ROUTE) bytes. */
 omnimoe_status omnimoe_router_logits(const omnimoe_dims* dims, int64_t L, const void* x,
-                                     const void* subkeys, float* logits, int canonical,
-                                     omnimoe_stream_t stream);
+                                     const void* subkeys, float* logits, int method, void* ws,
+                                     size_t ws_bytes, omnimoe_stream_t stream);
 
 /* Plain GEMM on the library's tcgen05 engine (bf16 in, fp32 out):
  * C[M][N] = A[M][K] . B[N][K]^T.  Exposed for engine tests / roofline. */

@@ -74,6 +74,14 @@ omnimoe_status validate_dims(const omnimoe_dims* dp) {
     set_error("unknown activation " + std::to_string(d.act));
     return OMNIMOE_ERR_UNSUPPORTED;
   }
+  if (d.router != OMNIMOE_ROUTER_EXACT && d.router != OMNIMOE_ROUTER_EXACT_F64) {
+    set_error("unknown router mode " + std::to_string(d.router));
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  if (d.group_size < 0) {
+    set_error("group_size must be >= 0");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
   if (d.expert_kernel != OMNIMOE_EXPERT_AUTO && d.expert_kernel != OMNIMOE_EXPERT_WARP) {
     set_error("unknown expert kernel " + std::to_string(d.expert_kernel));
     return OMNIMOE_ERR_UNSUPPORTED;
@@ -90,20 +98,15 @@ omnimoe_status validate_dims(const omnimoe_dims* dp) {
   return OMNIMOE_OK;
 }
 
-bool fast_logits(const omnimoe_dims& d) { return d.dtype == OMNIMOE_BF16 && d.cert_eps > 0.f; }
+bool i8_logits(const omnimoe_dims& d) { return d.dtype == OMNIMOE_BF16 && d.router == OMNIMOE_ROUTER_EXACT; }
 
-size_t route_ws(const omnimoe_dims& d, int64_t L, bool carve, void* ws, float** logits,
-                int32_t** flag_list, int32_t** flag_count) {
+size_t route_ws(const omnimoe_dims& d, int64_t L, void* ws, float** logits, void** sub_ws) {
   Carver c(ws);
   const int64_t T = L * d.n_heads;
-  float* lg = c.take<float>((size_t)T * (d.n_rows + d.n_cols));
-  int32_t* fl = c.take<int32_t>((size_t)std::max<int64_t>(T, 1));
-  int32_t* fc = c.take<int32_t>(1);
-  if (carve) {
-    *logits = lg;
-    *flag_list = fl;
-    *flag_count = fc;
-  }
+  float* lg = c.take<float>((size_t)std::max<int64_t>(T, 1) * (d.n_rows + d.n_cols));
+  void* sw = c.take<char>(exact_logits_ws_bytes(d, L));
+  if (logits) *logits = lg;
+  if (sub_ws) *sub_ws = sw;
   return c.bytes();
 }
 
@@ -124,7 +127,7 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
   Carver c(ws);
   const int64_t N = d.n_rows * d.n_cols;
   const int64_t M = L * d.n_heads * d.top_k;
-  const size_t rb = route_ws(d, L, false, nullptr, nullptr, nullptr, nullptr);
+  const size_t rb = route_ws(d, L, nullptr, nullptr, nullptr);
   void* rw = c.take<char>(rb);
   int32_t* idx = c.take<int32_t>((size_t)std::max<int64_t>(M, 1));
   float* gate = c.take<float>((size_t)std::max<int64_t>(M, 1));
@@ -159,41 +162,24 @@ omnimoe_status check_ws(size_t have, size_t need, const char* who) {
   return OMNIMOE_OK;
 }
 
+omnimoe_status logits_impl(const omnimoe_dims& d, int64_t L, const void* x, const void* subkeys, float* logits,
+                           void* sub_ws, cudaStream_t st) {
+  const int NC = (int)(d.n_heads * (d.n_rows + d.n_cols));
+  if (i8_logits(d)) return exact_logits(d, L, x, subkeys, logits, sub_ws, st);
+  return launch_exact_dd(d.dtype, x, subkeys, (int)d.d, NC, (int)L, logits, 0, nullptr, nullptr, st);
+}
+
+// a1 (exact logits, Q9) -> a2 + a3 (select_kernel)
 omnimoe_status route_impl(const omnimoe_dims& d, int64_t L, const void* x, const void* subkeys,
                           int32_t* idx, float* gate, float* score, void* ws, cudaStream_t st) {
   float* logits;
-  int32_t *flag_list, *flag_count;
-  route_ws(d, L, true, ws, &logits, &flag_list, &flag_count);
-  const int64_t T = L * d.n_heads;
-  const int R = (int)(d.n_rows + d.n_cols);
+  void* sub_ws;
+  route_ws(d, L, ws, &logits, &sub_ws);
   SelectParams sp;
   size_t smem;
-  OMNI_TRY(select_params(d, T, &sp, &smem));
-  if (!fast_logits(d)) {
-    sp.cert_eps = 0.f;
-    OMNI_TRY(launch_canon_logits(d.dtype, x, subkeys, (int)d.d, (int)d.n_heads, R, logits, (int)T,
-                                 nullptr, nullptr, st));
-    return launch_select(sp, smem, logits, idx, gate, score, nullptr, nullptr, nullptr, nullptr, st);
-  }
-  // a1: tcgen05 sub-key scoring GEMM, x [L][d] . subkeys [h*R][d]^T -> logits [L][h*R]
-  GemmArgs ga;
-  ga.M = (int)L;
-  ga.N = (int)(d.n_heads * R);
-  ga.K = (int)d.d;
-  ga.out_f32 = logits;
-  OMNI_TRY(gemm_bf16(EPI_F32, x, subkeys, ga, st));
-  if (cudaMemsetAsync(flag_count, 0, sizeof(int32_t), st) != cudaSuccess) {
-    set_error("route: memset failed");
-    return OMNIMOE_ERR_CUDA;
-  }
-  // a2+a3 on fast logits, flagging uncertified token-heads
-  sp.cert_eps = d.cert_eps;
-  OMNI_TRY(launch_select(sp, smem, logits, idx, gate, score, flag_list, flag_count, nullptr, nullptr, st));
-  // canonical fp64 logits + exact reselection for the flagged token-heads only
-  OMNI_TRY(launch_canon_logits(d.dtype, x, subkeys, (int)d.d, (int)d.n_heads, R, logits, (int)T,
-                               flag_list, flag_count, st));
-  sp.cert_eps = 0.f;
-  return launch_select(sp, smem, logits, idx, gate, score, nullptr, nullptr, flag_list, flag_count, st);
+  OMNI_TRY(select_params(d, L * d.n_heads, &sp, &smem));
+  OMNI_TRY(logits_impl(d, L, x, subkeys, logits, sub_ws, st));
+  return launch_select(sp, smem, logits, idx, gate, score, st);
 }
 
 omnimoe_status mlp_impl(const omnimoe_dims& d, int64_t L, const void* x, const void* wgu,
@@ -248,7 +234,7 @@ omnimoe_status omnimoe_workspace_size(const omnimoe_dims* dims, int64_t L, int w
   }
   const omnimoe_dims& d = *dims;
   switch (which) {
-    case OMNIMOE_WS_ROUTE: *bytes = route_ws(d, L, false, nullptr, nullptr, nullptr, nullptr); break;
+    case OMNIMOE_WS_ROUTE: *bytes = route_ws(d, L, nullptr, nullptr, nullptr); break;
     case OMNIMOE_WS_SCHEDULE: *bytes = schedule_ws_bytes(L, d.n_rows * d.n_cols); break;
     case OMNIMOE_WS_EXPERT: *bytes = expert_ws_bytes(d, L); break;
     case OMNIMOE_WS_LAYER: *bytes = layer_ws(d, L, nullptr, nullptr); break;
@@ -274,7 +260,12 @@ omnimoe_status omnimoe_route(const omnimoe_dims* dims, int64_t L, const void* x,
   OMNI_NONNULL(idx, "idx");
   OMNI_NONNULL(gate, "gate");
   OMNI_NONNULL(ws, "ws");
-  OMNI_TRY(check_ws(ws_bytes, route_ws(*dims, L, false, nullptr, nullptr, nullptr, nullptr), "route"));
+  OMNI_TRY(check_ws(ws_bytes, route_ws(*dims, L, nullptr, nullptr, nullptr), "route"));
+  {
+    SelectParams sp;
+    size_t smem;
+    OMNI_TRY(select_params(*dims, L * dims->n_heads, &sp, &smem));
+  }
   OMNI_TRY(check_device());
   return route_impl(*dims, L, x, subkeys, idx, gate, score, ws, (cudaStream_t)stream);
 }
@@ -402,25 +393,38 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
 }
 
 omnimoe_status omnimoe_router_logits(const omnimoe_dims* dims, int64_t L, const void* x, const void* subkeys,
-                                     float* logits, int canonical, omnimoe_stream_t stream) {
+                                     float* logits, int method, void* ws, size_t ws_bytes,
+                                     omnimoe_stream_t stream) {
   reset_launch_count();
   OMNI_TRY(validate_dims(dims));
   if (L == 0) return OMNIMOE_OK;
   OMNI_NONNULL(x, "x");
   OMNI_NONNULL(subkeys, "subkeys");
   OMNI_NONNULL(logits, "logits");
+  if (method < 0 || method > 2 || (method == 2 && dims->dtype != OMNIMOE_BF16)) {
+    set_error("router_logits: method must be 0 (route path), 1 (exact fp64) or 2 (bf16 tcgen05, bf16 only)");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (method == 0) {
+    OMNI_NONNULL(ws, "ws");
+    OMNI_TRY(check_ws(ws_bytes, route_ws(*dims, L, nullptr, nullptr, nullptr), "router_logits"));
+  }
   OMNI_TRY(check_device());
   const omnimoe_dims& d = *dims;
-  const int R = (int)(d.n_rows + d.n_cols);
-  if (canonical || d.dtype != OMNIMOE_BF16)
-    return launch_canon_logits(d.dtype, x, subkeys, (int)d.d, (int)d.n_heads, R, logits,
-                               (int)(L * d.n_heads), nullptr, nullptr, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int NC = (int)(d.n_heads * (d.n_rows + d.n_cols));
+  if (method == 0) {
+    void* sub_ws;
+    route_ws(d, L, ws, nullptr, &sub_ws);
+    return logits_impl(d, L, x, subkeys, logits, sub_ws, st);
+  }
+  if (method == 1) return launch_exact_dd(d.dtype, x, subkeys, (int)d.d, NC, (int)L, logits, 0, nullptr, nullptr, st);
   GemmArgs ga;
   ga.M = (int)L;
-  ga.N = (int)(d.n_heads * R);
+  ga.N = NC;
   ga.K = (int)d.d;
   ga.out_f32 = logits;
-  return gemm_bf16(EPI_F32, x, subkeys, ga, (cudaStream_t)stream);
+  return gemm_bf16(EPI_F32, x, subkeys, ga, st);
 }
 
 omnimoe_status omnimoe_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, const void* B, float* C,

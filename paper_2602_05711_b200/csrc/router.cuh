@@ -11,16 +11,21 @@ struct SelectParams {
   int n_rows, n_cols;  // N_r, N_c
   int top_k;           // K
   int kr1, kc1;        // min(K+1, N_r), min(K+1, N_c): per-half list lengths
-  int pr, pcol, pc;    // power-of-two padded sizes: rows, cols, candidates
-  float cert_eps;      // > 0: flag token-heads whose K/K+1 gap <= 4*cert_eps
+  int C;               // product candidates (a*b <= K+1)
+  int pkr, pkc, pkeep; // power-of-two sort sizes: row list, column list, K+1 selected
 };
 
 omnimoe_status select_params(const omnimoe_dims& d, int64_t T, SelectParams* p, size_t* smem);
 omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* logits, int32_t* idx,
-                             float* gate, float* score, int32_t* flag_list, int32_t* flag_count,
-                             const int32_t* list, const int32_t* list_count, cudaStream_t st);
-omnimoe_status launch_canon_logits(int dtype, const void* x, const void* sub, int d, int h, int R,
-                                   float* logits, int T, const int32_t* list,
-                                   const int32_t* list_count, cudaStream_t st);
+                             float* gate, float* score, cudaStream_t st);
+
+// a1: exact logits RN32(x . sub) (reading Q9), [L][h*(N_r+N_c)] fp32.
+size_t exact_logits_ws_bytes(const omnimoe_dims& d, int64_t L);
+omnimoe_status exact_logits(const omnimoe_dims& d, int64_t L, const void* x, const void* sub, float* logits,
+                            void* ws, cudaStream_t st);
+// exact fp64 double-double path: mode 0 all logits, 1 tokens in list, 2 sub-key rows in list.
+omnimoe_status launch_exact_dd(int dtype, const void* x, const void* sub, int d, int NC, int L,
+                               float* logits, int mode, const int32_t* list, const int32_t* list_count,
+                               cudaStream_t st);
 
 }  // namespace omni

@@ -19,6 +19,8 @@ LIB_PATH = os.path.join(_PKG, "libomnimoe.so")
 BF16, F32 = 0, 1
 SILU, IDENTITY = 0, 1
 EXPERT_AUTO, EXPERT_WARP = 0, 1
+ROUTER_EXACT, ROUTER_EXACT_F64 = 0, 1
+LOGITS_ROUTE, LOGITS_EXACT_F64, LOGITS_BF16_FAST = 0, 1, 2
 WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER = 0, 1, 2, 3
 
 
@@ -29,8 +31,8 @@ class OmniMoEError(RuntimeError):
 class Dims(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int64), ("n_rows", ctypes.c_int64), ("n_cols", ctypes.c_int64),
                 ("top_k", ctypes.c_int64), ("n_heads", ctypes.c_int64), ("d_ff", ctypes.c_int64),
-                ("dtype", ctypes.c_int32), ("act", ctypes.c_int32), ("cert_eps", ctypes.c_float),
-                ("expert_kernel", ctypes.c_int32)]
+                ("dtype", ctypes.c_int32), ("act", ctypes.c_int32), ("router", ctypes.c_int32),
+                ("expert_kernel", ctypes.c_int32), ("group_size", ctypes.c_int64)]
 
 
 class Plan(ctypes.Structure):
@@ -64,7 +66,7 @@ def load(path: str = LIB_PATH):
         "omnimoe_expert_fwd": [PD, I64, V, V, V, PP, V, I32, V, SZ, V],
         "omnimoe_shared_mlp": [PD, I64, V, V, V, V, V, V, SZ, V],
         "omnimoe_layer_fwd": [PD, I64, V, V, V, V, V, V, V, V, V, V, SZ, V],
-        "omnimoe_router_logits": [PD, I64, V, V, V, I32, V],
+        "omnimoe_router_logits": [PD, I64, V, V, V, I32, V, SZ, V],
         "omnimoe_gemm_bf16": [I64, I64, I64, V, V, V, V],
     }
     for name, args in sig.items():
@@ -100,8 +102,9 @@ class LayerDims:
     d_ff: int = 0
     dtype: int = BF16
     act: int = SILU
-    cert_eps: float = 0.0
+    router: int = ROUTER_EXACT
     expert_kernel: int = EXPERT_AUTO
+    group_size: int = 0
 
     @property
     def N(self) -> int:
@@ -113,7 +116,7 @@ class LayerDims:
 
     def c(self) -> Dims:
         return Dims(self.d, self.n_rows, self.n_cols, self.top_k, self.n_heads, self.d_ff,
-                    self.dtype, self.act, self.cert_eps, self.expert_kernel)
+                    self.dtype, self.act, self.router, self.expert_kernel, self.group_size)
 
 
 def _ptr(t):
@@ -262,13 +265,17 @@ def layer_fwd(dims: LayerDims, x, subkeys, W, V, w_gate_up=None, w_down=None, y=
     return (y, idx, gate) if return_routing else y
 
 
-def router_logits(dims: LayerDims, x, subkeys, canonical=False):
+def router_logits(dims: LayerDims, x, subkeys, method=LOGITS_ROUTE, ws=None):
+    """Sub-key logits [L][h][N_r+N_c] fp32.  method: LOGITS_ROUTE (what route uses),
+    LOGITS_EXACT_F64, LOGITS_BF16_FAST (inexact fp32-accumulated tcgen05, measurement only)."""
     L = x.shape[0]
     _req(x, "x", dims.torch_dtype, L * dims.d)
+    _req(subkeys, "subkeys", dims.torch_dtype, dims.n_heads * (dims.n_rows + dims.n_cols) * dims.d)
     out = torch.empty((L, dims.n_heads, dims.n_rows + dims.n_cols), dtype=torch.float32, device=x.device)
+    ws = ws if ws is not None else workspace(dims, L, WS_ROUTE, x.device)
     dc = dims.c()
-    _check(load().omnimoe_router_logits(ctypes.byref(dc), L, _ptr(x), _ptr(subkeys), _ptr(out),
-                                        int(canonical), _stream()), "router_logits")
+    _check(load().omnimoe_router_logits(ctypes.byref(dc), L, _ptr(x), _ptr(subkeys), _ptr(out), int(method),
+                                        _ptr(ws), ws.numel(), _stream()), "router_logits")
     return out
 
 

@@ -42,7 +42,8 @@ def test_sm100a_code_only(lib):
     out = subprocess.run(["cuobjdump", "--list-elf", build.LIB], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", build.LIB], capture_output=True, text=True).stdout
-    assert "UTCHMMA" in sass and "UTMALDG" in sass  # tcgen05 MMA + TMA in the GEMM engine
+    assert "UTCHMMA" in sass and "UTMALDG" in sass  # tcgen05 bf16 MMA + TMA in the GEMM engine
+    assert "UTCIMMA" in sass  # tcgen05 kind::i8 MMA of the exact router logits
 
 
 def test_host_side_validation_without_gpu(lib):
