@@ -47,8 +47,10 @@ enum { OMNIMOE_BF16 = 0, OMNIMOE_F32 = 1 };
 /* sigma of the atomic expert (Eq.Atomic).  SILU = z*sigmoid(z)
  * (reading Q1); IDENTITY exists for linearity tests only. */
 enum { OMNIMOE_SILU = 0, OMNIMOE_IDENTITY = 1 };
-/* Which routed-branch kernel omnimoe_expert_fwd runs. */
-enum { OMNIMOE_EXPERT_AUTO = 0, OMNIMOE_EXPERT_WARP = 1 };
+/* Which routed-branch kernel omnimoe_expert_fwd runs: AUTO
+ * follows the plan's group size; WARP (expert-major) requires B = 1; GROUP
+ * (run-major) requires B > 1. */
+enum { OMNIMOE_EXPERT_AUTO = 0, OMNIMOE_EXPERT_WARP = 1, OMNIMOE_EXPERT_GROUP = 2 };
 /* workspace query selector */
 enum { OMNIMOE_WS_ROUTE = 0, OMNIMOE_WS_SCHEDULE = 1, OMNIMOE_WS_EXPERT = 2, OMNIMOE_WS_LAYER = 3 };
 
@@ -82,18 +84,26 @@ typedef struct {
 } omnimoe_dims;
 
 /* Expert-centric plan for the local expert range [expert_begin, expert_end)
- * (Eq.Tasks + active compression + Eq.Sort with group size B = 1, PAPER:259-275;
- * reading Q14).  n_loc = expert_end - expert_begin.  All arrays are device
+ * (Eq.Tasks + active compression + Eq.Sort).  n_loc =
+ * expert_end - expert_begin; B = the group size resolved from dims.group_size
+ * (omnimoe_group_size()).  The tasks of active expert number tau (in ascending
+ * id order) belong to group q = floor(tau / B) and are sorted by
+ * (q, token) (Eq.Sort); B = 1 is the expert-major order.  Arrays are device
  * memory provided by the caller:
- *   expert_offsets int32[n_loc+1]  task segment of local expert e is
- *                                  [expert_offsets[e], expert_offsets[e+1])
- *   sorted_token   int32[M]        token of each task, expert-major, tokens
- *                                  ascending inside a segment
- *   sorted_gate    float[M]        its gate g
+ *   expert_offsets int32[n_loc+1]  task count prefix per local expert; entry
+ *                                  n_loc = m_loc, the number of in-range tasks
  *   active         int32[n_loc]    local ids of active experts, ascending
  *   n_active       int32[1]        |E_active| (stays on the device)
- * Only the first expert_offsets[n_loc] entries of sorted_* are meaningful
- * (tasks whose expert lies outside the range are not part of the plan). */
+ *   sorted_token   int32[M]        token of each task in (q, token) order
+ *   sorted_gate    float[M]        its gate g
+ *   sorted_expert  int32[M]        its local expert id
+ *   run_offsets    int32[M+1]      B > 1 only (nullable for B = 1): first task of
+ *                                  each run = the tasks of one token in one group
+ *   n_runs         int32[1]        B > 1 only: number of runs P
+ * For B = 1 the segment of local expert e is [expert_offsets[e],
+ * expert_offsets[e+1]) with tokens ascending.  Only the first
+ * m_loc entries of sorted_* are meaningful (tasks outside the range are not
+ * part of the plan). */
 typedef struct {
   int32_t* expert_offsets;
   int32_t* sorted_token;
@@ -101,7 +111,15 @@ typedef struct {
   int32_t* active;
   int32_t* n_active;
   int64_t expert_begin, expert_end;
+  int32_t* sorted_expert;
+  int32_t* run_offsets;
+  int32_t* n_runs;
 } omnimoe_plan;
+
+/* The group size B that omnimoe_schedule / omnimoe_expert_fwd use for dims
+ * (dims.group_size if > 0, else the library's choice: N_c in bf16 mode, 1 in
+ * fp32 mode).  Returns 0 on invalid dims. */
+int64_t omnimoe_group_size(const omnimoe_dims* dims);
 
 /* Bytes of workspace needed by entry point `which` (OMNIMOE_WS_*) for L
  * tokens (ROUTE, EXPERT, LAYER) or M tasks (SCHEDULE: pass M as L). */
@@ -128,8 +146,9 @@ omnimoe_status omnimoe_route(const omnimoe_dims* dims, int64_t L, const void* x,
 
 /* Expert-Centric Scheduling: flatten M tasks in token-major order
  * (Eq.Tasks), histogram + exclusive scan over local experts, active-list
- * compaction, stable LSD radix sort by local expert id (Eq.Sort; "radix sort",
- * PAPER:536).
+ * compaction, group ids q = floor(rank / B), stable LSD radix sort by q
+ * (Eq.Sort; "radix sort") -- stability over the token-major input
+ * makes tokens ascend inside each group -- and, for B > 1, run detection.
  *   idx   int32[M]  global expert ids of the tasks
  *   gate  float[M]
  *   token int32[M]  nullable: token of task t defaults to t / (h*K)
@@ -140,9 +159,11 @@ omnimoe_status omnimoe_schedule(const omnimoe_dims* dims, int64_t M, const int32
                                 void* ws, size_t ws_bytes, omnimoe_stream_t stream);
 
 /* Grouped atomic-expert compute + scatter-add (Eq.Grouped, the
- * routed branch of Eq.Assemble): for every active local expert e,
- * its rows w_e = W_loc[e], v_e = V_loc[e] are read once; for each task (l, g) of
- * its segment: z = x_l . w_e (fp32), a = g * sigma(z), y_routed[l] += a * v_e.
+ * routed branch of Eq.Assemble): for each task (l, e, g) of the
+ * plan: z = x_l . w_e (fp32), a = g * sigma(z), y_routed[l] += a * v_e.
+ * B = 1: one warp per active expert reads w_e, v_e once and walks its tokens.
+ * B > 1: one warp per run (group q, token l) keeps x_l and the partial y_l in
+ * registers over the run's experts and scatter-adds once per run.
  *   x         [L][d]
  *   W_loc     [n_loc][d]  rows of W for the plan's expert range
  *   V_loc     [n_loc][d]

@@ -38,13 +38,15 @@ def lib():
         _lib.oracle_exact_dot.argtypes = [P, P, i64]
         _lib.oracle_exact_dot.restype = ctypes.c_float
         _lib.oracle_route.argtypes = [i64, i64, i64, i64, P, c_int, i64, c_int, P, P, P, P, P, P]
-        _lib.oracle_schedule.argtypes = [i64, P, P, P, i64, i64, P, P, P, P, P]
+        _lib.oracle_schedule.argtypes = [i64, P, P, P, i64, i64, i64, P, P, P, P, P, P, P, P]
+        _lib.oracle_routed_grouped.argtypes = [i64, i64, i64, i64, P, P, P, P, P, P, P, c_int, P]
         _lib.oracle_routed_token_centric.argtypes = [i64, i64, i64, P, P, P, P, P, c_int, P, c_int]
         _lib.oracle_routed_expert_centric.argtypes = [i64, i64, i64, P, P, P, P, P, P, c_int, P]
         _lib.oracle_shared_mlp.argtypes = [i64, i64, i64, P, P, P, P, c_int]
         _lib.oracle_layer.argtypes = [i64, i64, i64, i64, i64, i64, i64, P, P, P, P, P, i64, P, P,
                                       c_int, P, P, P, c_int]
-        for f in ("oracle_logits", "oracle_route", "oracle_schedule", "oracle_routed_token_centric",
+        for f in ("oracle_logits", "oracle_route", "oracle_schedule", "oracle_routed_grouped",
+                  "oracle_routed_token_centric",
                   "oracle_routed_expert_centric", "oracle_shared_mlp", "oracle_layer"):
             getattr(_lib, f).restype = None
     return _lib
@@ -95,21 +97,40 @@ def route(logit_rows, n_rows, n_cols, K, method=PRODUCT, bsel=4096, nthreads=Non
     return out
 
 
-def schedule(ids, gates, tokens, n_begin, n_end):
+def schedule(ids, gates, tokens, n_begin, n_end, B=1):
+    """Expert-centric plan with group size B; see oracle_schedule."""
     ids = np.ascontiguousarray(ids, dtype=np.int32).reshape(-1)
     gates = _f64(gates).reshape(-1)
     tokens = np.ascontiguousarray(tokens, dtype=np.int32).reshape(-1)
     M, n_loc = ids.size, n_end - n_begin
     offsets = np.empty(n_loc + 1, np.int32)
-    st = np.empty(M, np.int32)
-    sg = np.empty(M, np.float64)
+    st = np.empty(max(M, 1), np.int32)
+    sg = np.empty(max(M, 1), np.float64)
+    se = np.empty(max(M, 1), np.int32)
+    ro = np.empty(max(M, 1), np.int32)
     active = np.empty(max(n_loc, 1), np.int32)
     na = np.zeros(1, np.int64)
-    lib().oracle_schedule(M, _p(ids), _p(gates), _p(tokens), n_begin, n_end, _p(offsets), _p(st),
-                          _p(sg), _p(active), _p(na))
+    nr = np.zeros(1, np.int64)
+    lib().oracle_schedule(M, _p(ids), _p(gates), _p(tokens), n_begin, n_end, B, _p(offsets), _p(st),
+                          _p(sg), _p(se), _p(active), _p(na), _p(ro), _p(nr))
     m_loc = int(offsets[-1])
-    return dict(offsets=offsets, sorted_token=st[:m_loc], sorted_gate=sg[:m_loc],
-                active=active[:int(na[0])], n_active=int(na[0]))
+    return dict(offsets=offsets, sorted_token=st[:m_loc], sorted_gate=sg[:m_loc], sorted_expert=se[:m_loc],
+                active=active[:int(na[0])], n_active=int(na[0]), run_offsets=ro[:int(nr[0])],
+                n_runs=int(nr[0]), B=B)
+
+
+def routed_grouped(x, W_loc, V_loc, plan, act=0):
+    """Eq.Grouped run by run over a plan from schedule(...)."""
+    x, W_loc, V_loc = _f64(x), _f64(W_loc), _f64(V_loc)
+    L, d = x.shape
+    ro = np.ascontiguousarray(plan["run_offsets"], dtype=np.int32)
+    st = np.ascontiguousarray(plan["sorted_token"], dtype=np.int32)
+    se = np.ascontiguousarray(plan["sorted_expert"], dtype=np.int32)
+    sg = _f64(plan["sorted_gate"])
+    y = np.empty((L, d))
+    lib().oracle_routed_grouped(L, d, st.size, ro.size, _p(ro), _p(st), _p(se), _p(sg), _p(x), _p(W_loc),
+                                _p(V_loc), act, _p(y))
+    return y
 
 
 def routed_token_centric(x, W, V, ids, gates, act=0, nthreads=None):

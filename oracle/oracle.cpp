@@ -287,35 +287,85 @@ void oracle_route(int64_t T, int64_t Nr, int64_t Nc, int64_t K, const float* log
   });
 }
 
-// O6-O7 Expert-Centric Scheduling with group size B = 1 (
-// reading Q14): tasks t in token-major order (Eq.Tasks) carry
-// (token[t], ids[t], gate[t]); tasks whose expert lies outside the local
-// range [n_begin, n_end) are not part of this plan.  A stable counting sort
-// by expert id (Eq.Sort with keys (q, l), radix-sortable per PAPER:536)
-// gives, for local expert e = id - n_begin:
-//   offsets[e] .. offsets[e+1]   its task segment (tokens ascending)
-//   sorted_token, sorted_gate    tasks in expert-major order
-//   active[0..n_active)          unique active experts ascending (E_active)
+// O6-O7 Expert-Centric Scheduling: tasks t in token-major
+// order (Eq.Tasks) carry (token[t], ids[t], gate[t]); tasks whose
+// expert lies outside the local range [n_begin, n_end) are not part of this
+// plan.  E_active = the distinct in-range experts sorted by id; the
+// tau-th of them belongs to group q = floor(tau / B); tasks are
+// sorted by (q, token) (Eq.Sort) with a stable counting sort on
+// q over the token-major list (tokens then ascend inside each group; tasks of
+// one token in one group keep their task order).  Outputs, for local expert
+// e = id - n_begin:
+//   offsets[e] .. offsets[e+1]   count prefix of expert e (its B = 1 segment)
+//   sorted_token/gate/expert     tasks in (q, token) order
+//   active[0..n_active)          E_active (local ids, ascending)
+//   run_offsets[0..n_runs)       first task of each maximal (q, token) run
 void oracle_schedule(int64_t M, const int32_t* ids, const double* gates, const int32_t* tokens,
-                     int64_t n_begin, int64_t n_end, int32_t* offsets, int32_t* sorted_token,
-                     double* sorted_gate, int32_t* active, int64_t* n_active) {
+                     int64_t n_begin, int64_t n_end, int64_t B, int32_t* offsets,
+                     int32_t* sorted_token, double* sorted_gate, int32_t* sorted_expert,
+                     int32_t* active, int64_t* n_active, int32_t* run_offsets, int64_t* n_runs) {
   int64_t n_loc = n_end - n_begin;
   std::vector<int64_t> cnt(n_loc + 1, 0);
   for (int64_t t = 0; t < M; ++t)
     if (ids[t] >= n_begin && ids[t] < n_end) cnt[ids[t] - n_begin + 1]++;
   for (int64_t e = 0; e < n_loc; ++e) cnt[e + 1] += cnt[e];
   for (int64_t e = 0; e <= n_loc; ++e) offsets[e] = (int32_t)cnt[e];
-  std::vector<int64_t> cursor(cnt.begin(), cnt.end() - 1);
-  for (int64_t t = 0; t < M; ++t) {  // stable: visits tasks in t order
-    if (ids[t] < n_begin || ids[t] >= n_end) continue;
-    int64_t p = cursor[ids[t] - n_begin]++;
-    sorted_token[p] = tokens[t];
-    sorted_gate[p] = gates[t];
-  }
+  // E_active and the group of each active expert
+  std::vector<int64_t> group(n_loc, -1);
   int64_t na = 0;
   for (int64_t e = 0; e < n_loc; ++e)
-    if (offsets[e + 1] > offsets[e]) active[na++] = (int32_t)e;
+    if (offsets[e + 1] > offsets[e]) {
+      group[e] = na / B;
+      active[na++] = (int32_t)e;
+    }
   *n_active = na;
+  const int64_t n_groups = (na + B - 1) / B;
+  // stable counting sort of the in-range tasks by group
+  std::vector<int64_t> gstart(n_groups + 1, 0);
+  for (int64_t t = 0; t < M; ++t)
+    if (ids[t] >= n_begin && ids[t] < n_end) gstart[group[ids[t] - n_begin] + 1]++;
+  for (int64_t q = 0; q < n_groups; ++q) gstart[q + 1] += gstart[q];
+  for (int64_t t = 0; t < M; ++t) {  // visits tasks in t order: stable
+    if (ids[t] < n_begin || ids[t] >= n_end) continue;
+    const int64_t e = ids[t] - n_begin;
+    const int64_t p = gstart[group[e]]++;
+    sorted_token[p] = tokens[t];
+    sorted_gate[p] = gates[t];
+    sorted_expert[p] = (int32_t)e;
+  }
+  // runs: maximal stretches of equal (group, token)
+  const int64_t m_loc = offsets[n_loc];
+  int64_t nr = 0;
+  for (int64_t p = 0; p < m_loc; ++p)
+    if (p == 0 || sorted_token[p] != sorted_token[p - 1] ||
+        group[sorted_expert[p]] != group[sorted_expert[p - 1]])
+      run_offsets[nr++] = (int32_t)p;
+  *n_runs = nr;
+}
+
+// Eq.Grouped executed run by run: for every run (group q,
+// token l) and every task (e, g) in it, y[l] += g * sigma(x_l . W_loc[e]) *
+// V_loc[e]; the per-run partial is accumulated first and then scatter-added.
+void oracle_routed_grouped(int64_t L, int64_t d, int64_t m_loc, int64_t n_runs,
+                           const int32_t* run_offsets, const int32_t* sorted_token,
+                           const int32_t* sorted_expert, const double* sorted_gate, const double* x,
+                           const double* W_loc, const double* V_loc, int act, double* y) {
+  for (int64_t i = 0; i < L * d; ++i) y[i] = 0.0;
+  std::vector<double> part(d);
+  for (int64_t r = 0; r < n_runs; ++r) {
+    const int64_t b = run_offsets[r], e = r + 1 < n_runs ? run_offsets[r + 1] : m_loc;
+    const int64_t l = sorted_token[b];
+    std::fill(part.begin(), part.end(), 0.0);
+    for (int64_t p = b; p < e; ++p) {
+      const double* w = W_loc + (int64_t)sorted_expert[p] * d;
+      const double* v = V_loc + (int64_t)sorted_expert[p] * d;
+      double z = 0.0;
+      for (int64_t c = 0; c < d; ++c) z += x[l * d + c] * w[c];
+      const double a = sorted_gate[p] * act_fn(z, act);
+      for (int64_t c = 0; c < d; ++c) part[c] += a * v[c];
+    }
+    for (int64_t c = 0; c < d; ++c) y[l * d + c] += part[c];
+  }
 }
 
 // O8 routed branch, token-centric -- the definition (Eq.Assemble,

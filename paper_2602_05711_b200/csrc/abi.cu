@@ -82,9 +82,17 @@ omnimoe_status validate_dims(const omnimoe_dims* dp) {
     set_error("group_size must be >= 0");
     return OMNIMOE_ERR_INVALID_ARGUMENT;
   }
-  if (d.expert_kernel != OMNIMOE_EXPERT_AUTO && d.expert_kernel != OMNIMOE_EXPERT_WARP) {
+  if (d.expert_kernel < OMNIMOE_EXPERT_AUTO || d.expert_kernel > OMNIMOE_EXPERT_GROUP) {
     set_error("unknown expert kernel " + std::to_string(d.expert_kernel));
     return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  {
+    const int64_t B = resolve_group_size(d);
+    if ((d.expert_kernel == OMNIMOE_EXPERT_WARP && B != 1) || (d.expert_kernel == OMNIMOE_EXPERT_GROUP && B < 2)) {
+      set_error("expert kernel " + std::to_string(d.expert_kernel) + " does not match group size B=" +
+                std::to_string(B) + " (WARP needs B = 1, GROUP needs B > 1)");
+      return OMNIMOE_ERR_INVALID_ARGUMENT;
+    }
   }
   const int64_t N = d.n_rows * d.n_cols;
   if (d.top_k > N) {
@@ -136,6 +144,9 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
   float* sg = c.take<float>((size_t)std::max<int64_t>(M, 1));
   int32_t* act = c.take<int32_t>(N);
   int32_t* na = c.take<int32_t>(1);
+  int32_t* se = c.take<int32_t>((size_t)std::max<int64_t>(M, 1));
+  int32_t* ro = c.take<int32_t>((size_t)M + 1);
+  int32_t* nr = c.take<int32_t>(1);
   const size_t sb = schedule_ws_bytes(M, N);
   void* sw = c.take<char>(sb);
   float* yr = c.take<float>((size_t)L * d.d);
@@ -145,7 +156,7 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
     o->route_bytes = rb;
     o->idx = idx;
     o->gate = gate;
-    o->plan = omnimoe_plan{off, st, sg, act, na, 0, N};
+    o->plan = omnimoe_plan{off, st, sg, act, na, 0, N, se, ro, nr};
     o->sched_ws = sw;
     o->y_routed = yr;
     o->H = H;
@@ -289,17 +300,23 @@ omnimoe_status omnimoe_schedule(const omnimoe_dims* dims, int64_t M, const int32
   OMNI_NONNULL(plan->expert_offsets, "plan.expert_offsets");
   OMNI_NONNULL(plan->active, "plan.active");
   OMNI_NONNULL(plan->n_active, "plan.n_active");
+  const int64_t B = resolve_group_size(*dims);
   if (M > 0) {
     OMNI_NONNULL(idx, "idx");
     OMNI_NONNULL(gate, "gate");
     OMNI_NONNULL(plan->sorted_token, "plan.sorted_token");
     OMNI_NONNULL(plan->sorted_gate, "plan.sorted_gate");
+    OMNI_NONNULL(plan->sorted_expert, "plan.sorted_expert");
+  }
+  if (B > 1) {
+    OMNI_NONNULL(plan->run_offsets, "plan.run_offsets (group size > 1)");
+    OMNI_NONNULL(plan->n_runs, "plan.n_runs (group size > 1)");
   }
   OMNI_NONNULL(ws, "ws");
   const int64_t n_loc = plan->expert_end - plan->expert_begin;
   OMNI_TRY(check_ws(ws_bytes, schedule_ws_bytes(M, n_loc), "schedule"));
   OMNI_TRY(check_device());
-  return schedule_run(M, idx, gate, token, dims->n_heads * dims->top_k, *plan, ws, (cudaStream_t)stream);
+  return schedule_run(M, idx, gate, token, dims->n_heads * dims->top_k, *plan, B, ws, (cudaStream_t)stream);
 }
 
 omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* W_loc,
@@ -322,6 +339,11 @@ omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const voi
   OMNI_NONNULL(plan->n_active, "plan.n_active");
   OMNI_NONNULL(plan->sorted_token, "plan.sorted_token");
   OMNI_NONNULL(plan->sorted_gate, "plan.sorted_gate");
+  if (resolve_group_size(*dims) > 1) {
+    OMNI_NONNULL(plan->sorted_expert, "plan.sorted_expert");
+    OMNI_NONNULL(plan->run_offsets, "plan.run_offsets (group size > 1)");
+    OMNI_NONNULL(plan->n_runs, "plan.n_runs (group size > 1)");
+  }
   OMNI_TRY(check_ws(ws_bytes, expert_ws_bytes(*dims, L), "expert_fwd"));
   OMNI_TRY(check_device());
   return expert_run(*dims, L, x, W_loc, V_loc, *plan, y_routed, accumulate, ws, (cudaStream_t)stream);
@@ -380,7 +402,7 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
   const int64_t M = L * d.n_heads * d.top_k;
   OMNI_TRY(route_impl(d, L, x, subkeys, idx, gate, nullptr, w.route_ws, st));
   const int r_launch = omnimoe_last_launch_count();
-  OMNI_TRY(schedule_run(M, idx, gate, nullptr, d.n_heads * d.top_k, w.plan, w.sched_ws, st));
+  OMNI_TRY(schedule_run(M, idx, gate, nullptr, d.n_heads * d.top_k, w.plan, resolve_group_size(d), w.sched_ws, st));
   OMNI_TRY(expert_run(d, L, x, W, V, w.plan, w.y_routed, 0, nullptr, st));
   if (d.d_ff > 0) {
     OMNI_TRY(mlp_impl(d, L, x, w_gate_up, w_down, w.y_routed, y, w.H, st));
@@ -448,6 +470,11 @@ omnimoe_status omnimoe_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A,
 }
 
 int omnimoe_last_launch_count(void) { return g_launches; }
+
+int64_t omnimoe_group_size(const omnimoe_dims* dims) {
+  if (validate_dims(dims) != OMNIMOE_OK) return 0;
+  return resolve_group_size(*dims);
+}
 
 const char* omnimoe_status_string(omnimoe_status s) {
   switch (s) {

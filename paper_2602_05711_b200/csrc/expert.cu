@@ -1,10 +1,20 @@
 // Grouped atomic-expert compute + scatter-add (Eq.Grouped), step
-// a6 of DESIGN.md.  Expert-major: one warp owns one active expert at a time,
-// holds its w_e / v_e rows in registers (read from HBM exactly once per layer,
-// D_expert = 2d|E_active|), then streams the expert's tasks in
-// ascending token order: gather x_l (128-bit loads), z = x_l . w_e in
-// fp32, a = g * sigma(z), and scatter-add a * v_e into y_routed[l] with
-// red.global.add.v4.f32.
+// a6 of DESIGN.md.
+//
+//  expert_warp_kernel   plan with B = 1 (expert-major): one warp owns one active
+//                       expert at a time, holds its w_e / v_e rows in registers
+//                       (read from HBM exactly once per layer, D_expert =
+//                       2d|E_active|), then streams the expert's
+//                       tasks in ascending token order: gather x_l,
+//                       z = x_l . w_e in fp32, a = g * sigma(z), scatter-add
+//                       a * v_e into y_routed[l] with red.global.add.v4.f32.
+//  expert_group_kernel  plan with B > 1, sorted by (group q, token l) (Eq.Sort):
+//                       one warp per run (q, l): x_l and an fp32 partial y_l live
+//                       in registers while the warp walks the run's experts
+//                       (w_e, v_e streamed; runs are taken in plan order, so the
+//                       warps in flight cover a window of ~1 group whose rows
+//                       stay L2-resident after one HBM read), then ONE red.v4
+//                       scatter per run instead of one per task.
 #include <string>
 
 #include "schedule.cuh"
@@ -109,6 +119,128 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+template <typename T, int NV>
+__global__ void __launch_bounds__(256)
+    expert_group_kernel(int d, const T* __restrict__ x, const T* __restrict__ W,
+                        const T* __restrict__ V, const int32_t* __restrict__ run_off,
+                        const int32_t* __restrict__ n_runs_p, const int32_t* __restrict__ m_loc_p,
+                        const int32_t* __restrict__ stok, const int32_t* __restrict__ sexp,
+                        const float* __restrict__ sgate, float* __restrict__ y, int act) {
+  constexpr int E = VecT<T>::E;
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * (int64_t)blockDim.x) >> 5);
+  const int n_runs = *n_runs_p, m_loc = *m_loc_p;
+  for (int r = gw; r < n_runs; r += nw) {
+    const int beg = run_off[r];
+    const int end = r + 1 < n_runs ? run_off[r + 1] : m_loc;
+    const int l = stok[beg];
+    const T* xl = x + (size_t)l * d;
+    uint4 xv[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int c = (j * 32 + lane) * E;
+      xv[j] = c < d ? ld_vec(xl + c) : make_uint4(0, 0, 0, 0);
+    }
+    float acc[NV][E];
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+#pragma unroll
+      for (int i = 0; i < E; ++i) acc[j][i] = 0.f;
+    for (int p0 = beg; p0 < end; p0 += 32) {
+      // the next (up to) 32 tasks' expert ids and gates, one per lane
+      const int pl = p0 + lane;
+      const int e_l = pl < end ? sexp[pl] : 0;
+      const float g_l = pl < end ? sgate[pl] : 0.f;
+      const int cnt = min(32, end - p0);
+      for (int t = 0; t < cnt; ++t) {
+        const int e = __shfl_sync(0xffffffffu, e_l, t);
+        const float g = __shfl_sync(0xffffffffu, g_l, t);
+        const T* we = W + (size_t)e * d;
+        const T* ve = V + (size_t)e * d;
+        uint4 wv[NV], vv[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          const int c = (j * 32 + lane) * E;
+          wv[j] = c < d ? ld_vec(we + c) : make_uint4(0, 0, 0, 0);
+          vv[j] = c < d ? ld_vec(ve + c) : make_uint4(0, 0, 0, 0);
+        }
+        float z = 0.f;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          float xf[E], wf[E];
+          VecT<T>::unpack(xv[j], xf);
+          VecT<T>::unpack(wv[j], wf);
+#pragma unroll
+          for (int i = 0; i < E; ++i) z = fmaf(xf[i], wf[i], z);
+        }
+        z = warp_sum(z);
+        const float a = g * (act == OMNIMOE_IDENTITY ? z : silu_f(z));
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          float vf[E];
+          VecT<T>::unpack(vv[j], vf);
+#pragma unroll
+          for (int i = 0; i < E; ++i) acc[j][i] = fmaf(a, vf[i], acc[j][i]);
+        }
+      }
+    }
+    float* yl = y + (size_t)l * d;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int c = (j * 32 + lane) * E;
+      if (c < d) {
+#pragma unroll
+        for (int i = 0; i < E; i += 4) red_add_v4(yl + c + i, acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);
+      }
+    }
+  }
+}
+
+template <typename T>
+omnimoe_status launch_group(int d, const void* x, const void* W, const void* V, const omnimoe_plan& plan,
+                            int64_t n_loc, float* y, int act, cudaStream_t st) {
+  constexpr int E = VecT<T>::E;
+  const int nv = (d + 32 * E - 1) / (32 * E);
+  auto X = static_cast<const T*>(x);
+  auto Wp = static_cast<const T*>(W);
+  auto Vp = static_cast<const T*>(V);
+  const int32_t* m_loc = plan.expert_offsets + n_loc;
+#define OMNI_GROUP_CASE(NVC)                                                                          \
+  case NVC: {                                                                                         \
+    int per_sm = 1;                                                                                   \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_group_kernel<T, NVC>, 256, 0);      \
+    expert_group_kernel<T, NVC><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(                          \
+        d, X, Wp, Vp, plan.run_offsets, plan.n_runs, m_loc, plan.sorted_token, plan.sorted_expert,    \
+        plan.sorted_gate, y, act);                                                                    \
+    break;                                                                                            \
+  }
+  switch (nv) {
+    OMNI_GROUP_CASE(1)
+    OMNI_GROUP_CASE(2)
+    OMNI_GROUP_CASE(4)
+    OMNI_GROUP_CASE(8)
+    default:
+      if (nv == 3) {
+        expert_group_kernel<T, 4><<<kSMs * 4, 256, 0, st>>>(d, X, Wp, Vp, plan.run_offsets, plan.n_runs, m_loc,
+                                                             plan.sorted_token, plan.sorted_expert,
+                                                             plan.sorted_gate, y, act);
+        break;
+      }
+      if (nv <= 8) {
+        expert_group_kernel<T, 8><<<kSMs * 4, 256, 0, st>>>(d, X, Wp, Vp, plan.run_offsets, plan.n_runs, m_loc,
+                                                             plan.sorted_token, plan.sorted_expert,
+                                                             plan.sorted_gate, y, act);
+        break;
+      }
+      set_error("expert_fwd: d too large for the grouped kernel (d <= " + std::to_string(256 * E) + ")");
+      return OMNIMOE_ERR_UNSUPPORTED;
+  }
+#undef OMNI_GROUP_CASE
+  OMNI_CHECK_LAUNCH("expert_group_kernel");
+  return OMNIMOE_OK;
+}
+
 template <typename T>
 omnimoe_status launch_warp(int d, const void* x, const void* W, const void* V,
                            const omnimoe_plan& plan, float* y, int act, cudaStream_t st) {
@@ -152,6 +284,12 @@ omnimoe_status launch_warp(int d, const void* x, const void* W, const void* V,
 
 size_t expert_ws_bytes(const omnimoe_dims&, int64_t) { return 0; }
 
+int64_t resolve_group_size(const omnimoe_dims& d) {
+  if (d.group_size > 0) return d.group_size;
+  if (d.dtype != OMNIMOE_BF16) return 1;  // fp32 correctness mode: expert-major
+  return d.n_cols;                         // one grid row of experts per group
+}
+
 omnimoe_status expert_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W,
                           const void* V, const omnimoe_plan& plan, float* y, int accumulate,
                           void*, cudaStream_t st) {
@@ -160,6 +298,12 @@ omnimoe_status expert_run(const omnimoe_dims& dm, int64_t L, const void* x, cons
       set_error("expert_fwd: memset failed");
       return OMNIMOE_ERR_CUDA;
     }
+  }
+  const int64_t B = resolve_group_size(dm);
+  const int64_t n_loc = plan.expert_end - plan.expert_begin;
+  if (B > 1) {
+    if (dm.dtype == OMNIMOE_BF16) return launch_group<__nv_bfloat16>((int)dm.d, x, W, V, plan, n_loc, y, dm.act, st);
+    return launch_group<float>((int)dm.d, x, W, V, plan, n_loc, y, dm.act, st);
   }
   if (dm.dtype == OMNIMOE_BF16) return launch_warp<__nv_bfloat16>((int)dm.d, x, W, V, plan, y, dm.act, st);
   return launch_warp<float>((int)dm.d, x, W, V, plan, y, dm.act, st);

@@ -50,8 +50,9 @@ __device__ int block_exclusive_scan(int v, int* total, int* warp_sums) {
   return wp + x - v;
 }
 
-// MODE 0: plain exclusive scan (out[i] = prefix);  MODE 1: compaction of
-// nonzero entries (out[prefix] = i).  FLAG: scan (in[i] > 0) instead of in[i].
+// MODE 0: plain exclusive scan of in (out[i] = prefix);  MODE 1: compaction of
+// nonzero entries (out[prefix] = i);  MODE 2: exclusive scan of (in > 0)
+// written densely (out[i] = number of nonzero entries before i).
 template <int MODE>
 __global__ void __launch_bounds__(kScanThreads)
     scan_reduce_kernel(const int32_t* __restrict__ in, int64_t n, int32_t* __restrict__ tile_sums) {
@@ -109,14 +110,14 @@ __global__ void __launch_bounds__(kScanThreads)
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
     const int64_t g = base + threadIdx.x * kScanItems + j;
-    if (MODE == 0) {
+    if (MODE != 1) {
       tile[threadIdx.x * kScanItems + j] = run;
     } else if (v[j] && g < n) {
       out[run] = (int32_t)g;
     }
     run += v[j];
   }
-  if (MODE == 0) {
+  if (MODE != 1) {
     __syncthreads();
     for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
       const int64_t g = base + i;
@@ -208,17 +209,42 @@ __global__ void __launch_bounds__(kRadixThreads)
   }
 }
 
+// B > 1: replace each in-range key (local expert id) by its group
+// q = rank_active(e) / B; out-of-range tasks keep a sentinel that
+// sorts behind every group.
+__global__ void group_keys_kernel(uint32_t* __restrict__ keys, int64_t M, int64_t n_loc,
+                                  const int32_t* __restrict__ rank, int64_t B, uint32_t sentinel) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < M;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t e = keys[t];
+    keys[t] = e < (uint32_t)n_loc ? (uint32_t)(rank[e] / B) : sentinel;
+  }
+}
+
+// run boundaries of the sorted plan: position p starts a run if its group or
+// its token differs from position p-1's.
+__global__ void run_flags_kernel(const uint32_t* __restrict__ skeys, const int32_t* __restrict__ stok,
+                                 int64_t M, const int32_t* __restrict__ m_loc_ptr,
+                                 int32_t* __restrict__ flags) {
+  const int64_t m_loc = *m_loc_ptr;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < M;
+       p += (int64_t)gridDim.x * blockDim.x)
+    flags[p] = p < m_loc && (p == 0 || skeys[p] != skeys[p - 1] || stok[p] != stok[p - 1]);
+}
+
 __global__ void gather_plan_kernel(const int32_t* __restrict__ order, int64_t M,
                                    const int32_t* __restrict__ m_loc_ptr,
                                    const int32_t* __restrict__ token, const float* __restrict__ gate,
-                                   int64_t hk, int32_t* __restrict__ sorted_token,
-                                   float* __restrict__ sorted_gate) {
+                                   const int32_t* __restrict__ ids, int64_t begin, int64_t hk,
+                                   int32_t* __restrict__ sorted_token, float* __restrict__ sorted_gate,
+                                   int32_t* __restrict__ sorted_expert) {
   const int64_t m_loc = *m_loc_ptr;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m_loc;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int32_t t = order[p];
     sorted_token[p] = token ? token[t] : (int32_t)(t / hk);
     sorted_gate[p] = gate[t];
+    sorted_expert[p] = (int32_t)(ids[t] - begin);
   }
 }
 
@@ -233,29 +259,32 @@ size_t schedule_ws_bytes(int64_t M, int64_t n_loc) {
   Carver c(nullptr);
   const int64_t nb = (M + kRadixTile - 1) / kRadixTile;
   c.take<int32_t>(n_loc + 1);                                 // cnt
+  c.take<int32_t>(n_loc + 1);                                 // rank among active
   c.take<uint32_t>(M); c.take<uint32_t>(M);                   // keys ping/pong
   c.take<int32_t>(M); c.take<int32_t>(M);                     // vals ping/pong
   c.take<int32_t>(256 * nb);                                  // radix hist
-  const int64_t scan_n = std::max<int64_t>(n_loc + 1, 256 * nb);
+  const int64_t scan_n = std::max<int64_t>(std::max<int64_t>(n_loc + 1, 256 * nb), M);
   c.take<int32_t>((scan_n + kScanTile - 1) / kScanTile + 1);  // tile sums
   return c.bytes();
 }
 
 omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, const int32_t* token,
-                            int64_t hk, const omnimoe_plan& plan, void* ws, cudaStream_t st) {
+                            int64_t hk, const omnimoe_plan& plan, int64_t B, void* ws, cudaStream_t st) {
   const int64_t n_loc = plan.expert_end - plan.expert_begin;
   const int64_t nb = (M + kRadixTile - 1) / kRadixTile;
   Carver c(ws);
   int32_t* cnt = c.take<int32_t>(n_loc + 1);
+  int32_t* rank = c.take<int32_t>(n_loc + 1);
   uint32_t* k0 = c.take<uint32_t>(M);
   uint32_t* k1 = c.take<uint32_t>(M);
   int32_t* v0 = c.take<int32_t>(M);
   int32_t* v1 = c.take<int32_t>(M);
   int32_t* hist = c.take<int32_t>(256 * nb);
-  const int64_t scan_n = std::max<int64_t>(n_loc + 1, 256 * nb);
+  const int64_t scan_n = std::max<int64_t>(std::max<int64_t>(n_loc + 1, 256 * nb), M);
   int32_t* tiles = c.take<int32_t>((scan_n + kScanTile - 1) / kScanTile + 1);
 
-  if (cudaMemsetAsync(cnt, 0, (n_loc + 1) * sizeof(int32_t), st) != cudaSuccess) {
+  if (cudaMemsetAsync(cnt, 0, (n_loc + 1) * sizeof(int32_t), st) != cudaSuccess ||
+      (B > 1 && cudaMemsetAsync(plan.n_runs, 0, sizeof(int32_t), st) != cudaSuccess)) {
     set_error("schedule: memset failed");
     return OMNIMOE_ERR_CUDA;
   }
@@ -268,9 +297,17 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
   // a4: active-expert compaction and |E_active|
   OMNI_TRY(scan<1>(cnt, n_loc, plan.active, plan.n_active, tiles, st));
   if (M == 0) return OMNIMOE_OK;
-  // a5: stable LSD radix sort of the local ids (sentinel n_loc included)
+  // a4: group of each expert = rank among the active experts / B
+  int64_t n_keys = n_loc;  // largest key value (the sentinel)
+  if (B > 1) {
+    OMNI_TRY(scan<2>(cnt, n_loc, rank, nullptr, tiles, st));
+    n_keys = (n_loc + B - 1) / B;
+    group_keys_kernel<<<grid_for(M, 256), 256, 0, st>>>(k0, M, n_loc, rank, B, (uint32_t)n_keys);
+    OMNI_CHECK_LAUNCH("group_keys_kernel");
+  }
+  // a5: stable LSD radix sort of the keys (sentinel included), task index payload
   int bits = 1;
-  while ((int64_t(1) << bits) <= n_loc) ++bits;
+  while ((int64_t(1) << bits) <= n_keys) ++bits;
   const int passes = (bits + 7) / 8;
   uint32_t *kin = k0, *kout = k1;
   int32_t *vin = nullptr, *vout = v0;
@@ -285,9 +322,17 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
     vin = vout;
     vout = (vout == v0) ? v1 : v0;
   }
-  gather_plan_kernel<<<grid_for(M, 256), 256, 0, st>>>(vin, M, plan.expert_offsets + n_loc, token, gate,
-                                                      hk, plan.sorted_token, plan.sorted_gate);
+  const int32_t* m_loc = plan.expert_offsets + n_loc;
+  gather_plan_kernel<<<grid_for(M, 256), 256, 0, st>>>(vin, M, m_loc, token, gate, ids, plan.expert_begin, hk,
+                                                      plan.sorted_token, plan.sorted_gate, plan.sorted_expert);
   OMNI_CHECK_LAUNCH("gather_plan_kernel");
+  if (B > 1) {
+    // runs: (group, token) boundaries of the sorted plan, compacted to run_offsets
+    int32_t* flags = reinterpret_cast<int32_t*>(kout);  // free buffer (kin holds the sorted keys)
+    run_flags_kernel<<<grid_for(M, 256), 256, 0, st>>>(kin, plan.sorted_token, M, m_loc, flags);
+    OMNI_CHECK_LAUNCH("run_flags_kernel");
+    OMNI_TRY(scan<1>(flags, M, plan.run_offsets, plan.n_runs, tiles, st));
+  }
   return OMNIMOE_OK;
 }
 

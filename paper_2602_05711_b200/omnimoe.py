@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_PKG, "libomnimoe.so")
 
 BF16, F32 = 0, 1
 SILU, IDENTITY = 0, 1
-EXPERT_AUTO, EXPERT_WARP = 0, 1
+EXPERT_AUTO, EXPERT_WARP, EXPERT_GROUP = 0, 1, 2
 ROUTER_EXACT, ROUTER_EXACT_F64 = 0, 1
 LOGITS_ROUTE, LOGITS_EXACT_F64, LOGITS_BF16_FAST = 0, 1, 2
 WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER = 0, 1, 2, 3
@@ -39,12 +39,14 @@ class Plan(ctypes.Structure):
     _fields_ = [("expert_offsets", ctypes.c_void_p), ("sorted_token", ctypes.c_void_p),
                 ("sorted_gate", ctypes.c_void_p), ("active", ctypes.c_void_p),
                 ("n_active", ctypes.c_void_p), ("expert_begin", ctypes.c_int64),
-                ("expert_end", ctypes.c_int64)]
+                ("expert_end", ctypes.c_int64), ("sorted_expert", ctypes.c_void_p),
+                ("run_offsets", ctypes.c_void_p), ("n_runs", ctypes.c_void_p)]
 
 
 EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnimoe_expert_fwd",
            "omnimoe_shared_mlp", "omnimoe_layer_fwd", "omnimoe_router_logits", "omnimoe_gemm_bf16",
-           "omnimoe_last_launch_count", "omnimoe_status_string", "omnimoe_last_error"]
+           "omnimoe_last_launch_count", "omnimoe_status_string", "omnimoe_last_error",
+           "omnimoe_group_size"]
 
 _lib = None
 
@@ -74,6 +76,8 @@ def load(path: str = LIB_PATH):
         f.argtypes = args
         f.restype = ctypes.c_int
     lib.omnimoe_last_launch_count.restype = ctypes.c_int
+    lib.omnimoe_group_size.argtypes = [PD]
+    lib.omnimoe_group_size.restype = ctypes.c_int64
     lib.omnimoe_status_string.restype = ctypes.c_char_p
     lib.omnimoe_status_string.argtypes = [ctypes.c_int]
     lib.omnimoe_last_error.restype = ctypes.c_char_p
@@ -168,10 +172,19 @@ def route(dims: LayerDims, x, subkeys, ws=None, want_score=True):
     return idx, gate, score
 
 
+def group_size(dims: LayerDims) -> int:
+    """The group size B the library uses for these dims."""
+    dc = dims.c()
+    return int(load().omnimoe_group_size(ctypes.byref(dc)))
+
+
 def new_plan(n_loc: int, M: int, device, expert_begin: int = 0):
     t = dict(expert_offsets=torch.empty(n_loc + 1, dtype=torch.int32, device=device),
              sorted_token=torch.empty(max(M, 1), dtype=torch.int32, device=device),
              sorted_gate=torch.empty(max(M, 1), dtype=torch.float32, device=device),
+             sorted_expert=torch.empty(max(M, 1), dtype=torch.int32, device=device),
+             run_offsets=torch.empty(M + 1, dtype=torch.int32, device=device),
+             n_runs=torch.zeros(1, dtype=torch.int32, device=device),
              active=torch.empty(max(n_loc, 1), dtype=torch.int32, device=device),
              n_active=torch.empty(1, dtype=torch.int32, device=device),
              expert_begin=expert_begin, expert_end=expert_begin + n_loc)
@@ -180,10 +193,12 @@ def new_plan(n_loc: int, M: int, device, expert_begin: int = 0):
 
 def _cplan(p) -> Plan:
     return Plan(p["expert_offsets"].data_ptr(), p["sorted_token"].data_ptr(), p["sorted_gate"].data_ptr(),
-                p["active"].data_ptr(), p["n_active"].data_ptr(), p["expert_begin"], p["expert_end"])
+                p["active"].data_ptr(), p["n_active"].data_ptr(), p["expert_begin"], p["expert_end"],
+                p["sorted_expert"].data_ptr(), p["run_offsets"].data_ptr(), p["n_runs"].data_ptr())
 
 
 def schedule(dims: LayerDims, idx, gate, token=None, expert_begin=0, expert_end=None, plan=None, ws=None):
+    """Expert-centric plan (a4 + a5) of the tasks (idx, gate) over the expert range."""
     M = idx.numel()
     _req(idx, "idx", torch.int32)
     _req(gate, "gate", torch.float32, M)
@@ -192,19 +207,12 @@ def schedule(dims: LayerDims, idx, gate, token=None, expert_begin=0, expert_end=
     expert_end = dims.N if expert_end is None else expert_end
     n_loc = expert_end - expert_begin
     plan = plan or new_plan(n_loc, M, idx.device, expert_begin)
-    ws = ws if ws is not None else torch.empty(max(workspace_size(dims, M, WS_SCHEDULE)
-                                                   if n_loc == dims.N else _sched_ws(dims, M, n_loc), 1),
+    ws = ws if ws is not None else torch.empty(max(workspace_size(dims, M, WS_SCHEDULE), 1),
                                                dtype=torch.uint8, device=idx.device)
     dc, cp = dims.c(), _cplan(plan)
     _check(load().omnimoe_schedule(ctypes.byref(dc), M, _ptr(idx), _ptr(gate), _ptr(token),
                                    ctypes.byref(cp), _ptr(ws), ws.numel(), _stream()), "schedule")
     return plan
-
-
-def _sched_ws(dims, M, n_loc):
-    # workspace for a shard: the library sizes by the plan's n_loc <= N, so the
-    # full-range size is an upper bound
-    return workspace_size(dims, M, WS_SCHEDULE)
 
 
 def expert_fwd(dims: LayerDims, x, W_loc, V_loc, plan, y_routed=None, accumulate=False, ws=None):

@@ -186,59 +186,75 @@ def test_route_k_equals_n():
 
 
 # ---------------------------------------------------------------- schedule
-def _check_plan(plan, ids, gates, toks, b, e):
-    p = oracle.schedule(ids, gates, toks, b, e)
+def _check_plan(plan, ids, gates, toks, b, e, B):
+    p = oracle.schedule(ids, gates, toks, b, e, B=B)
     m = int(p["offsets"][-1])
     np.testing.assert_array_equal(plan["expert_offsets"].cpu().numpy(), p["offsets"])
     np.testing.assert_array_equal(plan["sorted_token"].cpu().numpy()[:m], p["sorted_token"])
     np.testing.assert_array_equal(plan["sorted_gate"].cpu().numpy()[:m].astype(np.float64), p["sorted_gate"])
+    np.testing.assert_array_equal(plan["sorted_expert"].cpu().numpy()[:m], p["sorted_expert"])
     na = int(plan["n_active"].item())
     assert na == p["n_active"]
     np.testing.assert_array_equal(plan["active"].cpu().numpy()[:na], p["active"])
+    if B > 1:
+        nr = int(plan["n_runs"].item())
+        assert nr == p["n_runs"]
+        np.testing.assert_array_equal(plan["run_offsets"].cpu().numpy()[:nr], p["run_offsets"])
 
 
+@pytest.mark.parametrize("B", [1, 2, 1024])
 @pytest.mark.parametrize("N,L,HK,b,e", [(1024, 256, 8, 0, 1024), (65536, 2048, 64, 0, 65536),
                                         (1 << 20, 4096, 512, 0, 1 << 20), (1000, 300, 7, 250, 700),
                                         (5, 50, 3, 0, 5), (1 << 20, 16, 16, 1 << 19, 1 << 20)])
-def test_schedule_bit_exact(N, L, HK, b, e):
+def test_schedule_bit_exact(N, L, HK, b, e, B):
     rng = np.random.default_rng(N + L)
     ids = rng.integers(0, N, (L, HK)).astype(np.int32)
     gates = rng.random((L, HK)).astype(np.float32)
-    d = om.LayerDims(d=8, n_rows=N, n_cols=1, top_k=HK, d_ff=0)
+    d = om.LayerDims(d=8, n_rows=N, n_cols=1, top_k=HK, d_ff=0, group_size=B)
+    assert om.group_size(d) == B
     idx_t = torch.from_numpy(ids).cuda()
     g_t = torch.from_numpy(gates).cuda()
     plan = om.schedule(d, idx_t.reshape(-1), g_t.reshape(-1), expert_begin=b, expert_end=e)
     torch.cuda.synchronize()
     _check_plan(plan, ids.reshape(-1), gates.reshape(-1).astype(np.float64),
-                np.repeat(np.arange(L), HK).astype(np.int32), b, e)
+                np.repeat(np.arange(L), HK).astype(np.int32), b, e, B)
 
 
-def test_schedule_all_same_expert_and_empty():
-    d = om.LayerDims(d=8, n_rows=64, n_cols=64, top_k=4, d_ff=0)
+@pytest.mark.parametrize("B", [1, 64])
+def test_schedule_all_same_expert_and_empty(B):
+    d = om.LayerDims(d=8, n_rows=64, n_cols=64, top_k=4, d_ff=0, group_size=B)
     ids = np.full(40000, 17, np.int32)
     gates = np.linspace(0, 1, 40000).astype(np.float32)
     plan = om.schedule(d, torch.from_numpy(ids).cuda(), torch.from_numpy(gates).cuda())
     torch.cuda.synchronize()
-    _check_plan(plan, ids, gates.astype(np.float64), (np.arange(40000) // 4).astype(np.int32), 0, 4096)
+    _check_plan(plan, ids, gates.astype(np.float64), (np.arange(40000) // 4).astype(np.int32), 0, 4096, B)
     e = torch.empty(0, dtype=torch.int32, device="cuda")
     plan = om.schedule(d, e, torch.empty(0, device="cuda"))
     torch.cuda.synchronize()
     assert plan["n_active"].item() == 0 and plan["expert_offsets"].cpu().numpy().max() == 0
+    assert plan["n_runs"].item() == 0
 
 
 # ---------------------------------------------------------------- expert compute
+@pytest.mark.parametrize("B", [1, 2, 512])
 @pytest.mark.parametrize("dtype", [om.BF16, om.F32])
 @pytest.mark.parametrize("d,act", [(64, om.SILU), (72, om.SILU), (1024, om.SILU), (2048, om.SILU), (64, om.IDENTITY)])
-def test_expert_fwd_given_plan(dtype, d, act):
+def test_expert_fwd_given_plan(dtype, d, act, B):
+    if dtype == om.F32 and B > 1 and d > 1024:
+        pytest.skip("grouped kernel holds d/128 fp32 vectors per lane: d <= 1024 in fp32 mode")
     rng = np.random.default_rng(d)
     L, N, HK = 200, 3000, 12
-    dims = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, dtype=dtype, act=act)
+    dims = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, dtype=dtype, act=act, group_size=B)
     inp = make_inputs(dims, L, 9, skip=("subkeys",))
-    ids = np.stack([rng.choice(N, HK, replace=False) for _ in range(L)]).astype(np.int32)
+    # clustered ids (several tasks of a token share a group) plus repeats across tokens
+    base = rng.integers(0, N - 64, L)
+    ids = np.stack([b0 + rng.choice(64, HK, replace=False) for b0 in base]).astype(np.int32)
     gates = rng.random((L, HK)).astype(np.float32)
     plan = om.schedule(dims, torch.from_numpy(ids).cuda().reshape(-1), torch.from_numpy(gates).cuda().reshape(-1))
     y = om.expert_fwd(dims, inp["x"], inp["W"], inp["V"], plan)
     torch.cuda.synchronize()
+    if B > 1:
+        assert plan["n_runs"].item() < L * HK  # runs really merge tasks
     used = np.unique(ids)
     remap = np.searchsorted(used, ids)
     x = host_rows(dims, 9, "x", np.arange(L))
@@ -272,8 +288,9 @@ def test_shared_mlp(dtype, L, d, dff):
                                                (om.BF16, synth.DYADIC, om.ROUTER_EXACT),
                                                (om.F32, synth.NORMAL, om.ROUTER_EXACT),
                                                (om.F32, synth.DYADIC, om.ROUTER_EXACT)])
-def test_layer_c1(dtype, mode, router):
-    w = _dims("C1", dtype=dtype, router=router)
+@pytest.mark.parametrize("B", [0, 1, 5])
+def test_layer_c1(dtype, mode, router, B):
+    w = _dims("C1", dtype=dtype, router=router, group_size=B)
     dims = w.dims
     inp = make_inputs(dims, w.L, w.seed, mode)
     y, idx, gate = om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], inp["V"], inp["w_gate_up"],
@@ -310,3 +327,30 @@ def test_errors_are_loud():
         om.route(bad, inp["x"], torch.empty(1 * 8 * 64, dtype=torch.bfloat16, device="cuda"))
     with pytest.raises(om.OmniMoEError):
         om.route(w.dims, inp["x"].cpu(), inp["subkeys"])
+
+
+# ---------------------------------------------------------------- full-size, sampled
+@pytest.mark.parametrize("name", ["C3a", "C3b"])
+def test_layer_full_size_sampled(name):
+    """The bench workload at full size, in the bench's launch configuration
+    (one omnimoe_layer_fwd over all L tokens); the oracle recomputes sampled
+    tokens one by one (regenerating only the expert rows they select)."""
+    w = _dims(name)
+    dims = w.dims
+    inp = make_inputs(dims, w.L, w.seed)
+    y, idx, gate = om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], inp["V"], inp["w_gate_up"],
+                                inp["w_down"], return_routing=True)
+    torch.cuda.synchronize()
+    toks = np.array([0, 1, 777, 4096, 9999, w.L - 2, w.L - 1])
+    hr = lambda n, r=None: host_rows(dims, w.seed, n, r)
+    x = hr("x", toks)
+    sub = hr("subkeys").reshape(dims.n_heads, -1, dims.d)
+    lg = oracle.logits(x, sub)
+    r = oracle.route(lg.reshape(len(toks) * dims.n_heads, -1), dims.n_rows, dims.n_cols, dims.top_k)
+    np.testing.assert_array_equal(idx[toks].cpu().numpy().reshape(-1, dims.top_k), r["idx"])
+    used = np.unique(r["idx"])
+    idm = np.stack([used, np.arange(len(used))], 1)
+    ref = oracle.layer(x, sub, hr("W", used), hr("V", used), dims.n_rows, dims.n_cols, dims.top_k,
+                       hr("w_gate_up"), hr("w_down"), id_map=idm)
+    e_tok, e_elt = rel_errors(y[toks].float().cpu().numpy(), ref["y"])
+    assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)

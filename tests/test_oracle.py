@@ -246,6 +246,64 @@ def test_schedule_golden():
     assert list(p["sorted_token"]) == g["expected_sorted_token"]
 
 
+def test_schedule_grouped_golden():
+    g = GOLD["schedule_example_grouped"]
+    ids = np.array(g["ids"], np.int32).reshape(-1)
+    toks = np.repeat(np.arange(2), 2).astype(np.int32)
+    p = oracle.schedule(ids, np.ones(4), toks, 0, 10, B=g["B"])
+    assert list(p["sorted_token"]) == g["expected_sorted_token"]
+    assert list(p["sorted_expert"]) == g["expected_sorted_expert"]
+    assert list(p["run_offsets"]) == g["expected_run_offsets"]
+
+
+@pytest.mark.parametrize("B", [1, 2, 3, 7, 1000])
+def test_schedule_grouped_properties(B):
+    rng = np.random.default_rng(40 + B)
+    L, HK, N = 60, 5, 41
+    ids = rng.integers(0, N, (L, HK)).astype(np.int32)
+    gates = rng.random((L, HK))
+    toks = np.repeat(np.arange(L), HK).astype(np.int32)
+    for (b, e) in [(0, N), (7, 30)]:
+        p = oracle.schedule(ids, gates, toks, b, e, B=B)
+        fl = ids.reshape(-1)
+        sel = (fl >= b) & (fl < e)
+        active = sorted(set((fl[sel] - b).tolist()))
+        assert list(p["active"]) == active
+        grp = {ex: i // B for i, ex in enumerate(active)}
+        # multiset conservation
+        want = sorted(zip(toks[sel], fl[sel] - b, gates.reshape(-1)[sel]))
+        got = sorted(zip(p["sorted_token"], p["sorted_expert"], p["sorted_gate"]))
+        assert got == want
+        # sorted by (q, l) (Eq.Sort)
+        keys = [(grp[ex], l) for ex, l in zip(p["sorted_expert"], p["sorted_token"])]
+        assert keys == sorted(keys)
+        assert len(set(grp.values())) == -(-len(active) // B)  # N_groups = ceil(|E_active| / B)
+        # runs partition the plan into maximal constant (q, l) stretches
+        ro = list(p["run_offsets"]) + [len(keys)]
+        for r in range(len(ro) - 1):
+            assert len(set(keys[ro[r]:ro[r + 1]])) == 1
+            if r:
+                assert keys[ro[r]] != keys[ro[r] - 1]
+        if B == 1:  # expert-major: segment of e is [offsets[e], offsets[e+1])
+            for ex in active:
+                seg = p["sorted_expert"][p["offsets"][ex]:p["offsets"][ex + 1]]
+                assert np.all(seg == ex)
+
+
+@pytest.mark.parametrize("B", [1, 4, 64])
+def test_grouped_executor_equals_token_centric(B):
+    rng = np.random.default_rng(50 + B)
+    L, d, N, HK = 48, 24, 300, 9
+    x = rng.standard_normal((L, d))
+    W, V = rng.standard_normal((N, d)), rng.standard_normal((N, d))
+    ids = np.stack([rng.choice(N, HK, replace=False) for _ in range(L)]).astype(np.int32)
+    g = rng.random((L, HK))
+    yt = oracle.routed_token_centric(x, W, V, ids, g)
+    p = oracle.schedule(ids, g, np.repeat(np.arange(L), HK), 0, N, B=B)
+    yg = oracle.routed_grouped(x, W, V, p)
+    assert np.max(np.abs(yt - yg)) <= 1e-10 * max(1.0, np.max(np.abs(yt)))
+
+
 def test_schedule_properties():
     rng = np.random.default_rng(4)
     L, HK, N = 40, 6, 37
