@@ -129,6 +129,7 @@ struct LayerWs {
   void* sched_ws;
   float* y_routed;
   void* H;
+  void* expert_ws;
 };
 
 size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
@@ -150,6 +151,7 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
   const size_t sb = schedule_ws_bytes(M, N);
   void* sw = c.take<char>(sb);
   float* yr = c.take<float>((size_t)L * d.d);
+  void* ew = c.take<char>(expert_ws_bytes(d, L));
   void* H = c.take<char>((size_t)L * std::max<int64_t>(d.d_ff, 1) * elem_size(d));
   if (o) {
     o->route_ws = rw;
@@ -159,6 +161,7 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
     o->plan = omnimoe_plan{off, st, sg, act, na, 0, N, se, ro, nr};
     o->sched_ws = sw;
     o->y_routed = yr;
+    o->expert_ws = ew;
     o->H = H;
   }
   return c.bytes();
@@ -339,6 +342,7 @@ omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const voi
   OMNI_NONNULL(plan->n_active, "plan.n_active");
   OMNI_NONNULL(plan->sorted_token, "plan.sorted_token");
   OMNI_NONNULL(plan->sorted_gate, "plan.sorted_gate");
+  OMNI_NONNULL(ws, "ws");
   if (resolve_group_size(*dims) > 1) {
     OMNI_NONNULL(plan->sorted_expert, "plan.sorted_expert");
     OMNI_NONNULL(plan->run_offsets, "plan.run_offsets (group size > 1)");
@@ -403,7 +407,7 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
   OMNI_TRY(route_impl(d, L, x, subkeys, idx, gate, nullptr, w.route_ws, st));
   const int r_launch = omnimoe_last_launch_count();
   OMNI_TRY(schedule_run(M, idx, gate, nullptr, d.n_heads * d.top_k, w.plan, resolve_group_size(d), w.sched_ws, st));
-  OMNI_TRY(expert_run(d, L, x, W, V, w.plan, w.y_routed, 0, nullptr, st));
+  OMNI_TRY(expert_run(d, L, x, W, V, w.plan, w.y_routed, 0, w.expert_ws, st));
   if (d.d_ff > 0) {
     OMNI_TRY(mlp_impl(d, L, x, w_gate_up, w_down, w.y_routed, y, w.H, st));
   } else {

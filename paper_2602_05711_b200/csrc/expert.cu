@@ -15,9 +15,11 @@
 //                       warps in flight cover a window of ~1 group whose rows
 //                       stay L2-resident after one HBM read), then ONE red.v4
 //                       scatter per run instead of one per task.
+#include <cstdlib>
 #include <string>
 
 #include "schedule.cuh"
+#include "tcgen05.cuh"
 
 namespace omni {
 namespace {
@@ -125,13 +127,18 @@ __global__ void __launch_bounds__(256)
                         const T* __restrict__ V, const int32_t* __restrict__ run_off,
                         const int32_t* __restrict__ n_runs_p, const int32_t* __restrict__ m_loc_p,
                         const int32_t* __restrict__ stok, const int32_t* __restrict__ sexp,
-                        const float* __restrict__ sgate, float* __restrict__ y, int act) {
+                        const float* __restrict__ sgate, float* __restrict__ y, int act,
+                        int* __restrict__ work) {
   constexpr int E = VecT<T>::E;
+  constexpr int kChunk = 4;  // runs claimed per atomic
   const int lane = threadIdx.x & 31;
-  const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  const int nw = (int)((gridDim.x * (int64_t)blockDim.x) >> 5);
   const int n_runs = *n_runs_p, m_loc = *m_loc_p;
-  for (int r = gw; r < n_runs; r += nw) {
+  // runs are claimed in plan order through one counter, so the warps in flight
+  // always cover a narrow window of groups (their W/V rows stay L2-resident)
+  int r0 = 0;
+  if (lane == 0) r0 = atomicAdd(work, kChunk);
+  r0 = __shfl_sync(0xffffffffu, r0, 0);
+  for (int r = r0; r < n_runs;) {
     const int beg = run_off[r];
     const int end = r + 1 < n_runs ? run_off[r + 1] : m_loc;
     const int l = stok[beg];
@@ -194,25 +201,245 @@ __global__ void __launch_bounds__(256)
         for (int i = 0; i < E; i += 4) red_add_v4(yl + c + i, acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);
       }
     }
+    if (++r == r0 + kChunk) {
+      if (lane == 0) r0 = atomicAdd(work, kChunk);
+      r = r0 = __shfl_sync(0xffffffffu, r0, 0);
+    }
   }
+}
+
+// ---------------------------------------------------------------------------
+// expert_group_tma_kernel: the run-major executor with its expert rows staged by
+// the TMA engine.  Each warp is independent: lane 0 is its producer, issuing
+// 1-D cp.async.bulk copies of w_e, v_e (and x_l at the first task of a run) into
+// an S-deep ring of shared-memory stages completed on per-stage mbarriers; all
+// 32 lanes consume stage by stage (x_l held as fp32 in registers for the whole
+// run, dot product from shared memory, shuffle reduce, fp32 axpy into the run's
+// register accumulator), one red.v4 scatter per run.  Rows are in flight S-1
+// tasks ahead of the math, independent of the warp count.
+constexpr int kGChunk = 4;  // runs claimed per atomic
+
+struct StageMeta {
+  float g;
+  int tok;
+  int flags;  // 1: first task of its run, 2: last task of its run, 4: last task of its chunk
+  int pad;
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int NV, int S>
+__global__ void __launch_bounds__(256, 1)
+    expert_group_tma_kernel(int d, const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ W,
+                            const __nv_bfloat16* __restrict__ V, const int32_t* __restrict__ run_off,
+                            const int32_t* __restrict__ n_runs_p, const int32_t* __restrict__ m_loc_p,
+                            const int32_t* __restrict__ stok, const int32_t* __restrict__ sexp,
+                            const float* __restrict__ sgate, float* __restrict__ y, int act,
+                            int* __restrict__ work) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t row_bytes = (uint32_t)d * 2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                    // [nwarps][S]
+  StageMeta* metas = reinterpret_cast<StageMeta*>(bars + nwarps * S);    // [nwarps][S]
+  uint8_t* rows = reinterpret_cast<uint8_t*>(metas + nwarps * S);
+  rows = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(rows) + 127) & ~uintptr_t(127));
+  uint64_t* bar = bars + wid * S;
+  StageMeta* meta = metas + wid * S;
+  uint8_t* ring = rows + (size_t)wid * S * 2 * row_bytes;  // stage s: w_e | v_e
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) tc::mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int n_runs = *n_runs_p, m_loc = *m_loc_p;
+  // two-slot queue of claimed chunks; bnd[s]: lane i holds the first task of run r0+i
+  int nr[2], bnd[2];
+  auto claim = [&](int slot) {
+    int r = 0;
+    if (lane == 0) r = atomicAdd(work, kGChunk);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    const int n = max(0, min(kGChunk, n_runs - r));
+    const int b = (lane <= n && n > 0) ? (r + lane < n_runs ? run_off[r + lane] : m_loc) : 0;
+    if (slot) { nr[1] = n; bnd[1] = b; } else { nr[0] = n; bnd[0] = b; }
+  };
+  auto bound = [&](int slot, int i) { return __shfl_sync(0xffffffffu, slot ? bnd[1] : bnd[0], i); };
+  claim(0);
+  nr[1] = 0;
+  bnd[1] = 0;
+  // producer cursor: chunk slot ps, run prun inside it, task ppos in [.., pend)
+  int ps = 0, prun = 0, ppos = 0, pend = 0;
+  bool pdone = nr[0] == 0, pstart = true;
+  if (!pdone) {
+    ppos = bound(0, 0);
+    pend = bound(0, 1);
+  }
+  int cs = 0;  // consumer chunk slot
+  uint32_t pn = 0, cn = 0;
+  float xf[NV][8], acc[NV][8];
+  uint4 xnext[NV];  // x row of the next run to start, loaded ahead
+  int xnext_tok = -1;
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[j][i] = 0.f;
+
+  while (true) {
+    // ---- producer: keep S tasks in flight ----
+    while (!pdone && pn < cn + S) {
+      if (ppos == pend) {  // next run (and chunk)
+        const int nrun = prun + 1;
+        if (nrun == (ps ? nr[1] : nr[0])) {
+          if (cs != ps) break;  // the consumer still drains the other slot: retry later
+          ps ^= 1;
+          claim(ps);
+          prun = 0;
+          if ((ps ? nr[1] : nr[0]) == 0) {
+            pdone = true;
+            break;
+          }
+        } else {
+          prun = nrun;
+        }
+        ppos = bound(ps, prun);
+        pend = bound(ps, prun + 1);
+        pstart = true;
+      }
+      const int s = pn % S;
+      if (lane == 0) {
+        const int e = sexp[ppos];
+        StageMeta m;
+        m.g = sgate[ppos];
+        m.tok = stok[ppos];
+        const bool last_run = ppos + 1 == pend;
+        m.flags = (pstart ? 1 : 0) | (last_run ? 2 : 0) |
+                  ((last_run && prun + 1 == (ps ? nr[1] : nr[0])) ? 4 : 0);
+        meta[s] = m;
+        uint8_t* st = ring + (size_t)s * 2 * row_bytes;
+        tc::mbar_expect_tx(&bar[s], 2u * row_bytes);
+        bulk_g2s(st, W + (size_t)e * d, row_bytes, &bar[s]);
+        bulk_g2s(st + row_bytes, V + (size_t)e * d, row_bytes, &bar[s]);
+      }
+      pstart = false;
+      ++ppos;
+      ++pn;
+    }
+    if (cn == pn) break;  // nothing in flight and nothing more to issue
+    __syncwarp();  // lane 0's meta stores are visible to the whole warp
+    // ---- consumer: task cn ----
+    const int s = cn % S;
+    tc::mbar_wait(&bar[s], (cn / S) & 1);
+    const StageMeta m = meta[s];
+    const uint8_t* st = ring + (size_t)s * 2 * row_bytes;
+    if (m.flags & 1) {  // first task of a run: x_l into registers (prefetched if possible)
+      if (xnext_tok != m.tok) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) xnext[j] = ld_vec(x + (size_t)m.tok * d + (j * 32 + lane) * 8);
+      }
+#pragma unroll
+      for (int j = 0; j < NV; ++j) VecT<__nv_bfloat16>::unpack(xnext[j], xf[j]);
+      xnext_tok = -1;
+    }
+    // prefetch the x row of the next run that starts inside the ring
+    if (xnext_tok < 0) {
+      for (uint32_t q = cn + 1; q < pn; ++q) {
+        const StageMeta& mq = meta[q % S];
+        if (mq.flags & 1) {
+          xnext_tok = mq.tok;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) xnext[j] = ld_vec(x + (size_t)xnext_tok * d + (j * 32 + lane) * 8);
+          break;
+        }
+      }
+    }
+    float z = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const uint4 u = *reinterpret_cast<const uint4*>(st + (size_t)(j * 32 + lane) * 16);
+      float wf[8];
+      VecT<__nv_bfloat16>::unpack(u, wf);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) z = fmaf(xf[j][i], wf[i], z);
+    }
+    z = warp_sum(z);
+    const float a = m.g * (act == OMNIMOE_IDENTITY ? z : silu_f(z));
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const uint4 u = *reinterpret_cast<const uint4*>(st + row_bytes + (size_t)(j * 32 + lane) * 16);
+      float vf[8];
+      VecT<__nv_bfloat16>::unpack(u, vf);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[j][i] = fmaf(a, vf[i], acc[j][i]);
+    }
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // stage s may be refilled now
+    if (m.flags & 2) {
+      float* yl = y + (size_t)m.tok * d;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const int c = (j * 32 + lane) * 8;
+        red_add_v4(yl + c, acc[j][0], acc[j][1], acc[j][2], acc[j][3]);
+        red_add_v4(yl + c + 4, acc[j][4], acc[j][5], acc[j][6], acc[j][7]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[j][i] = 0.f;
+      }
+    }
+    if (m.flags & 4) cs ^= 1;
+    ++cn;
+  }
+}
+
+template <int NV, int S>
+omnimoe_status launch_group_tma(int d, const void* x, const void* W, const void* V, const omnimoe_plan& plan,
+                                const int32_t* m_loc, float* y, int act, int* work, cudaStream_t st) {
+  const size_t per_warp = (size_t)S * 2 * d * 2;
+  const int warps = (int)std::min<size_t>(8, (size_t)(200 * 1024) / per_warp);
+  const size_t smem = 128 + (size_t)warps * S * (8 + sizeof(StageMeta)) + (size_t)warps * per_warp + 128;
+  auto kern = expert_group_tma_kernel<NV, S>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    set_error("expert_fwd: cannot set shared memory of the TMA group kernel");
+    return OMNIMOE_ERR_CUDA;
+  }
+  kern<<<kSMs, warps * 32, smem, st>>>(d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W),
+                                       static_cast<const __nv_bfloat16*>(V), plan.run_offsets, plan.n_runs, m_loc,
+                                       plan.sorted_token, plan.sorted_expert, plan.sorted_gate, y, act, work);
+  OMNI_CHECK_LAUNCH("expert_group_tma_kernel");
+  return OMNIMOE_OK;
 }
 
 template <typename T>
 omnimoe_status launch_group(int d, const void* x, const void* W, const void* V, const omnimoe_plan& plan,
-                            int64_t n_loc, float* y, int act, cudaStream_t st) {
+                            int64_t n_loc, float* y, int act, int* work, cudaStream_t st) {
   constexpr int E = VecT<T>::E;
   const int nv = (d + 32 * E - 1) / (32 * E);
   auto X = static_cast<const T*>(x);
   auto Wp = static_cast<const T*>(W);
   auto Vp = static_cast<const T*>(V);
   const int32_t* m_loc = plan.expert_offsets + n_loc;
+  if (sizeof(T) == 2 && d % 256 == 0 && d <= 2048 && getenv("OMNIMOE_NO_TMA_GROUP") == nullptr) {
+    switch (d / 256) {
+      case 1: return launch_group_tma<1, 8>(d, x, W, V, plan, m_loc, y, act, work, st);
+      case 2: return launch_group_tma<2, 6>(d, x, W, V, plan, m_loc, y, act, work, st);
+      case 3: return launch_group_tma<3, 4>(d, x, W, V, plan, m_loc, y, act, work, st);
+      case 4: return launch_group_tma<4, 4>(d, x, W, V, plan, m_loc, y, act, work, st);
+      case 5: return launch_group_tma<5, 4>(d, x, W, V, plan, m_loc, y, act, work, st);
+      case 6: return launch_group_tma<6, 3>(d, x, W, V, plan, m_loc, y, act, work, st);
+      case 7: return launch_group_tma<7, 3>(d, x, W, V, plan, m_loc, y, act, work, st);
+      default: return launch_group_tma<8, 3>(d, x, W, V, plan, m_loc, y, act, work, st);
+    }
+  }
 #define OMNI_GROUP_CASE(NVC)                                                                          \
   case NVC: {                                                                                         \
     int per_sm = 1;                                                                                   \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_group_kernel<T, NVC>, 256, 0);      \
     expert_group_kernel<T, NVC><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(                          \
         d, X, Wp, Vp, plan.run_offsets, plan.n_runs, m_loc, plan.sorted_token, plan.sorted_expert,    \
-        plan.sorted_gate, y, act);                                                                    \
+        plan.sorted_gate, y, act, work);                                                              \
     break;                                                                                            \
   }
   switch (nv) {
@@ -224,13 +451,13 @@ omnimoe_status launch_group(int d, const void* x, const void* W, const void* V, 
       if (nv == 3) {
         expert_group_kernel<T, 4><<<kSMs * 4, 256, 0, st>>>(d, X, Wp, Vp, plan.run_offsets, plan.n_runs, m_loc,
                                                              plan.sorted_token, plan.sorted_expert,
-                                                             plan.sorted_gate, y, act);
+                                                             plan.sorted_gate, y, act, work);
         break;
       }
       if (nv <= 8) {
         expert_group_kernel<T, 8><<<kSMs * 4, 256, 0, st>>>(d, X, Wp, Vp, plan.run_offsets, plan.n_runs, m_loc,
                                                              plan.sorted_token, plan.sorted_expert,
-                                                             plan.sorted_gate, y, act);
+                                                             plan.sorted_gate, y, act, work);
         break;
       }
       set_error("expert_fwd: d too large for the grouped kernel (d <= " + std::to_string(256 * E) + ")");
@@ -282,7 +509,7 @@ omnimoe_status launch_warp(int d, const void* x, const void* W, const void* V,
 
 }  // namespace
 
-size_t expert_ws_bytes(const omnimoe_dims&, int64_t) { return 0; }
+size_t expert_ws_bytes(const omnimoe_dims&, int64_t) { return 256; }  // work counter
 
 int64_t resolve_group_size(const omnimoe_dims& d) {
   if (d.group_size > 0) return d.group_size;
@@ -292,7 +519,7 @@ int64_t resolve_group_size(const omnimoe_dims& d) {
 
 omnimoe_status expert_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W,
                           const void* V, const omnimoe_plan& plan, float* y, int accumulate,
-                          void*, cudaStream_t st) {
+                          void* ws, cudaStream_t st) {
   if (!accumulate) {
     if (cudaMemsetAsync(y, 0, (size_t)L * dm.d * sizeof(float), st) != cudaSuccess) {
       set_error("expert_fwd: memset failed");
@@ -302,8 +529,14 @@ omnimoe_status expert_run(const omnimoe_dims& dm, int64_t L, const void* x, cons
   const int64_t B = resolve_group_size(dm);
   const int64_t n_loc = plan.expert_end - plan.expert_begin;
   if (B > 1) {
-    if (dm.dtype == OMNIMOE_BF16) return launch_group<__nv_bfloat16>((int)dm.d, x, W, V, plan, n_loc, y, dm.act, st);
-    return launch_group<float>((int)dm.d, x, W, V, plan, n_loc, y, dm.act, st);
+    int* work = static_cast<int*>(ws);
+    if (cudaMemsetAsync(work, 0, sizeof(int), st) != cudaSuccess) {
+      set_error("expert_fwd: memset failed");
+      return OMNIMOE_ERR_CUDA;
+    }
+    if (dm.dtype == OMNIMOE_BF16)
+      return launch_group<__nv_bfloat16>((int)dm.d, x, W, V, plan, n_loc, y, dm.act, work, st);
+    return launch_group<float>((int)dm.d, x, W, V, plan, n_loc, y, dm.act, work, st);
   }
   if (dm.dtype == OMNIMOE_BF16) return launch_warp<__nv_bfloat16>((int)dm.d, x, W, V, plan, y, dm.act, st);
   return launch_warp<float>((int)dm.d, x, W, V, plan, y, dm.act, st);
