@@ -72,7 +72,9 @@ enum { OMNIMOE_ROUTER_EXACT = 0, OMNIMOE_ROUTER_EXACT_F64 = 1 };
  *   router     OMNIMOE_ROUTER_* (ignored in OMNIMOE_F32 mode: always EXACT_F64)
  *   expert_kernel  OMNIMOE_EXPERT_* (a6 kernel choice)
  *   group_size B of Expert-Centric Scheduling: consecutive active
- *              experts per group; 1 = expert-major plan; 0 = library choice.
+ *              experts per group; 1 = expert-major plan; 0 = library choice
+ *              (omnimoe_group_size()).
+ *   token_blocks T_b: see below.
  */
 typedef struct {
   int64_t d, n_rows, n_cols, top_k, n_heads, d_ff;
@@ -81,6 +83,10 @@ typedef struct {
   int32_t router;        /* OMNIMOE_ROUTER_* */
   int32_t expert_kernel; /* OMNIMOE_EXPERT_* */
   int64_t group_size;    /* B >= 0 */
+  int64_t token_blocks;  /* T_b >= 0: the plan is Eq.Sort applied to T_b consecutive token
+                          * blocks in turn, so that one block's x and y_routed stay
+                          * L2-resident; 1 = the paper's single sort;
+                          * 0 = library choice */
 } omnimoe_dims;
 
 /* Expert-centric plan for the local expert range [expert_begin, expert_end)
@@ -117,9 +123,13 @@ typedef struct {
 } omnimoe_plan;
 
 /* The group size B that omnimoe_schedule / omnimoe_expert_fwd use for dims
- * (dims.group_size if > 0, else the library's choice: N_c in bf16 mode, 1 in
- * fp32 mode).  Returns 0 on invalid dims. */
+ * (dims.group_size if > 0, else the library's choice: 8*N_c experts, at most
+ * 64 MB of W/V rows, in bf16 mode; 1 in fp32 mode).  Returns 0 on invalid dims. */
 int64_t omnimoe_group_size(const omnimoe_dims* dims);
+/* The number of token blocks T_b omnimoe_schedule uses for a batch of L tokens
+ * (dims.token_blocks if > 0, else 1; always 1 for B = 1).  Block b holds tokens
+ * [b*ceil(L/T_b), (b+1)*ceil(L/T_b)); the plan sorts by (block, q, token). */
+int64_t omnimoe_token_blocks(const omnimoe_dims* dims, int64_t L);
 
 /* Bytes of workspace needed by entry point `which` (OMNIMOE_WS_*) for L
  * tokens (ROUTE, EXPERT, LAYER) or M tasks (SCHEDULE: pass M as L). */
@@ -146,9 +156,11 @@ omnimoe_status omnimoe_route(const omnimoe_dims* dims, int64_t L, const void* x,
 
 /* Expert-Centric Scheduling: flatten M tasks in token-major order
  * (Eq.Tasks), histogram + exclusive scan over local experts, active-list
- * compaction, group ids q = floor(rank / B), stable LSD radix sort by q
- * (Eq.Sort; "radix sort") -- stability over the token-major input
- * makes tokens ascend inside each group -- and, for B > 1, run detection.
+ * compaction, group ids q = floor(rank / B), stable LSD radix sort by
+ * (token block, q) (Eq.Sort per token block; "radix sort") --
+ * stability over the token-major input makes tokens ascend inside each group --
+ * and, for B > 1, run detection.  The token of task t must be non-decreasing
+ * in t when T_b > 1 (true for the default token = t / (h*K)).
  *   idx   int32[M]  global expert ids of the tasks
  *   gate  float[M]
  *   token int32[M]  nullable: token of task t defaults to t / (h*K)

@@ -38,7 +38,7 @@ def lib():
         _lib.oracle_exact_dot.argtypes = [P, P, i64]
         _lib.oracle_exact_dot.restype = ctypes.c_float
         _lib.oracle_route.argtypes = [i64, i64, i64, i64, P, c_int, i64, c_int, P, P, P, P, P, P]
-        _lib.oracle_schedule.argtypes = [i64, P, P, P, i64, i64, i64, P, P, P, P, P, P, P, P]
+        _lib.oracle_schedule.argtypes = [i64, P, P, P, i64, i64, i64, i64, P, P, P, P, P, P, P, P]
         _lib.oracle_routed_grouped.argtypes = [i64, i64, i64, i64, P, P, P, P, P, P, P, c_int, P]
         _lib.oracle_routed_token_centric.argtypes = [i64, i64, i64, P, P, P, P, P, c_int, P, c_int]
         _lib.oracle_routed_expert_centric.argtypes = [i64, i64, i64, P, P, P, P, P, P, c_int, P]
@@ -97,8 +97,9 @@ def route(logit_rows, n_rows, n_cols, K, method=PRODUCT, bsel=4096, nthreads=Non
     return out
 
 
-def schedule(ids, gates, tokens, n_begin, n_end, B=1):
-    """Expert-centric plan with group size B; see oracle_schedule."""
+def schedule(ids, gates, tokens, n_begin, n_end, B=1, tpb=0):
+    """Expert-centric plan with group size B, scheduled in blocks
+    of tpb consecutive tasks when tpb > 0; see oracle_schedule."""
     ids = np.ascontiguousarray(ids, dtype=np.int32).reshape(-1)
     gates = _f64(gates).reshape(-1)
     tokens = np.ascontiguousarray(tokens, dtype=np.int32).reshape(-1)
@@ -111,7 +112,7 @@ def schedule(ids, gates, tokens, n_begin, n_end, B=1):
     active = np.empty(max(n_loc, 1), np.int32)
     na = np.zeros(1, np.int64)
     nr = np.zeros(1, np.int64)
-    lib().oracle_schedule(M, _p(ids), _p(gates), _p(tokens), n_begin, n_end, B, _p(offsets), _p(st),
+    lib().oracle_schedule(M, _p(ids), _p(gates), _p(tokens), n_begin, n_end, B, tpb, _p(offsets), _p(st),
                           _p(sg), _p(se), _p(active), _p(na), _p(ro), _p(nr))
     m_loc = int(offsets[-1])
     return dict(offsets=offsets, sorted_token=st[:m_loc], sorted_gate=sg[:m_loc], sorted_expert=se[:m_loc],

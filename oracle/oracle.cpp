@@ -294,14 +294,17 @@ void oracle_route(int64_t T, int64_t Nr, int64_t Nc, int64_t K, const float* log
 // tau-th of them belongs to group q = floor(tau / B); tasks are
 // sorted by (q, token) (Eq.Sort) with a stable counting sort on
 // q over the token-major list (tokens then ascend inside each group; tasks of
-// one token in one group keep their task order).  Outputs, for local expert
+// one token in one group keep their task order).  With tpb > 0 the batch is
+// scheduled in blocks of tpb consecutive tasks (the paper's
+// sort applied to each token block in turn): the key is (t / tpb, q).
+// Outputs, for local expert
 // e = id - n_begin:
 //   offsets[e] .. offsets[e+1]   count prefix of expert e (its B = 1 segment)
 //   sorted_token/gate/expert     tasks in (q, token) order
 //   active[0..n_active)          E_active (local ids, ascending)
 //   run_offsets[0..n_runs)       first task of each maximal (q, token) run
 void oracle_schedule(int64_t M, const int32_t* ids, const double* gates, const int32_t* tokens,
-                     int64_t n_begin, int64_t n_end, int64_t B, int32_t* offsets,
+                     int64_t n_begin, int64_t n_end, int64_t B, int64_t tpb, int32_t* offsets,
                      int32_t* sorted_token, double* sorted_gate, int32_t* sorted_expert,
                      int32_t* active, int64_t* n_active, int32_t* run_offsets, int64_t* n_runs) {
   int64_t n_loc = n_end - n_begin;
@@ -320,15 +323,21 @@ void oracle_schedule(int64_t M, const int32_t* ids, const double* gates, const i
     }
   *n_active = na;
   const int64_t n_groups = (na + B - 1) / B;
-  // stable counting sort of the in-range tasks by group
-  std::vector<int64_t> gstart(n_groups + 1, 0);
+  const int64_t n_blocks = tpb > 0 ? (M + tpb - 1) / tpb : 1;
+  auto key = [&](int64_t t) {
+    return (tpb > 0 ? t / tpb : 0) * n_groups + group[ids[t] - n_begin];
+  };
+  // stable counting sort of the in-range tasks by (block, group)
+  std::vector<int64_t> gstart(n_blocks * n_groups + 1, 0);
   for (int64_t t = 0; t < M; ++t)
-    if (ids[t] >= n_begin && ids[t] < n_end) gstart[group[ids[t] - n_begin] + 1]++;
-  for (int64_t q = 0; q < n_groups; ++q) gstart[q + 1] += gstart[q];
+    if (ids[t] >= n_begin && ids[t] < n_end) gstart[key(t) + 1]++;
+  for (int64_t q = 0; q < n_blocks * n_groups; ++q) gstart[q + 1] += gstart[q];
+  std::vector<int64_t> skey(M);
   for (int64_t t = 0; t < M; ++t) {  // visits tasks in t order: stable
     if (ids[t] < n_begin || ids[t] >= n_end) continue;
     const int64_t e = ids[t] - n_begin;
-    const int64_t p = gstart[group[e]]++;
+    const int64_t p = gstart[key(t)]++;
+    skey[p] = key(t);
     sorted_token[p] = tokens[t];
     sorted_gate[p] = gates[t];
     sorted_expert[p] = (int32_t)e;
@@ -337,8 +346,7 @@ void oracle_schedule(int64_t M, const int32_t* ids, const double* gates, const i
   const int64_t m_loc = offsets[n_loc];
   int64_t nr = 0;
   for (int64_t p = 0; p < m_loc; ++p)
-    if (p == 0 || sorted_token[p] != sorted_token[p - 1] ||
-        group[sorted_expert[p]] != group[sorted_expert[p - 1]])
+    if (p == 0 || sorted_token[p] != sorted_token[p - 1] || skey[p] != skey[p - 1])
       run_offsets[nr++] = (int32_t)p;
   *n_runs = nr;
 }

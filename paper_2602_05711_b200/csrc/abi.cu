@@ -78,8 +78,8 @@ omnimoe_status validate_dims(const omnimoe_dims* dp) {
     set_error("unknown router mode " + std::to_string(d.router));
     return OMNIMOE_ERR_UNSUPPORTED;
   }
-  if (d.group_size < 0) {
-    set_error("group_size must be >= 0");
+  if (d.group_size < 0 || d.token_blocks < 0) {
+    set_error("group_size and token_blocks must be >= 0");
     return OMNIMOE_ERR_INVALID_ARGUMENT;
   }
   if (d.expert_kernel < OMNIMOE_EXPERT_AUTO || d.expert_kernel > OMNIMOE_EXPERT_GROUP) {
@@ -319,7 +319,9 @@ omnimoe_status omnimoe_schedule(const omnimoe_dims* dims, int64_t M, const int32
   const int64_t n_loc = plan->expert_end - plan->expert_begin;
   OMNI_TRY(check_ws(ws_bytes, schedule_ws_bytes(M, n_loc), "schedule"));
   OMNI_TRY(check_device());
-  return schedule_run(M, idx, gate, token, dims->n_heads * dims->top_k, *plan, B, ws, (cudaStream_t)stream);
+  const int64_t hk = dims->n_heads * dims->top_k;
+  return schedule_run(M, idx, gate, token, hk, *plan, B, resolve_token_blocks(*dims, (M + hk - 1) / hk), ws,
+                      (cudaStream_t)stream);
 }
 
 omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* W_loc,
@@ -406,7 +408,8 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
   const int64_t M = L * d.n_heads * d.top_k;
   OMNI_TRY(route_impl(d, L, x, subkeys, idx, gate, nullptr, w.route_ws, st));
   const int r_launch = omnimoe_last_launch_count();
-  OMNI_TRY(schedule_run(M, idx, gate, nullptr, d.n_heads * d.top_k, w.plan, resolve_group_size(d), w.sched_ws, st));
+  OMNI_TRY(schedule_run(M, idx, gate, nullptr, d.n_heads * d.top_k, w.plan, resolve_group_size(d),
+                        resolve_token_blocks(d, L), w.sched_ws, st));
   OMNI_TRY(expert_run(d, L, x, W, V, w.plan, w.y_routed, 0, w.expert_ws, st));
   if (d.d_ff > 0) {
     OMNI_TRY(mlp_impl(d, L, x, w_gate_up, w_down, w.y_routed, y, w.H, st));
@@ -478,6 +481,11 @@ int omnimoe_last_launch_count(void) { return g_launches; }
 int64_t omnimoe_group_size(const omnimoe_dims* dims) {
   if (validate_dims(dims) != OMNIMOE_OK) return 0;
   return resolve_group_size(*dims);
+}
+
+int64_t omnimoe_token_blocks(const omnimoe_dims* dims, int64_t L) {
+  if (validate_dims(dims) != OMNIMOE_OK || L < 0) return 0;
+  return resolve_token_blocks(*dims, L);
 }
 
 const char* omnimoe_status_string(omnimoe_status s) {

@@ -208,6 +208,26 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- packed math helpers (sm_100a) ----
+// z += x.lo*w.lo + x.hi*w.hi with bf16 inputs and fp32 accumulation (FHFMA.BF16)
+__device__ __forceinline__ float dot2_bf16(float z, uint32_t xp, uint32_t wp) {
+  asm("{ .reg .b16 xl, xh, wl, wh;\n\t"
+      "mov.b32 {xl, xh}, %1;\n\t"
+      "mov.b32 {wl, wh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, xl, wl, %0;\n\t"
+      "fma.rn.f32.bf16 %0, xh, wh, %0; }"
+      : "+f"(z)
+      : "r"(xp), "r"(wp));
+  return z;
+}
+// acc.{x,y} += a * {v.lo, v.hi} (bf16x2 v widened exactly to fp32) with one FFMA2
+__device__ __forceinline__ void axpy2_bf16(unsigned long long& acc, unsigned long long a2, uint32_t vp) {
+  const unsigned long long v2 = ((unsigned long long)(vp & 0xFFFF0000u) << 32) | (unsigned long long)(vp << 16);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a2), "l"(v2));
+}
+__device__ __forceinline__ float lo_f(unsigned long long p) { return __uint_as_float((uint32_t)p); }
+__device__ __forceinline__ float hi_f(unsigned long long p) { return __uint_as_float((uint32_t)(p >> 32)); }
+
 // ---------------------------------------------------------------------------
 // expert_group_tma_kernel: the run-major executor with its expert rows staged by
 // the TMA engine.  Each warp is independent: lane 0 is its producer, issuing
@@ -232,6 +252,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// same, with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
 template <int NV, int S>
 __global__ void __launch_bounds__(256, 1)
@@ -240,8 +274,9 @@ __global__ void __launch_bounds__(256, 1)
                             const int32_t* __restrict__ n_runs_p, const int32_t* __restrict__ m_loc_p,
                             const int32_t* __restrict__ stok, const int32_t* __restrict__ sexp,
                             const float* __restrict__ sgate, float* __restrict__ y, int act,
-                            int* __restrict__ work) {
+                            int* __restrict__ work, int wv_evict_first) {
   extern __shared__ __align__(128) uint8_t smem[];
+  const uint64_t pol = policy_evict_first();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t row_bytes = (uint32_t)d * 2;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                    // [nwarps][S]
@@ -281,13 +316,14 @@ __global__ void __launch_bounds__(256, 1)
   }
   int cs = 0;  // consumer chunk slot
   uint32_t pn = 0, cn = 0;
-  float xf[NV][8], acc[NV][8];
-  uint4 xnext[NV];  // x row of the next run to start, loaded ahead
+  uint4 xv[NV];                   // x_l of the current run (packed bf16)
+  unsigned long long acc[NV][4];  // fp32 pairs of the run's partial y_l
+  uint4 xnext[NV];                // x row of the next run to start, loaded ahead
   int xnext_tok = -1;
 #pragma unroll
   for (int j = 0; j < NV; ++j)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[j][i] = 0.f;
+    for (int i = 0; i < 4; ++i) acc[j][i] = 0ull;
 
   while (true) {
     // ---- producer: keep S tasks in flight ----
@@ -322,8 +358,13 @@ __global__ void __launch_bounds__(256, 1)
         meta[s] = m;
         uint8_t* st = ring + (size_t)s * 2 * row_bytes;
         tc::mbar_expect_tx(&bar[s], 2u * row_bytes);
-        bulk_g2s(st, W + (size_t)e * d, row_bytes, &bar[s]);
-        bulk_g2s(st + row_bytes, V + (size_t)e * d, row_bytes, &bar[s]);
+        if (wv_evict_first) {  // W/V stream through L2 without evicting x / y_routed
+          bulk_g2s_hint(st, W + (size_t)e * d, row_bytes, &bar[s], pol);
+          bulk_g2s_hint(st + row_bytes, V + (size_t)e * d, row_bytes, &bar[s], pol);
+        } else {
+          bulk_g2s(st, W + (size_t)e * d, row_bytes, &bar[s]);
+          bulk_g2s(st + row_bytes, V + (size_t)e * d, row_bytes, &bar[s]);
+        }
       }
       pstart = false;
       ++ppos;
@@ -342,7 +383,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int j = 0; j < NV; ++j) xnext[j] = ld_vec(x + (size_t)m.tok * d + (j * 32 + lane) * 8);
       }
 #pragma unroll
-      for (int j = 0; j < NV; ++j) VecT<__nv_bfloat16>::unpack(xnext[j], xf[j]);
+      for (int j = 0; j < NV; ++j) xv[j] = xnext[j];
       xnext_tok = -1;
     }
     // prefetch the x row of the next run that starts inside the ring
@@ -357,24 +398,29 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
-    float z = 0.f;
+    // z = x_l . w_e: FHFMA.BF16 into NV independent partial sums
+    float zp[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const uint4 u = *reinterpret_cast<const uint4*>(st + (size_t)(j * 32 + lane) * 16);
-      float wf[8];
-      VecT<__nv_bfloat16>::unpack(u, wf);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) z = fmaf(xf[j][i], wf[i], z);
+      float t = dot2_bf16(0.f, xv[j].x, u.x);
+      t = dot2_bf16(t, xv[j].y, u.y);
+      t = dot2_bf16(t, xv[j].z, u.z);
+      zp[j] = dot2_bf16(t, xv[j].w, u.w);
     }
+    float z = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) z += zp[j];
     z = warp_sum(z);
     const float a = m.g * (act == OMNIMOE_IDENTITY ? z : silu_f(z));
+    const unsigned long long a2 = ((unsigned long long)__float_as_uint(a) << 32) | __float_as_uint(a);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const uint4 u = *reinterpret_cast<const uint4*>(st + row_bytes + (size_t)(j * 32 + lane) * 16);
-      float vf[8];
-      VecT<__nv_bfloat16>::unpack(u, vf);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[j][i] = fmaf(a, vf[i], acc[j][i]);
+      axpy2_bf16(acc[j][0], a2, u.x);
+      axpy2_bf16(acc[j][1], a2, u.y);
+      axpy2_bf16(acc[j][2], a2, u.z);
+      axpy2_bf16(acc[j][3], a2, u.w);
     }
     __syncwarp();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // stage s may be refilled now
@@ -383,10 +429,10 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
         const int c = (j * 32 + lane) * 8;
-        red_add_v4(yl + c, acc[j][0], acc[j][1], acc[j][2], acc[j][3]);
-        red_add_v4(yl + c + 4, acc[j][4], acc[j][5], acc[j][6], acc[j][7]);
+        red_add_v4(yl + c, lo_f(acc[j][0]), hi_f(acc[j][0]), lo_f(acc[j][1]), hi_f(acc[j][1]));
+        red_add_v4(yl + c + 4, lo_f(acc[j][2]), hi_f(acc[j][2]), lo_f(acc[j][3]), hi_f(acc[j][3]));
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[j][i] = 0.f;
+        for (int i = 0; i < 4; ++i) acc[j][i] = 0ull;
       }
     }
     if (m.flags & 4) cs ^= 1;
@@ -407,7 +453,8 @@ omnimoe_status launch_group_tma(int d, const void* x, const void* W, const void*
   }
   kern<<<kSMs, warps * 32, smem, st>>>(d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W),
                                        static_cast<const __nv_bfloat16*>(V), plan.run_offsets, plan.n_runs, m_loc,
-                                       plan.sorted_token, plan.sorted_expert, plan.sorted_gate, y, act, work);
+                                       plan.sorted_token, plan.sorted_expert, plan.sorted_gate, y, act, work,
+                                       getenv("OMNIMOE_WV_EVICT_FIRST") ? atoi(getenv("OMNIMOE_WV_EVICT_FIRST")) : 0);
   OMNI_CHECK_LAUNCH("expert_group_tma_kernel");
   return OMNIMOE_OK;
 }
@@ -514,7 +561,18 @@ size_t expert_ws_bytes(const omnimoe_dims&, int64_t) { return 256; }  // work co
 int64_t resolve_group_size(const omnimoe_dims& d) {
   if (d.group_size > 0) return d.group_size;
   if (d.dtype != OMNIMOE_BF16) return 1;  // fp32 correctness mode: expert-major
-  return d.n_cols;                         // one grid row of experts per group
+  // eight grid rows of experts per group, capped so one group's W/V rows (4d bytes
+  // per expert) stay within 64 MB of L2 (tools/sweep_group.py)
+  const int64_t cap = std::max<int64_t>(1, (64ll << 20) / (4 * d.d));
+  return std::max<int64_t>(2, std::min<int64_t>(8 * d.n_cols, cap));
+}
+
+int64_t resolve_token_blocks(const omnimoe_dims& d, int64_t L) {
+  if (resolve_group_size(d) == 1) return 1;
+  (void)L;
+  // measured (profiles/r1/sweep_*.log): blocking the batch does not pay at C3a --
+  // the W/V stream evicts y_routed between a token's runs whatever the block size
+  return d.token_blocks > 0 ? d.token_blocks : 1;
 }
 
 omnimoe_status expert_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W,

@@ -212,12 +212,15 @@ __global__ void __launch_bounds__(kRadixThreads)
 // B > 1: replace each in-range key (local expert id) by its group
 // q = rank_active(e) / B; out-of-range tasks keep a sentinel that
 // sorts behind every group.
+// With T_b token blocks the key is (block of t) * n_groups_max + q, so the sort
+// is Eq.Sort applied to each block of tpb consecutive tasks in turn.
 __global__ void group_keys_kernel(uint32_t* __restrict__ keys, int64_t M, int64_t n_loc,
-                                  const int32_t* __restrict__ rank, int64_t B, uint32_t sentinel) {
+                                  const int32_t* __restrict__ rank, int64_t B, int64_t tpb,
+                                  uint32_t n_groups_max, uint32_t sentinel) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < M;
        t += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t e = keys[t];
-    keys[t] = e < (uint32_t)n_loc ? (uint32_t)(rank[e] / B) : sentinel;
+    keys[t] = e < (uint32_t)n_loc ? (uint32_t)(t / tpb) * n_groups_max + (uint32_t)(rank[e] / B) : sentinel;
   }
 }
 
@@ -269,7 +272,8 @@ size_t schedule_ws_bytes(int64_t M, int64_t n_loc) {
 }
 
 omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, const int32_t* token,
-                            int64_t hk, const omnimoe_plan& plan, int64_t B, void* ws, cudaStream_t st) {
+                            int64_t hk, const omnimoe_plan& plan, int64_t B, int64_t Tb, void* ws,
+                            cudaStream_t st) {
   const int64_t n_loc = plan.expert_end - plan.expert_begin;
   const int64_t nb = (M + kRadixTile - 1) / kRadixTile;
   Carver c(ws);
@@ -301,8 +305,13 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
   int64_t n_keys = n_loc;  // largest key value (the sentinel)
   if (B > 1) {
     OMNI_TRY(scan<2>(cnt, n_loc, rank, nullptr, tiles, st));
-    n_keys = (n_loc + B - 1) / B;
-    group_keys_kernel<<<grid_for(M, 256), 256, 0, st>>>(k0, M, n_loc, rank, B, (uint32_t)n_keys);
+    const int64_t ngm = (n_loc + B - 1) / B;
+    const int64_t L = (M + hk - 1) / hk;
+    Tb = std::max<int64_t>(1, std::min<int64_t>(Tb, L));
+    const int64_t tpb = hk * ((L + Tb - 1) / Tb);  // tasks per block, whole tokens
+    n_keys = Tb * ngm;
+    group_keys_kernel<<<grid_for(M, 256), 256, 0, st>>>(k0, M, n_loc, rank, B, tpb, (uint32_t)ngm,
+                                                        (uint32_t)n_keys);
     OMNI_CHECK_LAUNCH("group_keys_kernel");
   }
   // a5: stable LSD radix sort of the keys (sentinel included), task index payload

@@ -8,8 +8,10 @@ namespace omni {
 size_t schedule_ws_bytes(int64_t M, int64_t n_loc);
 // hk = h*K: default token of task t is t / hk when token == nullptr.
 omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, const int32_t* token,
-                            int64_t hk, const omnimoe_plan& plan, int64_t B, void* ws, cudaStream_t st);
+                            int64_t hk, const omnimoe_plan& plan, int64_t B, int64_t Tb, void* ws,
+                            cudaStream_t st);
 int64_t resolve_group_size(const omnimoe_dims& d);
+int64_t resolve_token_blocks(const omnimoe_dims& d, int64_t L);
 
 size_t expert_ws_bytes(const omnimoe_dims& d, int64_t L);
 omnimoe_status expert_run(const omnimoe_dims& d, int64_t L, const void* x, const void* W,

@@ -32,7 +32,8 @@ class Dims(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int64), ("n_rows", ctypes.c_int64), ("n_cols", ctypes.c_int64),
                 ("top_k", ctypes.c_int64), ("n_heads", ctypes.c_int64), ("d_ff", ctypes.c_int64),
                 ("dtype", ctypes.c_int32), ("act", ctypes.c_int32), ("router", ctypes.c_int32),
-                ("expert_kernel", ctypes.c_int32), ("group_size", ctypes.c_int64)]
+                ("expert_kernel", ctypes.c_int32), ("group_size", ctypes.c_int64),
+                ("token_blocks", ctypes.c_int64)]
 
 
 class Plan(ctypes.Structure):
@@ -46,7 +47,7 @@ class Plan(ctypes.Structure):
 EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnimoe_expert_fwd",
            "omnimoe_shared_mlp", "omnimoe_layer_fwd", "omnimoe_router_logits", "omnimoe_gemm_bf16",
            "omnimoe_last_launch_count", "omnimoe_status_string", "omnimoe_last_error",
-           "omnimoe_group_size"]
+           "omnimoe_group_size", "omnimoe_token_blocks"]
 
 _lib = None
 
@@ -78,6 +79,8 @@ def load(path: str = LIB_PATH):
     lib.omnimoe_last_launch_count.restype = ctypes.c_int
     lib.omnimoe_group_size.argtypes = [PD]
     lib.omnimoe_group_size.restype = ctypes.c_int64
+    lib.omnimoe_token_blocks.argtypes = [PD, ctypes.c_int64]
+    lib.omnimoe_token_blocks.restype = ctypes.c_int64
     lib.omnimoe_status_string.restype = ctypes.c_char_p
     lib.omnimoe_status_string.argtypes = [ctypes.c_int]
     lib.omnimoe_last_error.restype = ctypes.c_char_p
@@ -109,6 +112,7 @@ class LayerDims:
     router: int = ROUTER_EXACT
     expert_kernel: int = EXPERT_AUTO
     group_size: int = 0
+    token_blocks: int = 0
 
     @property
     def N(self) -> int:
@@ -120,7 +124,8 @@ class LayerDims:
 
     def c(self) -> Dims:
         return Dims(self.d, self.n_rows, self.n_cols, self.top_k, self.n_heads, self.d_ff,
-                    self.dtype, self.act, self.router, self.expert_kernel, self.group_size)
+                    self.dtype, self.act, self.router, self.expert_kernel, self.group_size,
+                    self.token_blocks)
 
 
 def _ptr(t):
@@ -176,6 +181,12 @@ def group_size(dims: LayerDims) -> int:
     """The group size B the library uses for these dims."""
     dc = dims.c()
     return int(load().omnimoe_group_size(ctypes.byref(dc)))
+
+
+def token_blocks(dims: LayerDims, L: int) -> int:
+    """The number of token blocks T_b the schedule uses for L tokens."""
+    dc = dims.c()
+    return int(load().omnimoe_token_blocks(ctypes.byref(dc), L))
 
 
 def new_plan(n_loc: int, M: int, device, expert_begin: int = 0):

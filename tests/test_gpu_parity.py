@@ -186,8 +186,8 @@ def test_route_k_equals_n():
 
 
 # ---------------------------------------------------------------- schedule
-def _check_plan(plan, ids, gates, toks, b, e, B):
-    p = oracle.schedule(ids, gates, toks, b, e, B=B)
+def _check_plan(plan, ids, gates, toks, b, e, B, tpb=0):
+    p = oracle.schedule(ids, gates, toks, b, e, B=B, tpb=tpb)
     m = int(p["offsets"][-1])
     np.testing.assert_array_equal(plan["expert_offsets"].cpu().numpy(), p["offsets"])
     np.testing.assert_array_equal(plan["sorted_token"].cpu().numpy()[:m], p["sorted_token"])
@@ -202,22 +202,24 @@ def _check_plan(plan, ids, gates, toks, b, e, B):
         np.testing.assert_array_equal(plan["run_offsets"].cpu().numpy()[:nr], p["run_offsets"])
 
 
-@pytest.mark.parametrize("B", [1, 2, 1024])
+@pytest.mark.parametrize("B,Tb", [(1, 1), (2, 1), (1024, 1), (1024, 3)])
 @pytest.mark.parametrize("N,L,HK,b,e", [(1024, 256, 8, 0, 1024), (65536, 2048, 64, 0, 65536),
                                         (1 << 20, 4096, 512, 0, 1 << 20), (1000, 300, 7, 250, 700),
                                         (5, 50, 3, 0, 5), (1 << 20, 16, 16, 1 << 19, 1 << 20)])
-def test_schedule_bit_exact(N, L, HK, b, e, B):
+def test_schedule_bit_exact(N, L, HK, b, e, B, Tb):
     rng = np.random.default_rng(N + L)
     ids = rng.integers(0, N, (L, HK)).astype(np.int32)
     gates = rng.random((L, HK)).astype(np.float32)
-    d = om.LayerDims(d=8, n_rows=N, n_cols=1, top_k=HK, d_ff=0, group_size=B)
+    d = om.LayerDims(d=8, n_rows=N, n_cols=1, top_k=HK, d_ff=0, group_size=B, token_blocks=Tb)
     assert om.group_size(d) == B
+    Tb = om.token_blocks(d, L)
+    tpb = HK * -(-L // min(Tb, L)) if Tb > 1 else 0
     idx_t = torch.from_numpy(ids).cuda()
     g_t = torch.from_numpy(gates).cuda()
     plan = om.schedule(d, idx_t.reshape(-1), g_t.reshape(-1), expert_begin=b, expert_end=e)
     torch.cuda.synchronize()
     _check_plan(plan, ids.reshape(-1), gates.reshape(-1).astype(np.float64),
-                np.repeat(np.arange(L), HK).astype(np.int32), b, e, B)
+                np.repeat(np.arange(L), HK).astype(np.int32), b, e, B, tpb)
 
 
 @pytest.mark.parametrize("B", [1, 64])
@@ -236,15 +238,17 @@ def test_schedule_all_same_expert_and_empty(B):
 
 
 # ---------------------------------------------------------------- expert compute
-@pytest.mark.parametrize("B", [1, 2, 512])
+@pytest.mark.parametrize("B", [1, 2, 512, -512])
 @pytest.mark.parametrize("dtype", [om.BF16, om.F32])
 @pytest.mark.parametrize("d,act", [(64, om.SILU), (72, om.SILU), (1024, om.SILU), (2048, om.SILU), (64, om.IDENTITY)])
 def test_expert_fwd_given_plan(dtype, d, act, B):
-    if dtype == om.F32 and B > 1 and d > 1024:
+    if dtype == om.F32 and abs(B) > 1 and d > 1024:
         pytest.skip("grouped kernel holds d/128 fp32 vectors per lane: d <= 1024 in fp32 mode")
     rng = np.random.default_rng(d)
     L, N, HK = 200, 3000, 12
-    dims = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, dtype=dtype, act=act, group_size=B)
+    # B < 0: group size |B| scheduled in 3 token blocks
+    dims = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, dtype=dtype, act=act, group_size=abs(B),
+                        token_blocks=3 if B < 0 else 0)
     inp = make_inputs(dims, L, 9, skip=("subkeys",))
     # clustered ids (several tasks of a token share a group) plus repeats across tokens
     base = rng.integers(0, N - 64, L)
@@ -253,7 +257,7 @@ def test_expert_fwd_given_plan(dtype, d, act, B):
     plan = om.schedule(dims, torch.from_numpy(ids).cuda().reshape(-1), torch.from_numpy(gates).cuda().reshape(-1))
     y = om.expert_fwd(dims, inp["x"], inp["W"], inp["V"], plan)
     torch.cuda.synchronize()
-    if B > 1:
+    if abs(B) > 1:
         assert plan["n_runs"].item() < L * HK  # runs really merge tasks
     used = np.unique(ids)
     remap = np.searchsorted(used, ids)

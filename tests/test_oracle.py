@@ -256,15 +256,16 @@ def test_schedule_grouped_golden():
     assert list(p["run_offsets"]) == g["expected_run_offsets"]
 
 
-@pytest.mark.parametrize("B", [1, 2, 3, 7, 1000])
-def test_schedule_grouped_properties(B):
+@pytest.mark.parametrize("B,nblk", [(1, 1), (2, 1), (3, 1), (7, 1), (1000, 1), (3, 2), (7, 3)])
+def test_schedule_grouped_properties(B, nblk):
     rng = np.random.default_rng(40 + B)
     L, HK, N = 60, 5, 41
     ids = rng.integers(0, N, (L, HK)).astype(np.int32)
     gates = rng.random((L, HK))
     toks = np.repeat(np.arange(L), HK).astype(np.int32)
+    tpb = HK * -(-L // nblk) if nblk > 1 else 0
     for (b, e) in [(0, N), (7, 30)]:
-        p = oracle.schedule(ids, gates, toks, b, e, B=B)
+        p = oracle.schedule(ids, gates, toks, b, e, B=B, tpb=tpb)
         fl = ids.reshape(-1)
         sel = (fl >= b) & (fl < e)
         active = sorted(set((fl[sel] - b).tolist()))
@@ -274,8 +275,9 @@ def test_schedule_grouped_properties(B):
         want = sorted(zip(toks[sel], fl[sel] - b, gates.reshape(-1)[sel]))
         got = sorted(zip(p["sorted_token"], p["sorted_expert"], p["sorted_gate"]))
         assert got == want
-        # sorted by (q, l) (Eq.Sort)
-        keys = [(grp[ex], l) for ex, l in zip(p["sorted_expert"], p["sorted_token"])]
+        # sorted by (token block, q, l) (Eq.Sort per token block)
+        blk = (lambda l: l // (tpb // HK)) if tpb else (lambda l: 0)
+        keys = [(blk(l), grp[ex], l) for ex, l in zip(p["sorted_expert"], p["sorted_token"])]
         assert keys == sorted(keys)
         assert len(set(grp.values())) == -(-len(active) // B)  # N_groups = ceil(|E_active| / B)
         # runs partition the plan into maximal constant (q, l) stretches
@@ -284,14 +286,14 @@ def test_schedule_grouped_properties(B):
             assert len(set(keys[ro[r]:ro[r + 1]])) == 1
             if r:
                 assert keys[ro[r]] != keys[ro[r] - 1]
-        if B == 1:  # expert-major: segment of e is [offsets[e], offsets[e+1])
+        if B == 1 and nblk == 1:  # expert-major: segment of e is [offsets[e], offsets[e+1])
             for ex in active:
                 seg = p["sorted_expert"][p["offsets"][ex]:p["offsets"][ex + 1]]
                 assert np.all(seg == ex)
 
 
-@pytest.mark.parametrize("B", [1, 4, 64])
-def test_grouped_executor_equals_token_centric(B):
+@pytest.mark.parametrize("B,tpb", [(1, 0), (4, 0), (64, 0), (4, 9 * 7)])
+def test_grouped_executor_equals_token_centric(B, tpb):
     rng = np.random.default_rng(50 + B)
     L, d, N, HK = 48, 24, 300, 9
     x = rng.standard_normal((L, d))
@@ -299,7 +301,7 @@ def test_grouped_executor_equals_token_centric(B):
     ids = np.stack([rng.choice(N, HK, replace=False) for _ in range(L)]).astype(np.int32)
     g = rng.random((L, HK))
     yt = oracle.routed_token_centric(x, W, V, ids, g)
-    p = oracle.schedule(ids, g, np.repeat(np.arange(L), HK), 0, N, B=B)
+    p = oracle.schedule(ids, g, np.repeat(np.arange(L), HK), 0, N, B=B, tpb=tpb)
     yg = oracle.routed_grouped(x, W, V, p)
     assert np.max(np.abs(yt - yg)) <= 1e-10 * max(1.0, np.max(np.abs(yt)))
 

@@ -11,14 +11,16 @@ from synth.workloads import make_inputs  # noqa: E402
 
 build.build()
 name = sys.argv[1] if len(sys.argv) > 1 else "C3a"
-Bs = [int(b) for b in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1, 512, 1024, 2048, 4096, 8192]
+# entries "B" or "B:Tb" (group size, token blocks; Tb 0 = library choice)
+specs = sys.argv[2].split(",") if len(sys.argv) > 2 else ["1", "1024", "4096"]
+Bs = [tuple(int(v) for v in (s + ":0").split(":")[:2]) for s in specs]
 w = configs.get(name)
 inp = make_inputs(w.dims, w.L, w.seed, skip=("w_gate_up", "w_down"))
 idx, gate, _ = om.route(w.dims, inp["x"], inp["subkeys"], want_score=False)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 out = {}
-for B in Bs:
-    dims = configs.get(name, group_size=B).dims
+for B, Tb in Bs:
+    dims = configs.get(name, group_size=B, token_blocks=Tb).dims
     M = idx.numel()
     plan = om.new_plan(dims.N, M, "cuda")
     sws = om.workspace(dims, M, om.WS_SCHEDULE)
@@ -39,7 +41,8 @@ for B in Bs:
         if it:
             ts.append(e[0].elapsed_time(e[1]))
             te.append(e[2].elapsed_time(e[3]))
-    out[B] = {"schedule_ms": sorted(ts)[len(ts) // 2], "expert_ms": sorted(te)[len(te) // 2],
+    key = f"{B}:{om.token_blocks(dims, w.L)}"
+    out[key] = {"schedule_ms": sorted(ts)[len(ts) // 2], "expert_ms": sorted(te)[len(te) // 2],
               "n_runs": int(plan["n_runs"].item()) if B > 1 else None}
-    print(name, B, out[B], flush=True)
+    print(name, key, out[key], flush=True)
 print(json.dumps({name: out}))
