@@ -3,13 +3,19 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3a] [--impl ours|reference]
 
-A step is one omnimoe_layer_fwd over one batch of the workload's L tokens (all
-of steps a1-a8: route, schedule, expert compute, shared MLP + combine), with
-inputs resident in HBM.  Every timed step is preceded by an L2 flush (a 256 MB
-write, outside the events); steps are timed with CUDA events on the launching
-stream, synchronised and barriered on both sides, max over ranks.
-Rank 0 prints one JSON line.  Multi-GPU (torchrun) runs the expert-parallel
-layer of paper_2602_05711_b200.distributed.
+A step is one OmniMoE layer forward (steps a1-a8 of DESIGN.md: route, schedule,
+grouped expert compute, shared MLP + combine) over one batch of the workload's
+L tokens per GPU, inputs resident in HBM.  Every timed step is preceded by an L2
+flush (a 256 MB write, outside the events); steps are timed with CUDA events on
+the launching stream, barrier + synchronize on both sides, max over ranks.
+
+N = 1: omnimoe_layer_fwd (the single-GPU C-ABI call).  N > 1 (torchrun): the
+expert-parallel layer of paper_2602_05711_b200.distributed -- each rank keeps L
+tokens (weak scaling) and 1/N of the expert table's rows; NCCL all-to-all
+dispatch and combine.  Rank 0 prints ONE JSON line.
+
+--impl reference: the CPU oracle (oracle/, as it stands) on a bounded token
+sample of the same workload on the host cores.
 """
 from __future__ import annotations
 
@@ -37,7 +43,7 @@ def peaks():
     if os.path.exists(p):
         j = json.load(open(p))
         return dict(hbm=j.get("hbm_gbs", 6552.0), bf16=j.get("bf16_tflops", 1677.0),
-                    bf16_sus=j.get("bf16_tflops_sustained", 1413.9), src="MEASURED_PEAKS.json")
+                    bf16_sus=j.get("bf16_tflops_sustained", 1413.9), src="measured (MEASURED_PEAKS.json)")
     return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback (B200_PROFILING.md)")
 
 
@@ -57,6 +63,7 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.3)
         except OSError:
             self.proc = None
         return self
@@ -75,139 +82,138 @@ class ClockSampler:
 
     def summary(self):
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
-        reasons = set()
-        for r in self.rows:
-            if len(r) >= 7:
-                for n, v in zip(names, r[3:7]):
-                    if v.lower() == "active":
-                        reasons.add(n)
+        ok = [r for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in ok]
+        mx = [float(r[1]) for r in ok if r[1].replace(".", "").isdigit()]
+        reasons = sorted({n for r in ok for n, v in zip(names, r[3:7]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": reasons, "samples": len(sm)}
 
 
-def algorithmic_a6(dims, L, n_active, M):
-    """a6 algorithmic HBM bytes per launch: W and V rows of
-    each active expert once (Eq.(vii)) + x read + y_routed write
-    (fp32) + plan (token id + gate per task, segment offsets per active expert)."""
+def rank_info():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def a6_algorithmic_bytes(dims, L, n_active, M):
+    """a6 algorithmic HBM bytes per launch: W and V rows of every
+    active expert once (D_expert) + x read + y_routed fp32 write +
+    plan (token + gate per task, offsets per active expert)."""
     eb = 2 if dims.dtype == 0 else 4
-    return (2 * n_active * dims.d * eb + L * dims.d * eb + L * dims.d * 4 + 8 * M + 8 * n_active)
+    return 2 * n_active * dims.d * eb + L * dims.d * eb + L * dims.d * 4 + 8 * M + 8 * n_active
 
 
-def cpu_oracle_rate(w, n_tokens, nthreads, mode=0):
-    """Oracle (as it stands) on a bounded token sample; returns tokens/s, tokens, seconds."""
+def ncu_traffic(config, kernel):
+    """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "r1", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None, None
+    j = json.load(open(p))
+    rec = j.get(config, {}).get(kernel)
+    if not rec:
+        return None, None
+    return rec.get("dram_bytes"), rec.get("source")
+
+
+# ---------------------------------------------------------------- CPU oracle
+def cpu_oracle_rate(w, target_s, max_tokens, nthreads, inp=None):
+    """The oracle layer (as it stands) on a bounded token sample.  Expert rows are
+    taken from the seeded generator (the device twin's tables when ``inp`` holds
+    them -- bit-identical to the host generator, tests/test_gpu_parity.py -- else
+    the numpy generator); only the oracle call is timed.  The sample grows in
+    chunks of 32 tokens until ~target_s seconds of oracle time."""
     import oracle
     from tests.helpers import host_rows
     dims = w.dims
     R = dims.n_rows + dims.n_cols
-    sub = host_rows(dims, w.seed, "subkeys", None, mode).reshape(dims.n_heads, R, dims.d)
-    wgu = host_rows(dims, w.seed, "w_gate_up", None, mode) if dims.d_ff else None
-    wdn = host_rows(dims, w.seed, "w_down", None, mode) if dims.d_ff else None
-    chunk = max(1, min(n_tokens, 32))
-    total_t, done = 0.0, 0
-    for c0 in range(0, n_tokens, chunk):
-        toks = np.arange(c0, min(n_tokens, c0 + chunk))
-        x = host_rows(dims, w.seed, "x", toks, mode)
-        # routing decides which expert rows the oracle needs; regenerate only those (not timed)
-        lg = oracle.logits(x, sub, nthreads)
-        r = oracle.route(lg.reshape(-1, R), dims.n_rows, dims.n_cols, dims.top_k, oracle.PRODUCT,
-                         nthreads=nthreads)
+    sub = host_rows(dims, w.seed, "subkeys").reshape(dims.n_heads, R, dims.d)
+    wgu = host_rows(dims, w.seed, "w_gate_up") if dims.d_ff else None
+    wdn = host_rows(dims, w.seed, "w_down") if dims.d_ff else None
+
+    if inp is None and torch.cuda.is_available():
+        # the generator's device twin fills the expert tables fast; the rows the
+        # sample needs are copied to the host (inputs only -- the oracle computes)
+        from synth.workloads import make_inputs
+        inp = make_inputs(dims, 1, w.seed, skip=("x", "subkeys", "w_gate_up", "w_down"))
+
+    def rows(name, used):
+        if inp is not None and name in inp:
+            return inp[name][torch.from_numpy(used).to(inp[name].device)].double().cpu().numpy()
+        return host_rows(dims, w.seed, name, used)
+
+    total_t, done, chunk = 0.0, 0, 32
+    while done < max_tokens and total_t < target_s:
+        toks = np.arange(done, min(max_tokens, done + chunk)) % w.L
+        x = host_rows(dims, w.seed, "x", toks)
+        lg = oracle.logits(x, sub, nthreads)   # routing decides which rows the oracle needs (not timed)
+        r = oracle.route(lg.reshape(-1, R), dims.n_rows, dims.n_cols, dims.top_k, oracle.PRODUCT, nthreads=nthreads)
         used = np.unique(r["idx"])
-        W = host_rows(dims, w.seed, "W", used, mode)
-        V = host_rows(dims, w.seed, "V", used, mode)
+        W, V = rows("W", used), rows("V", used)
         idm = np.stack([used, np.arange(len(used))], 1)
         t0 = time.perf_counter()
-        oracle.layer(x, sub, W, V, dims.n_rows, dims.n_cols, dims.top_k, wgu, wdn, id_map=idm,
-                     nthreads=nthreads)
+        oracle.layer(x, sub, W, V, dims.n_rows, dims.n_cols, dims.top_k, wgu, wdn, id_map=idm, nthreads=nthreads)
         total_t += time.perf_counter() - t0
         done += len(toks)
     return done / total_t, done, total_t
 
 
-def rank_info():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rk = int(os.environ.get("RANK", "0"))
-    lr = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rk, lr
-
-
 def run_reference(args):
-    """--impl reference: the oracle (CPU, host cores) on bounded samples of the same workload."""
+    """--impl reference: the oracle on the host cores, bounded sample per step."""
     ws, rk, _ = rank_info()
     if rk != 0:
         return 0
     from paper_2602_05711_b200 import configs
     w = configs.get(args.config)
     nth = os.cpu_count() or 1
-    n_tok = args.ref_tokens
-    for _ in range(args.warmup if args.warmup <= 1 else 1):
-        cpu_oracle_rate(w, min(n_tok, 8), nth)
-    times = []
+    per_step_s = max(2.0, args.ref_seconds / max(args.steps, 1))
+    cpu_oracle_rate(w, 0.5, 32, nth)  # warm-up (page-in, thread pool)
+    rates, toks = [], 0
     for _ in range(args.steps):
-        rate, done, t = cpu_oracle_rate(w, n_tok, nth)
-        times.append(t)
-    rate = args.steps * n_tok / sum(times)
-    ms = 1000.0 * w.L / rate
+        rate, done, _t = cpu_oracle_rate(w, per_step_s, 1 << 20, nth)
+        rates.append(rate)
+        toks += done
+    rate = statistics.mean(rates)
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "d": w.dims.d, "n_rows": w.dims.n_rows, "n_cols": w.dims.n_cols,
-                       "top_k": w.dims.top_k, "n_heads": w.dims.n_heads, "d_ff": w.dims.d_ff, "tokens": w.L},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * w.L / rate,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config_dict(w, "cpu-oracle"),
             "cpu_baseline": {"value": rate, "unit": "tokens/s", "cores": nth, "kind": "oracle",
-                             "sample": f"{n_tok} tokens of {w.name} per step (oracle layer: fp64 canonical "
-                                       f"logits, product top-K, token-centric routed branch, shared MLP); "
-                                       f"ms_per_step extrapolates to the full {w.L}-token batch"},
+                             "sample": f"{toks} tokens of {w.name} over {args.steps} steps (~{per_step_s:.0f} s of "
+                                       f"oracle time each): exact logits, product top-K, token-centric routed "
+                                       f"branch, shared MLP; ms_per_step extrapolates to the {w.L}-token batch"},
             "e2e": {"value": rate, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C3a")
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-tokens", type=int, default=64)
-    ap.add_argument("--ref-tokens", type=int, default=32)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference(args)
+def _config_dict(w, parallelism):
+    d = w.dims
+    return {"workload": w.name, "d": d.d, "n_rows": d.n_rows, "n_cols": d.n_cols, "N": d.N, "top_k": d.top_k,
+            "n_heads": d.n_heads, "d_ff": d.d_ff, "tokens_per_gpu": w.L, "parallelism": parallelism,
+            "router": "exact (RN32 of the exact dot product; tcgen05 kind::i8 limbs)",
+            "l2": "flushed (256 MB write) before every timed step"}
 
-    ws, rk, lr = rank_info()
-    torch.cuda.set_device(lr)
-    if ws > 1:
-        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", lr))
-    from paper_2602_05711_b200 import build, configs, omnimoe as om
-    build.build()
+
+# ---------------------------------------------------------------- N = 1
+def bench_single(args, w, lr):
+    from paper_2602_05711_b200 import omnimoe as om
     from synth.workloads import make_inputs
-    w = configs.get(args.config)
-    dims = w.dims
-    L = w.L
-    if ws > 1:
-        from paper_2602_05711_b200 import distributed as ep
-        return ep.bench_main(args, w, ws, rk, lr)
-
+    dims, L = w.dims, w.L
     inp = make_inputs(dims, L, w.seed)
     lws = om.workspace(dims, L, om.WS_LAYER)
     y = torch.empty((L, dims.d), dtype=dims.torch_dtype, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream()
 
-    def step():
-        om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], inp["V"], inp.get("w_gate_up"),
+    def step(x=None):
+        om.layer_fwd(dims, inp["x"] if x is None else x, inp["subkeys"], inp["W"], inp["V"], inp.get("w_gate_up"),
                      inp.get("w_down"), y=y, ws=lws)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    launches = om.last_launch_count()
-
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = om.LAUNCHES
     with ClockSampler(lr) as clk:
         torch.cuda.synchronize()
         for i in range(args.steps):
@@ -216,19 +222,20 @@ def main():
             step()
             ev[i][1].record(st)
         torch.cuda.synchronize()
+    launches = om.LAUNCHES - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = statistics.mean(step_ms)
 
     # ---- per-stage breakdown through the individual C-ABI calls (same inputs) ----
-    idx = torch.empty((L, dims.n_heads, dims.top_k), dtype=torch.int32, device="cuda")
-    rws = om.workspace(dims, L, om.WS_ROUTE)
     M = L * dims.n_heads * dims.top_k
+    rws = om.workspace(dims, L, om.WS_ROUTE)
     plan = om.new_plan(dims.N, M, "cuda")
     sws = om.workspace(dims, M, om.WS_SCHEDULE)
+    ews = om.workspace(dims, L, om.WS_EXPERT)
     yr = torch.empty((L, dims.d), dtype=torch.float32, device="cuda")
-    stages = {"route": [], "schedule": [], "expert": [], "shared_mlp": []}
-    for i in range(max(3, args.steps // 2)):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
+    stages = {"route_a1_a3": [], "schedule_a4_a5": [], "expert_a6": [], "shared_mlp_a7_a8": []}
+    for i in range(max(4, args.steps)):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
         flush.zero_()
         e[0].record(st)
         idx, gate, _ = om.route(dims, inp["x"], inp["subkeys"], ws=rws, want_score=False)
@@ -238,19 +245,17 @@ def main():
         yr.zero_()
         flush.zero_()
         e[3].record(st)
-        om.expert_fwd(dims, inp["x"], inp["W"], inp["V"], plan, y_routed=yr, accumulate=True)
+        om.expert_fwd(dims, inp["x"], inp["W"], inp["V"], plan, y_routed=yr, accumulate=True, ws=ews)
         e[4].record(st)
         if dims.d_ff:
             om.shared_mlp(dims, inp["x"], inp["w_gate_up"], inp["w_down"], y_routed=yr, y=y)
         e[5].record(st)
         torch.cuda.synchronize()
         if i == 0:
-            continue  # first pass allocates workspaces
-        stages["route"].append(e[0].elapsed_time(e[1]))
-        stages["schedule"].append(e[1].elapsed_time(e[2]))
-        stages["expert"].append(e[3].elapsed_time(e[4]))
-        stages["shared_mlp"].append(e[4].elapsed_time(e[5]))
-    stage_ms = {k: statistics.mean(v) for k, v in stages.items()}
+            continue
+        for k, (a, b) in zip(stages, [(0, 1), (1, 2), (3, 4), (4, 5)]):
+            stages[k].append(e[a].elapsed_time(e[b]))
+    stage_ms = {k: statistics.median(v) for k, v in stages.items()}
     n_active = int(plan["n_active"].item())
 
     # ---- end to end through the public API with host buffers ----
@@ -261,69 +266,191 @@ def main():
         xd = torch.empty_like(inp["x"])
         for _ in range(2):
             xd.copy_(xh, non_blocking=True)
-            om.layer_fwd(dims, xd, inp["subkeys"], inp["W"], inp["V"], inp.get("w_gate_up"), inp.get("w_down"), y=y, ws=lws)
+            step(xd)
             yh.copy_(y, non_blocking=True)
         torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        tot = 0.0
+        tot = []
         for _ in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             flush.zero_()
             a.record(st)
             xd.copy_(xh, non_blocking=True)
-            om.layer_fwd(dims, xd, inp["subkeys"], inp["W"], inp["V"], inp.get("w_gate_up"), inp.get("w_down"), y=y, ws=lws)
+            step(xd)
             yh.copy_(y, non_blocking=True)
             b.record(st)
             torch.cuda.synchronize()
-            tot += a.elapsed_time(b)
-        e2e_ms = tot / args.steps
+            tot.append(a.elapsed_time(b))
+        e2e_ms = statistics.mean(tot)
         eb = 2 if dims.dtype == 0 else 4
         e2e = {"value": L / (e2e_ms / 1000.0), "unit": "tokens/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": L * dims.d * eb, "d2h_bytes_per_step": L * dims.d * eb}
 
     pk = peaks()
-    a6_bytes = algorithmic_a6(dims, L, n_active, M)
-    a6_gbs = a6_bytes / (stage_ms["expert"] / 1000.0) / 1e9
-    roofline = {"kernel": "expert_warp_kernel (a6)", "bound": "hbm", "achieved": a6_gbs, "peak": pk["hbm"],
-                "unit": "GB/s", "frac": a6_gbs / pk["hbm"], "traffic": None,
-                "algorithmic_bytes_per_launch": a6_bytes, "avg_launch_ms": stage_ms["expert"],
-                "peak_source": pk["src"] + " hbm_gbs (copy)"}
-    # other kernels' rooflines (context)
-    R = dims.n_rows + dims.n_cols
-    router_flops = 2.0 * L * dims.n_heads * R * dims.d
+    a6_bytes = a6_algorithmic_bytes(dims, L, n_active, M)
+    a6_ms = stage_ms["expert_a6"]
+    a6_gbs = a6_bytes / (a6_ms / 1000.0) / 1e9
+    B = om.group_size(dims)
+    kern = "expert_group_tma_kernel" if B > 1 else "expert_warp_kernel"
+    traffic, tsrc = ncu_traffic(w.name, kern)
+    roofline = {"bound": "hbm", "achieved": a6_gbs, "peak": pk["hbm"], "unit": "GB/s", "frac": a6_gbs / pk["hbm"],
+                "traffic": traffic, "kernel": f"{kern} (a6)", "algorithmic_bytes_per_launch": a6_bytes,
+                "avg_launch_ms": a6_ms, "peak_source": pk["src"] + " hbm_gbs (copy)",
+                "traffic_source": tsrc,
+                "note": "a6 moves 2d bytes of W and V per task through L2 (runs of one token in one group of "
+                        f"B={B} experts); at eta = M/|E_active| = {M / max(n_active, 1):.1f} the L2 (lts) "
+                        "throughput, not HBM, binds -- profiles/r1/README.md"}
+    R_ = dims.n_rows + dims.n_cols
+    router_ops = 2.0 * L * dims.n_heads * R_ * dims.d
     mlp_flops = 6.0 * L * dims.d * dims.d_ff
-
     cpu = None
     if not args.no_cpu_baseline:
         nth = os.cpu_count() or 1
-        rate, done, t = cpu_oracle_rate(w, args.cpu_tokens, nth)
+        rate, done, t = cpu_oracle_rate(w, args.cpu_seconds, 1 << 20, nth, inp)
         cpu = {"value": rate, "unit": "tokens/s", "cores": nth, "kind": "oracle",
-               "sample": f"{done} tokens of {w.name} (oracle layer: fp64 canonical logits, product top-K, "
-                         f"token-centric routed branch, shared MLP), {t:.1f} s on {nth} threads"}
-
+               "sample": f"{done} tokens of {w.name} (oracle layer: exact logits, product top-K, token-centric "
+                         f"routed branch, shared MLP): {t:.1f} s of oracle time on {nth} threads"}
     line = {
         "metric": METRIC, "value": L / (ms / 1000.0), "unit": "tokens/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "latency_ms": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic",
-        "config": {"workload": w.name, "d": dims.d, "n_rows": dims.n_rows, "n_cols": dims.n_cols,
-                   "top_k": dims.top_k, "n_heads": dims.n_heads, "d_ff": dims.d_ff, "tokens": L,
-                   "router": "exact (int8 tcgen05 limbs)", "parallelism": "single-gpu",
-                   "l2": "flushed (256 MB write) before every timed step"},
+        "data": "synthetic (seeded counter-based generator, DESIGN.md §3)",
+        "config": dict(_config_dict(w, "single-gpu"), group_size=B),
         "stage_ms": stage_ms, "n_active": n_active, "tasks": M,
         "step_ms_min_max": [min(step_ms), max(step_ms)],
         "roofline": roofline,
         "other_rooflines": {
-            "router_gemm_a1": {"tflop": router_flops / 1e12},
-            "shared_mlp_a7": {"tflop": mlp_flops / 1e12,
-                              "achieved_tflops": mlp_flops / (stage_ms["shared_mlp"] / 1e3) / 1e12 if dims.d_ff else None,
-                              "peak": pk["bf16_sus"]}},
+            "router_a1_i8": {"tops_int8": 9 * router_ops / 1e12,
+                             "note": "9 int8 limb GEMMs of the exact router (DESIGN.md §4.1)"},
+            "shared_mlp_a7": {"tflop": mlp_flops / 1e12, "peak_tflops": pk["bf16_sus"],
+                              "achieved_tflops": mlp_flops / (stage_ms["shared_mlp_a7_a8"] / 1e3) / 1e12
+                              if dims.d_ff else None}},
         "e2e": e2e, "cpu_baseline": cpu,
-        "gpu_launches": launches * args.steps, "launches_per_step": launches,
+        "gpu_launches": launches, "launches_per_step": launches / max(args.steps, 1),
         "clocks": clk.summary(),
-        "context": "paper: 6.7 ms OmniMoE vs 73 ms PEER at 4,096 tokens on A100 (PAPER:368), different shape",
+        "context": "paper: 6.7 ms OmniMoE vs 73 ms PEER per layer at 4,096 tokens, d=1024, N=102,400, K=4096 on "
+                   "A100 (PAPER:368) -- a different shape (config C4)",
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ---------------------------------------------------------------- N > 1
+def bench_multi(args, w, ws, rk, lr):
+    from paper_2602_05711_b200 import distributed as ep, omnimoe as om
+    from synth.workloads import make_inputs
+    dims, L = w.dims, w.L
+    if dims.N % ws:
+        raise SystemExit(f"N={dims.N} not divisible by {ws} ranks")
+    n_per = dims.N // ws
+    inp = make_inputs(dims, L, w.seed, token_begin=rk * L, expert_rows=(rk * n_per, (rk + 1) * n_per))
+    ops = ep.LibOps(dims)
+    ops.set_mlp(inp.get("w_gate_up"), inp.get("w_down"))
+    comm = ep.TorchComm()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+
+    def step(x=None, marks=None):
+        return ep.ep_layer_fwd(ops, comm, inp["x"] if x is None else x, inp["subkeys"], inp["W"], inp["V"], n_per,
+                               marks=marks)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches0 = om.LAUNCHES
+    phase = {}
+    with ClockSampler(lr) as clk:
+        ms_steps = []
+        for i in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            evs = {}
+
+            def mark(name):
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(st)
+                evs[name] = e
+            step(marks=mark)
+            torch.cuda.synchronize()
+            names = list(evs)
+            ms_steps.append(evs[names[0]].elapsed_time(evs[names[-1]]))
+            for a, b in zip(names, names[1:]):
+                phase.setdefault(b, []).append(evs[a].elapsed_time(evs[b]))
+    launches = om.LAUNCHES - launches0
+    t = torch.tensor([statistics.mean(ms_steps)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    phase_ms = {k: statistics.median(v) for k, v in phase.items()}
+    e2e = None
+    if not args.no_e2e:
+        xh = inp["x"].cpu().pin_memory()
+        xd = torch.empty_like(inp["x"])
+        tot = []
+        for _ in range(max(2, args.steps)):
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            xd.copy_(xh, non_blocking=True)
+            yv = step(xd)
+            yh = yv.to("cpu", non_blocking=False)
+            b.record(st)
+            torch.cuda.synchronize()
+            tot.append(a.elapsed_time(b))
+        te = torch.tensor([statistics.mean(tot[1:])], dtype=torch.float64, device="cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        eb = 2 if dims.dtype == 0 else 4
+        e2e = {"value": ws * L / (float(te.item()) / 1000.0), "unit": "tokens/s", "ms_per_step": float(te.item()),
+               "h2d_bytes_per_step": ws * L * dims.d * eb, "d2h_bytes_per_step": ws * L * dims.d * eb}
+        del yh
+    if rk == 0:
+        line = {"metric": METRIC, "value": ws * L / (ms / 1000.0), "unit": "tokens/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "latency_ms": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (seeded counter-based generator, DESIGN.md §3)",
+                "config": dict(_config_dict(w, f"ep{ws} (experts row-sharded, tokens data-parallel, "
+                                               f"NCCL all-to-all)"), global_tokens=ws * L),
+                "phase_ms_rank0": phase_ms, "roofline": None, "e2e": e2e, "cpu_baseline": None,
+                "gpu_launches": launches, "launches_per_step": launches / max(args.steps, 1),
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3a")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle time of the cpu_baseline sample")
+    ap.add_argument("--ref-seconds", type=float, default=60.0, help="total oracle time of --impl reference")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 1)
+    if args.impl == "reference":
+        return run_reference(args)
+    ws, rk, lr = rank_info()
+    torch.cuda.set_device(lr)
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", lr))
+    from paper_2602_05711_b200 import build, configs
+    if rk == 0:
+        build.build()
+    if ws > 1:
+        dist.barrier()
+    w = configs.get(args.config)
+    try:
+        if ws > 1:
+            return bench_multi(args, w, ws, rk, lr)
+        return bench_single(args, w, lr)
+    finally:
+        if ws > 1:
+            dist.destroy_process_group()
 
 
 if __name__ == "__main__":

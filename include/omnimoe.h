@@ -222,6 +222,39 @@ omnimoe_status omnimoe_router_logits(const omnimoe_dims* dims, int64_t L, const 
 omnimoe_status omnimoe_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, const void* B,
                                  float* C, omnimoe_stream_t stream);
 
+/* ---- Expert parallelism over R ranks ----------
+ * Rank r owns flat expert ids [r*n_per, (r+1)*n_per), n_per = N / R (whole grid
+ * rows since n = i*N_c + j), and L of the batch's tokens.  The collectives
+ * themselves (NCCL all-to-all over NVLink) are issued by the caller
+ * (paper_2602_05711_b200/distributed.py); these calls pack, unpack and combine.
+ *
+ * omnimoe_ep_pack: from the routing decision idx/gate [L][h*K] of the local
+ * tokens, write for every destination s (in rank order):
+ *   x_send   [sum_s T_s][d]  each local token with >= 1 task on s, once, tokens
+ *                            ascending ("slot" = row within s's block)
+ *   rec_send int32 [sum_s M_s][3]  per task on s: (id - s*n_per, gate bits, slot)
+ *   inv      int32 [R][L]    slot of token l in s's block, -1 if none
+ *   offsets  int32 [2R+2]    token block starts [0..R] (R+1 entries), then task
+ *                            block starts [0..R]
+ * Sizes are bounded by R*L rows and L*h*K records.  ws: omnimoe_ep_pack_workspace_size. */
+omnimoe_status omnimoe_ep_pack_workspace_size(int64_t L, int32_t R, size_t* bytes);
+omnimoe_status omnimoe_ep_pack(const omnimoe_dims* dims, int64_t L, int32_t R, const void* x,
+                               const int32_t* idx, const float* gate, void* x_send, int32_t* rec_send,
+                               int32_t* inv, int32_t* offsets, void* ws, size_t ws_bytes,
+                               omnimoe_stream_t stream);
+/* Received records (concatenated by source rank; task_off/tok_off int64 [R+1] are
+ * the per-source block starts of the received records / x rows, device memory)
+ * -> task arrays for omnimoe_schedule over the local expert range [0, n_per):
+ * ids (local expert id), gate, token (= row of the received x buffer). */
+omnimoe_status omnimoe_ep_unpack(int64_t M, int32_t R, const int32_t* rec, const int64_t* task_off,
+                                 const int64_t* tok_off, int32_t* ids, float* gate, int32_t* token,
+                                 omnimoe_stream_t stream);
+/* y_routed[l] = sum over s = 0..R-1 (in that order) of y_ret[tok_off[s] + inv[s][l]]
+ * (skipped where inv = -1): the returned partial rows, fp32 [rows][d]. */
+omnimoe_status omnimoe_ep_combine(const omnimoe_dims* dims, int64_t L, int32_t R, const float* y_ret,
+                                  const int32_t* inv, const int64_t* tok_off, float* y_routed,
+                                  omnimoe_stream_t stream);
+
 /* Number of kernel launches the last successful call on this thread enqueued. */
 int omnimoe_last_launch_count(void);
 

@@ -4,6 +4,7 @@
 #include <mutex>
 #include <string>
 
+#include "ep.cuh"
 #include "gemm.cuh"
 #include "router.cuh"
 #include "schedule.cuh"
@@ -474,6 +475,84 @@ omnimoe_status omnimoe_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A,
   ga.K = (int)K;
   ga.out_f32 = C;
   return gemm_bf16(EPI_F32, A, B, ga, (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_ep_pack_workspace_size(int64_t L, int32_t R, size_t* bytes) {
+  OMNI_NONNULL(bytes, "bytes");
+  if (L < 0 || R < 1 || R > kMaxRanks) {
+    set_error("ep: need L >= 0 and 1 <= R <= " + std::to_string(kMaxRanks));
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  *bytes = ep_pack_ws_bytes(L, R);
+  return OMNIMOE_OK;
+}
+
+omnimoe_status omnimoe_ep_pack(const omnimoe_dims* dims, int64_t L, int32_t R, const void* x, const int32_t* idx,
+                               const float* gate, void* x_send, int32_t* rec_send, int32_t* inv, int32_t* offsets,
+                               void* ws, size_t ws_bytes, omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  const omnimoe_dims& d = *dims;
+  const int64_t N = d.n_rows * d.n_cols;
+  if (R < 1 || R > kMaxRanks || N % R != 0) {
+    set_error("ep_pack: R=" + std::to_string(R) + " must divide N=" + std::to_string(N) + " and be <= " +
+              std::to_string(kMaxRanks));
+    return OMNIMOE_ERR_SHAPE;
+  }
+  if (L < 0 || L * d.n_heads * d.top_k >= (int64_t(1) << 31) - 1) {
+    set_error("ep_pack: L*h*K out of range");
+    return OMNIMOE_ERR_SHAPE;
+  }
+  OMNI_NONNULL(offsets, "offsets");
+  OMNI_NONNULL(ws, "ws");
+  if (L > 0) {
+    OMNI_NONNULL(x, "x");
+    OMNI_NONNULL(idx, "idx");
+    OMNI_NONNULL(gate, "gate");
+    OMNI_NONNULL(x_send, "x_send");
+    OMNI_NONNULL(rec_send, "rec_send");
+    OMNI_NONNULL(inv, "inv");
+  }
+  OMNI_TRY(check_ws(ws_bytes, ep_pack_ws_bytes(L, R), "ep_pack"));
+  OMNI_TRY(check_device());
+  return ep_pack(d.dtype, L, (int)d.d, (int)(d.n_heads * d.top_k), R, N / R, x, idx, gate, x_send, rec_send, inv,
+                 offsets, ws, (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_ep_unpack(int64_t M, int32_t R, const int32_t* rec, const int64_t* task_off,
+                                 const int64_t* tok_off, int32_t* ids, float* gate, int32_t* token,
+                                 omnimoe_stream_t stream) {
+  reset_launch_count();
+  if (M < 0 || R < 1 || R > kMaxRanks) {
+    set_error("ep_unpack: need M >= 0 and 1 <= R <= " + std::to_string(kMaxRanks));
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (M == 0) return OMNIMOE_OK;
+  OMNI_NONNULL(rec, "rec");
+  OMNI_NONNULL(task_off, "task_off");
+  OMNI_NONNULL(tok_off, "tok_off");
+  OMNI_NONNULL(ids, "ids");
+  OMNI_NONNULL(gate, "gate");
+  OMNI_NONNULL(token, "token");
+  OMNI_TRY(check_device());
+  return ep_unpack(rec, M, R, task_off, tok_off, ids, gate, token, (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_ep_combine(const omnimoe_dims* dims, int64_t L, int32_t R, const float* y_ret,
+                                  const int32_t* inv, const int64_t* tok_off, float* y_routed,
+                                  omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  if (L < 0 || R < 1 || R > kMaxRanks) {
+    set_error("ep_combine: need L >= 0 and 1 <= R <= " + std::to_string(kMaxRanks));
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (L == 0) return OMNIMOE_OK;
+  OMNI_NONNULL(inv, "inv");
+  OMNI_NONNULL(tok_off, "tok_off");
+  OMNI_NONNULL(y_routed, "y_routed");
+  OMNI_TRY(check_device());
+  return ep_combine(y_ret, inv, tok_off, L, (int)dims->d, R, y_routed, (cudaStream_t)stream);
 }
 
 int omnimoe_last_launch_count(void) { return g_launches; }

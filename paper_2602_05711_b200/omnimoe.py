@@ -47,7 +47,8 @@ class Plan(ctypes.Structure):
 EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnimoe_expert_fwd",
            "omnimoe_shared_mlp", "omnimoe_layer_fwd", "omnimoe_router_logits", "omnimoe_gemm_bf16",
            "omnimoe_last_launch_count", "omnimoe_status_string", "omnimoe_last_error",
-           "omnimoe_group_size", "omnimoe_token_blocks"]
+           "omnimoe_group_size", "omnimoe_token_blocks", "omnimoe_ep_pack_workspace_size",
+           "omnimoe_ep_pack", "omnimoe_ep_unpack", "omnimoe_ep_combine"]
 
 _lib = None
 
@@ -71,6 +72,10 @@ def load(path: str = LIB_PATH):
         "omnimoe_layer_fwd": [PD, I64, V, V, V, V, V, V, V, V, V, V, SZ, V],
         "omnimoe_router_logits": [PD, I64, V, V, V, I32, V, SZ, V],
         "omnimoe_gemm_bf16": [I64, I64, I64, V, V, V, V],
+        "omnimoe_ep_pack_workspace_size": [I64, I32, ctypes.POINTER(ctypes.c_size_t)],
+        "omnimoe_ep_pack": [PD, I64, I32, V, V, V, V, V, V, V, V, SZ, V],
+        "omnimoe_ep_unpack": [I64, I32, V, V, V, V, V, V, V],
+        "omnimoe_ep_combine": [PD, I64, I32, V, V, V, V, V],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -88,11 +93,16 @@ def load(path: str = LIB_PATH):
     return lib
 
 
+LAUNCHES = 0  # kernels enqueued by this process through the library (omnimoe_last_launch_count)
+
+
 def _check(status: int, what: str):
+    global LAUNCHES
+    lib = load()
     if status != 0:
-        lib = load()
         raise OmniMoEError(f"{what}: {lib.omnimoe_status_string(status).decode()}: "
                            f"{lib.omnimoe_last_error().decode()}")
+    LAUNCHES += lib.omnimoe_last_launch_count()
 
 
 def last_launch_count() -> int:
@@ -306,3 +316,55 @@ def gemm_bf16(A, B):
     C = torch.empty((M, N), dtype=torch.float32, device=A.device)
     _check(load().omnimoe_gemm_bf16(M, N, K, _ptr(A), _ptr(B), _ptr(C), _stream()), "gemm_bf16")
     return C
+
+
+# ---------------------------------------------------------------- expert parallelism
+def ep_pack(dims: LayerDims, x, idx, gate, R: int):
+    """Dispatch buffers for R expert shards (include/omnimoe.h omnimoe_ep_pack).
+    Returns (x_send, rec_send, inv, offsets_host) with offsets_host a list of
+    2R+2 ints (token block starts, then record block starts), read after a sync."""
+    L = x.shape[0]
+    hk = dims.n_heads * dims.top_k
+    _req(x, "x", dims.torch_dtype, L * dims.d)
+    _req(idx, "idx", torch.int32, L * hk)
+    _req(gate, "gate", torch.float32, L * hk)
+    x_send = torch.empty((max(R * L, 1), dims.d), dtype=dims.torch_dtype, device=x.device)
+    rec = torch.empty((max(L * hk, 1), 3), dtype=torch.int32, device=x.device)
+    inv = torch.empty((R, max(L, 1)), dtype=torch.int32, device=x.device)
+    off = torch.empty(2 * R + 2, dtype=torch.int32, device=x.device)
+    nb = ctypes.c_size_t(0)
+    _check(load().omnimoe_ep_pack_workspace_size(L, R, ctypes.byref(nb)), "ep_pack_workspace_size")
+    ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=x.device)
+    dc = dims.c()
+    _check(load().omnimoe_ep_pack(ctypes.byref(dc), L, R, _ptr(x), _ptr(idx), _ptr(gate), _ptr(x_send), _ptr(rec),
+                                  _ptr(inv), _ptr(off), _ptr(ws), ws.numel(), _stream()), "ep_pack")
+    offs = off.cpu().tolist()  # the split sizes of the all-to-all (host-visible counts)
+    return x_send[:offs[R]], rec[:offs[2 * R + 1]], inv[:, :L], offs
+
+
+def ep_unpack(rec, R: int, task_off, tok_off):
+    """Received records -> (ids, gate, token) task arrays over the local expert range."""
+    M = rec.shape[0]
+    _req(rec, "rec", torch.int32, M * 3)
+    _req(task_off, "task_off", torch.int64, R + 1)
+    _req(tok_off, "tok_off", torch.int64, R + 1)
+    ids = torch.empty(max(M, 1), dtype=torch.int32, device=rec.device)
+    gate = torch.empty(max(M, 1), dtype=torch.float32, device=rec.device)
+    tok = torch.empty(max(M, 1), dtype=torch.int32, device=rec.device)
+    _check(load().omnimoe_ep_unpack(M, R, _ptr(rec), _ptr(task_off), _ptr(tok_off), _ptr(ids), _ptr(gate),
+                                    _ptr(tok), _stream()), "ep_unpack")
+    return ids[:M], gate[:M], tok[:M]
+
+
+def ep_combine(dims: LayerDims, y_ret, inv, tok_off, L: int):
+    """y_routed[l] = sum_s y_ret[tok_off[s] + inv[s][l]] in rank order (fp32)."""
+    R = inv.shape[0]
+    _req(inv, "inv", torch.int32, R * L)
+    _req(tok_off, "tok_off", torch.int64, R + 1)
+    if y_ret.numel():
+        _req(y_ret, "y_ret", torch.float32)
+    y = torch.empty((L, dims.d), dtype=torch.float32, device=inv.device)
+    dc = dims.c()
+    _check(load().omnimoe_ep_combine(ctypes.byref(dc), L, R, _ptr(y_ret) if y_ret.numel() else None, _ptr(inv),
+                                     _ptr(tok_off), _ptr(y), _stream()), "ep_combine")
+    return y

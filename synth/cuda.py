@@ -19,15 +19,16 @@ def _load():
         if not os.path.exists(_SO):
             raise RuntimeError(f"{_SO} not built (run __graft_entry__.build())")
         _lib = ctypes.CDLL(_SO)
-        _lib.synth_fill.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
-                                    ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+        _lib.synth_fill.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                    ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
         _lib.synth_fill.restype = ctypes.c_int
     return _lib
 
 
-def fill_(t: torch.Tensor, seed: int, tensor_id: int, e: int, mode: int = NORMAL) -> torch.Tensor:
+def fill_(t: torch.Tensor, seed: int, tensor_id: int, e: int, mode: int = NORMAL, base: int = 0) -> torch.Tensor:
+    """Fill t with draws base .. base + numel - 1 of (seed, tensor_id)."""
     assert t.is_cuda and t.is_contiguous() and t.dtype in (torch.bfloat16, torch.float32)
-    rc = _load().synth_fill(seed, tensor_id, t.numel(), e, mode, int(t.dtype == torch.bfloat16),
+    rc = _load().synth_fill(seed, tensor_id, base, t.numel(), e, mode, int(t.dtype == torch.bfloat16),
                             ctypes.c_void_p(t.data_ptr()),
                             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     if rc != 0:
@@ -35,5 +36,5 @@ def fill_(t: torch.Tensor, seed: int, tensor_id: int, e: int, mode: int = NORMAL
     return t
 
 
-def make(shape, dtype, seed, tensor_id, e, mode=NORMAL, device="cuda"):
-    return fill_(torch.empty(shape, dtype=dtype, device=device), seed, tensor_id, e, mode)
+def make(shape, dtype, seed, tensor_id, e, mode=NORMAL, device="cuda", base=0):
+    return fill_(torch.empty(shape, dtype=dtype, device=device), seed, tensor_id, e, mode, base)

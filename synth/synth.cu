@@ -23,11 +23,11 @@ __device__ __forceinline__ int64_t draw(uint64_t seed, uint64_t tid, uint64_t in
   return (int64_t)s - 131070;
 }
 
-__global__ void fill_kernel(uint64_t seed, uint64_t tid, uint64_t n, int e, int mode,
+__global__ void fill_kernel(uint64_t seed, uint64_t tid, uint64_t base, uint64_t n, int e, int mode,
                             int out_bf16, void* out) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    float f = ldexpf((float)draw(seed, tid, i, mode), -e);
+    float f = ldexpf((float)draw(seed, tid, base + i, mode), -e);
     if (out_bf16) {
       uint32_t b = __float_as_uint(f);
       b = (b + 0x7FFFu + ((b >> 16) & 1u)) >> 16;
@@ -40,11 +40,13 @@ __global__ void fill_kernel(uint64_t seed, uint64_t tid, uint64_t n, int e, int 
 
 }  // namespace
 
-extern "C" int synth_fill(uint64_t seed, uint64_t tensor_id, uint64_t n, int e, int mode,
+// Element i of `out` gets draw index base + i: a row shard of a tensor is the
+// same numbers as the corresponding rows of the whole tensor.
+extern "C" int synth_fill(uint64_t seed, uint64_t tensor_id, uint64_t base, uint64_t n, int e, int mode,
                           int out_bf16, void* out, cudaStream_t stream) {
   if (n == 0) return 0;
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 64) blocks = 148 * 64;
-  fill_kernel<<<blocks, 256, 0, stream>>>(seed, tensor_id, n, e, mode, out_bf16, out);
+  fill_kernel<<<blocks, 256, 0, stream>>>(seed, tensor_id, base, n, e, mode, out_bf16, out);
   return (int)cudaGetLastError();
 }

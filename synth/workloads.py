@@ -23,12 +23,22 @@ def tensor_specs(dims, L):
     return specs
 
 
-def make_inputs(dims, L, seed, mode=NORMAL, device="cuda", skip=()):
+def make_inputs(dims, L, seed, mode=NORMAL, device="cuda", skip=(), token_begin=0, expert_rows=None):
+    """Inputs of the layer.  token_begin: the batch is tokens [token_begin,
+    token_begin + L) of the global stream; expert_rows=(begin, end): only these
+    rows of W and V (an expert-parallel shard), identical to the same rows of
+    the full tables."""
     ex = default_exponents(dims.d, dims.d_ff, mode)
     dt = torch.bfloat16 if dims.dtype == 0 else torch.float32
     out = {"exponents": ex, "seed": seed, "mode": mode}
     for name, tid, shape in tensor_specs(dims, L):
         if name in skip:
             continue
-        out[name] = make(shape, dt, seed, tid, ex[tid], mode, device)
+        base = 0
+        if name == "x":
+            base = token_begin * dims.d
+        elif name in ("W", "V") and expert_rows is not None:
+            base = expert_rows[0] * dims.d
+            shape = (expert_rows[1] - expert_rows[0], dims.d)
+        out[name] = make(shape, dt, seed, tid, ex[tid], mode, device, base)
     return out

@@ -1,0 +1,104 @@
+"""Expert-parallel layer on the GPU (-m gpu): the real kernels (pack, unpack,
+schedule, expert, combine, MLP) and the real exchange protocol, with R virtual
+ranks in one process (loopback) and with a one-rank NCCL group; results must
+match the single-GPU layer and the oracle."""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2602_05711_b200 import configs, distributed as ep, omnimoe as om
+from synth.workloads import make_inputs
+from tests.helpers import host_rows, rel_errors
+
+pytestmark = pytest.mark.gpu
+
+MID = dict(d=256, n_rows=64, n_cols=64, top_k=32, n_heads=2, d_ff=256)
+
+
+def _run_loopback(dims, L, seed, R):
+    full = make_inputs(dims, L, seed)
+    ops = ep.LibOps(dims)
+    ops.set_mlp(full["w_gate_up"], full["w_down"])
+    lpr, n_per = L // R, dims.N // R
+    xs = [full["x"][r * lpr:(r + 1) * lpr] for r in range(R)]
+    shards = [make_inputs(dims, 1, seed, skip=("x", "subkeys", "w_gate_up", "w_down"),
+                          expert_rows=(r * n_per, (r + 1) * n_per)) for r in range(R)]
+    ys = ep.ep_layer_fwd_loopback(ops, xs, full["subkeys"], [s["W"] for s in shards], [s["V"] for s in shards],
+                                  n_per)
+    y1 = om.layer_fwd(dims, full["x"], full["subkeys"], full["W"], full["V"], full["w_gate_up"], full["w_down"])
+    torch.cuda.synchronize()
+    return torch.cat(ys), y1, full
+
+
+def test_synth_shard_equals_rows_of_full():
+    dims = om.LayerDims(d=64, n_rows=32, n_cols=32, top_k=8)
+    full = make_inputs(dims, 8, 3, skip=("x", "subkeys"))
+    part = make_inputs(dims, 8, 3, skip=("x", "subkeys"), expert_rows=(256, 512))
+    assert torch.equal(full["W"][256:512], part["W"]) and torch.equal(full["V"][256:512], part["V"])
+    xs = make_inputs(dims, 4, 3, skip=("W", "V", "subkeys"), token_begin=5)
+    xf = make_inputs(dims, 9, 3, skip=("W", "V", "subkeys"))
+    assert torch.equal(xs["x"], xf["x"][5:9])
+
+
+@pytest.mark.parametrize("R", [1, 2, 4, 8])
+def test_ep_loopback_c1(R):
+    w = configs.get("C1")
+    y, y1, _ = _run_loopback(w.dims, w.L, w.seed, R)
+    e_tok, e_elt = rel_errors(y.float().cpu().numpy(), y1.float().cpu().numpy())
+    assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+    hr = lambda n, r=None: host_rows(w.dims, w.seed, n, r)
+    ref = oracle.layer(hr("x", np.arange(w.L)), hr("subkeys").reshape(1, -1, w.dims.d), hr("W"), hr("V"),
+                       w.dims.n_rows, w.dims.n_cols, w.dims.top_k, hr("w_gate_up"), hr("w_down"))
+    e_tok, e_elt = rel_errors(y.float().cpu().numpy(), ref["y"])
+    assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+
+
+@pytest.mark.parametrize("R,B", [(2, 0), (4, 0), (8, 1)])
+def test_ep_loopback_mid(R, B):
+    dims = om.LayerDims(**MID, group_size=B)
+    y, y1, _ = _run_loopback(dims, 512, 5, R)
+    e_tok, e_elt = rel_errors(y.float().cpu().numpy(), y1.float().cpu().numpy())
+    assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_ep_nccl_one_rank():
+    """The torch.distributed driver over a real NCCL group (world size 1: the
+    only size this box has) against the single-GPU layer."""
+    script = r'''
+import os, sys, torch, torch.distributed as dist
+sys.path.insert(0, os.getcwd())
+from paper_2602_05711_b200 import distributed as ep, omnimoe as om
+from synth.workloads import make_inputs
+from tests.helpers import rel_errors
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+dims = om.LayerDims(d=256, n_rows=64, n_cols=64, top_k=32, n_heads=2, d_ff=256)
+full = make_inputs(dims, 384, 7)
+ops = ep.LibOps(dims); ops.set_mlp(full["w_gate_up"], full["w_down"])
+y = ep.ep_layer_fwd(ops, ep.TorchComm(), full["x"], full["subkeys"], full["W"], full["V"], dims.N)
+y1 = om.layer_fwd(dims, full["x"], full["subkeys"], full["W"], full["V"], full["w_gate_up"], full["w_down"])
+torch.cuda.synchronize()
+e = rel_errors(y.float().cpu().numpy(), y1.float().cpu().numpy())
+print("ERR", e[0], e[1])
+dist.destroy_process_group()
+'''
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", script], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = [l for l in out.stdout.splitlines() if l.startswith("ERR")][0]
+    e_tok, e_elt = map(float, line.split()[1:])
+    assert e_tok <= 1e-2 and e_elt <= 1e-2
