@@ -166,10 +166,14 @@ def run_reference(args):
     w = configs.get(args.config)
     nth = os.cpu_count() or 1
     per_step_s = max(2.0, args.ref_seconds / max(args.steps, 1))
-    cpu_oracle_rate(w, 0.5, 32, nth)  # warm-up (page-in, thread pool)
+    tables = None
+    if torch.cuda.is_available():
+        from synth.workloads import make_inputs
+        tables = make_inputs(w.dims, 1, w.seed, skip=("x", "subkeys", "w_gate_up", "w_down"))
+    cpu_oracle_rate(w, 0.5, 32, nth, tables)  # warm-up (page-in, thread pool)
     rates, toks = [], 0
     for _ in range(args.steps):
-        rate, done, _t = cpu_oracle_rate(w, per_step_s, 1 << 20, nth)
+        rate, done, _t = cpu_oracle_rate(w, per_step_s, 1 << 20, nth, tables)
         rates.append(rate)
         toks += done
     rate = statistics.mean(rates)
