@@ -16,13 +16,13 @@
 //      score = key - lse_r - lse_c (Eq.S, Q8).
 // All reductions use fixed trees, compaction follows index order: the output is
 // bitwise deterministic and independent of L and of the batch.
+#include <cstdlib>
+
 #include "router.cuh"
 
 namespace omni {
 namespace {
 
-constexpr int kSelThreads = 256;
-constexpr int kWarps = kSelThreads / 32;
 
 struct U128 {
   uint64_t hi, lo;
@@ -52,26 +52,87 @@ __device__ __forceinline__ void set_byte(U128& k, int pos, uint32_t b) {
 __device__ __forceinline__ bool ge(const U128& x, const U128& y) { return !gt(y, x); }
 __device__ __forceinline__ bool ge(uint64_t x, uint64_t y) { return x >= y; }
 
+// ---------------------------------------------------------------------------
+// Cooperative primitives of a selection group: G = 32 (one warp per token-head,
+// __syncwarp only) or G = 256 (one CTA per token-head).  Each group owns a
+// SelShared and its key buffers in shared memory.
+template <int G>
+struct Grp {
+  static constexpr int kW = G / 32;
+  __device__ static __forceinline__ int tid() { return G == 32 ? (int)(threadIdx.x & 31) : (int)threadIdx.x; }
+  __device__ static __forceinline__ void sync() {
+    if (G == 32) __syncwarp();
+    else __syncthreads();
+  }
+};
+
+template <int G>
 struct SelShared {
   int hist[256];
-  int red_i[kWarps];
-  float red_f[kWarps];
+  int red_i[G / 32];
+  float red_f[G / 32];
   int bcast[4];
+  U128 red_k[G / 32];
+  U128 kmin;
 };
+
+__device__ __forceinline__ U128 shfl_xor_key(const U128& k, int o) {
+  return U128{__shfl_xor_sync(0xffffffffu, k.hi, o), __shfl_xor_sync(0xffffffffu, k.lo, o)};
+}
+__device__ __forceinline__ uint64_t shfl_xor_key(uint64_t k, int o) { return __shfl_xor_sync(0xffffffffu, k, o); }
+__device__ __forceinline__ U128 to128(const U128& k) { return k; }
+__device__ __forceinline__ U128 to128(uint64_t k) { return U128{0ull, k}; }
+__device__ __forceinline__ void from128(const U128& s, U128& k) { k = s; }
+__device__ __forceinline__ void from128(const U128& s, uint64_t& k) { k = s.lo; }
+
+// smallest of a[0..n) (keys unique), moved to a[n-1]; returns it
+template <int G, class KeyT>
+__device__ KeyT extract_min_last(KeyT* a, int n, SelShared<G>& sh) {
+  using g = Grp<G>;
+  KeyT m;
+  from128(U128{~0ull, ~0ull}, m);  // threads without elements offer the largest key
+  for (int i = g::tid(); i < n; i += G)
+    if (gt(m, a[i])) m = a[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const KeyT q = shfl_xor_key(m, o);
+    if (gt(m, q)) m = q;
+  }
+  if (G > 32) {
+    if ((threadIdx.x & 31) == 0) sh.red_k[threadIdx.x >> 5] = to128(m);
+    g::sync();
+    from128(sh.red_k[0], m);
+    for (int i = 1; i < g::kW; ++i) {
+      KeyT q;
+      from128(sh.red_k[i], q);
+      if (gt(m, q)) m = q;
+    }
+  }
+  for (int i = g::tid(); i < n - 1; i += G) {  // exactly one element equals m
+    const KeyT v = a[i];
+    if (!gt(v, m) && !gt(m, v)) {
+      a[i] = a[n - 1];
+      a[n - 1] = v;
+    }
+  }
+  g::sync();
+  return m;
+}
 
 // MSB-first radix select of the `want`-th largest of n unique keys produced by
 // keyf(i).  Returns a threshold thr such that exactly `want` keys satisfy
 // key >= thr.  Requires 1 <= want <= n.
-template <class KeyT, int NBYTES, class KeyF>
-__device__ KeyT radix_select(int n, int want, KeyF keyf, SelShared& sh) {
+template <int G, class KeyT, int NBYTES, class KeyF>
+__device__ KeyT radix_select(int n, int want, KeyF keyf, SelShared<G>& sh) {
+  using g = Grp<G>;
   KeyT pre{};
   int remaining = want;
   const int lane = threadIdx.x & 31;
   for (int pos = NBYTES - 1; pos >= 0; --pos) {
-    for (int i = threadIdx.x; i < 256; i += kSelThreads) sh.hist[i] = 0;
-    __syncthreads();
-    const int nloop = (n + kSelThreads - 1) / kSelThreads * kSelThreads;
-    for (int i = threadIdx.x; i < nloop; i += kSelThreads) {
+    for (int i = g::tid(); i < 256; i += G) sh.hist[i] = 0;
+    g::sync();
+    const int nloop = (n + G - 1) / G * G;
+    for (int i = g::tid(); i < nloop; i += G) {
       uint32_t dig = 256;
       if (i < n) {
         const KeyT k = keyf(i);
@@ -80,8 +141,8 @@ __device__ KeyT radix_select(int n, int want, KeyF keyf, SelShared& sh) {
       const unsigned peers = __match_any_sync(0xffffffffu, dig);
       if (dig < 256 && lane == __ffs(peers) - 1) atomicAdd(&sh.hist[dig], __popc(peers));
     }
-    __syncthreads();
-    if (threadIdx.x < 32) {
+    g::sync();
+    if (g::tid() < 32) {
       // suffix sums over bins 255..0; lane j owns bins [255-8j-7, 255-8j]
       int c[8], s = 0;
 #pragma unroll
@@ -95,7 +156,7 @@ __device__ KeyT radix_select(int n, int want, KeyF keyf, SelShared& sh) {
         const int y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
       }
-      int above = incl - s;  // keys in bins higher than this lane's bins
+      int above = incl - s;
       int found = -1, fabove = 0, fcnt = 0;
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
@@ -117,49 +178,52 @@ __device__ KeyT radix_select(int n, int want, KeyF keyf, SelShared& sh) {
         sh.bcast[2] = fcnt;
       }
     }
-    __syncthreads();
+    g::sync();
     const int b = sh.bcast[0];
     remaining -= sh.bcast[1];
     set_byte(pre, pos, (uint32_t)b);
     const bool done = sh.bcast[2] == remaining;  // the whole bucket is selected
-    __syncthreads();
+    g::sync();
     if (done) break;  // lower bytes of pre stay 0: key >= pre selects the bucket
   }
   return pre;
 }
 
-// deterministic compaction of the keys >= thr (index order) into out[0..)
-template <class KeyT, class KeyF>
-__device__ void compact_ge(int n, KeyT thr, KeyF keyf, KeyT* out, SelShared& sh) {
-  const int per = (n + kSelThreads - 1) / kSelThreads;
-  const int b0 = threadIdx.x * per, b1 = min(n, b0 + per);
+// deterministic compaction of the keys >= thr (STRICT: > thr) in index order into out[0..)
+template <int G, bool STRICT, class KeyT, class KeyF>
+__device__ void compact_ge(int n, KeyT thr, KeyF keyf, KeyT* out, SelShared<G>& sh) {
+  using g = Grp<G>;
+  const int per = (n + G - 1) / G;
+  const int b0 = g::tid() * per, b1 = min(n, b0 + per);
+  auto take = [&](const KeyT& k) { return STRICT ? gt(k, thr) : ge(k, thr); };
   int cnt = 0;
-  for (int i = b0; i < b1; ++i) cnt += ge(keyf(i), thr);
-  // block exclusive scan of cnt
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = b0; i < b1; ++i) cnt += take(keyf(i));
+  const int lane = threadIdx.x & 31;
   int x = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
-  if (lane == 31) sh.red_i[w] = x;
-  __syncthreads();
-  int off = 0;
-  for (int i = 0; i < w; ++i) off += sh.red_i[i];
-  off += x - cnt;
+  int off = x - cnt;
+  if (G > 32) {
+    const int w = threadIdx.x >> 5;
+    if (lane == 31) sh.red_i[w] = x;
+    g::sync();
+    for (int i = 0; i < w; ++i) off += sh.red_i[i];
+  }
   for (int i = b0; i < b1; ++i) {
     const KeyT k = keyf(i);
-    if (ge(k, thr)) out[off++] = k;
+    if (take(k)) out[off++] = k;
   }
-  __syncthreads();
+  g::sync();
 }
 
-template <class K>
+template <int G, class K>
 __device__ void bitonic_desc(K* a, int n) {  // n a power of two; padding must hold minimal keys
   for (int size = 2; size <= n; size <<= 1)
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < (n >> 1); i += kSelThreads) {
+      for (int i = Grp<G>::tid(); i < (n >> 1); i += G) {
         const int lo = 2 * i - (i & (stride - 1));
         const int hi = lo + stride;
         const bool desc = (lo & size) == 0;
@@ -169,18 +233,50 @@ __device__ void bitonic_desc(K* a, int n) {  // n a power of two; padding must h
           a[hi] = p;
         }
       }
-      __syncthreads();
+      Grp<G>::sync();
     }
 }
 
-__device__ float block_sum(float v, SelShared& sh) {
+// pow2 size used to sort the top `keep` of n unique keys: with a radix-selected
+// threshold the keep-th key is extracted and placed last, the keep-1 larger are sorted
+__host__ __device__ inline int sort_len(int keep, int n) {
+  int want = keep < n ? keep - 1 : keep, q = 1;
+  while (q < want) q <<= 1;
+  return q;
+}
+
+// top `keep` of n keys produced by keyf, sorted descending into out[0..keep)
+// (out holds max(sort_len, keep) entries; entries beyond keep are scratch)
+template <int G, class KeyT, int NBYTES, class KeyF>
+__device__ void top_sorted(int n, int keep, KeyF keyf, KeyT* out, SelShared<G>& sh) {
+  const int len = sort_len(keep, n);
+  if (keep < n) {
+    const KeyT thr = radix_select<G, KeyT, NBYTES>(n, keep, keyf, sh);
+    compact_ge<G, false>(n, thr, keyf, out, sh);             // exactly the top `keep` keys
+    const KeyT last = extract_min_last<G>(out, keep, sh);    // the keep-th key, not sorted
+    for (int i = keep - 1 + Grp<G>::tid(); i < len; i += G) out[i] = KeyT{};
+    Grp<G>::sync();
+    bitonic_desc<G>(out, len);
+    if (Grp<G>::tid() == 0) out[keep - 1] = last;
+  } else {
+    compact_ge<G, false>(n, KeyT{}, keyf, out, sh);          // all keys (every key is > 0)
+    for (int i = keep + Grp<G>::tid(); i < len; i += G) out[i] = KeyT{};
+    Grp<G>::sync();
+    bitonic_desc<G>(out, len);
+  }
+  Grp<G>::sync();
+}
+
+template <int G>
+__device__ float group_sum(float v, SelShared<G>& sh) {
   v = warp_sum(v);
+  if (G == 32) return v;
   const int w = threadIdx.x >> 5;
   __syncthreads();
   if ((threadIdx.x & 31) == 0) sh.red_f[w] = v;
   __syncthreads();
   float r = 0.f;
-  for (int i = 0; i < kWarps; ++i) r += sh.red_f[i];
+  for (int i = 0; i < G / 32; ++i) r += sh.red_f[i];
   __syncthreads();
   return r;
 }
@@ -209,77 +305,174 @@ __device__ __forceinline__ double key_value(const U128& k) {  // hi + lo as a do
   return ord64_inv(k.hi) + (double)ord32_inv((uint32_t)(k.lo >> 32));
 }
 
-// sorts the top k1 keys of one half into out[0..k1) (padded to pk1 with zeros)
-__device__ void half_topk(const float* lg, int n, int k1, int pk1, uint64_t* raw, uint64_t* out,
-                          SelShared& sh, float* lse) {
-  for (int i = threadIdx.x; i < n; i += kSelThreads) raw[i] = half_key(lg[i], (uint32_t)i);
-  __syncthreads();
-  auto keyf = [raw](int i) { return raw[i]; };
-  uint64_t thr = 0;
-  if (k1 < n) thr = radix_select<uint64_t, 8>(n, k1, keyf, sh);
-  compact_ge(n, thr, keyf, out, sh);
-  for (int i = k1 + threadIdx.x; i < pk1; i += kSelThreads) out[i] = 0ull;
-  __syncthreads();
-  bitonic_desc(out, pk1);
+// the top k1 keys of one half, sorted, into out[0..k1); *lse = logsumexp of the half
+template <int G>
+__device__ void half_topk(const float* __restrict__ lg, int n, int k1, uint64_t* out, SelShared<G>& sh,
+                          float* lse) {
+  auto keyf = [lg](int i) { return half_key(lg[i], (uint32_t)i); };
+  top_sorted<G, uint64_t, 8>(n, k1, keyf, out, sh);
   const float mx = half_val(out[0]);
   float s = 0.f;
-  for (int i = threadIdx.x; i < n; i += kSelThreads) s += __expf(lg[i] - mx);
-  s = block_sum(s, sh);
+  for (int i = Grp<G>::tid(); i < n; i += G) s += __expf(lg[i] - mx);
+  s = group_sum<G>(s, sh);
   *lse = mx + __logf(s);
 }
 
-__global__ void __launch_bounds__(kSelThreads)
+// ---------------------------------------------------------------------------
+// Small K (K + 1 <= 32): one WARP per token-head, no block barriers.  The t-th
+// largest key of a list is found by t rounds of "largest key below the previous
+// one" (each lane scans its strided share, then a shuffle max); lane t keeps it.
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ U128 warp_max_u128(U128 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const U128 q = shfl_xor_key(v, o);
+    if (gt(q, v)) v = q;
+  }
+  return v;
+}
+
+// lane t (< k1) returns the t-th largest half key of lg[0..n); *lse = logsumexp
+__device__ uint64_t warp_half_topk(const float* __restrict__ lg, int n, int k1, float* lse) {
+  const int lane = threadIdx.x & 31;
+  uint64_t mine = 0, prev = ~0ull;
+  for (int t = 0; t < k1; ++t) {
+    uint64_t best = 0;
+    for (int i = lane; i < n; i += 32) {
+      const uint64_t k = half_key(lg[i], (uint32_t)i);
+      if (k < prev && k > best) best = k;
+    }
+    best = warp_max_u64(best);
+    if (lane == t) mine = best;
+    prev = best;
+  }
+  const float mx = half_val(__shfl_sync(0xffffffffu, mine, 0));
+  float s = 0.f;
+  for (int i = lane; i < n; i += 32) s += __expf(lg[i] - mx);
+  s = warp_sum(s);
+  *lse = mx + __logf(s);
+  return mine;
+}
+
+__global__ void __launch_bounds__(256)
+    select_warp_kernel(SelectParams p, const float* __restrict__ logits, int32_t* __restrict__ idx,
+                       float* __restrict__ gate, float* __restrict__ score) {
+  __shared__ uint32_t cand[1024];
+  const int K1 = p.top_k + 1;
+  if (threadIdx.x == 0) {
+    int off = 0;
+    for (int a = 0; a < p.kr1; ++a) {
+      const int nb = min(p.kc1, K1 / (a + 1));
+      for (int b = 0; b < nb; ++b) cand[off++] = ((uint32_t)a << 16) | (uint32_t)b;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * (int64_t)blockDim.x) >> 5);
+  const int R = p.n_rows + p.n_cols;
+  const int C = p.C, keep = min(K1, C);
+  const uint32_t Nc = (uint32_t)p.n_cols;
+  for (int th = gw; th < p.T; th += nw) {
+    const float* lg = logits + (size_t)th * R;
+    float lse_r, lse_c;
+    const uint64_t kr = warp_half_topk(lg, p.n_rows, p.kr1, &lse_r);
+    const uint64_t kc = warp_half_topk(lg + p.n_rows, p.n_cols, p.kc1, &lse_c);
+    // candidate keys, at most ceil(C / 32) per lane (C <= 32 * (ln 32 + 1) < 160)
+    U128 ck[5];
+    const int per = (C + 31) / 32;
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+      const int c = lane + 32 * m;
+      const uint32_t ab = (m < per && c < C) ? cand[c] : 0u;
+      const uint64_t ka = __shfl_sync(0xffffffffu, kr, (int)(ab >> 16));
+      const uint64_t kb = __shfl_sync(0xffffffffu, kc, (int)(ab & 0xFFFF));
+      ck[m] = (m < per && c < C) ? cell_key(half_val(ka), half_val(kb), half_idx(ka) * Nc + half_idx(kb))
+                                 : U128{0ull, 0ull};
+    }
+    // the top `keep` candidates; lane t keeps the t-th
+    U128 mine{0ull, 0ull}, prev{~0ull, ~0ull};
+    for (int t = 0; t < keep; ++t) {
+      U128 best{0ull, 0ull};
+#pragma unroll
+      for (int m = 0; m < 5; ++m)
+        if (gt(prev, ck[m]) && gt(ck[m], best)) best = ck[m];
+      best = warp_max_u128(best);
+      if (lane == t) mine = best;
+      prev = best;
+    }
+    // gates: softmax over the first K keys (Eq.Gate)
+    const double k1v = key_value(U128{__shfl_sync(0xffffffffu, mine.hi, 0), __shfl_sync(0xffffffffu, mine.lo, 0)});
+    const double kv = key_value(mine);
+    const float ev = lane < p.top_k ? expf((float)(kv - k1v)) : 0.f;
+    const float es = warp_sum(ev);
+    if (lane < p.top_k) {
+      const size_t o = (size_t)th * p.top_k + lane;
+      idx[o] = (int32_t)(0xFFFFFFFFu - (uint32_t)mine.lo);
+      gate[o] = ev / es;
+      if (score) score[o] = (float)(kv - (double)lse_r - (double)lse_c);
+    }
+  }
+}
+
+// per-group shared memory: SelShared | kr (pkr u64) | kc (pkc u64) | sel (pkeep U128)
+template <int G>
+__host__ __device__ inline size_t group_bytes(const SelectParams& p) {
+  size_t b = (sizeof(SelShared<G>) + 15) / 16 * 16;
+  b += (size_t)(p.pkr + p.pkc) * 8;
+  b = (b + 15) / 16 * 16;
+  return b + (size_t)p.pkeep * 16;
+}
+
+template <int G>
+__global__ void __launch_bounds__(256)
     select_kernel(SelectParams p, const float* __restrict__ logits, int32_t* __restrict__ idx,
                   float* __restrict__ gate, float* __restrict__ score) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ SelShared sh;
-  // layout: sel (U128[pkeep]) | raw (u64[max(nr, nc)]) | kr (u64[pkr]) | kc (u64[pkc]) | cand (u32[C])
-  U128* sel = reinterpret_cast<U128*>(smem);
-  uint64_t* raw = reinterpret_cast<uint64_t*>(sel + p.pkeep);
-  uint64_t* kr = raw + max(p.n_rows, p.n_cols);
-  uint64_t* kc = kr + p.pkr;
-  uint32_t* cand = reinterpret_cast<uint32_t*>(kc + p.pkc);
-
-  const int R = p.n_rows + p.n_cols;
+  // CTA-wide candidate table (a, b) with a*b <= K+1 (0-based ranks), the same for every token-head
+  uint32_t* cand = reinterpret_cast<uint32_t*>(smem);
+  const size_t cand_bytes = ((size_t)p.C * 4 + 15) / 16 * 16;
   const int K1 = p.top_k + 1;
-  // candidate (a, b) pairs, the same for every token-head: row ranks a admit
-  // b < min(kc1, K1 / (a + 1)) (0-based ranks); packed a << 16 | b
-  if (threadIdx.x == 0) sh.bcast[3] = 0;
-  __syncthreads();
-  for (int a = threadIdx.x; a < p.kr1; a += kSelThreads) {
+  for (int a = threadIdx.x; a < p.kr1; a += blockDim.x) {
     int off = 0;
     for (int t = 0; t < a; ++t) off += min(p.kc1, K1 / (t + 1));
     const int nb = min(p.kc1, K1 / (a + 1));
     for (int b = 0; b < nb; ++b) cand[off + b] = ((uint32_t)a << 16) | (uint32_t)b;
   }
   __syncthreads();
+  const int gid = threadIdx.x / G, ngroups = blockDim.x / G;
+  uint8_t* base = smem + cand_bytes + (size_t)gid * group_bytes<G>(p);
+  SelShared<G>& sh = *reinterpret_cast<SelShared<G>*>(base);
+  uint64_t* kr = reinterpret_cast<uint64_t*>(base + (sizeof(SelShared<G>) + 15) / 16 * 16);
+  uint64_t* kc = kr + p.pkr;
+  U128* sel = reinterpret_cast<U128*>(base + ((sizeof(SelShared<G>) + 15) / 16 * 16 +
+                                              (size_t)(p.pkr + p.pkc) * 8 + 15) / 16 * 16);
+  const int R = p.n_rows + p.n_cols;
   const int C = p.C;
   const int keep = min(K1, C);
-
-  for (int th = blockIdx.x; th < p.T; th += gridDim.x) {
+  const uint32_t Nc = (uint32_t)p.n_cols;
+  for (int th = blockIdx.x * ngroups + gid; th < p.T; th += gridDim.x * ngroups) {
     const float* lg = logits + (size_t)th * R;
     float lse_r, lse_c;
-    half_topk(lg, p.n_rows, p.kr1, p.pkr, raw, kr, sh, &lse_r);
-    half_topk(lg + p.n_rows, p.n_cols, p.kc1, p.pkc, raw, kc, sh, &lse_c);
-    const uint32_t Nc = (uint32_t)p.n_cols;
+    half_topk<G>(lg, p.n_rows, p.kr1, kr, sh, &lse_r);
+    half_topk<G>(lg + p.n_rows, p.n_cols, p.kc1, kc, sh, &lse_c);
     auto ckey = [kr, kc, cand, Nc](int c) {
       const uint32_t ab = cand[c];
       const uint64_t ka = kr[ab >> 16], kb = kc[ab & 0xFFFF];
       return cell_key(half_val(ka), half_val(kb), half_idx(ka) * Nc + half_idx(kb));
     };
-    U128 thr{0ull, 0ull};
-    if (keep < C) thr = radix_select<U128, 16>(C, keep, ckey, sh);
-    compact_ge(C, thr, ckey, sel, sh);
-    for (int i = keep + threadIdx.x; i < p.pkeep; i += kSelThreads) sel[i] = U128{0ull, 0ull};
-    __syncthreads();
-    bitonic_desc(sel, p.pkeep);
+    top_sorted<G, U128, 16>(C, keep, ckey, sel, sh);
     // ---- gates: softmax over the K selected exact keys (Eq.Gate) ----
     const double k1v = key_value(sel[0]);
     float es = 0.f;
-    for (int k = threadIdx.x; k < p.top_k; k += kSelThreads) es += expf((float)(key_value(sel[k]) - k1v));
-    es = block_sum(es, sh);
+    for (int k = Grp<G>::tid(); k < p.top_k; k += G) es += expf((float)(key_value(sel[k]) - k1v));
+    es = group_sum<G>(es, sh);
     const float inv = 1.0f / es;
-    for (int k = threadIdx.x; k < p.top_k; k += kSelThreads) {
+    for (int k = Grp<G>::tid(); k < p.top_k; k += G) {
       const U128 q = sel[k];
       const double kv = key_value(q);
       const size_t o = (size_t)th * p.top_k + k;
@@ -287,14 +480,8 @@ __global__ void __launch_bounds__(kSelThreads)
       gate[o] = expf((float)(kv - k1v)) * inv;
       if (score) score[o] = (float)(kv - (double)lse_r - (double)lse_c);
     }
-    __syncthreads();
+    Grp<G>::sync();
   }
-}
-
-int pow2ceil(int v) {
-  int q = 1;
-  while (q < v) q <<= 1;
-  return q;
 }
 
 }  // namespace
@@ -311,15 +498,24 @@ omnimoe_status select_params(const omnimoe_dims& d, int64_t T, SelectParams* p, 
   int64_t C = 0;
   for (int64_t a = 1; a <= p->kr1; ++a) C += std::min<int64_t>(p->kc1, K1 / a);
   p->C = (int)C;
-  p->pkr = pow2ceil(p->kr1);
-  p->pkc = pow2ceil(p->kc1);
-  p->pkeep = pow2ceil((int)std::min<int64_t>(K1, C));
+  // buffers hold max(sorted length, list length) keys (sort_len: the last key is the
+  // radix-selected threshold and is not sorted)
+  p->pkr = std::max(sort_len(p->kr1, p->n_rows), p->kr1);
+  p->pkc = std::max(sort_len(p->kc1, p->n_cols), p->kc1);
+  const int keep = (int)std::min<int64_t>(K1, C);
+  p->pkeep = std::max(sort_len(keep, (int)C), keep);
   if (d.n_rows > 65535 || d.n_cols > 65535) {
     set_error("route: grid halves must be <= 65535");
     return OMNIMOE_ERR_UNSUPPORTED;
   }
-  *smem = (size_t)p->pkeep * 16 + (size_t)std::max(p->n_rows, p->n_cols) * 8 +
-          (size_t)(p->pkr + p->pkc) * 8 + (size_t)C * 4 + 16;
+  const size_t cand_bytes = ((size_t)C * 4 + 15) / 16 * 16;
+  // one CTA per token-head: measured faster than one warp per token-head at K = 512
+  // (the per-warp key buffers limit a warp-per-token-head kernel to 8 warps/SM);
+  // small K uses select_warp_kernel instead (launch_select)
+  p->group = getenv("OMNIMOE_SELECT_WARP_GROUP") && p->pkeep <= 1024 ? 32 : 256;
+  const size_t gb = p->group == 32 ? group_bytes<32>(*p) : group_bytes<256>(*p);
+  p->groups_per_cta = p->group == 32 ? (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024 - cand_bytes) / gb)) : 1;
+  *smem = cand_bytes + gb * p->groups_per_cta;
   if (*smem > 225 * 1024) {
     set_error("route: selection working set (" + std::to_string(*smem) +
               " bytes: K+1 sorted keys, both halves, " + std::to_string(C) +
@@ -331,20 +527,23 @@ omnimoe_status select_params(const omnimoe_dims& d, int64_t T, SelectParams* p, 
 
 omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* logits, int32_t* idx,
                              float* gate, float* score, cudaStream_t st) {
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    if (cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess) {
-      set_error("route: cannot set select_kernel shared memory");
-      return OMNIMOE_ERR_CUDA;
-    }
-    attr = smem;
+  if (p.top_k + 1 <= 32 && p.C <= 160) {  // small K: warp per token-head, repeated arg-max
+    const int grid = std::max(1, std::min((p.T + 7) / 8, kSMs * 8));
+    select_warp_kernel<<<grid, 256, 0, st>>>(p, logits, idx, gate, score);
+    OMNI_CHECK_LAUNCH("select_warp_kernel");
+    return OMNIMOE_OK;
+  }
+  auto kern = p.group == 32 ? select_kernel<32> : select_kernel<256>;
+  const int threads = p.group == 32 ? 32 * p.groups_per_cta : 256;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    set_error("route: cannot set select_kernel shared memory");
+    return OMNIMOE_ERR_CUDA;
   }
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel, kSelThreads, smem);
-  const int grid = std::min(p.T, kSMs * std::max(per_sm, 1));
-  if (grid <= 0) return OMNIMOE_OK;
-  select_kernel<<<grid, kSelThreads, smem, st>>>(p, logits, idx, gate, score);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  const int per_cta = threads / p.group;
+  const int grid = std::max(1, std::min((p.T + per_cta - 1) / per_cta, kSMs * std::max(per_sm, 1)));
+  kern<<<grid, threads, smem, st>>>(p, logits, idx, gate, score);
   OMNI_CHECK_LAUNCH("select_kernel");
   return OMNIMOE_OK;
 }

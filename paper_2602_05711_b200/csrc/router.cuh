@@ -12,7 +12,9 @@ struct SelectParams {
   int top_k;           // K
   int kr1, kc1;        // min(K+1, N_r), min(K+1, N_c): per-half list lengths
   int C;               // product candidates (a*b <= K+1)
-  int pkr, pkc, pkeep; // power-of-two sort sizes: row list, column list, K+1 selected
+  int pkr, pkc, pkeep; // key buffer lengths: row list, column list, K+1 selected
+  int group;           // threads cooperating on one token-head: 32 (warp) or 256 (CTA)
+  int groups_per_cta;
 };
 
 omnimoe_status select_params(const omnimoe_dims& d, int64_t T, SelectParams* p, size_t* smem);
