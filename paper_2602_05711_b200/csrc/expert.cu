@@ -266,6 +266,23 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void red_add_v4_hint(float* p, float a, float b, float c, float d, uint64_t pol) {
+  asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(a), "f"(b), "f"(c),
+               "f"(d), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_vec_hint(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
 
 template <int NV, int S>
 __global__ void __launch_bounds__(256, 1)
@@ -274,9 +291,13 @@ __global__ void __launch_bounds__(256, 1)
                             const int32_t* __restrict__ n_runs_p, const int32_t* __restrict__ m_loc_p,
                             const int32_t* __restrict__ stok, const int32_t* __restrict__ sexp,
                             const float* __restrict__ sgate, float* __restrict__ y, int act,
-                            int* __restrict__ work, int wv_evict_first) {
+                            int* __restrict__ work, int hints) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const uint64_t pol = policy_evict_first();
+  // L2 eviction priorities (hints bit 0: W/V evict_first, 1: y_routed evict_last,
+  // 2: x evict_last, 3: W/V evict_last)
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  const bool wv_hint = hints & 9, y_hint = hints & 2, x_hint = hints & 4;
+  const uint64_t pol = (hints & 1) ? pol_first : pol_last;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t row_bytes = (uint32_t)d * 2;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                    // [nwarps][S]
@@ -358,7 +379,7 @@ __global__ void __launch_bounds__(256, 1)
         meta[s] = m;
         uint8_t* st = ring + (size_t)s * 2 * row_bytes;
         tc::mbar_expect_tx(&bar[s], 2u * row_bytes);
-        if (wv_evict_first) {  // W/V stream through L2 without evicting x / y_routed
+        if (wv_hint) {
           bulk_g2s_hint(st, W + (size_t)e * d, row_bytes, &bar[s], pol);
           bulk_g2s_hint(st + row_bytes, V + (size_t)e * d, row_bytes, &bar[s], pol);
         } else {
@@ -380,7 +401,9 @@ __global__ void __launch_bounds__(256, 1)
     if (m.flags & 1) {  // first task of a run: x_l into registers (prefetched if possible)
       if (xnext_tok != m.tok) {
 #pragma unroll
-        for (int j = 0; j < NV; ++j) xnext[j] = ld_vec(x + (size_t)m.tok * d + (j * 32 + lane) * 8);
+        for (int j = 0; j < NV; ++j)
+          xnext[j] = x_hint ? ld_vec_hint(x + (size_t)m.tok * d + (j * 32 + lane) * 8, pol_last)
+                            : ld_vec(x + (size_t)m.tok * d + (j * 32 + lane) * 8);
       }
 #pragma unroll
       for (int j = 0; j < NV; ++j) xv[j] = xnext[j];
@@ -393,7 +416,9 @@ __global__ void __launch_bounds__(256, 1)
         if (mq.flags & 1) {
           xnext_tok = mq.tok;
 #pragma unroll
-          for (int j = 0; j < NV; ++j) xnext[j] = ld_vec(x + (size_t)xnext_tok * d + (j * 32 + lane) * 8);
+          for (int j = 0; j < NV; ++j)
+            xnext[j] = x_hint ? ld_vec_hint(x + (size_t)xnext_tok * d + (j * 32 + lane) * 8, pol_last)
+                              : ld_vec(x + (size_t)xnext_tok * d + (j * 32 + lane) * 8);
           break;
         }
       }
@@ -429,8 +454,13 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
         const int c = (j * 32 + lane) * 8;
-        red_add_v4(yl + c, lo_f(acc[j][0]), hi_f(acc[j][0]), lo_f(acc[j][1]), hi_f(acc[j][1]));
-        red_add_v4(yl + c + 4, lo_f(acc[j][2]), hi_f(acc[j][2]), lo_f(acc[j][3]), hi_f(acc[j][3]));
+        if (y_hint) {
+          red_add_v4_hint(yl + c, lo_f(acc[j][0]), hi_f(acc[j][0]), lo_f(acc[j][1]), hi_f(acc[j][1]), pol_last);
+          red_add_v4_hint(yl + c + 4, lo_f(acc[j][2]), hi_f(acc[j][2]), lo_f(acc[j][3]), hi_f(acc[j][3]), pol_last);
+        } else {
+          red_add_v4(yl + c, lo_f(acc[j][0]), hi_f(acc[j][0]), lo_f(acc[j][1]), hi_f(acc[j][1]));
+          red_add_v4(yl + c + 4, lo_f(acc[j][2]), hi_f(acc[j][2]), lo_f(acc[j][3]), hi_f(acc[j][3]));
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[j][i] = 0ull;
       }
@@ -454,7 +484,7 @@ omnimoe_status launch_group_tma(int d, const void* x, const void* W, const void*
   kern<<<kSMs, warps * 32, smem, st>>>(d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W),
                                        static_cast<const __nv_bfloat16*>(V), plan.run_offsets, plan.n_runs, m_loc,
                                        plan.sorted_token, plan.sorted_expert, plan.sorted_gate, y, act, work,
-                                       getenv("OMNIMOE_WV_EVICT_FIRST") ? atoi(getenv("OMNIMOE_WV_EVICT_FIRST")) : 0);
+                                       getenv("OMNIMOE_L2_HINTS") ? atoi(getenv("OMNIMOE_L2_HINTS")) : 0);
   OMNI_CHECK_LAUNCH("expert_group_tma_kernel");
   return OMNIMOE_OK;
 }

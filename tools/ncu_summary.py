@@ -17,8 +17,9 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
         "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct"]
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1e-9, "usecond": 1e-6,
-         "msecond": 1e-3, "second": 1}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+         # durations are stored in milliseconds
+         "nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3, "s": 1e3}
 
 
 def short(name):
@@ -42,6 +43,8 @@ def from_report(path):
                     continue
                 rec[m] = v * SCALE.get(units[i], 1)
         rec["dram_bytes"] = rec.get("dram__bytes_read.sum", 0) + rec.get("dram__bytes_write.sum", 0)
+        if "gpu__time_duration.sum" in rec:
+            rec["duration_ms"] = rec.pop("gpu__time_duration.sum")
         rec["source"] = os.path.relpath(path, ROOT)
         out[k] = rec
     return out
