@@ -230,6 +230,14 @@ def bench_single(args, w, lr):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = statistics.mean(step_ms)
 
+    if dims.expert_kernel == om.EXPERT_TOKEN:  # ablation run: the layer time is the result
+        print(json.dumps({"metric": METRIC, "value": L / (ms / 1000.0), "unit": "tokens/s", "n_gpus": 1,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                          "data": "synthetic", "config": dict(_config_dict(w, "single-gpu"),
+                                                              expert_kernel="token (ablation: w/o ECS)"),
+                          "gpu_launches": launches, "clocks": clk.summary()}), flush=True)
+        return 0
     # ---- per-stage breakdown through the individual C-ABI calls (same inputs) ----
     M = L * dims.n_heads * dims.top_k
     rws = om.workspace(dims, L, om.WS_ROUTE)
@@ -318,7 +326,7 @@ def bench_single(args, w, lr):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "latency_ms": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded counter-based generator, DESIGN.md §3)",
-        "config": dict(_config_dict(w, "single-gpu"), group_size=B),
+        "config": dict(_config_dict(w, "single-gpu"), group_size=B, expert_kernel=args.expert_kernel),
         "stage_ms": stage_ms, "n_active": n_active, "tasks": M,
         "step_ms_min_max": [min(step_ms), max(step_ms)],
         "roofline": roofline,
@@ -434,6 +442,9 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=60.0, help="total oracle time of --impl reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--expert-kernel", default="auto", choices=["auto", "token", "warp"],
+                    help="a6 executor: auto (grouped ECS), token (the paper's 'w/o ECS' ablation), "
+                         "warp (expert-major, B = 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
     if args.impl == "reference":
@@ -448,6 +459,10 @@ def main():
     if ws > 1:
         dist.barrier()
     w = configs.get(args.config)
+    if args.expert_kernel != "auto":
+        from paper_2602_05711_b200 import omnimoe as om
+        ek = {"token": om.EXPERT_TOKEN, "warp": om.EXPERT_WARP}[args.expert_kernel]
+        w = configs.get(args.config, expert_kernel=ek, group_size=1 if ek == om.EXPERT_WARP else 0)
     try:
         if ws > 1:
             return bench_multi(args, w, ws, rk, lr)

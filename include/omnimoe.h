@@ -49,8 +49,10 @@ enum { OMNIMOE_BF16 = 0, OMNIMOE_F32 = 1 };
 enum { OMNIMOE_SILU = 0, OMNIMOE_IDENTITY = 1 };
 /* Which routed-branch kernel omnimoe_expert_fwd runs: AUTO
  * follows the plan's group size; WARP (expert-major) requires B = 1; GROUP
- * (run-major) requires B > 1. */
-enum { OMNIMOE_EXPERT_AUTO = 0, OMNIMOE_EXPERT_WARP = 1, OMNIMOE_EXPERT_GROUP = 2 };
+ * (run-major) requires B > 1.  TOKEN is the paper's ablation "w/o Expert-Centric
+ * Scheduling" (Fig. 4a): omnimoe_layer_fwd skips the schedule and each
+ * token gathers its own experts' rows (omnimoe_expert_fwd does not accept it). */
+enum { OMNIMOE_EXPERT_AUTO = 0, OMNIMOE_EXPERT_WARP = 1, OMNIMOE_EXPERT_GROUP = 2, OMNIMOE_EXPERT_TOKEN = 3 };
 /* workspace query selector */
 enum { OMNIMOE_WS_ROUTE = 0, OMNIMOE_WS_SCHEDULE = 1, OMNIMOE_WS_EXPERT = 2, OMNIMOE_WS_LAYER = 3 };
 

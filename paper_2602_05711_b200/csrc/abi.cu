@@ -83,7 +83,7 @@ omnimoe_status validate_dims(const omnimoe_dims* dp) {
     set_error("group_size and token_blocks must be >= 0");
     return OMNIMOE_ERR_INVALID_ARGUMENT;
   }
-  if (d.expert_kernel < OMNIMOE_EXPERT_AUTO || d.expert_kernel > OMNIMOE_EXPERT_GROUP) {
+  if (d.expert_kernel < OMNIMOE_EXPERT_AUTO || d.expert_kernel > OMNIMOE_EXPERT_TOKEN) {
     set_error("unknown expert kernel " + std::to_string(d.expert_kernel));
     return OMNIMOE_ERR_UNSUPPORTED;
   }
@@ -346,6 +346,10 @@ omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const voi
   OMNI_NONNULL(plan->sorted_token, "plan.sorted_token");
   OMNI_NONNULL(plan->sorted_gate, "plan.sorted_gate");
   OMNI_NONNULL(ws, "ws");
+  if (dims->expert_kernel == OMNIMOE_EXPERT_TOKEN) {
+    set_error("expert_fwd: OMNIMOE_EXPERT_TOKEN runs from the routing decision (omnimoe_layer_fwd), not a plan");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
   if (resolve_group_size(*dims) > 1) {
     OMNI_NONNULL(plan->sorted_expert, "plan.sorted_expert");
     OMNI_NONNULL(plan->run_offsets, "plan.run_offsets (group size > 1)");
@@ -409,9 +413,13 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
   const int64_t M = L * d.n_heads * d.top_k;
   OMNI_TRY(route_impl(d, L, x, subkeys, idx, gate, nullptr, w.route_ws, st));
   const int r_launch = omnimoe_last_launch_count();
-  OMNI_TRY(schedule_run(M, idx, gate, nullptr, d.n_heads * d.top_k, w.plan, resolve_group_size(d),
-                        resolve_token_blocks(d, L), w.sched_ws, st));
-  OMNI_TRY(expert_run(d, L, x, W, V, w.plan, w.y_routed, 0, w.expert_ws, st));
+  if (d.expert_kernel == OMNIMOE_EXPERT_TOKEN) {  // ablation: no Expert-Centric Scheduling
+    OMNI_TRY(expert_token_run(d, L, x, W, V, idx, gate, 0, d.n_rows * d.n_cols, w.y_routed, 0, st));
+  } else {
+    OMNI_TRY(schedule_run(M, idx, gate, nullptr, d.n_heads * d.top_k, w.plan, resolve_group_size(d),
+                          resolve_token_blocks(d, L), w.sched_ws, st));
+    OMNI_TRY(expert_run(d, L, x, W, V, w.plan, w.y_routed, 0, w.expert_ws, st));
+  }
   if (d.d_ff > 0) {
     OMNI_TRY(mlp_impl(d, L, x, w_gate_up, w_down, w.y_routed, y, w.H, st));
   } else {

@@ -337,6 +337,8 @@ __global__ void __launch_bounds__(256, 1)
   }
   int cs = 0;  // consumer chunk slot
   uint32_t pn = 0, cn = 0;
+  int wb = -64, we = 0, wt = 0;   // task metadata window [wb, wb + 32): lane i holds task wb + i
+  float wg = 0.f;
   uint4 xv[NV];                   // x_l of the current run (packed bf16)
   unsigned long long acc[NV][4];  // fp32 pairs of the run's partial y_l
   uint4 xnext[NV];                // x row of the next run to start, loaded ahead
@@ -368,11 +370,20 @@ __global__ void __launch_bounds__(256, 1)
         pstart = true;
       }
       const int s = pn % S;
+      if (ppos < wb || ppos >= wb + 32) {  // refill the metadata window: 32 tasks, one per lane
+        wb = ppos;
+        const int q = wb + lane;
+        we = q < m_loc ? sexp[q] : 0;
+        wg = q < m_loc ? sgate[q] : 0.f;
+        wt = q < m_loc ? stok[q] : 0;
+      }
+      const int e = __shfl_sync(0xffffffffu, we, ppos - wb);
+      const float mg = __shfl_sync(0xffffffffu, wg, ppos - wb);
+      const int mt = __shfl_sync(0xffffffffu, wt, ppos - wb);
       if (lane == 0) {
-        const int e = sexp[ppos];
         StageMeta m;
-        m.g = sgate[ppos];
-        m.tok = stok[ppos];
+        m.g = mg;
+        m.tok = mt;
         const bool last_run = ppos + 1 == pend;
         m.flags = (pstart ? 1 : 0) | (last_run ? 2 : 0) |
                   ((last_run && prun + 1 == (ps ? nr[1] : nr[0])) ? 4 : 0);
@@ -489,6 +500,192 @@ omnimoe_status launch_group_tma(int d, const void* x, const void* W, const void*
   return OMNIMOE_OK;
 }
 
+// ---------------------------------------------------------------------------
+// expert_token_kernel: the token-centric execution the paper ablates ("w/o ECS",
+// PAPER:241, 253, 396; Fig. 4a): one warp per token walks its h*K routed experts in
+// routing order, gathering w_e and v_e from HBM for every task (no reuse across
+// tokens), z = x_l . w_e, y_l += g * sigma(z) * v_e in registers; y_routed[l] is
+// written once (no atomics).  Same arithmetic as the grouped kernels.
+template <int NV>
+__global__ void __launch_bounds__(256)
+    expert_token_kernel(int d, int64_t L, int hk, const __nv_bfloat16* __restrict__ x,
+                        const __nv_bfloat16* __restrict__ W, const __nv_bfloat16* __restrict__ V,
+                        const int32_t* __restrict__ idx, const float* __restrict__ gate, int64_t begin,
+                        int64_t end, float* __restrict__ y, int accumulate, int act) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t l = gw; l < L; l += nw) {
+    uint4 xv[NV];
+    unsigned long long acc[NV][4];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      xv[j] = ld_vec(x + (size_t)l * d + (j * 32 + lane) * 8);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[j][i] = 0ull;
+    }
+    for (int k0 = 0; k0 < hk; k0 += 32) {
+      const int kk = k0 + lane;
+      const int n_l = kk < hk ? idx[l * hk + kk] : -1;
+      const float g_l = kk < hk ? gate[l * hk + kk] : 0.f;
+      const int cnt = min(32, hk - k0);
+      for (int t = 0; t < cnt; ++t) {
+        const int n = __shfl_sync(0xffffffffu, n_l, t);
+        const float g = __shfl_sync(0xffffffffu, g_l, t);
+        if (n < begin || n >= end) continue;  // another shard's expert
+        const __nv_bfloat16* we = W + (size_t)(n - begin) * d;
+        const __nv_bfloat16* ve = V + (size_t)(n - begin) * d;
+        uint4 wv[NV], vv[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          wv[j] = ld_vec(we + (j * 32 + lane) * 8);
+          vv[j] = ld_vec(ve + (j * 32 + lane) * 8);
+        }
+        float zp[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          float t2 = dot2_bf16(0.f, xv[j].x, wv[j].x);
+          t2 = dot2_bf16(t2, xv[j].y, wv[j].y);
+          t2 = dot2_bf16(t2, xv[j].z, wv[j].z);
+          zp[j] = dot2_bf16(t2, xv[j].w, wv[j].w);
+        }
+        float z = 0.f;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) z += zp[j];
+        z = warp_sum(z);
+        const float a = g * (act == OMNIMOE_IDENTITY ? z : silu_f(z));
+        const unsigned long long a2 = ((unsigned long long)__float_as_uint(a) << 32) | __float_as_uint(a);
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          axpy2_bf16(acc[j][0], a2, vv[j].x);
+          axpy2_bf16(acc[j][1], a2, vv[j].y);
+          axpy2_bf16(acc[j][2], a2, vv[j].z);
+          axpy2_bf16(acc[j][3], a2, vv[j].w);
+        }
+      }
+    }
+    float* yl = y + (size_t)l * d;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      float4* dst = reinterpret_cast<float4*>(yl + (j * 32 + lane) * 8);
+      float4 a = make_float4(lo_f(acc[j][0]), hi_f(acc[j][0]), lo_f(acc[j][1]), hi_f(acc[j][1]));
+      float4 b = make_float4(lo_f(acc[j][2]), hi_f(acc[j][2]), lo_f(acc[j][3]), hi_f(acc[j][3]));
+      if (accumulate) {
+        const float4 p = dst[0], q = dst[1];
+        a.x += p.x; a.y += p.y; a.z += p.z; a.w += p.w;
+        b.x += q.x; b.y += q.y; b.z += q.z; b.w += q.w;
+      }
+      dst[0] = a;
+      dst[1] = b;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// expert_run_reg_kernel: run-major ECS executor with register loads (no shared
+// memory staging): one warp per run (group q, token l), runs claimed 4 at a time
+// in plan order; w_e, v_e loaded straight into registers for each task (L2-resident
+// within the group window), x_l and the fp32 partial y_l held in registers over the
+// run, one red.v4 scatter per run.  Task metadata for 32 tasks is loaded at once
+// (one per lane) and broadcast by shuffle.  Same arithmetic as the TMA kernel.
+template <int NV>
+__global__ void __launch_bounds__(256)
+    expert_run_reg_kernel(int d, const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ W,
+                          const __nv_bfloat16* __restrict__ V, const int32_t* __restrict__ run_off,
+                          const int32_t* __restrict__ n_runs_p, const int32_t* __restrict__ m_loc_p,
+                          const int32_t* __restrict__ stok, const int32_t* __restrict__ sexp,
+                          const float* __restrict__ sgate, float* __restrict__ y, int act,
+                          int* __restrict__ work) {
+  constexpr int kChunk = 4;
+  const int lane = threadIdx.x & 31;
+  const int n_runs = *n_runs_p, m_loc = *m_loc_p;
+  int r0 = 0;
+  if (lane == 0) r0 = atomicAdd(work, kChunk);
+  r0 = __shfl_sync(0xffffffffu, r0, 0);
+  while (r0 < n_runs) {
+    const int rend = min(r0 + kChunk, n_runs);
+    const int beg0 = run_off[r0];
+    const int end0 = rend < n_runs ? run_off[rend] : m_loc;
+    // run starts of this chunk, lane i holds run r0 + i
+    const int rs = (lane < rend - r0) ? run_off[r0 + lane] : end0;
+    for (int r = r0; r < rend; ++r) {
+      const int beg = __shfl_sync(0xffffffffu, rs, r - r0);
+      const int end = (r + 1 < rend) ? __shfl_sync(0xffffffffu, rs, r + 1 - r0) : end0;
+      const int l = stok[beg];
+      uint4 xv[NV];
+      unsigned long long acc[NV][4];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        xv[j] = ld_vec(x + (size_t)l * d + (j * 32 + lane) * 8);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[j][i] = 0ull;
+      }
+      for (int p0 = beg; p0 < end; p0 += 32) {
+        const int pl = p0 + lane;
+        const int e_l = pl < end ? sexp[pl] : 0;
+        const float g_l = pl < end ? sgate[pl] : 0.f;
+        const int cnt = min(32, end - p0);
+        for (int t = 0; t < cnt; ++t) {
+          const int e = __shfl_sync(0xffffffffu, e_l, t);
+          const float g = __shfl_sync(0xffffffffu, g_l, t);
+          const __nv_bfloat16* we = W + (size_t)e * d;
+          const __nv_bfloat16* ve = V + (size_t)e * d;
+          uint4 wv[NV], vv[NV];
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            wv[j] = ld_vec(we + (j * 32 + lane) * 8);
+            vv[j] = ld_vec(ve + (j * 32 + lane) * 8);
+          }
+          float zp[NV];
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            float t2 = dot2_bf16(0.f, xv[j].x, wv[j].x);
+            t2 = dot2_bf16(t2, xv[j].y, wv[j].y);
+            t2 = dot2_bf16(t2, xv[j].z, wv[j].z);
+            zp[j] = dot2_bf16(t2, xv[j].w, wv[j].w);
+          }
+          float z = 0.f;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) z += zp[j];
+          z = warp_sum(z);
+          const float a = g * (act == OMNIMOE_IDENTITY ? z : silu_f(z));
+          const unsigned long long a2 = ((unsigned long long)__float_as_uint(a) << 32) | __float_as_uint(a);
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            axpy2_bf16(acc[j][0], a2, vv[j].x);
+            axpy2_bf16(acc[j][1], a2, vv[j].y);
+            axpy2_bf16(acc[j][2], a2, vv[j].z);
+            axpy2_bf16(acc[j][3], a2, vv[j].w);
+          }
+        }
+      }
+      float* yl = y + (size_t)l * d;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const int c = (j * 32 + lane) * 8;
+        red_add_v4(yl + c, lo_f(acc[j][0]), hi_f(acc[j][0]), lo_f(acc[j][1]), hi_f(acc[j][1]));
+        red_add_v4(yl + c + 4, lo_f(acc[j][2]), hi_f(acc[j][2]), lo_f(acc[j][3]), hi_f(acc[j][3]));
+      }
+    }
+    (void)beg0;
+    if (lane == 0) r0 = atomicAdd(work, kChunk);
+    r0 = __shfl_sync(0xffffffffu, r0, 0);
+  }
+}
+
+template <int NV>
+omnimoe_status launch_run_reg(int d, const void* x, const void* W, const void* V, const omnimoe_plan& plan,
+                              const int32_t* m_loc, float* y, int act, int* work, cudaStream_t st) {
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_run_reg_kernel<NV>, 256, 0);
+  expert_run_reg_kernel<NV><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(
+      d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W),
+      static_cast<const __nv_bfloat16*>(V), plan.run_offsets, plan.n_runs, m_loc, plan.sorted_token,
+      plan.sorted_expert, plan.sorted_gate, y, act, work);
+  OMNI_CHECK_LAUNCH("expert_run_reg_kernel");
+  return OMNIMOE_OK;
+}
+
 template <typename T>
 omnimoe_status launch_group(int d, const void* x, const void* W, const void* V, const omnimoe_plan& plan,
                             int64_t n_loc, float* y, int act, int* work, cudaStream_t st) {
@@ -498,7 +695,23 @@ omnimoe_status launch_group(int d, const void* x, const void* W, const void* V, 
   auto Wp = static_cast<const T*>(W);
   auto Vp = static_cast<const T*>(V);
   const int32_t* m_loc = plan.expert_offsets + n_loc;
-  if (sizeof(T) == 2 && d % 256 == 0 && d <= 2048 && getenv("OMNIMOE_NO_TMA_GROUP") == nullptr) {
+  // register-load run kernel for d <= 1024 (enough warps resident to hide L2 latency);
+  // TMA-staged kernel above that (profiles/r1/sweep_executors.log)
+  const char* force = getenv("OMNIMOE_GROUP_KERNEL");  // "reg" | "tma" (measurement override)
+  const bool reg = force ? force[0] == 'r' : d <= 1024;
+  if (sizeof(T) == 2 && d % 256 == 0 && d <= 2048 && reg) {
+    switch (d / 256) {
+      case 1: return launch_run_reg<1>(d, x, W, V, plan, m_loc, y, act, work, st);
+      case 2: return launch_run_reg<2>(d, x, W, V, plan, m_loc, y, act, work, st);
+      case 3: return launch_run_reg<3>(d, x, W, V, plan, m_loc, y, act, work, st);
+      case 4: return launch_run_reg<4>(d, x, W, V, plan, m_loc, y, act, work, st);
+      case 5: return launch_run_reg<5>(d, x, W, V, plan, m_loc, y, act, work, st);
+      case 6: return launch_run_reg<6>(d, x, W, V, plan, m_loc, y, act, work, st);
+      case 7: return launch_run_reg<7>(d, x, W, V, plan, m_loc, y, act, work, st);
+      default: return launch_run_reg<8>(d, x, W, V, plan, m_loc, y, act, work, st);
+    }
+  }
+  if (sizeof(T) == 2 && d % 256 == 0 && d <= 2048) {
     switch (d / 256) {
       case 1: return launch_group_tma<1, 8>(d, x, W, V, plan, m_loc, y, act, work, st);
       case 2: return launch_group_tma<2, 6>(d, x, W, V, plan, m_loc, y, act, work, st);
@@ -587,6 +800,39 @@ omnimoe_status launch_warp(int d, const void* x, const void* W, const void* V,
 }  // namespace
 
 size_t expert_ws_bytes(const omnimoe_dims&, int64_t) { return 256; }  // work counter
+
+omnimoe_status expert_token_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* V,
+                                const int32_t* idx, const float* gate, int64_t begin, int64_t end, float* y,
+                                int accumulate, cudaStream_t st) {
+  if (dm.dtype != OMNIMOE_BF16 || dm.d % 256 != 0 || dm.d > 2048) {
+    set_error("token-centric executor: bf16 with d a multiple of 256, d <= 2048");
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  if (L == 0) return OMNIMOE_OK;
+  const int hk = (int)(dm.n_heads * dm.top_k);
+  const int grid = (int)std::min<int64_t>((L + 7) / 8, kSMs * 16);
+  auto X = static_cast<const __nv_bfloat16*>(x);
+  auto Wp = static_cast<const __nv_bfloat16*>(W);
+  auto Vp = static_cast<const __nv_bfloat16*>(V);
+  switch (dm.d / 256) {
+#define OMNI_TOK_CASE(NVC)                                                                                       \
+  case NVC:                                                                                                      \
+    expert_token_kernel<NVC><<<grid, 256, 0, st>>>((int)dm.d, L, hk, X, Wp, Vp, idx, gate, begin, end, y,         \
+                                                   accumulate, dm.act);                                          \
+    break;
+    OMNI_TOK_CASE(1)
+    OMNI_TOK_CASE(2)
+    OMNI_TOK_CASE(3)
+    OMNI_TOK_CASE(4)
+    OMNI_TOK_CASE(5)
+    OMNI_TOK_CASE(6)
+    OMNI_TOK_CASE(7)
+    OMNI_TOK_CASE(8)
+#undef OMNI_TOK_CASE
+  }
+  OMNI_CHECK_LAUNCH("expert_token_kernel");
+  return OMNIMOE_OK;
+}
 
 int64_t resolve_group_size(const omnimoe_dims& d) {
   if (d.group_size > 0) return d.group_size;

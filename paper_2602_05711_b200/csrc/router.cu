@@ -219,6 +219,10 @@ __device__ void compact_ge(int n, KeyT thr, KeyF keyf, KeyT* out, SelShared<G>& 
   g::sync();
 }
 
+// Pair i of a stage compares a[lo], a[lo + stride], lo = 2i - (i mod stride).  For
+// stride <= 32 the pairs of the 32 consecutive i of one warp stay inside one 64-key
+// block, so consecutive warp-local stages only need __syncwarp; a block barrier is
+// needed only around stages with stride >= 64.
 template <int G, class K>
 __device__ void bitonic_desc(K* a, int n) {  // n a power of two; padding must hold minimal keys
   for (int size = 2; size <= n; size <<= 1)
@@ -233,7 +237,9 @@ __device__ void bitonic_desc(K* a, int n) {  // n a power of two; padding must h
           a[hi] = p;
         }
       }
-      Grp<G>::sync();
+      const int next = stride > 1 ? stride >> 1 : size;  // stride of the next stage
+      if (G > 32 && (stride >= 64 || next >= 64 || (stride == 1 && size == n))) __syncthreads();
+      else __syncwarp();
     }
 }
 
@@ -429,7 +435,7 @@ __host__ __device__ inline size_t group_bytes(const SelectParams& p) {
 }
 
 template <int G>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(G > 256 ? G : 256)
     select_kernel(SelectParams p, const float* __restrict__ logits, int32_t* __restrict__ idx,
                   float* __restrict__ gate, float* __restrict__ score) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -437,10 +443,19 @@ __global__ void __launch_bounds__(256)
   uint32_t* cand = reinterpret_cast<uint32_t*>(smem);
   const size_t cand_bytes = ((size_t)p.C * 4 + 15) / 16 * 16;
   const int K1 = p.top_k + 1;
-  for (int a = threadIdx.x; a < p.kr1; a += blockDim.x) {
+  // row a holds min(kc1, K1 / (a+1)) candidates; its offset is a prefix sum computed by
+  // thread 0 into the table's tail (scratch, overwritten below in index order)
+  int* row_off = reinterpret_cast<int*>(smem + ((size_t)p.C * 4 + 15) / 16 * 16) ;
+  if (threadIdx.x == 0) {
     int off = 0;
-    for (int t = 0; t < a; ++t) off += min(p.kc1, K1 / (t + 1));
-    const int nb = min(p.kc1, K1 / (a + 1));
+    for (int a = 0; a < p.kr1; ++a) {
+      row_off[a] = off;
+      off += min(p.kc1, K1 / (a + 1));
+    }
+  }
+  __syncthreads();
+  for (int a = threadIdx.x; a < p.kr1; a += blockDim.x) {
+    const int off = row_off[a], nb = min(p.kc1, K1 / (a + 1));
     for (int b = 0; b < nb; ++b) cand[off + b] = ((uint32_t)a << 16) | (uint32_t)b;
   }
   __syncthreads();
@@ -512,8 +527,10 @@ omnimoe_status select_params(const omnimoe_dims& d, int64_t T, SelectParams* p, 
   // one CTA per token-head: measured faster than one warp per token-head at K = 512
   // (the per-warp key buffers limit a warp-per-token-head kernel to 8 warps/SM);
   // small K uses select_warp_kernel instead (launch_select)
-  p->group = getenv("OMNIMOE_SELECT_WARP_GROUP") && p->pkeep <= 1024 ? 32 : 256;
-  const size_t gb = p->group == 32 ? group_bytes<32>(*p) : group_bytes<256>(*p);
+  // one CTA per token-head (1024 threads when K is in the thousands: the key buffers then
+  // allow only one CTA per SM, and more threads hide more latency)
+  p->group = getenv("OMNIMOE_SELECT_WARP_GROUP") && p->pkeep <= 1024 ? 32 : (p->pkeep >= 2048 ? 1024 : 256);
+  const size_t gb = p->group == 32 ? group_bytes<32>(*p) : p->group == 256 ? group_bytes<256>(*p) : group_bytes<1024>(*p);
   p->groups_per_cta = p->group == 32 ? (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024 - cand_bytes) / gb)) : 1;
   *smem = cand_bytes + gb * p->groups_per_cta;
   if (*smem > 225 * 1024) {
@@ -533,8 +550,8 @@ omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* lo
     OMNI_CHECK_LAUNCH("select_warp_kernel");
     return OMNIMOE_OK;
   }
-  auto kern = p.group == 32 ? select_kernel<32> : select_kernel<256>;
-  const int threads = p.group == 32 ? 32 * p.groups_per_cta : 256;
+  auto kern = p.group == 32 ? select_kernel<32> : p.group == 256 ? select_kernel<256> : select_kernel<1024>;
+  const int threads = p.group == 32 ? 32 * p.groups_per_cta : p.group;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     set_error("route: cannot set select_kernel shared memory");
     return OMNIMOE_ERR_CUDA;

@@ -11,6 +11,10 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
                             int64_t hk, const omnimoe_plan& plan, int64_t B, int64_t Tb, void* ws,
                             cudaStream_t st);
 int64_t resolve_group_size(const omnimoe_dims& d);
+// token-centric ablation executor ("w/o ECS"): straight from the routing decision
+omnimoe_status expert_token_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* V,
+                                const int32_t* idx, const float* gate, int64_t begin, int64_t end, float* y,
+                                int accumulate, cudaStream_t st);
 int64_t resolve_token_blocks(const omnimoe_dims& d, int64_t L);
 
 size_t expert_ws_bytes(const omnimoe_dims& d, int64_t L);

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_PKG, "libomnimoe.so")
 
 BF16, F32 = 0, 1
 SILU, IDENTITY = 0, 1
-EXPERT_AUTO, EXPERT_WARP, EXPERT_GROUP = 0, 1, 2
+EXPERT_AUTO, EXPERT_WARP, EXPERT_GROUP, EXPERT_TOKEN = 0, 1, 2, 3
 ROUTER_EXACT, ROUTER_EXACT_F64 = 0, 1
 LOGITS_ROUTE, LOGITS_EXACT_F64, LOGITS_BF16_FAST = 0, 1, 2
 WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER = 0, 1, 2, 3

@@ -358,3 +358,25 @@ def test_layer_full_size_sampled(name):
                        hr("w_gate_up"), hr("w_down"), id_map=idm)
     e_tok, e_elt = rel_errors(y[toks].float().cpu().numpy(), ref["y"])
     assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+
+
+# ---------------------------------------------------------------- ablation executors (N1)
+@pytest.mark.parametrize("ek", [om.EXPERT_TOKEN, om.EXPERT_WARP])
+def test_layer_ablation_executors(ek):
+    """'w/o ECS' token-centric executor and the expert-major B = 1 plan give
+    the same layer as the default grouped path and as the oracle."""
+    dims = om.LayerDims(d=256, n_rows=64, n_cols=64, top_k=32, n_heads=2, d_ff=256, expert_kernel=ek,
+                        group_size=1 if ek == om.EXPERT_WARP else 0)
+    L = 300
+    inp = make_inputs(dims, L, 13)
+    y = om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], inp["V"], inp["w_gate_up"], inp["w_down"])
+    d0 = om.LayerDims(d=256, n_rows=64, n_cols=64, top_k=32, n_heads=2, d_ff=256)
+    y0 = om.layer_fwd(d0, inp["x"], inp["subkeys"], inp["W"], inp["V"], inp["w_gate_up"], inp["w_down"])
+    torch.cuda.synchronize()
+    e_tok, e_elt = rel_errors(y.float().cpu().numpy(), y0.float().cpu().numpy())
+    assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+    hr = lambda n, r=None: host_rows(dims, 13, n, r)
+    ref = oracle.layer(hr("x", np.arange(L)), hr("subkeys").reshape(2, -1, 256), hr("W"), hr("V"), 64, 64, 32,
+                       hr("w_gate_up"), hr("w_down"))
+    e_tok, e_elt = rel_errors(y.float().cpu().numpy(), ref["y"])
+    assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
