@@ -203,7 +203,10 @@ omnimoe_status omnimoe_shared_mlp(const omnimoe_dims* dims, int64_t L, const voi
  *   W, V       [N][d]
  *   w_gate_up, w_down  as in omnimoe_shared_mlp (ignored when d_ff == 0)
  *   y          [L][d]
- *   idx_out, gate_out  nullable copies of the routing decision [L][h][K] */
+ *   idx_out, gate_out  nullable copies of the routing decision [L][h][K]; the same
+ *              set and gates as omnimoe_route, but (for K + 1 > 32) in the order of the
+ *              Cartesian candidates (row rank, then column rank) instead of by key --
+ *              the layer never needs the sort */
 omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void* x,
                                  const void* subkeys, const void* W, const void* V,
                                  const void* w_gate_up, const void* w_down, void* y,

@@ -186,13 +186,14 @@ omnimoe_status logits_impl(const omnimoe_dims& d, int64_t L, const void* x, cons
 
 // a1 (exact logits, Q9) -> a2 + a3 (select_kernel)
 omnimoe_status route_impl(const omnimoe_dims& d, int64_t L, const void* x, const void* subkeys,
-                          int32_t* idx, float* gate, float* score, void* ws, cudaStream_t st) {
+                          int32_t* idx, float* gate, float* score, void* ws, cudaStream_t st, int sorted = 1) {
   float* logits;
   void* sub_ws;
   route_ws(d, L, ws, &logits, &sub_ws);
   SelectParams sp;
   size_t smem;
   OMNI_TRY(select_params(d, L * d.n_heads, &sp, &smem));
+  sp.sorted = sorted;
   OMNI_TRY(logits_impl(d, L, x, subkeys, logits, sub_ws, st));
   return launch_select(sp, smem, logits, idx, gate, score, st);
 }
@@ -411,7 +412,8 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
   int32_t* idx = idx_out ? idx_out : w.idx;
   float* gate = gate_out ? gate_out : w.gate;
   const int64_t M = L * d.n_heads * d.top_k;
-  OMNI_TRY(route_impl(d, L, x, subkeys, idx, gate, nullptr, w.route_ws, st));
+  // the layer does not need the ids sorted by key (the schedule re-sorts the tasks)
+  OMNI_TRY(route_impl(d, L, x, subkeys, idx, gate, nullptr, w.route_ws, st, /*sorted=*/0));
   const int r_launch = omnimoe_last_launch_count();
   if (d.expert_kernel == OMNIMOE_EXPERT_TOKEN) {  // ablation: no Expert-Centric Scheduling
     OMNI_TRY(expert_token_run(d, L, x, W, V, idx, gate, 0, d.n_rows * d.n_cols, w.y_routed, 0, st));

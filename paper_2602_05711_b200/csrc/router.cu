@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(G > 256 ? G : 256)
                                               (size_t)(p.pkr + p.pkc) * 8 + 15) / 16 * 16);
   const int R = p.n_rows + p.n_cols;
   const int C = p.C;
-  const int keep = min(K1, C);
+  const int keep = min(p.top_k, C);  // exact logits: no K+1-th key (gap) is needed
   const uint32_t Nc = (uint32_t)p.n_cols;
   for (int th = blockIdx.x * ngroups + gid; th < p.T; th += gridDim.x * ngroups) {
     const float* lg = logits + (size_t)th * R;
@@ -480,9 +480,14 @@ __global__ void __launch_bounds__(G > 256 ? G : 256)
       const uint64_t ka = kr[ab >> 16], kb = kc[ab & 0xFFFF];
       return cell_key(half_val(ka), half_val(kb), half_idx(ka) * Nc + half_idx(kb));
     };
-    top_sorted<G, U128, 16>(C, keep, ckey, sel, sh);
+    if (p.sorted) {
+      top_sorted<G, U128, 16>(C, keep, ckey, sel, sh);
+    } else {  // the K largest, in candidate order (no sort; cell (0,0) is the maximum)
+      const U128 thr = keep < C ? radix_select<G, U128, 16>(C, keep, ckey, sh) : U128{0ull, 0ull};
+      compact_ge<G, false>(C, thr, ckey, sel, sh);
+    }
     // ---- gates: softmax over the K selected exact keys (Eq.Gate) ----
-    const double k1v = key_value(sel[0]);
+    const double k1v = key_value(p.sorted ? sel[0] : ckey(0));
     float es = 0.f;
     for (int k = Grp<G>::tid(); k < p.top_k; k += G) es += expf((float)(key_value(sel[k]) - k1v));
     es = group_sum<G>(es, sh);
@@ -517,8 +522,9 @@ omnimoe_status select_params(const omnimoe_dims& d, int64_t T, SelectParams* p, 
   // radix-selected threshold and is not sorted)
   p->pkr = std::max(sort_len(p->kr1, p->n_rows), p->kr1);
   p->pkc = std::max(sort_len(p->kc1, p->n_cols), p->kc1);
-  const int keep = (int)std::min<int64_t>(K1, C);
+  const int keep = (int)std::min<int64_t>(d.top_k, C);
   p->pkeep = std::max(sort_len(keep, (int)C), keep);
+  p->sorted = 1;
   if (d.n_rows > 65535 || d.n_cols > 65535) {
     set_error("route: grid halves must be <= 65535");
     return OMNIMOE_ERR_UNSUPPORTED;

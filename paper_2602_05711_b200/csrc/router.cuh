@@ -15,6 +15,7 @@ struct SelectParams {
   int pkr, pkc, pkeep; // key buffer lengths: row list, column list, K+1 selected
   int group;           // threads cooperating on one token-head: 32 (warp) or 256 (CTA)
   int groups_per_cta;
+  int sorted;          // 1: ids by (key desc, id asc); 0: the K selected in candidate (rank) order
 };
 
 omnimoe_status select_params(const omnimoe_dims& d, int64_t T, SelectParams* p, size_t* smem);

@@ -17,6 +17,7 @@ for name in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["C2", "C3a", "C3b
     inp = make_inputs(w.dims, L, w.seed, skip=("W", "V", "w_gate_up", "w_down"))
     ws = om.workspace(w.dims, L, om.WS_ROUTE)
     res = {}
+    lws = om.workspace(w.dims, L, om.WS_LAYER) if False else None
     for what in ("logits", "route"):
         ts = []
         for it in range(6):
