@@ -204,6 +204,9 @@ def bench_single(args, w, lr):
     from synth.workloads import make_inputs
     dims, L = w.dims, w.L
     inp = make_inputs(dims, L, w.seed)
+    if dims.v_layout == om.V_SLICED:  # one-time weight re-layout (not part of a step)
+        inp["V"] = om.pack_v(dims, inp["V"])
+        torch.cuda.synchronize()
     lws = om.workspace(dims, L, om.WS_LAYER)
     y = torch.empty((L, dims.d), dtype=dims.torch_dtype, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -303,6 +306,8 @@ def bench_single(args, w, lr):
     a6_gbs = a6_bytes / (a6_ms / 1000.0) / 1e9
     B = om.group_size(dims)
     kern = "expert_group_tma_kernel" if B > 1 else "expert_warp_kernel"
+    if dims.v_layout == om.V_SLICED:
+        kern = "expert_dot_kernel + expert_vslice_kernel"
     traffic, tsrc = ncu_traffic(w.name, kern)
     roofline = {"bound": "hbm", "achieved": a6_gbs, "peak": pk["hbm"], "unit": "GB/s", "frac": a6_gbs / pk["hbm"],
                 "traffic": traffic, "kernel": f"{kern} (a6)", "algorithmic_bytes_per_launch": a6_bytes,
@@ -326,7 +331,8 @@ def bench_single(args, w, lr):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "latency_ms": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded counter-based generator, DESIGN.md §3)",
-        "config": dict(_config_dict(w, "single-gpu"), group_size=B, expert_kernel=args.expert_kernel),
+        "config": dict(_config_dict(w, "single-gpu"), group_size=B, expert_kernel=args.expert_kernel,
+                       v_layout=args.v_layout if dims.v_layout == om.V_SLICED else "rows"),
         "stage_ms": stage_ms, "n_active": n_active, "tasks": M,
         "step_ms_min_max": [min(step_ms), max(step_ms)],
         "roofline": roofline,
@@ -442,6 +448,9 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=60.0, help="total oracle time of --impl reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--v-layout", default="sliced", choices=["sliced", "rows"],
+                    help="layout of the V table: sliced ([d/32][N][32], the two-pass SLICED executor) or rows "
+                         "([N][d], the one-pass grouped executor)")
     ap.add_argument("--expert-kernel", default="auto", choices=["auto", "token", "warp"],
                     help="a6 executor: auto (grouped ECS), token (the paper's 'w/o ECS' ablation), "
                          "warp (expert-major, B = 1)")
@@ -458,9 +467,10 @@ def main():
         build.build()
     if ws > 1:
         dist.barrier()
-    w = configs.get(args.config)
+    from paper_2602_05711_b200 import omnimoe as om
+    sliced = args.v_layout == "sliced" and args.expert_kernel == "auto" and ws == 1
+    w = configs.get(args.config, v_layout=om.V_SLICED if sliced else om.V_ROWS)
     if args.expert_kernel != "auto":
-        from paper_2602_05711_b200 import omnimoe as om
         ek = {"token": om.EXPERT_TOKEN, "warp": om.EXPERT_WARP}[args.expert_kernel]
         w = configs.get(args.config, expert_kernel=ek, group_size=1 if ek == om.EXPERT_WARP else 0)
     try:

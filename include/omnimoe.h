@@ -52,7 +52,20 @@ enum { OMNIMOE_SILU = 0, OMNIMOE_IDENTITY = 1 };
  * (run-major) requires B > 1.  TOKEN is the paper's ablation "w/o Expert-Centric
  * Scheduling" (Fig. 4a): omnimoe_layer_fwd skips the schedule and each
  * token gathers its own experts' rows (omnimoe_expert_fwd does not accept it). */
-enum { OMNIMOE_EXPERT_AUTO = 0, OMNIMOE_EXPERT_WARP = 1, OMNIMOE_EXPERT_GROUP = 2, OMNIMOE_EXPERT_TOKEN = 3 };
+enum { OMNIMOE_EXPERT_AUTO = 0, OMNIMOE_EXPERT_WARP = 1, OMNIMOE_EXPERT_GROUP = 2, OMNIMOE_EXPERT_TOKEN = 3,
+       OMNIMOE_EXPERT_SLICED = 4 };
+/* Memory layout of the value table V (the down-projection rows v_n of Eq.WV,
+ * PAPER:172-176).  ROWS: [N][d], one row per expert.  SLICED: [d/32][N][32], i.e.
+ * the table cut into d/32 column slices of 32 elements, each slice stored
+ * expert-major (64 bytes per expert and slice); omnimoe_pack_v converts.  The
+ * SLICED executor (AUTO picks it for this layout, bf16 only) evaluates Eq.Grouped
+ * in two passes: (Z) the plan's runs compute a = g * sigma(x_l . w_e) for every
+ * task with w_e read once per group window; (V) slice by slice, every token
+ * gathers the slice of v_e of its tasks and accumulates a * v_e into its output
+ * slice.  One slice of V (64 N bytes) stays L2-resident while all tokens use it,
+ * so V is read from HBM once and y_routed is written once, without atomics
+ * (DESIGN.md §4.4). */
+enum { OMNIMOE_V_ROWS = 0, OMNIMOE_V_SLICED = 1 };
 /* workspace query selector */
 enum { OMNIMOE_WS_ROUTE = 0, OMNIMOE_WS_SCHEDULE = 1, OMNIMOE_WS_EXPERT = 2, OMNIMOE_WS_LAYER = 3 };
 
@@ -77,6 +90,8 @@ enum { OMNIMOE_ROUTER_EXACT = 0, OMNIMOE_ROUTER_EXACT_F64 = 1 };
  *              experts per group; 1 = expert-major plan; 0 = library choice
  *              (omnimoe_group_size()).
  *   token_blocks T_b: see below.
+ *   v_layout   OMNIMOE_V_ROWS | OMNIMOE_V_SLICED: layout of the V argument of
+ *              omnimoe_expert_fwd / omnimoe_layer_fwd (W is always [N][d]).
  */
 typedef struct {
   int64_t d, n_rows, n_cols, top_k, n_heads, d_ff;
@@ -89,6 +104,8 @@ typedef struct {
                           * blocks in turn, so that one block's x and y_routed stay
                           * L2-resident; 1 = the paper's single sort;
                           * 0 = library choice */
+  int32_t v_layout;      /* OMNIMOE_V_ROWS | OMNIMOE_V_SLICED */
+  int32_t reserved;
 } omnimoe_dims;
 
 /* Expert-centric plan for the local expert range [expert_begin, expert_end)
@@ -108,6 +125,13 @@ typedef struct {
  *   run_offsets    int32[M+1]      B > 1 only (nullable for B = 1): first task of
  *                                  each run = the tasks of one token in one group
  *   n_runs         int32[1]        B > 1 only: number of runs P
+ * Task-order arrays (nullable; required by the SLICED executor; tasks must be
+ * sorted by token, which the default token = t / (h*K) is):
+ *   sorted_task    int32[M]        task index t of each plan position
+ *   task_pair      int32[M][2]     task t: (local expert id, -1 outside the range;
+ *                                  bits of a_t = g*sigma(z), scratch of the SLICED executor)
+ *   token_offsets  int32[n_tokens+1]  first task of each token
+ *   n_tokens       number of tokens (input; 0: ceil(M / (h*K)))
  * For B = 1 the segment of local expert e is [expert_offsets[e],
  * expert_offsets[e+1]) with tokens ascending.  Only the first
  * m_loc entries of sorted_* are meaningful (tasks outside the range are not
@@ -122,6 +146,10 @@ typedef struct {
   int32_t* sorted_expert;
   int32_t* run_offsets;
   int32_t* n_runs;
+  int32_t* sorted_task;
+  int32_t* task_pair;
+  int32_t* token_offsets;
+  int64_t n_tokens;
 } omnimoe_plan;
 
 /* The group size B that omnimoe_schedule / omnimoe_expert_fwd use for dims
@@ -178,15 +206,25 @@ omnimoe_status omnimoe_schedule(const omnimoe_dims* dims, int64_t M, const int32
  * B = 1: one warp per active expert reads w_e, v_e once and walks its tokens.
  * B > 1: one warp per run (group q, token l) keeps x_l and the partial y_l in
  * registers over the run's experts and scatter-adds once per run.
+ * SLICED (dims.v_layout == OMNIMOE_V_SLICED, B > 1, the plan's task-order arrays
+ * set, tasks sorted by token, tokens < L): pass Z over the runs writes
+ * plan->task_pair[t][1], pass V writes every y_routed[l] slice once (no atomics,
+ * deterministic).
  *   x         [L][d]
  *   W_loc     [n_loc][d]  rows of W for the plan's expert range
- *   V_loc     [n_loc][d]
- *   y_routed  float [L][d]; zeroed first unless accumulate != 0
- * fp32 atomics: reproducible up to summation order. */
+ *   V_loc     [n_loc][d] (ROWS) or [d/32][n_loc][32] (SLICED)
+ *   y_routed  float [L][d]; overwritten unless accumulate != 0 (then added to)
+ * ROWS executors use fp32 atomics: reproducible up to summation order. */
 omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const void* x,
                                   const void* W_loc, const void* V_loc, const omnimoe_plan* plan,
                                   float* y_routed, int accumulate, void* ws, size_t ws_bytes,
                                   omnimoe_stream_t stream);
+
+/* V [n][d] (OMNIMOE_V_ROWS) -> V_sliced [d/32][n][32] (OMNIMOE_V_SLICED): a
+ * one-time weight re-layout (no arithmetic; bit-exact copy), d % 32 == 0.
+ * n = number of expert rows in the table (N, or n_loc for a shard). */
+omnimoe_status omnimoe_pack_v(const omnimoe_dims* dims, int64_t n, const void* V, void* V_sliced,
+                              omnimoe_stream_t stream);
 
 /* Shared dense MLP (SwiGLU without biases, reading Q2) plus
  * combine (Eq.MoE):
@@ -200,7 +238,8 @@ omnimoe_status omnimoe_shared_mlp(const omnimoe_dims* dims, int64_t L, const voi
 
 /* Whole layer forward (Eq.MoE / Eq.Assemble):
  * route -> schedule (full expert range) -> expert_fwd -> shared MLP + combine.
- *   W, V       [N][d]
+ *   W          [N][d]
+ *   V          [N][d] or, for dims.v_layout == OMNIMOE_V_SLICED, [d/32][N][32]
  *   w_gate_up, w_down  as in omnimoe_shared_mlp (ignored when d_ff == 0)
  *   y          [L][d]
  *   idx_out, gate_out  nullable copies of the routing decision [L][h][K]; the same

@@ -83,7 +83,24 @@ omnimoe_status validate_dims(const omnimoe_dims* dp) {
     set_error("group_size and token_blocks must be >= 0");
     return OMNIMOE_ERR_INVALID_ARGUMENT;
   }
-  if (d.expert_kernel < OMNIMOE_EXPERT_AUTO || d.expert_kernel > OMNIMOE_EXPERT_TOKEN) {
+  if (d.v_layout != OMNIMOE_V_ROWS && d.v_layout != OMNIMOE_V_SLICED) {
+    set_error("unknown V layout " + std::to_string(d.v_layout));
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  if (d.v_layout == OMNIMOE_V_SLICED) {
+    if (d.dtype != OMNIMOE_BF16 || d.d % 32 != 0 || d.d > 2048) {
+      set_error("V_SLICED layout: bf16 with d % 32 == 0 and d <= 2048 " + dims_str(d));
+      return OMNIMOE_ERR_UNSUPPORTED;
+    }
+    if (d.expert_kernel != OMNIMOE_EXPERT_AUTO && d.expert_kernel != OMNIMOE_EXPERT_SLICED) {
+      set_error("V_SLICED layout runs the SLICED executor only (expert_kernel AUTO or SLICED)");
+      return OMNIMOE_ERR_INVALID_ARGUMENT;
+    }
+  } else if (d.expert_kernel == OMNIMOE_EXPERT_SLICED) {
+    set_error("expert kernel SLICED needs dims.v_layout == OMNIMOE_V_SLICED");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (d.expert_kernel < OMNIMOE_EXPERT_AUTO || d.expert_kernel > OMNIMOE_EXPERT_SLICED) {
     set_error("unknown expert kernel " + std::to_string(d.expert_kernel));
     return OMNIMOE_ERR_UNSUPPORTED;
   }
@@ -149,6 +166,10 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
   int32_t* se = c.take<int32_t>((size_t)std::max<int64_t>(M, 1));
   int32_t* ro = c.take<int32_t>((size_t)M + 1);
   int32_t* nr = c.take<int32_t>(1);
+  const bool sliced = d.v_layout == OMNIMOE_V_SLICED;
+  int32_t* stask = sliced ? c.take<int32_t>((size_t)std::max<int64_t>(M, 1)) : nullptr;
+  int32_t* tpair = sliced ? c.take<int32_t>(2 * (size_t)std::max<int64_t>(M, 1)) : nullptr;
+  int32_t* toff = sliced ? c.take<int32_t>((size_t)L + 1) : nullptr;
   const size_t sb = schedule_ws_bytes(M, N);
   void* sw = c.take<char>(sb);
   float* yr = c.take<float>((size_t)L * d.d);
@@ -159,7 +180,7 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
     o->route_bytes = rb;
     o->idx = idx;
     o->gate = gate;
-    o->plan = omnimoe_plan{off, st, sg, act, na, 0, N, se, ro, nr};
+    o->plan = omnimoe_plan{off, st, sg, act, na, 0, N, se, ro, nr, stask, tpair, toff, L};
     o->sched_ws = sw;
     o->y_routed = yr;
     o->expert_ws = ew;
@@ -356,6 +377,11 @@ omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const voi
     OMNI_NONNULL(plan->run_offsets, "plan.run_offsets (group size > 1)");
     OMNI_NONNULL(plan->n_runs, "plan.n_runs (group size > 1)");
   }
+  if (dims->v_layout == OMNIMOE_V_SLICED) {
+    OMNI_NONNULL(plan->sorted_task, "plan.sorted_task (SLICED executor)");
+    OMNI_NONNULL(plan->task_pair, "plan.task_pair (SLICED executor)");
+    OMNI_NONNULL(plan->token_offsets, "plan.token_offsets (SLICED executor)");
+  }
   OMNI_TRY(check_ws(ws_bytes, expert_ws_bytes(*dims, L), "expert_fwd"));
   OMNI_TRY(check_device());
   return expert_run(*dims, L, x, W_loc, V_loc, *plan, y_routed, accumulate, ws, (cudaStream_t)stream);
@@ -415,6 +441,7 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
   // the layer does not need the ids sorted by key (the schedule re-sorts the tasks)
   OMNI_TRY(route_impl(d, L, x, subkeys, idx, gate, nullptr, w.route_ws, st, /*sorted=*/0));
   const int r_launch = omnimoe_last_launch_count();
+  w.plan.n_tokens = L;
   if (d.expert_kernel == OMNIMOE_EXPERT_TOKEN) {  // ablation: no Expert-Centric Scheduling
     OMNI_TRY(expert_token_run(d, L, x, W, V, idx, gate, 0, d.n_rows * d.n_cols, w.y_routed, 0, st));
   } else {
@@ -430,6 +457,29 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
   }
   (void)r_launch;
   return OMNIMOE_OK;
+}
+
+omnimoe_status omnimoe_pack_v(const omnimoe_dims* dims, int64_t n, const void* V, void* V_sliced,
+                              omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  if (dims->dtype != OMNIMOE_BF16 || dims->d % 32 != 0) {
+    set_error("pack_v: bf16 with d % 32 == 0 " + dims_str(*dims));
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  if (n < 0 || n >= (int64_t(1) << 31)) {
+    set_error("pack_v: n out of range");
+    return OMNIMOE_ERR_SHAPE;
+  }
+  if (n == 0) return OMNIMOE_OK;
+  OMNI_NONNULL(V, "V");
+  OMNI_NONNULL(V_sliced, "V_sliced");
+  if (V == V_sliced) {
+    set_error("pack_v: V and V_sliced must not alias");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  OMNI_TRY(check_device());
+  return pack_v(n, (int)dims->d, V, V_sliced, (cudaStream_t)stream);
 }
 
 omnimoe_status omnimoe_router_logits(const omnimoe_dims* dims, int64_t L, const void* x, const void* subkeys,

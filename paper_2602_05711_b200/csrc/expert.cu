@@ -24,6 +24,11 @@
 namespace omni {
 namespace {
 
+int env_int(const char* name, int dflt) {  // measurement overrides (tools/ sweeps)
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 template <typename T>
 struct VecT;
 template <>
@@ -264,6 +269,11 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -797,6 +807,319 @@ omnimoe_status launch_warp(int d, const void* x, const void* W, const void* V,
   return OMNIMOE_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// SLICED executor (dims.v_layout == OMNIMOE_V_SLICED).
+//
+// Per task the method needs one d-row of W (for z) and one d-row of V (for the
+// axpy); with random routing the only reuse is across the eta = M/|E_active|
+// tasks of an expert, so those rows cross L2 -> SM once per task whatever the
+// loop order, and every re-read that misses L2 costs HBM.  The executor splits
+// Eq.Grouped into two passes so that each keeps its working set in L2:
+//
+//  expert_dot_kernel (pass Z): the plan's runs (group q, token l) in plan order,
+//    x_l in registers, w_e streamed (the group's W rows stay L2-resident: D_expert
+//    once from HBM), a_t = g * sigma(x_l . w_e) written to task_pair[t][1].
+//  expert_vslice_kernel (pass V): slice-major.  For slice s (32 columns) every
+//    token l gathers the 64-byte slice of v_e of each of its tasks (token order,
+//    plan->token_offsets), accumulates a_t * v_e[s] in registers and writes its
+//    y_routed slice once.  The whole slice of V (64 N bytes, 67 MB at N = 2^20) is
+//    L2-resident while all tokens use it, so V is read from HBM once, and no
+//    atomics touch y_routed.
+template <int NV>
+__global__ void __launch_bounds__(256)
+    expert_dot_kernel(int d, const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ W,
+                      const int32_t* __restrict__ run_off, const int32_t* __restrict__ n_runs_p,
+                      const int32_t* __restrict__ m_loc_p, const int32_t* __restrict__ stok,
+                      const int32_t* __restrict__ sexp, const float* __restrict__ sgate,
+                      const int32_t* __restrict__ stask, int32_t* __restrict__ task_pair, int act,
+                      int* __restrict__ work) {
+  constexpr int kChunk = 4;
+  const int lane = threadIdx.x & 31;
+  const int n_runs = *n_runs_p, m_loc = *m_loc_p;
+  int r0 = 0;
+  if (lane == 0) r0 = atomicAdd(work, kChunk);
+  r0 = __shfl_sync(0xffffffffu, r0, 0);
+  while (r0 < n_runs) {
+    const int rend = min(r0 + kChunk, n_runs);
+    const int end0 = rend < n_runs ? run_off[rend] : m_loc;
+    const int rs = (lane < rend - r0) ? run_off[r0 + lane] : end0;  // lane i: start of run r0 + i
+    for (int r = r0; r < rend; ++r) {
+      const int beg = __shfl_sync(0xffffffffu, rs, r - r0);
+      const int end = (r + 1 < rend) ? __shfl_sync(0xffffffffu, rs, r + 1 - r0) : end0;
+      const int l = stok[beg];
+      uint4 xv[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const int c = (j * 32 + lane) * 8;
+        xv[j] = c < d ? ld_vec(x + (size_t)l * d + c) : make_uint4(0, 0, 0, 0);
+      }
+      for (int p0 = beg; p0 < end; p0 += 32) {
+        const int pl = p0 + lane;
+        const int e_l = pl < end ? sexp[pl] : 0;
+        const float g_l = pl < end ? sgate[pl] : 0.f;
+        const int t_l = pl < end ? stask[pl] : 0;
+        const int cnt = min(32, end - p0);
+        float my_a = 0.f;
+        for (int t = 0; t < cnt; t += 2) {  // two tasks in flight per warp
+          const int t1 = min(t + 1, cnt - 1);
+          const int e0 = __shfl_sync(0xffffffffu, e_l, t), e1 = __shfl_sync(0xffffffffu, e_l, t1);
+          const float g0 = __shfl_sync(0xffffffffu, g_l, t), g1 = __shfl_sync(0xffffffffu, g_l, t1);
+          const __nv_bfloat16* w0 = W + (size_t)e0 * d;
+          const __nv_bfloat16* w1 = W + (size_t)e1 * d;
+          uint4 a[NV], b[NV];
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            const int c = (j * 32 + lane) * 8;
+            a[j] = c < d ? ld_vec(w0 + c) : make_uint4(0, 0, 0, 0);
+            b[j] = c < d ? ld_vec(w1 + c) : make_uint4(0, 0, 0, 0);
+          }
+          float z0 = 0.f, z1 = 0.f;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            float u = dot2_bf16(0.f, xv[j].x, a[j].x);
+            u = dot2_bf16(u, xv[j].y, a[j].y);
+            u = dot2_bf16(u, xv[j].z, a[j].z);
+            z0 += dot2_bf16(u, xv[j].w, a[j].w);
+            float v = dot2_bf16(0.f, xv[j].x, b[j].x);
+            v = dot2_bf16(v, xv[j].y, b[j].y);
+            v = dot2_bf16(v, xv[j].z, b[j].z);
+            z1 += dot2_bf16(v, xv[j].w, b[j].w);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            z0 += __shfl_xor_sync(0xffffffffu, z0, o);
+            z1 += __shfl_xor_sync(0xffffffffu, z1, o);
+          }
+          const float a0 = g0 * (act == OMNIMOE_IDENTITY ? z0 : silu_f(z0));
+          const float a1 = g1 * (act == OMNIMOE_IDENTITY ? z1 : silu_f(z1));
+          if (lane == t) my_a = a0;
+          if (lane == t + 1) my_a = a1;
+        }
+        if (lane < cnt) task_pair[2 * (size_t)t_l + 1] = __float_as_int(my_a);
+      }
+    }
+    if (lane == 0) r0 = atomicAdd(work, kChunk);
+    r0 = __shfl_sync(0xffffffffu, r0, 0);
+  }
+}
+
+__device__ __forceinline__ int2 ld_pair(const int32_t* p, uint64_t pol) {
+  int2 r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.b32 {%0, %1}, [%2], %3;"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+// pass V: one warp per (slice, token) item; lane = (task sub-group g8 = lane/4,
+// column quad c4 = lane%4): 8 tasks per load instruction, 8 bf16 columns per lane.
+// The (expert, a) pairs of the next 64 tasks -- possibly of the next item, which
+// is claimed one item ahead -- are loaded while the current 64 are processed.
+__global__ void __launch_bounds__(256)
+    expert_vslice_kernel(int d, int64_t L, int64_t n_loc, const int32_t* __restrict__ tok_off, int64_t n_tok,
+                         const int32_t* __restrict__ task_pair, const __nv_bfloat16* __restrict__ Vs,
+                         float* __restrict__ y, int accumulate, int* __restrict__ work, int stream_hint) {
+  const int lane = threadIdx.x & 31, c4 = lane & 3, g8 = lane >> 2;
+  const int S = d / 32;
+  const int64_t n_items = (int64_t)S * L;
+  const uint64_t pol = stream_hint ? policy_evict_first() : policy_evict_normal();
+  // item i: slice i / L, token i % L
+  auto claim = [&]() {
+    int64_t v = 0;
+    if (lane == 0) v = atomicAdd(work, 1);
+    return (int64_t)__shfl_sync(0xffffffffu, (int)v, 0);
+  };
+  auto range = [&](int64_t item, int& beg, int& end) {
+    beg = end = 0;
+    if (item < n_items) {
+      const int64_t l = item % L;
+      if (l < n_tok) {
+        beg = tok_off[l];
+        end = tok_off[l + 1];
+      }
+    }
+  };
+  auto fetch = [&](int p0, int end, int2& pa, int2& pb) {
+    pa = (p0 + lane < end) ? ld_pair(task_pair + 2 * (size_t)(p0 + lane), pol) : make_int2(-1, 0);
+    pb = (p0 + 32 + lane < end) ? ld_pair(task_pair + 2 * (size_t)(p0 + 32 + lane), pol) : make_int2(-1, 0);
+  };
+  int64_t it = claim();
+  int beg, end;
+  range(it, beg, end);
+  int2 na, nb;
+  fetch(beg, end, na, nb);
+  while (it < n_items) {
+    const int64_t nxt = claim();
+    int nbeg, nend;
+    range(nxt, nbeg, nend);
+    const int s = (int)(it / L);
+    const int64_t l = it - (int64_t)s * L;
+    const __nv_bfloat16* vs = Vs + (size_t)s * n_loc * 32 + c4 * 8;
+    unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
+    for (int p0 = beg; p0 < end; p0 += 64) {
+      const int2 ca = na, cb = nb;
+      if (p0 + 64 < end) fetch(p0 + 64, end, na, nb);
+      else fetch(nbeg, nend, na, nb);  // the next item's first tasks
+      const int n_r = min(8, (end - p0 + 7) >> 3);  // rounds of 8 tasks holding work
+      uint4 v[8];
+      float a[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int src = (r & 3) * 8 + g8;
+        const int e = __shfl_sync(0xffffffffu, r < 4 ? ca.x : cb.x, src);
+        a[r] = __int_as_float(__shfl_sync(0xffffffffu, r < 4 ? ca.y : cb.y, src));
+        if (e < 0) a[r] = 0.f;
+        v[r] = (r < n_r && e >= 0) ? ld_vec(vs + (size_t)e * 32) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const unsigned long long a2 = ((unsigned long long)__float_as_uint(a[r]) << 32) | __float_as_uint(a[r]);
+        axpy2_bf16(acc[0], a2, v[r].x);
+        axpy2_bf16(acc[1], a2, v[r].y);
+        axpy2_bf16(acc[2], a2, v[r].z);
+        axpy2_bf16(acc[3], a2, v[r].w);
+      }
+    }
+    if (beg == end) fetch(nbeg, nend, na, nb);
+    float f[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = lo_f(acc[i]);
+      f[2 * i + 1] = hi_f(acc[i]);
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] += __shfl_xor_sync(0xffffffffu, f[i], o);
+    if (g8 == 0) {
+      float4* dst = reinterpret_cast<float4*>(y + (size_t)l * d + s * 32 + c4 * 8);
+      float4 u = make_float4(f[0], f[1], f[2], f[3]), w = make_float4(f[4], f[5], f[6], f[7]);
+      if (accumulate) {
+        const float4 p = dst[0], q = dst[1];
+        u.x += p.x; u.y += p.y; u.z += p.z; u.w += p.w;
+        w.x += q.x; w.y += q.y; w.z += q.z; w.w += q.w;
+      }
+      dst[0] = u;
+      dst[1] = w;
+    }
+    it = nxt;
+    beg = nbeg;
+    end = nend;
+  }
+}
+
+// V [n][d] -> V_sliced [d/32][n][32] (16-byte moves; bit-exact)
+__global__ void pack_v_kernel(const uint4* __restrict__ V, uint4* __restrict__ Vs, int64_t n, int d) {
+  const int64_t per_row = d / 8, total = n * per_row;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / per_row;
+    const int q = (int)(i - row * per_row);
+    Vs[((size_t)(q >> 2) * n + row) * 4 + (q & 3)] = V[i];
+  }
+}
+
+
+// pass Z on an expert-major plan (B = 1): one warp per active
+// expert holds w_e in registers (W streamed from HBM once, in ascending expert
+// order) and walks the expert's tasks: x_l gathered from L2 (x is the only
+// reused operand: 2dL bytes), a_t = g * sigma(x_l . w_e) -> task_pair[t][1].  Two
+// tasks' x rows are in flight per warp.
+template <int NV>
+__global__ void __launch_bounds__(256)
+    expert_zdot_kernel(int d, const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ W,
+                       const int32_t* __restrict__ offsets, const int32_t* __restrict__ active,
+                       const int32_t* __restrict__ n_active, const int32_t* __restrict__ stok,
+                       const float* __restrict__ sgate, const int32_t* __restrict__ stask,
+                       int32_t* __restrict__ task_pair, int act, int* __restrict__ work, int w_hint) {
+  const int lane = threadIdx.x & 31;
+  const int na = *n_active;
+  const uint64_t pol = w_hint ? policy_evict_first() : policy_evict_normal();
+  int tau = 0;
+  if (lane == 0) tau = atomicAdd(work, 1);
+  tau = __shfl_sync(0xffffffffu, tau, 0);
+  while (tau < na) {
+    const int e = active[tau];
+    const int beg = offsets[e], end = offsets[e + 1];
+    uint4 wv[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int c = (j * 32 + lane) * 8;
+      wv[j] = c < d ? ld_vec_hint(W + (size_t)e * d + c, pol) : make_uint4(0, 0, 0, 0);
+    }
+    int nxt = 0;
+    if (lane == 0) nxt = atomicAdd(work, 1);  // claim the next expert early
+    for (int p0 = beg; p0 < end; p0 += 32) {
+      const int pl = p0 + lane;
+      const int l_l = pl < end ? stok[pl] : 0;
+      const float g_l = pl < end ? sgate[pl] : 0.f;
+      const int t_l = pl < end ? stask[pl] : 0;
+      const int cnt = min(32, end - p0);
+      float my_a = 0.f;
+      for (int t = 0; t < cnt; t += 2) {
+        const int t1 = min(t + 1, cnt - 1);
+        const int l0 = __shfl_sync(0xffffffffu, l_l, t), l1 = __shfl_sync(0xffffffffu, l_l, t1);
+        const float g0 = __shfl_sync(0xffffffffu, g_l, t), g1 = __shfl_sync(0xffffffffu, g_l, t1);
+        uint4 a[NV], b[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          const int c = (j * 32 + lane) * 8;
+          a[j] = c < d ? ld_vec(x + (size_t)l0 * d + c) : make_uint4(0, 0, 0, 0);
+          b[j] = c < d ? ld_vec(x + (size_t)l1 * d + c) : make_uint4(0, 0, 0, 0);
+        }
+        float z0 = 0.f, z1 = 0.f;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          float u = dot2_bf16(0.f, wv[j].x, a[j].x);
+          u = dot2_bf16(u, wv[j].y, a[j].y);
+          u = dot2_bf16(u, wv[j].z, a[j].z);
+          z0 += dot2_bf16(u, wv[j].w, a[j].w);
+          float v = dot2_bf16(0.f, wv[j].x, b[j].x);
+          v = dot2_bf16(v, wv[j].y, b[j].y);
+          v = dot2_bf16(v, wv[j].z, b[j].z);
+          z1 += dot2_bf16(v, wv[j].w, b[j].w);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          z0 += __shfl_xor_sync(0xffffffffu, z0, o);
+          z1 += __shfl_xor_sync(0xffffffffu, z1, o);
+        }
+        const float a0 = g0 * (act == OMNIMOE_IDENTITY ? z0 : silu_f(z0));
+        const float a1 = g1 * (act == OMNIMOE_IDENTITY ? z1 : silu_f(z1));
+        if (lane == t) my_a = a0;
+        if (lane == t + 1) my_a = a1;
+      }
+      if (lane < cnt) task_pair[2 * (size_t)t_l + 1] = __float_as_int(my_a);
+    }
+    tau = __shfl_sync(0xffffffffu, nxt, 0);
+  }
+}
+
+template <int NV>
+omnimoe_status launch_zdot(int d, const void* x, const void* W, const omnimoe_plan& plan, int act, int* work,
+                           cudaStream_t st) {
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_zdot_kernel<NV>, 256, 0);
+  expert_zdot_kernel<NV><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(
+      d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W), plan.expert_offsets,
+      plan.active, plan.n_active, plan.sorted_token, plan.sorted_gate, plan.sorted_task, plan.task_pair, act, work,
+      env_int("OMNIMOE_W_HINT", 1));
+  OMNI_CHECK_LAUNCH("expert_zdot_kernel");
+  return OMNIMOE_OK;
+}
+
+template <int NV>
+omnimoe_status launch_dot(int d, const void* x, const void* W, const omnimoe_plan& plan, const int32_t* m_loc,
+                          int act, int* work, cudaStream_t st) {
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_dot_kernel<NV>, 256, 0);
+  expert_dot_kernel<NV><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(
+      d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W), plan.run_offsets, plan.n_runs,
+      m_loc, plan.sorted_token, plan.sorted_expert, plan.sorted_gate, plan.sorted_task, plan.task_pair, act, work);
+  OMNI_CHECK_LAUNCH("expert_dot_kernel");
+  return OMNIMOE_OK;
+}
+
 }  // namespace
 
 size_t expert_ws_bytes(const omnimoe_dims&, int64_t) { return 256; }  // work counter
@@ -837,6 +1160,7 @@ omnimoe_status expert_token_run(const omnimoe_dims& dm, int64_t L, const void* x
 int64_t resolve_group_size(const omnimoe_dims& d) {
   if (d.group_size > 0) return d.group_size;
   if (d.dtype != OMNIMOE_BF16) return 1;  // fp32 correctness mode: expert-major
+  if (d.v_layout == OMNIMOE_V_SLICED) return 1;  // SLICED pass Z walks an expert-major plan
   // eight grid rows of experts per group, capped so one group's W/V rows (4d bytes
   // per expert) stay within 64 MB of L2 (tools/sweep_group.py)
   const int64_t cap = std::max<int64_t>(1, (64ll << 20) / (4 * d.d));
@@ -851,9 +1175,61 @@ int64_t resolve_token_blocks(const omnimoe_dims& d, int64_t L) {
   return d.token_blocks > 0 ? d.token_blocks : 1;
 }
 
+omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* Vs,
+                                 const omnimoe_plan& plan, float* y, int accumulate, void* ws, cudaStream_t st) {
+  const int64_t n_loc = plan.expert_end - plan.expert_begin;
+  int* work = static_cast<int*>(ws);
+  if (cudaMemsetAsync(work, 0, 2 * sizeof(int), st) != cudaSuccess) {
+    set_error("expert_fwd: memset failed");
+    return OMNIMOE_ERR_CUDA;
+  }
+  const int32_t* m_loc = plan.expert_offsets + n_loc;
+  const int d = (int)dm.d;
+  omnimoe_status s = OMNIMOE_OK;
+  if (resolve_group_size(dm) == 1) {  // expert-major plan: w_e in registers, x from L2
+    switch ((d + 255) / 256) {
+      case 1: s = launch_zdot<1>(d, x, W, plan, dm.act, work, st); break;
+      case 2: s = launch_zdot<2>(d, x, W, plan, dm.act, work, st); break;
+      case 3: s = launch_zdot<3>(d, x, W, plan, dm.act, work, st); break;
+      case 4: s = launch_zdot<4>(d, x, W, plan, dm.act, work, st); break;
+      case 5: s = launch_zdot<5>(d, x, W, plan, dm.act, work, st); break;
+      case 6: s = launch_zdot<6>(d, x, W, plan, dm.act, work, st); break;
+      case 7: s = launch_zdot<7>(d, x, W, plan, dm.act, work, st); break;
+      default: s = launch_zdot<8>(d, x, W, plan, dm.act, work, st); break;
+    }
+  } else switch ((d + 255) / 256) {
+    case 1: s = launch_dot<1>(d, x, W, plan, m_loc, dm.act, work, st); break;
+    case 2: s = launch_dot<2>(d, x, W, plan, m_loc, dm.act, work, st); break;
+    case 3: s = launch_dot<3>(d, x, W, plan, m_loc, dm.act, work, st); break;
+    case 4: s = launch_dot<4>(d, x, W, plan, m_loc, dm.act, work, st); break;
+    case 5: s = launch_dot<5>(d, x, W, plan, m_loc, dm.act, work, st); break;
+    case 6: s = launch_dot<6>(d, x, W, plan, m_loc, dm.act, work, st); break;
+    case 7: s = launch_dot<7>(d, x, W, plan, m_loc, dm.act, work, st); break;
+    default: s = launch_dot<8>(d, x, W, plan, m_loc, dm.act, work, st); break;
+  }
+  OMNI_TRY(s);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_vslice_kernel, 256, 0);
+  per_sm = std::max(1, std::min(per_sm, env_int("OMNIMOE_V_BLOCKS", per_sm)));
+  const int64_t n_tok = plan.n_tokens > 0 ? plan.n_tokens : L;
+  expert_vslice_kernel<<<kSMs * per_sm, 256, 0, st>>>(
+      d, L, n_loc, plan.token_offsets, n_tok, plan.task_pair, static_cast<const __nv_bfloat16*>(Vs), y,
+      accumulate, work + 1, env_int("OMNIMOE_V_HINT", 1));
+  OMNI_CHECK_LAUNCH("expert_vslice_kernel");
+  return OMNIMOE_OK;
+}
+
+omnimoe_status pack_v(int64_t n, int d, const void* V, void* Vs, cudaStream_t st) {
+  if (n == 0) return OMNIMOE_OK;
+  pack_v_kernel<<<kSMs * 8, 256, 0, st>>>(static_cast<const uint4*>(V), static_cast<uint4*>(Vs), n, d);
+  OMNI_CHECK_LAUNCH("pack_v_kernel");
+  return OMNIMOE_OK;
+}
+
 omnimoe_status expert_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W,
                           const void* V, const omnimoe_plan& plan, float* y, int accumulate,
                           void* ws, cudaStream_t st) {
+  if (dm.v_layout == OMNIMOE_V_SLICED) return expert_sliced_run(dm, L, x, W, V, plan, y, accumulate, ws, st);
   if (!accumulate) {
     if (cudaMemsetAsync(y, 0, (size_t)L * dm.d * sizeof(float), st) != cudaSuccess) {
       set_error("expert_fwd: memset failed");

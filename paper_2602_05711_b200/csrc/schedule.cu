@@ -19,13 +19,26 @@ constexpr int kRadixThreads = 256, kRadixRounds = 16, kRadixTile = kRadixThreads
 
 __global__ void hist_keys_kernel(const int32_t* __restrict__ ids, int64_t M, int64_t begin,
                                  int64_t n_loc, uint32_t* __restrict__ keys,
-                                 int32_t* __restrict__ cnt) {
+                                 int32_t* __restrict__ cnt, int32_t* __restrict__ task_pair) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < M;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = (int64_t)ids[t] - begin;
     const bool in = e >= 0 && e < n_loc;
     keys[t] = in ? (uint32_t)e : (uint32_t)n_loc;
+    if (task_pair) task_pair[2 * t] = in ? (int32_t)e : -1;
     if (in) atomicAdd(&cnt[e], 1);
+  }
+}
+
+// token_offsets[l] = first task of token l (tasks sorted by token), for l in
+// [0, n_tokens]; thread t fills the offsets of the tokens in (token(t-1), token(t)].
+__global__ void token_offsets_kernel(int64_t M, const int32_t* __restrict__ token, int64_t hk, int64_t n_tokens,
+                                     int32_t* __restrict__ off) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= M;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cur = t < M ? (token ? (int64_t)token[t] : t / hk) : n_tokens;
+    const int64_t prev = t > 0 ? (token ? (int64_t)token[t - 1] : (t - 1) / hk) : -1;
+    for (int64_t l = prev + 1; l <= cur && l <= n_tokens; ++l) off[l] = (int32_t)t;
   }
 }
 
@@ -240,7 +253,7 @@ __global__ void gather_plan_kernel(const int32_t* __restrict__ order, int64_t M,
                                    const int32_t* __restrict__ token, const float* __restrict__ gate,
                                    const int32_t* __restrict__ ids, int64_t begin, int64_t hk,
                                    int32_t* __restrict__ sorted_token, float* __restrict__ sorted_gate,
-                                   int32_t* __restrict__ sorted_expert) {
+                                   int32_t* __restrict__ sorted_expert, int32_t* __restrict__ sorted_task) {
   const int64_t m_loc = *m_loc_ptr;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m_loc;
        p += (int64_t)gridDim.x * blockDim.x) {
@@ -248,6 +261,7 @@ __global__ void gather_plan_kernel(const int32_t* __restrict__ order, int64_t M,
     sorted_token[p] = token ? token[t] : (int32_t)(t / hk);
     sorted_gate[p] = gate[t];
     sorted_expert[p] = (int32_t)(ids[t] - begin);
+    if (sorted_task) sorted_task[p] = t;
   }
 }
 
@@ -293,8 +307,14 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
     return OMNIMOE_ERR_CUDA;
   }
   if (M > 0) {
-    hist_keys_kernel<<<grid_for(M, 256), 256, 0, st>>>(ids, M, plan.expert_begin, n_loc, k0, cnt);
+    hist_keys_kernel<<<grid_for(M, 256), 256, 0, st>>>(ids, M, plan.expert_begin, n_loc, k0, cnt,
+                                                       plan.task_pair);
     OMNI_CHECK_LAUNCH("hist_keys_kernel");
+  }
+  if (plan.token_offsets) {
+    const int64_t n_tok = plan.n_tokens > 0 ? plan.n_tokens : (M + hk - 1) / hk;
+    token_offsets_kernel<<<grid_for(M + 1, 256), 256, 0, st>>>(M, token, hk, n_tok, plan.token_offsets);
+    OMNI_CHECK_LAUNCH("token_offsets_kernel");
   }
   // a4: offsets (exclusive scan of counts; entry n_loc holds the total m_loc)
   OMNI_TRY(scan<0>(cnt, n_loc + 1, plan.expert_offsets, nullptr, tiles, st));
@@ -333,7 +353,8 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
   }
   const int32_t* m_loc = plan.expert_offsets + n_loc;
   gather_plan_kernel<<<grid_for(M, 256), 256, 0, st>>>(vin, M, m_loc, token, gate, ids, plan.expert_begin, hk,
-                                                      plan.sorted_token, plan.sorted_gate, plan.sorted_expert);
+                                                      plan.sorted_token, plan.sorted_gate, plan.sorted_expert,
+                                                      plan.sorted_task);
   OMNI_CHECK_LAUNCH("gather_plan_kernel");
   if (B > 1) {
     // runs: (group, token) boundaries of the sorted plan, compacted to run_offsets

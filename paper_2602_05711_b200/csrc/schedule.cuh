@@ -17,6 +17,9 @@ omnimoe_status expert_token_run(const omnimoe_dims& dm, int64_t L, const void* x
                                 int accumulate, cudaStream_t st);
 int64_t resolve_token_blocks(const omnimoe_dims& d, int64_t L);
 
+// V [n][d] -> [d/32][n][32] (omnimoe_pack_v)
+omnimoe_status pack_v(int64_t n, int d, const void* V, void* Vs, cudaStream_t st);
+
 size_t expert_ws_bytes(const omnimoe_dims& d, int64_t L);
 omnimoe_status expert_run(const omnimoe_dims& d, int64_t L, const void* x, const void* W,
                           const void* V, const omnimoe_plan& plan, float* y, int accumulate,

@@ -18,7 +18,8 @@ LIB_PATH = os.path.join(_PKG, "libomnimoe.so")
 
 BF16, F32 = 0, 1
 SILU, IDENTITY = 0, 1
-EXPERT_AUTO, EXPERT_WARP, EXPERT_GROUP, EXPERT_TOKEN = 0, 1, 2, 3
+EXPERT_AUTO, EXPERT_WARP, EXPERT_GROUP, EXPERT_TOKEN, EXPERT_SLICED = 0, 1, 2, 3, 4
+V_ROWS, V_SLICED = 0, 1
 ROUTER_EXACT, ROUTER_EXACT_F64 = 0, 1
 LOGITS_ROUTE, LOGITS_EXACT_F64, LOGITS_BF16_FAST = 0, 1, 2
 WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER = 0, 1, 2, 3
@@ -33,7 +34,7 @@ class Dims(ctypes.Structure):
                 ("top_k", ctypes.c_int64), ("n_heads", ctypes.c_int64), ("d_ff", ctypes.c_int64),
                 ("dtype", ctypes.c_int32), ("act", ctypes.c_int32), ("router", ctypes.c_int32),
                 ("expert_kernel", ctypes.c_int32), ("group_size", ctypes.c_int64),
-                ("token_blocks", ctypes.c_int64)]
+                ("token_blocks", ctypes.c_int64), ("v_layout", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class Plan(ctypes.Structure):
@@ -41,14 +42,16 @@ class Plan(ctypes.Structure):
                 ("sorted_gate", ctypes.c_void_p), ("active", ctypes.c_void_p),
                 ("n_active", ctypes.c_void_p), ("expert_begin", ctypes.c_int64),
                 ("expert_end", ctypes.c_int64), ("sorted_expert", ctypes.c_void_p),
-                ("run_offsets", ctypes.c_void_p), ("n_runs", ctypes.c_void_p)]
+                ("run_offsets", ctypes.c_void_p), ("n_runs", ctypes.c_void_p),
+                ("sorted_task", ctypes.c_void_p), ("task_pair", ctypes.c_void_p), ("token_offsets", ctypes.c_void_p),
+                ("n_tokens", ctypes.c_int64)]
 
 
 EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnimoe_expert_fwd",
            "omnimoe_shared_mlp", "omnimoe_layer_fwd", "omnimoe_router_logits", "omnimoe_gemm_bf16",
            "omnimoe_last_launch_count", "omnimoe_status_string", "omnimoe_last_error",
            "omnimoe_group_size", "omnimoe_token_blocks", "omnimoe_ep_pack_workspace_size",
-           "omnimoe_ep_pack", "omnimoe_ep_unpack", "omnimoe_ep_combine"]
+           "omnimoe_ep_pack", "omnimoe_ep_unpack", "omnimoe_ep_combine", "omnimoe_pack_v"]
 
 _lib = None
 
@@ -76,6 +79,7 @@ def load(path: str = LIB_PATH):
         "omnimoe_ep_pack": [PD, I64, I32, V, V, V, V, V, V, V, V, SZ, V],
         "omnimoe_ep_unpack": [I64, I32, V, V, V, V, V, V, V],
         "omnimoe_ep_combine": [PD, I64, I32, V, V, V, V, V],
+        "omnimoe_pack_v": [PD, I64, V, V, V],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -123,6 +127,7 @@ class LayerDims:
     expert_kernel: int = EXPERT_AUTO
     group_size: int = 0
     token_blocks: int = 0
+    v_layout: int = V_ROWS
 
     @property
     def N(self) -> int:
@@ -135,7 +140,7 @@ class LayerDims:
     def c(self) -> Dims:
         return Dims(self.d, self.n_rows, self.n_cols, self.top_k, self.n_heads, self.d_ff,
                     self.dtype, self.act, self.router, self.expert_kernel, self.group_size,
-                    self.token_blocks)
+                    self.token_blocks, self.v_layout, 0)
 
 
 def _ptr(t):
@@ -199,8 +204,14 @@ def token_blocks(dims: LayerDims, L: int) -> int:
     return int(load().omnimoe_token_blocks(ctypes.byref(dc), L))
 
 
-def new_plan(n_loc: int, M: int, device, expert_begin: int = 0):
-    t = dict(expert_offsets=torch.empty(n_loc + 1, dtype=torch.int32, device=device),
+def new_plan(n_loc: int, M: int, device, expert_begin: int = 0, n_tokens: int = 0):
+    """Plan buffers (omnimoe_plan).  n_tokens: tokens of the task list (0: M / (h*K))
+    -- the task-order arrays used by the SLICED executor are always allocated."""
+    t = dict(sorted_task=torch.empty(max(M, 1), dtype=torch.int32, device=device),
+             task_pair=torch.empty((max(M, 1), 2), dtype=torch.int32, device=device),
+             token_offsets=torch.empty(max(n_tokens, M) + 1, dtype=torch.int32, device=device),
+             n_tokens=n_tokens,
+expert_offsets=torch.empty(n_loc + 1, dtype=torch.int32, device=device),
              sorted_token=torch.empty(max(M, 1), dtype=torch.int32, device=device),
              sorted_gate=torch.empty(max(M, 1), dtype=torch.float32, device=device),
              sorted_expert=torch.empty(max(M, 1), dtype=torch.int32, device=device),
@@ -215,11 +226,15 @@ def new_plan(n_loc: int, M: int, device, expert_begin: int = 0):
 def _cplan(p) -> Plan:
     return Plan(p["expert_offsets"].data_ptr(), p["sorted_token"].data_ptr(), p["sorted_gate"].data_ptr(),
                 p["active"].data_ptr(), p["n_active"].data_ptr(), p["expert_begin"], p["expert_end"],
-                p["sorted_expert"].data_ptr(), p["run_offsets"].data_ptr(), p["n_runs"].data_ptr())
+                p["sorted_expert"].data_ptr(), p["run_offsets"].data_ptr(), p["n_runs"].data_ptr(),
+                p["sorted_task"].data_ptr(), p["task_pair"].data_ptr(),
+                p["token_offsets"].data_ptr(), p["n_tokens"])
 
 
-def schedule(dims: LayerDims, idx, gate, token=None, expert_begin=0, expert_end=None, plan=None, ws=None):
-    """Expert-centric plan (a4 + a5) of the tasks (idx, gate) over the expert range."""
+def schedule(dims: LayerDims, idx, gate, token=None, expert_begin=0, expert_end=None, plan=None, ws=None,
+             n_tokens=0):
+    """Expert-centric plan (a4 + a5) of the tasks (idx, gate) over the expert range.
+    n_tokens: number of tokens when `token` is given (tasks sorted by token)."""
     M = idx.numel()
     _req(idx, "idx", torch.int32)
     _req(gate, "gate", torch.float32, M)
@@ -227,13 +242,23 @@ def schedule(dims: LayerDims, idx, gate, token=None, expert_begin=0, expert_end=
         _req(token, "token", torch.int32, M)
     expert_end = dims.N if expert_end is None else expert_end
     n_loc = expert_end - expert_begin
-    plan = plan or new_plan(n_loc, M, idx.device, expert_begin)
+    plan = plan or new_plan(n_loc, M, idx.device, expert_begin, n_tokens)
     ws = ws if ws is not None else torch.empty(max(workspace_size(dims, M, WS_SCHEDULE), 1),
                                                dtype=torch.uint8, device=idx.device)
     dc, cp = dims.c(), _cplan(plan)
     _check(load().omnimoe_schedule(ctypes.byref(dc), M, _ptr(idx), _ptr(gate), _ptr(token),
                                    ctypes.byref(cp), _ptr(ws), ws.numel(), _stream()), "schedule")
     return plan
+
+
+def pack_v(dims: LayerDims, V):
+    """V [n][d] -> the SLICED layout [d/32][n][32] (include/omnimoe.h omnimoe_pack_v)."""
+    n = V.numel() // dims.d
+    _req(V, "V", dims.torch_dtype, n * dims.d)
+    out = torch.empty((dims.d // 32, n, 32), dtype=V.dtype, device=V.device)
+    dc = dims.c()
+    _check(load().omnimoe_pack_v(ctypes.byref(dc), n, _ptr(V), _ptr(out), _stream()), "pack_v")
+    return out
 
 
 def expert_fwd(dims: LayerDims, x, W_loc, V_loc, plan, y_routed=None, accumulate=False, ws=None):

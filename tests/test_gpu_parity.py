@@ -381,3 +381,125 @@ def test_layer_ablation_executors(ek):
                        hr("w_gate_up"), hr("w_down"))
     e_tok, e_elt = rel_errors(y.float().cpu().numpy(), ref["y"])
     assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+
+
+# ---------------------------------------------------------------- SLICED executor (V_SLICED layout)
+def test_pack_v_is_a_pure_relayout():
+    dims = om.LayerDims(d=2048, n_rows=37, n_cols=11, top_k=4, v_layout=om.V_SLICED)
+    inp = make_inputs(dims, 1, 5, skip=("x", "subkeys", "W"))
+    Vs = om.pack_v(dims, inp["V"])
+    torch.cuda.synchronize()
+    want = inp["V"].view(dims.N, dims.d // 32, 32).permute(1, 0, 2).contiguous()  # test-side re-layout
+    assert torch.equal(Vs.view(torch.int16), want.view(torch.int16))
+
+
+@pytest.mark.parametrize("B", [0, 2, 512])
+@pytest.mark.parametrize("d,act", [(64, om.SILU), (96, om.SILU), (1024, om.SILU), (2048, om.SILU),
+                                   (64, om.IDENTITY)])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_expert_fwd_sliced_given_plan(d, act, B, accumulate):
+    rng = np.random.default_rng(d + B)
+    L, N, HK = 200, 3000, 12
+    dims = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, act=act, group_size=B, v_layout=om.V_SLICED)
+    inp = make_inputs(dims, L, 9, skip=("subkeys",))
+    base = rng.integers(0, N - 64, L)
+    ids = np.stack([b0 + rng.choice(64, HK, replace=False) for b0 in base]).astype(np.int32)
+    ids[7] = ids[3]  # two tokens with identical expert lists
+    gates = rng.random((L, HK)).astype(np.float32)
+    plan = om.schedule(dims, torch.from_numpy(ids).cuda().reshape(-1), torch.from_numpy(gates).cuda().reshape(-1))
+    Vs = om.pack_v(dims, inp["V"])
+    y0 = torch.randn(L, d, device="cuda") if accumulate else None
+    y = om.expert_fwd(dims, inp["x"], inp["W"], Vs, plan, y_routed=None if y0 is None else y0.clone(),
+                      accumulate=accumulate)
+    torch.cuda.synchronize()
+    used = np.unique(ids)
+    remap = np.searchsorted(used, ids)
+    x = host_rows(dims, 9, "x", np.arange(L))
+    ref = oracle.routed_token_centric(x, host_rows(dims, 9, "W", used), host_rows(dims, 9, "V", used), remap,
+                                      gates.astype(np.float64), act)
+    if accumulate:
+        ref = ref + y0.cpu().double().numpy()
+    e_tok, e_elt = rel_errors(y.cpu().numpy(), ref)
+    assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+
+
+def test_expert_fwd_sliced_shard_and_empty_tokens():
+    """Expert range of a shard (tasks outside it are skipped) and tokens with no
+    tasks in range (their y_routed rows are written as zeros)."""
+    rng = np.random.default_rng(3)
+    L, N, HK, b, e = 150, 4096, 8, 1024, 2048
+    dims = om.LayerDims(d=256, n_rows=N, n_cols=1, top_k=HK, d_ff=0, group_size=64, v_layout=om.V_SLICED)
+    inp = make_inputs(dims, L, 4, skip=("subkeys",))
+    ids = rng.integers(0, N, (L, HK)).astype(np.int32)
+    ids[10] = rng.integers(3000, N, HK)  # token 10: nothing in [b, e)
+    gates = rng.random((L, HK)).astype(np.float32)
+    plan = om.schedule(dims, torch.from_numpy(ids).cuda().reshape(-1), torch.from_numpy(gates).cuda().reshape(-1),
+                       expert_begin=b, expert_end=e)
+    Vs = om.pack_v(dims, inp["V"][b:e].contiguous())
+    y = om.expert_fwd(dims, inp["x"], inp["W"][b:e].contiguous(), Vs, plan)
+    torch.cuda.synchronize()
+    x = host_rows(dims, 4, "x", np.arange(L))
+    mask = (ids >= b) & (ids < e)
+    used = np.arange(b, e)
+    remap = np.where(mask, ids - b, 0)
+    g = np.where(mask, gates, 0).astype(np.float64)
+    ref = oracle.routed_token_centric(x, host_rows(dims, 4, "W", used), host_rows(dims, 4, "V", used), remap, g)
+    assert np.all(y[10].cpu().numpy() == 0)
+    e_tok, e_elt = rel_errors(np.delete(y.cpu().numpy(), 10, 0), np.delete(ref, 10, 0))
+    assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+
+
+@pytest.mark.parametrize("mode", [synth.NORMAL, synth.DYADIC])
+@pytest.mark.parametrize("B", [0, 5])
+def test_layer_c1_sliced(mode, B):
+    w = _dims("C1", group_size=B, v_layout=om.V_SLICED)
+    dims = w.dims
+    inp = make_inputs(dims, w.L, w.seed, mode)
+    Vs = om.pack_v(dims, inp["V"])
+    y, idx, gate = om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], Vs, inp["w_gate_up"], inp["w_down"],
+                                return_routing=True)
+    y2 = om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], Vs, inp["w_gate_up"], inp["w_down"])
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2)  # no atomics on the SLICED path: bitwise deterministic
+    hr = lambda n, r=None: host_rows(dims, w.seed, n, r, mode)
+    ref = oracle.layer(hr("x", np.arange(w.L)), hr("subkeys").reshape(1, -1, dims.d), hr("W"), hr("V"),
+                       dims.n_rows, dims.n_cols, dims.top_k, hr("w_gate_up"), hr("w_down"))
+    assert np.array_equal(np.sort(idx.cpu().numpy(), -1), np.sort(ref["idx"], -1))
+    e_tok, e_elt = rel_errors(y.float().cpu().numpy(), ref["y"])
+    assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+
+
+@pytest.mark.parametrize("name", ["C3a", "C3b", "C4"])
+def test_layer_full_size_sampled_sliced(name):
+    """The bench configuration (V in the SLICED layout) at full size; sampled
+    tokens recomputed by the oracle."""
+    w = _dims(name, v_layout=om.V_SLICED)
+    dims = w.dims
+    inp = make_inputs(dims, w.L, w.seed)
+    inp["V"] = om.pack_v(dims, inp["V"])
+    y, idx, gate = om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], inp["V"], inp["w_gate_up"],
+                                inp["w_down"], return_routing=True)
+    torch.cuda.synchronize()
+    toks = np.array([0, 1, 777, w.L // 2 + 3, w.L - 2, w.L - 1])
+    hr = lambda n, r=None: host_rows(dims, w.seed, n, r)
+    x = hr("x", toks)
+    sub = hr("subkeys").reshape(dims.n_heads, -1, dims.d)
+    lg = oracle.logits(x, sub)
+    r = oracle.route(lg.reshape(len(toks) * dims.n_heads, -1), dims.n_rows, dims.n_cols, dims.top_k)
+    np.testing.assert_array_equal(np.sort(idx[toks].cpu().numpy().reshape(-1, dims.top_k), -1),
+                                  np.sort(r["idx"], -1))
+    used = np.unique(r["idx"])
+    idm = np.stack([used, np.arange(len(used))], 1)
+    ref = oracle.layer(x, sub, hr("W", used), hr("V", used), dims.n_rows, dims.n_cols, dims.top_k,
+                       hr("w_gate_up"), hr("w_down"), id_map=idm)
+    e_tok, e_elt = rel_errors(y[toks].float().cpu().numpy(), ref["y"])
+    assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+
+
+def test_sliced_layout_errors():
+    with pytest.raises(om.OmniMoEError, match="UNSUPPORTED"):
+        om.workspace_size(om.LayerDims(d=64, n_rows=4, n_cols=4, top_k=2, dtype=om.F32, v_layout=om.V_SLICED), 8,
+                          om.WS_LAYER)
+    with pytest.raises(om.OmniMoEError, match="INVALID_ARGUMENT"):
+        om.workspace_size(om.LayerDims(d=64, n_rows=4, n_cols=4, top_k=2, expert_kernel=om.EXPERT_SLICED), 8,
+                          om.WS_LAYER)

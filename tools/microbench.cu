@@ -62,6 +62,37 @@ __global__ void ffma_rate(float* out, int iters) {
   if (s == 1234.5f) out[0] = s;
 }
 
+
+// 128-byte pieces (8 lanes x 16 B) at byte offset `off` of random rows: the access
+// pattern of a slice-major pass over an expert table (4 pieces per warp instruction)
+__global__ void piece_gather(const uint4* __restrict__ tab, int nrows, int row_vec, int off_vec, int n_per_warp,
+                             uint32_t salt, uint4* sink) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll 4
+  for (int k = 0; k < n_per_warp; k += 4) {
+    uint32_t r = hash32((gw * 7919u + k + (lane >> 3)) ^ salt) % nrows;
+    uint4 v = tab[(size_t)r * row_vec + off_vec + (lane & 7)];
+    acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
+  }
+  if (acc.x == 0x12345678u) sink[0] = acc;
+}
+
+// 64-byte pieces (4 lanes x 16 B), 8 per warp instruction
+__global__ void piece64_gather(const uint4* __restrict__ tab, int nrows, int n_per_warp, uint32_t salt, uint4* sink) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll 4
+  for (int k = 0; k < n_per_warp; k += 8) {
+    uint32_t r = hash32((gw * 7919u + k + (lane >> 2)) ^ salt) & (nrows - 1);
+    uint4 v = tab[(size_t)r * 4 + (lane & 3)];
+    acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
+  }
+  if (acc.x == 0x12345678u) sink[0] = acc;
+}
+
 template <class F>
 float time_ms(F f, int reps = 5) {
   cudaEvent_t a, b;
@@ -103,6 +134,38 @@ int main() {
     int rows = (int)(tb / 8192);
     ms = time_ms([&] { red_scatter<<<nw / 8, 256>>>(tab, rows, 2048, 16); });
     printf(", \"red_v4_scatter_8KB_rows_%zuMB_gbs\": %.1f", tb >> 20, (double)nw * 16 * 8192 / ms / 1e6);
+  }
+
+  // slice-pass pattern: 128 B pieces of random rows among 524288 rows of 4 KB (67 MB of lines)
+  {
+    const int prow = 524288, pnpw = 1024, pw = sms * 64;
+    ms = time_ms([&] { piece_gather<<<pw / 8, 256>>>(big, prow, 256, 0, pnpw, 0u, sink); });
+    printf(", \"l2_piece128_gather_67MB_gbs\": %.1f", (double)pw * pnpw * 128 / ms / 1e6);
+    // the same over 1M rows (134 MB of lines: exceeds L2)
+    ms = time_ms([&] { piece_gather<<<pw / 8, 256>>>(big, 1 << 20, 256, 0, pnpw, 0u, sink); });
+    printf(", \"piece128_gather_134MB_gbs\": %.1f", (double)pw * pnpw * 128 / ms / 1e6);
+    // a sweep of 32 slices (cold first touch of each slice), 4.2M pieces per slice
+    const int npw2 = 4 * 1048576 / pw;
+    ms = time_ms([&] {
+      for (int s = 0; s < 32; ++s) piece_gather<<<pw / 8, 256>>>(big, prow, 256, s * 8, npw2, 77u * s, sink);
+    }, 3);
+    printf(", \"piece128_slice_sweep_gbs\": %.1f, \"piece128_slice_sweep_ms\": %.3f",
+           (double)pw * npw2 * 32 * 128 / ms / 1e6, ms);
+
+    // the same pieces packed contiguously (slice-major layout: 67 MB span, within TLB reach)
+    ms = time_ms([&] { piece_gather<<<pw / 8, 256>>>(big, prow, 8, 0, pnpw, 0u, sink); });
+    printf(", \"l2_piece128_packed_67MB_gbs\": %.1f", (double)pw * pnpw * 128 / ms / 1e6);
+    ms = time_ms([&] {
+      for (int s = 0; s < 32; ++s) piece_gather<<<pw / 8, 256>>>(big + (size_t)s * prow * 8, prow, 8, 0, npw2, 77u * s, sink);
+    }, 3);
+    printf(", \"piece128_packed_sweep_gbs\": %.1f, \"piece128_packed_sweep_ms\": %.3f",
+           (double)pw * npw2 * 32 * 128 / ms / 1e6, ms);
+    ms = time_ms([&] { piece64_gather<<<pw / 8, 256>>>(big, 1 << 20, pnpw * 2, 0u, sink); });
+    printf(", \"l2_piece64_packed_67MB_gbs\": %.1f", (double)pw * pnpw * 2 * 64 / ms / 1e6);
+    ms = time_ms([&] {
+      for (int s = 0; s < 32; ++s) piece64_gather<<<pw / 8, 256>>>(big + (size_t)s * (1 << 20) * 4, 1 << 20, npw2 * 2, 77u * s, sink);
+    }, 3);
+    printf(", \"piece64_packed_sweep_gbs\": %.1f", (double)pw * npw2 * 2 * 32 * 64 / ms / 1e6);
   }
   // FFMA rate
   float* o; CK(cudaMalloc(&o, 64));
