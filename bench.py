@@ -204,6 +204,7 @@ def bench_single(args, w, lr):
     from synth.workloads import make_inputs
     dims, L = w.dims, w.L
     inp = make_inputs(dims, L, w.seed)
+    oinp = dict(inp)  # the oracle sample reads expert rows in the [N][d] layout
     if dims.v_layout == om.V_SLICED:  # one-time weight re-layout (not part of a step)
         inp["V"] = om.pack_v(dims, inp["V"])
         torch.cuda.synchronize()
@@ -244,7 +245,7 @@ def bench_single(args, w, lr):
     # ---- per-stage breakdown through the individual C-ABI calls (same inputs) ----
     M = L * dims.n_heads * dims.top_k
     rws = om.workspace(dims, L, om.WS_ROUTE)
-    plan = om.new_plan(dims.N, M, "cuda")
+    plan = om.new_plan(dims.N, M, "cuda", dims=dims)
     sws = om.workspace(dims, M, om.WS_SCHEDULE)
     ews = om.workspace(dims, L, om.WS_EXPERT)
     yr = torch.empty((L, dims.d), dtype=torch.float32, device="cuda")
@@ -322,7 +323,7 @@ def bench_single(args, w, lr):
     cpu = None
     if not args.no_cpu_baseline:
         nth = os.cpu_count() or 1
-        rate, done, t = cpu_oracle_rate(w, args.cpu_seconds, 1 << 20, nth, inp)
+        rate, done, t = cpu_oracle_rate(w, args.cpu_seconds, 1 << 20, nth, oinp)
         cpu = {"value": rate, "unit": "tokens/s", "cores": nth, "kind": "oracle",
                "sample": f"{done} tokens of {w.name} (oracle layer: exact logits, product top-K, token-centric "
                          f"routed branch, shared MLP): {t:.1f} s of oracle time on {nth} threads"}

@@ -125,13 +125,19 @@ typedef struct {
  *   run_offsets    int32[M+1]      B > 1 only (nullable for B = 1): first task of
  *                                  each run = the tasks of one token in one group
  *   n_runs         int32[1]        B > 1 only: number of runs P
- * Task-order arrays (nullable; required by the SLICED executor; tasks must be
- * sorted by token, which the default token = t / (h*K) is):
- *   sorted_task    int32[M]        task index t of each plan position
- *   task_pair      int32[M][2]     task t: (local expert id, -1 outside the range;
- *                                  bits of a_t = g*sigma(z), scratch of the SLICED executor)
- *   token_offsets  int32[n_tokens+1]  first task of each token
- *   n_tokens       number of tokens (input; 0: ceil(M / (h*K)))
+ * V-order arrays (nullable; required by the SLICED executor; tasks must be
+ * sorted by token, which the default token = t / (h*K) is).  The V order sorts
+ * the tasks by (token, band) stably, band = local expert id / ceil(n_loc / n_b)
+ * with n_b = omnimoe_v_bands(dims, n_loc) (band n_b: outside the range; with
+ * n_b = 1 the V order is the task order and out-of-range tasks stay in segment
+ * (l, 0) with expert -1):
+ *   sorted_task     int32[M]        V-order position of each plan position's task
+ *   task_pair       int32[M][2]     per V-order position: (local expert id, -1
+ *                                   outside the range; bits of a = g*sigma(z), the
+ *                                   scratch of the SLICED executor)
+ *   token_offsets   int32[n_tokens*(n_b+1)+1]  start of segment (l, b) at entry
+ *                                   l*(n_b+1) + b
+ *   n_tokens        number of tokens (input; 0: ceil(M / (h*K)))
  * For B = 1 the segment of local expert e is [expert_offsets[e],
  * expert_offsets[e+1]) with tokens ascending.  Only the first
  * m_loc entries of sorted_* are meaningful (tasks outside the range are not
@@ -156,6 +162,11 @@ typedef struct {
  * (dims.group_size if > 0, else the library's choice: 8*N_c experts, at most
  * 64 MB of W/V rows, in bf16 mode; 1 in fp32 mode).  Returns 0 on invalid dims. */
 int64_t omnimoe_group_size(const omnimoe_dims* dims);
+/* Number of expert bands n_b of the SLICED executor's pass V for a local expert
+ * range of n_loc rows: the V rows of one band and one 32-column slice (64 bytes
+ * each) are kept near 32 MB so that they stay L2-resident while every token uses
+ * them.  1 for the ROWS layout; 0 on invalid dims. */
+int64_t omnimoe_v_bands(const omnimoe_dims* dims, int64_t n_loc);
 /* The number of token blocks T_b omnimoe_schedule uses for a batch of L tokens
  * (dims.token_blocks if > 0, else 1; always 1 for B = 1).  Block b holds tokens
  * [b*ceil(L/T_b), (b+1)*ceil(L/T_b)); the plan sorts by (block, q, token). */

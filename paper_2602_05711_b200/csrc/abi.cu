@@ -169,7 +169,7 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
   const bool sliced = d.v_layout == OMNIMOE_V_SLICED;
   int32_t* stask = sliced ? c.take<int32_t>((size_t)std::max<int64_t>(M, 1)) : nullptr;
   int32_t* tpair = sliced ? c.take<int32_t>(2 * (size_t)std::max<int64_t>(M, 1)) : nullptr;
-  int32_t* toff = sliced ? c.take<int32_t>((size_t)L + 1) : nullptr;
+  int32_t* toff = sliced ? c.take<int32_t>((size_t)L * (resolve_v_bands(d, N) + 1) + 1) : nullptr;
   const size_t sb = schedule_ws_bytes(M, N);
   void* sw = c.take<char>(sb);
   float* yr = c.take<float>((size_t)L * d.d);
@@ -343,7 +343,8 @@ omnimoe_status omnimoe_schedule(const omnimoe_dims* dims, int64_t M, const int32
   OMNI_TRY(check_ws(ws_bytes, schedule_ws_bytes(M, n_loc), "schedule"));
   OMNI_TRY(check_device());
   const int64_t hk = dims->n_heads * dims->top_k;
-  return schedule_run(M, idx, gate, token, hk, *plan, B, resolve_token_blocks(*dims, (M + hk - 1) / hk), ws,
+  return schedule_run(M, idx, gate, token, hk, *plan, B, resolve_token_blocks(*dims, (M + hk - 1) / hk),
+                      resolve_v_bands(*dims, n_loc), ws,
                       (cudaStream_t)stream);
 }
 
@@ -446,7 +447,7 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
     OMNI_TRY(expert_token_run(d, L, x, W, V, idx, gate, 0, d.n_rows * d.n_cols, w.y_routed, 0, st));
   } else {
     OMNI_TRY(schedule_run(M, idx, gate, nullptr, d.n_heads * d.top_k, w.plan, resolve_group_size(d),
-                          resolve_token_blocks(d, L), w.sched_ws, st));
+                          resolve_token_blocks(d, L), resolve_v_bands(d, d.n_rows * d.n_cols), w.sched_ws, st));
     OMNI_TRY(expert_run(d, L, x, W, V, w.plan, w.y_routed, 0, w.expert_ws, st));
   }
   if (d.d_ff > 0) {
@@ -620,6 +621,11 @@ int omnimoe_last_launch_count(void) { return g_launches; }
 int64_t omnimoe_group_size(const omnimoe_dims* dims) {
   if (validate_dims(dims) != OMNIMOE_OK) return 0;
   return resolve_group_size(*dims);
+}
+
+int64_t omnimoe_v_bands(const omnimoe_dims* dims, int64_t n_loc) {
+  if (validate_dims(dims) != OMNIMOE_OK || n_loc < 1) return 0;
+  return resolve_v_bands(*dims, n_loc);
 }
 
 int64_t omnimoe_token_blocks(const omnimoe_dims* dims, int64_t L) {

@@ -917,9 +917,10 @@ __device__ __forceinline__ int2 ld_pair(const int32_t* p, uint64_t pol) {
 // The (expert, a) pairs of the next 64 tasks -- possibly of the next item, which
 // is claimed one item ahead -- are loaded while the current 64 are processed.
 __global__ void __launch_bounds__(256)
-    expert_vslice_kernel(int d, int64_t L, int64_t n_loc, const int32_t* __restrict__ tok_off, int64_t n_tok,
-                         const int32_t* __restrict__ task_pair, const __nv_bfloat16* __restrict__ Vs,
-                         float* __restrict__ y, int accumulate, int* __restrict__ work, int stream_hint) {
+    expert_vslice_kernel(int d, int64_t L, int64_t n_loc, const int32_t* __restrict__ seg, int seg_stride,
+                         int band, int64_t n_tok, const int32_t* __restrict__ task_pair,
+                         const __nv_bfloat16* __restrict__ Vs, float* __restrict__ y, int accumulate,
+                         int* __restrict__ work, int stream_hint) {
   const int lane = threadIdx.x & 31, c4 = lane & 3, g8 = lane >> 2;
   const int S = d / 32;
   const int64_t n_items = (int64_t)S * L;
@@ -935,8 +936,8 @@ __global__ void __launch_bounds__(256)
     if (item < n_items) {
       const int64_t l = item % L;
       if (l < n_tok) {
-        beg = tok_off[l];
-        end = tok_off[l + 1];
+        beg = seg[l * seg_stride + band];
+        end = seg[l * seg_stride + band + 1];
       }
     }
   };
@@ -1167,6 +1168,15 @@ int64_t resolve_group_size(const omnimoe_dims& d) {
   return std::max<int64_t>(2, std::min<int64_t>(8 * d.n_cols, cap));
 }
 
+int64_t resolve_v_bands(const omnimoe_dims& d, int64_t n_loc) {
+  if (d.v_layout != OMNIMOE_V_SLICED || n_loc < 1) return 1;
+  // one band x one 32-column slice of V = 64 bytes per expert row, kept <= 64 MB:
+  // at C3a (67 MB per slice) 1 and 2 bands run equally fast (pass V is bound by L2
+  // throughput either way), 4 bands are slower (profiles/r1/README.md)
+  const int64_t target = (int64_t)std::max(1, env_int("OMNIMOE_V_BAND_KB", 68 << 10)) << 10;
+  return std::max<int64_t>(1, std::min<int64_t>(32, (n_loc * 64 + target - 1) / target));
+}
+
 int64_t resolve_token_blocks(const omnimoe_dims& d, int64_t L) {
   if (resolve_group_size(d) == 1) return 1;
   (void)L;
@@ -1179,7 +1189,7 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
                                  const omnimoe_plan& plan, float* y, int accumulate, void* ws, cudaStream_t st) {
   const int64_t n_loc = plan.expert_end - plan.expert_begin;
   int* work = static_cast<int*>(ws);
-  if (cudaMemsetAsync(work, 0, 2 * sizeof(int), st) != cudaSuccess) {
+  if (cudaMemsetAsync(work, 0, 64 * sizeof(int), st) != cudaSuccess) {
     set_error("expert_fwd: memset failed");
     return OMNIMOE_ERR_CUDA;
   }
@@ -1212,10 +1222,16 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_vslice_kernel, 256, 0);
   per_sm = std::max(1, std::min(per_sm, env_int("OMNIMOE_V_BLOCKS", per_sm)));
   const int64_t n_tok = plan.n_tokens > 0 ? plan.n_tokens : L;
-  expert_vslice_kernel<<<kSMs * per_sm, 256, 0, st>>>(
-      d, L, n_loc, plan.token_offsets, n_tok, plan.task_pair, static_cast<const __nv_bfloat16*>(Vs), y,
-      accumulate, work + 1, env_int("OMNIMOE_V_HINT", 1));
-  OMNI_CHECK_LAUNCH("expert_vslice_kernel");
+  const int nb = (int)resolve_v_bands(dm, n_loc);
+  // one launch per expert band: its slices of V stay L2-resident while all tokens
+  // use them; band b > 0 adds to the slices band b - 1 wrote (stream order: the
+  // summation order is fixed, the result bitwise deterministic)
+  for (int b = 0; b < nb; ++b) {
+    expert_vslice_kernel<<<kSMs * per_sm, 256, 0, st>>>(
+        d, L, n_loc, plan.token_offsets, nb + 1, b, n_tok, plan.task_pair, static_cast<const __nv_bfloat16*>(Vs),
+        y, b > 0 ? 1 : accumulate, work + 1 + b, env_int("OMNIMOE_V_HINT", 1));
+    OMNI_CHECK_LAUNCH("expert_vslice_kernel");
+  }
   return OMNIMOE_OK;
 }
 

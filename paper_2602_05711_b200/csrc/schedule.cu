@@ -17,6 +17,58 @@ namespace {
 constexpr int kScanThreads = 256, kScanItems = 16, kScanTile = kScanThreads * kScanItems;
 constexpr int kRadixThreads = 256, kRadixRounds = 16, kRadixTile = kRadixThreads * kRadixRounds;
 
+// V order (SLICED executor): one warp per token stably partitions the token's
+// tasks by band b = e / band_size (b = nb outside the local range); dest[t] = the
+// task's V-order position, task_pair[dest].x = its local expert id (-1 outside),
+// seg[l*(nb+1) + b] = start of segment (l, b).
+__global__ void band_partition_kernel(const int32_t* __restrict__ ids, int64_t begin, int64_t n_loc,
+                                      const int32_t* __restrict__ tok_off, int64_t n_tok, int nb, int64_t band_size,
+                                      int32_t* __restrict__ dest, int32_t* __restrict__ task_pair,
+                                      int32_t* __restrict__ seg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  if (gw == 0 && lane == 0) seg[n_tok * (nb + 1)] = tok_off[n_tok];
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t l = gw; l < n_tok; l += nw) {
+    const int beg = tok_off[l], end = tok_off[l + 1];
+    auto band_of = [&](int t) {
+      const int64_t e = (int64_t)ids[t] - begin;
+      return (e >= 0 && e < n_loc) ? (int)(e / band_size) : nb;
+    };
+    int cnt = 0;  // lane b < nb+1 counts band b
+    for (int t0 = beg; t0 < end; t0 += 32) {
+      const int b = t0 + lane < end ? band_of(t0 + lane) : nb + 1;
+      for (int q = 0; q <= nb; ++q) {
+        const int c = __popc(__ballot_sync(0xffffffffu, b == q));
+        if (lane == q) cnt += c;
+      }
+    }
+    int incl = cnt;  // exclusive prefix over lanes 0..nb
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int pos = beg + incl - cnt;  // lane q: next position of band q
+    if (lane <= nb) seg[l * (nb + 1) + lane] = pos;
+    for (int t0 = beg; t0 < end; t0 += 32) {
+      const int t = t0 + lane;
+      const int b = t < end ? band_of(t) : nb + 1;
+      int q_pos = 0;
+      for (int q = 0; q <= nb; ++q) {
+        const unsigned m = __ballot_sync(0xffffffffu, b == q);
+        const int base = __shfl_sync(0xffffffffu, pos, q);
+        if (b == q) q_pos = base + __popc(m & lt);
+        if (lane == q) pos += __popc(m);
+      }
+      if (t < end) {
+        dest[t] = q_pos;
+        task_pair[2 * (size_t)q_pos] = b < nb ? (int32_t)(ids[t] - begin) : -1;
+      }
+    }
+  }
+}
+
 __global__ void hist_keys_kernel(const int32_t* __restrict__ ids, int64_t M, int64_t begin,
                                  int64_t n_loc, uint32_t* __restrict__ keys,
                                  int32_t* __restrict__ cnt, int32_t* __restrict__ task_pair) {
@@ -25,20 +77,25 @@ __global__ void hist_keys_kernel(const int32_t* __restrict__ ids, int64_t M, int
     const int64_t e = (int64_t)ids[t] - begin;
     const bool in = e >= 0 && e < n_loc;
     keys[t] = in ? (uint32_t)e : (uint32_t)n_loc;
-    if (task_pair) task_pair[2 * t] = in ? (int32_t)e : -1;
+    if (task_pair) task_pair[2 * t] = in ? (int32_t)e : -1;  // one band: V order = task order
     if (in) atomicAdd(&cnt[e], 1);
   }
 }
 
-// token_offsets[l] = first task of token l (tasks sorted by token), for l in
+// off[l * stride] = first task of token l (tasks sorted by token), for l in
 // [0, n_tokens]; thread t fills the offsets of the tokens in (token(t-1), token(t)].
+// stride 2 (one band): off[2l + 1] = off[2(l+1)] too, i.e. segment (l, 0) is the
+// whole token and segment (l, 1) (outside the range) is empty.
 __global__ void token_offsets_kernel(int64_t M, const int32_t* __restrict__ token, int64_t hk, int64_t n_tokens,
-                                     int32_t* __restrict__ off) {
+                                     int32_t* __restrict__ off, int stride) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= M;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t cur = t < M ? (token ? (int64_t)token[t] : t / hk) : n_tokens;
     const int64_t prev = t > 0 ? (token ? (int64_t)token[t - 1] : (t - 1) / hk) : -1;
-    for (int64_t l = prev + 1; l <= cur && l <= n_tokens; ++l) off[l] = (int32_t)t;
+    for (int64_t l = prev + 1; l <= cur && l <= n_tokens; ++l) {
+      off[l * stride] = (int32_t)t;
+      if (stride == 2 && l > 0) off[2 * l - 1] = (int32_t)t;
+    }
   }
 }
 
@@ -253,7 +310,8 @@ __global__ void gather_plan_kernel(const int32_t* __restrict__ order, int64_t M,
                                    const int32_t* __restrict__ token, const float* __restrict__ gate,
                                    const int32_t* __restrict__ ids, int64_t begin, int64_t hk,
                                    int32_t* __restrict__ sorted_token, float* __restrict__ sorted_gate,
-                                   int32_t* __restrict__ sorted_expert, int32_t* __restrict__ sorted_task) {
+                                   int32_t* __restrict__ sorted_expert, int32_t* __restrict__ sorted_task,
+                                   const int32_t* __restrict__ dest) {
   const int64_t m_loc = *m_loc_ptr;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m_loc;
        p += (int64_t)gridDim.x * blockDim.x) {
@@ -261,7 +319,7 @@ __global__ void gather_plan_kernel(const int32_t* __restrict__ order, int64_t M,
     sorted_token[p] = token ? token[t] : (int32_t)(t / hk);
     sorted_gate[p] = gate[t];
     sorted_expert[p] = (int32_t)(ids[t] - begin);
-    if (sorted_task) sorted_task[p] = t;
+    if (sorted_task) sorted_task[p] = dest ? dest[t] : t;
   }
 }
 
@@ -282,12 +340,14 @@ size_t schedule_ws_bytes(int64_t M, int64_t n_loc) {
   c.take<int32_t>(256 * nb);                                  // radix hist
   const int64_t scan_n = std::max<int64_t>(std::max<int64_t>(n_loc + 1, 256 * nb), M);
   c.take<int32_t>((scan_n + kScanTile - 1) / kScanTile + 1);  // tile sums
+  c.take<int32_t>(M + 2);                                     // per-token task offsets (V order)
+  c.take<int32_t>(std::max<int64_t>(M, 1));                   // V-order destination of each task
   return c.bytes();
 }
 
 omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, const int32_t* token,
-                            int64_t hk, const omnimoe_plan& plan, int64_t B, int64_t Tb, void* ws,
-                            cudaStream_t st) {
+                            int64_t hk, const omnimoe_plan& plan, int64_t B, int64_t Tb, int64_t n_bands,
+                            void* ws, cudaStream_t st) {
   const int64_t n_loc = plan.expert_end - plan.expert_begin;
   const int64_t nb = (M + kRadixTile - 1) / kRadixTile;
   Carver c(ws);
@@ -300,6 +360,9 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
   int32_t* hist = c.take<int32_t>(256 * nb);
   const int64_t scan_n = std::max<int64_t>(std::max<int64_t>(n_loc + 1, 256 * nb), M);
   int32_t* tiles = c.take<int32_t>((scan_n + kScanTile - 1) / kScanTile + 1);
+  int32_t* tok_off = c.take<int32_t>(M + 2);
+  int32_t* dest = c.take<int32_t>(std::max<int64_t>(M, 1));
+  const bool vorder = plan.task_pair && plan.token_offsets && plan.sorted_task;
 
   if (cudaMemsetAsync(cnt, 0, (n_loc + 1) * sizeof(int32_t), st) != cudaSuccess ||
       (B > 1 && cudaMemsetAsync(plan.n_runs, 0, sizeof(int32_t), st) != cudaSuccess)) {
@@ -308,13 +371,27 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
   }
   if (M > 0) {
     hist_keys_kernel<<<grid_for(M, 256), 256, 0, st>>>(ids, M, plan.expert_begin, n_loc, k0, cnt,
-                                                       plan.task_pair);
+                                                       vorder && n_bands == 1 ? plan.task_pair : nullptr);
     OMNI_CHECK_LAUNCH("hist_keys_kernel");
   }
-  if (plan.token_offsets) {
+  if (vorder) {  // the SLICED executor's (token, band) order
     const int64_t n_tok = plan.n_tokens > 0 ? plan.n_tokens : (M + hk - 1) / hk;
-    token_offsets_kernel<<<grid_for(M + 1, 256), 256, 0, st>>>(M, token, hk, n_tok, plan.token_offsets);
-    OMNI_CHECK_LAUNCH("token_offsets_kernel");
+    if (n_tok > M + 1) {
+      set_error("schedule: n_tokens larger than the task count + 1 is not supported");
+      return OMNIMOE_ERR_SHAPE;
+    }
+    if (n_bands == 1) {  // V order = task order; out-of-range tasks carry expert -1
+      token_offsets_kernel<<<grid_for(M + 1, 256), 256, 0, st>>>(M, token, hk, n_tok, plan.token_offsets, 2);
+      OMNI_CHECK_LAUNCH("token_offsets_kernel");
+    } else {
+      token_offsets_kernel<<<grid_for(M + 1, 256), 256, 0, st>>>(M, token, hk, n_tok, tok_off, 1);
+      OMNI_CHECK_LAUNCH("token_offsets_kernel");
+      const int64_t band_size = (n_loc + n_bands - 1) / n_bands;
+      band_partition_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((n_tok + 7) / 8, kSMs * 16)), 256, 0,
+                              st>>>(ids, plan.expert_begin, n_loc, tok_off, n_tok, (int)n_bands, band_size, dest,
+                                    plan.task_pair, plan.token_offsets);
+      OMNI_CHECK_LAUNCH("band_partition_kernel");
+    }
   }
   // a4: offsets (exclusive scan of counts; entry n_loc holds the total m_loc)
   OMNI_TRY(scan<0>(cnt, n_loc + 1, plan.expert_offsets, nullptr, tiles, st));
@@ -354,7 +431,7 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
   const int32_t* m_loc = plan.expert_offsets + n_loc;
   gather_plan_kernel<<<grid_for(M, 256), 256, 0, st>>>(vin, M, m_loc, token, gate, ids, plan.expert_begin, hk,
                                                       plan.sorted_token, plan.sorted_gate, plan.sorted_expert,
-                                                      plan.sorted_task);
+                                                      vorder ? plan.sorted_task : nullptr, vorder && n_bands > 1 ? dest : nullptr);
   OMNI_CHECK_LAUNCH("gather_plan_kernel");
   if (B > 1) {
     // runs: (group, token) boundaries of the sorted plan, compacted to run_offsets

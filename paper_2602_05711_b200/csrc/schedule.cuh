@@ -5,17 +5,18 @@
 
 namespace omni {
 
-size_t schedule_ws_bytes(int64_t M, int64_t n_loc);
+size_t schedule_ws_bytes(int64_t M, int64_t n_loc);  // + M + 1 ints of V-order scratch
 // hk = h*K: default token of task t is t / hk when token == nullptr.
 omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, const int32_t* token,
-                            int64_t hk, const omnimoe_plan& plan, int64_t B, int64_t Tb, void* ws,
-                            cudaStream_t st);
+                            int64_t hk, const omnimoe_plan& plan, int64_t B, int64_t Tb, int64_t n_bands,
+                            void* ws, cudaStream_t st);
 int64_t resolve_group_size(const omnimoe_dims& d);
 // token-centric ablation executor ("w/o ECS"): straight from the routing decision
 omnimoe_status expert_token_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* V,
                                 const int32_t* idx, const float* gate, int64_t begin, int64_t end, float* y,
                                 int accumulate, cudaStream_t st);
 int64_t resolve_token_blocks(const omnimoe_dims& d, int64_t L);
+int64_t resolve_v_bands(const omnimoe_dims& d, int64_t n_loc);
 
 // V [n][d] -> [d/32][n][32] (omnimoe_pack_v)
 omnimoe_status pack_v(int64_t n, int d, const void* V, void* Vs, cudaStream_t st);

@@ -51,7 +51,8 @@ EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnim
            "omnimoe_shared_mlp", "omnimoe_layer_fwd", "omnimoe_router_logits", "omnimoe_gemm_bf16",
            "omnimoe_last_launch_count", "omnimoe_status_string", "omnimoe_last_error",
            "omnimoe_group_size", "omnimoe_token_blocks", "omnimoe_ep_pack_workspace_size",
-           "omnimoe_ep_pack", "omnimoe_ep_unpack", "omnimoe_ep_combine", "omnimoe_pack_v"]
+           "omnimoe_ep_pack", "omnimoe_ep_unpack", "omnimoe_ep_combine", "omnimoe_pack_v",
+           "omnimoe_v_bands"]
 
 _lib = None
 
@@ -88,6 +89,8 @@ def load(path: str = LIB_PATH):
     lib.omnimoe_last_launch_count.restype = ctypes.c_int
     lib.omnimoe_group_size.argtypes = [PD]
     lib.omnimoe_group_size.restype = ctypes.c_int64
+    lib.omnimoe_v_bands.argtypes = [PD, ctypes.c_int64]
+    lib.omnimoe_v_bands.restype = ctypes.c_int64
     lib.omnimoe_token_blocks.argtypes = [PD, ctypes.c_int64]
     lib.omnimoe_token_blocks.restype = ctypes.c_int64
     lib.omnimoe_status_string.restype = ctypes.c_char_p
@@ -204,12 +207,19 @@ def token_blocks(dims: LayerDims, L: int) -> int:
     return int(load().omnimoe_token_blocks(ctypes.byref(dc), L))
 
 
-def new_plan(n_loc: int, M: int, device, expert_begin: int = 0, n_tokens: int = 0):
-    """Plan buffers (omnimoe_plan).  n_tokens: tokens of the task list (0: M / (h*K))
-    -- the task-order arrays used by the SLICED executor are always allocated."""
+def v_bands(dims: LayerDims, n_loc: int) -> int:
+    """Expert bands of the SLICED executor's pass V for n_loc local experts."""
+    dc = dims.c()
+    return int(load().omnimoe_v_bands(ctypes.byref(dc), n_loc))
+
+
+def new_plan(n_loc: int, M: int, device, expert_begin: int = 0, n_tokens: int = 0, dims: LayerDims = None):
+    """Plan buffers (omnimoe_plan).  n_tokens: tokens of the task list (0: M / (h*K));
+    the V-order arrays of the SLICED executor are always allocated (for dims' bands)."""
+    nb = v_bands(dims, n_loc) if dims is not None else 1
     t = dict(sorted_task=torch.empty(max(M, 1), dtype=torch.int32, device=device),
              task_pair=torch.empty((max(M, 1), 2), dtype=torch.int32, device=device),
-             token_offsets=torch.empty(max(n_tokens, M) + 1, dtype=torch.int32, device=device),
+             token_offsets=torch.empty(max(n_tokens, M, 1) * (nb + 1) + 1, dtype=torch.int32, device=device),
              n_tokens=n_tokens,
 expert_offsets=torch.empty(n_loc + 1, dtype=torch.int32, device=device),
              sorted_token=torch.empty(max(M, 1), dtype=torch.int32, device=device),
@@ -242,7 +252,7 @@ def schedule(dims: LayerDims, idx, gate, token=None, expert_begin=0, expert_end=
         _req(token, "token", torch.int32, M)
     expert_end = dims.N if expert_end is None else expert_end
     n_loc = expert_end - expert_begin
-    plan = plan or new_plan(n_loc, M, idx.device, expert_begin, n_tokens)
+    plan = plan or new_plan(n_loc, M, idx.device, expert_begin, n_tokens, dims)
     ws = ws if ws is not None else torch.empty(max(workspace_size(dims, M, WS_SCHEDULE), 1),
                                                dtype=torch.uint8, device=idx.device)
     dc, cp = dims.c(), _cplan(plan)

@@ -393,11 +393,19 @@ def test_pack_v_is_a_pure_relayout():
     assert torch.equal(Vs.view(torch.int16), want.view(torch.int16))
 
 
+@pytest.fixture(params=[0, 16], ids=["bands_default", "bands_16KB"])
+def v_band_kb(request, monkeypatch):
+    """0: the library's expert bands (1 at these sizes); 16: 16 KB bands (several)."""
+    if request.param:
+        monkeypatch.setenv("OMNIMOE_V_BAND_KB", str(request.param))
+    return request.param
+
+
 @pytest.mark.parametrize("B", [0, 2, 512])
 @pytest.mark.parametrize("d,act", [(64, om.SILU), (96, om.SILU), (1024, om.SILU), (2048, om.SILU),
                                    (64, om.IDENTITY)])
 @pytest.mark.parametrize("accumulate", [False, True])
-def test_expert_fwd_sliced_given_plan(d, act, B, accumulate):
+def test_expert_fwd_sliced_given_plan(d, act, B, accumulate, v_band_kb):
     rng = np.random.default_rng(d + B)
     L, N, HK = 200, 3000, 12
     dims = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, act=act, group_size=B, v_layout=om.V_SLICED)
@@ -407,6 +415,7 @@ def test_expert_fwd_sliced_given_plan(d, act, B, accumulate):
     ids[7] = ids[3]  # two tokens with identical expert lists
     gates = rng.random((L, HK)).astype(np.float32)
     plan = om.schedule(dims, torch.from_numpy(ids).cuda().reshape(-1), torch.from_numpy(gates).cuda().reshape(-1))
+    assert om.v_bands(dims, N) == (1 if not v_band_kb else -(-N * 64 // (v_band_kb << 10)))
     Vs = om.pack_v(dims, inp["V"])
     y0 = torch.randn(L, d, device="cuda") if accumulate else None
     y = om.expert_fwd(dims, inp["x"], inp["W"], Vs, plan, y_routed=None if y0 is None else y0.clone(),
@@ -423,7 +432,7 @@ def test_expert_fwd_sliced_given_plan(d, act, B, accumulate):
     assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
 
 
-def test_expert_fwd_sliced_shard_and_empty_tokens():
+def test_expert_fwd_sliced_shard_and_empty_tokens(v_band_kb):
     """Expert range of a shard (tasks outside it are skipped) and tokens with no
     tasks in range (their y_routed rows are written as zeros)."""
     rng = np.random.default_rng(3)
@@ -451,7 +460,7 @@ def test_expert_fwd_sliced_shard_and_empty_tokens():
 
 @pytest.mark.parametrize("mode", [synth.NORMAL, synth.DYADIC])
 @pytest.mark.parametrize("B", [0, 5])
-def test_layer_c1_sliced(mode, B):
+def test_layer_c1_sliced(mode, B, v_band_kb):
     w = _dims("C1", group_size=B, v_layout=om.V_SLICED)
     dims = w.dims
     inp = make_inputs(dims, w.L, w.seed, mode)

@@ -93,6 +93,20 @@ __global__ void piece64_gather(const uint4* __restrict__ tab, int nrows, int n_p
   if (acc.x == 0x12345678u) sink[0] = acc;
 }
 
+// 32-byte pieces (2 lanes x 16 B), 16 per warp instruction
+__global__ void piece32_gather(const uint4* __restrict__ tab, int nrows, int n_per_warp, uint32_t salt, uint4* sink) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll 4
+  for (int k = 0; k < n_per_warp; k += 16) {
+    uint32_t r = hash32((gw * 7919u + k + (lane >> 1)) ^ salt) & (nrows - 1);
+    uint4 v = tab[(size_t)r * 2 + (lane & 1)];
+    acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
+  }
+  if (acc.x == 0x12345678u) sink[0] = acc;
+}
+
 template <class F>
 float time_ms(F f, int reps = 5) {
   cudaEvent_t a, b;
@@ -166,6 +180,16 @@ int main() {
       for (int s = 0; s < 32; ++s) piece64_gather<<<pw / 8, 256>>>(big + (size_t)s * (1 << 20) * 4, 1 << 20, npw2 * 2, 77u * s, sink);
     }, 3);
     printf(", \"piece64_packed_sweep_gbs\": %.1f", (double)pw * npw2 * 2 * 32 * 64 / ms / 1e6);
+    ms = time_ms([&] { piece32_gather<<<pw / 8, 256>>>(big, 1 << 20, pnpw * 4, 0u, sink); });
+    printf(", \"l2_piece32_packed_33MB_gbs\": %.1f", (double)pw * pnpw * 4 * 32 / ms / 1e6);
+    ms = time_ms([&] {
+      for (int s = 0; s < 64; ++s) piece32_gather<<<pw / 8, 256>>>(big + (size_t)s * (1 << 20) * 2, 1 << 20, npw2 * 4, 77u * s, sink);
+    }, 3);
+    printf(", \"piece32_packed_sweep_gbs\": %.1f", (double)pw * npw2 * 4 * 64 * 32 / ms / 1e6);
+    ms = time_ms([&] {
+      for (int s = 0; s < 64; ++s) piece64_gather<<<pw / 8, 256>>>(big + (size_t)s * (1 << 19) * 4, 1 << 19, npw2 * 2, 77u * s, sink);
+    }, 3);
+    printf(", \"piece64_packed_sweep_33MB_gbs\": %.1f", (double)pw * npw2 * 2 * 64 * 64 / ms / 1e6);
   }
   // FFMA rate
   float* o; CK(cudaMalloc(&o, 64));
