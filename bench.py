@@ -20,6 +20,7 @@ sample of the same workload on the host cores.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -244,7 +245,8 @@ def bench_single(args, w, lr):
         return 0
     # ---- per-stage breakdown through the individual C-ABI calls (same inputs) ----
     M = L * dims.n_heads * dims.top_k
-    rws = om.workspace(dims, L, om.WS_ROUTE)
+    rdims = dataclasses.replace(dims, route_order=om.ORDER_CANDIDATE)  # the layer's routing (no final sort)
+    rws = om.workspace(rdims, L, om.WS_ROUTE)
     plan = om.new_plan(dims.N, M, "cuda", dims=dims)
     sws = om.workspace(dims, M, om.WS_SCHEDULE)
     ews = om.workspace(dims, L, om.WS_EXPERT)
@@ -254,7 +256,7 @@ def bench_single(args, w, lr):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
         flush.zero_()
         e[0].record(st)
-        idx, gate, _ = om.route(dims, inp["x"], inp["subkeys"], ws=rws, want_score=False)
+        idx, gate, _ = om.route(rdims, inp["x"], inp["subkeys"], ws=rws, want_score=False)
         e[1].record(st)
         om.schedule(dims, idx.reshape(-1), gate.reshape(-1), plan=plan, ws=sws)
         e[2].record(st)
@@ -362,6 +364,9 @@ def bench_multi(args, w, ws, rk, lr):
         raise SystemExit(f"N={dims.N} not divisible by {ws} ranks")
     n_per = dims.N // ws
     inp = make_inputs(dims, L, w.seed, token_begin=rk * L, expert_rows=(rk * n_per, (rk + 1) * n_per))
+    if dims.v_layout == om.V_SLICED:  # one-time re-layout of this rank's V shard
+        inp["V"] = om.pack_v(dims, inp["V"])
+        torch.cuda.synchronize()
     ops = ep.LibOps(dims)
     ops.set_mlp(inp.get("w_gate_up"), inp.get("w_down"))
     comm = ep.TorchComm()
@@ -469,7 +474,7 @@ def main():
     if ws > 1:
         dist.barrier()
     from paper_2602_05711_b200 import omnimoe as om
-    sliced = args.v_layout == "sliced" and args.expert_kernel == "auto" and ws == 1
+    sliced = args.v_layout == "sliced" and args.expert_kernel == "auto"
     w = configs.get(args.config, v_layout=om.V_SLICED if sliced else om.V_ROWS)
     if args.expert_kernel != "auto":
         ek = {"token": om.EXPERT_TOKEN, "warp": om.EXPERT_WARP}[args.expert_kernel]

@@ -92,7 +92,12 @@ enum { OMNIMOE_ROUTER_EXACT = 0, OMNIMOE_ROUTER_EXACT_F64 = 1 };
  *   token_blocks T_b: see below.
  *   v_layout   OMNIMOE_V_ROWS | OMNIMOE_V_SLICED: layout of the V argument of
  *              omnimoe_expert_fwd / omnimoe_layer_fwd (W is always [N][d]).
+ *   route_order  order of the K ids omnimoe_route writes per token-head: KEY (by
+ *              exact key desc, id asc -- Eq.TopK's ranking) or CANDIDATE (the order
+ *              of the Cartesian candidates, row rank then column rank: same set and
+ *              gates, no final sort; what omnimoe_layer_fwd uses internally).
  */
+enum { OMNIMOE_ORDER_KEY = 0, OMNIMOE_ORDER_CANDIDATE = 1 };
 typedef struct {
   int64_t d, n_rows, n_cols, top_k, n_heads, d_ff;
   int32_t dtype;         /* OMNIMOE_BF16 | OMNIMOE_F32 */
@@ -105,7 +110,7 @@ typedef struct {
                           * L2-resident; 1 = the paper's single sort;
                           * 0 = library choice */
   int32_t v_layout;      /* OMNIMOE_V_ROWS | OMNIMOE_V_SLICED */
-  int32_t reserved;
+  int32_t route_order;   /* omnimoe_route output order: OMNIMOE_ORDER_KEY | OMNIMOE_ORDER_CANDIDATE */
 } omnimoe_dims;
 
 /* Expert-centric plan for the local expert range [expert_begin, expert_end)

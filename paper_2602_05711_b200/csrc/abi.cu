@@ -83,6 +83,10 @@ omnimoe_status validate_dims(const omnimoe_dims* dp) {
     set_error("group_size and token_blocks must be >= 0");
     return OMNIMOE_ERR_INVALID_ARGUMENT;
   }
+  if (d.route_order != OMNIMOE_ORDER_KEY && d.route_order != OMNIMOE_ORDER_CANDIDATE) {
+    set_error("unknown route order " + std::to_string(d.route_order));
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
   if (d.v_layout != OMNIMOE_V_ROWS && d.v_layout != OMNIMOE_V_SLICED) {
     set_error("unknown V layout " + std::to_string(d.v_layout));
     return OMNIMOE_ERR_UNSUPPORTED;
@@ -304,7 +308,8 @@ omnimoe_status omnimoe_route(const omnimoe_dims* dims, int64_t L, const void* x,
     OMNI_TRY(select_params(*dims, L * dims->n_heads, &sp, &smem));
   }
   OMNI_TRY(check_device());
-  return route_impl(*dims, L, x, subkeys, idx, gate, score, ws, (cudaStream_t)stream);
+  return route_impl(*dims, L, x, subkeys, idx, gate, score, ws, (cudaStream_t)stream,
+                    dims->route_order == OMNIMOE_ORDER_CANDIDATE ? 0 : 1);
 }
 
 omnimoe_status omnimoe_schedule(const omnimoe_dims* dims, int64_t M, const int32_t* idx, const float* gate,

@@ -504,6 +504,266 @@ __global__ void __launch_bounds__(G > 256 ? G : 256)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Large K, candidate-order output (the layer path, sorted == 0): one WARP per
+// token-head, no block barriers.  Selections use bucket refinement on 64-bit
+// order-preserving integer keys: each pass histograms the keys inside the current
+// range [lo, hi] into 256 buckets of width 2^shift (span >> shift < 256), keeps the
+// bucket holding the want-th largest, and stops when the whole range is taken or
+// holds one key value (ties, resolved on the full key) -- at most 8 passes.
+struct WPred {  // selected <=> bk > thr || (bk == thr && full >= kmin)
+  uint64_t thr;
+  U128 kmin;
+};
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// items: slots m = 0..nslot-1 of this lane; bkf(m, ok) -> bucket key (ok = item
+// exists); fullf(m) -> full key (needed only for ties).  lo0: a lower bound of the
+// want-th largest bucket key (items below it are never selected).
+template <class BkF, class FullF>
+__device__ WPred warp_select_top(int nslot, BkF bkf, FullF fullf, int want, uint64_t lo0, int* hist) {
+  const int lane = threadIdx.x & 31;
+  uint64_t lo = ~0ull, hi = 0;
+  int cnt = 0;
+  for (int m = 0; m < nslot; ++m) {
+    bool ok;
+    const uint64_t k = bkf(m, ok);
+    if (ok && k >= lo0) {
+      lo = min(lo, k);
+      hi = max(hi, k);
+      ++cnt;
+    }
+  }
+  lo = warp_min_u64(lo);
+  hi = warp_max_u64(hi);
+  cnt = warp_sum(cnt);
+  int r = want;
+  while (r < cnt && lo < hi) {
+    const uint64_t span = hi - lo;
+    const int shift = max(0, 64 - __clzll((long long)span) - 8);  // span >> shift < 256
+#pragma unroll
+    for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
+    __syncwarp();
+    for (int m = 0; m < nslot; ++m) {
+      bool ok;
+      const uint64_t k = bkf(m, ok);
+      if (ok && k >= lo && k <= hi) atomicAdd(&hist[(int)((k - lo) >> shift)], 1);
+    }
+    __syncwarp();
+    // suffix counts from the top bucket: lane j owns buckets 255-8j .. 255-8j-7
+    int c[8], sum = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      c[t] = hist[255 - 8 * lane - t];
+      sum += c[t];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int above = incl - sum, found = -1, fabove = 0, fcnt = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      if (found < 0 && above < r && above + c[t] >= r) {
+        found = 255 - 8 * lane - t;
+        fabove = above;
+        fcnt = c[t];
+      }
+      above += c[t];
+    }
+    const int src = __ffs(__ballot_sync(0xffffffffu, found >= 0)) - 1;
+    const int b = __shfl_sync(0xffffffffu, found, src);
+    r -= __shfl_sync(0xffffffffu, fabove, src);
+    cnt = __shfl_sync(0xffffffffu, fcnt, src);
+    const uint64_t nlo = lo + ((uint64_t)b << shift);
+    const uint64_t w = (shift == 0) ? 0ull : ((1ull << shift) - 1ull);
+    hi = (hi - nlo > w) ? nlo + w : hi;
+    lo = nlo;
+    __syncwarp();  // the histogram is cleared again by the next pass
+  }
+  WPred p;
+  p.thr = lo;
+  p.kmin = U128{0ull, 0ull};
+  if (r < cnt) {  // one bucket-key value, more items than wanted: the r largest full keys
+    U128 prev{~0ull, ~0ull};
+    for (int t = 0; t < r; ++t) {
+      U128 best{0ull, 0ull};
+      for (int m = 0; m < nslot; ++m) {
+        bool ok;
+        const uint64_t k = bkf(m, ok);
+        if (ok && k == lo) {
+          const U128 f = fullf(m);
+          if (gt(prev, f) && gt(f, best)) best = f;
+        }
+      }
+      prev = warp_max_u128(best);
+    }
+    p.kmin = prev;
+  }
+  return p;
+}
+
+__device__ __forceinline__ bool wsel(const WPred& p, uint64_t bk) { return bk > p.thr; }
+
+// bitonic sort (descending) of a[0..n), n a power of two, by one warp
+__device__ void warp_bitonic_desc(uint64_t* a, int n) {
+  const int lane = threadIdx.x & 31;
+  for (int size = 2; size <= n; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = lane; i < (n >> 1); i += 32) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool desc = (lo & size) == 0;
+        const uint64_t p = a[lo], q = a[hi];
+        if (desc ? q > p : p > q) {
+          a[lo] = q;
+          a[hi] = p;
+        }
+      }
+      __syncwarp();
+    }
+}
+
+// the top k1 half keys of lg[0..n) (n <= 1024), sorted descending into out[0..P)
+// (P = pow2 >= k1, padded with 0); returns logsumexp of the half if want_lse
+__device__ float warp_half_sorted(const float* __restrict__ lg, int n, int k1, int P, uint64_t* out, int* hist,
+                                  bool want_lse) {
+  const int lane = threadIdx.x & 31;
+  const int nslot = (n + 31) >> 5;
+  auto bkf = [&](int m, bool& ok) {  // the half's logits stay in L1 over the passes
+    const int i = lane + 32 * m;
+    ok = i < n;
+    return ok ? half_key(lg[i], (uint32_t)i) : 0ull;
+  };
+  WPred p;
+  p.thr = 0;
+  p.kmin = U128{0ull, 0ull};
+  if (k1 < n) p = warp_select_top(nslot, bkf, [&](int m) { bool ok; return U128{bkf(m, ok), 0ull}; }, k1, 0ull, hist);
+  // compact the selected keys (bucket keys are unique: bk >= thr) in slot order
+  int base = 0;
+  for (int m = 0; m < nslot; ++m) {
+    bool ok;
+    const uint64_t k = bkf(m, ok);
+    const bool sel = ok && (k1 >= n || k >= p.thr);
+    const unsigned bal = __ballot_sync(0xffffffffu, sel);
+    if (sel) out[base + __popc(bal & ((1u << lane) - 1u))] = k;
+    base += __popc(bal);
+  }
+  for (int i = k1 + lane; i < P; i += 32) out[i] = 0ull;
+  __syncwarp();
+  warp_bitonic_desc(out, P);
+  if (!want_lse) return 0.f;
+  const float mx = half_val(out[0]);
+  float sum = 0.f;
+  for (int m = 0; m < nslot; ++m) {
+    bool ok;
+    const uint64_t k = bkf(m, ok);
+    if (ok) sum += __expf(half_val(k) - mx);
+  }
+  return mx + __logf(warp_sum(sum));
+}
+
+// smem: cand[C] (a << 16 | b, (a+1)(b+1) <= K) | per warp: kr[Pr], kc[Pc] (u64), hist[256]
+__global__ void __launch_bounds__(256)
+    select_bucket_kernel(SelectParams p, int C, int Pr, int Pc, const float* __restrict__ logits,
+                         int32_t* __restrict__ idx, float* __restrict__ gate, float* __restrict__ score) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* cand = reinterpret_cast<uint32_t*>(smem);
+  const int K = p.top_k;
+  const int kr = min(K, p.n_rows), kc = min(K, p.n_cols);
+  if (threadIdx.x == 0) {  // rows a in order, columns b < min(kc, K / (a+1))
+    int off = 0;
+    for (int a = 0; a < kr; ++a) {
+      const int nb = min(kc, K / (a + 1));
+      for (int b = 0; b < nb; ++b) cand[off++] = ((uint32_t)a << 16) | (uint32_t)b;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t cand_bytes = ((size_t)C * 4 + 15) / 16 * 16;
+  const size_t per_warp = (size_t)(Pr + Pc) * 8 + 256 * 4;
+  uint8_t* base = smem + cand_bytes + (size_t)wid * per_warp;
+  uint64_t* skr = reinterpret_cast<uint64_t*>(base);
+  uint64_t* skc = skr + Pr;
+  int* hist = reinterpret_cast<int*>(skc + Pc);
+  const int R = p.n_rows + p.n_cols;
+  const uint32_t Nc = (uint32_t)p.n_cols;
+  const int nslot = (C + 31) >> 5;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + wid, nw = gridDim.x * (blockDim.x >> 5);
+  for (int th = gw; th < p.T; th += nw) {
+    const float* lg = logits + (size_t)th * R;
+    const float lse_r = warp_half_sorted(lg, p.n_rows, kr, Pr, skr, hist, score != nullptr);
+    const float lse_c = warp_half_sorted(lg + p.n_rows, p.n_cols, kc, Pc, skc, hist, score != nullptr);
+    auto hi_of = [&](int c, uint32_t& id, float& vr, float& vc) {
+      const uint32_t ab = cand[c];
+      const uint64_t ka = skr[ab >> 16], kb = skc[ab & 0xFFFF];
+      vr = half_val(ka);
+      vc = half_val(kb);
+      id = half_idx(ka) * Nc + half_idx(kb);
+      return ((double)vr + (double)vc) + 0.0;
+    };
+    auto bkf = [&](int m, bool& ok) {
+      const int c = lane + 32 * m;
+      ok = c < C;
+      uint32_t id;
+      float vr, vc;
+      return ok ? ord64(hi_of(c, id, vr, vc)) : 0ull;
+    };
+    auto fullf = [&](int m) {
+      uint32_t id;
+      float vr, vc;
+      hi_of(lane + 32 * m, id, vr, vc);
+      return cell_key(vr, vc, id);
+    };
+    // lower bound of the K-th largest key: for A rows and B = ceil(K/A) columns, the
+    // A*B >= K cells of the block all have keys >= s_r[A-1] + s_c[B-1]
+    uint64_t lb = 0;
+    for (int A = 1 + lane; A <= kr; A += 32) {
+      const int B = (K + A - 1) / A;
+      if (B <= kc) lb = max(lb, ord64(((double)half_val(skr[A - 1]) + (double)half_val(skc[B - 1])) + 0.0));
+    }
+    lb = warp_max_u64(lb);
+    const WPred sel = warp_select_top(nslot, bkf, fullf, K, lb, hist);
+    // outputs in candidate order; gates = softmax over the K exact keys (hi part; the
+    // TwoSum remainder is below 2^-53 relative)
+    uint32_t id0;
+    float r0, c0;
+    const double k1v = hi_of(0, id0, r0, c0);
+    float es = 0.f;
+    int o = 0;
+    const size_t ob = (size_t)th * K;
+    for (int m = 0; m < nslot; ++m) {
+      const int c = lane + 32 * m;
+      uint32_t id = 0;
+      float vr = 0.f, vc = 0.f;
+      const double h = c < C ? hi_of(c, id, vr, vc) : 0.0;
+      const uint64_t bk = c < C ? ord64(h) : 0ull;
+      bool take = c < C && bk >= sel.thr;
+      if (take && bk == sel.thr && (sel.kmin.hi | sel.kmin.lo)) take = ge(cell_key(vr, vc, id), sel.kmin);
+      const unsigned bal = __ballot_sync(0xffffffffu, take);
+      if (take) {
+        const int pos = o + __popc(bal & ((1u << lane) - 1u));
+        const float e = expf((float)(h - k1v));
+        es += e;
+        idx[ob + pos] = (int32_t)id;
+        gate[ob + pos] = e;
+        if (score) score[ob + pos] = (float)(h - (double)lse_r - (double)lse_c);
+      }
+      o += __popc(bal);
+    }
+    const float inv = 1.0f / warp_sum(es);
+    __syncwarp();
+    for (int k = lane; k < K; k += 32) gate[ob + k] *= inv;
+  }
+}
+
 }  // namespace
 
 // host --------------------------------------------------------------------
@@ -555,6 +815,33 @@ omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* lo
     select_warp_kernel<<<grid, 256, 0, st>>>(p, logits, idx, gate, score);
     OMNI_CHECK_LAUNCH("select_warp_kernel");
     return OMNIMOE_OK;
+  }
+  if (!p.sorted && p.top_k >= 32 && p.n_rows <= 1024 && p.n_cols <= 1024 && !getenv("OMNIMOE_SELECT_CTA")) {
+    // candidate-order output (the layer path): warp per token-head, bucket selection
+    const int K = p.top_k, kr = std::min(K, p.n_rows), kc = std::min(K, p.n_cols);
+    int C = 0;
+    for (int a = 0; a < kr; ++a) C += std::min(kc, K / (a + 1));
+    int Pr = 1, Pc = 1;
+    while (Pr < kr) Pr <<= 1;
+    while (Pc < kc) Pc <<= 1;
+    const size_t cand_bytes = ((size_t)C * 4 + 15) / 16 * 16;
+    const size_t per_warp = (size_t)(Pr + Pc) * 8 + 256 * 4;
+    int warps = 8;
+    while (warps > 1 && cand_bytes + warps * per_warp > 200 * 1024) warps >>= 1;
+    const size_t sm = cand_bytes + warps * per_warp;
+    if (sm <= 200 * 1024) {
+      if (cudaFuncSetAttribute(select_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+          cudaSuccess) {
+        set_error("route: cannot set select_bucket_kernel shared memory");
+        return OMNIMOE_ERR_CUDA;
+      }
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_bucket_kernel, warps * 32, sm);
+      const int grid = std::max(1, std::min((p.T + warps - 1) / warps, kSMs * std::max(per_sm, 1)));
+      select_bucket_kernel<<<grid, warps * 32, sm, st>>>(p, C, Pr, Pc, logits, idx, gate, score);
+      OMNI_CHECK_LAUNCH("select_bucket_kernel");
+      return OMNIMOE_OK;
+    }
   }
   auto kern = p.group == 32 ? select_kernel<32> : p.group == 256 ? select_kernel<256> : select_kernel<1024>;
   const int threads = p.group == 32 ? 32 * p.groups_per_cta : p.group;

@@ -52,11 +52,15 @@ class LibOps:
         return om.ep_unpack(rec, R, task_off, tok_off)
 
     def expert(self, x_recv, W_loc, V_loc, ids, gate, tok, n_loc):
-        y = torch.zeros((x_recv.shape[0], self.dims.d), dtype=torch.float32, device=x_recv.device)
-        if ids.numel() == 0 or x_recv.shape[0] == 0:
-            return y
-        plan = om.schedule(self.dims, ids, gate, token=tok, expert_begin=0, expert_end=n_loc)
-        return om.expert_fwd(self.dims, x_recv, W_loc, V_loc, plan, y_routed=y, accumulate=True)
+        """V_loc is [n_loc][d], or [d/32][n_loc][32] when dims.v_layout is V_SLICED
+        (om.pack_v of the shard); the SLICED executor writes every row of y."""
+        sliced = self.dims.v_layout == om.V_SLICED
+        rows = x_recv.shape[0]
+        if ids.numel() == 0 or rows == 0:
+            return torch.zeros((rows, self.dims.d), dtype=torch.float32, device=x_recv.device)
+        y = (torch.empty if sliced else torch.zeros)((rows, self.dims.d), dtype=torch.float32, device=x_recv.device)
+        plan = om.schedule(self.dims, ids, gate, token=tok, expert_begin=0, expert_end=n_loc, n_tokens=rows)
+        return om.expert_fwd(self.dims, x_recv, W_loc, V_loc, plan, y_routed=y, accumulate=not sliced)
 
     def combine(self, y_ret, inv, tok_off, L):
         return om.ep_combine(self.dims, y_ret, inv, tok_off, L)

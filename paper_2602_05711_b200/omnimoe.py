@@ -20,6 +20,7 @@ BF16, F32 = 0, 1
 SILU, IDENTITY = 0, 1
 EXPERT_AUTO, EXPERT_WARP, EXPERT_GROUP, EXPERT_TOKEN, EXPERT_SLICED = 0, 1, 2, 3, 4
 V_ROWS, V_SLICED = 0, 1
+ORDER_KEY, ORDER_CANDIDATE = 0, 1
 ROUTER_EXACT, ROUTER_EXACT_F64 = 0, 1
 LOGITS_ROUTE, LOGITS_EXACT_F64, LOGITS_BF16_FAST = 0, 1, 2
 WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER = 0, 1, 2, 3
@@ -34,7 +35,7 @@ class Dims(ctypes.Structure):
                 ("top_k", ctypes.c_int64), ("n_heads", ctypes.c_int64), ("d_ff", ctypes.c_int64),
                 ("dtype", ctypes.c_int32), ("act", ctypes.c_int32), ("router", ctypes.c_int32),
                 ("expert_kernel", ctypes.c_int32), ("group_size", ctypes.c_int64),
-                ("token_blocks", ctypes.c_int64), ("v_layout", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("token_blocks", ctypes.c_int64), ("v_layout", ctypes.c_int32), ("route_order", ctypes.c_int32)]
 
 
 class Plan(ctypes.Structure):
@@ -131,6 +132,7 @@ class LayerDims:
     group_size: int = 0
     token_blocks: int = 0
     v_layout: int = V_ROWS
+    route_order: int = ORDER_KEY
 
     @property
     def N(self) -> int:
@@ -143,7 +145,7 @@ class LayerDims:
     def c(self) -> Dims:
         return Dims(self.d, self.n_rows, self.n_cols, self.top_k, self.n_heads, self.d_ff,
                     self.dtype, self.act, self.router, self.expert_kernel, self.group_size,
-                    self.token_blocks, self.v_layout, 0)
+                    self.token_blocks, self.v_layout, self.route_order)
 
 
 def _ptr(t):

@@ -29,9 +29,11 @@ def _run_loopback(dims, L, seed, R):
     xs = [full["x"][r * lpr:(r + 1) * lpr] for r in range(R)]
     shards = [make_inputs(dims, 1, seed, skip=("x", "subkeys", "w_gate_up", "w_down"),
                           expert_rows=(r * n_per, (r + 1) * n_per)) for r in range(R)]
-    ys = ep.ep_layer_fwd_loopback(ops, xs, full["subkeys"], [s["W"] for s in shards], [s["V"] for s in shards],
-                                  n_per)
-    y1 = om.layer_fwd(dims, full["x"], full["subkeys"], full["W"], full["V"], full["w_gate_up"], full["w_down"])
+    sl = dims.v_layout == om.V_SLICED
+    vs = [om.pack_v(dims, s["V"]) if sl else s["V"] for s in shards]
+    ys = ep.ep_layer_fwd_loopback(ops, xs, full["subkeys"], [s["W"] for s in shards], vs, n_per)
+    y1 = om.layer_fwd(dims, full["x"], full["subkeys"], full["W"], om.pack_v(dims, full["V"]) if sl else full["V"],
+                      full["w_gate_up"], full["w_down"])
     torch.cuda.synchronize()
     return torch.cat(ys), y1, full
 
@@ -47,8 +49,9 @@ def test_synth_shard_equals_rows_of_full():
 
 
 @pytest.mark.parametrize("R", [1, 2, 4, 8])
-def test_ep_loopback_c1(R):
-    w = configs.get("C1")
+@pytest.mark.parametrize("vl", [om.V_ROWS, om.V_SLICED])
+def test_ep_loopback_c1(R, vl):
+    w = configs.get("C1", v_layout=vl)
     y, y1, _ = _run_loopback(w.dims, w.L, w.seed, R)
     e_tok, e_elt = rel_errors(y.float().cpu().numpy(), y1.float().cpu().numpy())
     assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
@@ -59,9 +62,10 @@ def test_ep_loopback_c1(R):
     assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
 
 
-@pytest.mark.parametrize("R,B", [(2, 0), (4, 0), (8, 1)])
-def test_ep_loopback_mid(R, B):
-    dims = om.LayerDims(**MID, group_size=B)
+@pytest.mark.parametrize("R,B,vl", [(2, 0, om.V_ROWS), (4, 0, om.V_ROWS), (8, 1, om.V_ROWS), (2, 0, om.V_SLICED),
+                                    (8, 0, om.V_SLICED)])
+def test_ep_loopback_mid(R, B, vl):
+    dims = om.LayerDims(**MID, group_size=B, v_layout=vl)
     y, y1, _ = _run_loopback(dims, 512, 5, R)
     e_tok, e_elt = rel_errors(y.float().cpu().numpy(), y1.float().cpu().numpy())
     assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
@@ -88,6 +92,12 @@ dims = om.LayerDims(d=256, n_rows=64, n_cols=64, top_k=32, n_heads=2, d_ff=256)
 full = make_inputs(dims, 384, 7)
 ops = ep.LibOps(dims); ops.set_mlp(full["w_gate_up"], full["w_down"])
 y = ep.ep_layer_fwd(ops, ep.TorchComm(), full["x"], full["subkeys"], full["W"], full["V"], dims.N)
+sd = om.LayerDims(d=256, n_rows=64, n_cols=64, top_k=32, n_heads=2, d_ff=256, v_layout=om.V_SLICED)
+so = ep.LibOps(sd); so.set_mlp(full["w_gate_up"], full["w_down"])
+ys = ep.ep_layer_fwd(so, ep.TorchComm(), full["x"], full["subkeys"], full["W"], om.pack_v(sd, full["V"]), dims.N)
+torch.cuda.synchronize()
+es = rel_errors(ys.float().cpu().numpy(), y.float().cpu().numpy())
+assert es[0] <= 1e-2 and es[1] <= 1e-2, es
 y1 = om.layer_fwd(dims, full["x"], full["subkeys"], full["W"], full["V"], full["w_gate_up"], full["w_down"])
 torch.cuda.synchronize()
 e = rel_errors(y.float().cpu().numpy(), y1.float().cpu().numpy())

@@ -512,3 +512,22 @@ def test_sliced_layout_errors():
     with pytest.raises(om.OmniMoEError, match="INVALID_ARGUMENT"):
         om.workspace_size(om.LayerDims(d=64, n_rows=4, n_cols=4, top_k=2, expert_kernel=om.EXPERT_SLICED), 8,
                           om.WS_LAYER)
+
+
+@pytest.mark.parametrize("name,L", [("C1", 256), ("C3a", 64), ("C4", 16), ("C4pp", 48)])
+def test_route_candidate_order(name, L):
+    """ORDER_CANDIDATE (the layer's routing, warp bucket selection): same id sets and
+    gates as the key-ordered route, ids in Cartesian candidate order."""
+    w = _dims(name)
+    wc = _dims(name, route_order=om.ORDER_CANDIDATE)
+    inp = make_inputs(w.dims, L, w.seed, skip=("W", "V", "w_gate_up", "w_down"))
+    a, ga, sa = om.route(w.dims, inp["x"], inp["subkeys"])
+    b, gb, sb = om.route(wc.dims, inp["x"], inp["subkeys"])
+    torch.cuda.synchronize()
+    K = w.dims.top_k
+    a, b = a.cpu().numpy().reshape(-1, K), b.cpu().numpy().reshape(-1, K)
+    oa, ob = np.argsort(a, -1), np.argsort(b, -1)
+    np.testing.assert_array_equal(np.take_along_axis(a, oa, -1), np.take_along_axis(b, ob, -1))
+    for x_, y_ in [(ga, gb), (sa, sb)]:
+        x_, y_ = x_.cpu().numpy().reshape(-1, K), y_.cpu().numpy().reshape(-1, K)
+        np.testing.assert_allclose(np.take_along_axis(x_, oa, -1), np.take_along_axis(y_, ob, -1), atol=1e-6)

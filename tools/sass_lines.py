@@ -1,0 +1,39 @@
+"""Attribute ncu per-SASS samples/instructions to CUDA source lines.
+    python tools/sass_lines.py <nvdisasm --print-line-info output> <ncu --page source --csv> <kernel substr> <src file>"""
+import collections
+import csv
+import re
+import sys
+
+sass, prof, kname, srcf = sys.argv[1:5]
+txt = open(sass).read().split('\n')
+start = [i for i, l in enumerate(txt) if l.startswith('//----') and kname in l][0]
+end = [i for i, l in enumerate(txt[start + 1:], start + 1) if l.startswith('//----')]
+end = end[0] if end else len(txt)
+addr2line, cur = {}, None
+for l in txt[start:end]:
+    m = re.search(r'line (\d+)', l)
+    if l.strip().startswith('//##') and m:
+        cur = int(m.group(1))
+        continue
+    m = re.match(r'\s*/\*([0-9a-f]+)\*/', l)
+    if m and cur is not None:
+        addr2line[int(m.group(1), 16)] = cur
+rows = list(csv.reader(open(prof)))
+h = rows[1]
+ai, si, ii = h.index('Address'), h.index('Warp Stall Sampling (All Samples)'), h.index('Instructions Executed')
+samp, ins, base = collections.Counter(), collections.Counter(), None
+for r in rows[2:]:
+    try:
+        a = int(r[ai], 16)
+    except ValueError:
+        continue
+    base = a if base is None else base
+    ln = addr2line.get(a - base, -1)
+    samp[ln] += float(r[si] or 0)
+    ins[ln] += float(r[ii] or 0)
+tot, toti = sum(samp.values()), sum(ins.values())
+src = open(srcf).read().split('\n')
+print('samples', tot, 'instructions', toti)
+for ln, s_ in samp.most_common(int(sys.argv[5]) if len(sys.argv) > 5 else 30):
+    print(f"{ln:5d} {100 * s_ / tot:5.1f}% samp {100 * ins[ln] / toti:5.1f}% ins | {src[ln - 1].strip()[:100] if ln > 0 else ''}")
