@@ -96,6 +96,9 @@ def rank_info():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
+L2_GATHER_GBS = 14404.1  # measured: random 4 KB row gathers from an L2-resident table (tools/microbench.cu)
+
+
 def a6_algorithmic_bytes(dims, L, n_active, M):
     """a6 algorithmic HBM bytes per launch: W and V rows of every
     active expert once (D_expert) + x read + y_routed fp32 write +
@@ -252,8 +255,10 @@ def bench_single(args, w, lr):
     ews = om.workspace(dims, L, om.WS_EXPERT)
     yr = torch.empty((L, dims.d), dtype=torch.float32, device="cuda")
     stages = {"route_a1_a3": [], "schedule_a4_a5": [], "expert_a6": [], "shared_mlp_a7_a8": []}
+    sliced = dims.v_layout == om.V_SLICED
+    passes = {"a6_pass_z": [], "a6_pass_v": []}
     for i in range(max(4, args.steps)):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
         flush.zero_()
         e[0].record(st)
         idx, gate, _ = om.route(rdims, inp["x"], inp["subkeys"], ws=rws, want_score=False)
@@ -263,7 +268,12 @@ def bench_single(args, w, lr):
         yr.zero_()
         flush.zero_()
         e[3].record(st)
-        om.expert_fwd(dims, inp["x"], inp["W"], inp["V"], plan, y_routed=yr, accumulate=True, ws=ews)
+        if sliced:  # the two passes of the SLICED executor, timed apart
+            om.expert_fwd(dims, inp["x"], inp["W"], inp["V"], plan, y_routed=yr, accumulate=True, ws=ews, passes=1)
+            e[6].record(st)
+            om.expert_fwd(dims, inp["x"], inp["W"], inp["V"], plan, y_routed=yr, accumulate=True, ws=ews, passes=2)
+        else:
+            om.expert_fwd(dims, inp["x"], inp["W"], inp["V"], plan, y_routed=yr, accumulate=True, ws=ews)
         e[4].record(st)
         if dims.d_ff:
             om.shared_mlp(dims, inp["x"], inp["w_gate_up"], inp["w_down"], y_routed=yr, y=y)
@@ -273,7 +283,12 @@ def bench_single(args, w, lr):
             continue
         for k, (a, b) in zip(stages, [(0, 1), (1, 2), (3, 4), (4, 5)]):
             stages[k].append(e[a].elapsed_time(e[b]))
+        if sliced:
+            passes["a6_pass_z"].append(e[3].elapsed_time(e[6]))
+            passes["a6_pass_v"].append(e[6].elapsed_time(e[4]))
     stage_ms = {k: statistics.median(v) for k, v in stages.items()}
+    if sliced:
+        stage_ms.update({k: statistics.median(v) for k, v in passes.items()})
     n_active = int(plan["n_active"].item())
 
     # ---- end to end through the public API with host buffers ----
@@ -304,21 +319,40 @@ def bench_single(args, w, lr):
                "h2d_bytes_per_step": L * dims.d * eb, "d2h_bytes_per_step": L * dims.d * eb}
 
     pk = peaks()
-    a6_bytes = a6_algorithmic_bytes(dims, L, n_active, M)
-    a6_ms = stage_ms["expert_a6"]
-    a6_gbs = a6_bytes / (a6_ms / 1000.0) / 1e9
     B = om.group_size(dims)
-    kern = "expert_group_tma_kernel" if B > 1 else "expert_warp_kernel"
-    if dims.v_layout == om.V_SLICED:
-        kern = "expert_dot_kernel + expert_vslice_kernel"
+    eta = M / max(n_active, 1)
+    other = {}
+    if sliced:
+        # the two kernels of the SLICED executor; the dominant one is the roofline
+        eb = 2
+        zb = n_active * dims.d * eb + L * dims.d * eb + 12 * M + 4 * M              # W rows once, x, plan, a
+        vb = n_active * dims.d * eb + 8 * M + 4 * L * dims.d                       # V rows once, pairs, y write
+        zl2 = M * dims.d * eb + n_active * dims.d * eb + 12 * M                    # x per task + W + plan
+        vl2 = M * dims.d * eb + 8 * M * (dims.d // 32)                             # v slices per task + pairs per slice
+        cand = {"expert_zdot_kernel": (zb, zl2, stage_ms["a6_pass_z"]),
+                "expert_vslice_kernel": (vb, vl2, stage_ms["a6_pass_v"])}
+        kern = max(cand, key=lambda k: cand[k][2])
+        for k, (hb, l2b, kms) in cand.items():
+            other[k] = {"algorithmic_hbm_bytes": hb, "ms": kms, "hbm_gbs": hb / kms / 1e6,
+                        "hbm_frac": hb / kms / 1e6 / pk["hbm"], "l2_bytes_dataflow": l2b,
+                        "l2_gbs": l2b / kms / 1e6, "l2_frac": l2b / kms / 1e6 / L2_GATHER_GBS}
+        a6_bytes, l2_bytes, a6_ms = cand[kern]
+    else:
+        kern = "expert_group_tma_kernel" if B > 1 else "expert_warp_kernel"
+        a6_bytes, a6_ms = a6_algorithmic_bytes(dims, L, n_active, M), stage_ms["expert_a6"]
+        l2_bytes = 2 * M * dims.d * 2
+    a6_gbs = a6_bytes / (a6_ms / 1000.0) / 1e9
     traffic, tsrc = ncu_traffic(w.name, kern)
     roofline = {"bound": "hbm", "achieved": a6_gbs, "peak": pk["hbm"], "unit": "GB/s", "frac": a6_gbs / pk["hbm"],
                 "traffic": traffic, "kernel": f"{kern} (a6)", "algorithmic_bytes_per_launch": a6_bytes,
                 "avg_launch_ms": a6_ms, "peak_source": pk["src"] + " hbm_gbs (copy)",
                 "traffic_source": tsrc,
-                "note": "a6 moves 2d bytes of W and V per task through L2 (runs of one token in one group of "
-                        f"B={B} experts); at eta = M/|E_active| = {M / max(n_active, 1):.1f} the L2 (lts) "
-                        "throughput, not HBM, binds -- profiles/r1/README.md"}
+                "l2": {"bytes_per_launch": l2_bytes, "achieved_gbs": l2_bytes / (a6_ms / 1000.0) / 1e9,
+                       "peak_gbs": L2_GATHER_GBS, "frac": l2_bytes / (a6_ms / 1000.0) / 1e9 / L2_GATHER_GBS,
+                       "peak_source": "tools/microbench.cu l2_gather_4KB_rows_gbs (profiles/r1/microbench.json)"},
+                "note": f"every task moves a d-row of x (pass Z) and of V (pass V) through L2 whatever the loop "
+                        f"order (eta = M/|E_active| = {eta:.1f} tasks share an expert, the only reuse); the binding "
+                        "roofline is L2 -> SM throughput, not HBM -- DESIGN.md §4.4, profiles/r1/README.md"}
     R_ = dims.n_rows + dims.n_cols
     router_ops = 2.0 * L * dims.n_heads * R_ * dims.d
     mlp_flops = 6.0 * L * dims.d * dims.d_ff
@@ -339,6 +373,7 @@ def bench_single(args, w, lr):
         "stage_ms": stage_ms, "n_active": n_active, "tasks": M,
         "step_ms_min_max": [min(step_ms), max(step_ms)],
         "roofline": roofline,
+        "a6_kernels": other,
         "other_rooflines": {
             "router_a1_i8": {"tops_int8": 9 * router_ops / 1e12,
                              "note": "9 int8 limb GEMMs of the exact router (DESIGN.md §4.1)"},

@@ -236,6 +236,14 @@ omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const voi
                                   float* y_routed, int accumulate, void* ws, size_t ws_bytes,
                                   omnimoe_stream_t stream);
 
+/* One pass of the SLICED executor, for measurement (pass 1: Z, writes
+ * plan->task_pair a-values; pass 2: V, reads them and writes y_routed); pass 3 =
+ * omnimoe_expert_fwd.  Arguments as omnimoe_expert_fwd. */
+omnimoe_status omnimoe_expert_fwd_pass(const omnimoe_dims* dims, int64_t L, const void* x,
+                                       const void* W_loc, const void* V_loc, const omnimoe_plan* plan,
+                                       float* y_routed, int accumulate, int pass, void* ws,
+                                       size_t ws_bytes, omnimoe_stream_t stream);
+
 /* V [n][d] (OMNIMOE_V_ROWS) -> V_sliced [d/32][n][32] (OMNIMOE_V_SLICED): a
  * one-time weight re-layout (no arithmetic; bit-exact copy), d % 32 == 0.
  * n = number of expert rows in the table (N, or n_loc for a shard). */

@@ -353,9 +353,13 @@ omnimoe_status omnimoe_schedule(const omnimoe_dims* dims, int64_t M, const int32
                       (cudaStream_t)stream);
 }
 
-omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* W_loc,
-                                  const void* V_loc, const omnimoe_plan* plan, float* y_routed,
-                                  int accumulate, void* ws, size_t ws_bytes, omnimoe_stream_t stream) {
+}  // extern "C"
+
+namespace omni {
+namespace {
+omnimoe_status expert_fwd_impl(const omnimoe_dims* dims, int64_t L, const void* x, const void* W_loc,
+                               const void* V_loc, const omnimoe_plan* plan, float* y_routed, int accumulate,
+                               void* ws, size_t ws_bytes, omnimoe_stream_t stream, int passes) {
   reset_launch_count();
   OMNI_TRY(validate_dims(dims));
   if (L < 0) {
@@ -390,7 +394,31 @@ omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const voi
   }
   OMNI_TRY(check_ws(ws_bytes, expert_ws_bytes(*dims, L), "expert_fwd"));
   OMNI_TRY(check_device());
+  if (passes != 3) {
+    if (dims->v_layout != OMNIMOE_V_SLICED || passes < 1 || passes > 3) {
+      set_error("expert_fwd_pass: pass 1 (Z) or 2 (V) of the SLICED executor only");
+      return OMNIMOE_ERR_INVALID_ARGUMENT;
+    }
+    return expert_sliced_run(*dims, L, x, W_loc, V_loc, *plan, y_routed, accumulate, ws, (cudaStream_t)stream,
+                             passes);
+  }
   return expert_run(*dims, L, x, W_loc, V_loc, *plan, y_routed, accumulate, ws, (cudaStream_t)stream);
+}
+}  // namespace
+}  // namespace omni
+
+extern "C" {
+omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* W_loc,
+                                  const void* V_loc, const omnimoe_plan* plan, float* y_routed,
+                                  int accumulate, void* ws, size_t ws_bytes, omnimoe_stream_t stream) {
+  return expert_fwd_impl(dims, L, x, W_loc, V_loc, plan, y_routed, accumulate, ws, ws_bytes, stream, 3);
+}
+
+omnimoe_status omnimoe_expert_fwd_pass(const omnimoe_dims* dims, int64_t L, const void* x, const void* W_loc,
+                                       const void* V_loc, const omnimoe_plan* plan, float* y_routed,
+                                       int accumulate, int pass, void* ws, size_t ws_bytes,
+                                       omnimoe_stream_t stream) {
+  return expert_fwd_impl(dims, L, x, W_loc, V_loc, plan, y_routed, accumulate, ws, ws_bytes, stream, pass);
 }
 
 omnimoe_status omnimoe_shared_mlp(const omnimoe_dims* dims, int64_t L, const void* x, const void* w_gate_up,

@@ -1186,7 +1186,8 @@ int64_t resolve_token_blocks(const omnimoe_dims& d, int64_t L) {
 }
 
 omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* Vs,
-                                 const omnimoe_plan& plan, float* y, int accumulate, void* ws, cudaStream_t st) {
+                                 const omnimoe_plan& plan, float* y, int accumulate, void* ws, cudaStream_t st,
+                                 int passes) {
   const int64_t n_loc = plan.expert_end - plan.expert_begin;
   int* work = static_cast<int*>(ws);
   if (cudaMemsetAsync(work, 0, 64 * sizeof(int), st) != cudaSuccess) {
@@ -1196,7 +1197,8 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
   const int32_t* m_loc = plan.expert_offsets + n_loc;
   const int d = (int)dm.d;
   omnimoe_status s = OMNIMOE_OK;
-  if (resolve_group_size(dm) == 1) {  // expert-major plan: w_e in registers, x from L2
+  if (!(passes & 1)) {
+  } else if (resolve_group_size(dm) == 1) {  // expert-major plan: w_e in registers, x from L2
     switch ((d + 255) / 256) {
       case 1: s = launch_zdot<1>(d, x, W, plan, dm.act, work, st); break;
       case 2: s = launch_zdot<2>(d, x, W, plan, dm.act, work, st); break;
@@ -1218,6 +1220,7 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
     default: s = launch_dot<8>(d, x, W, plan, m_loc, dm.act, work, st); break;
   }
   OMNI_TRY(s);
+  if (!(passes & 2)) return OMNIMOE_OK;
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_vslice_kernel, 256, 0);
   per_sm = std::max(1, std::min(per_sm, env_int("OMNIMOE_V_BLOCKS", per_sm)));
@@ -1245,7 +1248,7 @@ omnimoe_status pack_v(int64_t n, int d, const void* V, void* Vs, cudaStream_t st
 omnimoe_status expert_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W,
                           const void* V, const omnimoe_plan& plan, float* y, int accumulate,
                           void* ws, cudaStream_t st) {
-  if (dm.v_layout == OMNIMOE_V_SLICED) return expert_sliced_run(dm, L, x, W, V, plan, y, accumulate, ws, st);
+  if (dm.v_layout == OMNIMOE_V_SLICED) return expert_sliced_run(dm, L, x, W, V, plan, y, accumulate, ws, st, 3);
   if (!accumulate) {
     if (cudaMemsetAsync(y, 0, (size_t)L * dm.d * sizeof(float), st) != cudaSuccess) {
       set_error("expert_fwd: memset failed");

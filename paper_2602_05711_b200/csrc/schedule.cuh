@@ -22,6 +22,10 @@ int64_t resolve_v_bands(const omnimoe_dims& d, int64_t n_loc);
 omnimoe_status pack_v(int64_t n, int d, const void* V, void* Vs, cudaStream_t st);
 
 size_t expert_ws_bytes(const omnimoe_dims& d, int64_t L);
+// SLICED executor; passes: bit 0 = pass Z, bit 1 = pass V
+omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* Vs,
+                                 const omnimoe_plan& plan, float* y, int accumulate, void* ws, cudaStream_t st,
+                                 int passes);
 omnimoe_status expert_run(const omnimoe_dims& d, int64_t L, const void* x, const void* W,
                           const void* V, const omnimoe_plan& plan, float* y, int accumulate,
                           void* ws, cudaStream_t st);

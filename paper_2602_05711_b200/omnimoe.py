@@ -53,7 +53,7 @@ EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnim
            "omnimoe_last_launch_count", "omnimoe_status_string", "omnimoe_last_error",
            "omnimoe_group_size", "omnimoe_token_blocks", "omnimoe_ep_pack_workspace_size",
            "omnimoe_ep_pack", "omnimoe_ep_unpack", "omnimoe_ep_combine", "omnimoe_pack_v",
-           "omnimoe_v_bands"]
+           "omnimoe_v_bands", "omnimoe_expert_fwd_pass"]
 
 _lib = None
 
@@ -73,6 +73,7 @@ def load(path: str = LIB_PATH):
         "omnimoe_route": [PD, I64, V, V, V, V, V, V, SZ, V],
         "omnimoe_schedule": [PD, I64, V, V, V, PP, V, SZ, V],
         "omnimoe_expert_fwd": [PD, I64, V, V, V, PP, V, I32, V, SZ, V],
+        "omnimoe_expert_fwd_pass": [PD, I64, V, V, V, PP, V, I32, I32, V, SZ, V],
         "omnimoe_shared_mlp": [PD, I64, V, V, V, V, V, V, SZ, V],
         "omnimoe_layer_fwd": [PD, I64, V, V, V, V, V, V, V, V, V, V, SZ, V],
         "omnimoe_router_logits": [PD, I64, V, V, V, I32, V, SZ, V],
@@ -273,7 +274,9 @@ def pack_v(dims: LayerDims, V):
     return out
 
 
-def expert_fwd(dims: LayerDims, x, W_loc, V_loc, plan, y_routed=None, accumulate=False, ws=None):
+def expert_fwd(dims: LayerDims, x, W_loc, V_loc, plan, y_routed=None, accumulate=False, ws=None, passes=3):
+    """passes: 3 = the whole routed branch; 1 / 2 = pass Z / pass V of the SLICED
+    executor alone (measurement, omnimoe_expert_fwd_pass)."""
     L = x.shape[0]
     n_loc = plan["expert_end"] - plan["expert_begin"]
     _req(x, "x", dims.torch_dtype, L * dims.d)
@@ -285,9 +288,14 @@ def expert_fwd(dims: LayerDims, x, W_loc, V_loc, plan, y_routed=None, accumulate
     _req(y_routed, "y_routed", torch.float32, L * dims.d)
     ws = ws if ws is not None else workspace(dims, L, WS_EXPERT, x.device)
     dc, cp = dims.c(), _cplan(plan)
-    _check(load().omnimoe_expert_fwd(ctypes.byref(dc), L, _ptr(x), _ptr(W_loc), _ptr(V_loc),
-                                     ctypes.byref(cp), _ptr(y_routed), int(accumulate), _ptr(ws),
-                                     ws.numel(), _stream()), "expert_fwd")
+    if passes == 3:
+        _check(load().omnimoe_expert_fwd(ctypes.byref(dc), L, _ptr(x), _ptr(W_loc), _ptr(V_loc),
+                                         ctypes.byref(cp), _ptr(y_routed), int(accumulate), _ptr(ws),
+                                         ws.numel(), _stream()), "expert_fwd")
+    else:
+        _check(load().omnimoe_expert_fwd_pass(ctypes.byref(dc), L, _ptr(x), _ptr(W_loc), _ptr(V_loc),
+                                              ctypes.byref(cp), _ptr(y_routed), int(accumulate), int(passes),
+                                              _ptr(ws), ws.numel(), _stream()), "expert_fwd_pass")
     return y_routed
 
 
