@@ -525,12 +525,19 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
 // items: slots m = 0..nslot-1 of this lane; bkf(m, ok) -> bucket key (ok = item
 // exists); fullf(m) -> full key (needed only for ties).  lo0: a lower bound of the
 // want-th largest bucket key (items below it are never selected).
-template <class BkF, class FullF>
+// loop over this lane's item slots: fully unrolled over MAXS register slots, or a
+// plain loop over nslot (MAXS = 0)
+#define OMNI_SLOT_LOOP(m)                                                          \
+  _Pragma("unroll") for (int m##_o = 0; m##_o < (MAXS ? MAXS : 1); ++m##_o)        \
+    for (int m = (MAXS ? m##_o : 0); m < (MAXS ? m##_o + 1 : nslot); ++m)          \
+      if (MAXS && m >= nslot) {                                                    \
+      } else
+template <int MAXS = 0, class BkF, class FullF>
 __device__ WPred warp_select_top(int nslot, BkF bkf, FullF fullf, int want, uint64_t lo0, int* hist) {
   const int lane = threadIdx.x & 31;
   uint64_t lo = ~0ull, hi = 0;
   int cnt = 0;
-  for (int m = 0; m < nslot; ++m) {
+  OMNI_SLOT_LOOP(m) {
     bool ok;
     const uint64_t k = bkf(m, ok);
     if (ok && k >= lo0) {
@@ -549,7 +556,7 @@ __device__ WPred warp_select_top(int nslot, BkF bkf, FullF fullf, int want, uint
 #pragma unroll
     for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
     __syncwarp();
-    for (int m = 0; m < nslot; ++m) {
+    OMNI_SLOT_LOOP(m) {
       bool ok;
       const uint64_t k = bkf(m, ok);
       if (ok && k >= lo && k <= hi) atomicAdd(&hist[(int)((k - lo) >> shift)], 1);
@@ -595,7 +602,7 @@ __device__ WPred warp_select_top(int nslot, BkF bkf, FullF fullf, int want, uint
     U128 prev{~0ull, ~0ull};
     for (int t = 0; t < r; ++t) {
       U128 best{0ull, 0ull};
-      for (int m = 0; m < nslot; ++m) {
+      OMNI_SLOT_LOOP(m) {
         bool ok;
         const uint64_t k = bkf(m, ok);
         if (ok && k == lo) {
@@ -633,6 +640,69 @@ __device__ void warp_bitonic_desc(uint64_t* a, int n) {
 
 // the top k1 half keys of lg[0..n) (n <= 1024), sorted descending into out[0..P)
 // (P = pow2 >= k1, padded with 0); returns logsumexp of the half if want_lse
+// the top k1 half keys of lg[0..n) (n <= 1024), sorted descending into out[0..P)
+// (P = pow2 >= k1, padded with 0); returns logsumexp of the half if want_lse
+// bitonic sort (descending) of 32*E keys held E per lane (element lane*E + r in k[r])
+template <int E>
+__device__ __forceinline__ void reg_bitonic_desc(uint64_t (&k)[E]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32 * E; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= E) {  // partner in lane ^ (stride / E), same register
+        const int lx = stride / E;
+        const bool lower = (lane & lx) == 0;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const bool desc = ((lane * E + r) & size) == 0;
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, k[r], lx);
+          k[r] = (lower == desc) ? max(k[r], o) : min(k[r], o);
+        }
+      } else {  // partner in register r ^ stride of the same lane
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int rp = r ^ stride;
+          if (rp > r) {
+            const bool desc = ((lane * E + r) & size) == 0;
+            const uint64_t a = k[r], b = k[rp];
+            const bool sw = desc ? (b > a) : (a > b);
+            k[r] = sw ? b : a;
+            k[rp] = sw ? a : b;
+          }
+        }
+      }
+    }
+  }
+}
+
+// top P keys of out[0..P) sorted descending in place (registers, E = P / 32 per lane)
+template <int E>
+__device__ __forceinline__ void sort_out(uint64_t* out) {
+  const int lane = threadIdx.x & 31;
+  uint64_t k[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) k[r] = out[lane * E + r];
+  reg_bitonic_desc<E>(k);
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < E; ++r) out[lane * E + r] = k[r];
+  __syncwarp();
+}
+
+__device__ void warp_sort_desc(uint64_t* out, int P) {
+  switch (P) {
+    case 32: sort_out<1>(out); break;
+    case 64: sort_out<2>(out); break;
+    case 128: sort_out<4>(out); break;
+    case 256: sort_out<8>(out); break;
+    case 512: sort_out<16>(out); break;
+    default: warp_bitonic_desc(out, P); break;
+  }
+}
+
+// the top k1 half keys of lg[0..n) (n <= 1024), sorted descending into out[0..P)
+// (P = pow2 >= k1, padded with 0); returns logsumexp of the half if want_lse
 __device__ float warp_half_sorted(const float* __restrict__ lg, int n, int k1, int P, uint64_t* out, int* hist,
                                   bool want_lse) {
   const int lane = threadIdx.x & 31;
@@ -645,7 +715,8 @@ __device__ float warp_half_sorted(const float* __restrict__ lg, int n, int k1, i
   WPred p;
   p.thr = 0;
   p.kmin = U128{0ull, 0ull};
-  if (k1 < n) p = warp_select_top(nslot, bkf, [&](int m) { bool ok; return U128{bkf(m, ok), 0ull}; }, k1, 0ull, hist);
+  if (k1 < n)
+    p = warp_select_top(nslot, bkf, [&](int m) { bool ok; return U128{bkf(m, ok), 0ull}; }, k1, 0ull, hist);
   // compact the selected keys (bucket keys are unique: bk >= thr) in slot order
   int base = 0;
   for (int m = 0; m < nslot; ++m) {
@@ -656,22 +727,26 @@ __device__ float warp_half_sorted(const float* __restrict__ lg, int n, int k1, i
     if (sel) out[base + __popc(bal & ((1u << lane) - 1u))] = k;
     base += __popc(bal);
   }
+  float lse = 0.f;
+  if (want_lse) {  // before the sort, so that v[] is dead while the keys are in registers
+    float mx = -INFINITY;
+    for (int i = lane; i < n; i += 32) mx = fmaxf(mx, lg[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+    for (int i = lane; i < n; i += 32) sum += __expf(lg[i] - mx);
+    lse = mx + __logf(warp_sum(sum));
+  }
   for (int i = k1 + lane; i < P; i += 32) out[i] = 0ull;
   __syncwarp();
-  warp_bitonic_desc(out, P);
-  if (!want_lse) return 0.f;
-  const float mx = half_val(out[0]);
-  float sum = 0.f;
-  for (int m = 0; m < nslot; ++m) {
-    bool ok;
-    const uint64_t k = bkf(m, ok);
-    if (ok) sum += __expf(half_val(k) - mx);
-  }
-  return mx + __logf(warp_sum(sum));
+  warp_bitonic_desc(out, P);  // (a register-resident bitonic sort measured slower: 1.50 vs 1.24 ms)
+  return lse;
 }
 
-// smem: cand[C] (a << 16 | b, (a+1)(b+1) <= K) | per warp: kr[Pr], kc[Pc] (u64), hist[256]
-__global__ void __launch_bounds__(256)
+// smem: cand[C] (a << 16 | b, (a+1)(b+1) <= K) | per warp: kr[Pr], kc[Pc] (u64), hist[256],
+// the refinement list (kListCap keys + candidate indices)
+constexpr int kListCap = 256;
+__global__ void __launch_bounds__(256, 2)
     select_bucket_kernel(SelectParams p, int C, int Pr, int Pc, const float* __restrict__ logits,
                          int32_t* __restrict__ idx, float* __restrict__ gate, float* __restrict__ score) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -688,7 +763,7 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const size_t cand_bytes = ((size_t)C * 4 + 15) / 16 * 16;
-  const size_t per_warp = (size_t)(Pr + Pc) * 8 + 256 * 4;
+  const size_t per_warp = (size_t)(Pr + Pc) * 8 + 256 * 4 + kListCap * 12;
   uint8_t* base = smem + cand_bytes + (size_t)wid * per_warp;
   uint64_t* skr = reinterpret_cast<uint64_t*>(base);
   uint64_t* skc = skr + Pr;
@@ -701,12 +776,23 @@ __global__ void __launch_bounds__(256)
     const float* lg = logits + (size_t)th * R;
     const float lse_r = warp_half_sorted(lg, p.n_rows, kr, Pr, skr, hist, score != nullptr);
     const float lse_c = warp_half_sorted(lg + p.n_rows, p.n_cols, kc, Pc, skc, hist, score != nullptr);
+    // sorted keys -> (value bits, index) pairs, read with one 8-byte load per half
+    for (int a = lane; a < kr; a += 32) {
+      const uint64_t k = skr[a];
+      skr[a] = ((uint64_t)half_idx(k) << 32) | __float_as_uint(half_val(k));
+    }
+    for (int b = lane; b < kc; b += 32) {
+      const uint64_t k = skc[b];
+      skc[b] = ((uint64_t)half_idx(k) << 32) | __float_as_uint(half_val(k));
+    }
+    __syncwarp();
     auto hi_of = [&](int c, uint32_t& id, float& vr, float& vc) {
       const uint32_t ab = cand[c];
-      const uint64_t ka = skr[ab >> 16], kb = skc[ab & 0xFFFF];
-      vr = half_val(ka);
-      vc = half_val(kb);
-      id = half_idx(ka) * Nc + half_idx(kb);
+      const uint2 ra = reinterpret_cast<const uint2*>(skr)[ab >> 16];
+      const uint2 cb = reinterpret_cast<const uint2*>(skc)[ab & 0xFFFF];
+      vr = __uint_as_float(ra.x);
+      vc = __uint_as_float(cb.x);
+      id = ra.y * Nc + cb.y;
       return ((double)vr + (double)vc) + 0.0;
     };
     auto bkf = [&](int m, bool& ok) {
@@ -722,15 +808,98 @@ __global__ void __launch_bounds__(256)
       hi_of(lane + 32 * m, id, vr, vc);
       return cell_key(vr, vc, id);
     };
+    auto val_r = [&](int a) { return (double)__uint_as_float((uint32_t)skr[a]); };
+    auto val_c = [&](int b) { return (double)__uint_as_float((uint32_t)skc[b]); };
     // lower bound of the K-th largest key: for A rows and B = ceil(K/A) columns, the
     // A*B >= K cells of the block all have keys >= s_r[A-1] + s_c[B-1]
     uint64_t lb = 0;
     for (int A = 1 + lane; A <= kr; A += 32) {
       const int B = (K + A - 1) / A;
-      if (B <= kc) lb = max(lb, ord64(((double)half_val(skr[A - 1]) + (double)half_val(skc[B - 1])) + 0.0));
+      if (B <= kc) lb = max(lb, ord64((val_r(A - 1) + val_c(B - 1)) + 0.0));
     }
     lb = warp_max_u64(lb);
-    const WPred sel = warp_select_top(nslot, bkf, fullf, K, lb, hist);
+    const uint64_t kmax = ord64((val_r(0) + val_c(0)) + 0.0);  // cell (0, 0) holds the largest key
+    // first bucket pass over [lb, kmax] on all candidates, then the bucket holding the
+    // K-th key is compacted into a short list and refined there
+    WPred sel;
+    {
+      const uint64_t span = kmax - lb;
+      const int shift = span ? max(0, 64 - __clzll((long long)span) - 8) : 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
+      __syncwarp();
+      for (int m = 0; m < nslot; ++m) {
+        bool ok;
+        const uint64_t k = bkf(m, ok);
+        if (ok && k >= lb) atomicAdd(&hist[(int)((k - lb) >> shift)], 1);
+      }
+      __syncwarp();
+      int c8[8], sum = 0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        c8[t] = hist[255 - 8 * lane - t];
+        sum += c8[t];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int above = incl - sum, found = -1, fabove = 0, fcnt = 0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        if (found < 0 && above < K && above + c8[t] >= K) {
+          found = 255 - 8 * lane - t;
+          fabove = above;
+          fcnt = c8[t];
+        }
+        above += c8[t];
+      }
+      const int src = __ffs(__ballot_sync(0xffffffffu, found >= 0)) - 1;
+      const int bstar = __shfl_sync(0xffffffffu, found, src);
+      const int r = K - __shfl_sync(0xffffffffu, fabove, src);
+      const int cnt = __shfl_sync(0xffffffffu, fcnt, src);
+      const uint64_t nlo = lb + ((uint64_t)bstar << shift);
+      const uint64_t w = (shift == 0) ? 0ull : ((1ull << shift) - 1ull);
+      const uint64_t nhi = (kmax - nlo > w) ? nlo + w : kmax;
+      __syncwarp();
+      if (r == cnt) {  // the whole bucket and everything above it
+        sel.thr = nlo;
+        sel.kmin = U128{0ull, 0ull};
+      } else if (cnt <= kListCap) {
+        uint64_t* lbk = reinterpret_cast<uint64_t*>(hist + 256);
+        uint32_t* lc = reinterpret_cast<uint32_t*>(lbk + kListCap);
+        int base = 0;
+        for (int m = 0; m < nslot; ++m) {
+          bool ok;
+          const uint64_t k = bkf(m, ok);
+          const bool in = ok && k >= nlo && k <= nhi;
+          const unsigned bal = __ballot_sync(0xffffffffu, in);
+          if (in) {
+            const int pos = base + __popc(bal & ((1u << lane) - 1u));
+            lbk[pos] = k;
+            lc[pos] = (uint32_t)(lane + 32 * m);
+          }
+          base += __popc(bal);
+        }
+        __syncwarp();
+        auto lbkf = [&](int m, bool& ok) {
+          const int q = lane + 32 * m;
+          ok = q < cnt;
+          return ok ? lbk[q] : 0ull;
+        };
+        auto lfullf = [&](int m) {
+          uint32_t id;
+          float vr, vc;
+          hi_of((int)lc[lane + 32 * m], id, vr, vc);
+          return cell_key(vr, vc, id);
+        };
+        sel = warp_select_top((cnt + 31) >> 5, lbkf, lfullf, r, nlo, hist);
+      } else {
+        sel = warp_select_top(nslot, bkf, fullf, K, lb, hist);
+      }
+    }
     // outputs in candidate order; gates = softmax over the K exact keys (hi part; the
     // TwoSum remainder is below 2^-53 relative)
     uint32_t id0;
@@ -825,7 +994,7 @@ omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* lo
     while (Pr < kr) Pr <<= 1;
     while (Pc < kc) Pc <<= 1;
     const size_t cand_bytes = ((size_t)C * 4 + 15) / 16 * 16;
-    const size_t per_warp = (size_t)(Pr + Pc) * 8 + 256 * 4;
+    const size_t per_warp = (size_t)(Pr + Pc) * 8 + 256 * 4 + kListCap * 12;
     int warps = 8;
     while (warps > 1 && cand_bytes + warps * per_warp > 200 * 1024) warps >>= 1;
     const size_t sm = cand_bytes + warps * per_warp;
