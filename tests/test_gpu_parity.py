@@ -401,11 +401,19 @@ def v_band_kb(request, monkeypatch):
     return request.param
 
 
+@pytest.fixture(params=["auto", "warp"])
+def v_mode(request, monkeypatch):
+    """pass V kernel: auto (8 tokens per warp for h*K <= 64) or forced one token per warp."""
+    if request.param == "warp":
+        monkeypatch.setenv("OMNIMOE_V_GROUP_MAX_TASKS", "0")
+    return request.param
+
+
 @pytest.mark.parametrize("B", [0, 2, 512])
 @pytest.mark.parametrize("d,act", [(64, om.SILU), (96, om.SILU), (1024, om.SILU), (2048, om.SILU),
                                    (64, om.IDENTITY)])
 @pytest.mark.parametrize("accumulate", [False, True])
-def test_expert_fwd_sliced_given_plan(d, act, B, accumulate, v_band_kb):
+def test_expert_fwd_sliced_given_plan(d, act, B, accumulate, v_band_kb, v_mode):
     rng = np.random.default_rng(d + B)
     L, N, HK = 200, 3000, 12
     dims = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, act=act, group_size=B, v_layout=om.V_SLICED)
@@ -432,7 +440,7 @@ def test_expert_fwd_sliced_given_plan(d, act, B, accumulate, v_band_kb):
     assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
 
 
-def test_expert_fwd_sliced_shard_and_empty_tokens(v_band_kb):
+def test_expert_fwd_sliced_shard_and_empty_tokens(v_band_kb, v_mode):
     """Expert range of a shard (tasks outside it are skipped) and tokens with no
     tasks in range (their y_routed rows are written as zeros)."""
     rng = np.random.default_rng(3)
@@ -460,7 +468,7 @@ def test_expert_fwd_sliced_shard_and_empty_tokens(v_band_kb):
 
 @pytest.mark.parametrize("mode", [synth.NORMAL, synth.DYADIC])
 @pytest.mark.parametrize("B", [0, 5])
-def test_layer_c1_sliced(mode, B, v_band_kb):
+def test_layer_c1_sliced(mode, B, v_band_kb, v_mode):
     w = _dims("C1", group_size=B, v_layout=om.V_SLICED)
     dims = w.dims
     inp = make_inputs(dims, w.L, w.seed, mode)
