@@ -1044,11 +1044,16 @@ __global__ void __launch_bounds__(256)
     const __nv_bfloat16* vs = Vs + (size_t)s * n_loc * 32 + c4 * 8;
     const int nmax = __reduce_max_sync(0xffffffffu, n);
     unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
+    int2 nx[8];  // the (expert, a) pairs of the next 8 tasks, loaded one step ahead
+#pragma unroll
+    for (int t = 0; t < 8; ++t) nx[t] = t < n ? ld_pair(task_pair + 2 * (size_t)(beg + t), pol) : make_int2(-1, 0);
     for (int q = 0; q < nmax; q += 8) {
       int2 pr[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t)
-        pr[t] = q + t < n ? ld_pair(task_pair + 2 * (size_t)(beg + q + t), pol) : make_int2(-1, 0);
+      for (int t = 0; t < 8; ++t) {
+        pr[t] = nx[t];
+        nx[t] = q + 8 + t < n ? ld_pair(task_pair + 2 * (size_t)(beg + q + 8 + t), pol) : make_int2(-1, 0);
+      }
       uint4 v[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) v[t] = pr[t].x >= 0 ? ld_vec(vs + (size_t)pr[t].x * 32) : make_uint4(0, 0, 0, 0);
