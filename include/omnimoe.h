@@ -323,6 +323,16 @@ omnimoe_status omnimoe_ep_combine(const omnimoe_dims* dims, int64_t L, int32_t R
                                   const int32_t* inv, const int64_t* tok_off, float* y_routed,
                                   omnimoe_stream_t stream);
 
+/* Load metrics of a plan's routing (after PKM / PEER): with c_e the
+ * task count of local expert e (plan->expert_offsets), M = sum c_e, n = n_loc and
+ * z_e = c_e / M:  stats[0] = Expert Usage = |{e : c_e > 0}| / n,
+ *                 stats[1] = Unevenness = D_KL(z || U) = sum_{c_e > 0} z_e log(n z_e).
+ * stats: device fp64[2]; ws: omnimoe_load_stats_workspace_size() bytes.  Summation
+ * order is fixed (deterministic). */
+omnimoe_status omnimoe_load_stats(const omnimoe_plan* plan, double* stats, void* ws, size_t ws_bytes,
+                                  omnimoe_stream_t stream);
+size_t omnimoe_load_stats_workspace_size(void);
+
 /* Number of kernel launches the last successful call on this thread enqueued. */
 int omnimoe_last_launch_count(void);
 

@@ -43,11 +43,14 @@ def lib():
         _lib.oracle_routed_token_centric.argtypes = [i64, i64, i64, P, P, P, P, P, c_int, P, c_int]
         _lib.oracle_routed_expert_centric.argtypes = [i64, i64, i64, P, P, P, P, P, P, c_int, P]
         _lib.oracle_shared_mlp.argtypes = [i64, i64, i64, P, P, P, P, c_int]
+        _lib.oracle_load_stats.argtypes = [i64, P, P]
+        _lib.oracle_dense_route.argtypes = [i64, i64, i64, P, c_int, P, P, P, P]
         _lib.oracle_layer.argtypes = [i64, i64, i64, i64, i64, i64, i64, P, P, P, P, P, i64, P, P,
                                       c_int, P, P, P, c_int]
         for f in ("oracle_logits", "oracle_route", "oracle_schedule", "oracle_routed_grouped",
                   "oracle_routed_token_centric",
-                  "oracle_routed_expert_centric", "oracle_shared_mlp", "oracle_layer"):
+                  "oracle_routed_expert_centric", "oracle_shared_mlp", "oracle_layer", "oracle_load_stats",
+                  "oracle_dense_route"):
             getattr(_lib, f).restype = None
     return _lib
 
@@ -94,6 +97,25 @@ def route(logit_rows, n_rows, n_cols, K, method=PRODUCT, bsel=4096, nthreads=Non
     lib().oracle_route(T, n_rows, n_cols, K, _p(lg), method, bsel, nthreads or default_threads(),
                        _p(out["idx"]), _p(out["gate"]), _p(out["score"]), _p(out["key_hi"]),
                        _p(out["key_lo"]), _p(out["gap"]))
+    return out
+
+
+def load_stats(counts):
+    """(Expert Usage, Unevenness) of per-expert task counts."""
+    c = np.ascontiguousarray(counts, dtype=np.int64).reshape(-1)
+    out = np.zeros(2)
+    lib().oracle_load_stats(c.size, _p(c), _p(out))
+    return float(out[0]), float(out[1])
+
+
+def dense_route(logit_rows, K, nthreads=None):
+    """Ablation 'w/o CPR': exact top-K of dense scores [T][N] by (value
+    desc, id asc); dict(idx, gate, key, gap)."""
+    lg = np.ascontiguousarray(logit_rows, dtype=np.float32)
+    T, N = lg.shape
+    out = dict(idx=np.empty((T, K), np.int32), gate=np.empty((T, K)), key=np.empty((T, K)), gap=np.empty(T))
+    lib().oracle_dense_route(T, N, K, _p(lg), nthreads or default_threads(), _p(out["idx"]), _p(out["gate"]),
+                             _p(out["key"]), _p(out["gap"]))
     return out
 
 

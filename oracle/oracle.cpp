@@ -224,6 +224,52 @@ void select_blockmerge(const float* sr, int64_t Nr, const float* sc, int64_t Nc,
 
 extern "C" {
 
+// Load metrics of a routing decision (following PKM/PEER): with
+// z_i = c_i / M the normalised retrieval frequency of expert i (c_i tasks, M
+// tasks in total, N experts),
+//   Expert Usage = |{i : z_i > 0}| / N
+//   Unevenness   = D_KL(z || U) = sum_{i: z_i > 0} z_i log(N z_i).
+// out[0] = usage, out[1] = unevenness (0, 0 when M = 0).
+void oracle_load_stats(int64_t N, const int64_t* counts, double* out) {
+  int64_t M = 0, used = 0;
+  for (int64_t i = 0; i < N; ++i) {
+    M += counts[i];
+    used += counts[i] > 0;
+  }
+  double kl = 0.0;
+  for (int64_t i = 0; i < N; ++i)
+    if (counts[i] > 0) {
+      const double z = (double)counts[i] / (double)M;
+      kl += z * std::log((double)N * z);
+    }
+  out[0] = M > 0 ? (double)used / (double)N : 0.0;
+  out[1] = M > 0 ? kl : 0.0;
+}
+
+// The ablation "w/o Cartesian Product Router": a dense routing
+// projection scores every expert, s = x W_g (logits [T][N] fp32), and the
+// router takes the exact top-K of the N scores by (value desc, id asc) (the
+// tie rule of Q7), gates = softmax over the selected (Eq.Gate).
+// Brute force: sort all N.  gap[t] = s_K - s_{K+1} (+inf when K == N).
+void oracle_dense_route(int64_t T, int64_t N, int64_t K, const float* logits, int nthreads, int32_t* idx,
+                        double* gate, double* key, double* gap) {
+  parallel_for(T, nthreads, [&](int64_t t) {
+    const float* s = logits + t * N;
+    std::vector<int64_t> ord(N);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return s[a] > s[b]; });
+    const double k1 = s[ord[0]];
+    double den = 0.0;
+    for (int64_t k = 0; k < K; ++k) den += std::exp((double)s[ord[k]] - k1);
+    for (int64_t k = 0; k < K; ++k) {
+      idx[t * K + k] = (int32_t)ord[k];
+      key[t * K + k] = s[ord[k]];
+      gate[t * K + k] = std::exp((double)s[ord[k]] - k1) / den;
+    }
+    gap[t] = K < N ? (double)s[ord[K - 1]] - (double)s[ord[K]] : INFINITY;
+  });
+}
+
 // O1 logits (Eq.Logits; reading Q9): for each token l, head h
 // and sub-key row r (rows [0,N_r) are W_r's columns, rows [N_r, N_r+N_c) are
 // W_c's), s = RN32(sum_k x[l][k]*sub[h][r][k]) -- the fp32 round-to-nearest-

@@ -649,6 +649,24 @@ omnimoe_status omnimoe_ep_combine(const omnimoe_dims* dims, int64_t L, int32_t R
   return ep_combine(y_ret, inv, tok_off, L, (int)dims->d, R, y_routed, (cudaStream_t)stream);
 }
 
+omnimoe_status omnimoe_load_stats(const omnimoe_plan* plan, double* stats, void* ws, size_t ws_bytes,
+                                  omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_NONNULL(plan, "plan");
+  OMNI_NONNULL(plan->expert_offsets, "plan.expert_offsets");
+  OMNI_NONNULL(stats, "stats");
+  OMNI_NONNULL(ws, "ws");
+  if (plan->expert_end <= plan->expert_begin) {
+    set_error("load_stats: empty expert range");
+    return OMNIMOE_ERR_SHAPE;
+  }
+  OMNI_TRY(check_ws(ws_bytes, load_stats_ws_bytes(), "load_stats"));
+  OMNI_TRY(check_device());
+  return load_stats_run(*plan, stats, ws, (cudaStream_t)stream);
+}
+
+size_t omnimoe_load_stats_workspace_size(void) { return load_stats_ws_bytes(); }
+
 int omnimoe_last_launch_count(void) { return g_launches; }
 
 int64_t omnimoe_group_size(const omnimoe_dims* dims) {

@@ -323,12 +323,67 @@ __global__ void gather_plan_kernel(const int32_t* __restrict__ order, int64_t M,
   }
 }
 
+// load metrics of a plan: per block, in a fixed order, the number of
+// used experts and sum_{c>0} (c/M) log(n_loc c / M) over the block's experts
+__global__ void __launch_bounds__(256)
+    load_stats_kernel(const int32_t* __restrict__ off, int64_t n_loc, double* __restrict__ partial) {
+  __shared__ double su[256], sk[256];
+  const double M = (double)off[n_loc];
+  double used = 0.0, kl = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_loc; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = off[e + 1] - off[e];
+    if (c > 0) {
+      const double z = (double)c / M;
+      used += 1.0;
+      kl += z * log((double)n_loc * z);
+    }
+  }
+  su[threadIdx.x] = used;
+  sk[threadIdx.x] = kl;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      su[threadIdx.x] += su[threadIdx.x + o];
+      sk[threadIdx.x] += sk[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = su[0];
+    partial[2 * blockIdx.x + 1] = sk[0];
+  }
+}
+
+__global__ void load_stats_final_kernel(const double* __restrict__ partial, int nblk, int64_t n_loc,
+                                        const int32_t* __restrict__ off, double* __restrict__ out) {
+  double u = 0.0, k = 0.0;
+  for (int b = 0; b < nblk; ++b) {
+    u += partial[2 * b];
+    k += partial[2 * b + 1];
+  }
+  const bool any = off[n_loc] > 0;
+  out[0] = any ? u / (double)n_loc : 0.0;
+  out[1] = any ? k : 0.0;
+}
+
 int grid_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
   return (int)std::min<int64_t>(std::max<int64_t>(b, 1), kSMs * 16);
 }
 
 }  // namespace
+
+size_t load_stats_ws_bytes() { return 2 * kSMs * 2 * sizeof(double); }
+
+omnimoe_status load_stats_run(const omnimoe_plan& plan, double* out, void* ws, cudaStream_t st) {
+  const int64_t n_loc = plan.expert_end - plan.expert_begin;
+  const int nblk = kSMs * 2;
+  load_stats_kernel<<<nblk, 256, 0, st>>>(plan.expert_offsets, n_loc, static_cast<double*>(ws));
+  OMNI_CHECK_LAUNCH("load_stats_kernel");
+  load_stats_final_kernel<<<1, 1, 0, st>>>(static_cast<const double*>(ws), nblk, n_loc, plan.expert_offsets, out);
+  OMNI_CHECK_LAUNCH("load_stats_final_kernel");
+  return OMNIMOE_OK;
+}
 
 size_t schedule_ws_bytes(int64_t M, int64_t n_loc) {
   Carver c(nullptr);

@@ -5,7 +5,10 @@
 
 namespace omni {
 
-size_t schedule_ws_bytes(int64_t M, int64_t n_loc);  // + M + 1 ints of V-order scratch
+size_t schedule_ws_bytes(int64_t M, int64_t n_loc);
+// Expert Usage / Unevenness of a plan -> out[2] (device fp64)
+size_t load_stats_ws_bytes();
+omnimoe_status load_stats_run(const omnimoe_plan& plan, double* out, void* ws, cudaStream_t st);  // + M + 1 ints of V-order scratch
 // hk = h*K: default token of task t is t / hk when token == nullptr.
 omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, const int32_t* token,
                             int64_t hk, const omnimoe_plan& plan, int64_t B, int64_t Tb, int64_t n_bands,

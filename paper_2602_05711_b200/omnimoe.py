@@ -53,7 +53,8 @@ EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnim
            "omnimoe_last_launch_count", "omnimoe_status_string", "omnimoe_last_error",
            "omnimoe_group_size", "omnimoe_token_blocks", "omnimoe_ep_pack_workspace_size",
            "omnimoe_ep_pack", "omnimoe_ep_unpack", "omnimoe_ep_combine", "omnimoe_pack_v",
-           "omnimoe_v_bands", "omnimoe_expert_fwd_pass"]
+           "omnimoe_v_bands", "omnimoe_expert_fwd_pass", "omnimoe_load_stats",
+           "omnimoe_load_stats_workspace_size"]
 
 _lib = None
 
@@ -83,6 +84,7 @@ def load(path: str = LIB_PATH):
         "omnimoe_ep_unpack": [I64, I32, V, V, V, V, V, V, V],
         "omnimoe_ep_combine": [PD, I64, I32, V, V, V, V, V],
         "omnimoe_pack_v": [PD, I64, V, V, V],
+        "omnimoe_load_stats": [PP, V, V, SZ, V],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -91,6 +93,8 @@ def load(path: str = LIB_PATH):
     lib.omnimoe_last_launch_count.restype = ctypes.c_int
     lib.omnimoe_group_size.argtypes = [PD]
     lib.omnimoe_group_size.restype = ctypes.c_int64
+    lib.omnimoe_load_stats_workspace_size.restype = ctypes.c_size_t
+    lib.omnimoe_load_stats_workspace_size.argtypes = []
     lib.omnimoe_v_bands.argtypes = [PD, ctypes.c_int64]
     lib.omnimoe_v_bands.restype = ctypes.c_int64
     lib.omnimoe_token_blocks.argtypes = [PD, ctypes.c_int64]
@@ -262,6 +266,18 @@ def schedule(dims: LayerDims, idx, gate, token=None, expert_begin=0, expert_end=
     _check(load().omnimoe_schedule(ctypes.byref(dc), M, _ptr(idx), _ptr(gate), _ptr(token),
                                    ctypes.byref(cp), _ptr(ws), ws.numel(), _stream()), "schedule")
     return plan
+
+
+def load_stats(plan):
+    """(Expert Usage, Unevenness) of a plan's routing as a device
+    fp64 tensor [2] (omnimoe_load_stats)."""
+    lib = load()
+    dev = plan["expert_offsets"].device
+    out = torch.empty(2, dtype=torch.float64, device=dev)
+    ws = torch.empty(lib.omnimoe_load_stats_workspace_size(), dtype=torch.uint8, device=dev)
+    cp = _cplan(plan)
+    _check(lib.omnimoe_load_stats(ctypes.byref(cp), _ptr(out), _ptr(ws), ws.numel(), _stream()), "load_stats")
+    return out
 
 
 def pack_v(dims: LayerDims, V):

@@ -539,3 +539,16 @@ def test_route_candidate_order(name, L):
     for x_, y_ in [(ga, gb), (sa, sb)]:
         x_, y_ = x_.cpu().numpy().reshape(-1, K), y_.cpu().numpy().reshape(-1, K)
         np.testing.assert_allclose(np.take_along_axis(x_, oa, -1), np.take_along_axis(y_, ob, -1), atol=1e-6)
+
+
+# ---------------------------------------------------------------- N1: load metrics
+@pytest.mark.parametrize("N,M,skew", [(1024, 2048, 0.0), (1 << 20, 1 << 20, 0.0), (4096, 50000, 2.0)])
+def test_load_stats_match_oracle(N, M, skew):
+    rng = np.random.default_rng(N + M)
+    p = rng.random(N) ** (1 + 8 * skew)
+    ids = rng.choice(N, M, p=p / p.sum()).astype(np.int32)
+    d = om.LayerDims(d=8, n_rows=N, n_cols=1, top_k=1, d_ff=0, group_size=1)
+    plan = om.schedule(d, torch.from_numpy(ids).cuda(), torch.ones(M, device="cuda"))
+    got = om.load_stats(plan).cpu().numpy()
+    want = oracle.load_stats(np.bincount(ids, minlength=N))
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-15)

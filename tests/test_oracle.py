@@ -433,3 +433,48 @@ def test_traffic_and_flop_formulas_golden():
     assert 2 * f["d"] * f["N"] == f["dense_flops"]
     rt = math.isqrt(f["N"])
     assert (2 * f["d"] * f["N"]) / (2 * f["d"] * (rt + rt)) == f["ratio"]
+
+
+# ---------------------------------------------------------------- N1: load metrics and the dense-router ablation
+def test_load_stats_closed_forms():
+    """Expert Usage and Unevenness on cases with closed forms."""
+    import math
+    u, kl = oracle.load_stats(np.full(64, 3))          # uniform load: all used, KL = 0
+    assert u == 1.0 and abs(kl) < 1e-15
+    c = np.zeros(1000, np.int64)
+    c[17] = 5                                          # one expert takes everything
+    u, kl = oracle.load_stats(c)
+    assert u == 1 / 1000 and abs(kl - math.log(1000)) < 1e-12
+    u, kl = oracle.load_stats([2, 1, 1, 0])            # hand example: z = (1/2, 1/4, 1/4, 0)
+    assert u == 0.75 and abs(kl - 0.5 * math.log(2)) < 1e-15
+    assert oracle.load_stats(np.zeros(8, np.int64)) == (0.0, 0.0)
+
+
+def test_load_stats_matches_textbook_kl():
+    from scipy.stats import entropy
+    rng = np.random.default_rng(3)
+    c = rng.poisson(2.0, 5000)
+    u, kl = oracle.load_stats(c)
+    z = c / c.sum()
+    assert u == np.count_nonzero(c) / c.size
+    assert abs(kl - entropy(z, np.full(c.size, 1 / c.size))) < 1e-12
+
+
+def test_dense_route_pins():
+    """The 'w/o CPR' router: exact top-K by (value desc, id asc)."""
+    rng = np.random.default_rng(5)
+    s = rng.standard_normal((50, 300)).astype(np.float32)
+    s[:, 100] = s[:, 7]                                 # exact ties: the lower id first
+    s[3, :] = 0.25                                      # a row of equal values -> ids [0..K)
+    r = oracle.dense_route(s, 12)
+    for t in range(50):                                 # independent formulation: lexsort on (-value, id)
+        order = np.lexsort((np.arange(300), -s[t].astype(np.float64)))[:12]
+        np.testing.assert_array_equal(r["idx"][t], order)
+    np.testing.assert_array_equal(r["idx"][3], np.arange(12))
+    np.testing.assert_allclose(r["gate"].sum(1), 1.0, atol=1e-12)
+    k1 = oracle.dense_route(s, 1)
+    np.testing.assert_array_equal(k1["idx"][:, 0], np.argmax(s, 1))  # K = 1: the (first) arg-max
+    g = oracle.dense_route(np.log(np.array([[0.6, 0.3, 0.1]], np.float32)), 2)["gate"][0]
+    np.testing.assert_allclose(g, [0.6 / 0.9, 0.3 / 0.9], rtol=1e-6)  # softmax over the selected only
+    sh = oracle.dense_route(s + np.float32(4.0), 12)   # shift invariance (exact in fp32 here)
+    np.testing.assert_array_equal(sh["idx"][:3], r["idx"][:3])
