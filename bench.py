@@ -238,13 +238,20 @@ def bench_single(args, w, lr):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = statistics.mean(step_ms)
 
-    if dims.expert_kernel == om.EXPERT_TOKEN:  # ablation run: the layer time is the result
+    ablation = []
+    if dims.expert_kernel == om.EXPERT_TOKEN:
+        ablation.append("w/o Expert-Centric Scheduling (token-centric executor, PAPER:396)")
+    if dims.router == om.ROUTER_DENSE:
+        ablation.append("w/o Cartesian Product Router (dense gate projection, PAPER:395, 414)")
+    if args.no_shared_mlp:
+        ablation.append("w/o Shared Dense MLP (PAPER:394)")
+    if ablation:  # ablation run (PAPER Table 4 rows): the layer time is the result
         print(json.dumps({"metric": METRIC, "value": L / (ms / 1000.0), "unit": "tokens/s", "n_gpus": 1,
                           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-                          "data": "synthetic", "config": dict(_config_dict(w, "single-gpu"),
-                                                              expert_kernel="token (ablation: w/o ECS)"),
-                          "gpu_launches": launches, "clocks": clk.summary()}), flush=True)
+                          "data": "synthetic", "config": dict(_config_dict(w, "single-gpu"), ablation=ablation),
+                          "workspace_bytes": lws.numel(), "gpu_launches": launches, "clocks": clk.summary()}),
+              flush=True)
         return 0
     # ---- per-stage breakdown through the individual C-ABI calls (same inputs) ----
     M = L * dims.n_heads * dims.top_k
@@ -493,6 +500,9 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=60.0, help="total oracle time of --impl reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--router", default="cpr", choices=["cpr", "dense"],
+                    help="cpr: the Cartesian Product Router; dense: the paper's 'w/o CPR' ablation")
+    ap.add_argument("--no-shared-mlp", action="store_true", help="ablation 'w/o Shared Dense MLP' (d_ff = 0)")
     ap.add_argument("--v-layout", default="sliced", choices=["sliced", "rows"],
                     help="layout of the V table: sliced ([d/32][N][32], the two-pass SLICED executor) or rows "
                          "([N][d], the one-pass grouped executor)")
@@ -518,6 +528,12 @@ def main():
     if args.expert_kernel != "auto":
         ek = {"token": om.EXPERT_TOKEN, "warp": om.EXPERT_WARP}[args.expert_kernel]
         w = configs.get(args.config, expert_kernel=ek, group_size=1 if ek == om.EXPERT_WARP else 0)
+    if args.router == "dense":
+        w = configs.get(w.name, **{k: getattr(w.dims, k) for k in ("v_layout", "expert_kernel", "group_size")},
+                        router=om.ROUTER_DENSE)
+    if args.no_shared_mlp:
+        w = configs.get(w.name, **{k: getattr(w.dims, k) for k in ("v_layout", "expert_kernel", "group_size",
+                                                                   "router")}, d_ff=0)
     try:
         if ws > 1:
             return bench_multi(args, w, ws, rk, lr)

@@ -74,7 +74,14 @@ enum { OMNIMOE_WS_ROUTE = 0, OMNIMOE_WS_SCHEDULE = 1, OMNIMOE_WS_EXPERT = 2, OMN
  *   EXACT      tcgen05 kind::i8 products of 3 int8 digits per operand (fast);
  *              rows whose exponents span > 22 bits fall back to EXACT_F64.
  *   EXACT_F64  fp64 double-double dot products on CUDA cores (slow reference). */
-enum { OMNIMOE_ROUTER_EXACT = 0, OMNIMOE_ROUTER_EXACT_F64 = 1 };
+enum { OMNIMOE_ROUTER_EXACT = 0, OMNIMOE_ROUTER_EXACT_F64 = 1, OMNIMOE_ROUTER_DENSE = 2 };
+/* OMNIMOE_ROUTER_DENSE is the paper's ablation "w/o Cartesian Product Router"
+ * (PAPER:395, 414): a standard dense routing projection.  `subkeys` then holds h
+ * dense gate tables [h][N][d] (one row per expert, N = n_rows * n_cols); logits =
+ * x . W_g^T on the tcgen05 bf16 GEMM with fp32 accumulation (NOT the exact RN32 of
+ * Q9), materialised as [L][h][N] fp32 (the "full-dimension logits" the paper blames,
+ * PAPER:414); exact top-K of the N logits by (value desc, id asc); gates = softmax
+ * over the selected.  bf16 only; ids always in key order. */
 
 /* Layer dimensions.
  *   d          hidden size (multiple of 8)
@@ -191,7 +198,8 @@ omnimoe_status omnimoe_workspace_size(const omnimoe_dims* dims, int64_t L, int w
  * keys (Eq.Gate; Q11).
  *   x        [L][d]
  *   subkeys  [h][n_rows + n_cols][d]: row r < n_rows is column r of W_r^h,
- *            row n_rows + c is column c of W_c^h (K-major operand)
+ *            row n_rows + c is column c of W_c^h (K-major operand);
+ *            [h][N][d] gate rows for OMNIMOE_ROUTER_DENSE
  *   idx      int32 [L][h][K]  flat expert ids, ordered by (key desc, id asc)
  *   gate     float [L][h][K]
  *   score    float [L][h][K]  nullable; p_r[i] + p_c[j] (Eq.LSM + Eq.S)

@@ -75,7 +75,11 @@ omnimoe_status validate_dims(const omnimoe_dims* dp) {
     set_error("unknown activation " + std::to_string(d.act));
     return OMNIMOE_ERR_UNSUPPORTED;
   }
-  if (d.router != OMNIMOE_ROUTER_EXACT && d.router != OMNIMOE_ROUTER_EXACT_F64) {
+  if (d.router == OMNIMOE_ROUTER_DENSE && d.dtype != OMNIMOE_BF16) {
+    set_error("the dense-router ablation runs in bf16 only");
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  if (d.router != OMNIMOE_ROUTER_EXACT && d.router != OMNIMOE_ROUTER_EXACT_F64 && d.router != OMNIMOE_ROUTER_DENSE) {
     set_error("unknown router mode " + std::to_string(d.router));
     return OMNIMOE_ERR_UNSUPPORTED;
   }
@@ -130,11 +134,15 @@ omnimoe_status validate_dims(const omnimoe_dims* dp) {
 
 bool i8_logits(const omnimoe_dims& d) { return d.dtype == OMNIMOE_BF16 && d.router == OMNIMOE_ROUTER_EXACT; }
 
+bool dense_router(const omnimoe_dims& d) { return d.router == OMNIMOE_ROUTER_DENSE; }
+// logits per token-head: N_r + N_c (Cartesian) or N (dense ablation)
+int64_t logit_cols(const omnimoe_dims& d) { return dense_router(d) ? d.n_rows * d.n_cols : d.n_rows + d.n_cols; }
+
 size_t route_ws(const omnimoe_dims& d, int64_t L, void* ws, float** logits, void** sub_ws) {
   Carver c(ws);
   const int64_t T = L * d.n_heads;
-  float* lg = c.take<float>((size_t)std::max<int64_t>(T, 1) * (d.n_rows + d.n_cols));
-  void* sw = c.take<char>(exact_logits_ws_bytes(d, L));
+  float* lg = c.take<float>((size_t)std::max<int64_t>(T, 1) * logit_cols(d));
+  void* sw = c.take<char>(dense_router(d) ? 0 : exact_logits_ws_bytes(d, L));
   if (logits) *logits = lg;
   if (sub_ws) *sub_ws = sw;
   return c.bytes();
@@ -205,6 +213,14 @@ omnimoe_status check_ws(size_t have, size_t need, const char* who) {
 omnimoe_status logits_impl(const omnimoe_dims& d, int64_t L, const void* x, const void* subkeys, float* logits,
                            void* sub_ws, cudaStream_t st) {
   const int NC = (int)(d.n_heads * (d.n_rows + d.n_cols));
+  if (dense_router(d)) {  // ablation: the dense projection on the bf16 GEMM engine
+    GemmArgs ga;
+    ga.M = (int)L;
+    ga.N = (int)(d.n_heads * d.n_rows * d.n_cols);
+    ga.K = (int)d.d;
+    ga.out_f32 = logits;
+    return gemm_bf16(EPI_F32, x, subkeys, ga, st);
+  }
   if (i8_logits(d)) return exact_logits(d, L, x, subkeys, logits, sub_ws, st);
   return launch_exact_dd(d.dtype, x, subkeys, (int)d.d, NC, (int)L, logits, 0, nullptr, nullptr, st);
 }
@@ -215,6 +231,10 @@ omnimoe_status route_impl(const omnimoe_dims& d, int64_t L, const void* x, const
   float* logits;
   void* sub_ws;
   route_ws(d, L, ws, &logits, &sub_ws);
+  if (dense_router(d)) {
+    OMNI_TRY(logits_impl(d, L, x, subkeys, logits, sub_ws, st));
+    return launch_dense_select(d, L * d.n_heads, logits, idx, gate, score, st);
+  }
   SelectParams sp;
   size_t smem;
   OMNI_TRY(select_params(d, L * d.n_heads, &sp, &smem));
@@ -302,7 +322,7 @@ omnimoe_status omnimoe_route(const omnimoe_dims* dims, int64_t L, const void* x,
   OMNI_NONNULL(gate, "gate");
   OMNI_NONNULL(ws, "ws");
   OMNI_TRY(check_ws(ws_bytes, route_ws(*dims, L, nullptr, nullptr, nullptr), "route"));
-  {
+  if (!dense_router(*dims)) {
     SelectParams sp;
     size_t smem;
     OMNI_TRY(select_params(*dims, L * dims->n_heads, &sp, &smem));

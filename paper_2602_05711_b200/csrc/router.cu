@@ -933,6 +933,44 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Ablation "w/o Cartesian Product Router": one 1024-thread CTA
+// per token-head takes the exact top-K of its N dense logits by (value desc, id
+// asc) -- radix select over the (value, ~id) keys, compaction, bitonic sort of the
+// K survivors -- and writes ids and softmax gates in key order; score = s - lse.
+__global__ void __launch_bounds__(1024)
+    dense_select_kernel(int T, int N, int K, int plen, const float* __restrict__ logits, int32_t* __restrict__ idx,
+                        float* __restrict__ gate, float* __restrict__ score) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  SelShared<1024>& sh = *reinterpret_cast<SelShared<1024>*>(smem);
+  uint64_t* sel = reinterpret_cast<uint64_t*>(smem + (sizeof(SelShared<1024>) + 15) / 16 * 16);
+  for (int th = blockIdx.x; th < T; th += gridDim.x) {
+    const float* lg = logits + (size_t)th * N;
+    auto keyf = [lg](int i) { return half_key(lg[i], (uint32_t)i); };
+    top_sorted<1024, uint64_t, 8>(N, K, keyf, sel, sh);
+    const float mx = half_val(sel[0]);
+    float es = 0.f;
+    for (int k = threadIdx.x; k < K; k += 1024) es += expf(half_val(sel[k]) - mx);
+    es = group_sum<1024>(es, sh);
+    float lse = 0.f;
+    if (score) {
+      float s = 0.f;
+      for (int i = threadIdx.x; i < N; i += 1024) s += __expf(lg[i] - mx);
+      lse = mx + __logf(group_sum<1024>(s, sh));
+    }
+    for (int k = threadIdx.x; k < K; k += 1024) {
+      const uint64_t q = sel[k];
+      const size_t o = (size_t)th * K + k;
+      idx[o] = (int32_t)half_idx(q);
+      gate[o] = expf(half_val(q) - mx) / es;
+      if (score) score[o] = half_val(q) - lse;
+    }
+    __syncthreads();
+  }
+  (void)plen;
+}
+
 }  // namespace
 
 // host --------------------------------------------------------------------
@@ -974,6 +1012,28 @@ omnimoe_status select_params(const omnimoe_dims& d, int64_t T, SelectParams* p, 
               " product candidates) exceeds shared memory");
     return OMNIMOE_ERR_UNSUPPORTED;
   }
+  return OMNIMOE_OK;
+}
+
+omnimoe_status launch_dense_select(const omnimoe_dims& d, int64_t T, const float* logits, int32_t* idx, float* gate,
+                                   float* score, cudaStream_t st) {
+  const int64_t N = d.n_rows * d.n_cols;
+  const int K = (int)d.top_k;
+  const int plen = std::max(sort_len(K, (int)N), K);
+  const size_t sm = (sizeof(SelShared<1024>) + 15) / 16 * 16 + (size_t)plen * 8;
+  if (sm > 200 * 1024) {
+    set_error("dense router: K=" + std::to_string(K) + " sorted keys exceed shared memory");
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  if (cudaFuncSetAttribute(dense_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
+    set_error("dense router: cannot set shared memory");
+    return OMNIMOE_ERR_CUDA;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dense_select_kernel, 1024, sm);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(T, (int64_t)kSMs * std::max(per_sm, 1)));
+  dense_select_kernel<<<grid, 1024, sm, st>>>((int)T, (int)N, K, plen, logits, idx, gate, score);
+  OMNI_CHECK_LAUNCH("dense_select_kernel");
   return OMNIMOE_OK;
 }
 

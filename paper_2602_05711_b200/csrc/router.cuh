@@ -19,6 +19,9 @@ struct SelectParams {
 };
 
 omnimoe_status select_params(const omnimoe_dims& d, int64_t T, SelectParams* p, size_t* smem);
+// ablation "w/o CPR": exact top-K of T rows of N dense logits (key order)
+omnimoe_status launch_dense_select(const omnimoe_dims& d, int64_t T, const float* logits, int32_t* idx, float* gate,
+                                   float* score, cudaStream_t st);
 omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* logits, int32_t* idx,
                              float* gate, float* score, cudaStream_t st);
 

@@ -21,7 +21,7 @@ SILU, IDENTITY = 0, 1
 EXPERT_AUTO, EXPERT_WARP, EXPERT_GROUP, EXPERT_TOKEN, EXPERT_SLICED = 0, 1, 2, 3, 4
 V_ROWS, V_SLICED = 0, 1
 ORDER_KEY, ORDER_CANDIDATE = 0, 1
-ROUTER_EXACT, ROUTER_EXACT_F64 = 0, 1
+ROUTER_EXACT, ROUTER_EXACT_F64, ROUTER_DENSE = 0, 1, 2
 LOGITS_ROUTE, LOGITS_EXACT_F64, LOGITS_BF16_FAST = 0, 1, 2
 WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER = 0, 1, 2, 3
 
@@ -144,6 +144,12 @@ class LayerDims:
         return self.n_rows * self.n_cols
 
     @property
+    def router_rows(self) -> int:
+        """Rows of each head's router table: N_r + N_c sub-keys, or N gate rows for the
+        dense-router ablation."""
+        return self.N if self.router == ROUTER_DENSE else self.n_rows + self.n_cols
+
+    @property
     def torch_dtype(self):
         return torch.bfloat16 if self.dtype == BF16 else torch.float32
 
@@ -190,7 +196,7 @@ def workspace(dims: LayerDims, L: int, which: int, device=None) -> torch.Tensor:
 def route(dims: LayerDims, x, subkeys, ws=None, want_score=True):
     L = x.shape[0]
     _req(x, "x", dims.torch_dtype, L * dims.d)
-    _req(subkeys, "subkeys", dims.torch_dtype, dims.n_heads * (dims.n_rows + dims.n_cols) * dims.d)
+    _req(subkeys, "subkeys", dims.torch_dtype, dims.n_heads * dims.router_rows * dims.d)
     K, h = dims.top_k, dims.n_heads
     idx = torch.empty((L, h, K), dtype=torch.int32, device=x.device)
     gate = torch.empty((L, h, K), dtype=torch.float32, device=x.device)
@@ -336,7 +342,7 @@ def layer_fwd(dims: LayerDims, x, subkeys, W, V, w_gate_up=None, w_down=None, y=
               return_routing=False):
     L = x.shape[0]
     _req(x, "x", dims.torch_dtype, L * dims.d)
-    _req(subkeys, "subkeys", dims.torch_dtype, dims.n_heads * (dims.n_rows + dims.n_cols) * dims.d)
+    _req(subkeys, "subkeys", dims.torch_dtype, dims.n_heads * dims.router_rows * dims.d)
     _req(W, "W", dims.torch_dtype, dims.N * dims.d)
     _req(V, "V", dims.torch_dtype, dims.N * dims.d)
     if dims.d_ff:
@@ -360,8 +366,8 @@ def router_logits(dims: LayerDims, x, subkeys, method=LOGITS_ROUTE, ws=None):
     LOGITS_EXACT_F64, LOGITS_BF16_FAST (inexact fp32-accumulated tcgen05, measurement only)."""
     L = x.shape[0]
     _req(x, "x", dims.torch_dtype, L * dims.d)
-    _req(subkeys, "subkeys", dims.torch_dtype, dims.n_heads * (dims.n_rows + dims.n_cols) * dims.d)
-    out = torch.empty((L, dims.n_heads, dims.n_rows + dims.n_cols), dtype=torch.float32, device=x.device)
+    _req(subkeys, "subkeys", dims.torch_dtype, dims.n_heads * dims.router_rows * dims.d)
+    out = torch.empty((L, dims.n_heads, dims.router_rows), dtype=torch.float32, device=x.device)
     ws = ws if ws is not None else workspace(dims, L, WS_ROUTE, x.device)
     dc = dims.c()
     _check(load().omnimoe_router_logits(ctypes.byref(dc), L, _ptr(x), _ptr(subkeys), _ptr(out), int(method),

@@ -13,8 +13,8 @@ from .cuda import make
 
 def tensor_specs(dims, L):
     """(name, tensor id, shape) of every input of the layer."""
-    R = dims.n_rows + dims.n_cols
     N = dims.n_rows * dims.n_cols
+    R = N if getattr(dims, "router", 0) == 2 else dims.n_rows + dims.n_cols  # dense-router ablation: N gate rows
     specs = [("x", TID_X, (L, dims.d)), ("subkeys", TID_SUBKEYS, (dims.n_heads, R, dims.d)),
              ("W", TID_W, (N, dims.d)), ("V", TID_V, (N, dims.d))]
     if dims.d_ff:

@@ -11,7 +11,7 @@ import synth
 def host_rows(dims, seed, name, rows=None, mode=synth.NORMAL):
     """Exact float64 values of rows of an input tensor (regenerated on the host)."""
     ex = synth.default_exponents(dims.d, dims.d_ff, mode)
-    R = dims.n_rows + dims.n_cols
+    R = dims.n_rows * dims.n_cols if getattr(dims, "router", 0) == 2 else dims.n_rows + dims.n_cols
     tid, ncols, nrows = {
         "x": (synth.TID_X, dims.d, None),
         "subkeys": (synth.TID_SUBKEYS, dims.d, dims.n_heads * R),

@@ -552,3 +552,45 @@ def test_load_stats_match_oracle(N, M, skew):
     got = om.load_stats(plan).cpu().numpy()
     want = oracle.load_stats(np.bincount(ids, minlength=N))
     np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-15)
+
+
+# ---------------------------------------------------------------- N1: the dense-router ablation ("w/o CPR")
+@pytest.mark.parametrize("d,nr,nc,K,h,L", [(64, 32, 32, 8, 2, 200), (256, 64, 64, 100, 1, 130),
+                                           (1024, 320, 320, 4096, 1, 12)])
+def test_dense_router_selection_exact(d, nr, nc, K, h, L):
+    """Given the GEMM's logits, the dense top-K is exact (ids in key order, gates);
+    the logits themselves are the bf16 GEMM's fp32-accumulated dot products."""
+    dims = om.LayerDims(d=d, n_rows=nr, n_cols=nc, top_k=K, n_heads=h, router=om.ROUTER_DENSE)
+    inp = make_inputs(dims, L, 21, skip=("W", "V", "w_gate_up", "w_down"))
+    idx, gate, score = om.route(dims, inp["x"], inp["subkeys"])
+    lg = om.router_logits(dims, inp["x"], inp["subkeys"])
+    torch.cuda.synchronize()
+    rows = lg.cpu().numpy().reshape(L * h, -1)
+    ref = oracle.dense_route(rows, K)
+    np.testing.assert_array_equal(idx.cpu().numpy().reshape(-1, K), ref["idx"])
+    np.testing.assert_allclose(gate.cpu().numpy().reshape(-1, K), ref["gate"], atol=1e-6)
+    lse = np.log(np.exp(rows.astype(np.float64) - rows.max(1, keepdims=True)).sum(1)) + rows.max(1)
+    np.testing.assert_allclose(score.cpu().numpy().reshape(-1, K), ref["key"] - lse[:, None], atol=1e-4)
+    # the logits against the exact dot products (an fp32-accumulated GEMM: not RN32-exact)
+    x = host_rows(dims, 21, "x", np.arange(L))
+    sub = host_rows(dims, 21, "subkeys").reshape(h, -1, d)
+    exact = oracle.logits(x, sub).reshape(L * h, -1)
+    assert np.abs(rows.astype(np.float64) - exact).max() <= 2e-5 * max(1.0, np.abs(exact).max())
+
+
+def test_layer_dense_router():
+    """The 'w/o CPR' layer: dense routing + the same schedule / SLICED executor /
+    shared MLP, against the oracle evaluated on the GPU's routing decision."""
+    dims = om.LayerDims(d=64, n_rows=32, n_cols=32, top_k=8, d_ff=128, router=om.ROUTER_DENSE, v_layout=om.V_SLICED)
+    L = 256
+    inp = make_inputs(dims, L, 0)
+    y, idx, gate = om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], om.pack_v(dims, inp["V"]),
+                                inp["w_gate_up"], inp["w_down"], return_routing=True)
+    torch.cuda.synchronize()
+    hr = lambda n, r=None: host_rows(dims, 0, n, r)
+    x = hr("x", np.arange(L))
+    ids = idx.cpu().numpy().reshape(L, -1)
+    ref = oracle.routed_token_centric(x, hr("W"), hr("V"), ids, gate.cpu().numpy().reshape(L, -1).astype(np.float64))
+    ref += oracle.shared_mlp(x, hr("w_gate_up"), hr("w_down"))
+    e_tok, e_elt = rel_errors(y.float().cpu().numpy(), ref)
+    assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
