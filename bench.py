@@ -96,6 +96,13 @@ def rank_info():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
+def expected_eta(dims, L):
+    """Tasks per active expert under uniform routing: M / (N (1 - (1 - 1/N)^M))."""
+    import math
+    N, M = dims.N, L * dims.n_heads * dims.top_k
+    return M / (N * -math.expm1(-M / N))
+
+
 L2_GATHER_GBS = 14404.1  # measured: random 4 KB row gathers from an L2-resident table (tools/microbench.cu)
 
 
@@ -263,6 +270,7 @@ def bench_single(args, w, lr):
     yr = torch.empty((L, dims.d), dtype=torch.float32, device="cuda")
     stages = {"route_a1_a3": [], "schedule_a4_a5": [], "expert_a6": [], "shared_mlp_a7_a8": []}
     sliced = dims.v_layout == om.V_SLICED
+    token = om.layer_executor(dims, L) == om.EXPERT_TOKEN  # low eta: the layer skips ECS
     passes = {"a6_pass_z": [], "a6_pass_v": []}
     for i in range(max(4, args.steps)):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
@@ -275,7 +283,9 @@ def bench_single(args, w, lr):
         yr.zero_()
         flush.zero_()
         e[3].record(st)
-        if sliced:  # the two passes of the SLICED executor, timed apart
+        if token:
+            om.expert_fwd_tokens(dims, inp["x"], inp["W"], inp["V"], idx, gate, y_routed=yr, accumulate=True)
+        elif sliced:  # the two passes of the SLICED executor, timed apart
             om.expert_fwd(dims, inp["x"], inp["W"], inp["V"], plan, y_routed=yr, accumulate=True, ws=ews, passes=1)
             e[6].record(st)
             om.expert_fwd(dims, inp["x"], inp["W"], inp["V"], plan, y_routed=yr, accumulate=True, ws=ews, passes=2)
@@ -294,6 +304,8 @@ def bench_single(args, w, lr):
             passes["a6_pass_z"].append(e[3].elapsed_time(e[6]))
             passes["a6_pass_v"].append(e[6].elapsed_time(e[4]))
     stage_ms = {k: statistics.median(v) for k, v in stages.items()}
+    if token:  # the plan was built for the load metrics only; the layer does not schedule
+        stage_ms["schedule_a4_a5"] = 0.0
     usage, uneven = om.load_stats(plan).cpu().tolist()  # Expert Usage / Unevenness
     if sliced:
         stage_ms.update({k: statistics.median(v) for k, v in passes.items()})
@@ -346,7 +358,7 @@ def bench_single(args, w, lr):
                         "l2_gbs": l2b / kms / 1e6, "l2_frac": l2b / kms / 1e6 / L2_GATHER_GBS}
         a6_bytes, l2_bytes, a6_ms = cand[kern]
     else:
-        kern = "expert_group_tma_kernel" if B > 1 else "expert_warp_kernel"
+        kern = "expert_token_kernel" if token else ("expert_group_tma_kernel" if B > 1 else "expert_warp_kernel")
         a6_bytes, a6_ms = a6_algorithmic_bytes(dims, L, n_active, M), stage_ms["expert_a6"]
         l2_bytes = 2 * M * dims.d * 2
     a6_gbs = a6_bytes / (a6_ms / 1000.0) / 1e9
@@ -377,7 +389,12 @@ def bench_single(args, w, lr):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded counter-based generator, DESIGN.md §3)",
         "config": dict(_config_dict(w, "single-gpu"), group_size=B, expert_kernel=args.expert_kernel,
-                       v_layout=args.v_layout if dims.v_layout == om.V_SLICED else "rows"),
+                       v_layout="sliced" if dims.v_layout == om.V_SLICED else "rows",
+                       executor={om.EXPERT_TOKEN: "token-centric (eta < 2: no expert reuse; ECS skipped)",
+                                 om.EXPERT_SLICED: "SLICED (ECS pass Z + slice-major pass V)",
+                                 om.EXPERT_GROUP: "grouped ECS (rows)",
+                                 om.EXPERT_WARP: "expert-major ECS (rows)"}[om.layer_executor(dims, L)],
+                       eta=expected_eta(dims, L)),
         "stage_ms": stage_ms, "n_active": n_active, "tasks": M,
         "load": {"expert_usage": usage, "unevenness": uneven,
                  "note": "PAPER:405-410 (paper's full model: usage 100%, unevenness 0.24 with trained routers; "
@@ -503,9 +520,10 @@ def main():
     ap.add_argument("--router", default="cpr", choices=["cpr", "dense"],
                     help="cpr: the Cartesian Product Router; dense: the paper's 'w/o CPR' ablation")
     ap.add_argument("--no-shared-mlp", action="store_true", help="ablation 'w/o Shared Dense MLP' (d_ff = 0)")
-    ap.add_argument("--v-layout", default="sliced", choices=["sliced", "rows"],
-                    help="layout of the V table: sliced ([d/32][N][32], the two-pass SLICED executor) or rows "
-                         "([N][d], the one-pass grouped executor)")
+    ap.add_argument("--v-layout", default="auto", choices=["auto", "sliced", "rows"],
+                    help="layout of the V table: sliced ([d/32][N][32], the two-pass SLICED executor), rows "
+                         "([N][d]: grouped ECS, or token-centric when eta < 2), or auto: sliced for "
+                         "2 <= eta <= 32 tasks per active expert, rows otherwise (profiles/r1/README.md)")
     ap.add_argument("--expert-kernel", default="auto", choices=["auto", "token", "warp"],
                     help="a6 executor: auto (grouped ECS), token (the paper's 'w/o ECS' ablation), "
                          "warp (expert-major, B = 1)")
@@ -523,7 +541,10 @@ def main():
     if ws > 1:
         dist.barrier()
     from paper_2602_05711_b200 import omnimoe as om
-    sliced = args.v_layout == "sliced" and args.expert_kernel == "auto"
+    w = configs.get(args.config)
+    eta = expected_eta(w.dims, w.L)
+    sliced = args.expert_kernel == "auto" and (args.v_layout == "sliced" or
+                                               (args.v_layout == "auto" and 2.0 <= eta <= 32.0))
     w = configs.get(args.config, v_layout=om.V_SLICED if sliced else om.V_ROWS)
     if args.expert_kernel != "auto":
         ek = {"token": om.EXPERT_TOKEN, "warp": om.EXPERT_WARP}[args.expert_kernel]

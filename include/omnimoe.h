@@ -268,6 +268,21 @@ omnimoe_status omnimoe_shared_mlp(const omnimoe_dims* dims, int64_t L, const voi
                                   const void* w_gate_up, const void* w_down, const float* y_routed,
                                   void* y, void* ws, size_t ws_bytes, omnimoe_stream_t stream);
 
+/* The paper's ablation "w/o Expert-Centric Scheduling": the routed
+ * branch token by token straight from the routing decision (idx, gate [L][h*K],
+ * global ids), every task gathering its own w_e and v_e rows; y_routed[l] written
+ * once (added to when accumulate != 0).  V in the ROWS layout; bf16, d % 256 == 0. */
+omnimoe_status omnimoe_expert_fwd_tokens(const omnimoe_dims* dims, int64_t L, const void* x, const void* W,
+                                         const void* V, const int32_t* idx, const float* gate,
+                                         float* y_routed, int accumulate, omnimoe_stream_t stream);
+
+/* The routed-branch executor omnimoe_layer_fwd runs for dims and L tokens
+ * (OMNIMOE_EXPERT_*; -1 on invalid dims).  With expert_kernel AUTO: SLICED for the
+ * SLICED layout; for the ROWS layout TOKEN when eta = M / E|E_active| < 2 under
+ * uniform routing (then no expert is shared by two tasks and Expert-Centric
+ * Scheduling has nothing to reuse -- measured faster), else GROUP. */
+int32_t omnimoe_layer_executor(const omnimoe_dims* dims, int64_t L);
+
 /* Whole layer forward (Eq.MoE / Eq.Assemble):
  * route -> schedule (full expert range) -> expert_fwd -> shared MLP + combine.
  *   W          [N][d]

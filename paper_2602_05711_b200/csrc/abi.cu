@@ -496,7 +496,7 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
   OMNI_TRY(route_impl(d, L, x, subkeys, idx, gate, nullptr, w.route_ws, st, /*sorted=*/0));
   const int r_launch = omnimoe_last_launch_count();
   w.plan.n_tokens = L;
-  if (d.expert_kernel == OMNIMOE_EXPERT_TOKEN) {  // ablation: no Expert-Centric Scheduling
+  if (layer_uses_token_executor(d, L)) {  // no expert shared by two tasks (or the "w/o ECS" ablation)
     OMNI_TRY(expert_token_run(d, L, x, W, V, idx, gate, 0, d.n_rows * d.n_cols, w.y_routed, 0, st));
   } else {
     OMNI_TRY(schedule_run(M, idx, gate, nullptr, d.n_heads * d.top_k, w.plan, resolve_group_size(d),
@@ -534,6 +534,38 @@ omnimoe_status omnimoe_pack_v(const omnimoe_dims* dims, int64_t n, const void* V
   }
   OMNI_TRY(check_device());
   return pack_v(n, (int)dims->d, V, V_sliced, (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_expert_fwd_tokens(const omnimoe_dims* dims, int64_t L, const void* x, const void* W,
+                                         const void* V, const int32_t* idx, const float* gate, float* y_routed,
+                                         int accumulate, omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  if (L < 0) {
+    set_error("L must be >= 0");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (L == 0) return OMNIMOE_OK;
+  OMNI_NONNULL(x, "x");
+  OMNI_NONNULL(W, "W");
+  OMNI_NONNULL(V, "V");
+  OMNI_NONNULL(idx, "idx");
+  OMNI_NONNULL(gate, "gate");
+  OMNI_NONNULL(y_routed, "y_routed");
+  if (dims->v_layout != OMNIMOE_V_ROWS) {
+    set_error("expert_fwd_tokens: V in the ROWS layout");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  OMNI_TRY(check_device());
+  return expert_token_run(*dims, L, x, W, V, idx, gate, 0, dims->n_rows * dims->n_cols, y_routed, accumulate,
+                          (cudaStream_t)stream);
+}
+
+int32_t omnimoe_layer_executor(const omnimoe_dims* dims, int64_t L) {
+  if (validate_dims(dims) != OMNIMOE_OK || L < 0) return -1;
+  if (layer_uses_token_executor(*dims, L)) return OMNIMOE_EXPERT_TOKEN;
+  if (dims->v_layout == OMNIMOE_V_SLICED) return OMNIMOE_EXPERT_SLICED;
+  return resolve_group_size(*dims) > 1 ? OMNIMOE_EXPERT_GROUP : OMNIMOE_EXPERT_WARP;
 }
 
 omnimoe_status omnimoe_router_logits(const omnimoe_dims* dims, int64_t L, const void* x, const void* subkeys,

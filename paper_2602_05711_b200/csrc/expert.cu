@@ -1240,6 +1240,20 @@ int64_t resolve_group_size(const omnimoe_dims& d) {
   return std::max<int64_t>(2, std::min<int64_t>(8 * d.n_cols, cap));
 }
 
+double expected_eta(const omnimoe_dims& d, int64_t L) {
+  const double N = (double)(d.n_rows * d.n_cols), M = (double)L * d.n_heads * d.top_k;
+  const double active = N * -expm1(-M / N);  // N (1 - (1 - 1/N)^M), N large
+  return active > 0 ? M / active : 0.0;
+}
+
+bool layer_uses_token_executor(const omnimoe_dims& d, int64_t L) {
+  if (d.expert_kernel == OMNIMOE_EXPERT_TOKEN) return true;
+  // measured (profiles/r1/README.md, C3b / C5s at eta ~ 1.1): with no expert shared by two
+  // tasks, scheduling and two passes cost more than they save; full-row gathers win
+  return d.expert_kernel == OMNIMOE_EXPERT_AUTO && d.v_layout == OMNIMOE_V_ROWS && d.dtype == OMNIMOE_BF16 &&
+         d.d % 256 == 0 && d.d <= 2048 && expected_eta(d, L) < env_int("OMNIMOE_TOKEN_ETA_X100", 200) / 100.0;
+}
+
 int64_t resolve_v_bands(const omnimoe_dims& d, int64_t n_loc) {
   if (d.v_layout != OMNIMOE_V_SLICED || n_loc < 1) return 1;
   // one band x one 32-column slice of V = 64 bytes per expert row, kept <= 64 MB:

@@ -20,6 +20,11 @@ omnimoe_status expert_token_run(const omnimoe_dims& dm, int64_t L, const void* x
                                 int accumulate, cudaStream_t st);
 int64_t resolve_token_blocks(const omnimoe_dims& d, int64_t L);
 int64_t resolve_v_bands(const omnimoe_dims& d, int64_t n_loc);
+// eta = M / E|E_active| under uniform routing: tasks per active expert
+double expected_eta(const omnimoe_dims& d, int64_t L);
+// layer_fwd runs the token-centric executor (no schedule): the "w/o ECS" ablation, or
+// AUTO with the ROWS layout when expected_eta < 2 (no reuse for ECS to exploit)
+bool layer_uses_token_executor(const omnimoe_dims& d, int64_t L);
 
 // V [n][d] -> [d/32][n][32] (omnimoe_pack_v)
 omnimoe_status pack_v(int64_t n, int d, const void* V, void* Vs, cudaStream_t st);

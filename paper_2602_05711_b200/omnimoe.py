@@ -54,7 +54,7 @@ EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnim
            "omnimoe_group_size", "omnimoe_token_blocks", "omnimoe_ep_pack_workspace_size",
            "omnimoe_ep_pack", "omnimoe_ep_unpack", "omnimoe_ep_combine", "omnimoe_pack_v",
            "omnimoe_v_bands", "omnimoe_expert_fwd_pass", "omnimoe_load_stats",
-           "omnimoe_load_stats_workspace_size"]
+           "omnimoe_load_stats_workspace_size", "omnimoe_expert_fwd_tokens", "omnimoe_layer_executor"]
 
 _lib = None
 
@@ -85,6 +85,7 @@ def load(path: str = LIB_PATH):
         "omnimoe_ep_combine": [PD, I64, I32, V, V, V, V, V],
         "omnimoe_pack_v": [PD, I64, V, V, V],
         "omnimoe_load_stats": [PP, V, V, SZ, V],
+        "omnimoe_expert_fwd_tokens": [PD, I64, V, V, V, V, V, V, I32, V],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -93,6 +94,8 @@ def load(path: str = LIB_PATH):
     lib.omnimoe_last_launch_count.restype = ctypes.c_int
     lib.omnimoe_group_size.argtypes = [PD]
     lib.omnimoe_group_size.restype = ctypes.c_int64
+    lib.omnimoe_layer_executor.argtypes = [PD, ctypes.c_int64]
+    lib.omnimoe_layer_executor.restype = ctypes.c_int32
     lib.omnimoe_load_stats_workspace_size.restype = ctypes.c_size_t
     lib.omnimoe_load_stats_workspace_size.argtypes = []
     lib.omnimoe_v_bands.argtypes = [PD, ctypes.c_int64]
@@ -284,6 +287,28 @@ def load_stats(plan):
     cp = _cplan(plan)
     _check(lib.omnimoe_load_stats(ctypes.byref(cp), _ptr(out), _ptr(ws), ws.numel(), _stream()), "load_stats")
     return out
+
+
+def layer_executor(dims: LayerDims, L: int) -> int:
+    """The routed-branch executor (EXPERT_*) omnimoe_layer_fwd uses for L tokens."""
+    dc = dims.c()
+    return int(load().omnimoe_layer_executor(ctypes.byref(dc), L))
+
+
+def expert_fwd_tokens(dims: LayerDims, x, W, V, idx, gate, y_routed=None, accumulate=False):
+    """'w/o ECS' token-centric routed branch from the routing decision (omnimoe_expert_fwd_tokens)."""
+    L = x.shape[0]
+    hk = dims.n_heads * dims.top_k
+    _req(x, "x", dims.torch_dtype, L * dims.d)
+    _req(idx, "idx", torch.int32, L * hk)
+    _req(gate, "gate", torch.float32, L * hk)
+    if y_routed is None:
+        y_routed = torch.empty((L, dims.d), dtype=torch.float32, device=x.device)
+        accumulate = False
+    dc = dims.c()
+    _check(load().omnimoe_expert_fwd_tokens(ctypes.byref(dc), L, _ptr(x), _ptr(W), _ptr(V), _ptr(idx), _ptr(gate),
+                                            _ptr(y_routed), int(accumulate), _stream()), "expert_fwd_tokens")
+    return y_routed
 
 
 def pack_v(dims: LayerDims, V):

@@ -594,3 +594,20 @@ def test_layer_dense_router():
     ref += oracle.shared_mlp(x, hr("w_gate_up"), hr("w_down"))
     e_tok, e_elt = rel_errors(y.float().cpu().numpy(), ref)
     assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+
+
+def test_layer_low_eta_uses_token_executor():
+    """AUTO + ROWS at eta < 2 (no expert shared by two tasks) runs the token-centric
+    executor without a schedule; results against the oracle."""
+    dims = om.LayerDims(d=256, n_rows=64, n_cols=64, top_k=2, d_ff=256)
+    L = 200
+    assert om.layer_executor(dims, L) == om.EXPERT_TOKEN
+    assert om.layer_executor(om.LayerDims(d=256, n_rows=64, n_cols=64, top_k=64, d_ff=256), L) == om.EXPERT_GROUP
+    inp = make_inputs(dims, L, 17)
+    y = om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], inp["V"], inp["w_gate_up"], inp["w_down"])
+    torch.cuda.synchronize()
+    hr = lambda n, r=None: host_rows(dims, 17, n, r)
+    ref = oracle.layer(hr("x", np.arange(L)), hr("subkeys").reshape(1, -1, 256), hr("W"), hr("V"), 64, 64, 2,
+                       hr("w_gate_up"), hr("w_down"))
+    e_tok, e_elt = rel_errors(y.float().cpu().numpy(), ref["y"])
+    assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
