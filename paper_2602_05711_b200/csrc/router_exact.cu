@@ -19,6 +19,7 @@
 //                        of the (hi, lo) pair: the F32-mode path and the fallback
 //                        for flagged rows.  Exact whenever the running sums fit
 //                        106 bits (always for bf16 rows).
+#include <cstdlib>
 #include <string>
 
 #include "router.cuh"
@@ -27,6 +28,11 @@
 namespace omni {
 namespace {
 using namespace tc;
+
+int env_int(const char* name, int dflt) {  // measurement overrides (tools/ sweeps)
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
 
 constexpr int kMaxBits = 22;  // |X| < 2^22 => three balanced base-256 digits fit int8
 
@@ -115,12 +121,18 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
-constexpr int IBM = 128, IBN = 64, IBK = 128 /*bytes = int8 elements*/, kIStages = 3;
+#ifndef OMNI_I8_BN
+#define OMNI_I8_BN 64
+#endif
+#ifndef OMNI_I8_STAGES
+#define OMNI_I8_STAGES 3
+#endif
+constexpr int IBM = 128, IBN = OMNI_I8_BN, IBK = 128 /*bytes = int8 elements*/, kIStages = OMNI_I8_STAGES;
 constexpr int kIABytes = IBM * IBK;  // one limb
 constexpr int kIBBytes = IBN * IBK;
 constexpr int kIStageBytes = 3 * kIABytes + 3 * kIBBytes;  // 72 KB
 constexpr int kISmemBytes = kIStages * kIStageBytes + 1024 + 256;
-constexpr int kITmemCols = 512;  // 5 accumulators x 64 columns, rounded up to a power of two
+constexpr int kITmemCols = 512;  // 5 accumulators x IBN (<= 96) columns, rounded up to a power of two
 // instruction descriptor, kind::i8: D = s32, A = B = s8, K-major, M = 128, N = 64
 constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(IBN >> 3) << 17) |
                               ((uint32_t)(IBM >> 4) << 24);
@@ -132,6 +144,35 @@ struct I8Args {
   float* out;         // [M][N]
 };
 
+// CN > 1: a cluster of CN CTAs along N shares the A (token) limbs: CTA r loads rows
+// [r*IBM/CN, (r+1)*IBM/CN) of each A limb and multicasts them to the whole cluster,
+// so each CTA pulls 1/CN of the A bytes from L2; a stage is released when the MMAs of
+// all CN CTAs are done with it (their commits arrive on every CTA's empty barrier).
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+template <int CN>
 __global__ void __launch_bounds__(256, 1)
     gemm_i8_exact_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          I8Args args) {
@@ -153,7 +194,7 @@ __global__ void __launch_bounds__(256, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     for (int s = 0; s < kIStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CN);
     }
     mbar_init(tfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -165,8 +206,11 @@ __global__ void __launch_bounds__(256, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (CN > 1) cluster_sync_all();  // peers' barriers are initialised before any multicast
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  const uint32_t crank = CN > 1 ? cluster_rank() : 0;
+  constexpr uint16_t kMask = (uint16_t)((1u << CN) - 1u);
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer: 3 A limbs + 3 B limbs per K block ----------------
@@ -176,10 +220,19 @@ __global__ void __launch_bounds__(256, 1)
       mbar_expect_tx(&full[s], kIStageBytes);
 #pragma unroll
       for (int p = 0; p < 3; ++p) {
-        tma_load_2d(&tmA, &full[s], sA + (s * 3 + p) * kIABytes, kb * IBK, p * args.M + m0);
+        if (CN > 1) {
+          constexpr int rows = IBM / CN;
+          tma_load_2d_mc(&tmA, &full[s], sA + (s * 3 + p) * kIABytes + crank * rows * IBK, kb * IBK,
+                         p * args.M + m0 + (int)crank * rows, kMask);
+        } else {
+          tma_load_2d(&tmA, &full[s], sA + (s * 3 + p) * kIABytes, kb * IBK, p * args.M + m0);
+        }
         tma_load_2d(&tmB, &full[s], sB + (s * 3 + p) * kIBBytes, kb * IBK, p * args.N + n0);
       }
     }
+    if (CN > 1)  // drain: every peer's commits for every stage have arrived before exit
+      for (int kb = num_kb; kb < num_kb + kIStages; ++kb)
+        mbar_wait(&empty[kb % kIStages], ((kb / kIStages) & 1) ^ 1);
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer: D_{p+q} += X_p . W_q^T ----------------
     for (int kb = 0; kb < num_kb; ++kb) {
@@ -198,7 +251,8 @@ __global__ void __launch_bounds__(256, 1)
             umma_i8(tmem + (uint32_t)((p + q) * IBN), sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32),
                     kIdescI8, !(kb == 0 && k == 0 && first_pair));
         }
-      umma_commit(&empty[s]);
+      if (CN > 1) umma_commit_mc(&empty[s], kMask);
+      else umma_commit(&empty[s]);
     }
     umma_commit(tfull);
   } else if (warp >= 4) {
@@ -239,6 +293,7 @@ __global__ void __launch_bounds__(256, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (CN > 1) cluster_sync_all();  // no CTA leaves while a peer may still signal or fill it
   if (warp == 2) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kITmemCols));
@@ -407,23 +462,49 @@ omnimoe_status exact_logits(const omnimoe_dims& d, int64_t L, const void* x, con
 
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_i8_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kISmemBytes) !=
-        cudaSuccess) {
-      set_error("route: cannot set dynamic shared memory size of the i8 GEMM");
-      return OMNIMOE_ERR_CUDA;
-    }
+    for (auto k : {gemm_i8_exact_kernel<1>, gemm_i8_exact_kernel<2>, gemm_i8_exact_kernel<4>})
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kISmemBytes) != cudaSuccess) {
+        set_error("route: cannot set dynamic shared memory size of the i8 GEMM");
+        return OMNIMOE_ERR_CUDA;
+      }
     attr_set = true;
   }
+  // clusters of CN CTAs along N multicast the A limbs (CN | number of N tiles)
+  const int n_tiles = (NC + IBN - 1) / IBN;
+  int CN = std::max(1, std::min(4, env_int("OMNIMOE_I8_CLUSTER", 1)));
+  while (CN > 1 && n_tiles % CN) CN >>= 1;
   CUtensorMap mA, mB;
-  const bool ok = make_map_2d(&mA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, w.limbs_x, 3 * (uint64_t)L, d.d, IBK, IBM) &&
-                  make_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, w.limbs_w, 3 * (uint64_t)NC, d.d, IBK, IBN);
+  const bool ok =
+      make_map_2d(&mA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, w.limbs_x, 3 * (uint64_t)L, d.d, IBK, IBM / CN) &&
+      make_map_2d(&mB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, w.limbs_w, 3 * (uint64_t)NC, d.d, IBK, IBN);
   if (!ok) {
     set_error("route: cuTensorMapEncodeTiled failed for the limb operands");
     return OMNIMOE_ERR_INVALID_ARGUMENT;
   }
   I8Args a{(int)L, NC, (int)d.d, w.ex, w.ew, logits};
-  dim3 grid((NC + IBN - 1) / IBN, (unsigned)((L + IBM - 1) / IBM));
-  gemm_i8_exact_kernel<<<grid, 256, kISmemBytes, st>>>(mA, mB, a);
+  dim3 grid(n_tiles, (unsigned)((L + IBM - 1) / IBM));
+  if (CN == 1) {
+    gemm_i8_exact_kernel<1><<<grid, 256, kISmemBytes, st>>>(mA, mB, a);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = kISmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CN;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = CN == 4 ? cudaLaunchKernelEx(&cfg, gemm_i8_exact_kernel<4>, mA, mB, a)
+                            : cudaLaunchKernelEx(&cfg, gemm_i8_exact_kernel<2>, mA, mB, a);
+    if (e != cudaSuccess) {
+      set_error(std::string("gemm_i8_exact_kernel (cluster launch): ") + cudaGetErrorString(e));
+      return OMNIMOE_ERR_CUDA;
+    }
+  }
   OMNI_CHECK_LAUNCH("gemm_i8_exact_kernel");
   // rows whose exponents do not fit 22 bits: exact fp64 path (no-ops when the lists are empty)
   OMNI_TRY(launch_exact_dd(d.dtype, x, sub, (int)d.d, NC, (int)L, logits, 1, w.bad_x, w.counts, st));
