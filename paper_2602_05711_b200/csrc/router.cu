@@ -364,67 +364,6 @@ __device__ uint64_t warp_half_topk(const float* __restrict__ lg, int n, int k1, 
   return mine;
 }
 
-__global__ void __launch_bounds__(256)
-    select_warp_kernel(SelectParams p, const float* __restrict__ logits, int32_t* __restrict__ idx,
-                       float* __restrict__ gate, float* __restrict__ score) {
-  __shared__ uint32_t cand[1024];
-  const int K1 = p.top_k + 1;
-  if (threadIdx.x == 0) {
-    int off = 0;
-    for (int a = 0; a < p.kr1; ++a) {
-      const int nb = min(p.kc1, K1 / (a + 1));
-      for (int b = 0; b < nb; ++b) cand[off++] = ((uint32_t)a << 16) | (uint32_t)b;
-    }
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  const int nw = (int)((gridDim.x * (int64_t)blockDim.x) >> 5);
-  const int R = p.n_rows + p.n_cols;
-  const int C = p.C, keep = min(K1, C);
-  const uint32_t Nc = (uint32_t)p.n_cols;
-  for (int th = gw; th < p.T; th += nw) {
-    const float* lg = logits + (size_t)th * R;
-    float lse_r, lse_c;
-    const uint64_t kr = warp_half_topk(lg, p.n_rows, p.kr1, &lse_r);
-    const uint64_t kc = warp_half_topk(lg + p.n_rows, p.n_cols, p.kc1, &lse_c);
-    // candidate keys, at most ceil(C / 32) per lane (C <= 32 * (ln 32 + 1) < 160)
-    U128 ck[5];
-    const int per = (C + 31) / 32;
-#pragma unroll
-    for (int m = 0; m < 5; ++m) {
-      const int c = lane + 32 * m;
-      const uint32_t ab = (m < per && c < C) ? cand[c] : 0u;
-      const uint64_t ka = __shfl_sync(0xffffffffu, kr, (int)(ab >> 16));
-      const uint64_t kb = __shfl_sync(0xffffffffu, kc, (int)(ab & 0xFFFF));
-      ck[m] = (m < per && c < C) ? cell_key(half_val(ka), half_val(kb), half_idx(ka) * Nc + half_idx(kb))
-                                 : U128{0ull, 0ull};
-    }
-    // the top `keep` candidates; lane t keeps the t-th
-    U128 mine{0ull, 0ull}, prev{~0ull, ~0ull};
-    for (int t = 0; t < keep; ++t) {
-      U128 best{0ull, 0ull};
-#pragma unroll
-      for (int m = 0; m < 5; ++m)
-        if (gt(prev, ck[m]) && gt(ck[m], best)) best = ck[m];
-      best = warp_max_u128(best);
-      if (lane == t) mine = best;
-      prev = best;
-    }
-    // gates: softmax over the first K keys (Eq.Gate)
-    const double k1v = key_value(U128{__shfl_sync(0xffffffffu, mine.hi, 0), __shfl_sync(0xffffffffu, mine.lo, 0)});
-    const double kv = key_value(mine);
-    const float ev = lane < p.top_k ? expf((float)(kv - k1v)) : 0.f;
-    const float es = warp_sum(ev);
-    if (lane < p.top_k) {
-      const size_t o = (size_t)th * p.top_k + lane;
-      idx[o] = (int32_t)(0xFFFFFFFFu - (uint32_t)mine.lo);
-      gate[o] = ev / es;
-      if (score) score[o] = (float)(kv - (double)lse_r - (double)lse_c);
-    }
-  }
-}
-
 // per-group shared memory: SelShared | kr (pkr u64) | kc (pkc u64) | sel (pkeep U128)
 template <int G>
 __host__ __device__ inline size_t group_bytes(const SelectParams& p) {
@@ -741,6 +680,88 @@ __device__ float warp_half_sorted(const float* __restrict__ lg, int n, int k1, i
   __syncwarp();
   warp_bitonic_desc(out, P);  // (a register-resident bitonic sort measured slower: 1.50 vs 1.24 ms)
   return lse;
+}
+
+// lane t (< k1 <= 32) returns the t-th largest half key of lg[0..n); *lse = logsumexp.
+// Long halves (n > 256): bucket selection of the top k1 + a 32-key warp sort; short
+// halves: k1 rounds of "largest key below the previous one".
+__device__ uint64_t warp_half_topk_any(const float* __restrict__ lg, int n, int k1, float* lse, int* hist,
+                                       uint64_t* srt) {
+  if (n <= 256) return warp_half_topk(lg, n, k1, lse);
+  const int lane = threadIdx.x & 31;
+  warp_half_sorted(lg, n, k1, 32, srt, hist, false);
+  const uint64_t mine = lane < k1 ? srt[lane] : 0ull;
+  const float mx = half_val(__shfl_sync(0xffffffffu, srt[0], 0));
+  __syncwarp();
+  float sm = 0.f;
+  for (int i = lane; i < n; i += 32) sm += __expf(lg[i] - mx);
+  *lse = mx + __logf(warp_sum(sm));
+  return mine;
+}
+
+__global__ void __launch_bounds__(256)
+    select_warp_kernel(SelectParams p, const float* __restrict__ logits, int32_t* __restrict__ idx,
+                       float* __restrict__ gate, float* __restrict__ score) {
+  __shared__ uint32_t cand[1024];
+  __shared__ int hist_all[8][256];      // per-warp bucket histograms (long halves)
+  __shared__ uint64_t sorted_all[8][32];  // per-warp top-k1 keys of a half
+  const int K1 = p.top_k + 1;
+  if (threadIdx.x == 0) {
+    int off = 0;
+    for (int a = 0; a < p.kr1; ++a) {
+      const int nb = min(p.kc1, K1 / (a + 1));
+      for (int b = 0; b < nb; ++b) cand[off++] = ((uint32_t)a << 16) | (uint32_t)b;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * (int64_t)blockDim.x) >> 5);
+  const int R = p.n_rows + p.n_cols;
+  const int C = p.C, keep = min(K1, C);
+  const uint32_t Nc = (uint32_t)p.n_cols;
+  for (int th = gw; th < p.T; th += nw) {
+    const float* lg = logits + (size_t)th * R;
+    float lse_r, lse_c;
+    int* hist = hist_all[(threadIdx.x >> 5) & 7];
+    uint64_t* srt = sorted_all[(threadIdx.x >> 5) & 7];
+    const uint64_t kr = warp_half_topk_any(lg, p.n_rows, p.kr1, &lse_r, hist, srt);
+    const uint64_t kc = warp_half_topk_any(lg + p.n_rows, p.n_cols, p.kc1, &lse_c, hist, srt);
+    // candidate keys, at most ceil(C / 32) per lane (C <= 32 * (ln 32 + 1) < 160)
+    U128 ck[5];
+    const int per = (C + 31) / 32;
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+      const int c = lane + 32 * m;
+      const uint32_t ab = (m < per && c < C) ? cand[c] : 0u;
+      const uint64_t ka = __shfl_sync(0xffffffffu, kr, (int)(ab >> 16));
+      const uint64_t kb = __shfl_sync(0xffffffffu, kc, (int)(ab & 0xFFFF));
+      ck[m] = (m < per && c < C) ? cell_key(half_val(ka), half_val(kb), half_idx(ka) * Nc + half_idx(kb))
+                                 : U128{0ull, 0ull};
+    }
+    // the top `keep` candidates; lane t keeps the t-th
+    U128 mine{0ull, 0ull}, prev{~0ull, ~0ull};
+    for (int t = 0; t < keep; ++t) {
+      U128 best{0ull, 0ull};
+#pragma unroll
+      for (int m = 0; m < 5; ++m)
+        if (gt(prev, ck[m]) && gt(ck[m], best)) best = ck[m];
+      best = warp_max_u128(best);
+      if (lane == t) mine = best;
+      prev = best;
+    }
+    // gates: softmax over the first K keys (Eq.Gate)
+    const double k1v = key_value(U128{__shfl_sync(0xffffffffu, mine.hi, 0), __shfl_sync(0xffffffffu, mine.lo, 0)});
+    const double kv = key_value(mine);
+    const float ev = lane < p.top_k ? expf((float)(kv - k1v)) : 0.f;
+    const float es = warp_sum(ev);
+    if (lane < p.top_k) {
+      const size_t o = (size_t)th * p.top_k + lane;
+      idx[o] = (int32_t)(0xFFFFFFFFu - (uint32_t)mine.lo);
+      gate[o] = ev / es;
+      if (score) score[o] = (float)(kv - (double)lse_r - (double)lse_c);
+    }
+  }
 }
 
 // smem: cand[C] (a << 16 | b, (a+1)(b+1) <= K) | per warp: kr[Pr], kc[Pc] (u64), hist[256],
