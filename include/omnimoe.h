@@ -252,6 +252,23 @@ omnimoe_status omnimoe_expert_fwd_pass(const omnimoe_dims* dims, int64_t L, cons
                                        float* y_routed, int accumulate, int pass, void* ws,
                                        size_t ws_bytes, omnimoe_stream_t stream);
 
+/* N2: backward of the routed branch for a fixed routing decision
+ * (Eq.Assemble, differentiated term by term): with z = x_l . w_e,
+ * s = sigma(z), q = dy_l . v_e for each task (l, e, g) of the plan,
+ *   dgate[t] = s q                      (task order t = ((l*h)+head)*K + k)
+ *   dV_e = sum g s dy_l,  dW_e = sum dz x_l,  dz = g q sigma'(z)
+ *   dx_l = sum_t dz_t w_e               (written, or added when accumulate_dx)
+ *   x, dy [L][d]; W_loc, V_loc [n_loc][d] (ROWS); W_sliced = omnimoe_pack_v(W_loc)
+ *   (the dx pass reads W slice by slice like pass V reads V); plan: the expert-major
+ *   plan (group size 1) with its V-order arrays and one band; dW_act, dV_act fp32
+ *   [n_loc][d]: row tau = the expert plan->active[tau] (tau < n_active; other rows
+ *   untouched); dgate fp32 [M].  bf16, d % 64 == 0, d <= 2048; no atomics (the
+ *   expert rows are owned by one warp pair, dx by one warp per slice). */
+omnimoe_status omnimoe_expert_bwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* W_loc,
+                                  const void* V_loc, const void* W_sliced, const omnimoe_plan* plan,
+                                  const void* dy, float* dx, float* dW_act, float* dV_act, float* dgate,
+                                  int accumulate_dx, void* ws, size_t ws_bytes, omnimoe_stream_t stream);
+
 /* V [n][d] (OMNIMOE_V_ROWS) -> V_sliced [d/32][n][32] (OMNIMOE_V_SLICED): a
  * one-time weight re-layout (no arithmetic; bit-exact copy), d % 32 == 0.
  * n = number of expert rows in the table (N, or n_loc for a shard). */

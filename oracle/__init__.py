@@ -45,12 +45,13 @@ def lib():
         _lib.oracle_shared_mlp.argtypes = [i64, i64, i64, P, P, P, P, c_int]
         _lib.oracle_load_stats.argtypes = [i64, P, P]
         _lib.oracle_dense_route.argtypes = [i64, i64, i64, P, c_int, P, P, P, P]
+        _lib.oracle_routed_bwd.argtypes = [i64, i64, i64, P, P, P, P, P, P, c_int, i64, P, P, P, P]
         _lib.oracle_layer.argtypes = [i64, i64, i64, i64, i64, i64, i64, P, P, P, P, P, i64, P, P,
                                       c_int, P, P, P, c_int]
         for f in ("oracle_logits", "oracle_route", "oracle_schedule", "oracle_routed_grouped",
                   "oracle_routed_token_centric",
                   "oracle_routed_expert_centric", "oracle_shared_mlp", "oracle_layer", "oracle_load_stats",
-                  "oracle_dense_route"):
+                  "oracle_dense_route", "oracle_routed_bwd"):
             getattr(_lib, f).restype = None
     return _lib
 
@@ -97,6 +98,20 @@ def route(logit_rows, n_rows, n_cols, K, method=PRODUCT, bsel=4096, nthreads=Non
     lib().oracle_route(T, n_rows, n_cols, K, _p(lg), method, bsel, nthreads or default_threads(),
                        _p(out["idx"]), _p(out["gate"]), _p(out["score"]), _p(out["key_hi"]),
                        _p(out["key_lo"]), _p(out["gap"]))
+    return out
+
+
+def routed_bwd(x, W, V, ids, gates, dy, act=0):
+    """N2: gradients of the routed branch for fixed routing -> dict(dx, dW, dV, dgate)
+    (dW, dV shaped like W, V; ids index their rows)."""
+    x, W, V, gates, dy = _f64(x), _f64(W), _f64(V), _f64(gates), _f64(dy)
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    L, d = x.shape
+    HK = ids.size // max(L, 1)
+    rows = W.shape[0]
+    out = dict(dx=np.empty((L, d)), dW=np.empty((rows, d)), dV=np.empty((rows, d)), dgate=np.empty((L, HK)))
+    lib().oracle_routed_bwd(L, d, HK, _p(x), _p(W), _p(V), _p(ids), _p(gates), _p(dy), act, rows, _p(out["dx"]),
+                            _p(out["dW"]), _p(out["dV"]), _p(out["dgate"]))
     return out
 
 

@@ -270,6 +270,41 @@ void oracle_dense_route(int64_t T, int64_t N, int64_t K, const float* logits, in
   });
 }
 
+// N2 (backward of the routed branch) for a fixed routing decision:
+// y_l = sum_k g_lk sigma(z_lk) v_n,  z_lk = x_l . w_n,  n = ids[l][k]  (Eq.Assemble).
+// Given dy = dLoss/dy (all fp64), the gradients follow the chain rule term by term:
+//   q = dy_l . v_n,  dgate_lk = sigma(z) q,  dz = g q sigma'(z),
+//   dV_n += g sigma(z) dy_l,  dW_n += dz x_l,  dx_l += dz w_n.
+// sigma = SiLU (reading Q1): sigma'(z) = s(z) (1 + z (1 - s(z))), s = logistic; IDENTITY: 1.
+// dW, dV: [rows][d] indexed like W, V (ids index their rows).
+void oracle_routed_bwd(int64_t L, int64_t d, int64_t HK, const double* x, const double* W, const double* V,
+                       const int32_t* ids, const double* gates, const double* dy, int act, int64_t rows,
+                       double* dx, double* dW, double* dV, double* dgate) {
+  std::fill(dx, dx + L * d, 0.0);
+  std::fill(dW, dW + rows * d, 0.0);
+  std::fill(dV, dV + rows * d, 0.0);
+  for (int64_t l = 0; l < L; ++l)
+    for (int64_t k = 0; k < HK; ++k) {
+      const int64_t n = ids[l * HK + k];
+      const double g = gates[l * HK + k];
+      double z = 0.0, q = 0.0;
+      for (int64_t c = 0; c < d; ++c) {
+        z += x[l * d + c] * W[n * d + c];
+        q += dy[l * d + c] * V[n * d + c];
+      }
+      const double lg = 1.0 / (1.0 + std::exp(-z));
+      const double s = act ? z : z * lg;
+      const double sp = act ? 1.0 : lg * (1.0 + z * (1.0 - lg));
+      const double dz = g * q * sp;
+      dgate[l * HK + k] = s * q;
+      for (int64_t c = 0; c < d; ++c) {
+        dV[n * d + c] += g * s * dy[l * d + c];
+        dW[n * d + c] += dz * x[l * d + c];
+        dx[l * d + c] += dz * W[n * d + c];
+      }
+    }
+}
+
 // O1 logits (Eq.Logits; reading Q9): for each token l, head h
 // and sub-key row r (rows [0,N_r) are W_r's columns, rows [N_r, N_r+N_c) are
 // W_c's), s = RN32(sum_k x[l][k]*sub[h][r][k]) -- the fp32 round-to-nearest-

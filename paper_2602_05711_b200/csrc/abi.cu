@@ -561,6 +561,47 @@ omnimoe_status omnimoe_expert_fwd_tokens(const omnimoe_dims* dims, int64_t L, co
                           (cudaStream_t)stream);
 }
 
+omnimoe_status omnimoe_expert_bwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* W_loc,
+                                  const void* V_loc, const void* W_sliced, const omnimoe_plan* plan,
+                                  const void* dy, float* dx, float* dW_act, float* dV_act, float* dgate,
+                                  int accumulate_dx, void* ws, size_t ws_bytes, omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  const omnimoe_dims& d = *dims;
+  if (d.dtype != OMNIMOE_BF16 || d.d % 64 != 0 || d.d > 2048) {
+    set_error("expert_bwd: bf16 with d % 64 == 0 and d <= 2048 " + dims_str(d));
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  if (L < 0) {
+    set_error("L must be >= 0");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (L == 0) return OMNIMOE_OK;
+  const void* req[] = {x, W_loc, V_loc, W_sliced, plan, dy, dx, dW_act, dV_act, dgate, ws};
+  for (const void* p : req)
+    if (!p) {
+      set_error("expert_bwd: a required pointer is null");
+      return OMNIMOE_ERR_INVALID_ARGUMENT;
+    }
+  OMNI_NONNULL(plan->sorted_task, "plan.sorted_task");
+  OMNI_NONNULL(plan->task_pair, "plan.task_pair");
+  OMNI_NONNULL(plan->token_offsets, "plan.token_offsets");
+  omnimoe_dims ds = d;
+  ds.v_layout = OMNIMOE_V_SLICED;
+  if (resolve_group_size(d) != 1 && d.group_size != 1) {
+    set_error("expert_bwd: needs the expert-major plan (group_size 1 or the SLICED layout)");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (resolve_v_bands(ds, plan->expert_end - plan->expert_begin) != 1) {
+    set_error("expert_bwd: one expert band only (64 * n_loc bytes <= the band size)");
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  OMNI_TRY(check_ws(ws_bytes, expert_ws_bytes(d, L), "expert_bwd"));
+  OMNI_TRY(check_device());
+  return expert_bwd_run(ds, L, x, W_loc, V_loc, W_sliced, *plan, dy, dx, dW_act, dV_act, dgate, accumulate_dx, ws,
+                        (cudaStream_t)stream);
+}
+
 int32_t omnimoe_layer_executor(const omnimoe_dims* dims, int64_t L) {
   if (validate_dims(dims) != OMNIMOE_OK || L < 0) return -1;
   if (layer_uses_token_executor(*dims, L)) return OMNIMOE_EXPERT_TOKEN;

@@ -1193,6 +1193,118 @@ omnimoe_status launch_dot(int d, const void* x, const void* W, const omnimoe_pla
   return OMNIMOE_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// N2: backward of the routed branch for a fixed routing decision,
+// on the expert-major plan (B = 1): a PAIR of warps per active expert, warp h of the
+// pair owning columns [h d/2, (h+1) d/2): w_e and v_e halves in registers; per task
+// the x_l and dy_l halves are gathered, the partial dots z = x_l . w_e and
+// q = dy_l . v_e are exchanged through shared memory (double-buffered, one named
+// barrier per task), then dV_e += g s(z) dy_l and dW_e += dz x_l accumulate in
+// registers (dz = g q s'(z)), and the expert's dW, dV rows are written once --
+// no atomics.  Per task: dgate = s(z) q (task order) and dz into task_pair.y for the
+// token-stationary dx pass (expert_vslice_kernel over the sliced W).
+template <int NVH>
+__global__ void __launch_bounds__(256)
+    expert_bwd_kernel(int d, const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ W,
+                      const __nv_bfloat16* __restrict__ V, const __nv_bfloat16* __restrict__ dy,
+                      const int32_t* __restrict__ offsets, const int32_t* __restrict__ active,
+                      const int32_t* __restrict__ n_active, const int32_t* __restrict__ stok,
+                      const float* __restrict__ sgate, const int32_t* __restrict__ stask,
+                      int32_t* __restrict__ task_pair, float* __restrict__ dgate, float* __restrict__ dW_act,
+                      float* __restrict__ dV_act, int act) {
+  __shared__ float xch[4][2][2][2];  // [pair][parity][half][z, q]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, pair = warp >> 1, h = warp & 1;
+  const int half = d / 2, c0 = h * half;
+  const int na = *n_active;
+  const int np = gridDim.x * 4;
+  int parity = 0;
+  for (int tau = blockIdx.x * 4 + pair; tau < na; tau += np) {
+    const int e = active[tau];
+    const int beg = offsets[e], end = offsets[e + 1];
+    uint4 wv[NVH], vv[NVH];
+    unsigned long long aw[NVH][4], av[NVH][4];
+#pragma unroll
+    for (int j = 0; j < NVH; ++j) {
+      const int c = (j * 32 + lane) * 8;
+      wv[j] = c < half ? ld_vec(W + (size_t)e * d + c0 + c) : make_uint4(0, 0, 0, 0);
+      vv[j] = c < half ? ld_vec(V + (size_t)e * d + c0 + c) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) aw[j][i] = av[j][i] = 0ull;
+    }
+    for (int p = beg; p < end; ++p) {
+      const int l = stok[p];
+      const float g = sgate[p];
+      uint4 xh[NVH], dh[NVH];
+#pragma unroll
+      for (int j = 0; j < NVH; ++j) {
+        const int c = (j * 32 + lane) * 8;
+        xh[j] = c < half ? ld_vec(x + (size_t)l * d + c0 + c) : make_uint4(0, 0, 0, 0);
+        dh[j] = c < half ? ld_vec(dy + (size_t)l * d + c0 + c) : make_uint4(0, 0, 0, 0);
+      }
+      float zp = 0.f, qp = 0.f;
+#pragma unroll
+      for (int j = 0; j < NVH; ++j) {
+        float u = dot2_bf16(0.f, xh[j].x, wv[j].x);
+        u = dot2_bf16(u, xh[j].y, wv[j].y);
+        u = dot2_bf16(u, xh[j].z, wv[j].z);
+        zp += dot2_bf16(u, xh[j].w, wv[j].w);
+        float v = dot2_bf16(0.f, dh[j].x, vv[j].x);
+        v = dot2_bf16(v, dh[j].y, vv[j].y);
+        v = dot2_bf16(v, dh[j].z, vv[j].z);
+        qp += dot2_bf16(v, dh[j].w, vv[j].w);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        zp += __shfl_xor_sync(0xffffffffu, zp, o);
+        qp += __shfl_xor_sync(0xffffffffu, qp, o);
+      }
+      if (lane == 0) {
+        xch[pair][parity][h][0] = zp;
+        xch[pair][parity][h][1] = qp;
+      }
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+      const float z = xch[pair][parity][0][0] + xch[pair][parity][1][0];  // same order in both warps
+      const float q = xch[pair][parity][0][1] + xch[pair][parity][1][1];
+      parity ^= 1;
+      const float lg = 1.0f / (1.0f + __expf(-z));
+      const float sz = act == OMNIMOE_IDENTITY ? z : z * lg;
+      const float sp = act == OMNIMOE_IDENTITY ? 1.0f : lg * (1.0f + z * (1.0f - lg));
+      const float a = g * sz, dz = g * q * sp;
+      if (h == 0 && lane == 0) {
+        const int t = stask[p];
+        dgate[t] = sz * q;
+        task_pair[2 * (size_t)t + 1] = __float_as_int(dz);
+      }
+      const unsigned long long a2 = ((unsigned long long)__float_as_uint(a) << 32) | __float_as_uint(a);
+      const unsigned long long z2 = ((unsigned long long)__float_as_uint(dz) << 32) | __float_as_uint(dz);
+#pragma unroll
+      for (int j = 0; j < NVH; ++j) {
+        axpy2_bf16(av[j][0], a2, dh[j].x);
+        axpy2_bf16(av[j][1], a2, dh[j].y);
+        axpy2_bf16(av[j][2], a2, dh[j].z);
+        axpy2_bf16(av[j][3], a2, dh[j].w);
+        axpy2_bf16(aw[j][0], z2, xh[j].x);
+        axpy2_bf16(aw[j][1], z2, xh[j].y);
+        axpy2_bf16(aw[j][2], z2, xh[j].z);
+        axpy2_bf16(aw[j][3], z2, xh[j].w);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NVH; ++j) {
+      const int c = (j * 32 + lane) * 8;
+      if (c < half) {
+        float4* dw = reinterpret_cast<float4*>(dW_act + (size_t)tau * d + c0 + c);
+        float4* dv = reinterpret_cast<float4*>(dV_act + (size_t)tau * d + c0 + c);
+        dw[0] = make_float4(lo_f(aw[j][0]), hi_f(aw[j][0]), lo_f(aw[j][1]), hi_f(aw[j][1]));
+        dw[1] = make_float4(lo_f(aw[j][2]), hi_f(aw[j][2]), lo_f(aw[j][3]), hi_f(aw[j][3]));
+        dv[0] = make_float4(lo_f(av[j][0]), hi_f(av[j][0]), lo_f(av[j][1]), hi_f(av[j][1]));
+        dv[1] = make_float4(lo_f(av[j][2]), hi_f(av[j][2]), lo_f(av[j][3]), hi_f(av[j][3]));
+      }
+    }
+  }
+}
+
 }  // namespace
 
 size_t expert_ws_bytes(const omnimoe_dims&, int64_t) { return 256; }  // work counter
@@ -1340,6 +1452,38 @@ omnimoe_status pack_v(int64_t n, int d, const void* V, void* Vs, cudaStream_t st
   pack_v_kernel<<<kSMs * 8, 256, 0, st>>>(static_cast<const uint4*>(V), static_cast<uint4*>(Vs), n, d);
   OMNI_CHECK_LAUNCH("pack_v_kernel");
   return OMNIMOE_OK;
+}
+
+omnimoe_status expert_bwd_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* V,
+                              const void* Ws, const omnimoe_plan& plan, const void* dy, float* dx, float* dW_act,
+                              float* dV_act, float* dgate, int accumulate_dx, void* ws, cudaStream_t st) {
+  const int d = (int)dm.d;
+  const int nvh = (d / 2 + 255) / 256;
+  int per_sm = 1;
+  auto X = static_cast<const __nv_bfloat16*>(x);
+  auto Wp = static_cast<const __nv_bfloat16*>(W);
+  auto Vp = static_cast<const __nv_bfloat16*>(V);
+  auto D = static_cast<const __nv_bfloat16*>(dy);
+#define OMNI_BWD_CASE(N)                                                                                        \
+  case N:                                                                                                      \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_bwd_kernel<N>, 256, 0);                      \
+    expert_bwd_kernel<N><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(                                          \
+        d, X, Wp, Vp, D, plan.expert_offsets, plan.active, plan.n_active, plan.sorted_token, plan.sorted_gate, \
+        plan.sorted_task, plan.task_pair, dgate, dW_act, dV_act, dm.act);                                      \
+    break;
+  switch (nvh) {
+    OMNI_BWD_CASE(1)
+    OMNI_BWD_CASE(2)
+    OMNI_BWD_CASE(3)
+    default:
+      OMNI_BWD_CASE(4)
+  }
+#undef OMNI_BWD_CASE
+  OMNI_CHECK_LAUNCH("expert_bwd_kernel");
+  // dx_l = sum_t dz_t w_e: the token-stationary slice pass over the sliced W
+  omnimoe_dims dv = dm;
+  dv.v_layout = OMNIMOE_V_SLICED;
+  return expert_sliced_run(dv, L, x, W, Ws, plan, dx, accumulate_dx, ws, st, 2);
 }
 
 omnimoe_status expert_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W,

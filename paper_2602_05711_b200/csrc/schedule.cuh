@@ -34,6 +34,10 @@ size_t expert_ws_bytes(const omnimoe_dims& d, int64_t L);
 omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* Vs,
                                  const omnimoe_plan& plan, float* y, int accumulate, void* ws, cudaStream_t st,
                                  int passes);
+// N2: routed-branch backward (expert-major plan, one band)
+omnimoe_status expert_bwd_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* V,
+                              const void* Ws, const omnimoe_plan& plan, const void* dy, float* dx, float* dW_act,
+                              float* dV_act, float* dgate, int accumulate_dx, void* ws, cudaStream_t st);
 omnimoe_status expert_run(const omnimoe_dims& d, int64_t L, const void* x, const void* W,
                           const void* V, const omnimoe_plan& plan, float* y, int accumulate,
                           void* ws, cudaStream_t st);

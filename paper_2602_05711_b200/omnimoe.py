@@ -54,7 +54,8 @@ EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnim
            "omnimoe_group_size", "omnimoe_token_blocks", "omnimoe_ep_pack_workspace_size",
            "omnimoe_ep_pack", "omnimoe_ep_unpack", "omnimoe_ep_combine", "omnimoe_pack_v",
            "omnimoe_v_bands", "omnimoe_expert_fwd_pass", "omnimoe_load_stats",
-           "omnimoe_load_stats_workspace_size", "omnimoe_expert_fwd_tokens", "omnimoe_layer_executor"]
+           "omnimoe_load_stats_workspace_size", "omnimoe_expert_fwd_tokens", "omnimoe_layer_executor",
+           "omnimoe_expert_bwd"]
 
 _lib = None
 
@@ -86,6 +87,7 @@ def load(path: str = LIB_PATH):
         "omnimoe_pack_v": [PD, I64, V, V, V],
         "omnimoe_load_stats": [PP, V, V, SZ, V],
         "omnimoe_expert_fwd_tokens": [PD, I64, V, V, V, V, V, V, I32, V],
+        "omnimoe_expert_bwd": [PD, I64, V, V, V, V, PP, V, V, V, V, V, I32, V, SZ, V],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -287,6 +289,33 @@ def load_stats(plan):
     cp = _cplan(plan)
     _check(lib.omnimoe_load_stats(ctypes.byref(cp), _ptr(out), _ptr(ws), ws.numel(), _stream()), "load_stats")
     return out
+
+
+def expert_bwd(dims: LayerDims, x, W_loc, V_loc, W_sliced, plan, dy, dx=None, accumulate_dx=False, ws=None):
+    """N2: routed-branch backward for the plan's routing (omnimoe_expert_bwd).
+    Returns (dx [L][d], dW_act, dV_act [n_active][d] in plan['active'] order, dgate [M])."""
+    L = x.shape[0]
+    n_loc = plan["expert_end"] - plan["expert_begin"]
+    M = plan["sorted_task"].numel()
+    _req(x, "x", dims.torch_dtype, L * dims.d)
+    _req(dy, "dy", dims.torch_dtype, L * dims.d)
+    _req(W_loc, "W_loc", dims.torch_dtype, n_loc * dims.d)
+    _req(V_loc, "V_loc", dims.torch_dtype, n_loc * dims.d)
+    _req(W_sliced, "W_sliced", dims.torch_dtype, n_loc * dims.d)
+    dev = x.device
+    if dx is None:
+        dx = torch.empty((L, dims.d), dtype=torch.float32, device=dev)
+        accumulate_dx = False
+    dW = torch.empty((n_loc, dims.d), dtype=torch.float32, device=dev)
+    dV = torch.empty((n_loc, dims.d), dtype=torch.float32, device=dev)
+    dg = torch.empty(max(M, 1), dtype=torch.float32, device=dev)
+    ws = ws if ws is not None else workspace(dims, L, WS_EXPERT, dev)
+    dc, cp = dims.c(), _cplan(plan)
+    _check(load().omnimoe_expert_bwd(ctypes.byref(dc), L, _ptr(x), _ptr(W_loc), _ptr(V_loc), _ptr(W_sliced),
+                                     ctypes.byref(cp), _ptr(dy), _ptr(dx), _ptr(dW), _ptr(dV), _ptr(dg),
+                                     int(accumulate_dx), _ptr(ws), ws.numel(), _stream()), "expert_bwd")
+    na = int(plan["n_active"].item())
+    return dx, dW[:na], dV[:na], dg[:M]
 
 
 def layer_executor(dims: LayerDims, L: int) -> int:

@@ -611,3 +611,33 @@ def test_layer_low_eta_uses_token_executor():
                        hr("w_gate_up"), hr("w_down"))
     e_tok, e_elt = rel_errors(y.float().cpu().numpy(), ref["y"])
     assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+
+
+# ---------------------------------------------------------------- N2: routed-branch backward
+@pytest.mark.parametrize("d,act", [(64, om.SILU), (256, om.SILU), (1024, om.SILU), (2048, om.SILU), (128, om.IDENTITY)])
+def test_expert_bwd_matches_oracle(d, act):
+    rng = np.random.default_rng(d + act)
+    L, N, HK = 200, 3000, 12
+    dims = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, act=act, group_size=1)
+    inp = make_inputs(dims, L, 9, skip=("subkeys",))
+    base = rng.integers(0, N - 64, L)
+    ids = np.stack([b0 + rng.choice(64, HK, replace=False) for b0 in base]).astype(np.int32)
+    gates = rng.random((L, HK)).astype(np.float32)
+    plan = om.schedule(dims, torch.from_numpy(ids).cuda().reshape(-1), torch.from_numpy(gates).cuda().reshape(-1))
+    dy = torch.randn(L, d, device="cuda", generator=torch.Generator(device="cuda").manual_seed(d)).to(torch.bfloat16)
+    sd = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, v_layout=om.V_SLICED)
+    Ws = om.pack_v(sd, inp["W"])
+    dx, dW, dV, dg = om.expert_bwd(dims, inp["x"], inp["W"], inp["V"], Ws, plan, dy)
+    torch.cuda.synchronize()
+    used = np.unique(ids)
+    remap = np.searchsorted(used, ids)
+    ref = oracle.routed_bwd(host_rows(dims, 9, "x", np.arange(L)), host_rows(dims, 9, "W", used),
+                            host_rows(dims, 9, "V", used), remap, gates.astype(np.float64),
+                            dy.double().cpu().numpy(), act)
+    act_ids = plan["active"][:int(plan["n_active"].item())].cpu().numpy()
+    np.testing.assert_array_equal(act_ids, used)
+    for got, want in ((dx, ref["dx"]), (dW, ref["dW"]), (dV, ref["dV"])):
+        e_tok, e_elt = rel_errors(got.cpu().numpy(), want)
+        assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+    np.testing.assert_allclose(dg.cpu().numpy(), ref["dgate"].reshape(-1),
+                               atol=1e-2 * np.abs(ref["dgate"]).max(), rtol=1e-2)

@@ -478,3 +478,49 @@ def test_dense_route_pins():
     np.testing.assert_allclose(g, [0.6 / 0.9, 0.3 / 0.9], rtol=1e-6)  # softmax over the selected only
     sh = oracle.dense_route(s + np.float32(4.0), 12)   # shift invariance (exact in fp32 here)
     np.testing.assert_array_equal(sh["idx"][:3], r["idx"][:3])
+
+
+# ---------------------------------------------------------------- N2: backward of the routed branch
+@pytest.mark.parametrize("act", [0, 1])
+def test_routed_bwd_matches_finite_differences(act):
+    """Every gradient of oracle.routed_bwd against central differences of the
+    forward oracle (loss = sum dy * y_routed), all in fp64."""
+    rng = np.random.default_rng(11 + act)
+    L, d, rows, HK = 5, 6, 9, 3
+    x = rng.standard_normal((L, d))
+    W = rng.standard_normal((rows, d)) * 0.5
+    V = rng.standard_normal((rows, d))
+    ids = np.stack([rng.choice(rows, HK, replace=False) for _ in range(L)]).astype(np.int32)
+    ids[2] = ids[0]                                   # two tokens sharing experts
+    g = rng.random((L, HK))
+    dy = rng.standard_normal((L, d))
+    grad = oracle.routed_bwd(x, W, V, ids, g, dy, act)
+
+    def loss(x_, W_, V_, g_):
+        return float((dy * oracle.routed_token_centric(x_, W_, V_, ids, g_, act)).sum())
+
+    h = 1e-6
+    for name, arr in (("dx", x), ("dW", W), ("dV", V), ("dgate", g)):
+        fd = np.zeros_like(arr)
+        for i in np.ndindex(arr.shape):
+            p_, m_ = arr.copy(), arr.copy()
+            p_[i] += h
+            m_[i] -= h
+            args_p = {"dx": (p_, W, V, g), "dW": (x, p_, V, g), "dV": (x, W, p_, g), "dgate": (x, W, V, p_)}[name]
+            args_m = {"dx": (m_, W, V, g), "dW": (x, m_, V, g), "dV": (x, W, m_, g), "dgate": (x, W, V, m_)}[name]
+            fd[i] = (loss(*args_p) - loss(*args_m)) / (2 * h)
+        np.testing.assert_allclose(grad[name], fd, rtol=1e-6, atol=1e-7, err_msg=name)
+
+
+def test_routed_bwd_closed_form():
+    """d = 2, one task: x = [1, 0], w = [2, 0], v = [1, 1], g = 1, dy = [1, 0]:
+    y = SiLU(2) v; dgate = SiLU(2) (dy . v) = SiLU(2); dV = SiLU(2) dy."""
+    s2 = 2 / (1 + np.exp(-2.0))
+    r = oracle.routed_bwd(np.array([[1.0, 0]]), np.array([[2.0, 0]]), np.array([[1.0, 1]]), np.array([[0]]),
+                          np.array([[1.0]]), np.array([[1.0, 0]]))
+    np.testing.assert_allclose(r["dgate"], [[s2]], rtol=1e-15)
+    np.testing.assert_allclose(r["dV"], [[s2, 0]], rtol=1e-15)
+    lg = 1 / (1 + np.exp(-2.0))
+    sp = lg * (1 + 2 * (1 - lg))
+    np.testing.assert_allclose(r["dx"], [[2 * sp, 0]], rtol=1e-14)   # dz = q sigma'(2) = sigma'(2); dx = dz w
+    np.testing.assert_allclose(r["dW"], [[sp, 0]], rtol=1e-14)       # dW = dz x
