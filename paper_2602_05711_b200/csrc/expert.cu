@@ -1204,7 +1204,7 @@ omnimoe_status launch_dot(int d, const void* x, const void* W, const omnimoe_pla
 // registers (dz = g q s'(z)), and the expert's dW, dV rows are written once --
 // no atomics.  Per task: dgate = s(z) q (task order) and dz into task_pair.y for the
 // token-stationary dx pass (expert_vslice_kernel over the sliced W).
-template <int NVH>
+template <int NVH, int G>
 __global__ void __launch_bounds__(256)
     expert_bwd_kernel(int d, const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ W,
                       const __nv_bfloat16* __restrict__ V, const __nv_bfloat16* __restrict__ dy,
@@ -1213,13 +1213,14 @@ __global__ void __launch_bounds__(256)
                       const float* __restrict__ sgate, const int32_t* __restrict__ stask,
                       int32_t* __restrict__ task_pair, float* __restrict__ dgate, float* __restrict__ dW_act,
                       float* __restrict__ dV_act, int act) {
-  __shared__ float xch[4][2][2][2];  // [pair][parity][half][z, q]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, pair = warp >> 1, h = warp & 1;
-  const int half = d / 2, c0 = h * half;
+  constexpr int kGroups = 8 / G;  // expert groups (of G warps) per CTA
+  __shared__ float xch[kGroups][2][G][2];  // [group][parity][part][z, q]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, pair = warp / G, h = warp % G;
+  const int half = d / G, c0 = h * half;  // this warp's column part
   const int na = *n_active;
-  const int np = gridDim.x * 4;
+  const int np = gridDim.x * kGroups;
   int parity = 0;
-  for (int tau = blockIdx.x * 4 + pair; tau < na; tau += np) {
+  for (int tau = blockIdx.x * kGroups + pair; tau < na; tau += np) {
     const int e = active[tau];
     const int beg = offsets[e], end = offsets[e + 1];
     uint4 wv[NVH], vv[NVH];
@@ -1263,9 +1264,13 @@ __global__ void __launch_bounds__(256)
         xch[pair][parity][h][0] = zp;
         xch[pair][parity][h][1] = qp;
       }
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
-      const float z = xch[pair][parity][0][0] + xch[pair][parity][1][0];  // same order in both warps
-      const float q = xch[pair][parity][0][1] + xch[pair][parity][1][1];
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + pair), "r"(32 * G) : "memory");
+      float z = 0.f, q = 0.f;  // the same summation order in every warp of the group
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        z += xch[pair][parity][u][0];
+        q += xch[pair][parity][u][1];
+      }
       parity ^= 1;
       const float lg = 1.0f / (1.0f + __expf(-z));
       const float sz = act == OMNIMOE_IDENTITY ? z : z * lg;
@@ -1458,25 +1463,26 @@ omnimoe_status expert_bwd_run(const omnimoe_dims& dm, int64_t L, const void* x, 
                               const void* Ws, const omnimoe_plan& plan, const void* dy, float* dx, float* dW_act,
                               float* dV_act, float* dgate, int accumulate_dx, void* ws, cudaStream_t st) {
   const int d = (int)dm.d;
-  const int nvh = (d / 2 + 255) / 256;
+  // d >= 1024: four warps per expert (a quarter of the columns each: more warps resident),
+  // else a pair
+  const bool quad = d >= 1024;
+  const int nvh = (d / (quad ? 4 : 2) + 255) / 256;
   int per_sm = 1;
   auto X = static_cast<const __nv_bfloat16*>(x);
   auto Wp = static_cast<const __nv_bfloat16*>(W);
   auto Vp = static_cast<const __nv_bfloat16*>(V);
   auto D = static_cast<const __nv_bfloat16*>(dy);
-#define OMNI_BWD_CASE(N)                                                                                        \
-  case N:                                                                                                      \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_bwd_kernel<N>, 256, 0);                      \
-    expert_bwd_kernel<N><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(                                          \
+#define OMNI_BWD_CASE(N, G)                                                                                     \
+  {                                                                                                            \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_bwd_kernel<N, G>, 256, 0);                   \
+    expert_bwd_kernel<N, G><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(                                       \
         d, X, Wp, Vp, D, plan.expert_offsets, plan.active, plan.n_active, plan.sorted_token, plan.sorted_gate, \
         plan.sorted_task, plan.task_pair, dgate, dW_act, dV_act, dm.act);                                      \
-    break;
-  switch (nvh) {
-    OMNI_BWD_CASE(1)
-    OMNI_BWD_CASE(2)
-    OMNI_BWD_CASE(3)
-    default:
-      OMNI_BWD_CASE(4)
+  }
+  if (quad) {
+    if (nvh <= 1) OMNI_BWD_CASE(1, 4) else OMNI_BWD_CASE(2, 4)
+  } else {
+    if (nvh <= 1) OMNI_BWD_CASE(1, 2) else OMNI_BWD_CASE(2, 2)
   }
 #undef OMNI_BWD_CASE
   OMNI_CHECK_LAUNCH("expert_bwd_kernel");
