@@ -46,12 +46,14 @@ def lib():
         _lib.oracle_load_stats.argtypes = [i64, P, P]
         _lib.oracle_dense_route.argtypes = [i64, i64, i64, P, c_int, P, P, P, P]
         _lib.oracle_routed_bwd.argtypes = [i64, i64, i64, P, P, P, P, P, P, c_int, i64, P, P, P, P]
+        _lib.oracle_router_bwd.argtypes = [i64, i64, i64, i64, i64, i64, P, P, P, P, P, P, P]
+        _lib.oracle_mlp_bwd.argtypes = [i64, i64, i64, P, P, P, P, P, P, P]
         _lib.oracle_layer.argtypes = [i64, i64, i64, i64, i64, i64, i64, P, P, P, P, P, i64, P, P,
                                       c_int, P, P, P, c_int]
         for f in ("oracle_logits", "oracle_route", "oracle_schedule", "oracle_routed_grouped",
                   "oracle_routed_token_centric",
                   "oracle_routed_expert_centric", "oracle_shared_mlp", "oracle_layer", "oracle_load_stats",
-                  "oracle_dense_route", "oracle_routed_bwd"):
+                  "oracle_dense_route", "oracle_routed_bwd", "oracle_router_bwd", "oracle_mlp_bwd"):
             getattr(_lib, f).restype = None
     return _lib
 
@@ -113,6 +115,32 @@ def routed_bwd(x, W, V, ids, gates, dy, act=0):
     lib().oracle_routed_bwd(L, d, HK, _p(x), _p(W), _p(V), _p(ids), _p(gates), _p(dy), act, rows, _p(out["dx"]),
                             _p(out["dW"]), _p(out["dV"]), _p(out["dgate"]))
     return out
+
+
+def router_bwd(x, subkeys, n_rows, n_cols, idx, gate, dgate):
+    """N2 router part: (dx [L][d], dsub [h][R][d]) for fixed selections idx [L][h][K]."""
+    x, sub = _f64(x), _f64(subkeys)
+    L, d = x.shape
+    h = sub.shape[0]
+    idx = np.ascontiguousarray(idx, dtype=np.int32)
+    K = idx.shape[-1]
+    dx = np.zeros((L, d))
+    dsub = np.empty(sub.shape)
+    lib().oracle_router_bwd(L, d, h, n_rows, n_cols, K, _p(x), _p(sub), _p(idx), _p(_f64(gate)), _p(_f64(dgate)),
+                            _p(dx), _p(dsub))
+    return dx, dsub
+
+
+def mlp_bwd(x, w_gu, w_down, dy):
+    """N2 shared-MLP part: (dx, dw_gate_up, dw_down)."""
+    x, w_gu, w_down, dy = _f64(x), _f64(w_gu), _f64(w_down), _f64(dy)
+    L, d = x.shape
+    dff = w_down.shape[1]
+    dx = np.zeros((L, d))
+    dgu = np.empty(w_gu.shape)
+    ddn = np.empty(w_down.shape)
+    lib().oracle_mlp_bwd(L, d, dff, _p(x), _p(w_gu), _p(w_down), _p(dy), _p(dx), _p(dgu), _p(ddn))
+    return dx, dgu, ddn
 
 
 def load_stats(counts):

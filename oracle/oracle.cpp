@@ -305,6 +305,81 @@ void oracle_routed_bwd(int64_t L, int64_t d, int64_t HK, const double* x, const 
     }
 }
 
+// N2, router part: gradients through Eq.Gate (softmax over the K selected keys,
+// PAPER:136-139) and Eq.S / Eq.Logits (key = s_r[i] + s_c[j], s = x . sub, PAPER:
+// 211-224) with the selection held fixed (top-K is piecewise constant).  Per token-
+// head: dkappa_k = g_k (dgate_k - sum_j g_j dgate_j); ds_r[i] += dkappa, ds_c[j] +=
+// dkappa; dsub[h][r] += ds[l][h][r] x_l; dx_l += sum_r ds[l][h][r] sub[h][r].
+// gate: the forward gates; dx accumulates; dsub [h][Nr+Nc][d] is overwritten.
+void oracle_router_bwd(int64_t L, int64_t d, int64_t h, int64_t Nr, int64_t Nc, int64_t K, const double* x,
+                       const double* sub, const int32_t* idx, const double* gate, const double* dgate, double* dx,
+                       double* dsub) {
+  const int64_t R = Nr + Nc;
+  std::fill(dsub, dsub + h * R * d, 0.0);
+  std::vector<double> ds(R);
+  for (int64_t l = 0; l < L; ++l)
+    for (int64_t hh = 0; hh < h; ++hh) {
+      const int64_t t = l * h + hh;
+      double dot = 0.0;
+      for (int64_t k = 0; k < K; ++k) dot += gate[t * K + k] * dgate[t * K + k];
+      std::fill(ds.begin(), ds.end(), 0.0);
+      for (int64_t k = 0; k < K; ++k) {
+        const double dk = gate[t * K + k] * (dgate[t * K + k] - dot);
+        const int64_t n = idx[t * K + k];
+        ds[n / Nc] += dk;
+        ds[Nr + n % Nc] += dk;
+      }
+      for (int64_t r = 0; r < R; ++r) {
+        if (ds[r] == 0.0) continue;
+        const double* sr = sub + (hh * R + r) * d;
+        double* dr = dsub + (hh * R + r) * d;
+        for (int64_t c = 0; c < d; ++c) {
+          dr[c] += ds[r] * x[l * d + c];
+          dx[l * d + c] += ds[r] * sr[c];
+        }
+      }
+    }
+}
+
+// N2, shared MLP (reading Q2): G = x W_g^T, U = x W_u^T, H = SiLU(G) U, y = H W_down^T.
+// dH = dy W_down; dU = dH SiLU(G); dG = dH U SiLU'(G); dW_down = dy^T H;
+// dW_gu = [dG dU]^T x (gate rows then up rows); dx += dG W_g + dU W_u.
+void oracle_mlp_bwd(int64_t L, int64_t d, int64_t dff, const double* x, const double* w_gu, const double* w_down,
+                    const double* dy, double* dx, double* dw_gu, double* dw_down) {
+  std::fill(dw_gu, dw_gu + 2 * dff * d, 0.0);
+  std::fill(dw_down, dw_down + d * dff, 0.0);
+  std::vector<double> G(dff), U(dff), H(dff), dH(dff);
+  for (int64_t l = 0; l < L; ++l) {
+    const double* xl = x + l * d;
+    const double* gl = dy + l * d;
+    for (int64_t f = 0; f < dff; ++f) {
+      double g = 0.0, u = 0.0;
+      for (int64_t c = 0; c < d; ++c) {
+        g += xl[c] * w_gu[f * d + c];
+        u += xl[c] * w_gu[(dff + f) * d + c];
+      }
+      G[f] = g;
+      U[f] = u;
+      H[f] = g / (1.0 + std::exp(-g)) * u;
+      double s = 0.0;
+      for (int64_t c = 0; c < d; ++c) s += gl[c] * w_down[c * dff + f];
+      dH[f] = s;
+    }
+    for (int64_t c = 0; c < d; ++c)
+      for (int64_t f = 0; f < dff; ++f) dw_down[c * dff + f] += gl[c] * H[f];
+    for (int64_t f = 0; f < dff; ++f) {
+      const double sg = 1.0 / (1.0 + std::exp(-G[f]));
+      const double silu = G[f] * sg, dsilu = sg * (1.0 + G[f] * (1.0 - sg));
+      const double dU = dH[f] * silu, dG = dH[f] * U[f] * dsilu;
+      for (int64_t c = 0; c < d; ++c) {
+        dw_gu[f * d + c] += dG * xl[c];
+        dw_gu[(dff + f) * d + c] += dU * xl[c];
+        dx[l * d + c] += dG * w_gu[f * d + c] + dU * w_gu[(dff + f) * d + c];
+      }
+    }
+  }
+}
+
 // O1 logits (Eq.Logits; reading Q9): for each token l, head h
 // and sub-key row r (rows [0,N_r) are W_r's columns, rows [N_r, N_r+N_c) are
 // W_c's), s = RN32(sum_k x[l][k]*sub[h][r][k]) -- the fp32 round-to-nearest-

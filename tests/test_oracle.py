@@ -524,3 +524,51 @@ def test_routed_bwd_closed_form():
     sp = lg * (1 + 2 * (1 - lg))
     np.testing.assert_allclose(r["dx"], [[2 * sp, 0]], rtol=1e-14)   # dz = q sigma'(2) = sigma'(2); dx = dz w
     np.testing.assert_allclose(r["dW"], [[sp, 0]], rtol=1e-14)       # dW = dz x
+
+
+def _fd(f, arr, h=1e-6):
+    g = np.zeros_like(arr)
+    for i in np.ndindex(arr.shape):
+        p_, m_ = arr.copy(), arr.copy()
+        p_[i] += h
+        m_[i] -= h
+        g[i] = (f(p_) - f(m_)) / (2 * h)
+    return g
+
+
+def test_router_bwd_matches_finite_differences():
+    """loss = sum dgate * gate(x, sub) with the selected cells fixed (softmax over the
+    selected keys, key = s_r + s_c, s = x . sub), against the analytic chain."""
+    rng = np.random.default_rng(2)
+    L, d, h, Nr, Nc, K = 3, 5, 2, 4, 3, 4
+    x = rng.standard_normal((L, d))
+    sub = rng.standard_normal((h, Nr + Nc, d))
+    idx = np.stack([np.stack([rng.choice(Nr * Nc, K, replace=False) for _ in range(h)]) for _ in range(L)])
+    idx = idx.astype(np.int32)
+    dg = rng.standard_normal((L, h, K))
+
+    def gates(x_, sub_):
+        s = np.einsum("ld,hrd->lhr", x_, sub_)
+        key = s[..., :Nr][np.arange(L)[:, None, None], np.arange(h)[None, :, None], idx // Nc] + \
+            s[..., Nr:][np.arange(L)[:, None, None], np.arange(h)[None, :, None], idx % Nc]
+        e = np.exp(key - key.max(-1, keepdims=True))
+        return e / e.sum(-1, keepdims=True)
+
+    g0 = gates(x, sub)
+    dx, dsub = oracle.router_bwd(x, sub, Nr, Nc, idx, g0, dg)
+    np.testing.assert_allclose(dx, _fd(lambda a: float((dg * gates(a, sub)).sum()), x), rtol=1e-6, atol=1e-8)
+    np.testing.assert_allclose(dsub, _fd(lambda a: float((dg * gates(x, a)).sum()), sub), rtol=1e-6, atol=1e-8)
+
+
+def test_mlp_bwd_matches_finite_differences():
+    rng = np.random.default_rng(4)
+    L, d, dff = 3, 5, 4
+    x = rng.standard_normal((L, d))
+    wgu = rng.standard_normal((2 * dff, d)) * 0.5
+    wdn = rng.standard_normal((d, dff)) * 0.5
+    dy = rng.standard_normal((L, d))
+    dx, dgu, ddn = oracle.mlp_bwd(x, wgu, wdn, dy)
+    loss = lambda x_, a_, b_: float((dy * oracle.shared_mlp(x_, a_, b_)).sum())
+    np.testing.assert_allclose(dx, _fd(lambda a: loss(a, wgu, wdn), x), rtol=1e-6, atol=1e-8)
+    np.testing.assert_allclose(dgu, _fd(lambda a: loss(x, a, wdn), wgu), rtol=1e-6, atol=1e-8)
+    np.testing.assert_allclose(ddn, _fd(lambda a: loss(x, wgu, a), wdn), rtol=1e-6, atol=1e-8)
