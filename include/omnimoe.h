@@ -67,7 +67,8 @@ enum { OMNIMOE_EXPERT_AUTO = 0, OMNIMOE_EXPERT_WARP = 1, OMNIMOE_EXPERT_GROUP = 
  * (DESIGN.md §4.4). */
 enum { OMNIMOE_V_ROWS = 0, OMNIMOE_V_SLICED = 1 };
 /* workspace query selector */
-enum { OMNIMOE_WS_ROUTE = 0, OMNIMOE_WS_SCHEDULE = 1, OMNIMOE_WS_EXPERT = 2, OMNIMOE_WS_LAYER = 3 };
+enum { OMNIMOE_WS_ROUTE = 0, OMNIMOE_WS_SCHEDULE = 1, OMNIMOE_WS_EXPERT = 2, OMNIMOE_WS_LAYER = 3,
+       OMNIMOE_WS_ROUTER_BWD = 4, OMNIMOE_WS_MLP_BWD = 5 };
 
 /* How omnimoe_route computes the sub-key logits.  Both give the same bits:
  * logit = RN32(exact dot product x . w) (reading Q9).
@@ -268,6 +269,30 @@ omnimoe_status omnimoe_expert_bwd(const omnimoe_dims* dims, int64_t L, const voi
                                   const void* V_loc, const void* W_sliced, const omnimoe_plan* plan,
                                   const void* dy, float* dx, float* dW_act, float* dV_act, float* dgate,
                                   int accumulate_dx, void* ws, size_t ws_bytes, omnimoe_stream_t stream);
+
+/* N2, router part: gradients through the gates (softmax over the K selected keys,
+ * Eq.Gate) and the sub-key logits (key = s_r[i] + s_c[j], s = x . sub,
+ * Eq.S / Eq.Logits) with the selection held fixed:
+ *   dkappa_k = g_k (dgate_k - sum_j g_j dgate_j);  ds_r[i] += dkappa, ds_c[j] += dkappa
+ *   dsub[h][r] = sum_l ds[l][h][r] x_l   (fp32 [h][N_r+N_c][d], overwritten)
+ *   dx_l (+)= sum_{h,r} ds[l][h][r] sub[h][r]   (fp32 [L][d]; added when accumulate_dx)
+ *   idx, gate [L][h][K]: the forward's routing (any order); dgate [L][h][K] (from
+ *   omnimoe_expert_bwd).  ds is rounded to bf16 for the tcgen05 GEMMs.
+ *   ws: omnimoe_workspace_size(OMNIMOE_WS_ROUTER_BWD). */
+omnimoe_status omnimoe_router_bwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* subkeys,
+                                  const int32_t* idx, const float* gate, const float* dgate, float* dx,
+                                  int accumulate_dx, float* dsubkeys, void* ws, size_t ws_bytes,
+                                  omnimoe_stream_t stream);
+
+/* N2, shared MLP (reading Q2): with G|U = x W_gu^T, H = SiLU(G) U:
+ *   dw_down = dy^T H (fp32 [d][d_ff]), dw_gate_up = [dG|dU]^T x (fp32 [2 d_ff][d]),
+ *   dx (+)= [dG|dU] W_gu, where dU = dH SiLU(G), dG = dH U SiLU'(G), dH = dy W_down.
+ *   bf16 operands on the tcgen05 GEMM engine, fp32 results.
+ *   ws: omnimoe_workspace_size(OMNIMOE_WS_MLP_BWD). */
+omnimoe_status omnimoe_shared_mlp_bwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* w_gate_up,
+                                      const void* w_down, const void* dy, float* dx, int accumulate_dx,
+                                      float* dw_gate_up, float* dw_down, void* ws, size_t ws_bytes,
+                                      omnimoe_stream_t stream);
 
 /* V [n][d] (OMNIMOE_V_ROWS) -> V_sliced [d/32][n][32] (OMNIMOE_V_SLICED): a
  * one-time weight re-layout (no arithmetic; bit-exact copy), d % 32 == 0.

@@ -4,6 +4,7 @@
 #include <mutex>
 #include <string>
 
+#include "backward.cuh"
 #include "ep.cuh"
 #include "gemm.cuh"
 #include "router.cuh"
@@ -299,6 +300,8 @@ omnimoe_status omnimoe_workspace_size(const omnimoe_dims* dims, int64_t L, int w
     case OMNIMOE_WS_SCHEDULE: *bytes = schedule_ws_bytes(L, d.n_rows * d.n_cols); break;
     case OMNIMOE_WS_EXPERT: *bytes = expert_ws_bytes(d, L); break;
     case OMNIMOE_WS_LAYER: *bytes = layer_ws(d, L, nullptr, nullptr); break;
+    case OMNIMOE_WS_ROUTER_BWD: *bytes = router_bwd_ws_bytes(d, L); break;
+    case OMNIMOE_WS_MLP_BWD: *bytes = mlp_bwd_ws_bytes(d, L); break;
     default:
       set_error("unknown workspace selector " + std::to_string(which));
       return OMNIMOE_ERR_INVALID_ARGUMENT;
@@ -600,6 +603,52 @@ omnimoe_status omnimoe_expert_bwd(const omnimoe_dims* dims, int64_t L, const voi
   OMNI_TRY(check_device());
   return expert_bwd_run(ds, L, x, W_loc, V_loc, W_sliced, *plan, dy, dx, dW_act, dV_act, dgate, accumulate_dx, ws,
                         (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_router_bwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* subkeys,
+                                  const int32_t* idx, const float* gate, const float* dgate, float* dx,
+                                  int accumulate_dx, float* dsubkeys, void* ws, size_t ws_bytes,
+                                  omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  if (dims->dtype != OMNIMOE_BF16 || dims->router == OMNIMOE_ROUTER_DENSE) {
+    set_error("router_bwd: the bf16 Cartesian router only");
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  if (L <= 0) return L == 0 ? OMNIMOE_OK : OMNIMOE_ERR_INVALID_ARGUMENT;
+  const void* req[] = {x, subkeys, idx, gate, dgate, dx, dsubkeys, ws};
+  for (const void* p : req)
+    if (!p) {
+      set_error("router_bwd: a required pointer is null");
+      return OMNIMOE_ERR_INVALID_ARGUMENT;
+    }
+  OMNI_TRY(check_ws(ws_bytes, router_bwd_ws_bytes(*dims, L), "router_bwd"));
+  OMNI_TRY(check_device());
+  return router_bwd_run(*dims, L, x, subkeys, idx, gate, dgate, dx, accumulate_dx, dsubkeys, ws,
+                        (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_shared_mlp_bwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* w_gate_up,
+                                      const void* w_down, const void* dy, float* dx, int accumulate_dx,
+                                      float* dw_gate_up, float* dw_down, void* ws, size_t ws_bytes,
+                                      omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  if (dims->dtype != OMNIMOE_BF16 || dims->d_ff < 1) {
+    set_error("shared_mlp_bwd: bf16 with d_ff >= 1");
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  if (L <= 0) return L == 0 ? OMNIMOE_OK : OMNIMOE_ERR_INVALID_ARGUMENT;
+  const void* req[] = {x, w_gate_up, w_down, dy, dx, dw_gate_up, dw_down, ws};
+  for (const void* p : req)
+    if (!p) {
+      set_error("shared_mlp_bwd: a required pointer is null");
+      return OMNIMOE_ERR_INVALID_ARGUMENT;
+    }
+  OMNI_TRY(check_ws(ws_bytes, mlp_bwd_ws_bytes(*dims, L), "shared_mlp_bwd"));
+  OMNI_TRY(check_device());
+  return mlp_bwd_run(*dims, L, x, w_gate_up, w_down, dy, dx, accumulate_dx, dw_gate_up, dw_down, ws,
+                     (cudaStream_t)stream);
 }
 
 int32_t omnimoe_layer_executor(const omnimoe_dims* dims, int64_t L) {

@@ -23,7 +23,7 @@ V_ROWS, V_SLICED = 0, 1
 ORDER_KEY, ORDER_CANDIDATE = 0, 1
 ROUTER_EXACT, ROUTER_EXACT_F64, ROUTER_DENSE = 0, 1, 2
 LOGITS_ROUTE, LOGITS_EXACT_F64, LOGITS_BF16_FAST = 0, 1, 2
-WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER = 0, 1, 2, 3
+WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER, WS_ROUTER_BWD, WS_MLP_BWD = 0, 1, 2, 3, 4, 5
 
 
 class OmniMoEError(RuntimeError):
@@ -55,7 +55,7 @@ EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnim
            "omnimoe_ep_pack", "omnimoe_ep_unpack", "omnimoe_ep_combine", "omnimoe_pack_v",
            "omnimoe_v_bands", "omnimoe_expert_fwd_pass", "omnimoe_load_stats",
            "omnimoe_load_stats_workspace_size", "omnimoe_expert_fwd_tokens", "omnimoe_layer_executor",
-           "omnimoe_expert_bwd"]
+           "omnimoe_expert_bwd", "omnimoe_router_bwd", "omnimoe_shared_mlp_bwd"]
 
 _lib = None
 
@@ -88,6 +88,8 @@ def load(path: str = LIB_PATH):
         "omnimoe_load_stats": [PP, V, V, SZ, V],
         "omnimoe_expert_fwd_tokens": [PD, I64, V, V, V, V, V, V, I32, V],
         "omnimoe_expert_bwd": [PD, I64, V, V, V, V, PP, V, V, V, V, V, I32, V, SZ, V],
+        "omnimoe_router_bwd": [PD, I64, V, V, V, V, V, V, I32, V, V, SZ, V],
+        "omnimoe_shared_mlp_bwd": [PD, I64, V, V, V, V, V, I32, V, V, V, SZ, V],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -316,6 +318,39 @@ def expert_bwd(dims: LayerDims, x, W_loc, V_loc, W_sliced, plan, dy, dx=None, ac
                                      int(accumulate_dx), _ptr(ws), ws.numel(), _stream()), "expert_bwd")
     na = int(plan["n_active"].item())
     return dx, dW[:na], dV[:na], dg[:M]
+
+
+def router_bwd(dims: LayerDims, x, subkeys, idx, gate, dgate, dx=None, accumulate_dx=False):
+    """N2 router part (omnimoe_router_bwd) -> (dx [L][d] fp32, dsubkeys [h][R][d] fp32)."""
+    L = x.shape[0]
+    dev = x.device
+    if dx is None:
+        dx = torch.empty((L, dims.d), dtype=torch.float32, device=dev)
+        accumulate_dx = False
+    dsub = torch.empty((dims.n_heads, dims.n_rows + dims.n_cols, dims.d), dtype=torch.float32, device=dev)
+    ws = workspace(dims, L, WS_ROUTER_BWD, dev)
+    dc = dims.c()
+    _check(load().omnimoe_router_bwd(ctypes.byref(dc), L, _ptr(x), _ptr(subkeys), _ptr(idx.contiguous()),
+                                     _ptr(gate.contiguous()), _ptr(dgate.contiguous()), _ptr(dx),
+                                     int(accumulate_dx), _ptr(dsub), _ptr(ws), ws.numel(), _stream()), "router_bwd")
+    return dx, dsub
+
+
+def shared_mlp_bwd(dims: LayerDims, x, w_gate_up, w_down, dy, dx=None, accumulate_dx=False):
+    """N2 shared-MLP part (omnimoe_shared_mlp_bwd) -> (dx, dw_gate_up, dw_down), fp32."""
+    L = x.shape[0]
+    dev = x.device
+    if dx is None:
+        dx = torch.empty((L, dims.d), dtype=torch.float32, device=dev)
+        accumulate_dx = False
+    dgu = torch.empty((2 * dims.d_ff, dims.d), dtype=torch.float32, device=dev)
+    ddn = torch.empty((dims.d, dims.d_ff), dtype=torch.float32, device=dev)
+    ws = workspace(dims, L, WS_MLP_BWD, dev)
+    dc = dims.c()
+    _check(load().omnimoe_shared_mlp_bwd(ctypes.byref(dc), L, _ptr(x), _ptr(w_gate_up), _ptr(w_down), _ptr(dy),
+                                         _ptr(dx), int(accumulate_dx), _ptr(dgu), _ptr(ddn), _ptr(ws), ws.numel(),
+                                         _stream()), "shared_mlp_bwd")
+    return dx, dgu, ddn
 
 
 def layer_executor(dims: LayerDims, L: int) -> int:

@@ -641,3 +641,39 @@ def test_expert_bwd_matches_oracle(d, act):
         assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
     np.testing.assert_allclose(dg.cpu().numpy(), ref["dgate"].reshape(-1),
                                atol=1e-2 * np.abs(ref["dgate"]).max(), rtol=1e-2)
+
+
+@pytest.mark.parametrize("d,nr,nc,K,h,L", [(64, 32, 32, 8, 1, 256), (256, 64, 64, 64, 2, 300), (1024, 256, 256, 512, 1, 64)])
+def test_router_bwd_matches_oracle(d, nr, nc, K, h, L):
+    dims = om.LayerDims(d=d, n_rows=nr, n_cols=nc, top_k=K, n_heads=h, d_ff=0)
+    inp = make_inputs(dims, L, 31, skip=("W", "V", "w_gate_up", "w_down"))
+    idx, gate, _ = om.route(dims, inp["x"], inp["subkeys"])
+    dg = torch.randn(L, h, K, device="cuda", generator=torch.Generator(device="cuda").manual_seed(7))
+    dx0 = torch.randn(L, d, device="cuda")
+    dx, dsub = om.router_bwd(dims, inp["x"], inp["subkeys"], idx, gate, dg, dx=dx0.clone(), accumulate_dx=True)
+    torch.cuda.synchronize()
+    x = host_rows(dims, 31, "x", np.arange(L))
+    sub = host_rows(dims, 31, "subkeys").reshape(h, nr + nc, d)
+    rdx, rdsub = oracle.router_bwd(x, sub, nr, nc, idx.cpu().numpy(), gate.cpu().double().numpy(),
+                                   dg.cpu().double().numpy())
+    e = rel_errors((dx - dx0).cpu().numpy(), rdx)
+    assert e[0] <= 1e-2 and e[1] <= 1e-2, e
+    used = np.abs(rdsub).reshape(-1, d).sum(1) > 0        # sub-key rows never selected get 0
+    got = dsub.cpu().numpy().reshape(-1, d)
+    assert np.all(got[~used] == 0)
+    e = rel_errors(got[used], rdsub.reshape(-1, d)[used])
+    assert e[0] <= 1e-2 and e[1] <= 1e-2, e
+
+
+@pytest.mark.parametrize("L,d,dff", [(256, 64, 128), (300, 256, 512), (130, 1024, 1024)])
+def test_shared_mlp_bwd_matches_oracle(L, d, dff):
+    dims = om.LayerDims(d=d, n_rows=2, n_cols=2, top_k=1, d_ff=dff)
+    inp = make_inputs(dims, L, 13, skip=("subkeys", "W", "V"))
+    dy = torch.randn(L, d, device="cuda", generator=torch.Generator(device="cuda").manual_seed(3)).to(torch.bfloat16)
+    dx, dgu, ddn = om.shared_mlp_bwd(dims, inp["x"], inp["w_gate_up"], inp["w_down"], dy)
+    torch.cuda.synchronize()
+    rdx, rdgu, rddn = oracle.mlp_bwd(host_rows(dims, 13, "x", np.arange(L)), host_rows(dims, 13, "w_gate_up"),
+                                     host_rows(dims, 13, "w_down"), dy.double().cpu().numpy())
+    for got, want in ((dx, rdx), (dgu, rdgu), (ddn, rddn)):
+        e = rel_errors(got.cpu().numpy().reshape(want.shape[0], -1), want.reshape(want.shape[0], -1))
+        assert e[0] <= 1e-2 and e[1] <= 1e-2, e
