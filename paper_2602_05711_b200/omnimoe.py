@@ -353,6 +353,26 @@ def shared_mlp_bwd(dims: LayerDims, x, w_gate_up, w_down, dy, dx=None, accumulat
     return dx, dgu, ddn
 
 
+def layer_bwd(dims: LayerDims, x, subkeys, W, V, W_sliced, w_gate_up, w_down, idx, gate, plan, dy):
+    """N2: the layer's backward for the forward's routing decision (idx, gate [L][h][K],
+    the plan of those tasks with group size 1): routed branch (omnimoe_expert_bwd), router
+    gates (omnimoe_router_bwd) and shared MLP (omnimoe_shared_mlp_bwd), dx summed over the
+    three.  Returns dict(dx, dsubkeys, dW_act, dV_act, active, dgate, dw_gate_up, dw_down)."""
+    rd = dims if dims.group_size == 1 else _replace(dims, group_size=1)
+    dx, dW, dV, dg = expert_bwd(rd, x, W, V, W_sliced, plan, dy)
+    _, dsub = router_bwd(dims, x, subkeys, idx, gate, dg.reshape(gate.shape), dx=dx, accumulate_dx=True)
+    out = dict(dx=dx, dsubkeys=dsub, dW_act=dW, dV_act=dV, active=plan["active"][:dW.shape[0]], dgate=dg)
+    if dims.d_ff:
+        _, dgu, ddn = shared_mlp_bwd(dims, x, w_gate_up, w_down, dy, dx=dx, accumulate_dx=True)
+        out.update(dw_gate_up=dgu, dw_down=ddn)
+    return out
+
+
+def _replace(d, **kw):
+    import dataclasses
+    return dataclasses.replace(d, **kw)
+
+
 def layer_executor(dims: LayerDims, L: int) -> int:
     """The routed-branch executor (EXPERT_*) omnimoe_layer_fwd uses for L tokens."""
     dc = dims.c()

@@ -677,3 +677,37 @@ def test_shared_mlp_bwd_matches_oracle(L, d, dff):
     for got, want in ((dx, rdx), (dgu, rdgu), (ddn, rddn)):
         e = rel_errors(got.cpu().numpy().reshape(want.shape[0], -1), want.reshape(want.shape[0], -1))
         assert e[0] <= 1e-2 and e[1] <= 1e-2, e
+
+
+def test_layer_bwd_composition():
+    """N2 end to end at a C1-like shape: the three backward calls against the oracle's
+    routed / router / MLP backward on the GPU's own routing (dx summed over all three)."""
+    w = _dims("C1", v_layout=om.V_SLICED)
+    dims = w.dims
+    L = w.L
+    inp = make_inputs(dims, L, w.seed)
+    Vs, Ws = om.pack_v(dims, inp["V"]), om.pack_v(dims, inp["W"])
+    idx, gate, _ = om.route(dims, inp["x"], inp["subkeys"])
+    plan = om.schedule(dims, idx.reshape(-1), gate.reshape(-1))
+    dy = torch.randn(L, dims.d, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5)).to(torch.bfloat16)
+    g = om.layer_bwd(dims, inp["x"], inp["subkeys"], inp["W"], inp["V"], Ws, inp["w_gate_up"], inp["w_down"],
+                     idx, gate, plan, dy)
+    torch.cuda.synchronize()
+    hr = lambda n, r=None: host_rows(dims, w.seed, n, r)
+    x, W, V = hr("x", np.arange(L)), hr("W"), hr("V")
+    ids = idx.cpu().numpy().reshape(L, -1)
+    gt = gate.cpu().double().numpy().reshape(L, -1)
+    dyn = dy.double().cpu().numpy()
+    rb = oracle.routed_bwd(x, W, V, ids, gt, dyn)
+    rdx, rdsub = oracle.router_bwd(x, hr("subkeys").reshape(1, -1, dims.d), dims.n_rows, dims.n_cols,
+                                   idx.cpu().numpy(), gate.cpu().double().numpy(), rb["dgate"].reshape(L, 1, -1))
+    mdx, mdgu, mddn = oracle.mlp_bwd(x, hr("w_gate_up"), hr("w_down"), dyn)
+    act = g["active"].cpu().numpy()
+    checks = [(g["dx"], rb["dx"] + rdx + mdx), (g["dsubkeys"].reshape(-1, dims.d), rdsub.reshape(-1, dims.d)),
+              (g["dW_act"], rb["dW"][act]), (g["dV_act"], rb["dV"][act]), (g["dw_gate_up"], mdgu),
+              (g["dw_down"], mddn)]
+    for got, want in checks:
+        got = got.cpu().numpy()
+        keep = np.abs(want).sum(1) > 0
+        e = rel_errors(got[keep], want[keep])
+        assert e[0] <= 1e-2 and e[1] <= 1e-2, e
