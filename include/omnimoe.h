@@ -341,6 +341,22 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
                                  int32_t* idx_out, float* gate_out, void* ws, size_t ws_bytes,
                                  omnimoe_stream_t stream);
 
+/* omnimoe_layer_fwd for activations in (pinned) HOST memory, with the transfers
+ * overlapped: x is copied to the caller's device buffer x_dev in `chunks` token
+ * chunks on copy_stream while the chunks already copied are routed on stream (the
+ * router is per token and batch-independent: the routing is bit-identical); the
+ * schedule and routed branch run on the whole batch; the shared MLP's second GEMM
+ * (+ combine) runs chunk by chunk and each chunk of y (device buffer y_dev) is copied
+ * to y_host on copy_stream while the next is computed.  The call is complete on
+ * `stream` once y_host holds the result.  Chunks are whole multiples of 128 tokens.
+ *   x_host, y_host [L][d] host (pinned for overlap); x_dev, y_dev [L][d] device;
+ *   copy_stream: a second stream of the caller's; ws as omnimoe_layer_fwd. */
+omnimoe_status omnimoe_layer_fwd_host(const omnimoe_dims* dims, int64_t L, const void* x_host, void* x_dev,
+                                      const void* subkeys, const void* W, const void* V,
+                                      const void* w_gate_up, const void* w_down, void* y_dev, void* y_host,
+                                      int chunks, void* ws, size_t ws_bytes, omnimoe_stream_t stream,
+                                      omnimoe_stream_t copy_stream);
+
 /* The sub-key logits of the route call, for measurement and parity:
  * logits float [L][h][n_rows+n_cols].  method 0: the route path (dims.router);
  * 1: exact fp64 double-double kernel; 2: bf16 tcgen05 GEMM with fp32

@@ -3,6 +3,7 @@
 // synchronisation, no CPU fallback.
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "backward.cuh"
 #include "ep.cuh"
@@ -656,6 +657,118 @@ int32_t omnimoe_layer_executor(const omnimoe_dims* dims, int64_t L) {
   if (layer_uses_token_executor(*dims, L)) return OMNIMOE_EXPERT_TOKEN;
   if (dims->v_layout == OMNIMOE_V_SLICED) return OMNIMOE_EXPERT_SLICED;
   return resolve_group_size(*dims) > 1 ? OMNIMOE_EXPERT_GROUP : OMNIMOE_EXPERT_WARP;
+}
+
+omnimoe_status omnimoe_layer_fwd_host(const omnimoe_dims* dims, int64_t L, const void* x_host, void* x_dev,
+                                      const void* subkeys, const void* W, const void* V, const void* w_gate_up,
+                                      const void* w_down, void* y_dev, void* y_host, int chunks, void* ws,
+                                      size_t ws_bytes, omnimoe_stream_t stream, omnimoe_stream_t copy_stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  const omnimoe_dims& d = *dims;
+  if (L < 0 || L * d.n_heads * d.top_k >= (int64_t(1) << 31) - 1) {
+    set_error("L*h*K must be < 2^31-1");
+    return OMNIMOE_ERR_SHAPE;
+  }
+  if (L == 0) return OMNIMOE_OK;
+  const void* req[] = {x_host, x_dev, subkeys, W, V, y_dev, y_host, ws, copy_stream};
+  for (const void* p : req)
+    if (!p) {
+      set_error("layer_fwd_host: a required pointer / stream is null");
+      return OMNIMOE_ERR_INVALID_ARGUMENT;
+    }
+  if (d.d_ff > 0) {
+    OMNI_NONNULL(w_gate_up, "w_gate_up");
+    OMNI_NONNULL(w_down, "w_down");
+  }
+  if (chunks < 1 || chunks > 64) {
+    set_error("layer_fwd_host: chunks must be in [1, 64]");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  OMNI_TRY(check_ws(ws_bytes, layer_ws(d, L, nullptr, nullptr), "layer_fwd_host"));
+  OMNI_TRY(check_device());
+  cudaStream_t st = (cudaStream_t)stream, cs = (cudaStream_t)copy_stream;
+  // per-thread event pool (host resources; no device memory)
+  thread_local std::vector<cudaEvent_t> evs;
+  const size_t need = 2 * (size_t)chunks + 1;
+  while (evs.size() < need) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      set_error("layer_fwd_host: cannot create events");
+      return OMNIMOE_ERR_CUDA;
+    }
+    evs.push_back(e);
+  }
+  LayerWs w;
+  layer_ws(d, L, ws, &w);
+  const size_t eb = elem_size(d);
+  const int64_t hk = d.n_heads * d.top_k, M = L * hk;
+  const int64_t Lc = (((L + chunks - 1) / chunks) + 127) / 128 * 128;  // whole 128-row GEMM tiles
+  int n_ch = 0;
+  // 1. copy x chunk by chunk (copy stream) while routing the chunks already copied:
+  //    routing is per token and batch-independent, so chunked routing is bit-identical
+  for (int64_t l0 = 0; l0 < L; l0 += Lc, ++n_ch) {
+    const int64_t n = std::min(Lc, L - l0);
+    if (cudaMemcpyAsync(static_cast<char*>(x_dev) + l0 * d.d * eb, static_cast<const char*>(x_host) + l0 * d.d * eb,
+                        n * d.d * eb, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+        cudaEventRecord(evs[n_ch], cs) != cudaSuccess || cudaStreamWaitEvent(st, evs[n_ch], 0) != cudaSuccess) {
+      set_error("layer_fwd_host: host-to-device copy failed");
+      return OMNIMOE_ERR_CUDA;
+    }
+    OMNI_TRY(route_impl(d, n, static_cast<const char*>(x_dev) + l0 * d.d * eb, subkeys, w.idx + l0 * hk,
+                        w.gate + l0 * hk, nullptr, w.route_ws, st, /*sorted=*/0));
+  }
+  // 2. the routed branch over the whole batch (Expert-Centric Scheduling needs every task)
+  w.plan.n_tokens = L;
+  if (layer_uses_token_executor(d, L)) {
+    OMNI_TRY(expert_token_run(d, L, x_dev, W, V, w.idx, w.gate, 0, d.n_rows * d.n_cols, w.y_routed, 0, st));
+  } else {
+    OMNI_TRY(schedule_run(M, w.idx, w.gate, nullptr, hk, w.plan, resolve_group_size(d), resolve_token_blocks(d, L),
+                          resolve_v_bands(d, d.n_rows * d.n_cols), w.sched_ws, st));
+    OMNI_TRY(expert_run(d, L, x_dev, W, V, w.plan, w.y_routed, 0, w.expert_ws, st));
+  }
+  // 3. shared MLP: GEMM-1 whole, GEMM-2 (+ combine) chunk by chunk, each chunk of y copied
+  //    back on the copy stream while the next is computed
+  if (d.d_ff > 0) {
+    GemmArgs g1;
+    g1.M = (int)L;
+    g1.N = (int)d.d_ff;
+    g1.K = (int)d.d;
+    g1.out = w.H;
+    if (d.dtype == OMNIMOE_BF16) OMNI_TRY(gemm_bf16(EPI_SWIGLU, x_dev, w_gate_up, g1, st));
+    else OMNI_TRY(gemm_f32(EPI_SWIGLU, static_cast<const float*>(x_dev), static_cast<const float*>(w_gate_up), g1, st));
+  }
+  int c = 0;
+  for (int64_t l0 = 0; l0 < L; l0 += Lc, ++c) {
+    const int64_t n = std::min(Lc, L - l0);
+    void* yc = static_cast<char*>(y_dev) + l0 * d.d * eb;
+    if (d.d_ff > 0) {
+      GemmArgs g2;
+      g2.M = (int)n;
+      g2.N = (int)d.d;
+      g2.K = (int)d.d_ff;
+      g2.out = yc;
+      g2.addend = w.y_routed + l0 * d.d;
+      const void* Hc = static_cast<const char*>(w.H) + l0 * d.d_ff * eb;
+      if (d.dtype == OMNIMOE_BF16) OMNI_TRY(gemm_bf16(EPI_ADD, Hc, w_down, g2, st));
+      else OMNI_TRY(gemm_f32(EPI_ADD, static_cast<const float*>(Hc), static_cast<const float*>(w_down), g2, st));
+    } else {
+      cast_out_kernel<<<kSMs * 4, 256, 0, st>>>(w.y_routed + l0 * d.d, yc, n * d.d, d.dtype == OMNIMOE_BF16);
+      OMNI_CHECK_LAUNCH("cast_out_kernel");
+    }
+    if (cudaEventRecord(evs[n_ch + c], st) != cudaSuccess || cudaStreamWaitEvent(cs, evs[n_ch + c], 0) != cudaSuccess ||
+        cudaMemcpyAsync(static_cast<char*>(y_host) + l0 * d.d * eb, yc, n * d.d * eb, cudaMemcpyDeviceToHost, cs) !=
+            cudaSuccess) {
+      set_error("layer_fwd_host: device-to-host copy failed");
+      return OMNIMOE_ERR_CUDA;
+    }
+  }
+  // the call completes on `stream` once y is on the host
+  if (cudaEventRecord(evs[2 * chunks], cs) != cudaSuccess || cudaStreamWaitEvent(st, evs[2 * chunks], 0) != cudaSuccess) {
+    set_error("layer_fwd_host: event failed");
+    return OMNIMOE_ERR_CUDA;
+  }
+  return OMNIMOE_OK;
 }
 
 omnimoe_status omnimoe_router_logits(const omnimoe_dims* dims, int64_t L, const void* x, const void* subkeys,

@@ -55,7 +55,7 @@ EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnim
            "omnimoe_ep_pack", "omnimoe_ep_unpack", "omnimoe_ep_combine", "omnimoe_pack_v",
            "omnimoe_v_bands", "omnimoe_expert_fwd_pass", "omnimoe_load_stats",
            "omnimoe_load_stats_workspace_size", "omnimoe_expert_fwd_tokens", "omnimoe_layer_executor",
-           "omnimoe_expert_bwd", "omnimoe_router_bwd", "omnimoe_shared_mlp_bwd"]
+           "omnimoe_expert_bwd", "omnimoe_router_bwd", "omnimoe_shared_mlp_bwd", "omnimoe_layer_fwd_host"]
 
 _lib = None
 
@@ -89,6 +89,7 @@ def load(path: str = LIB_PATH):
         "omnimoe_expert_fwd_tokens": [PD, I64, V, V, V, V, V, V, I32, V],
         "omnimoe_expert_bwd": [PD, I64, V, V, V, V, PP, V, V, V, V, V, I32, V, SZ, V],
         "omnimoe_router_bwd": [PD, I64, V, V, V, V, V, V, I32, V, V, SZ, V],
+        "omnimoe_layer_fwd_host": [PD, I64, V, V, V, V, V, V, V, V, V, I32, V, SZ, V, V],
         "omnimoe_shared_mlp_bwd": [PD, I64, V, V, V, V, V, I32, V, V, V, SZ, V],
     }
     for name, args in sig.items():
@@ -468,6 +469,27 @@ def layer_fwd(dims: LayerDims, x, subkeys, W, V, w_gate_up=None, w_down=None, y=
                                     _ptr(w_gate_up), _ptr(w_down), _ptr(y), _ptr(idx), _ptr(gate),
                                     _ptr(ws), ws.numel(), _stream()), "layer_fwd")
     return (y, idx, gate) if return_routing else y
+
+
+def layer_fwd_host(dims: LayerDims, x_host, subkeys, W, V, w_gate_up=None, w_down=None, y_host=None, x_dev=None,
+                   y_dev=None, ws=None, chunks=4, copy_stream=None):
+    """omnimoe_layer_fwd_host: x and y in (pinned) host memory, transfers overlapped with the
+    router and the shared MLP.  Returns y_host; complete on the current stream."""
+    L = x_host.shape[0]
+    if x_host.is_cuda:
+        raise OmniMoEError("x_host must be a host tensor")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    x_dev = x_dev if x_dev is not None else torch.empty((L, dims.d), dtype=dims.torch_dtype, device=dev)
+    y_dev = y_dev if y_dev is not None else torch.empty((L, dims.d), dtype=dims.torch_dtype, device=dev)
+    y_host = y_host if y_host is not None else torch.empty((L, dims.d), dtype=dims.torch_dtype).pin_memory()
+    copy_stream = copy_stream or torch.cuda.Stream()
+    ws = ws if ws is not None else workspace(dims, L, WS_LAYER, dev)
+    dc = dims.c()
+    _check(load().omnimoe_layer_fwd_host(ctypes.byref(dc), L, ctypes.c_void_p(x_host.data_ptr()), _ptr(x_dev),
+                                         _ptr(subkeys), _ptr(W), _ptr(V), _ptr(w_gate_up), _ptr(w_down), _ptr(y_dev),
+                                         ctypes.c_void_p(y_host.data_ptr()), int(chunks), _ptr(ws), ws.numel(),
+                                         _stream(), ctypes.c_void_p(copy_stream.cuda_stream)), "layer_fwd_host")
+    return y_host
 
 
 def router_logits(dims: LayerDims, x, subkeys, method=LOGITS_ROUTE, ws=None):

@@ -711,3 +711,18 @@ def test_layer_bwd_composition():
         keep = np.abs(want).sum(1) > 0
         e = rel_errors(got[keep], want[keep])
         assert e[0] <= 1e-2 and e[1] <= 1e-2, e
+
+
+@pytest.mark.parametrize("name,L,chunks,vl", [("C1", 256, 1, om.V_SLICED), ("C1", 300, 3, om.V_SLICED),
+                                              ("C3a", 1000, 4, om.V_SLICED), ("C3b", 777, 4, om.V_ROWS)])
+def test_layer_fwd_host_equals_device_call(name, L, chunks, vl):
+    """The host-buffer call (chunked, transfers overlapped) gives the device call's bits."""
+    w = _dims(name, v_layout=vl)
+    dims = w.dims
+    inp = make_inputs(dims, L, w.seed)
+    V = om.pack_v(dims, inp["V"]) if vl == om.V_SLICED else inp["V"]
+    y = om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], V, inp["w_gate_up"], inp["w_down"])
+    xh = inp["x"].cpu().pin_memory()
+    yh = om.layer_fwd_host(dims, xh, inp["subkeys"], inp["W"], V, inp["w_gate_up"], inp["w_down"], chunks=chunks)
+    torch.cuda.synchronize()
+    assert torch.equal(yh.view(torch.int16), y.cpu().view(torch.int16))
