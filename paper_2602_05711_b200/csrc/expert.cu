@@ -1233,16 +1233,33 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int i = 0; i < 4; ++i) aw[j][i] = av[j][i] = 0ull;
     }
-    for (int p = beg; p < end; ++p) {
+    // the next task's x and dy parts (and gate, task index) are loaded one task ahead
+    uint4 nxh[NVH], ndh[NVH];
+    float ng = 0.f;
+    int nt = 0;
+    auto fetch = [&](int p) {
+      if (p >= end) return;
       const int l = stok[p];
-      const float g = sgate[p];
-      uint4 xh[NVH], dh[NVH];
+      ng = sgate[p];
+      nt = stask[p];
 #pragma unroll
       for (int j = 0; j < NVH; ++j) {
         const int c = (j * 32 + lane) * 8;
-        xh[j] = c < half ? ld_vec(x + (size_t)l * d + c0 + c) : make_uint4(0, 0, 0, 0);
-        dh[j] = c < half ? ld_vec(dy + (size_t)l * d + c0 + c) : make_uint4(0, 0, 0, 0);
+        nxh[j] = c < half ? ld_vec(x + (size_t)l * d + c0 + c) : make_uint4(0, 0, 0, 0);
+        ndh[j] = c < half ? ld_vec(dy + (size_t)l * d + c0 + c) : make_uint4(0, 0, 0, 0);
       }
+    };
+    fetch(beg);
+    for (int p = beg; p < end; ++p) {
+      const float g = ng;
+      const int tcur = nt;
+      uint4 xh[NVH], dh[NVH];
+#pragma unroll
+      for (int j = 0; j < NVH; ++j) {
+        xh[j] = nxh[j];
+        dh[j] = ndh[j];
+      }
+      fetch(p + 1);
       float zp = 0.f, qp = 0.f;
 #pragma unroll
       for (int j = 0; j < NVH; ++j) {
@@ -1277,7 +1294,7 @@ __global__ void __launch_bounds__(256)
       const float sp = act == OMNIMOE_IDENTITY ? 1.0f : lg * (1.0f + z * (1.0f - lg));
       const float a = g * sz, dz = g * q * sp;
       if (h == 0 && lane == 0) {
-        const int t = stask[p];
+        const int t = tcur;
         dgate[t] = sz * q;
         task_pair[2 * (size_t)t + 1] = __float_as_int(dz);
       }
