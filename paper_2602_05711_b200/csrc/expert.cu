@@ -1104,10 +1104,11 @@ __global__ void __launch_bounds__(256)
                        const int32_t* __restrict__ offsets, const int32_t* __restrict__ active,
                        const int32_t* __restrict__ n_active, const int32_t* __restrict__ stok,
                        const float* __restrict__ sgate, const int32_t* __restrict__ stask,
-                       int32_t* __restrict__ task_pair, int act, int* __restrict__ work, int w_hint) {
+                       int32_t* __restrict__ task_pair, int act, int* __restrict__ work, int w_hint, int x_hint) {
   const int lane = threadIdx.x & 31;
   const int na = *n_active;
   const uint64_t pol = w_hint ? policy_evict_first() : policy_evict_normal();
+  const uint64_t xpol = x_hint ? policy_evict_last() : policy_evict_normal();
   int tau = 0;
   if (lane == 0) tau = atomicAdd(work, 1);
   tau = __shfl_sync(0xffffffffu, tau, 0);
@@ -1137,8 +1138,8 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
           const int c = (j * 32 + lane) * 8;
-          a[j] = c < d ? ld_vec(x + (size_t)l0 * d + c) : make_uint4(0, 0, 0, 0);
-          b[j] = c < d ? ld_vec(x + (size_t)l1 * d + c) : make_uint4(0, 0, 0, 0);
+          a[j] = c < d ? ld_vec_hint(x + (size_t)l0 * d + c, xpol) : make_uint4(0, 0, 0, 0);
+          b[j] = c < d ? ld_vec_hint(x + (size_t)l1 * d + c, xpol) : make_uint4(0, 0, 0, 0);
         }
         float z0 = 0.f, z1 = 0.f;
 #pragma unroll
@@ -1176,7 +1177,7 @@ omnimoe_status launch_zdot(int d, const void* x, const void* W, const omnimoe_pl
   expert_zdot_kernel<NV><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(
       d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W), plan.expert_offsets,
       plan.active, plan.n_active, plan.sorted_token, plan.sorted_gate, plan.sorted_task, plan.task_pair, act, work,
-      env_int("OMNIMOE_W_HINT", 1));
+      env_int("OMNIMOE_W_HINT", 1), env_int("OMNIMOE_X_HINT", 0));
   OMNI_CHECK_LAUNCH("expert_zdot_kernel");
   return OMNIMOE_OK;
 }
