@@ -1,6 +1,8 @@
 // tcgen05 GEMM engine for sm_100a (router sub-key scoring a1, shared MLP a7/a8).
 //
-// One CTA computes a 128 x 256 fp32 tile of C = A . B^T in TMEM:
+// Persistent: one CTA per SM walks 128 x 256 output tiles (static round-robin); the fp32
+// tile accumulates in one of two 256-column TMEM buffers so that the epilogue of tile i
+// overlaps the MMAs of tile i+1 (tfull / tempty mbarriers between the roles):
 //   warp 0 (one lane)  TMA producer: 2-D cp.async.bulk.tensor loads of A (128x64)
 //                      and B (2 x 128x64) bf16 boxes, 128B swizzle, into a
 //                      kStages-deep SMEM ring guarded by full/empty mbarriers;
@@ -39,13 +41,15 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sB = smem + kStages * kABytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = empty + kStages;   // [2]: MMA -> epilogue
+  uint64_t* tempty = tfull + 2;        // [2]: epilogue -> MMA (4 warp arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM;
-  const int nt = blockIdx.x;
   const int num_kb = (args.K + BK - 1) / BK;
+  const int ncols = (EPI == EPI_SWIGLU) ? BN / 2 : BN;
+  const int n_nt = (args.N + ncols - 1) / ncols;
+  const int n_tiles = n_nt * ((args.M + BM - 1) / BM);
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -54,13 +58,16 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -69,10 +76,13 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer ----------------
-    for (int kb = 0; kb < num_kb; ++kb) {
-      const int s = kb % kStages;
-      const uint32_t ph = (kb / kStages) & 1;
+    // ---------------- TMA producer (one K-block ring across all tiles) ----------------
+    int g = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x)
+    for (int kb = 0; kb < num_kb; ++kb, ++g) {
+      const int m0 = (t / n_nt) * BM, nt = t % n_nt;
+      const int s = g % kStages;
+      const uint32_t ph = (g / kStages) & 1;
       mbar_wait(&empty[s], ph ^ 1);
       mbar_expect_tx(&full[s], kStageBytes);
       tma_load_2d(&tmA, &full[s], sA + s * kABytes, kb * BK, m0);
@@ -86,25 +96,36 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread) ----------------
-    for (int kb = 0; kb < num_kb; ++kb) {
-      const int s = kb % kStages;
-      const uint32_t ph = (kb / kStages) & 1;
-      mbar_wait(&full[s], ph);
+    int g = 0, it = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      const int b = it & 1;
+      mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);  // the epilogue has drained this buffer
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a0 = smem_u32(sA + s * kABytes), b0 = smem_u32(sB + s * kBBytes);
+      const uint32_t acc = tmem + (uint32_t)(b * BN);
+      for (int kb = 0; kb < num_kb; ++kb, ++g) {
+        const int s = g % kStages;
+        const uint32_t ph = (g / kStages) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a0 = smem_u32(sA + s * kABytes), b0 = smem_u32(sB + s * kBBytes);
 #pragma unroll
-      for (int k = 0; k < BK / 16; ++k)
-        umma_f16(tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), kIdesc, (kb | k) != 0);
-      umma_commit(&empty[s]);
+        for (int k = 0; k < BK / 16; ++k)
+          umma_f16(acc, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), kIdesc, (kb | k) != 0);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(&tfull[b]);
     }
-    umma_commit(tfull);
   } else if (warp >= 4) {
     // ---------------- epilogue (TMEM -> registers -> global) ----------------
-    mbar_wait(tfull, 0);
+    int it = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+    const int m0 = (t / n_nt) * BM, nt = t % n_nt;
+    const int b = it & 1;
+    mbar_wait(&tfull[b], (it >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int q = warp - 4;  // TMEM lane quarter == warp id % 4
     const int row = m0 + q * 32 + lane;
-    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN);
     const bool row_ok = row < args.M;
     if (EPI == EPI_SWIGLU) {
       __nv_bfloat16* H = reinterpret_cast<__nv_bfloat16*>(args.out);
@@ -182,12 +203,17 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
+    // this warp's TMEM lanes of buffer b are read: release it to the MMA issuer
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 2) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
   }
 }
 
@@ -220,8 +246,8 @@ omnimoe_status launch_tc(const void* A, const void* B, const GemmArgs& a, cudaSt
     return OMNIMOE_ERR_INVALID_ARGUMENT;
   }
   const int ncols = (EPI == EPI_SWIGLU) ? BN / 2 : BN;
-  dim3 grid((a.N + ncols - 1) / ncols, (a.M + BM - 1) / BM);
-  gemm_tc_kernel<EPI><<<grid, 256, kSmemBytes, st>>>(mA, mB, mB2, a);
+  const int64_t tiles = (int64_t)((a.N + ncols - 1) / ncols) * ((a.M + BM - 1) / BM);
+  gemm_tc_kernel<EPI><<<(int)std::min<int64_t>(tiles, kSMs), 256, kSmemBytes, st>>>(mA, mB, mB2, a);
   OMNI_CHECK_LAUNCH("gemm_tc_kernel");
   return OMNIMOE_OK;
 }
