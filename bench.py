@@ -271,6 +271,8 @@ def bench_single(args, w, lr):
     stages = {"route_a1_a3": [], "schedule_a4_a5": [], "expert_a6": [], "shared_mlp_a7_a8": []}
     sliced = dims.v_layout == om.V_SLICED
     token = om.layer_executor(dims, L) == om.EXPERT_TOKEN  # low eta: the layer skips ECS
+    dense = om.layer_executor(dims, L) == om.EXPERT_DENSE  # high eta: two GEMMs
+    dws = om.workspace(dims, L, om.WS_LAYER) if dense else None  # (covers the dense scratch)
     passes = {"a6_pass_z": [], "a6_pass_v": []}
     for i in range(max(4, args.steps)):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
@@ -285,6 +287,8 @@ def bench_single(args, w, lr):
         e[3].record(st)
         if token:
             om.expert_fwd_tokens(dims, inp["x"], inp["W"], inp["V"], idx, gate, y_routed=yr, accumulate=True)
+        elif dense:
+            om.expert_fwd_dense(dims, inp["x"], inp["W"], inp["V"], idx, gate, y_routed=yr, ws=dws)
         elif sliced:  # the two passes of the SLICED executor, timed apart
             om.expert_fwd(dims, inp["x"], inp["W"], inp["V"], plan, y_routed=yr, accumulate=True, ws=ews, passes=1)
             e[6].record(st)
@@ -304,7 +308,7 @@ def bench_single(args, w, lr):
             passes["a6_pass_z"].append(e[3].elapsed_time(e[6]))
             passes["a6_pass_v"].append(e[6].elapsed_time(e[4]))
     stage_ms = {k: statistics.median(v) for k, v in stages.items()}
-    if token:  # the plan was built for the load metrics only; the layer does not schedule
+    if token or dense:  # the plan was built for the load metrics only; the layer does not schedule
         stage_ms["schedule_a4_a5"] = 0.0
     usage, uneven = om.load_stats(plan).cpu().tolist()  # Expert Usage / Unevenness
     if sliced:
@@ -364,11 +368,20 @@ def bench_single(args, w, lr):
         a6_bytes, l2_bytes, a6_ms = cand[kern]
     else:
         kern = "expert_token_kernel" if token else ("expert_group_tma_kernel" if B > 1 else "expert_warp_kernel")
+        if dense:
+            kern = "gemm_tc_kernel (dense routed branch)"
         a6_bytes, a6_ms = a6_algorithmic_bytes(dims, L, n_active, M), stage_ms["expert_a6"]
         l2_bytes = 2 * M * dims.d * 2
     a6_gbs = a6_bytes / (a6_ms / 1000.0) / 1e9
     traffic, tsrc = ncu_traffic(w.name, kern)
-    roofline = {"bound": "hbm", "achieved": a6_gbs, "peak": pk["hbm"], "unit": "GB/s", "frac": a6_gbs / pk["hbm"],
+    if dense:  # two dense GEMMs: the tensor roofline (L x N x d MACs each)
+        tf = 2 * 2.0 * L * dims.N * dims.d / (a6_ms / 1000.0) / 1e12
+        roofline = {"bound": "tensor", "achieved": tf, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
+                    "frac": tf / pk["bf16_sus"], "traffic": None, "kernel": "gemm_tc_kernel x2 (dense routed branch)",
+                    "avg_launch_ms": a6_ms, "peak_source": pk["src"] + " bf16 sustained",
+                    "note": f"eta = {eta:.0f}: Z = x W^T and y = A V on tcgen05 (DESIGN.md §4.4)"}
+    if not dense:
+      roofline = {"bound": "hbm", "achieved": a6_gbs, "peak": pk["hbm"], "unit": "GB/s", "frac": a6_gbs / pk["hbm"],
                 "traffic": traffic, "kernel": f"{kern} (a6)", "algorithmic_bytes_per_launch": a6_bytes,
                 "avg_launch_ms": a6_ms, "peak_source": pk["src"] + " hbm_gbs (copy)",
                 "traffic_source": tsrc,
@@ -396,6 +409,7 @@ def bench_single(args, w, lr):
         "config": dict(_config_dict(w, "single-gpu"), group_size=B, expert_kernel=args.expert_kernel,
                        v_layout="sliced" if dims.v_layout == om.V_SLICED else "rows",
                        executor={om.EXPERT_TOKEN: "token-centric (eta < 2: no expert reuse; ECS skipped)",
+                                 om.EXPERT_DENSE: "dense tcgen05 GEMMs (eta >= 64; ECS skipped)",
                                  om.EXPERT_SLICED: "SLICED (ECS pass Z + slice-major pass V)",
                                  om.EXPERT_GROUP: "grouped ECS (rows)",
                                  om.EXPERT_WARP: "expert-major ECS (rows)"}[om.layer_executor(dims, L)],

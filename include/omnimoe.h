@@ -53,7 +53,7 @@ enum { OMNIMOE_SILU = 0, OMNIMOE_IDENTITY = 1 };
  * Scheduling" (Fig. 4a): omnimoe_layer_fwd skips the schedule and each
  * token gathers its own experts' rows (omnimoe_expert_fwd does not accept it). */
 enum { OMNIMOE_EXPERT_AUTO = 0, OMNIMOE_EXPERT_WARP = 1, OMNIMOE_EXPERT_GROUP = 2, OMNIMOE_EXPERT_TOKEN = 3,
-       OMNIMOE_EXPERT_SLICED = 4 };
+       OMNIMOE_EXPERT_SLICED = 4, OMNIMOE_EXPERT_DENSE = 5 /* reported by omnimoe_layer_executor only */ };
 /* Memory layout of the value table V (the down-projection rows v_n of Eq.WV,
  * PAPER:172-176).  ROWS: [N][d], one row per expert.  SLICED: [d/32][N][32], i.e.
  * the table cut into d/32 column slices of 32 elements, each slice stored
@@ -318,11 +318,23 @@ omnimoe_status omnimoe_expert_fwd_tokens(const omnimoe_dims* dims, int64_t L, co
                                          const void* V, const int32_t* idx, const float* gate,
                                          float* y_routed, int accumulate, omnimoe_stream_t stream);
 
+/* The routed branch as two dense tcgen05 GEMMs (the executor omnimoe_layer_fwd picks
+ * at eta >= 64): Z = x W^T [L][N] fp32; A = gate * sigma(Z) on the selected cells, 0
+ * elsewhere (bf16); y_routed = A V (written, fp32).  idx, gate [L][h*K] global ids;
+ * one head; V in the ROWS layout; ws: omnimoe_dense_workspace_size(). */
+size_t omnimoe_dense_workspace_size(const omnimoe_dims* dims, int64_t L);
+omnimoe_status omnimoe_expert_fwd_dense(const omnimoe_dims* dims, int64_t L, const void* x, const void* W,
+                                        const void* V, const int32_t* idx, const float* gate, float* y_routed,
+                                        void* ws, size_t ws_bytes, omnimoe_stream_t stream);
+
 /* The routed-branch executor omnimoe_layer_fwd runs for dims and L tokens
  * (OMNIMOE_EXPERT_*; -1 on invalid dims).  With expert_kernel AUTO: SLICED for the
  * SLICED layout; for the ROWS layout TOKEN when eta = M / E|E_active| < 2 under
  * uniform routing (then no expert is shared by two tasks and Expert-Centric
- * Scheduling has nothing to reuse -- measured faster), else GROUP. */
+ * Scheduling has nothing to reuse -- measured faster); DENSE when
+ * eta >= 64 with one head (every expert shared by ~100 tokens: the routed branch as
+ * two tcgen05 GEMMs, Z = x W^T, A = gate * sigma(Z) on the selected cells, y = A V);
+ * else GROUP. */
 int32_t omnimoe_layer_executor(const omnimoe_dims* dims, int64_t L);
 
 /* Whole layer forward (Eq.MoE / Eq.Assemble):

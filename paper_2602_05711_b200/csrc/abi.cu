@@ -187,7 +187,7 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
   const size_t sb = schedule_ws_bytes(M, N);
   void* sw = c.take<char>(sb);
   float* yr = c.take<float>((size_t)L * d.d);
-  void* ew = c.take<char>(expert_ws_bytes(d, L));
+  void* ew = c.take<char>(layer_uses_dense_executor(d, L) ? dense_expert_ws_bytes(d, L) : expert_ws_bytes(d, L));
   void* H = c.take<char>((size_t)L * std::max<int64_t>(d.d_ff, 1) * elem_size(d));
   if (o) {
     o->route_ws = rw;
@@ -502,6 +502,8 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
   w.plan.n_tokens = L;
   if (layer_uses_token_executor(d, L)) {  // no expert shared by two tasks (or the "w/o ECS" ablation)
     OMNI_TRY(expert_token_run(d, L, x, W, V, idx, gate, 0, d.n_rows * d.n_cols, w.y_routed, 0, st));
+  } else if (layer_uses_dense_executor(d, L)) {  // every expert shared by ~100 tokens: two GEMMs
+    OMNI_TRY(dense_expert_run(d, L, x, W, V, idx, gate, w.y_routed, w.expert_ws, st));
   } else {
     OMNI_TRY(schedule_run(M, idx, gate, nullptr, d.n_heads * d.top_k, w.plan, resolve_group_size(d),
                           resolve_token_blocks(d, L), resolve_v_bands(d, d.n_rows * d.n_cols), w.sched_ws, st));
@@ -652,9 +654,36 @@ omnimoe_status omnimoe_shared_mlp_bwd(const omnimoe_dims* dims, int64_t L, const
                      (cudaStream_t)stream);
 }
 
+size_t omnimoe_dense_workspace_size(const omnimoe_dims* dims, int64_t L) {
+  if (validate_dims(dims) != OMNIMOE_OK || L < 0) return 0;
+  return dense_expert_ws_bytes(*dims, L);
+}
+
+omnimoe_status omnimoe_expert_fwd_dense(const omnimoe_dims* dims, int64_t L, const void* x, const void* W,
+                                        const void* V, const int32_t* idx, const float* gate, float* y_routed,
+                                        void* ws, size_t ws_bytes, omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  if (dims->dtype != OMNIMOE_BF16 || dims->n_heads != 1 || dims->v_layout != OMNIMOE_V_ROWS) {
+    set_error("expert_fwd_dense: bf16, one head, V in the ROWS layout");
+    return OMNIMOE_ERR_UNSUPPORTED;
+  }
+  if (L <= 0) return L == 0 ? OMNIMOE_OK : OMNIMOE_ERR_INVALID_ARGUMENT;
+  const void* req[] = {x, W, V, idx, gate, y_routed, ws};
+  for (const void* p : req)
+    if (!p) {
+      set_error("expert_fwd_dense: a required pointer is null");
+      return OMNIMOE_ERR_INVALID_ARGUMENT;
+    }
+  OMNI_TRY(check_ws(ws_bytes, dense_expert_ws_bytes(*dims, L), "expert_fwd_dense"));
+  OMNI_TRY(check_device());
+  return dense_expert_run(*dims, L, x, W, V, idx, gate, y_routed, ws, (cudaStream_t)stream);
+}
+
 int32_t omnimoe_layer_executor(const omnimoe_dims* dims, int64_t L) {
   if (validate_dims(dims) != OMNIMOE_OK || L < 0) return -1;
   if (layer_uses_token_executor(*dims, L)) return OMNIMOE_EXPERT_TOKEN;
+  if (layer_uses_dense_executor(*dims, L)) return OMNIMOE_EXPERT_DENSE;
   if (dims->v_layout == OMNIMOE_V_SLICED) return OMNIMOE_EXPERT_SLICED;
   return resolve_group_size(*dims) > 1 ? OMNIMOE_EXPERT_GROUP : OMNIMOE_EXPERT_WARP;
 }
@@ -722,6 +751,8 @@ omnimoe_status omnimoe_layer_fwd_host(const omnimoe_dims* dims, int64_t L, const
   w.plan.n_tokens = L;
   if (layer_uses_token_executor(d, L)) {
     OMNI_TRY(expert_token_run(d, L, x_dev, W, V, w.idx, w.gate, 0, d.n_rows * d.n_cols, w.y_routed, 0, st));
+  } else if (layer_uses_dense_executor(d, L)) {
+    OMNI_TRY(dense_expert_run(d, L, x_dev, W, V, w.idx, w.gate, w.y_routed, w.expert_ws, st));
   } else {
     OMNI_TRY(schedule_run(M, w.idx, w.gate, nullptr, hk, w.plan, resolve_group_size(d), resolve_token_blocks(d, L),
                           resolve_v_bands(d, d.n_rows * d.n_cols), w.sched_ws, st));

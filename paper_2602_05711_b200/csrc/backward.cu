@@ -15,10 +15,10 @@
 #include "gemm.cuh"
 
 namespace omni {
-namespace {
 
 // out[c][r] = in[r][c] for 2-byte elements (out row stride ld >= R, columns r in [R, ld)
 // zero-filled so that the GEMM's K = ld stays a multiple of 8), 32 x 32 tiles in smem
+namespace {
 __global__ void __launch_bounds__(256) transpose16_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out,
                                                           int64_t R, int64_t C, int64_t ld) {
   __shared__ uint16_t tile[32][33];
@@ -38,9 +38,9 @@ __global__ void __launch_bounds__(256) transpose16_kernel(const uint16_t* __rest
   }
 }
 
-int64_t pad8(int64_t n) { return (n + 7) / 8 * 8; }
+}  // namespace
 
-omnimoe_status transpose16(const void* in, void* out, int64_t R, int64_t C, cudaStream_t st, int64_t ld = 0) {
+omnimoe_status transpose16(const void* in, void* out, int64_t R, int64_t C, cudaStream_t st, int64_t ld) {
   if (ld == 0) ld = R;
   if (R == 0 || C == 0) return OMNIMOE_OK;
   const int64_t tiles = ((ld + 31) / 32) * ((C + 31) / 32);
@@ -49,6 +49,9 @@ omnimoe_status transpose16(const void* in, void* out, int64_t R, int64_t C, cuda
   OMNI_CHECK_LAUNCH("transpose16_kernel");
   return OMNIMOE_OK;
 }
+
+
+namespace {
 
 __global__ void add_f32_kernel(float* __restrict__ dst, const float* __restrict__ src, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

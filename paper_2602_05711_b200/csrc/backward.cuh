@@ -5,6 +5,10 @@
 
 namespace omni {
 
+inline int64_t pad8(int64_t n) { return (n + 7) / 8 * 8; }
+// out[c][r] = in[r][c] for 2-byte elements; out row stride ld (0: R), columns [R, ld) zeroed
+omnimoe_status transpose16(const void* in, void* out, int64_t R, int64_t C, cudaStream_t st, int64_t ld = 0);
+
 // N2: router-gate and shared-MLP backward (backward.cu)
 size_t router_bwd_ws_bytes(const omnimoe_dims& d, int64_t L);
 size_t mlp_bwd_ws_bytes(const omnimoe_dims& d, int64_t L);

@@ -25,6 +25,11 @@ double expected_eta(const omnimoe_dims& d, int64_t L);
 // layer_fwd runs the token-centric executor (no schedule): the "w/o ECS" ablation, or
 // AUTO with the ROWS layout when expected_eta < 2 (no reuse for ECS to exploit)
 bool layer_uses_token_executor(const omnimoe_dims& d, int64_t L);
+// dense.cu: the routed branch as two tcgen05 GEMMs when eta is large (AUTO, ROWS, bf16, h = 1)
+bool layer_uses_dense_executor(const omnimoe_dims& d, int64_t L);
+size_t dense_expert_ws_bytes(const omnimoe_dims& d, int64_t L);
+omnimoe_status dense_expert_run(const omnimoe_dims& d, int64_t L, const void* x, const void* W, const void* V,
+                                const int32_t* idx, const float* gate, float* y_routed, void* ws, cudaStream_t st);
 
 // V [n][d] -> [d/32][n][32] (omnimoe_pack_v)
 omnimoe_status pack_v(int64_t n, int d, const void* V, void* Vs, cudaStream_t st);

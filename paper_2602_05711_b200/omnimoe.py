@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_PKG, "libomnimoe.so")
 
 BF16, F32 = 0, 1
 SILU, IDENTITY = 0, 1
-EXPERT_AUTO, EXPERT_WARP, EXPERT_GROUP, EXPERT_TOKEN, EXPERT_SLICED = 0, 1, 2, 3, 4
+EXPERT_AUTO, EXPERT_WARP, EXPERT_GROUP, EXPERT_TOKEN, EXPERT_SLICED, EXPERT_DENSE = 0, 1, 2, 3, 4, 5
 V_ROWS, V_SLICED = 0, 1
 ORDER_KEY, ORDER_CANDIDATE = 0, 1
 ROUTER_EXACT, ROUTER_EXACT_F64, ROUTER_DENSE = 0, 1, 2
@@ -55,7 +55,8 @@ EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnim
            "omnimoe_ep_pack", "omnimoe_ep_unpack", "omnimoe_ep_combine", "omnimoe_pack_v",
            "omnimoe_v_bands", "omnimoe_expert_fwd_pass", "omnimoe_load_stats",
            "omnimoe_load_stats_workspace_size", "omnimoe_expert_fwd_tokens", "omnimoe_layer_executor",
-           "omnimoe_expert_bwd", "omnimoe_router_bwd", "omnimoe_shared_mlp_bwd", "omnimoe_layer_fwd_host"]
+           "omnimoe_expert_bwd", "omnimoe_router_bwd", "omnimoe_shared_mlp_bwd", "omnimoe_layer_fwd_host",
+           "omnimoe_expert_fwd_dense", "omnimoe_dense_workspace_size"]
 
 _lib = None
 
@@ -89,6 +90,7 @@ def load(path: str = LIB_PATH):
         "omnimoe_expert_fwd_tokens": [PD, I64, V, V, V, V, V, V, I32, V],
         "omnimoe_expert_bwd": [PD, I64, V, V, V, V, PP, V, V, V, V, V, I32, V, SZ, V],
         "omnimoe_router_bwd": [PD, I64, V, V, V, V, V, V, I32, V, V, SZ, V],
+        "omnimoe_expert_fwd_dense": [PD, I64, V, V, V, V, V, V, V, SZ, V],
         "omnimoe_layer_fwd_host": [PD, I64, V, V, V, V, V, V, V, V, V, I32, V, SZ, V, V],
         "omnimoe_shared_mlp_bwd": [PD, I64, V, V, V, V, V, I32, V, V, V, SZ, V],
     }
@@ -99,6 +101,8 @@ def load(path: str = LIB_PATH):
     lib.omnimoe_last_launch_count.restype = ctypes.c_int
     lib.omnimoe_group_size.argtypes = [PD]
     lib.omnimoe_group_size.restype = ctypes.c_int64
+    lib.omnimoe_dense_workspace_size.argtypes = [PD, ctypes.c_int64]
+    lib.omnimoe_dense_workspace_size.restype = ctypes.c_size_t
     lib.omnimoe_layer_executor.argtypes = [PD, ctypes.c_int64]
     lib.omnimoe_layer_executor.restype = ctypes.c_int32
     lib.omnimoe_load_stats_workspace_size.restype = ctypes.c_size_t
@@ -372,6 +376,22 @@ def layer_bwd(dims: LayerDims, x, subkeys, W, V, W_sliced, w_gate_up, w_down, id
 def _replace(d, **kw):
     import dataclasses
     return dataclasses.replace(d, **kw)
+
+
+def expert_fwd_dense(dims: LayerDims, x, W, V, idx, gate, y_routed=None, ws=None):
+    """The routed branch as two dense tcgen05 GEMMs (omnimoe_expert_fwd_dense)."""
+    L = x.shape[0]
+    lib = load()
+    dc = dims.c()
+    if y_routed is None:
+        y_routed = torch.empty((L, dims.d), dtype=torch.float32, device=x.device)
+    if ws is None:
+        ws = torch.empty(max(lib.omnimoe_dense_workspace_size(ctypes.byref(dc), L), 1), dtype=torch.uint8,
+                         device=x.device)
+    _check(lib.omnimoe_expert_fwd_dense(ctypes.byref(dc), L, _ptr(x), _ptr(W), _ptr(V), _ptr(idx.contiguous()),
+                                        _ptr(gate.contiguous()), _ptr(y_routed), _ptr(ws), ws.numel(), _stream()),
+           "expert_fwd_dense")
+    return y_routed
 
 
 def layer_executor(dims: LayerDims, L: int) -> int:

@@ -726,3 +726,34 @@ def test_layer_fwd_host_equals_device_call(name, L, chunks, vl):
     yh = om.layer_fwd_host(dims, xh, inp["subkeys"], inp["W"], V, inp["w_gate_up"], inp["w_down"], chunks=chunks)
     torch.cuda.synchronize()
     assert torch.equal(yh.view(torch.int16), y.cpu().view(torch.int16))
+
+
+def test_layer_high_eta_uses_dense_executor():
+    """AUTO + ROWS at eta >= 64 (one head) runs the routed branch as two tcgen05 GEMMs;
+    results against the oracle on the GPU's routing decision, and the same layer with
+    the grouped executor."""
+    dims = om.LayerDims(d=256, n_rows=32, n_cols=32, top_k=256, d_ff=256)
+    L = 1024
+    assert om.layer_executor(dims, L) == om.EXPERT_DENSE
+    inp = make_inputs(dims, L, 23)
+    y, idx, gate = om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], inp["V"], inp["w_gate_up"],
+                                inp["w_down"], return_routing=True)
+    g = om.LayerDims(d=256, n_rows=32, n_cols=32, top_k=256, d_ff=256, expert_kernel=om.EXPERT_GROUP, group_size=64)
+    y_g = om.layer_fwd(g, inp["x"], inp["subkeys"], inp["W"], inp["V"], inp["w_gate_up"], inp["w_down"])
+    torch.cuda.synchronize()
+    hr = lambda n, r=None: host_rows(dims, 23, n, r)
+    x = hr("x", np.arange(L))
+    ref = oracle.routed_token_centric(x, hr("W"), hr("V"), idx.cpu().numpy().reshape(L, -1),
+                                      gate.cpu().double().numpy().reshape(L, -1))
+    ref += oracle.shared_mlp(x, hr("w_gate_up"), hr("w_down"))
+    # the routed branch alone (fp32) against the oracle: the executor's own error
+    yr = om.expert_fwd_dense(dims, inp["x"], inp["W"], inp["V"], idx.reshape(L, -1), gate.reshape(L, -1))
+    torch.cuda.synchronize()
+    routed = oracle.routed_token_centric(x, hr("W"), hr("V"), idx.cpu().numpy().reshape(L, -1),
+                                         gate.cpu().double().numpy().reshape(L, -1))
+    e = rel_errors(yr.cpu().numpy(), routed)
+    assert e[0] <= 1e-2 and e[1] <= 1e-2, e
+    # the layers (bf16 outputs): dense vs grouped executor, and against the oracle per token
+    e = rel_errors(y.float().cpu().numpy(), y_g.float().cpu().numpy())
+    assert e[0] <= 1e-2 and e[1] <= 1e-2, e
+    assert rel_errors(y.float().cpu().numpy(), ref)[0] <= 1e-2
