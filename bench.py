@@ -409,7 +409,7 @@ def bench_single(args, w, lr):
         "config": dict(_config_dict(w, "single-gpu"), group_size=B, expert_kernel=args.expert_kernel,
                        v_layout="sliced" if dims.v_layout == om.V_SLICED else "rows",
                        executor={om.EXPERT_TOKEN: "token-centric (eta < 2: no expert reuse; ECS skipped)",
-                                 om.EXPERT_DENSE: "dense tcgen05 GEMMs (eta >= 64; ECS skipped)",
+                                 om.EXPERT_DENSE: "dense tcgen05 GEMMs (K >= N/40; ECS skipped)",
                                  om.EXPERT_SLICED: "SLICED (ECS pass Z + slice-major pass V)",
                                  om.EXPERT_GROUP: "grouped ECS (rows)",
                                  om.EXPERT_WARP: "expert-major ECS (rows)"}[om.layer_executor(dims, L)],
@@ -563,8 +563,11 @@ def main():
     from paper_2602_05711_b200 import omnimoe as om
     w = configs.get(args.config)
     eta = expected_eta(w.dims, w.L)
+    # auto: the V layout whose executor the measurements favour -- rows for
+    # the token-centric (eta < 2) and dense (K >= N/40) executors, SLICED for 2 <= eta <= 32
+    dense_rows = om.layer_executor(w.dims, w.L) == om.EXPERT_DENSE
     sliced = args.expert_kernel == "auto" and (args.v_layout == "sliced" or
-                                               (args.v_layout == "auto" and 2.0 <= eta <= 32.0))
+                                               (args.v_layout == "auto" and 2.0 <= eta <= 32.0 and not dense_rows))
     w = configs.get(args.config, v_layout=om.V_SLICED if sliced else om.V_ROWS)
     if args.expert_kernel != "auto":
         ek = {"token": om.EXPERT_TOKEN, "warp": om.EXPERT_WARP}[args.expert_kernel]

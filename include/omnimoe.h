@@ -319,7 +319,7 @@ omnimoe_status omnimoe_expert_fwd_tokens(const omnimoe_dims* dims, int64_t L, co
                                          float* y_routed, int accumulate, omnimoe_stream_t stream);
 
 /* The routed branch as two dense tcgen05 GEMMs (the executor omnimoe_layer_fwd picks
- * at eta >= 64): Z = x W^T [L][N] fp32; A = gate * sigma(Z) on the selected cells, 0
+ * when one head selects K >= N/40 experts and eta >= 32): Z = x W^T [L][N] fp32; A = gate * sigma(Z) on the selected cells, 0
  * elsewhere (bf16); y_routed = A V (written, fp32).  idx, gate [L][h*K] global ids;
  * one head; V in the ROWS layout; ws: omnimoe_dense_workspace_size(). */
 size_t omnimoe_dense_workspace_size(const omnimoe_dims* dims, int64_t L);
@@ -332,9 +332,8 @@ omnimoe_status omnimoe_expert_fwd_dense(const omnimoe_dims* dims, int64_t L, con
  * SLICED layout; for the ROWS layout TOKEN when eta = M / E|E_active| < 2 under
  * uniform routing (then no expert is shared by two tasks and Expert-Centric
  * Scheduling has nothing to reuse -- measured faster); DENSE when
- * eta >= 64 with one head (every expert shared by ~100 tokens: the routed branch as
- * two tcgen05 GEMMs, Z = x W^T, A = gate * sigma(Z) on the selected cells, y = A V);
- * else GROUP. */
+ * one head selects K >= N/40 experts and eta >= 32 (the routed branch as two tcgen05
+ * GEMMs, Z = x W^T, A = gate * sigma(Z) on the selected cells, y = A V); else GROUP. */
 int32_t omnimoe_layer_executor(const omnimoe_dims* dims, int64_t L);
 
 /* Whole layer forward (Eq.MoE / Eq.Assemble):

@@ -34,10 +34,14 @@ int env_int_d(const char* name, int dflt) {
 
 bool layer_uses_dense_executor(const omnimoe_dims& d, int64_t L) {
   const int64_t N = d.n_rows * d.n_cols;
-  // one head: the K ids of a token are distinct, so A is written without accumulation
+  // Dense work is 4 L N d FLOPs on ~1.2 PF/s of tensor cores; the gather executors move
+  // 4 d bytes per task (L K tasks) at ~12 TB/s from L2: dense wins once K / N exceeds
+  // ~1% (measured: C4 and C4' at K/N = 4%: 4.2 vs 7.0 ms and 1.9 vs 2.8 ms; C4'' at
+  // 0.5%: 2.9 vs 1.4 ms), so the rule asks for K >= N / 40 and eta >= 32 (every expert
+  // shared by many tokens).  One head: a token's K ids are distinct, A needs no sums.
   return d.expert_kernel == OMNIMOE_EXPERT_AUTO && d.v_layout == OMNIMOE_V_ROWS && d.dtype == OMNIMOE_BF16 &&
-         d.n_heads == 1 && expected_eta(d, L) >= env_int_d("OMNIMOE_DENSE_ETA", 64) &&
-         (double)L * pad8(N) * 6.0 <= 32.0 * (1 << 30);
+         d.n_heads == 1 && d.top_k * env_int_d("OMNIMOE_DENSE_RATIO", 40) >= N &&
+         expected_eta(d, L) >= 32.0 && (double)L * pad8(N) * 6.0 <= 32.0 * (1 << 30);
 }
 
 size_t dense_expert_ws_bytes(const omnimoe_dims& d, int64_t L) {
