@@ -757,3 +757,28 @@ def test_layer_high_eta_uses_dense_executor():
     e = rel_errors(y.float().cpu().numpy(), y_g.float().cpu().numpy())
     assert e[0] <= 1e-2 and e[1] <= 1e-2, e
     assert rel_errors(y.float().cpu().numpy(), ref)[0] <= 1e-2
+
+
+def test_layer_full_size_sampled_dense_c4():
+    """C4 at full size in the bench's configuration (ROWS layout -> the dense executor);
+    sampled tokens recomputed by the oracle."""
+    w = _dims("C4")
+    dims = w.dims
+    assert om.layer_executor(dims, w.L) == om.EXPERT_DENSE
+    inp = make_inputs(dims, w.L, w.seed)
+    y, idx, gate = om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], inp["V"], inp["w_gate_up"],
+                                inp["w_down"], return_routing=True)
+    torch.cuda.synchronize()
+    toks = np.array([0, 5, 2048, w.L - 1])
+    hr = lambda n, r=None: host_rows(dims, w.seed, n, r)
+    x = hr("x", toks)
+    sub = hr("subkeys").reshape(dims.n_heads, -1, dims.d)
+    r = oracle.route(oracle.logits(x, sub).reshape(len(toks), -1), dims.n_rows, dims.n_cols, dims.top_k)
+    np.testing.assert_array_equal(np.sort(idx[toks].cpu().numpy().reshape(-1, dims.top_k), -1),
+                                  np.sort(r["idx"], -1))
+    used = np.unique(r["idx"])
+    idm = np.stack([used, np.arange(len(used))], 1)
+    ref = oracle.layer(x, sub, hr("W", used), hr("V", used), dims.n_rows, dims.n_cols, dims.top_k,
+                       hr("w_gate_up"), hr("w_down"), id_map=idm)
+    e = rel_errors(y[toks].float().cpu().numpy(), ref["y"])
+    assert e[0] <= 1e-2 and e[1] <= 1e-2, e
