@@ -140,13 +140,16 @@ bool dense_router(const omnimoe_dims& d) { return d.router == OMNIMOE_ROUTER_DEN
 // logits per token-head: N_r + N_c (Cartesian) or N (dense ablation)
 int64_t logit_cols(const omnimoe_dims& d) { return dense_router(d) ? d.n_rows * d.n_cols : d.n_rows + d.n_cols; }
 
-size_t route_ws(const omnimoe_dims& d, int64_t L, void* ws, float** logits, void** sub_ws) {
+size_t route_ws(const omnimoe_dims& d, int64_t L, void* ws, float** logits, void** sub_ws,
+                uint32_t** cand = nullptr) {
   Carver c(ws);
   const int64_t T = L * d.n_heads;
   float* lg = c.take<float>((size_t)std::max<int64_t>(T, 1) * logit_cols(d));
   void* sw = c.take<char>(dense_router(d) ? 0 : exact_logits_ws_bytes(d, L));
+  uint32_t* ct = c.take<uint32_t>(dense_router(d) ? 0 : select_cand_ws_bytes(d) / 4);
   if (logits) *logits = lg;
   if (sub_ws) *sub_ws = sw;
+  if (cand) *cand = ct;
   return c.bytes();
 }
 
@@ -232,7 +235,8 @@ omnimoe_status route_impl(const omnimoe_dims& d, int64_t L, const void* x, const
                           int32_t* idx, float* gate, float* score, void* ws, cudaStream_t st, int sorted = 1) {
   float* logits;
   void* sub_ws;
-  route_ws(d, L, ws, &logits, &sub_ws);
+  uint32_t* cand;
+  route_ws(d, L, ws, &logits, &sub_ws, &cand);
   if (dense_router(d)) {
     OMNI_TRY(logits_impl(d, L, x, subkeys, logits, sub_ws, st));
     return launch_dense_select(d, L * d.n_heads, logits, idx, gate, score, st);
@@ -242,7 +246,7 @@ omnimoe_status route_impl(const omnimoe_dims& d, int64_t L, const void* x, const
   OMNI_TRY(select_params(d, L * d.n_heads, &sp, &smem));
   sp.sorted = sorted;
   OMNI_TRY(logits_impl(d, L, x, subkeys, logits, sub_ws, st));
-  return launch_select(sp, smem, logits, idx, gate, score, st);
+  return launch_select(sp, smem, logits, idx, gate, score, cand, st);
 }
 
 omnimoe_status mlp_impl(const omnimoe_dims& d, int64_t L, const void* x, const void* wgu,

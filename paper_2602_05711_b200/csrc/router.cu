@@ -23,7 +23,6 @@
 namespace omni {
 namespace {
 
-
 struct U128 {
   uint64_t hi, lo;
 };
@@ -443,7 +442,6 @@ __global__ void __launch_bounds__(G > 256 ? G : 256)
   }
 }
 
-
 // ---------------------------------------------------------------------------
 // Large K, candidate-order output (the layer path, sorted == 0): one WARP per
 // token-head, no block barriers.  Selections use bucket refinement on 64-bit
@@ -555,8 +553,6 @@ __device__ WPred warp_select_top(int nslot, BkF bkf, FullF fullf, int want, uint
   }
   return p;
 }
-
-__device__ __forceinline__ bool wsel(const WPred& p, uint64_t bk) { return bk > p.thr; }
 
 // bitonic sort (descending) of a[0..n), n a power of two, by one warp
 __device__ void warp_bitonic_desc(uint64_t* a, int n) {
@@ -706,23 +702,50 @@ __global__ void __launch_bounds__(256)
 // smem: cand[C] (a << 16 | b, (a+1)(b+1) <= K) | per warp: kr[Pr], kc[Pc] (u64), hist[256],
 // the refinement list (kListCap keys + candidate indices)
 constexpr int kListCap = 256;
+// the candidate table: rows a in order, columns b < min(kc, K / (a+1)); one 1024-thread
+// block (kr <= 1024): row lengths, a block scan, then one warp per row writes its entries
+__global__ void __launch_bounds__(1024) cand_table_kernel(int K, int kr, int kc, uint32_t* __restrict__ cand) {
+  __shared__ int off[1025];
+  __shared__ int wsum[32];
+  const int a = threadIdx.x, lane = a & 31, w = a >> 5;
+  const int nb = a < kr ? min(kc, K / (a + 1)) : 0;
+  int inc = nb;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  int base = 0;
+  for (int i = 0; i < w; ++i) base += wsum[i];
+  off[a] = base + inc - nb;
+  __syncthreads();
+  for (int r = w; r < kr; r += 32) {
+    const int n = min(kc, K / (r + 1)), o = off[r];
+    for (int b = lane; b < n; b += 32) cand[o + b] = ((uint32_t)r << 16) | (uint32_t)b;
+  }
+}
+
+// CAND_SMEM: the candidate table is copied into shared memory (when it fits next to two
+// CTAs' per-warp buffers); otherwise it is read from global memory through L1
+template <bool CAND_SMEM>
 __global__ void __launch_bounds__(256, 2)
-    select_bucket_kernel(SelectParams p, int C, int Pr, int Pc, const float* __restrict__ logits,
-                         int32_t* __restrict__ idx, float* __restrict__ gate, float* __restrict__ score) {
+    select_bucket_kernel(SelectParams p, int C, int Pr, int Pc, const uint32_t* __restrict__ cand_g,
+                         const float* __restrict__ logits, int32_t* __restrict__ idx, float* __restrict__ gate,
+                         float* __restrict__ score) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint32_t* cand = reinterpret_cast<uint32_t*>(smem);
   const int K = p.top_k;
   const int kr = min(K, p.n_rows), kc = min(K, p.n_cols);
-  if (threadIdx.x == 0) {  // rows a in order, columns b < min(kc, K / (a+1))
-    int off = 0;
-    for (int a = 0; a < kr; ++a) {
-      const int nb = min(kc, K / (a + 1));
-      for (int b = 0; b < nb; ++b) cand[off++] = ((uint32_t)a << 16) | (uint32_t)b;
-    }
-  }
-  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const size_t cand_bytes = ((size_t)C * 4 + 15) / 16 * 16;
+  const size_t cand_bytes = CAND_SMEM ? ((size_t)C * 4 + 15) / 16 * 16 : 0;
+  const uint32_t* cand = cand_g;
+  if (CAND_SMEM) {
+    uint32_t* cs = reinterpret_cast<uint32_t*>(smem);
+    for (int i = threadIdx.x; i < C; i += blockDim.x) cs[i] = cand_g[i];
+    __syncthreads();
+    cand = cs;
+  }
   const size_t per_warp = (size_t)(Pr + Pc) * 8 + 256 * 4 + kListCap * 12;
   uint8_t* base = smem + cand_bytes + (size_t)wid * per_warp;
   uint64_t* skr = reinterpret_cast<uint64_t*>(base);
@@ -747,7 +770,7 @@ __global__ void __launch_bounds__(256, 2)
     }
     __syncwarp();
     auto hi_of = [&](int c, uint32_t& id, float& vr, float& vc) {
-      const uint32_t ab = cand[c];
+      const uint32_t ab = CAND_SMEM ? cand[c] : __ldg(cand + c);
       const uint2 ra = reinterpret_cast<const uint2*>(skr)[ab >> 16];
       const uint2 cb = reinterpret_cast<const uint2*>(skc)[ab & 0xFFFF];
       vr = __uint_as_float(ra.x);
@@ -893,7 +916,6 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
-
 // ---------------------------------------------------------------------------
 // Ablation "w/o Cartesian Product Router": one 1024-thread CTA
 // per token-head takes the exact top-K of its N dense logits by (value desc, id
@@ -997,37 +1019,58 @@ omnimoe_status launch_dense_select(const omnimoe_dims& d, int64_t T, const float
   return OMNIMOE_OK;
 }
 
+namespace {
+int bucket_cand_count(int64_t K, int64_t n_rows, int64_t n_cols) {
+  const int64_t kr = std::min(K, n_rows), kc = std::min(K, n_cols);
+  int64_t C = 0;
+  for (int64_t a = 0; a < kr; ++a) C += std::min(kc, K / (a + 1));
+  return (int)C;
+}
+}  // namespace
+
+size_t select_cand_ws_bytes(const omnimoe_dims& d) {
+  return (size_t)bucket_cand_count(d.top_k, d.n_rows, d.n_cols) * 4;
+}
+
 omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* logits, int32_t* idx,
-                             float* gate, float* score, cudaStream_t st) {
+                             float* gate, float* score, uint32_t* cand_ws, cudaStream_t st) {
   if (p.top_k + 1 <= 32 && p.C <= 160) {  // small K: warp per token-head, repeated arg-max
     const int grid = std::max(1, std::min((p.T + 7) / 8, kSMs * 8));
     select_warp_kernel<<<grid, 256, 0, st>>>(p, logits, idx, gate, score);
     OMNI_CHECK_LAUNCH("select_warp_kernel");
     return OMNIMOE_OK;
   }
-  if (!p.sorted && p.top_k >= 32 && p.n_rows <= 1024 && p.n_cols <= 1024 && !getenv("OMNIMOE_SELECT_CTA")) {
+  if (!p.sorted && p.top_k >= 32 && p.n_rows <= 1024 && p.n_cols <= 1024 && cand_ws &&
+      !getenv("OMNIMOE_SELECT_CTA")) {
     // candidate-order output (the layer path): warp per token-head, bucket selection
     const int K = p.top_k, kr = std::min(K, p.n_rows), kc = std::min(K, p.n_cols);
-    int C = 0;
-    for (int a = 0; a < kr; ++a) C += std::min(kc, K / (a + 1));
+    const int C = bucket_cand_count(K, p.n_rows, p.n_cols);
     int Pr = 1, Pc = 1;
     while (Pr < kr) Pr <<= 1;
     while (Pc < kc) Pc <<= 1;
-    const size_t cand_bytes = ((size_t)C * 4 + 15) / 16 * 16;
     const size_t per_warp = (size_t)(Pr + Pc) * 8 + 256 * 4 + kListCap * 12;
+    const size_t cand_bytes = ((size_t)C * 4 + 15) / 16 * 16;
     int warps = 8;
-    while (warps > 1 && cand_bytes + warps * per_warp > 200 * 1024) warps >>= 1;
-    const size_t sm = cand_bytes + warps * per_warp;
+    while (warps > 1 && warps * per_warp > 200 * 1024) warps >>= 1;
+    // the candidate table: in shared memory when that still allows two CTAs per SM or
+    // when one wave of one CTA per SM covers all token-heads (C4p: 0.51 vs 0.59 ms); else
+    // in global memory, read through L1, for twice the resident warps (C4: 1.17 vs 1.49 ms)
+    const bool fits = cand_bytes + warps * per_warp <= 200 * 1024;
+    const bool in_smem =
+        fits && (2 * (cand_bytes + warps * per_warp) <= 220 * 1024 || (int64_t)p.T <= (int64_t)warps * kSMs);
+    const size_t sm = (in_smem ? cand_bytes : 0) + warps * per_warp;
     if (sm <= 200 * 1024) {
-      if (cudaFuncSetAttribute(select_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
-          cudaSuccess) {
+      cand_table_kernel<<<1, 1024, 0, st>>>(K, kr, kc, cand_ws);
+      OMNI_CHECK_LAUNCH("cand_table_kernel");
+      auto kern = in_smem ? select_bucket_kernel<true> : select_bucket_kernel<false>;
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
         set_error("route: cannot set select_bucket_kernel shared memory");
         return OMNIMOE_ERR_CUDA;
       }
       int per_sm = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_bucket_kernel, warps * 32, sm);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, sm);
       const int grid = std::max(1, std::min((p.T + warps - 1) / warps, kSMs * std::max(per_sm, 1)));
-      select_bucket_kernel<<<grid, warps * 32, sm, st>>>(p, C, Pr, Pc, logits, idx, gate, score);
+      kern<<<grid, warps * 32, sm, st>>>(p, C, Pr, Pc, cand_ws, logits, idx, gate, score);
       OMNI_CHECK_LAUNCH("select_bucket_kernel");
       return OMNIMOE_OK;
     }

@@ -22,8 +22,11 @@ omnimoe_status select_params(const omnimoe_dims& d, int64_t T, SelectParams* p, 
 // ablation "w/o CPR": exact top-K of T rows of N dense logits (key order)
 omnimoe_status launch_dense_select(const omnimoe_dims& d, int64_t T, const float* logits, int32_t* idx, float* gate,
                                    float* score, cudaStream_t st);
+// device scratch of the layer-path selection: its product-candidate table (global memory,
+// read through L1 so that the shared memory holds only per-warp buffers)
+size_t select_cand_ws_bytes(const omnimoe_dims& d);
 omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* logits, int32_t* idx,
-                             float* gate, float* score, cudaStream_t st);
+                             float* gate, float* score, uint32_t* cand_ws, cudaStream_t st);
 
 // a1: exact logits RN32(x . sub) (reading Q9), [L][h*(N_r+N_c)] fp32.
 size_t exact_logits_ws_bytes(const omnimoe_dims& d, int64_t L);
