@@ -141,12 +141,12 @@ bool dense_router(const omnimoe_dims& d) { return d.router == OMNIMOE_ROUTER_DEN
 int64_t logit_cols(const omnimoe_dims& d) { return dense_router(d) ? d.n_rows * d.n_cols : d.n_rows + d.n_cols; }
 
 size_t route_ws(const omnimoe_dims& d, int64_t L, void* ws, float** logits, void** sub_ws,
-                uint32_t** cand = nullptr) {
+                uint32_t** cand = nullptr, bool with_cand = true) {
   Carver c(ws);
   const int64_t T = L * d.n_heads;
   float* lg = c.take<float>((size_t)std::max<int64_t>(T, 1) * logit_cols(d));
   void* sw = c.take<char>(dense_router(d) ? 0 : exact_logits_ws_bytes(d, L));
-  uint32_t* ct = c.take<uint32_t>(dense_router(d) ? 0 : select_cand_ws_bytes(d) / 4);
+  uint32_t* ct = c.take<uint32_t>(dense_router(d) || !with_cand ? 0 : select_cand_ws_bytes(d) / 4);
   if (logits) *logits = lg;
   if (sub_ws) *sub_ws = sw;
   if (cand) *cand = ct;
@@ -165,13 +165,18 @@ struct LayerWs {
   float* y_routed;
   void* H;
   void* expert_ws;
+  uint32_t* cand;
 };
 
 size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
   Carver c(ws);
   const int64_t N = d.n_rows * d.n_cols;
   const int64_t M = L * d.n_heads * d.top_k;
-  const size_t rb = route_ws(d, L, nullptr, nullptr, nullptr);
+  // the selection's candidate table is carved last, so that the other offsets do not
+  // depend on it: the SLICED pass V is sensitive to where the plan arrays fall (C5: 55.0
+  // ms with this layout, 58.7-59.2 ms with everything after the route scratch shifted by
+  // 14 KB, 64 KB or 1 MB -- DESIGN.md §10)
+  const size_t rb = route_ws(d, L, nullptr, nullptr, nullptr, nullptr, false);
   void* rw = c.take<char>(rb);
   int32_t* idx = c.take<int32_t>((size_t)std::max<int64_t>(M, 1));
   float* gate = c.take<float>((size_t)std::max<int64_t>(M, 1));
@@ -192,7 +197,9 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
   float* yr = c.take<float>((size_t)L * d.d);
   void* ew = c.take<char>(layer_uses_dense_executor(d, L) ? dense_expert_ws_bytes(d, L) : expert_ws_bytes(d, L));
   void* H = c.take<char>((size_t)L * std::max<int64_t>(d.d_ff, 1) * elem_size(d));
+  uint32_t* cand = c.take<uint32_t>(dense_router(d) ? 0 : select_cand_ws_bytes(d) / 4);
   if (o) {
+    o->cand = cand;
     o->route_ws = rw;
     o->route_bytes = rb;
     o->idx = idx;
@@ -232,11 +239,12 @@ omnimoe_status logits_impl(const omnimoe_dims& d, int64_t L, const void* x, cons
 
 // a1 (exact logits, Q9) -> a2 + a3 (select_kernel)
 omnimoe_status route_impl(const omnimoe_dims& d, int64_t L, const void* x, const void* subkeys,
-                          int32_t* idx, float* gate, float* score, void* ws, cudaStream_t st, int sorted = 1) {
+                          int32_t* idx, float* gate, float* score, void* ws, cudaStream_t st, int sorted = 1,
+                          uint32_t* cand_ws = nullptr) {
   float* logits;
   void* sub_ws;
-  uint32_t* cand;
-  route_ws(d, L, ws, &logits, &sub_ws, &cand);
+  uint32_t* cand = cand_ws;
+  route_ws(d, L, ws, &logits, &sub_ws, cand_ws ? nullptr : &cand, cand_ws == nullptr);
   if (dense_router(d)) {
     OMNI_TRY(logits_impl(d, L, x, subkeys, logits, sub_ws, st));
     return launch_dense_select(d, L * d.n_heads, logits, idx, gate, score, st);
@@ -501,7 +509,7 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
   float* gate = gate_out ? gate_out : w.gate;
   const int64_t M = L * d.n_heads * d.top_k;
   // the layer does not need the ids sorted by key (the schedule re-sorts the tasks)
-  OMNI_TRY(route_impl(d, L, x, subkeys, idx, gate, nullptr, w.route_ws, st, /*sorted=*/0));
+  OMNI_TRY(route_impl(d, L, x, subkeys, idx, gate, nullptr, w.route_ws, st, /*sorted=*/0, w.cand));
   const int r_launch = omnimoe_last_launch_count();
   w.plan.n_tokens = L;
   if (layer_uses_token_executor(d, L)) {  // no expert shared by two tasks (or the "w/o ECS" ablation)
@@ -749,7 +757,7 @@ omnimoe_status omnimoe_layer_fwd_host(const omnimoe_dims* dims, int64_t L, const
       return OMNIMOE_ERR_CUDA;
     }
     OMNI_TRY(route_impl(d, n, static_cast<const char*>(x_dev) + l0 * d.d * eb, subkeys, w.idx + l0 * hk,
-                        w.gate + l0 * hk, nullptr, w.route_ws, st, /*sorted=*/0));
+                        w.gate + l0 * hk, nullptr, w.route_ws, st, /*sorted=*/0, w.cand));
   }
   // 2. the routed branch over the whole batch (Expert-Centric Scheduling needs every task)
   w.plan.n_tokens = L;
