@@ -782,3 +782,28 @@ def test_layer_full_size_sampled_dense_c4():
                        hr("w_gate_up"), hr("w_down"), id_map=idm)
     e = rel_errors(y[toks].float().cpu().numpy(), ref["y"])
     assert e[0] <= 1e-2 and e[1] <= 1e-2, e
+
+
+@pytest.mark.parametrize("d,nr,nc,K,L,act", [
+    (96, 37, 37, 5, 200, om.SILU),        # N = 1369 (not a multiple of 8, 32 or 64), d % 64 != 0
+    (128, 40, 40, 800, 130, om.SILU),     # K / N = 50%: dense chunks, gates beyond the staged 16
+    (64, 16, 16, 256, 257, om.IDENTITY),  # every expert selected by every token
+    (256, 64, 48, 40, 1, om.SILU),        # one token
+])
+def test_expert_fwd_dense_ragged(d, nr, nc, K, L, act):
+    """The dense executor (gated GEMM epilogue + MN-major V operand) on ragged shapes, from a
+    seeded random routing, against the oracle's token-centric routed branch."""
+    dims = om.LayerDims(d=d, n_rows=nr, n_cols=nc, top_k=K, d_ff=0, act=act)
+    N = nr * nc
+    inp = make_inputs(dims, L, 41)
+    g = torch.Generator().manual_seed(L * 1000 + K)
+    ids = torch.stack([torch.randperm(N, generator=g)[:K] for _ in range(L)]).to(torch.int32)
+    gates = torch.rand((L, K), generator=g, dtype=torch.float32) + 0.05
+    gates /= gates.sum(-1, keepdim=True)
+    yr = om.expert_fwd_dense(dims, inp["x"], inp["W"], inp["V"], ids.cuda(), gates.cuda())
+    torch.cuda.synchronize()
+    hr = lambda n, r=None: host_rows(dims, 41, n, r)
+    ref = oracle.routed_token_centric(hr("x", np.arange(L)), hr("W"), hr("V"), ids.numpy(),
+                                      gates.double().numpy(), act=act)
+    e = rel_errors(yr.cpu().numpy(), ref)
+    assert e[0] <= 1e-2 and e[1] <= 1e-2, e
