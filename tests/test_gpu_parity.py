@@ -789,6 +789,7 @@ def test_layer_full_size_sampled_dense_c4():
     (128, 40, 40, 800, 130, om.SILU),     # K / N = 50%: dense chunks, gates beyond the staged 16
     (64, 16, 16, 256, 257, om.IDENTITY),  # every expert selected by every token
     (256, 64, 48, 40, 1, om.SILU),        # one token
+    (64, 600, 600, 64, 9, om.SILU),       # N = 360,000: rows too wide for the shared-memory prep
 ])
 def test_expert_fwd_dense_ragged(d, nr, nc, K, L, act):
     """The dense executor (gated GEMM epilogue + MN-major V operand) on ragged shapes, from a
