@@ -300,6 +300,151 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// Persistent variant (CN = 1, the default): one CTA per SM walks the (m, n) tiles, n
+// fastest (consecutive CTAs share the token limbs in L2); the TMA producer keeps its stage
+// ring running across tiles, so the next tile's first K blocks load while the epilogue
+// drains TMEM; 8 epilogue warps (two per TMEM lane quarter, one column half each).  The
+// 480-column accumulator set is single-buffered: the MMAs of tile i+1 start once the
+// epilogue has read tile i's accumulators (tempty).
+constexpr int kIEpiWarps = 8;
+__global__ void __launch_bounds__(128 + 32 * kIEpiWarps, 1)
+    gemm_i8_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           I8Args args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kIStages * 3 * kIABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kIStages * kIStageBytes);
+  uint64_t* empty = full + kIStages;
+  uint64_t* tfull = empty + kIStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_kb = (args.K + IBK - 1) / IBK;
+  const int n_nt = (args.N + IBN - 1) / IBN;
+  const int n_tiles = n_nt * ((args.M + IBM - 1) / IBM);
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int s = 0; s < kIStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, kIEpiWarps);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kITmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer: one stage ring across all tiles ----------------
+    int g = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const int m0 = (t / n_nt) * IBM, n0 = (t % n_nt) * IBN;
+      for (int kb = 0; kb < num_kb; ++kb, ++g) {
+        const int s = g % kIStages;
+        mbar_wait(&empty[s], ((g / kIStages) & 1) ^ 1);
+        mbar_expect_tx(&full[s], kIStageBytes);
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+          tma_load_2d(&tmA, &full[s], sA + (s * 3 + p) * kIABytes, kb * IBK, p * args.M + m0);
+          tma_load_2d(&tmB, &full[s], sB + (s * 3 + p) * kIBBytes, kb * IBK, p * args.N + n0);
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer: D_{p+q} += X_p . W_q^T ----------------
+    int g = 0, it = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      mbar_wait(tempty, (it & 1) ^ 1);  // the epilogue has read the previous tile
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int kb = 0; kb < num_kb; ++kb, ++g) {
+        const int s = g % kIStages;
+        mbar_wait(&full[s], (g / kIStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const uint32_t a0 = smem_u32(sA + (s * 3 + p) * kIABytes);
+            const uint32_t b0 = smem_u32(sB + (s * 3 + q) * kIBBytes);
+            const bool first_pair = (p == 0 || q == 2);
+#pragma unroll
+            for (int k = 0; k < IBK / 32; ++k)
+              umma_i8(tmem + (uint32_t)((p + q) * IBN), sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32),
+                      kIdescI8, !(kb == 0 && k == 0 && first_pair));
+          }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tfull);
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: exact int64 combination, one rounding ----------------
+    const int e = warp - 4, qd = e & 3, h = e >> 2;
+    constexpr int kChunks = IBN / 16;
+    const int c_lo = h * kChunks / 2, c_hi = (h + 1) * kChunks / 2;
+    int it = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      const int m0 = (t / n_nt) * IBM, n0 = (t % n_nt) * IBN;
+      const int row = m0 + qd * 32 + lane;
+      const bool row_ok = row < args.M;
+      const int exr = row_ok ? args.ex[row] : 0;
+      mbar_wait(tfull, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16);
+#pragma unroll 1
+      for (int c = c_lo; c < c_hi; ++c) {
+        uint32_t D[5][16];
+#pragma unroll
+        for (int s = 0; s < 5; ++s) tmem_ld16(tbase + s * IBN + c * 16, D[s]);
+        tmem_wait_ld();
+        if (c == c_hi - 1) {  // every accumulator column of this warp is in registers
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty)) : "memory");
+        }
+        const int col0 = n0 + c * 16;
+        if (!row_ok || col0 >= args.N) continue;
+        float o[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int64_t S = (int64_t)(int32_t)D[0][j] + ((int64_t)(int32_t)D[1][j] << 8) +
+                            ((int64_t)(int32_t)D[2][j] << 16) + ((int64_t)(int32_t)D[3][j] << 24) +
+                            ((int64_t)(int32_t)D[4][j] << 32);
+          const int col = min(col0 + j, args.N - 1);
+          o[j] = ldexpf(__ll2float_rn(S), exr + args.ew[col]);
+        }
+        float* dst = args.out + (size_t)row * args.N + col0;
+        if (col0 + 16 <= args.N && (args.N % 4) == 0) {
+          float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) d4[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (col0 + j < args.N) dst[j] = o[j];
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kITmemCols));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // exact fp64 double-double dot + correct RN32
 template <typename T>
@@ -462,7 +607,7 @@ omnimoe_status exact_logits(const omnimoe_dims& d, int64_t L, const void* x, con
 
   static bool attr_set = false;
   if (!attr_set) {
-    for (auto k : {gemm_i8_exact_kernel<1>, gemm_i8_exact_kernel<2>, gemm_i8_exact_kernel<4>})
+    for (auto k : {gemm_i8_exact_kernel<1>, gemm_i8_exact_kernel<2>, gemm_i8_exact_kernel<4>, gemm_i8_persist_kernel})
       if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kISmemBytes) != cudaSuccess) {
         set_error("route: cannot set dynamic shared memory size of the i8 GEMM");
         return OMNIMOE_ERR_CUDA;
@@ -483,7 +628,11 @@ omnimoe_status exact_logits(const omnimoe_dims& d, int64_t L, const void* x, con
   }
   I8Args a{(int)L, NC, (int)d.d, w.ex, w.ew, logits};
   dim3 grid(n_tiles, (unsigned)((L + IBM - 1) / IBM));
-  if (CN == 1) {
+  if (CN == 1 && env_int("OMNIMOE_I8_PERSIST", 1)) {
+    const int64_t tiles = (int64_t)grid.x * grid.y;
+    gemm_i8_persist_kernel<<<(int)std::min<int64_t>(tiles, kSMs), 128 + 32 * kIEpiWarps, kISmemBytes, st>>>(mA, mB,
+                                                                                                         a);
+  } else if (CN == 1) {
     gemm_i8_exact_kernel<1><<<grid, 256, kISmemBytes, st>>>(mA, mB, a);
   } else {
     cudaLaunchConfig_t cfg = {};
