@@ -195,6 +195,8 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
   const size_t sb = schedule_ws_bytes(M, N);
   void* sw = c.take<char>(sb);
   float* yr = c.take<float>((size_t)L * d.d);
+  // measurement override: pad before the executor's work counters (placement study)
+  if (const char* pad = getenv("OMNIMOE_WS_PAD_COUNTERS")) c.take<char>((size_t)atoll(pad));
   void* ew = c.take<char>(layer_uses_dense_executor(d, L) ? dense_expert_ws_bytes(d, L) : expert_ws_bytes(d, L));
   void* H = c.take<char>((size_t)L * std::max<int64_t>(d.d_ff, 1) * elem_size(d));
   uint32_t* cand = c.take<uint32_t>(dense_router(d) ? 0 : select_cand_ws_bytes(d) / 4);
