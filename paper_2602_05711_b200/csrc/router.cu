@@ -573,7 +573,7 @@ __device__ void warp_bitonic_desc(uint64_t* a, int n) {
     }
 }
 
-// the top k1 half keys of lg[0..n) (n <= 1024), sorted descending into out[0..P)
+// the top k1 half keys of lg[0..n), sorted descending into out[0..P)
 // (P = pow2 >= k1, padded with 0); returns logsumexp of the half if want_lse
 __device__ float warp_half_sorted(const float* __restrict__ lg, int n, int k1, int P, uint64_t* out, int* hist,
                                   bool want_lse) {
@@ -1040,7 +1040,8 @@ omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* lo
     OMNI_CHECK_LAUNCH("select_warp_kernel");
     return OMNIMOE_OK;
   }
-  if (!p.sorted && p.top_k >= 32 && p.n_rows <= 1024 && p.n_cols <= 1024 && cand_ws &&
+  if (!p.sorted && p.top_k >= 32 && std::min(p.top_k, p.n_rows) <= 1024 && std::min(p.top_k, p.n_cols) <= 1024 &&
+      cand_ws &&
       !getenv("OMNIMOE_SELECT_CTA")) {
     // candidate-order output (the layer path): warp per token-head, bucket selection
     const int K = p.top_k, kr = std::min(K, p.n_rows), kc = std::min(K, p.n_cols);
