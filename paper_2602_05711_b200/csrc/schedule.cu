@@ -311,14 +311,15 @@ __global__ void gather_plan_kernel(const int32_t* __restrict__ order, int64_t M,
                                    const int32_t* __restrict__ ids, int64_t begin, int64_t hk,
                                    int32_t* __restrict__ sorted_token, float* __restrict__ sorted_gate,
                                    int32_t* __restrict__ sorted_expert, int32_t* __restrict__ sorted_task,
-                                   const int32_t* __restrict__ dest) {
+                                   const int32_t* __restrict__ dest, const uint32_t* __restrict__ skeys) {
   const int64_t m_loc = *m_loc_ptr;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m_loc;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int32_t t = order[p];
     sorted_token[p] = token ? token[t] : (int32_t)(t / hk);
     sorted_gate[p] = gate[t];
-    sorted_expert[p] = (int32_t)(ids[t] - begin);
+    // B = 1: the sorted keys are the local expert ids (coalesced, instead of a gather)
+    sorted_expert[p] = skeys ? (int32_t)skeys[p] : (int32_t)(ids[t] - begin);
     if (sorted_task) sorted_task[p] = dest ? dest[t] : t;
   }
 }
@@ -486,7 +487,8 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
   const int32_t* m_loc = plan.expert_offsets + n_loc;
   gather_plan_kernel<<<grid_for(M, 256), 256, 0, st>>>(vin, M, m_loc, token, gate, ids, plan.expert_begin, hk,
                                                       plan.sorted_token, plan.sorted_gate, plan.sorted_expert,
-                                                      vorder ? plan.sorted_task : nullptr, vorder && n_bands > 1 ? dest : nullptr);
+                                                      vorder ? plan.sorted_task : nullptr, vorder && n_bands > 1 ? dest : nullptr,
+                                                      B > 1 ? nullptr : kin);
   OMNI_CHECK_LAUNCH("gather_plan_kernel");
   if (B > 1) {
     // runs: (group, token) boundaries of the sorted plan, compacted to run_offsets
