@@ -2,7 +2,8 @@
 
 Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
 ``--impl reference``) may import this package.  The product path
-(paper_2602_05711_b200) never imports it; tests/test_hygiene.py enforces that.
+(paper_2602_05711_b200) never imports it; tests/test_abi_cpu.py::test_product_never_imports_oracle
+enforces that.
 See oracle/oracle.cpp for the citations of each function.
 """
 from __future__ import annotations

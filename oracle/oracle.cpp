@@ -11,7 +11,7 @@
 // Citations: "PAPER:n" = /root/reference/PAPER.md line n (section / equation
 // named alongside); "Q#" = a reading listed in DESIGN.md "Readings".
 //
-// Pins: every function below is pinned by tests/test_oracle_*.py (-m "not gpu")
+// Pins: every function below is pinned by tests/test_oracle.py (-m "not gpu")
 // against closed forms, brute force, invariants and SPEC worked examples,
 // EXCEPT absolute layer outputs at paper scale, which the paper never prints:
 // "parity unpinned" for absolute values (P12) -- only the
@@ -384,12 +384,80 @@ void oracle_mlp_bwd(int64_t L, int64_t d, int64_t dff, const double* x, const do
 // and sub-key row r (rows [0,N_r) are W_r's columns, rows [N_r, N_r+N_c) are
 // W_c's), s = RN32(sum_k x[l][k]*sub[h][r][k]) -- the fp32 round-to-nearest-
 // even of the EXACT real dot product (exact_dot_rn32 above).
+// The same function as exact_dot_rn32 per (token, head, row), organised for
+// speed: every row is written ONCE as integers at the row's finest exponent,
+// v_k = M_k * 2^E_row (exact; M_k = m_k * 2^(e_k - E_row)), so that a dot
+// product is sum_k Mx_k * Mw_k (exact in a 128-bit integer) times
+// 2^(E_x + E_w), rounded once (round_int128_to_f32).  A row whose integers do
+// not fit 62 bits, or a pair whose products could exceed the accumulator, is
+// left to exact_dot_rn32 (tests/test_oracle.py::test_logits_row_integer_path
+// checks both routes against Python Fractions).
+struct IntRow {
+  std::vector<int64_t> M;
+  int E = 0;
+  int bits = 0;     // bits of max |M_k|
+  bool ok = false;  // false: use exact_dot_rn32
+};
+
+inline IntRow int_row(const double* v, int64_t d) {
+  IntRow r;
+  std::vector<Dyadic> q(d);
+  int emin = 1 << 30;
+  for (int64_t k = 0; k < d; ++k) {
+    q[k] = to_dyadic(v[k]);
+    if (!q[k].ok) return r;
+    if (q[k].m != 0) emin = std::min(emin, q[k].e);
+  }
+  r.M.assign(d, 0);
+  r.E = emin == (1 << 30) ? 0 : emin;
+  uint64_t amax = 0;
+  for (int64_t k = 0; k < d; ++k) {
+    if (q[k].m == 0) continue;
+    const int sh = q[k].e - r.E;
+    const uint64_t a = (uint64_t)(q[k].m < 0 ? -q[k].m : q[k].m);
+    int b = 0;
+    for (uint64_t t = a; t; t >>= 1) ++b;
+    if (b + sh > 62) return r;  // r.ok stays false
+    r.M[k] = q[k].m * ((int64_t)1 << sh);
+    amax = std::max(amax, a << sh);
+  }
+  for (uint64_t t = amax; t; t >>= 1) ++r.bits;
+  r.ok = true;
+  return r;
+}
+
 void oracle_logits(int64_t L, int64_t d, int64_t h, int64_t R, const double* x, const double* sub,
                    float* out, int nthreads) {
-  parallel_for(L, nthreads, [&](int64_t l) {
+  std::vector<IntRow> wrow(h * R);
+  parallel_for(h * R, nthreads, [&](int64_t r) { wrow[r] = int_row(sub + r * d, d); });
+  int lg = 0;
+  while (((int64_t)1 << lg) < d) ++lg;
+  const int64_t TB = 16;  // tokens per block: each sub-key row is read once per block
+  parallel_for((L + TB - 1) / TB, nthreads, [&](int64_t blk) {
+    const int64_t l0 = blk * TB, l1 = std::min(L, l0 + TB);
+    std::vector<IntRow> xr(l1 - l0);
+    for (int64_t l = l0; l < l1; ++l) xr[l - l0] = int_row(x + l * d, d);
     for (int64_t hh = 0; hh < h; ++hh)
-      for (int64_t r = 0; r < R; ++r)
-        out[(l * h + hh) * R + r] = exact_dot_rn32(x + l * d, sub + (hh * R + r) * d, d);
+      for (int64_t r = 0; r < R; ++r) {
+        const IntRow& wr = wrow[hh * R + r];
+        for (int64_t l = l0; l < l1; ++l) {
+          const IntRow& xl = xr[l - l0];
+          float& o = out[(l * h + hh) * R + r];
+          if (!xl.ok || !wr.ok || xl.bits + wr.bits + lg > 125) {
+            o = exact_dot_rn32(x + l * d, sub + (hh * R + r) * d, d);
+            continue;
+          }
+          __int128 S = 0;
+          if (xl.bits + wr.bits + lg <= 62) {  // every partial sum fits int64
+            int64_t s64 = 0;
+            for (int64_t k = 0; k < d; ++k) s64 += xl.M[k] * wr.M[k];
+            S = s64;
+          } else {
+            for (int64_t k = 0; k < d; ++k) S += (__int128)xl.M[k] * wr.M[k];
+          }
+          o = round_int128_to_f32(S, xl.E + wr.E);
+        }
+      }
   });
 }
 

@@ -1,7 +1,7 @@
 // Device twin of synth/__init__.py: the seeded counter-based input generator.
 // Holds no arithmetic of the OmniMoE method; it only fills buffers with
 // (seed, tensor id, index) -> v * 2^-e draws, bit-identical to the numpy
-// implementation (tests/test_gpu_synth.py checks this).  Built into
+// implementation (tests/test_gpu_parity.py::test_synth_device_matches_host checks this).  Built into
 // synth/libsynth.so, separate from the product library.
 #include <cstdint>
 #include <cuda_runtime.h>

@@ -141,6 +141,28 @@ def test_logsoftmax_golden_via_scores():
     np.testing.assert_allclose(r["score"][0], [g["expected"][1], g["expected"][0]], atol=1e-7)
 
 
+def test_scores_are_log_probabilities_of_whole_halves_k_lt_n():
+    """score = kappa - lse_r - lse_c with each lse over the WHOLE half (Eq.LSM,
+    PAPER:215-219), not over the selected keys: rows with softmax probabilities
+    [.1, .2, .3, .4], columns [.5, .5], K = 3 < N = 8.  Closed form: the top 3 cells
+    are (3,0), (3,1) (exact tie: lower flat id 6 first, Q7), (2,0); scores are
+    log(p_r p_c) = log .2, log .2, log .15; gates = softmax over the selected keys
+    (Eq.Gate) = [4, 4, 3] / 11.  An lse over the selected keys only would give
+    log(4/11) instead."""
+    lg = np.array([[np.log(1.0), np.log(2.0), np.log(3.0), np.log(4.0), 0.0, 0.0]], dtype=np.float32)
+    for m in (oracle.BRUTE, oracle.PRODUCT, oracle.BLOCKMERGE):
+        r = oracle.route(lg, 4, 2, 3, method=m, bsel=3)
+        assert list(r["idx"][0]) == [6, 7, 4]
+        np.testing.assert_allclose(r["score"][0], np.log([0.2, 0.2, 0.15]), atol=1e-6)
+        np.testing.assert_allclose(r["gate"][0], np.array([4, 4, 3]) / 11.0, atol=1e-6)
+    # a second shape: 3 x 3 grid with K = 2, rows [.5, .25, .25], columns [.7, .2, .1]
+    lg = np.array([[np.log(2.0), 0.0, 0.0, np.log(7.0), np.log(2.0), np.log(1.0)]], dtype=np.float32)
+    r = oracle.route(lg, 3, 3, 2)
+    assert list(r["idx"][0]) == [0, 3]  # (0,0) .35, then (1,0) and (2,0) tie at .175: id 3 < 6
+    np.testing.assert_allclose(r["score"][0], np.log([0.35, 0.175]), atol=1e-6)
+    assert r["gap"][0] == 0.0  # K-th and (K+1)-th keys are exactly equal
+
+
 # ---- P4: invariants ----------------------------------------------------------------
 def test_shift_invariance_and_normalisation():
     rng = np.random.default_rng(9)
@@ -233,6 +255,44 @@ def test_exact_dot_double_rounding_cases():
     # contract: fp32-representable inputs only; anything else is reported as NaN
     assert np.isnan(oracle.exact_dot([0.1], [1.0]))
     assert np.isnan(oracle.exact_dot([2.0 ** 100, 2.0 ** -100], [1.0, 1.0]))
+
+
+def test_logits_row_integer_path_vs_fractions():
+    """oracle.logits writes each row once as integers at its finest exponent and sums
+    the products in int64 / int128 (rows that do not fit fall back to the per-dot
+    routine): every logit must still be RN32 of the exact Fraction dot product,
+    for narrow rows (int64 sums), wide rows (int128 sums) and rows beyond 62-bit
+    integers (fallback), and for the double-rounding and cancellation cases."""
+    rng = np.random.default_rng(77)
+    d = 40
+    rows = []
+    for kind in range(6):
+        for _ in range(3):
+            if kind == 0:  # bf16 generator-like
+                v = synth.bf16_bits_to_f64(synth.f32_to_bf16_bits(rng.standard_normal(d).astype(np.float32)))
+            elif kind == 1:  # fp32 over +-12 binades: int128 sums
+                v = (rng.standard_normal(d) * 2.0 ** rng.integers(-12, 12, d)).astype(np.float32).astype(np.float64)
+            elif kind == 2:  # exponent spread > 62 bits: fallback route
+                v = (rng.standard_normal(d) * 2.0 ** rng.integers(-50, 50, d)).astype(np.float32).astype(np.float64)
+            elif kind == 3:  # zeros and a zero row
+                v = np.where(rng.random(d) < 0.5, 0.0, rng.integers(-4, 5, d) / 64.0)
+            elif kind == 4:
+                v = np.zeros(d)
+            else:  # 1 + 2^-24 + 2^-60 padded: the double-rounding case inside a longer row
+                v = np.zeros(d)
+                v[:3] = [1.0, 2.0 ** -24, 2.0 ** -60]
+            rows.append(v)
+    X = np.array(rows)
+    W = np.concatenate([X[::-1], np.ones((1, d))])[None]  # [1][R][d], includes the all-ones row
+    got = oracle.logits(X, W)
+    for i in range(X.shape[0]):
+        for r in range(W.shape[1]):
+            per_dot = oracle.exact_dot(X[i], W[0, r])
+            if np.isnan(per_dot):  # beyond the 128-bit accumulator: NaN by contract, on both routes
+                assert np.isnan(got[i, 0, r]), (i, r)
+                continue
+            want = _rn32_of_fraction(_exact_dot(X[i], W[0, r]))
+            assert got[i, 0, r] == want == per_dot, (i, r, got[i, 0, r], want)
 
 
 # ---- P5: schedule + executor identity ----------------------------------------------
