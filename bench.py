@@ -127,14 +127,19 @@ def ncu_traffic(config, kernel):
 
 
 # ---------------------------------------------------------------- CPU oracle
-def cpu_oracle_rate(w, target_s, max_tokens, nthreads, inp=None):
+def cpu_oracle_rate(w, target_s, max_tokens, nthreads, inp=None, gpu=None):
     """The oracle layer (as it stands) on a bounded token sample.  Expert rows are
     taken from the seeded generator (the device twin's tables when ``inp`` holds
     them -- bit-identical to the host generator, tests/test_gpu_parity.py -- else
-    the numpy generator); only the oracle call is timed.  The sample grows in
-    chunks of 32 tokens until ~target_s seconds of oracle time."""
+    the host twins); only the oracle call is timed.  The sample grows in
+    chunks of 32 tokens until ~target_s seconds of oracle time.
+
+    gpu = (y, idx) of the timed layer (host arrays): the same sample then yields
+    the north star's parity counters -- token-heads whose id set differs from the
+    oracle's (mismatch), of those the ones inside the 1e-6 score-gap allowance
+    (allowed, reading Q10) and the rest (disallowed) -- and e_tok / e_elt (Q17)."""
     import oracle
-    from tests.helpers import host_rows
+    from tests.helpers import host_rows, rel_errors, routing_counts
     dims = w.dims
     R = dims.n_rows + dims.n_cols
     sub = host_rows(dims, w.seed, "subkeys").reshape(dims.n_heads, R, dims.d)
@@ -153,6 +158,8 @@ def cpu_oracle_rate(w, target_s, max_tokens, nthreads, inp=None):
         return host_rows(dims, w.seed, name, used)
 
     total_t, done, chunk = 0.0, 0, 32
+    par = {"tokens": 0, "token_heads": 0, "mismatch": 0, "allowed": 0, "disallowed": 0, "gate_err": 0.0,
+           "e_tok": 0.0, "e_elt": 0.0}
     while done < max_tokens and total_t < target_s:
         toks = np.arange(done, min(max_tokens, done + chunk)) % w.L
         x = host_rows(dims, w.seed, "x", toks)
@@ -162,10 +169,22 @@ def cpu_oracle_rate(w, target_s, max_tokens, nthreads, inp=None):
         W, V = rows("W", used), rows("V", used)
         idm = np.stack([used, np.arange(len(used))], 1)
         t0 = time.perf_counter()
-        oracle.layer(x, sub, W, V, dims.n_rows, dims.n_cols, dims.top_k, wgu, wdn, id_map=idm, nthreads=nthreads)
+        ref = oracle.layer(x, sub, W, V, dims.n_rows, dims.n_cols, dims.top_k, wgu, wdn, id_map=idm,
+                           nthreads=nthreads)
         total_t += time.perf_counter() - t0
         done += len(toks)
-    return done / total_t, done, total_t
+        if gpu is not None:
+            gy, gidx, ggate = gpu
+            K = dims.top_k
+            c = routing_counts(gidx[toks].reshape(-1, K), ggate[toks].reshape(-1, K), r, lg.reshape(-1, R),
+                               dims.n_rows, dims.n_cols)
+            et, ee = rel_errors(gy[toks], ref["y"])
+            par["tokens"] += len(toks)
+            for k in ("token_heads", "mismatch", "allowed", "disallowed"):
+                par[k] += c[k]
+            par["e_tok"], par["e_elt"] = max(par["e_tok"], et), max(par["e_elt"], ee)
+            par["gate_err"] = max(par["gate_err"], c["gate_err"])
+    return done / total_t, done, total_t, par
 
 
 def run_reference(args):
@@ -184,7 +203,7 @@ def run_reference(args):
     cpu_oracle_rate(w, 0.5, 32, nth, tables)  # warm-up (page-in, thread pool)
     rates, toks = [], 0
     for _ in range(args.steps):
-        rate, done, _t = cpu_oracle_rate(w, per_step_s, 1 << 20, nth, tables)
+        rate, done, _t, _ = cpu_oracle_rate(w, per_step_s, 1 << 20, nth, tables)
         rates.append(rate)
         toks += done
     rate = statistics.mean(rates)
@@ -394,10 +413,18 @@ def bench_single(args, w, lr):
     R_ = dims.n_rows + dims.n_cols
     router_ops = 2.0 * L * dims.n_heads * R_ * dims.d
     mlp_flops = 6.0 * L * dims.d * dims.d_ff
-    cpu = None
+    cpu = parity = None
     if not args.no_cpu_baseline:
         nth = os.cpu_count() or 1
-        rate, done, t = cpu_oracle_rate(w, args.cpu_seconds, 1 << 20, nth, oinp)
+        # the timed layer's output and routing on the same inputs, for the parity counters
+        yo, io, go = om.layer_fwd(dims, inp["x"], inp["subkeys"], inp["W"], inp["V"], inp.get("w_gate_up"),
+                                 inp.get("w_down"), return_routing=True, ws=lws)
+        gpu = (yo.float().cpu().numpy(), io.cpu().numpy().reshape(L, -1), go.cpu().numpy().reshape(L, -1))
+        del yo, io, go
+        rate, done, t, parity = cpu_oracle_rate(w, args.cpu_seconds, 1 << 20, nth, oinp, gpu)
+        parity["note"] = ("layer output of the timed call vs oracle.layer on the cpu_baseline sample: router id "
+                          "sets per token-head (reading Q10: mismatches allowed only where the oracle's score gap "
+                          "< 1e-6), e_tok / e_elt (Q17, bound 1e-2 in bf16)")
         cpu = {"value": rate, "unit": "tokens/s", "cores": nth, "kind": "oracle",
                "sample": f"{done} tokens of {w.name} (oracle layer: exact logits, product top-K, token-centric "
                          f"routed branch, shared MLP): {t:.1f} s of oracle time on {nth} threads"}
@@ -427,7 +454,7 @@ def bench_single(args, w, lr):
             "shared_mlp_a7": {"tflop": mlp_flops / 1e12, "peak_tflops": pk["bf16_sus"],
                               "achieved_tflops": mlp_flops / (stage_ms["shared_mlp_a7_a8"] / 1e3) / 1e12
                               if dims.d_ff else None}},
-        "e2e": e2e, "cpu_baseline": cpu,
+        "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
         "gpu_launches": launches, "launches_per_step": launches / max(args.steps, 1),
         "clocks": clk.summary(),
         "context": "paper: 6.7 ms OmniMoE vs 73 ms PEER per layer at 4,096 tokens, d=1024, N=102,400, K=4096 on "

@@ -68,7 +68,7 @@ enum { OMNIMOE_EXPERT_AUTO = 0, OMNIMOE_EXPERT_WARP = 1, OMNIMOE_EXPERT_GROUP = 
 enum { OMNIMOE_V_ROWS = 0, OMNIMOE_V_SLICED = 1 };
 /* workspace query selector */
 enum { OMNIMOE_WS_ROUTE = 0, OMNIMOE_WS_SCHEDULE = 1, OMNIMOE_WS_EXPERT = 2, OMNIMOE_WS_LAYER = 3,
-       OMNIMOE_WS_ROUTER_BWD = 4, OMNIMOE_WS_MLP_BWD = 5 };
+       OMNIMOE_WS_ROUTER_BWD = 4, OMNIMOE_WS_MLP_BWD = 5, OMNIMOE_WS_MLP = 6 };
 
 /* How omnimoe_route computes the sub-key logits.  Both give the same bits:
  * logit = RN32(exact dot product x . w) (reading Q9).
@@ -302,13 +302,15 @@ omnimoe_status omnimoe_pack_v(const omnimoe_dims* dims, int64_t n, const void* V
 
 /* Shared dense MLP (SwiGLU without biases, reading Q2) plus
  * combine (Eq.MoE):
- *   H = silu(x W_gate^T) * (x W_up^T)  (bf16 in OMNIMOE_BF16 mode)
+ *   H = silu(x W_gate^T) * (x W_up^T)  (in OMNIMOE_BF16 mode a bf16 pair hi + lo, ~16
+ *                                       significant bits, when d_ff % 64 == 0, else bf16)
  *   y = H W_down^T + y_routed           (y_routed nullable -> treated as 0)
  *   w_gate_up [2*d_ff][d] (gate rows, then up rows), w_down [d][d_ff],
  *   y [L][d] (bf16 or fp32 per dtype). */
 omnimoe_status omnimoe_shared_mlp(const omnimoe_dims* dims, int64_t L, const void* x,
                                   const void* w_gate_up, const void* w_down, const float* y_routed,
                                   void* y, void* ws, size_t ws_bytes, omnimoe_stream_t stream);
+/*   ws: omnimoe_workspace_size(dims, L, OMNIMOE_WS_MLP) bytes (holds H). */
 
 /* The paper's ablation "w/o Expert-Centric Scheduling": the routed
  * branch token by token straight from the routing decision (idx, gate [L][h*K],

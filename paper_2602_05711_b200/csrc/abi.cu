@@ -3,6 +3,7 @@
 // synchronisation, no CPU fallback.
 #include <mutex>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "backward.cuh"
@@ -134,7 +135,11 @@ omnimoe_status validate_dims(const omnimoe_dims* dp) {
   return OMNIMOE_OK;
 }
 
-bool i8_logits(const omnimoe_dims& d) { return d.dtype == OMNIMOE_BF16 && d.router == OMNIMOE_ROUTER_EXACT; }
+// the int8 limb GEMM is exact while every int32 partial sum fits: |digit products| <= 2^14 summed
+// over d terms, so d < 2^16; wider rows take the exact fp64 double-double kernel
+bool i8_logits(const omnimoe_dims& d) {
+  return d.dtype == OMNIMOE_BF16 && d.router == OMNIMOE_ROUTER_EXACT && d.d < 65536;
+}
 
 bool dense_router(const omnimoe_dims& d) { return d.router == OMNIMOE_ROUTER_DENSE; }
 // logits per token-head: N_r + N_c (Cartesian) or N (dense ablation)
@@ -154,6 +159,12 @@ size_t route_ws(const omnimoe_dims& d, int64_t L, void* ws, float** logits, void
 }
 
 size_t elem_size(const omnimoe_dims& d) { return d.dtype == OMNIMOE_BF16 ? 2 : 4; }
+// bf16 mode carries the shared MLP's hidden activations H into GEMM-2 as a bf16 pair
+// [hi | lo] (~16 significant bits; reading Q16) whenever d_ff is a whole number of 64-wide
+// K blocks; otherwise as one bf16 value
+bool h_split(const omnimoe_dims& d) { return d.dtype == OMNIMOE_BF16 && d.d_ff % 64 == 0; }
+int64_t h_cols(const omnimoe_dims& d) { return std::max<int64_t>(d.d_ff, 1) * (h_split(d) ? 2 : 1); }
+size_t h_bytes(const omnimoe_dims& d, int64_t L) { return (size_t)L * h_cols(d) * elem_size(d); }
 
 struct LayerWs {
   void* route_ws;
@@ -198,7 +209,7 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
   // measurement override: pad before the executor's work counters (placement study)
   if (const char* pad = getenv("OMNIMOE_WS_PAD_COUNTERS")) c.take<char>((size_t)atoll(pad));
   void* ew = c.take<char>(layer_uses_dense_executor(d, L) ? dense_expert_ws_bytes(d, L) : expert_ws_bytes(d, L));
-  void* H = c.take<char>((size_t)L * std::max<int64_t>(d.d_ff, 1) * elem_size(d));
+  void* H = c.take<char>(h_bytes(d, L));
   uint32_t* cand = c.take<uint32_t>(dense_router(d) ? 0 : select_cand_ws_bytes(d) / 4);
   if (o) {
     o->cand = cand;
@@ -266,10 +277,12 @@ omnimoe_status mlp_impl(const omnimoe_dims& d, int64_t L, const void* x, const v
   g1.N = (int)d.d_ff;
   g1.K = (int)d.d;
   g1.out = H;
+  g1.h_split = h_split(d);
   GemmArgs g2;
   g2.M = (int)L;
   g2.N = (int)d.d;
-  g2.K = (int)d.d_ff;
+  g2.K = (int)h_cols(d);  // y = [H_hi | H_lo] [W_down | W_down]^T when split
+  g2.b_kwrap = h_split(d) ? (int)d.d_ff : 0;
   g2.out = y;
   g2.addend = y_routed;
   if (d.dtype == OMNIMOE_BF16) {
@@ -317,6 +330,7 @@ omnimoe_status omnimoe_workspace_size(const omnimoe_dims* dims, int64_t L, int w
     case OMNIMOE_WS_LAYER: *bytes = layer_ws(d, L, nullptr, nullptr); break;
     case OMNIMOE_WS_ROUTER_BWD: *bytes = router_bwd_ws_bytes(d, L); break;
     case OMNIMOE_WS_MLP_BWD: *bytes = mlp_bwd_ws_bytes(d, L); break;
+    case OMNIMOE_WS_MLP: *bytes = h_bytes(d, L); break;
     default:
       set_error("unknown workspace selector " + std::to_string(which));
       return OMNIMOE_ERR_INVALID_ARGUMENT;
@@ -474,7 +488,7 @@ omnimoe_status omnimoe_shared_mlp(const omnimoe_dims* dims, int64_t L, const voi
   OMNI_NONNULL(w_down, "w_down");
   OMNI_NONNULL(y, "y");
   OMNI_NONNULL(ws, "ws");
-  const size_t need = (size_t)L * dims->d_ff * elem_size(*dims);
+  const size_t need = h_bytes(*dims, L);
   OMNI_TRY(check_ws(ws_bytes, need, "shared_mlp"));
   OMNI_TRY(check_device());
   return mlp_impl(*dims, L, x, w_gate_up, w_down, y_routed, y, ws, (cudaStream_t)stream);
@@ -731,9 +745,15 @@ omnimoe_status omnimoe_layer_fwd_host(const omnimoe_dims* dims, int64_t L, const
   OMNI_TRY(check_ws(ws_bytes, layer_ws(d, L, nullptr, nullptr), "layer_fwd_host"));
   OMNI_TRY(check_device());
   cudaStream_t st = (cudaStream_t)stream, cs = (cudaStream_t)copy_stream;
-  // per-thread event pool (host resources; no device memory)
-  thread_local std::vector<cudaEvent_t> evs;
-  const size_t need = 2 * (size_t)chunks + 1;
+  // event pool per (thread, device): events belong to the device current when they were created
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    set_error("layer_fwd_host: cudaGetDevice failed");
+    return OMNIMOE_ERR_CUDA;
+  }
+  thread_local std::map<int, std::vector<cudaEvent_t>> pools;
+  std::vector<cudaEvent_t>& evs = pools[dev];
+  const size_t need = 2 * (size_t)chunks + 2;
   while (evs.size() < need) {
     cudaEvent_t e;
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
@@ -748,6 +768,12 @@ omnimoe_status omnimoe_layer_fwd_host(const omnimoe_dims* dims, int64_t L, const
   const int64_t hk = d.n_heads * d.top_k, M = L * hk;
   const int64_t Lc = (((L + chunks - 1) / chunks) + 127) / 128 * 128;  // whole 128-row GEMM tiles
   int n_ch = 0;
+  // 0. the copy stream starts after everything already enqueued on `stream` (earlier work
+  //    may still read x_dev, or the caller's allocator may have just recycled it there)
+  if (cudaEventRecord(evs[2 * chunks + 1], st) != cudaSuccess || cudaStreamWaitEvent(cs, evs[2 * chunks + 1], 0) != cudaSuccess) {
+    set_error("layer_fwd_host: event failed");
+    return OMNIMOE_ERR_CUDA;
+  }
   // 1. copy x chunk by chunk (copy stream) while routing the chunks already copied:
   //    routing is per token and batch-independent, so chunked routing is bit-identical
   for (int64_t l0 = 0; l0 < L; l0 += Lc, ++n_ch) {
@@ -780,6 +806,7 @@ omnimoe_status omnimoe_layer_fwd_host(const omnimoe_dims* dims, int64_t L, const
     g1.N = (int)d.d_ff;
     g1.K = (int)d.d;
     g1.out = w.H;
+    g1.h_split = h_split(d);
     if (d.dtype == OMNIMOE_BF16) OMNI_TRY(gemm_bf16(EPI_SWIGLU, x_dev, w_gate_up, g1, st));
     else OMNI_TRY(gemm_f32(EPI_SWIGLU, static_cast<const float*>(x_dev), static_cast<const float*>(w_gate_up), g1, st));
   }
@@ -791,10 +818,11 @@ omnimoe_status omnimoe_layer_fwd_host(const omnimoe_dims* dims, int64_t L, const
       GemmArgs g2;
       g2.M = (int)n;
       g2.N = (int)d.d;
-      g2.K = (int)d.d_ff;
+      g2.K = (int)h_cols(d);
+      g2.b_kwrap = h_split(d) ? (int)d.d_ff : 0;
       g2.out = yc;
       g2.addend = w.y_routed + l0 * d.d;
-      const void* Hc = static_cast<const char*>(w.H) + l0 * d.d_ff * eb;
+      const void* Hc = static_cast<const char*>(w.H) + l0 * h_cols(d) * eb;
       if (d.dtype == OMNIMOE_BF16) OMNI_TRY(gemm_bf16(EPI_ADD, Hc, w_down, g2, st));
       else OMNI_TRY(gemm_f32(EPI_ADD, static_cast<const float*>(Hc), static_cast<const float*>(w_down), g2, st));
     } else {

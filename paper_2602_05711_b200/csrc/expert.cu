@@ -747,6 +747,7 @@ omnimoe_status launch_group(int d, const void* x, const void* W, const void* V, 
     OMNI_GROUP_CASE(2)
     OMNI_GROUP_CASE(4)
     OMNI_GROUP_CASE(8)
+    OMNI_GROUP_CASE(16)  // fp32 at d = 2048 (all-fp32 mode at the paper's width)
     default:
       if (nv == 3) {
         expert_group_kernel<T, 4><<<kSMs * 4, 256, 0, st>>>(d, X, Wp, Vp, plan.run_offsets, plan.n_runs, m_loc,

@@ -104,8 +104,9 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
         for (int i = 0; i < BN / 64; ++i)
           tma_load_2d(&tmB, &full[s], sB + s * kBBytes + i * (kBBytes / (BN / 64)), nt * BN + 64 * i, kb * BK);
       } else {
-        tma_load_2d(&tmB, &full[s], sB + s * kBBytes, kb * BK, nt * BN);
-        tma_load_2d(&tmB, &full[s], sB + s * kBBytes + kBBytes / 2, kb * BK, nt * BN + BN / 2);
+        const int kB = args.b_kwrap ? (kb * BK) % args.b_kwrap : kb * BK;
+        tma_load_2d(&tmB, &full[s], sB + s * kBBytes, kB, nt * BN);
+        tma_load_2d(&tmB, &full[s], sB + s * kBBytes + kBBytes / 2, kB, nt * BN + BN / 2);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -162,22 +163,33 @@ __global__ void __launch_bounds__(128 + 32 * kEpiWarps, 1)
         tmem_ld32(tbase + BN / 2 + c * 32, u);
         const int col0 = nt * (BN / 2) + c * 32;
         if (!row_ok) continue;
-        __nv_bfloat16* dst = H + (size_t)row * args.N + col0;
+        __nv_bfloat16* dst = H + (size_t)row * (args.h_split ? 2 * args.N : args.N) + col0;
         if (col0 + 32 <= args.N && (args.N % 8) == 0) {
-          uint32_t p[16];
+          uint32_t p[16], pl[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
-            p[i] = pack_bf16x2(silu_f(g0) * __uint_as_float(u[2 * i]),
-                               silu_f(g1) * __uint_as_float(u[2 * i + 1]));
+            const float h0 = silu_f(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
+            const float h1 = silu_f(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+            p[i] = pack_bf16x2(h0, h1);
+            pl[i] = pack_bf16x2(h0 - __uint_as_float(p[i] << 16), h1 - __uint_as_float(p[i] & 0xFFFF0000u));
           }
           uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
           for (int i = 0; i < 4; ++i) d4[i] = make_uint4(p[4 * i], p[4 * i + 1], p[4 * i + 2], p[4 * i + 3]);
+          if (args.h_split) {
+            uint4* l4 = reinterpret_cast<uint4*>(dst + args.N);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) l4[i] = make_uint4(pl[4 * i], pl[4 * i + 1], pl[4 * i + 2], pl[4 * i + 3]);
+          }
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            if (col0 + i < args.N) dst[i] = __float2bfloat16_rn(silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]));
+            if (col0 + i < args.N) {
+              const float h = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
+              const __nv_bfloat16 hi = __float2bfloat16_rn(h);
+              dst[i] = hi;
+              if (args.h_split) dst[args.N + i] = __float2bfloat16_rn(h - __bfloat162float(hi));
+            }
         }
       }
     } else if (EPI == EPI_GATED) {
@@ -336,7 +348,11 @@ omnimoe_status launch_tc(const void* A, const void* B, const GemmArgs& a, cudaSt
     ok = ok && make_map(&mB, B, (uint64_t)(a.b_rows > 0 ? a.b_rows : a.K), a.N, 64);
     mB2 = mB;
   } else {
-    ok = ok && make_map(&mB, B, a.N, a.K, BN / 2);
+    if (a.b_kwrap && (a.b_kwrap % BK != 0 || a.K % a.b_kwrap != 0)) {
+      set_error("gemm: b_kwrap must be a multiple of 64 dividing K");
+      return OMNIMOE_ERR_INVALID_ARGUMENT;
+    }
+    ok = ok && make_map(&mB, B, a.N, a.b_kwrap ? a.b_kwrap : a.K, BN / 2);
     mB2 = mB;
   }
   if (!ok) {

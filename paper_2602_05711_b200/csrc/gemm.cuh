@@ -34,6 +34,12 @@ struct GemmArgs {
   // i.e. C = A . B instead of A . B^T -- no transposed copy (EPI_F32 only)
   int b_mn = 0;
   int64_t b_rows = 0;
+  // EPI_SWIGLU: write H as a bf16 pair, row m = [hi (N) | lo (N)], hi = bf16(h), lo = bf16(h - hi)
+  // (~16 significant bits for the GEMM that contracts it; out row stride 2N)
+  int h_split = 0;
+  // B's K extent when smaller than A's: K block kb of A meets K block kb mod (b_kwrap / 64) of B
+  // (C = [H_hi | H_lo] . [B | B]^T without a duplicated B); b_kwrap % 64 == 0, K % b_kwrap == 0
+  int b_kwrap = 0;
 };
 
 // bf16 operands.  For EPI_SWIGLU, B is w_gate_up [2N][K]: gate rows [0,N), up rows [N,2N).

@@ -406,6 +406,16 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
                             void* ws, cudaStream_t st) {
   const int64_t n_loc = plan.expert_end - plan.expert_begin;
   const int64_t nb = (M + kRadixTile - 1) / kRadixTile;
+  if (B > 1 && M > 0) {  // (token block, group) keys are uint32 with n_keys as the out-of-range sentinel
+    const int64_t L = (M + hk - 1) / hk;
+    const int64_t tb = std::max<int64_t>(1, std::min<int64_t>(Tb, L));
+    const int64_t ngm = (n_loc + B - 1) / B;
+    if (tb * ngm >= (int64_t(1) << 32) - 1) {
+      set_error("schedule: token_blocks (" + std::to_string(tb) + ") x groups (" + std::to_string(ngm) +
+                ") must be < 2^32 - 1");
+      return OMNIMOE_ERR_SHAPE;
+    }
+  }
   Carver c(ws);
   int32_t* cnt = c.take<int32_t>(n_loc + 1);
   int32_t* rank = c.take<int32_t>(n_loc + 1);

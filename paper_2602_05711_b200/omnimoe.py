@@ -23,7 +23,7 @@ V_ROWS, V_SLICED = 0, 1
 ORDER_KEY, ORDER_CANDIDATE = 0, 1
 ROUTER_EXACT, ROUTER_EXACT_F64, ROUTER_DENSE = 0, 1, 2
 LOGITS_ROUTE, LOGITS_EXACT_F64, LOGITS_BF16_FAST = 0, 1, 2
-WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER, WS_ROUTER_BWD, WS_MLP_BWD = 0, 1, 2, 3, 4, 5
+WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER, WS_ROUTER_BWD, WS_MLP_BWD, WS_MLP = 0, 1, 2, 3, 4, 5, 6
 
 
 class OmniMoEError(RuntimeError):
@@ -459,8 +459,7 @@ def shared_mlp(dims: LayerDims, x, w_gate_up, w_down, y_routed=None, y=None, ws=
     if y_routed is not None:
         _req(y_routed, "y_routed", torch.float32, L * dims.d)
     y = y if y is not None else torch.empty((L, dims.d), dtype=dims.torch_dtype, device=x.device)
-    ws = ws if ws is not None else torch.empty(max(L * dims.d_ff * (2 if dims.dtype == BF16 else 4), 1),
-                                               dtype=torch.uint8, device=x.device)
+    ws = ws if ws is not None else workspace(dims, L, WS_MLP, x.device)
     dc = dims.c()
     _check(load().omnimoe_shared_mlp(ctypes.byref(dc), L, _ptr(x), _ptr(w_gate_up), _ptr(w_down),
                                      _ptr(y_routed), _ptr(y), _ptr(ws), ws.numel(), _stream()),

@@ -111,3 +111,44 @@ def default_exponents(d: int, d_ff: int, mode: int = NORMAL) -> dict:
         TID_W_GATE_UP: scale_exponent(1.0 / math.sqrt(d)),
         TID_W_DOWN: scale_exponent(1.0 / math.sqrt(max(d_ff, 1))),
     }
+
+
+# ---------------------------------------------------------------- C host twin (speed only)
+_HOST_SO = None
+
+
+def build_host(force: bool = False) -> str:
+    """Compile synth/synth_host.c (gcc, no CUDA) into synth/libsynth_host.so."""
+    import os
+    import subprocess
+    here = os.path.dirname(os.path.abspath(__file__))
+    src, so = os.path.join(here, "synth_host.c"), os.path.join(here, "libsynth_host.so")
+    if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-o", so, src, "-lm"])
+    return so
+
+
+def _host_lib():
+    global _HOST_SO
+    if _HOST_SO is None:
+        import ctypes
+        lib = ctypes.CDLL(build_host())
+        P = ctypes.c_void_p
+        lib.synth_rows_f64.argtypes = [ctypes.c_uint64, ctypes.c_uint64, P, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int]
+        lib.synth_rows_f64.restype = None
+        _HOST_SO = lib
+    return _HOST_SO
+
+
+def rows_f64(seed, tensor_id, rows, ncols, e, mode=NORMAL, bf16=True, nthreads=None) -> np.ndarray:
+    """Decoded (exact float64) rows of a [*, ncols] tensor stored as bf16 (or fp32),
+    computed by the C twin; identical to bf16_bits_to_f64(gen_rows_bf16_bits(...))
+    (resp. gen_rows_f32(...).astype(float64))."""
+    import os
+    rows = np.ascontiguousarray(rows, dtype=np.int64).reshape(-1)
+    out = np.empty((len(rows), ncols), dtype=np.float64)
+    if len(rows) and ncols:
+        _host_lib().synth_rows_f64(seed, tensor_id, rows.ctypes.data, len(rows), ncols, e, mode, int(bf16),
+                                   out.ctypes.data, nthreads or os.cpu_count() or 1)
+    return out

@@ -22,10 +22,8 @@ def host_rows(dims, seed, name, rows=None, mode=synth.NORMAL):
     }[name]
     if rows is None:
         rows = np.arange(nrows)
-    if dims.dtype == 0:
-        b = synth.gen_rows_bf16_bits(seed, tid, rows, ncols, ex[tid], mode)
-        return synth.bf16_bits_to_f64(b)
-    return synth.gen_rows_f32(seed, tid, rows, ncols, ex[tid], mode).astype(np.float64)
+    # the C twin of the generator (bit-identical to the numpy one: tests/test_synth.py::test_c_twin_matches_numpy)
+    return synth.rows_f64(seed, tid, rows, ncols, ex[tid], mode, bf16=dims.dtype == 0)
 
 
 def oracle_keys(logit_rows, n_rows, n_cols, ids):
@@ -60,6 +58,29 @@ def compare_routing(gpu_idx, gpu_gate, orc, logit_rows, n_rows, n_cols, allow_ga
         else:
             disallowed += 1
     return dict(mismatch=mism, allowed=allowed, disallowed=disallowed, gate_err=gate_err)
+
+
+def routing_counts(gpu_idx, gpu_gate, orc, logit_rows, n_rows, n_cols, allow_gap=1e-6):
+    """compare_routing for whole batches: set equality is checked vectorised, the
+    Q10 allowance only on the token-heads whose sets differ; the gate error is
+    taken over all token-heads with equal sets."""
+    gi = np.asarray(gpu_idx).reshape(orc["idx"].shape)
+    gg = np.asarray(gpu_gate).reshape(orc["idx"].shape)
+    og = np.argsort(gi, -1, kind="stable")
+    oo = np.argsort(orc["idx"], -1, kind="stable")
+    gs, os_ = np.take_along_axis(gi, og, -1), np.take_along_axis(orc["idx"], oo, -1)
+    same = np.all(gs == os_, -1)
+    gate_err = 0.0
+    if same.any():
+        d = np.abs(np.take_along_axis(gg, og, -1) - np.take_along_axis(orc["gate"], oo, -1))[same]
+        gate_err = float(d.max())
+    bad = np.flatnonzero(~same)
+    r = dict(mismatch=0, allowed=0, disallowed=0, gate_err=gate_err, token_heads=int(gi.shape[0]))
+    if len(bad):
+        sub = {k: orc[k][bad] for k in ("idx", "gate", "key_hi", "key_lo")}
+        c = compare_routing(gi[bad], gg[bad], sub, logit_rows[bad], n_rows, n_cols, allow_gap)
+        r.update(mismatch=c["mismatch"], allowed=c["allowed"], disallowed=c["disallowed"])
+    return r
 
 
 def rel_errors(y, ref):

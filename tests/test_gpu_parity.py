@@ -222,6 +222,18 @@ def test_schedule_bit_exact(N, L, HK, b, e, B, Tb):
                 np.repeat(np.arange(L), HK).astype(np.int32), b, e, B, tpb)
 
 
+def test_schedule_rejects_key_overflow():
+    """(token block, group) keys are uint32: token_blocks x ceil(n_loc / B) must stay
+    below 2^32 - 1 or the call fails before launching anything."""
+    L, N = 16384, 1 << 20
+    d = om.LayerDims(d=8, n_rows=N, n_cols=1, top_k=1, d_ff=0, group_size=2, token_blocks=L)
+    ids = torch.zeros(L, dtype=torch.int32, device="cuda")
+    with pytest.raises(om.OmniMoEError, match="SHAPE"):
+        om.schedule(d, ids, torch.ones(L, device="cuda"))
+    d2 = om.LayerDims(d=8, n_rows=N, n_cols=1, top_k=1, d_ff=0, group_size=2, token_blocks=4096)
+    om.schedule(d2, ids, torch.ones(L, device="cuda"))  # 4096 x 2^19 = 2^31: fits
+
+
 @pytest.mark.parametrize("B", [1, 64])
 def test_schedule_all_same_expert_and_empty(B):
     d = om.LayerDims(d=8, n_rows=64, n_cols=64, top_k=4, d_ff=0, group_size=B)
@@ -242,8 +254,6 @@ def test_schedule_all_same_expert_and_empty(B):
 @pytest.mark.parametrize("dtype", [om.BF16, om.F32])
 @pytest.mark.parametrize("d,act", [(64, om.SILU), (72, om.SILU), (1024, om.SILU), (2048, om.SILU), (64, om.IDENTITY)])
 def test_expert_fwd_given_plan(dtype, d, act, B):
-    if dtype == om.F32 and abs(B) > 1 and d > 1024:
-        pytest.skip("grouped kernel holds d/128 fp32 vectors per lane: d <= 1024 in fp32 mode")
     rng = np.random.default_rng(d)
     L, N, HK = 200, 3000, 12
     # B < 0: group size |B| scheduled in 3 token blocks
@@ -272,7 +282,7 @@ def test_expert_fwd_given_plan(dtype, d, act, B):
 
 # ---------------------------------------------------------------- shared MLP
 @pytest.mark.parametrize("dtype", [om.BF16, om.F32])
-@pytest.mark.parametrize("L,d,dff", [(256, 64, 128), (300, 1024, 1024), (130, 256, 72)])
+@pytest.mark.parametrize("L,d,dff", [(256, 64, 128), (300, 1024, 1024), (130, 256, 72), (2048, 2048, 2048)])
 def test_shared_mlp(dtype, L, d, dff):
     dims = om.LayerDims(d=d, n_rows=2, n_cols=2, top_k=1, d_ff=dff, dtype=dtype)
     inp = make_inputs(dims, L, 11, skip=("subkeys", "W", "V"))
@@ -284,6 +294,10 @@ def test_shared_mlp(dtype, L, d, dff):
     e_tok, e_elt = rel_errors(y.float().cpu().numpy(), ref)
     tol = 1e-5 if dtype == om.F32 else 1e-2
     assert e_tok <= tol and e_elt <= tol, (e_tok, e_elt)
+    if dtype == om.BF16 and dff % 64 == 0:
+        # H enters GEMM-2 as a bf16 hi + lo pair: what is left is y's own bf16 rounding
+        # (<= 2^-8 relative) plus fp32 accumulation
+        assert e_elt <= 4.5e-3, e_elt
 
 
 # ---------------------------------------------------------------- whole layer
@@ -538,7 +552,9 @@ def test_route_candidate_order(name, L):
     np.testing.assert_array_equal(np.take_along_axis(a, oa, -1), np.take_along_axis(b, ob, -1))
     # scores = key - lse_r - lse_c: the two kernels sum a half's exp terms in different
     # orders (fp32, 2048 terms at C5), so scores get the oracle protocol's 1e-4
-    for x_, y_, tol in [(ga, gb, 1e-6), (sa, sb, 1e-4)]:
+    # (1e-6 wherever the halves are at most 1024 keys, which holds for all but C5)
+    stol = 1e-4 if name == "C5" else 1e-6
+    for x_, y_, tol in [(ga, gb, 1e-6), (sa, sb, stol)]:
         x_, y_ = x_.cpu().numpy().reshape(-1, K), y_.cpu().numpy().reshape(-1, K)
         np.testing.assert_allclose(np.take_along_axis(x_, oa, -1), np.take_along_axis(y_, ob, -1), atol=tol)
 
