@@ -574,6 +574,8 @@ def main():
     ap.add_argument("--expert-kernel", default="auto", choices=["auto", "token", "warp"],
                     help="a6 executor: auto (grouped ECS), token (the paper's 'w/o ECS' ablation), "
                          "warp (expert-major, B = 1)")
+    ap.add_argument("--v-band-mb", type=float, default=0.0,
+                    help="SLICED pass V: L2 budget of one band step (dims.v_band_bytes; 0 = library choice)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
     if args.impl == "reference":
@@ -595,7 +597,8 @@ def main():
     dense_rows = om.layer_executor(w.dims, w.L) == om.EXPERT_DENSE
     sliced = args.expert_kernel == "auto" and (args.v_layout == "sliced" or
                                                (args.v_layout == "auto" and 2.0 <= eta <= 32.0 and not dense_rows))
-    w = configs.get(args.config, v_layout=om.V_SLICED if sliced else om.V_ROWS)
+    w = configs.get(args.config, v_layout=om.V_SLICED if sliced else om.V_ROWS,
+                    v_band_bytes=int(args.v_band_mb * (1 << 20)))
     if args.expert_kernel != "auto":
         ek = {"token": om.EXPERT_TOKEN, "warp": om.EXPERT_WARP}[args.expert_kernel]
         w = configs.get(args.config, expert_kernel=ek, group_size=1 if ek == om.EXPERT_WARP else 0)

@@ -104,6 +104,10 @@ enum { OMNIMOE_ROUTER_EXACT = 0, OMNIMOE_ROUTER_EXACT_F64 = 1, OMNIMOE_ROUTER_DE
  *              exact key desc, id asc -- Eq.TopK's ranking) or CANDIDATE (the order
  *              of the Cartesian candidates, row rank then column rank: same set and
  *              gates, no final sort; what omnimoe_layer_fwd uses internally).
+ *   v_band_bytes  SLICED pass V: L2 budget of what one pass-V step keeps resident
+ *              (one expert band's part of a 32-column slice of V); 0 = library
+ *              choice (68 MB).  Determines n_b
+ *              (omnimoe_v_bands).  Performance only: results do not depend on it.
  */
 enum { OMNIMOE_ORDER_KEY = 0, OMNIMOE_ORDER_CANDIDATE = 1 };
 typedef struct {
@@ -119,6 +123,8 @@ typedef struct {
                           * 0 = library choice */
   int32_t v_layout;      /* OMNIMOE_V_ROWS | OMNIMOE_V_SLICED */
   int32_t route_order;   /* omnimoe_route output order: OMNIMOE_ORDER_KEY | OMNIMOE_ORDER_CANDIDATE */
+  int64_t v_band_bytes;  /* >= 0 */
+  int64_t reserved;      /* must be 0 */
 } omnimoe_dims;
 
 /* Expert-centric plan for the local expert range [expert_begin, expert_end)
@@ -141,7 +147,9 @@ typedef struct {
  * V-order arrays (nullable; required by the SLICED executor; tasks must be
  * sorted by token, which the default token = t / (h*K) is).  The V order sorts
  * the tasks by (token, band) stably, band = local expert id / ceil(n_loc / n_b)
- * with n_b = omnimoe_v_bands(dims, n_loc) (band n_b: outside the range; with
+ * with n_b = omnimoe_v_bands(dims, n_loc, n_tok), n_tok = n_tokens if > 0, else
+ * ceil(M / (h*K)) in omnimoe_schedule and L in omnimoe_expert_fwd -- the two must
+ * agree (they do for the default token = t / (h*K)) (band n_b: outside the range; with
  * n_b = 1 the V order is the task order and out-of-range tasks stay in segment
  * (l, 0) with expert -1):
  *   sorted_task     int32[M]        V-order position of each plan position's task
@@ -176,10 +184,11 @@ typedef struct {
  * 64 MB of W/V rows, in bf16 mode; 1 in fp32 mode).  Returns 0 on invalid dims. */
 int64_t omnimoe_group_size(const omnimoe_dims* dims);
 /* Number of expert bands n_b of the SLICED executor's pass V for a local expert
- * range of n_loc rows: the V rows of one band and one 32-column slice (64 bytes
- * each) are kept near 32 MB so that they stay L2-resident while every token uses
- * them.  1 for the ROWS layout; 0 on invalid dims. */
-int64_t omnimoe_v_bands(const omnimoe_dims* dims, int64_t n_loc);
+ * range of n_loc rows and n_tok tokens: pass V sweeps the 32-column slices of V one
+ * band at a time; the band's part of a slice (64 bytes per expert) is kept within
+ * dims.v_band_bytes (68 MB) so that it stays L2-resident while every token uses it
+ * (DESIGN.md §4.4).  Independent of dims.v_layout; 0 on invalid dims. */
+int64_t omnimoe_v_bands(const omnimoe_dims* dims, int64_t n_loc, int64_t n_tok);
 /* The number of token blocks T_b omnimoe_schedule uses for a batch of L tokens
  * (dims.token_blocks if > 0, else 1; always 1 for B = 1).  Block b holds tokens
  * [b*ceil(L/T_b), (b+1)*ceil(L/T_b)); the plan sorts by (block, q, token). */

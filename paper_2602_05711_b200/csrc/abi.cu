@@ -90,6 +90,10 @@ omnimoe_status validate_dims(const omnimoe_dims* dp) {
     set_error("group_size and token_blocks must be >= 0");
     return OMNIMOE_ERR_INVALID_ARGUMENT;
   }
+  if (d.v_band_bytes < 0 || d.reserved != 0) {
+    set_error("v_band_bytes must be >= 0 and reserved 0 " + dims_str(d));
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
   if (d.route_order != OMNIMOE_ORDER_KEY && d.route_order != OMNIMOE_ORDER_CANDIDATE) {
     set_error("unknown route order " + std::to_string(d.route_order));
     return OMNIMOE_ERR_UNSUPPORTED;
@@ -202,7 +206,7 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
   const bool sliced = d.v_layout == OMNIMOE_V_SLICED;
   int32_t* stask = sliced ? c.take<int32_t>((size_t)std::max<int64_t>(M, 1)) : nullptr;
   int32_t* tpair = sliced ? c.take<int32_t>(2 * (size_t)std::max<int64_t>(M, 1)) : nullptr;
-  int32_t* toff = sliced ? c.take<int32_t>((size_t)L * (resolve_v_bands(d, N) + 1) + 1) : nullptr;
+  int32_t* toff = sliced ? c.take<int32_t>((size_t)L * (resolve_v_bands(d, N, L) + 1) + 1) : nullptr;
   const size_t sb = schedule_ws_bytes(M, N);
   void* sw = c.take<char>(sb);
   float* yr = c.take<float>((size_t)L * d.d);
@@ -400,9 +404,9 @@ omnimoe_status omnimoe_schedule(const omnimoe_dims* dims, int64_t M, const int32
   OMNI_TRY(check_ws(ws_bytes, schedule_ws_bytes(M, n_loc), "schedule"));
   OMNI_TRY(check_device());
   const int64_t hk = dims->n_heads * dims->top_k;
+  const int64_t n_tok = plan->n_tokens > 0 ? plan->n_tokens : (M + hk - 1) / hk;
   return schedule_run(M, idx, gate, token, hk, *plan, B, resolve_token_blocks(*dims, (M + hk - 1) / hk),
-                      resolve_v_bands(*dims, n_loc), ws,
-                      (cudaStream_t)stream);
+                      resolve_v_bands(*dims, n_loc, std::max<int64_t>(n_tok, 1)), ws, (cudaStream_t)stream);
 }
 
 }  // extern "C"
@@ -534,7 +538,7 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
     OMNI_TRY(dense_expert_run(d, L, x, W, V, idx, gate, w.y_routed, w.expert_ws, st));
   } else {
     OMNI_TRY(schedule_run(M, idx, gate, nullptr, d.n_heads * d.top_k, w.plan, resolve_group_size(d),
-                          resolve_token_blocks(d, L), resolve_v_bands(d, d.n_rows * d.n_cols), w.sched_ws, st));
+                          resolve_token_blocks(d, L), resolve_v_bands(d, d.n_rows * d.n_cols, L), w.sched_ws, st));
     OMNI_TRY(expert_run(d, L, x, W, V, w.plan, w.y_routed, 0, w.expert_ws, st));
   }
   if (d.d_ff > 0) {
@@ -625,10 +629,6 @@ omnimoe_status omnimoe_expert_bwd(const omnimoe_dims* dims, int64_t L, const voi
   if (resolve_group_size(d) != 1 && d.group_size != 1) {
     set_error("expert_bwd: needs the expert-major plan (group_size 1 or the SLICED layout)");
     return OMNIMOE_ERR_INVALID_ARGUMENT;
-  }
-  if (resolve_v_bands(ds, plan->expert_end - plan->expert_begin) != 1) {
-    set_error("expert_bwd: one expert band only (64 * n_loc bytes <= the band size)");
-    return OMNIMOE_ERR_UNSUPPORTED;
   }
   OMNI_TRY(check_ws(ws_bytes, expert_ws_bytes(d, L), "expert_bwd"));
   OMNI_TRY(check_device());
@@ -795,7 +795,7 @@ omnimoe_status omnimoe_layer_fwd_host(const omnimoe_dims* dims, int64_t L, const
     OMNI_TRY(dense_expert_run(d, L, x_dev, W, V, w.idx, w.gate, w.y_routed, w.expert_ws, st));
   } else {
     OMNI_TRY(schedule_run(M, w.idx, w.gate, nullptr, hk, w.plan, resolve_group_size(d), resolve_token_blocks(d, L),
-                          resolve_v_bands(d, d.n_rows * d.n_cols), w.sched_ws, st));
+                          resolve_v_bands(d, d.n_rows * d.n_cols, L), w.sched_ws, st));
     OMNI_TRY(expert_run(d, L, x_dev, W, V, w.plan, w.y_routed, 0, w.expert_ws, st));
   }
   // 3. shared MLP: GEMM-1 whole, GEMM-2 (+ combine) chunk by chunk, each chunk of y copied
@@ -1002,9 +1002,9 @@ int64_t omnimoe_group_size(const omnimoe_dims* dims) {
   return resolve_group_size(*dims);
 }
 
-int64_t omnimoe_v_bands(const omnimoe_dims* dims, int64_t n_loc) {
-  if (validate_dims(dims) != OMNIMOE_OK || n_loc < 1) return 0;
-  return resolve_v_bands(*dims, n_loc);
+int64_t omnimoe_v_bands(const omnimoe_dims* dims, int64_t n_loc, int64_t n_tok) {
+  if (validate_dims(dims) != OMNIMOE_OK || n_loc < 1 || n_tok < 1) return 0;
+  return resolve_v_bands(*dims, n_loc, n_tok);
 }
 
 int64_t omnimoe_token_blocks(const omnimoe_dims* dims, int64_t L) {

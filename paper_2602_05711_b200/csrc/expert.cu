@@ -15,6 +15,7 @@
 //                       warps in flight cover a window of ~1 group whose rows
 //                       stay L2-resident after one HBM read), then ONE red.v4
 //                       scatter per run instead of one per task.
+#include <cmath>
 #include <cstdlib>
 #include <string>
 
@@ -917,7 +918,8 @@ __device__ __forceinline__ int2 ld_pair(const int32_t* p, uint64_t pol) {
 // column quad c4 = lane%4): 8 tasks per load instruction, 8 bf16 columns per lane.
 // The (expert, a) pairs of the next 64 tasks -- possibly of the next item, which
 // is claimed one item ahead -- are loaded while the current 64 are processed.
-__global__ void __launch_bounds__(256)
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB)
     expert_vslice_kernel(int d, int64_t L, int64_t n_loc, const int32_t* __restrict__ seg, int seg_stride,
                          int band, int64_t n_tok, const int32_t* __restrict__ task_pair,
                          const __nv_bfloat16* __restrict__ Vs, float* __restrict__ y, int accumulate,
@@ -1099,8 +1101,8 @@ __global__ void pack_v_kernel(const uint4* __restrict__ V, uint4* __restrict__ V
 // order) and walks the expert's tasks: x_l gathered from L2 (x is the only
 // reused operand: 2dL bytes), a_t = g * sigma(x_l . w_e) -> task_pair[t][1].  Two
 // tasks' x rows are in flight per warp.
-template <int NV>
-__global__ void __launch_bounds__(256)
+template <int NV, int MINB, int T>
+__global__ void __launch_bounds__(256, MINB)
     expert_zdot_kernel(int d, const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ W,
                        const int32_t* __restrict__ offsets, const int32_t* __restrict__ active,
                        const int32_t* __restrict__ n_active, const int32_t* __restrict__ stok,
@@ -1131,38 +1133,40 @@ __global__ void __launch_bounds__(256)
       const int t_l = pl < end ? stask[pl] : 0;
       const int cnt = min(32, end - p0);
       float my_a = 0.f;
-      for (int t = 0; t < cnt; t += 2) {
-        const int t1 = min(t + 1, cnt - 1);
-        const int l0 = __shfl_sync(0xffffffffu, l_l, t), l1 = __shfl_sync(0xffffffffu, l_l, t1);
-        const float g0 = __shfl_sync(0xffffffffu, g_l, t), g1 = __shfl_sync(0xffffffffu, g_l, t1);
-        uint4 a[NV], b[NV];
+      for (int t = 0; t < cnt; t += T) {  // T tasks' x rows in flight per warp
+        int lt[T];
+        uint4 xr[T][NV];
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-          const int c = (j * 32 + lane) * 8;
-          a[j] = c < d ? ld_vec_hint(x + (size_t)l0 * d + c, xpol) : make_uint4(0, 0, 0, 0);
-          b[j] = c < d ? ld_vec_hint(x + (size_t)l1 * d + c, xpol) : make_uint4(0, 0, 0, 0);
-        }
-        float z0 = 0.f, z1 = 0.f;
+        for (int u = 0; u < T; ++u) {
+          lt[u] = __shfl_sync(0xffffffffu, l_l, min(t + u, cnt - 1));
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-          float u = dot2_bf16(0.f, wv[j].x, a[j].x);
-          u = dot2_bf16(u, wv[j].y, a[j].y);
-          u = dot2_bf16(u, wv[j].z, a[j].z);
-          z0 += dot2_bf16(u, wv[j].w, a[j].w);
-          float v = dot2_bf16(0.f, wv[j].x, b[j].x);
-          v = dot2_bf16(v, wv[j].y, b[j].y);
-          v = dot2_bf16(v, wv[j].z, b[j].z);
-          z1 += dot2_bf16(v, wv[j].w, b[j].w);
+          for (int j = 0; j < NV; ++j) {
+            const int c = (j * 32 + lane) * 8;
+            xr[u][j] = c < d ? ld_vec_hint(x + (size_t)lt[u] * d + c, xpol) : make_uint4(0, 0, 0, 0);
+          }
+        }
+        float z[T];
+#pragma unroll
+        for (int u = 0; u < T; ++u) {
+          z[u] = 0.f;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            float q = dot2_bf16(0.f, wv[j].x, xr[u][j].x);
+            q = dot2_bf16(q, wv[j].y, xr[u][j].y);
+            q = dot2_bf16(q, wv[j].z, xr[u][j].z);
+            z[u] += dot2_bf16(q, wv[j].w, xr[u][j].w);
+          }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          z0 += __shfl_xor_sync(0xffffffffu, z0, o);
-          z1 += __shfl_xor_sync(0xffffffffu, z1, o);
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int u = 0; u < T; ++u) z[u] += __shfl_xor_sync(0xffffffffu, z[u], o);
+#pragma unroll
+        for (int u = 0; u < T; ++u) {
+          const float g = __shfl_sync(0xffffffffu, g_l, min(t + u, cnt - 1));
+          const float a = g * (act == OMNIMOE_IDENTITY ? z[u] : silu_f(z[u]));
+          if (lane == t + u) my_a = a;
         }
-        const float a0 = g0 * (act == OMNIMOE_IDENTITY ? z0 : silu_f(z0));
-        const float a1 = g1 * (act == OMNIMOE_IDENTITY ? z1 : silu_f(z1));
-        if (lane == t) my_a = a0;
-        if (lane == t + 1) my_a = a1;
       }
       if (lane < cnt) task_pair[2 * (size_t)t_l + 1] = __float_as_int(my_a);
     }
@@ -1173,12 +1177,17 @@ __global__ void __launch_bounds__(256)
 template <int NV>
 omnimoe_status launch_zdot(int d, const void* x, const void* W, const omnimoe_plan& plan, int act, int* work,
                            cudaStream_t st) {
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_zdot_kernel<NV>, 256, 0);
-  expert_zdot_kernel<NV><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(
-      d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W), plan.expert_offsets,
-      plan.active, plan.n_active, plan.sorted_token, plan.sorted_gate, plan.sorted_task, plan.task_pair, act, work,
-      env_int("OMNIMOE_W_HINT", 1), env_int("OMNIMOE_X_HINT", 0));
+  auto go = [&](auto kern) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+    kern<<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(
+        d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W), plan.expert_offsets,
+        plan.active, plan.n_active, plan.sorted_token, plan.sorted_gate, plan.sorted_task, plan.task_pair, act, work,
+        env_int("OMNIMOE_W_HINT", 1), env_int("OMNIMOE_X_HINT", 0));
+  };
+  // 80 registers (3 CTAs per SM) with two x rows in flight per warp: pass Z 3.27 -> 2.25 ms at
+  // C3a against 64 registers / 4 CTAs (profiles/r2/occupancy/); 2 CTAs or 4 rows in flight: no gain
+  go(expert_zdot_kernel<NV, 3, 2>);
   OMNI_CHECK_LAUNCH("expert_zdot_kernel");
   return OMNIMOE_OK;
 }
@@ -1331,7 +1340,7 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
-size_t expert_ws_bytes(const omnimoe_dims&, int64_t) { return 256; }  // work counter
+size_t expert_ws_bytes(const omnimoe_dims&, int64_t) { return 256; }  // work counters
 
 omnimoe_status expert_token_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* V,
                                 const int32_t* idx, const float* gate, int64_t begin, int64_t end, float* y,
@@ -1390,13 +1399,18 @@ bool layer_uses_token_executor(const omnimoe_dims& d, int64_t L) {
          d.d % 256 == 0 && d.d <= 2048 && expected_eta(d, L) < env_int("OMNIMOE_TOKEN_ETA_X100", 200) / 100.0;
 }
 
-int64_t resolve_v_bands(const omnimoe_dims& d, int64_t n_loc) {
-  if (d.v_layout != OMNIMOE_V_SLICED || n_loc < 1) return 1;
-  // one band x one 32-column slice of V = 64 bytes per expert row, kept <= 64 MB:
-  // at C3a (67 MB per slice) 1 and 2 bands run equally fast (pass V is bound by L2
-  // throughput either way), 4 bands are slower (profiles/r1/README.md)
-  const int64_t target = (int64_t)std::max(1, env_int("OMNIMOE_V_BAND_KB", 68 << 10)) << 10;
-  return std::max<int64_t>(1, std::min<int64_t>(32, (n_loc * 64 + target - 1) / target));
+// pass V geometry: pass V sweeps the 32-column slices of V one band of
+// experts at a time (one launch per band, item order (slice, token) inside it); the
+// band's part of a slice (64 bytes per expert) is kept within dims.v_band_bytes (68 MB
+// of the 126 MB L2) so that it stays resident while every token uses it.  More bands
+// than that measured slower (C3a: 1 band 3.45 ms, 2 bands 3.50, 4 bands 5.16; C5: 4
+// bands beat 8 -- profiles/r2/bands/): every band multiplies the (slice, token) items
+// and their fixed costs, and bands > 0 re-read the output rows.
+int64_t resolve_v_bands(const omnimoe_dims& d, int64_t n_loc, int64_t n_tok) {
+  (void)n_tok;
+  if (n_loc < 1) return 1;
+  const int64_t budget = d.v_band_bytes > 0 ? d.v_band_bytes : (68ll << 20);
+  return std::max<int64_t>(1, std::min<int64_t>(30, (64 * n_loc + budget - 1) / budget));
 }
 
 int64_t resolve_token_blocks(const omnimoe_dims& d, int64_t L) {
@@ -1443,11 +1457,13 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
   }
   OMNI_TRY(s);
   if (!(passes & 2)) return OMNIMOE_OK;
+  // 64 registers, 4 CTAs per SM (48 / 5: 3.46 ms at C3a, 64 / 4: 3.36, 78 / 3: 3.48; profiles/r2/occupancy/)
+  auto vkern = expert_vslice_kernel<4>;
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_vslice_kernel, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vkern, 256, 0);
   per_sm = std::max(1, std::min(per_sm, env_int("OMNIMOE_V_BLOCKS", per_sm)));
   const int64_t n_tok = plan.n_tokens > 0 ? plan.n_tokens : L;
-  const int nb = (int)resolve_v_bands(dm, n_loc);
+  const int nb = (int)resolve_v_bands(dm, n_loc, std::max<int64_t>(n_tok, 1));
   // one launch per expert band: its slices of V stay L2-resident while all tokens
   // use them; band b > 0 adds to the slices band b - 1 wrote (stream order: the
   // summation order is fixed, the result bitwise deterministic)
@@ -1462,7 +1478,7 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
           y, b > 0 ? 1 : accumulate, env_int("OMNIMOE_V_HINT", 1), work + 1 + b);
       OMNI_CHECK_LAUNCH("expert_vslice_group_kernel");
     } else {
-      expert_vslice_kernel<<<kSMs * per_sm, 256, 0, st>>>(
+      vkern<<<kSMs * per_sm, 256, 0, st>>>(
           d, L, n_loc, plan.token_offsets, nb + 1, b, n_tok, plan.task_pair, static_cast<const __nv_bfloat16*>(Vs),
           y, b > 0 ? 1 : accumulate, work + 1 + b, env_int("OMNIMOE_V_HINT", 1));
       OMNI_CHECK_LAUNCH("expert_vslice_kernel");

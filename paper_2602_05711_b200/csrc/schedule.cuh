@@ -19,7 +19,8 @@ omnimoe_status expert_token_run(const omnimoe_dims& dm, int64_t L, const void* x
                                 const int32_t* idx, const float* gate, int64_t begin, int64_t end, float* y,
                                 int accumulate, cudaStream_t st);
 int64_t resolve_token_blocks(const omnimoe_dims& d, int64_t L);
-int64_t resolve_v_bands(const omnimoe_dims& d, int64_t n_loc);
+// SLICED pass V: n_b expert bands for n_loc local experts and n_tok tokens
+int64_t resolve_v_bands(const omnimoe_dims& d, int64_t n_loc, int64_t n_tok);
 // eta = M / E|E_active| under uniform routing: tasks per active expert
 double expected_eta(const omnimoe_dims& d, int64_t L);
 // layer_fwd runs the token-centric executor (no schedule): the "w/o ECS" ablation, or
@@ -39,7 +40,7 @@ size_t expert_ws_bytes(const omnimoe_dims& d, int64_t L);
 omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* Vs,
                                  const omnimoe_plan& plan, float* y, int accumulate, void* ws, cudaStream_t st,
                                  int passes);
-// N2: routed-branch backward (expert-major plan, one band)
+// N2: routed-branch backward (expert-major plan)
 omnimoe_status expert_bwd_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* V,
                               const void* Ws, const omnimoe_plan& plan, const void* dy, float* dx, float* dW_act,
                               float* dV_act, float* dgate, int accumulate_dx, void* ws, cudaStream_t st);

@@ -35,7 +35,8 @@ class Dims(ctypes.Structure):
                 ("top_k", ctypes.c_int64), ("n_heads", ctypes.c_int64), ("d_ff", ctypes.c_int64),
                 ("dtype", ctypes.c_int32), ("act", ctypes.c_int32), ("router", ctypes.c_int32),
                 ("expert_kernel", ctypes.c_int32), ("group_size", ctypes.c_int64),
-                ("token_blocks", ctypes.c_int64), ("v_layout", ctypes.c_int32), ("route_order", ctypes.c_int32)]
+                ("token_blocks", ctypes.c_int64), ("v_layout", ctypes.c_int32), ("route_order", ctypes.c_int32),
+                ("v_band_bytes", ctypes.c_int64), ("reserved", ctypes.c_int64)]
 
 
 class Plan(ctypes.Structure):
@@ -107,7 +108,7 @@ def load(path: str = LIB_PATH):
     lib.omnimoe_layer_executor.restype = ctypes.c_int32
     lib.omnimoe_load_stats_workspace_size.restype = ctypes.c_size_t
     lib.omnimoe_load_stats_workspace_size.argtypes = []
-    lib.omnimoe_v_bands.argtypes = [PD, ctypes.c_int64]
+    lib.omnimoe_v_bands.argtypes = [PD, ctypes.c_int64, ctypes.c_int64]
     lib.omnimoe_v_bands.restype = ctypes.c_int64
     lib.omnimoe_token_blocks.argtypes = [PD, ctypes.c_int64]
     lib.omnimoe_token_blocks.restype = ctypes.c_int64
@@ -150,6 +151,7 @@ class LayerDims:
     token_blocks: int = 0
     v_layout: int = V_ROWS
     route_order: int = ORDER_KEY
+    v_band_bytes: int = 0
 
     @property
     def N(self) -> int:
@@ -168,7 +170,7 @@ class LayerDims:
     def c(self) -> Dims:
         return Dims(self.d, self.n_rows, self.n_cols, self.top_k, self.n_heads, self.d_ff,
                     self.dtype, self.act, self.router, self.expert_kernel, self.group_size,
-                    self.token_blocks, self.v_layout, self.route_order)
+                    self.token_blocks, self.v_layout, self.route_order, self.v_band_bytes, 0)
 
 
 def _ptr(t):
@@ -232,16 +234,17 @@ def token_blocks(dims: LayerDims, L: int) -> int:
     return int(load().omnimoe_token_blocks(ctypes.byref(dc), L))
 
 
-def v_bands(dims: LayerDims, n_loc: int) -> int:
-    """Expert bands of the SLICED executor's pass V for n_loc local experts."""
+def v_bands(dims: LayerDims, n_loc: int, n_tok: int) -> int:
+    """Expert bands of the SLICED executor's pass V for n_loc local experts and n_tok tokens."""
     dc = dims.c()
-    return int(load().omnimoe_v_bands(ctypes.byref(dc), n_loc))
+    return int(load().omnimoe_v_bands(ctypes.byref(dc), n_loc, n_tok))
 
 
 def new_plan(n_loc: int, M: int, device, expert_begin: int = 0, n_tokens: int = 0, dims: LayerDims = None):
     """Plan buffers (omnimoe_plan).  n_tokens: tokens of the task list (0: M / (h*K));
     the V-order arrays of the SLICED executor are always allocated (for dims' bands)."""
-    nb = v_bands(dims, n_loc) if dims is not None else 1
+    n_tok = n_tokens if n_tokens > 0 else (-(-M // (dims.n_heads * dims.top_k)) if dims is not None else M)
+    nb = v_bands(dims, n_loc, max(n_tok, 1)) if dims is not None else 1
     t = dict(sorted_task=torch.empty(max(M, 1), dtype=torch.int32, device=device),
              task_pair=torch.empty((max(M, 1), 2), dtype=torch.int32, device=device),
              token_offsets=torch.empty(max(n_tokens, M, 1) * (nb + 1) + 1, dtype=torch.int32, device=device),

@@ -104,7 +104,7 @@ def test_layer_c5_full_size_sliced():
     SLICED executor with the expert bands the bench runs; 256 tokens recomputed."""
     w = configs.get("C5", v_layout=om.V_SLICED)
     dims = w.dims
-    assert om.layer_executor(dims, w.L) == om.EXPERT_SLICED and om.v_bands(dims, dims.N) > 1
+    assert om.layer_executor(dims, w.L) == om.EXPERT_SLICED and om.v_bands(dims, dims.N, w.L) > 1
     inp = make_inputs(dims, w.L, w.seed)
     inp["V"] = om.pack_v(dims, inp["V"])
     torch.cuda.synchronize()

@@ -407,17 +407,17 @@ def test_pack_v_is_a_pure_relayout():
     assert torch.equal(Vs.view(torch.int16), want.view(torch.int16))
 
 
-@pytest.fixture(params=[0, 16], ids=["bands_default", "bands_16KB"])
-def v_band_kb(request, monkeypatch):
-    """0: the library's expert bands (1 at these sizes); 16: 16 KB bands (several)."""
-    if request.param:
-        monkeypatch.setenv("OMNIMOE_V_BAND_KB", str(request.param))
+@pytest.fixture(params=[{}, {"v_band_bytes": 16 << 10}], ids=["bands_default", "bands_16KB"])
+def v_geom(request):
+    """Pass-V bands (dims.v_band_bytes): the library's choice (one band at these sizes)
+    or 16 KB bands (several)."""
     return request.param
 
 
 @pytest.fixture(params=["auto", "warp"])
 def v_mode(request, monkeypatch):
-    """pass V kernel: auto (8 tokens per warp for h*K <= 64) or forced one token per warp."""
+    """pass V kernel for one slice per item: auto (8 tokens per warp for h*K <= 64) or
+    forced one token per warp."""
     if request.param == "warp":
         monkeypatch.setenv("OMNIMOE_V_GROUP_MAX_TASKS", "0")
     return request.param
@@ -427,17 +427,19 @@ def v_mode(request, monkeypatch):
 @pytest.mark.parametrize("d,act", [(64, om.SILU), (96, om.SILU), (1024, om.SILU), (2048, om.SILU),
                                    (64, om.IDENTITY)])
 @pytest.mark.parametrize("accumulate", [False, True])
-def test_expert_fwd_sliced_given_plan(d, act, B, accumulate, v_band_kb, v_mode):
+def test_expert_fwd_sliced_given_plan(d, act, B, accumulate, v_geom, v_mode):
     rng = np.random.default_rng(d + B)
     L, N, HK = 200, 3000, 12
-    dims = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, act=act, group_size=B, v_layout=om.V_SLICED)
+    dims = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, act=act, group_size=B, v_layout=om.V_SLICED,
+                        **v_geom)
     inp = make_inputs(dims, L, 9, skip=("subkeys",))
     base = rng.integers(0, N - 64, L)
     ids = np.stack([b0 + rng.choice(64, HK, replace=False) for b0 in base]).astype(np.int32)
     ids[7] = ids[3]  # two tokens with identical expert lists
     gates = rng.random((L, HK)).astype(np.float32)
     plan = om.schedule(dims, torch.from_numpy(ids).cuda().reshape(-1), torch.from_numpy(gates).cuda().reshape(-1))
-    assert om.v_bands(dims, N) == (1 if not v_band_kb else -(-N * 64 // (v_band_kb << 10)))
+    want = -(-(N * 64) // v_geom["v_band_bytes"]) if v_geom else 1
+    assert om.v_bands(dims, N, L) == want
     Vs = om.pack_v(dims, inp["V"])
     y0 = torch.randn(L, d, device="cuda") if accumulate else None
     y = om.expert_fwd(dims, inp["x"], inp["W"], Vs, plan, y_routed=None if y0 is None else y0.clone(),
@@ -454,12 +456,12 @@ def test_expert_fwd_sliced_given_plan(d, act, B, accumulate, v_band_kb, v_mode):
     assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
 
 
-def test_expert_fwd_sliced_shard_and_empty_tokens(v_band_kb, v_mode):
+def test_expert_fwd_sliced_shard_and_empty_tokens(v_geom, v_mode):
     """Expert range of a shard (tasks outside it are skipped) and tokens with no
     tasks in range (their y_routed rows are written as zeros)."""
     rng = np.random.default_rng(3)
     L, N, HK, b, e = 150, 4096, 8, 1024, 2048
-    dims = om.LayerDims(d=256, n_rows=N, n_cols=1, top_k=HK, d_ff=0, group_size=64, v_layout=om.V_SLICED)
+    dims = om.LayerDims(d=256, n_rows=N, n_cols=1, top_k=HK, d_ff=0, group_size=64, v_layout=om.V_SLICED, **v_geom)
     inp = make_inputs(dims, L, 4, skip=("subkeys",))
     ids = rng.integers(0, N, (L, HK)).astype(np.int32)
     ids[10] = rng.integers(3000, N, HK)  # token 10: nothing in [b, e)
@@ -482,8 +484,8 @@ def test_expert_fwd_sliced_shard_and_empty_tokens(v_band_kb, v_mode):
 
 @pytest.mark.parametrize("mode", [synth.NORMAL, synth.DYADIC])
 @pytest.mark.parametrize("B", [0, 5])
-def test_layer_c1_sliced(mode, B, v_band_kb, v_mode):
-    w = _dims("C1", group_size=B, v_layout=om.V_SLICED)
+def test_layer_c1_sliced(mode, B, v_geom, v_mode):
+    w = _dims("C1", group_size=B, v_layout=om.V_SLICED, **v_geom)
     dims = w.dims
     inp = make_inputs(dims, w.L, w.seed, mode)
     Vs = om.pack_v(dims, inp["V"])
