@@ -376,7 +376,7 @@ def bench_single(args, w, lr):
         zb = n_active * dims.d * eb + L * dims.d * eb + 12 * M + 4 * M              # W rows once, x, plan, a
         vb = n_active * dims.d * eb + 8 * M + 4 * L * dims.d                       # V rows once, pairs, y write
         zl2 = M * dims.d * eb + n_active * dims.d * eb + 12 * M                    # x per task + W + plan
-        vl2 = M * dims.d * eb + 8 * M * (dims.d // 32)                             # v slices per task + pairs per slice
+        vl2 = M * dims.d * eb + 8 * M * (dims.d // 64)                             # v slices per task + pairs per slice
         cand = {"expert_zdot_kernel": (zb, zl2, stage_ms["a6_pass_z"]),
                 "expert_vslice_kernel": (vb, vl2, stage_ms["a6_pass_v"])}
         kern = max(cand, key=lambda k: cand[k][2])

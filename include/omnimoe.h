@@ -55,14 +55,14 @@ enum { OMNIMOE_SILU = 0, OMNIMOE_IDENTITY = 1 };
 enum { OMNIMOE_EXPERT_AUTO = 0, OMNIMOE_EXPERT_WARP = 1, OMNIMOE_EXPERT_GROUP = 2, OMNIMOE_EXPERT_TOKEN = 3,
        OMNIMOE_EXPERT_SLICED = 4, OMNIMOE_EXPERT_DENSE = 5 /* reported by omnimoe_layer_executor only */ };
 /* Memory layout of the value table V (the down-projection rows v_n of Eq.WV,
- * PAPER:172-176).  ROWS: [N][d], one row per expert.  SLICED: [d/32][N][32], i.e.
- * the table cut into d/32 column slices of 32 elements, each slice stored
- * expert-major (64 bytes per expert and slice); omnimoe_pack_v converts.  The
+ * PAPER:172-176).  ROWS: [N][d], one row per expert.  SLICED: [d/64][N][64], i.e.
+ * the table cut into d/64 column slices of 64 elements, each slice stored
+ * expert-major (128 bytes per expert and slice; d % 64 == 0); omnimoe_pack_v converts.  The
  * SLICED executor (AUTO picks it for this layout, bf16 only) evaluates Eq.Grouped
  * in two passes: (Z) the plan's runs compute a = g * sigma(x_l . w_e) for every
  * task with w_e read once per group window; (V) slice by slice, every token
  * gathers the slice of v_e of its tasks and accumulates a * v_e into its output
- * slice.  One slice of V (64 N bytes) stays L2-resident while all tokens use it,
+ * slice.  One band of a slice of V (<= 68 MB) stays L2-resident while all tokens use it,
  * so V is read from HBM once and y_routed is written once, without atomics
  * (DESIGN.md §4.4). */
 enum { OMNIMOE_V_ROWS = 0, OMNIMOE_V_SLICED = 1 };
@@ -105,7 +105,7 @@ enum { OMNIMOE_ROUTER_EXACT = 0, OMNIMOE_ROUTER_EXACT_F64 = 1, OMNIMOE_ROUTER_DE
  *              of the Cartesian candidates, row rank then column rank: same set and
  *              gates, no final sort; what omnimoe_layer_fwd uses internally).
  *   v_band_bytes  SLICED pass V: L2 budget of what one pass-V step keeps resident
- *              (one expert band's part of a 32-column slice of V); 0 = library
+ *              (one expert band's part of a 64-column slice of V); 0 = library
  *              choice (68 MB).  Determines n_b
  *              (omnimoe_v_bands).  Performance only: results do not depend on it.
  */
@@ -184,8 +184,8 @@ typedef struct {
  * 64 MB of W/V rows, in bf16 mode; 1 in fp32 mode).  Returns 0 on invalid dims. */
 int64_t omnimoe_group_size(const omnimoe_dims* dims);
 /* Number of expert bands n_b of the SLICED executor's pass V for a local expert
- * range of n_loc rows and n_tok tokens: pass V sweeps the 32-column slices of V one
- * band at a time; the band's part of a slice (64 bytes per expert) is kept within
+ * range of n_loc rows and n_tok tokens: pass V sweeps the 64-column slices of V one
+ * band at a time; the band's part of a slice (128 bytes per expert) is kept within
  * dims.v_band_bytes (68 MB) so that it stays L2-resident while every token uses it
  * (DESIGN.md §4.4).  Independent of dims.v_layout; 0 on invalid dims. */
 int64_t omnimoe_v_bands(const omnimoe_dims* dims, int64_t n_loc, int64_t n_tok);
@@ -246,7 +246,7 @@ omnimoe_status omnimoe_schedule(const omnimoe_dims* dims, int64_t M, const int32
  * deterministic).
  *   x         [L][d]
  *   W_loc     [n_loc][d]  rows of W for the plan's expert range
- *   V_loc     [n_loc][d] (ROWS) or [d/32][n_loc][32] (SLICED)
+ *   V_loc     [n_loc][d] (ROWS) or [d/64][n_loc][64] (SLICED)
  *   y_routed  float [L][d]; overwritten unless accumulate != 0 (then added to)
  * ROWS executors use fp32 atomics: reproducible up to summation order. */
 omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const void* x,
@@ -303,8 +303,8 @@ omnimoe_status omnimoe_shared_mlp_bwd(const omnimoe_dims* dims, int64_t L, const
                                       float* dw_gate_up, float* dw_down, void* ws, size_t ws_bytes,
                                       omnimoe_stream_t stream);
 
-/* V [n][d] (OMNIMOE_V_ROWS) -> V_sliced [d/32][n][32] (OMNIMOE_V_SLICED): a
- * one-time weight re-layout (no arithmetic; bit-exact copy), d % 32 == 0.
+/* V [n][d] (OMNIMOE_V_ROWS) -> V_sliced [d/64][n][64] (OMNIMOE_V_SLICED): a
+ * one-time weight re-layout (no arithmetic; bit-exact copy), d % 64 == 0.
  * n = number of expert rows in the table (N, or n_loc for a shard). */
 omnimoe_status omnimoe_pack_v(const omnimoe_dims* dims, int64_t n, const void* V, void* V_sliced,
                               omnimoe_stream_t stream);
@@ -350,7 +350,7 @@ int32_t omnimoe_layer_executor(const omnimoe_dims* dims, int64_t L);
 /* Whole layer forward (Eq.MoE / Eq.Assemble):
  * route -> schedule (full expert range) -> expert_fwd -> shared MLP + combine.
  *   W          [N][d]
- *   V          [N][d] or, for dims.v_layout == OMNIMOE_V_SLICED, [d/32][N][32]
+ *   V          [N][d] or, for dims.v_layout == OMNIMOE_V_SLICED, [d/64][N][64]
  *   w_gate_up, w_down  as in omnimoe_shared_mlp (ignored when d_ff == 0)
  *   y          [L][d]
  *   idx_out, gate_out  nullable copies of the routing decision [L][h][K]; the same

@@ -103,8 +103,8 @@ omnimoe_status validate_dims(const omnimoe_dims* dp) {
     return OMNIMOE_ERR_UNSUPPORTED;
   }
   if (d.v_layout == OMNIMOE_V_SLICED) {
-    if (d.dtype != OMNIMOE_BF16 || d.d % 32 != 0 || d.d > 2048) {
-      set_error("V_SLICED layout: bf16 with d % 32 == 0 and d <= 2048 " + dims_str(d));
+    if (d.dtype != OMNIMOE_BF16 || d.d % 64 != 0 || d.d > 2048) {
+      set_error("V_SLICED layout: bf16 with d % 64 == 0 and d <= 2048 " + dims_str(d));
       return OMNIMOE_ERR_UNSUPPORTED;
     }
     if (d.expert_kernel != OMNIMOE_EXPERT_AUTO && d.expert_kernel != OMNIMOE_EXPERT_SLICED) {
@@ -555,8 +555,8 @@ omnimoe_status omnimoe_pack_v(const omnimoe_dims* dims, int64_t n, const void* V
                               omnimoe_stream_t stream) {
   reset_launch_count();
   OMNI_TRY(validate_dims(dims));
-  if (dims->dtype != OMNIMOE_BF16 || dims->d % 32 != 0) {
-    set_error("pack_v: bf16 with d % 32 == 0 " + dims_str(*dims));
+  if (dims->dtype != OMNIMOE_BF16 || dims->d % 64 != 0) {
+    set_error("pack_v: bf16 with d % 64 == 0 " + dims_str(*dims));
     return OMNIMOE_ERR_UNSUPPORTED;
   }
   if (n < 0 || n >= (int64_t(1) << 31)) {

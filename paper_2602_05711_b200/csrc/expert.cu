@@ -914,27 +914,43 @@ __device__ __forceinline__ int2 ld_pair(const int32_t* p, uint64_t pol) {
   return r;
 }
 
-// pass V: one warp per (slice, token) item; lane = (task sub-group g8 = lane/4,
-// column quad c4 = lane%4): 8 tasks per load instruction, 8 bf16 columns per lane.
-// The (expert, a) pairs of the next 64 tasks -- possibly of the next item, which
-// is claimed one item ahead -- are loaded while the current 64 are processed.
-template <int MINB>
+// 32-byte load (LDG.256, sm_100): 16 bf16 of a 128-byte V slice piece
+struct U8 {
+  uint32_t w[8];
+};
+__device__ __forceinline__ U8 ld256(const void* p) {
+  U8 r;
+  asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]),
+                 "=r"(r.w[7])
+               : "l"(p));
+  return r;
+}
+
+// pass V: one warp per (slice, token) item over the SLICED layout [d/64][n][64] (one
+// 128-byte piece per expert and slice); lane = (task sub-slot g8 = lane / 4, 32-byte
+// quarter c4 = lane % 4 of the piece): 8 tasks per 256-bit load instruction, 16 bf16
+// columns per lane.  The (expert, a) pairs of the next window -- possibly of the next
+// item, which is claimed one item ahead -- are loaded while the current one is
+// processed.  Items (slice, token) are claimed in order from one counter so that the
+// warps in flight stay within ~one slice (a static round-robin lets warps drift over
+// many slices: C3a pass V 3.45 -> 13.6 ms in round 1).
+template <int MINB, int W>
 __global__ void __launch_bounds__(256, MINB)
     expert_vslice_kernel(int d, int64_t L, int64_t n_loc, const int32_t* __restrict__ seg, int seg_stride,
                          int band, int64_t n_tok, const int32_t* __restrict__ task_pair,
                          const __nv_bfloat16* __restrict__ Vs, float* __restrict__ y, int accumulate,
-                         int* __restrict__ work, int stream_hint) {
+                         int* __restrict__ work) {
+  constexpr int WT = 8 * W;    // tasks per window: W rounds of 8 tasks, one 32-byte load per lane each
+  constexpr int NP = (WT + 31) / 32;  // (expert, a) pairs per lane and window
   const int lane = threadIdx.x & 31, c4 = lane & 3, g8 = lane >> 2;
-  const int S = d / 32;
+  const int S = d / 64;
   const int64_t n_items = (int64_t)S * L;
-  const uint64_t pol = stream_hint ? policy_evict_first() : policy_evict_normal();
-  // item i: slice i / L, token i % L, claimed in order from one counter so that the
-  // warps in flight stay within ~one slice (a static round-robin lets warps drift over
-  // many slices: C3a pass V 3.45 -> 13.6 ms)
+  const uint64_t pol = policy_evict_first();
   auto claim = [&]() {
-    int64_t v = 0;
+    int v = 0;
     if (lane == 0) v = atomicAdd(work, 1);
-    return (int64_t)__shfl_sync(0xffffffffu, (int)v, 0);
+    return (int64_t)__shfl_sync(0xffffffffu, v, 0);
   };
   auto range = [&](int64_t item, int& beg, int& end) {
     beg = end = 0;
@@ -946,68 +962,93 @@ __global__ void __launch_bounds__(256, MINB)
       }
     }
   };
-  auto fetch = [&](int p0, int end, int2& pa, int2& pb) {
-    pa = (p0 + lane < end) ? ld_pair(task_pair + 2 * (size_t)(p0 + lane), pol) : make_int2(-1, 0);
-    pb = (p0 + 32 + lane < end) ? ld_pair(task_pair + 2 * (size_t)(p0 + 32 + lane), pol) : make_int2(-1, 0);
+  auto fetch = [&](int p0, int end, int2 (&pp)[NP]) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k)
+      pp[k] = (32 * k + lane < WT && p0 + 32 * k + lane < end)
+                  ? ld_pair(task_pair + 2 * (size_t)(p0 + 32 * k + lane), pol)
+                  : make_int2(-1, 0);
   };
+  // the output quarter this lane adds to (band > 0 or accumulate) is copied into shared
+  // memory by cp.async when the item starts and read when it ends: no dependent round
+  // trip at the end of the item and no registers held across it
+  __shared__ __align__(16) float ysm[8][4][16];
+  float* my_y = ysm[threadIdx.x >> 5][c4];
   int64_t it = claim();
   int beg, end;
   range(it, beg, end);
-  int2 na, nb;
-  fetch(beg, end, na, nb);
+  int2 np_[NP];
+  fetch(beg, end, np_);
   while (it < n_items) {
     const int64_t nxt = claim();
     int nbeg, nend;
     range(nxt, nbeg, nend);
     const int s = (int)(it / L);
     const int64_t l = it - (int64_t)s * L;
-    const __nv_bfloat16* vs = Vs + (size_t)s * n_loc * 32 + c4 * 8;
-    unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
-    for (int p0 = beg; p0 < end; p0 += 64) {
-      const int2 ca = na, cb = nb;
-      if (p0 + 64 < end) fetch(p0 + 64, end, na, nb);
-      else fetch(nbeg, nend, na, nb);  // the next item's first tasks
-      const int n_r = min(8, (end - p0 + 7) >> 3);  // rounds of 8 tasks holding work
-      uint4 v[8];
-      float a[8];
+    float* yq = y + (size_t)l * d + s * 64 + c4 * 16;
+    if (accumulate && g8 == 0) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
+      for (int q = 0; q < 4; ++q)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(my_y + 4 * q)), "l"(yq + 4 * q)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    const __nv_bfloat16* vs = Vs + (size_t)s * n_loc * 64 + c4 * 16;
+    unsigned long long acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0ull;
+    for (int p0 = beg; p0 < end; p0 += WT) {
+      int2 cp[NP];
+#pragma unroll
+      for (int k = 0; k < NP; ++k) cp[k] = np_[k];
+      if (p0 + WT < end) fetch(p0 + WT, end, np_);
+      else fetch(nbeg, nend, np_);  // the next item's first tasks
+      const int n_r = min(W, (end - p0 + 7) >> 3);  // rounds of 8 tasks holding work
+      U8 v[W];
+      float a[W];
+#pragma unroll
+      for (int r = 0; r < W; ++r) {
         const int src = (r & 3) * 8 + g8;
-        const int e = __shfl_sync(0xffffffffu, r < 4 ? ca.x : cb.x, src);
-        a[r] = __int_as_float(__shfl_sync(0xffffffffu, r < 4 ? ca.y : cb.y, src));
+        const int e = __shfl_sync(0xffffffffu, cp[r >> 2].x, src);
+        a[r] = __int_as_float(__shfl_sync(0xffffffffu, cp[r >> 2].y, src));
         if (e < 0) a[r] = 0.f;
-        v[r] = (r < n_r && e >= 0) ? ld_vec(vs + (size_t)e * 32) : make_uint4(0, 0, 0, 0);
+        if (r < n_r && e >= 0) {
+          v[r] = ld256(vs + (size_t)e * 64);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[r].w[i] = 0u;
+        }
       }
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
+      for (int r = 0; r < W; ++r) {
         const unsigned long long a2 = ((unsigned long long)__float_as_uint(a[r]) << 32) | __float_as_uint(a[r]);
-        axpy2_bf16(acc[0], a2, v[r].x);
-        axpy2_bf16(acc[1], a2, v[r].y);
-        axpy2_bf16(acc[2], a2, v[r].z);
-        axpy2_bf16(acc[3], a2, v[r].w);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) axpy2_bf16(acc[i], a2, v[r].w[i]);
       }
     }
-    if (beg == end) fetch(nbeg, nend, na, nb);
-    float f[8];
+    if (beg == end) fetch(nbeg, nend, np_);
+    float f[16];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 8; ++i) {
       f[2 * i] = lo_f(acc[i]);
       f[2 * i + 1] = hi_f(acc[i]);
     }
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) f[i] += __shfl_xor_sync(0xffffffffu, f[i], o);
+      for (int i = 0; i < 16; ++i) f[i] += __shfl_xor_sync(0xffffffffu, f[i], o);
     if (g8 == 0) {
-      float4* dst = reinterpret_cast<float4*>(y + (size_t)l * d + s * 32 + c4 * 8);
-      float4 u = make_float4(f[0], f[1], f[2], f[3]), w = make_float4(f[4], f[5], f[6], f[7]);
-      if (accumulate) {
-        const float4 p = dst[0], q = dst[1];
-        u.x += p.x; u.y += p.y; u.z += p.z; u.w += p.w;
-        w.x += q.x; w.y += q.y; w.z += q.z; w.w += q.w;
+      float4* dst = reinterpret_cast<float4*>(yq);
+      if (accumulate) asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float4 u = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+        if (accumulate) {
+          const float4 p = reinterpret_cast<const float4*>(my_y)[q];
+          u.x += p.x; u.y += p.y; u.z += p.z; u.w += p.w;
+        }
+        dst[q] = u;
       }
-      dst[0] = u;
-      dst[1] = w;
     }
     it = nxt;
     beg = nbeg;
@@ -1016,21 +1057,19 @@ __global__ void __launch_bounds__(256, MINB)
 }
 
 // pass V for few tasks per token (h*K <= 64): one warp per (slice, 8 consecutive
-// tokens), lane group g8 = lane / 4 owns one token, 8 of its tasks per step (8 pieces
-// in flight per lane); no cross-lane reduction.
+// tokens), lane group g8 = lane / 4 owns one token, 4 of its tasks per step (one
+// 32-byte quarter of each 128-byte piece per lane); no cross-lane reduction.
 __global__ void __launch_bounds__(256)
     expert_vslice_group_kernel(int d, int64_t L, int64_t n_loc, const int32_t* __restrict__ seg, int seg_stride,
                                int band, int64_t n_tok, const int32_t* __restrict__ task_pair,
                                const __nv_bfloat16* __restrict__ Vs, float* __restrict__ y, int accumulate,
-                               int stream_hint, int* __restrict__ work) {
+                               int* __restrict__ work) {
+  constexpr int T = 4;
   const int lane = threadIdx.x & 31, c4 = lane & 3, g8 = lane >> 2;
-  const int S = d / 32;
+  const int S = d / 64;
   const int64_t n_tc = (L + 7) / 8;
   const int64_t n_items = (int64_t)S * n_tc;
-  const uint64_t pol = stream_hint ? policy_evict_first() : policy_evict_normal();
-  // items claimed in order from one counter: the warps in flight stay within ~one
-  // slice, whose V rows are then L2-resident (a static round-robin lets warps drift
-  // over many slices)
+  const uint64_t pol = policy_evict_first();
   auto claim = [&]() {
     int v = 0;
     if (lane == 0) v = atomicAdd(work, 1);
@@ -1044,54 +1083,61 @@ __global__ void __launch_bounds__(256)
       beg = seg[l * seg_stride + band];
       n = seg[l * seg_stride + band + 1] - beg;
     }
-    const __nv_bfloat16* vs = Vs + (size_t)s * n_loc * 32 + c4 * 8;
+    const __nv_bfloat16* vs = Vs + (size_t)s * n_loc * 64 + c4 * 16;
     const int nmax = __reduce_max_sync(0xffffffffu, n);
-    unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
-    int2 nx[8];  // the (expert, a) pairs of the next 8 tasks, loaded one step ahead
+    unsigned long long acc[8];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) nx[t] = t < n ? ld_pair(task_pair + 2 * (size_t)(beg + t), pol) : make_int2(-1, 0);
-    for (int q = 0; q < nmax; q += 8) {
-      int2 pr[8];
+    for (int i = 0; i < 8; ++i) acc[i] = 0ull;
+    int2 nx[T];  // the (expert, a) pairs of the next T tasks, loaded one step ahead
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
+    for (int t = 0; t < T; ++t) nx[t] = t < n ? ld_pair(task_pair + 2 * (size_t)(beg + t), pol) : make_int2(-1, 0);
+    for (int q = 0; q < nmax; q += T) {
+      int2 pr[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
         pr[t] = nx[t];
-        nx[t] = q + 8 + t < n ? ld_pair(task_pair + 2 * (size_t)(beg + q + 8 + t), pol) : make_int2(-1, 0);
+        nx[t] = q + T + t < n ? ld_pair(task_pair + 2 * (size_t)(beg + q + T + t), pol) : make_int2(-1, 0);
       }
-      uint4 v[8];
+      U8 v[T];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) v[t] = pr[t].x >= 0 ? ld_vec(vs + (size_t)pr[t].x * 32) : make_uint4(0, 0, 0, 0);
+      for (int t = 0; t < T; ++t) {
+        if (pr[t].x >= 0) {
+          v[t] = ld256(vs + (size_t)pr[t].x * 64);
+        } else {
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
+          for (int i = 0; i < 8; ++i) v[t].w[i] = 0u;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
         const float a = pr[t].x >= 0 ? __int_as_float(pr[t].y) : 0.f;
         const unsigned long long a2 = ((unsigned long long)__float_as_uint(a) << 32) | __float_as_uint(a);
-        axpy2_bf16(acc[0], a2, v[t].x);
-        axpy2_bf16(acc[1], a2, v[t].y);
-        axpy2_bf16(acc[2], a2, v[t].z);
-        axpy2_bf16(acc[3], a2, v[t].w);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) axpy2_bf16(acc[i], a2, v[t].w[i]);
       }
     }
     if (l < L) {
-      float4* dst = reinterpret_cast<float4*>(y + (size_t)l * d + s * 32 + c4 * 8);
-      float4 u = make_float4(lo_f(acc[0]), hi_f(acc[0]), lo_f(acc[1]), hi_f(acc[1]));
-      float4 w = make_float4(lo_f(acc[2]), hi_f(acc[2]), lo_f(acc[3]), hi_f(acc[3]));
-      if (accumulate) {
-        const float4 p = dst[0], q = dst[1];
-        u.x += p.x; u.y += p.y; u.z += p.z; u.w += p.w;
-        w.x += q.x; w.y += q.y; w.z += q.z; w.w += q.w;
+      float4* dst = reinterpret_cast<float4*>(y + (size_t)l * d + s * 64 + c4 * 16);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float4 u = make_float4(lo_f(acc[2 * q]), hi_f(acc[2 * q]), lo_f(acc[2 * q + 1]), hi_f(acc[2 * q + 1]));
+        if (accumulate) {
+          const float4 p = dst[q];
+          u.x += p.x; u.y += p.y; u.z += p.z; u.w += p.w;
+        }
+        dst[q] = u;
       }
-      dst[0] = u;
-      dst[1] = w;
     }
   }
 }
 
-// V [n][d] -> V_sliced [d/32][n][32] (16-byte moves; bit-exact)
+// V [n][d] -> V_sliced [d/64][n][64] (16-byte moves; bit-exact)
 __global__ void pack_v_kernel(const uint4* __restrict__ V, uint4* __restrict__ Vs, int64_t n, int d) {
   const int64_t per_row = d / 8, total = n * per_row;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / per_row;
     const int q = (int)(i - row * per_row);
-    Vs[((size_t)(q >> 2) * n + row) * 4 + (q & 3)] = V[i];
+    Vs[((size_t)(q >> 3) * n + row) * 8 + (q & 7)] = V[i];
   }
 }
 
@@ -1155,6 +1201,85 @@ __global__ void __launch_bounds__(256, MINB)
             q = dot2_bf16(q, wv[j].y, xr[u][j].y);
             q = dot2_bf16(q, wv[j].z, xr[u][j].z);
             z[u] += dot2_bf16(q, wv[j].w, xr[u][j].w);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int u = 0; u < T; ++u) z[u] += __shfl_xor_sync(0xffffffffu, z[u], o);
+#pragma unroll
+        for (int u = 0; u < T; ++u) {
+          const float g = __shfl_sync(0xffffffffu, g_l, min(t + u, cnt - 1));
+          const float a = g * (act == OMNIMOE_IDENTITY ? z[u] : silu_f(z[u]));
+          if (lane == t + u) my_a = a;
+        }
+      }
+      if (lane < cnt) task_pair[2 * (size_t)t_l + 1] = __float_as_int(my_a);
+    }
+    tau = __shfl_sync(0xffffffffu, nxt, 0);
+  }
+}
+
+// pass Z with 32-byte loads (LDG.256): the same arithmetic and order of work as
+// expert_zdot_kernel, half the load instructions per row (d % 512 == 0)
+__device__ __forceinline__ U8 ld256_hint(const void* p, uint64_t pol) {
+  U8 r;
+  asm volatile("ld.global.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]),
+                 "=r"(r.w[7])
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+template <int NV8, int MINB, int T>
+__global__ void __launch_bounds__(256, MINB)
+    expert_zdot256_kernel(int d, const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ W,
+                          const int32_t* __restrict__ offsets, const int32_t* __restrict__ active,
+                          const int32_t* __restrict__ n_active, const int32_t* __restrict__ stok,
+                          const float* __restrict__ sgate, const int32_t* __restrict__ stask,
+                          int32_t* __restrict__ task_pair, int act, int* __restrict__ work) {
+  const int lane = threadIdx.x & 31;
+  const int na = *n_active;
+  const uint64_t pol = policy_evict_first(), xpol = policy_evict_normal();
+  int tau = 0;
+  if (lane == 0) tau = atomicAdd(work, 1);
+  tau = __shfl_sync(0xffffffffu, tau, 0);
+  while (tau < na) {
+    const int e = active[tau];
+    const int beg = offsets[e], end = offsets[e + 1];
+    U8 wv[NV8];
+#pragma unroll
+    for (int j = 0; j < NV8; ++j) wv[j] = ld256_hint(W + (size_t)e * d + (j * 32 + lane) * 16, pol);
+    int nxt = 0;
+    if (lane == 0) nxt = atomicAdd(work, 1);  // claim the next expert early
+    for (int p0 = beg; p0 < end; p0 += 32) {
+      const int pl = p0 + lane;
+      const int l_l = pl < end ? stok[pl] : 0;
+      const float g_l = pl < end ? sgate[pl] : 0.f;
+      const int t_l = pl < end ? stask[pl] : 0;
+      const int cnt = min(32, end - p0);
+      float my_a = 0.f;
+      for (int t = 0; t < cnt; t += T) {
+        U8 xr[T][NV8];
+#pragma unroll
+        for (int u = 0; u < T; ++u) {
+          const int lt = __shfl_sync(0xffffffffu, l_l, min(t + u, cnt - 1));
+#pragma unroll
+          for (int j = 0; j < NV8; ++j) xr[u][j] = ld256_hint(x + (size_t)lt * d + (j * 32 + lane) * 16, xpol);
+        }
+        float z[T];
+#pragma unroll
+        for (int u = 0; u < T; ++u) {
+          z[u] = 0.f;
+#pragma unroll
+          for (int j = 0; j < NV8; ++j) {
+            float q = 0.f, q2 = 0.f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              q = dot2_bf16(q, wv[j].w[i], xr[u][j].w[i]);
+              q2 = dot2_bf16(q2, wv[j].w[4 + i], xr[u][j].w[4 + i]);
+            }
+            z[u] += q + q2;
           }
         }
 #pragma unroll
@@ -1399,9 +1524,9 @@ bool layer_uses_token_executor(const omnimoe_dims& d, int64_t L) {
          d.d % 256 == 0 && d.d <= 2048 && expected_eta(d, L) < env_int("OMNIMOE_TOKEN_ETA_X100", 200) / 100.0;
 }
 
-// pass V geometry: pass V sweeps the 32-column slices of V one band of
+// pass V geometry: pass V sweeps the 64-column slices of V one band of
 // experts at a time (one launch per band, item order (slice, token) inside it); the
-// band's part of a slice (64 bytes per expert) is kept within dims.v_band_bytes (68 MB
+// band's part of a slice (128 bytes per expert) is kept within dims.v_band_bytes (68 MB
 // of the 126 MB L2) so that it stays resident while every token uses it.  More bands
 // than that measured slower (C3a: 1 band 3.45 ms, 2 bands 3.50, 4 bands 5.16; C5: 4
 // bands beat 8 -- profiles/r2/bands/): every band multiplies the (slice, token) items
@@ -1410,7 +1535,15 @@ int64_t resolve_v_bands(const omnimoe_dims& d, int64_t n_loc, int64_t n_tok) {
   (void)n_tok;
   if (n_loc < 1) return 1;
   const int64_t budget = d.v_band_bytes > 0 ? d.v_band_bytes : (68ll << 20);
-  return std::max<int64_t>(1, std::min<int64_t>(30, (64 * n_loc + budget - 1) / budget));
+  const int64_t by_l2 = std::max<int64_t>(1, std::min<int64_t>(30, (128 * n_loc + budget - 1) / budget));
+  if (d.v_band_bytes > 0) return by_l2;
+  // but at least ~128 tasks per (token, band) item: the item's fixed costs (claim, segment
+  // bounds, first pairs, reduction, output write) outweigh the L2 misses of a chunk above
+  // the budget (C5: 4 bands of 134 MB 16.3 ms, 8 bands of 67 MB 19.0 ms; C3a: 2 bands of
+  // 67 MB 2.82 ms, 1 band of 134 MB 3.16 ms -- profiles/r2/slices128/)
+  const double N = (double)(d.n_rows * d.n_cols);
+  const double tasks_per_token = (double)(d.n_heads * d.top_k) * std::min(1.0, (double)n_loc / N);
+  return std::min<int64_t>(by_l2, std::max<int64_t>(1, (int64_t)(tasks_per_token / 128.0)));
 }
 
 int64_t resolve_token_blocks(const omnimoe_dims& d, int64_t L) {
@@ -1434,6 +1567,24 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
   const int d = (int)dm.d;
   omnimoe_status s = OMNIMOE_OK;
   if (!(passes & 1)) {
+  } else if (resolve_group_size(dm) == 1 && d % 512 == 0 && d <= 2048) {
+    // 32-byte loads, 80 registers (3 CTAs per SM), two x rows in flight: C3a pass Z 2.26 -> 2.17 ms
+    // against 16-byte loads (<4,3,2> 2.17, <4,4,2> 2.21, <4,2,3> 2.29; profiles/r2/slices128/)
+    auto go = [&](auto kern) {
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+      kern<<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(
+          d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W), plan.expert_offsets,
+          plan.active, plan.n_active, plan.sorted_token, plan.sorted_gate, plan.sorted_task, plan.task_pair, dm.act,
+          work);
+    };
+    switch (d / 512) {
+      case 1: go(expert_zdot256_kernel<1, 3, 2>); break;
+      case 2: go(expert_zdot256_kernel<2, 3, 2>); break;
+      case 3: go(expert_zdot256_kernel<3, 3, 2>); break;
+      default: go(expert_zdot256_kernel<4, 3, 2>); break;
+    }
+    OMNI_CHECK_LAUNCH("expert_zdot256_kernel");
   } else if (resolve_group_size(dm) == 1) {  // expert-major plan: w_e in registers, x from L2
     switch ((d + 255) / 256) {
       case 1: s = launch_zdot<1>(d, x, W, plan, dm.act, work, st); break;
@@ -1457,11 +1608,11 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
   }
   OMNI_TRY(s);
   if (!(passes & 2)) return OMNIMOE_OK;
-  // 64 registers, 4 CTAs per SM (48 / 5: 3.46 ms at C3a, 64 / 4: 3.36, 78 / 3: 3.48; profiles/r2/occupancy/)
-  auto vkern = expert_vslice_kernel<4>;
+  // 80 registers (3 CTAs per SM), 4 rounds of 8 tasks per window (C3a pass V: <3,4> 2.82 ms,
+  // <4,4> 2.92, <3,6> 2.96, <2,8> 3.12; profiles/r2/slices128/)
+  auto vkern = expert_vslice_kernel<3, 4>;
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vkern, 256, 0);
-  per_sm = std::max(1, std::min(per_sm, env_int("OMNIMOE_V_BLOCKS", per_sm)));
   const int64_t n_tok = plan.n_tokens > 0 ? plan.n_tokens : L;
   const int nb = (int)resolve_v_bands(dm, n_loc, std::max<int64_t>(n_tok, 1));
   // one launch per expert band: its slices of V stay L2-resident while all tokens
@@ -1475,12 +1626,12 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
     if (grouped) {
       expert_vslice_group_kernel<<<kSMs * std::max(gper_sm, 1), 256, 0, st>>>(
           d, L, n_loc, plan.token_offsets, nb + 1, b, n_tok, plan.task_pair, static_cast<const __nv_bfloat16*>(Vs),
-          y, b > 0 ? 1 : accumulate, env_int("OMNIMOE_V_HINT", 1), work + 1 + b);
+          y, b > 0 ? 1 : accumulate, work + 1 + b);
       OMNI_CHECK_LAUNCH("expert_vslice_group_kernel");
     } else {
       vkern<<<kSMs * per_sm, 256, 0, st>>>(
           d, L, n_loc, plan.token_offsets, nb + 1, b, n_tok, plan.task_pair, static_cast<const __nv_bfloat16*>(Vs),
-          y, b > 0 ? 1 : accumulate, work + 1 + b, env_int("OMNIMOE_V_HINT", 1));
+          y, b > 0 ? 1 : accumulate, work + 1 + b);
       OMNI_CHECK_LAUNCH("expert_vslice_kernel");
     }
   }

@@ -52,7 +52,7 @@ class LibOps:
         return om.ep_unpack(rec, R, task_off, tok_off)
 
     def expert(self, x_recv, W_loc, V_loc, ids, gate, tok, n_loc):
-        """V_loc is [n_loc][d], or [d/32][n_loc][32] when dims.v_layout is V_SLICED
+        """V_loc is [n_loc][d], or [d/64][n_loc][64] when dims.v_layout is V_SLICED
         (om.pack_v of the shard); the SLICED executor writes every row of y."""
         sliced = self.dims.v_layout == om.V_SLICED
         rows = x_recv.shape[0]

@@ -420,10 +420,10 @@ def expert_fwd_tokens(dims: LayerDims, x, W, V, idx, gate, y_routed=None, accumu
 
 
 def pack_v(dims: LayerDims, V):
-    """V [n][d] -> the SLICED layout [d/32][n][32] (include/omnimoe.h omnimoe_pack_v)."""
+    """V [n][d] -> the SLICED layout [d/64][n][64] (include/omnimoe.h omnimoe_pack_v)."""
     n = V.numel() // dims.d
     _req(V, "V", dims.torch_dtype, n * dims.d)
-    out = torch.empty((dims.d // 32, n, 32), dtype=V.dtype, device=V.device)
+    out = torch.empty((dims.d // 64, n, 64), dtype=V.dtype, device=V.device)
     dc = dims.c()
     _check(load().omnimoe_pack_v(ctypes.byref(dc), n, _ptr(V), _ptr(out), _stream()), "pack_v")
     return out

@@ -403,7 +403,7 @@ def test_pack_v_is_a_pure_relayout():
     inp = make_inputs(dims, 1, 5, skip=("x", "subkeys", "W"))
     Vs = om.pack_v(dims, inp["V"])
     torch.cuda.synchronize()
-    want = inp["V"].view(dims.N, dims.d // 32, 32).permute(1, 0, 2).contiguous()  # test-side re-layout
+    want = inp["V"].view(dims.N, dims.d // 64, 64).permute(1, 0, 2).contiguous()  # test-side re-layout
     assert torch.equal(Vs.view(torch.int16), want.view(torch.int16))
 
 
@@ -424,7 +424,7 @@ def v_mode(request, monkeypatch):
 
 
 @pytest.mark.parametrize("B", [0, 2, 512])
-@pytest.mark.parametrize("d,act", [(64, om.SILU), (96, om.SILU), (1024, om.SILU), (2048, om.SILU),
+@pytest.mark.parametrize("d,act", [(64, om.SILU), (192, om.SILU), (1024, om.SILU), (2048, om.SILU),
                                    (64, om.IDENTITY)])
 @pytest.mark.parametrize("accumulate", [False, True])
 def test_expert_fwd_sliced_given_plan(d, act, B, accumulate, v_geom, v_mode):
@@ -438,7 +438,7 @@ def test_expert_fwd_sliced_given_plan(d, act, B, accumulate, v_geom, v_mode):
     ids[7] = ids[3]  # two tokens with identical expert lists
     gates = rng.random((L, HK)).astype(np.float32)
     plan = om.schedule(dims, torch.from_numpy(ids).cuda().reshape(-1), torch.from_numpy(gates).cuda().reshape(-1))
-    want = -(-(N * 64) // v_geom["v_band_bytes"]) if v_geom else 1
+    want = -(-(N * 128) // v_geom["v_band_bytes"]) if v_geom else 1
     assert om.v_bands(dims, N, L) == want
     Vs = om.pack_v(dims, inp["V"])
     y0 = torch.randn(L, d, device="cuda") if accumulate else None
@@ -536,6 +536,8 @@ def test_sliced_layout_errors():
     with pytest.raises(om.OmniMoEError, match="INVALID_ARGUMENT"):
         om.workspace_size(om.LayerDims(d=64, n_rows=4, n_cols=4, top_k=2, expert_kernel=om.EXPERT_SLICED), 8,
                           om.WS_LAYER)
+    with pytest.raises(om.OmniMoEError, match="UNSUPPORTED"):  # 64-column slices: d % 64 == 0
+        om.workspace_size(om.LayerDims(d=96, n_rows=4, n_cols=4, top_k=2, v_layout=om.V_SLICED), 8, om.WS_LAYER)
 
 
 @pytest.mark.parametrize("name,L", [("C1", 256), ("C3a", 64), ("C4", 16), ("C4pp", 48), ("C5", 48)])

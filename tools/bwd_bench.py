@@ -45,6 +45,6 @@ M = L * dims.n_heads * dims.top_k
 na = int(plan["n_active"].item())
 d = dims.d
 hbm = na * d * 2 * 2 + na * d * 4 * 2 + L * d * 2 * 2 + L * d * 4 + 16 * M  # W, V once; dW, dV; x, dy; dx; plan
-l2 = M * d * 2 * 2 + M * d * 2 + 8 * M * (d // 32)  # x and dy rows per task; W slice per task; pairs per slice
+l2 = M * d * 2 * 2 + M * d * 2 + 8 * M * (d // 64)  # x and dy rows per task; W slice per task; pairs per slice
 print(json.dumps({"config": name, "layer_bwd_ms": sum(part_ms.values()), "part_ms": part_ms, "ms": t, "tasks": M, "n_active": na, "algorithmic_hbm_bytes": hbm,
                   "hbm_gbs": hbm / t / 1e6, "l2_dataflow_bytes": l2, "l2_gbs": l2 / t / 1e6}))
