@@ -3,11 +3,17 @@
 // Tasks t = ((l*h)+head)*K + k arrive in token-major order (Eq.Tasks,
 // PAPER:261-265).  a4: per-local-expert histogram, exclusive scan ->
 // expert_offsets, compaction of active experts (E_active).
-// a5: stable LSD radix sort (8-bit digits, "radix sort") of the
-// local expert ids with the task index as payload; stability over the
-// token-major input gives tokens ascending inside each expert segment, i.e.
-// Eq.Sort with group size B = 1 (reading Q14).  Tasks outside the local
-// expert range get the sentinel key n_loc and sort behind every segment.
+// a5, B = 1 (the expert-major plan): a counting sort -- each task claims a slot of its
+// expert's segment [offsets[e], offsets[e+1]) with an atomic countdown (arbitrary order
+// inside the segment), then every segment is sorted by task index, which restores the
+// order a stable sort of the token-major task list gives (tokens ascending inside each
+// expert segment, Eq.Sort with group size B = 1, reading Q14), and the plan arrays are
+// written from it.  One pass over the tasks instead of the three (histogram + scatter)
+// rounds of an 8-bit LSD radix sort.
+// a5, B > 1: stable LSD radix sort (8-bit digits, "radix sort") of the (token
+// block, group) keys with the task index as payload; stability over the token-major
+// input gives tokens ascending inside each group.  Tasks outside the local expert range
+// get the sentinel key and sort behind every segment.
 // Everything is deterministic (no order-dependent atomics reach the output).
 #include "schedule.cuh"
 
@@ -22,16 +28,19 @@ constexpr int kRadixThreads = 256, kRadixRounds = 16, kRadixTile = kRadixThreads
 // task's V-order position, task_pair[dest].x = its local expert id (-1 outside),
 // seg[l*(nb+1) + b] = start of segment (l, b).
 __global__ void band_partition_kernel(const int32_t* __restrict__ ids, int64_t begin, int64_t n_loc,
-                                      const int32_t* __restrict__ tok_off, int64_t n_tok, int nb, int64_t band_size,
+                                      const int32_t* __restrict__ tok_off, int64_t hk, int64_t M, int64_t n_tok,
+                                      int nb, int64_t band_size,
                                       int32_t* __restrict__ dest, int32_t* __restrict__ task_pair,
                                       int32_t* __restrict__ seg) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
-  if (gw == 0 && lane == 0) seg[n_tok * (nb + 1)] = tok_off[n_tok];
+  // tok_off == nullptr: the default token of task t is t / hk
+  auto toff = [&](int64_t l) { return tok_off ? (int64_t)tok_off[l] : std::min<int64_t>(l * hk, M); };
+  if (gw == 0 && lane == 0) seg[n_tok * (nb + 1)] = (int32_t)toff(n_tok);
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t l = gw; l < n_tok; l += nw) {
-    const int beg = tok_off[l], end = tok_off[l + 1];
+    const int beg = (int)toff(l), end = (int)toff(l + 1);
     auto band_of = [&](int t) {
       const int64_t e = (int64_t)ids[t] - begin;
       return (e >= 0 && e < n_loc) ? (int)(e / band_size) : nb;
@@ -76,7 +85,7 @@ __global__ void hist_keys_kernel(const int32_t* __restrict__ ids, int64_t M, int
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = (int64_t)ids[t] - begin;
     const bool in = e >= 0 && e < n_loc;
-    keys[t] = in ? (uint32_t)e : (uint32_t)n_loc;
+    if (keys) keys[t] = in ? (uint32_t)e : (uint32_t)n_loc;
     if (task_pair) task_pair[2 * t] = in ? (int32_t)e : -1;  // one band: V order = task order
     if (in) atomicAdd(&cnt[e], 1);
   }
@@ -324,6 +333,152 @@ __global__ void gather_plan_kernel(const int32_t* __restrict__ order, int64_t M,
   }
 }
 
+// B = 1: task t -> a slot of its expert's segment (the countdown of cnt[e] gives slots
+// n_e - 1 .. 0 in arbitrary order; segment_sort_kernel restores task order)
+__global__ void count_scatter_kernel(const int32_t* __restrict__ ids, const float* __restrict__ gate, int64_t M,
+                                     int64_t begin, int64_t n_loc, const int32_t* __restrict__ off,
+                                     int32_t* __restrict__ cnt, int2* __restrict__ perm) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < M; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = (int64_t)ids[t] - begin;
+    if (e >= 0 && e < n_loc) perm[off[e] + atomicSub(&cnt[e], 1) - 1] = make_int2((int32_t)t, __float_as_int(gate[t]));
+  }
+}
+
+// a segment of n <= 16 (task, gate) pairs sorted by task index in registers: 16-input
+// bitonic network on 64-bit words (task index in the high half: the indices are distinct)
+__device__ __forceinline__ void cswap64(unsigned long long& x, unsigned long long& y, bool up) {
+  const bool sw = up ? (x > y) : (x < y);
+  const unsigned long long tx = x;
+  x = sw ? y : x;
+  y = sw ? tx : y;
+}
+__device__ __forceinline__ void sort16(unsigned long long (&v)[16]) {
+#pragma unroll
+  for (int k = 2; k <= 16; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int l = i ^ j;
+        if (l > i) cswap64(v[i], v[l], (i & k) == 0);
+      }
+}
+__device__ __forceinline__ unsigned long long pack_tg(int2 p) {
+  return ((unsigned long long)(uint32_t)p.x << 32) | (uint32_t)p.y;
+}
+
+// one warp per 32 consecutive active experts.  Their segments are contiguous in the plan
+// ([off[e_0], off[e_31 + 1]): inactive experts have empty segments), so the warp stages
+// the region's (task, gate) pairs in shared memory with coalesced loads, every lane sorts
+// its expert's segment (n <= 16, E n = eta ~ 8) in registers, and the warp writes the
+// region's plan entries with coalesced stores.  Regions over the staging capacity and
+// segments over 16 tasks take the per-lane / queued paths.
+constexpr int kSegCap = 512;  // pairs staged per warp (E region = 32 eta ~ 256)
+__global__ void __launch_bounds__(256)
+    segment_sort_kernel(const int32_t* __restrict__ active, const int32_t* __restrict__ n_active_p,
+                        const int32_t* __restrict__ off, const int2* __restrict__ perm,
+                        const int32_t* __restrict__ token, int64_t hk, const int32_t* __restrict__ dest,
+                        int32_t* __restrict__ sorted_token, float* __restrict__ sorted_gate,
+                        int32_t* __restrict__ sorted_expert, int32_t* __restrict__ sorted_task,
+                        int32_t* __restrict__ big_list, int32_t* __restrict__ big_count) {
+  __shared__ int2 stage[8][kSegCap];
+  __shared__ int32_t eid[8][kSegCap];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int2* st = stage[wib];
+  int32_t* ei = eid[wib];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  const int na = *n_active_p;
+  for (int i = lane; i < kSegCap; i += 32) ei[i] = -1;
+  __syncwarp();
+  auto emit = [&](int64_t p, int2 tg, int e) {
+    const int32_t t = tg.x;
+    sorted_token[p] = token ? token[t] : (int32_t)(t / hk);
+    sorted_gate[p] = __int_as_float(tg.y);
+    sorted_expert[p] = e;
+    if (sorted_task) sorted_task[p] = dest ? dest[t] : t;
+  };
+  for (int64_t base = gw * 32; base < na; base += nw * 32) {
+    const bool valid = base + lane < na;
+    const int e = valid ? active[base + lane] : 0;
+    const int a = valid ? off[e] : 0, n = valid ? off[e + 1] - a : 0;
+    const int A0 = __shfl_sync(0xffffffffu, a, 0);
+    const int last = (int)(na - 1 - base < 31 ? na - 1 - base : 31);
+    const int A1 = __shfl_sync(0xffffffffu, a + n, last);
+    const bool big = n > 16;
+    if (big) big_list[atomicAdd(big_count, 1)] = e;
+    if (A1 - A0 <= kSegCap) {
+      for (int p = A0 + lane; p < A1; p += 32) st[p - A0] = perm[p];
+      __syncwarp();
+      if (!big && n > 0) {
+        unsigned long long v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = i < n ? pack_tg(st[a - A0 + i]) : ~0ull;
+        sort16(v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i < n) {
+            st[a - A0 + i] = make_int2((int32_t)(v[i] >> 32), (int32_t)(uint32_t)v[i]);
+            ei[a - A0 + i] = e;
+          }
+      }
+      __syncwarp();
+      for (int p = A0 + lane; p < A1; p += 32) {
+        // big segments are written by segment_sort_big_kernel
+        if (ei[p - A0] >= 0) emit(p, st[p - A0], ei[p - A0]);
+      }
+      __syncwarp();
+      for (int p = A0 + lane; p < A1; p += 32) ei[p - A0] = -1;  // reset for the next region
+      __syncwarp();
+    } else if (!big && n > 0) {  // region over capacity: this lane's segment from global memory
+      unsigned long long v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = i < n ? pack_tg(perm[a + i]) : ~0ull;
+      sort16(v);
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (i < n) emit(a + i, make_int2((int32_t)(v[i] >> 32), (int32_t)(uint32_t)v[i]), e);
+    }
+  }
+}
+
+// segments longer than 16 tasks (the tail of the per-expert load: ~0.4 % of the active
+// experts at eta = 8; or skewed routing): one WARP per segment; the rank of every task
+// index is the number of smaller ones, counted with shuffles over 32-wide chunks of the
+// segment -- O(n^2 / 32) per segment, which the load statistics keep small
+__global__ void __launch_bounds__(256)
+    segment_sort_big_kernel(const int32_t* __restrict__ big_list, const int32_t* __restrict__ big_count,
+                            const int32_t* __restrict__ off, const int2* __restrict__ perm,
+                            const int32_t* __restrict__ token, int64_t hk, const int32_t* __restrict__ dest,
+                            int32_t* __restrict__ sorted_token, float* __restrict__ sorted_gate,
+                            int32_t* __restrict__ sorted_expert, int32_t* __restrict__ sorted_task) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  const int nbig = *big_count;
+  for (int64_t q = gw; q < nbig; q += nw) {
+    const int e = big_list[q];
+    const int a = off[e], n = off[e + 1] - a;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+      const int i = c0 + lane;
+      const int2 tg = i < n ? perm[a + i] : make_int2(INT32_MAX, 0);
+      int rank = 0;
+      for (int j0 = 0; j0 < n; j0 += 32) {
+        const int32_t u = j0 + lane < n ? perm[a + j0 + lane].x : INT32_MAX;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) rank += __shfl_sync(0xffffffffu, u, k) < tg.x;
+      }
+      if (i < n) {
+        const int64_t p = a + rank;
+        sorted_token[p] = token ? token[tg.x] : (int32_t)(tg.x / hk);
+        sorted_gate[p] = __int_as_float(tg.y);
+        sorted_expert[p] = e;
+        if (sorted_task) sorted_task[p] = dest ? dest[tg.x] : tg.x;
+      }
+    }
+  }
+}
+
 // load metrics of a plan: per block, in a fixed order, the number of
 // used experts and sum_{c>0} (c/M) log(n_loc c / M) over the block's experts
 __global__ void __launch_bounds__(256)
@@ -436,7 +591,7 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
     return OMNIMOE_ERR_CUDA;
   }
   if (M > 0) {
-    hist_keys_kernel<<<grid_for(M, 256), 256, 0, st>>>(ids, M, plan.expert_begin, n_loc, k0, cnt,
+    hist_keys_kernel<<<grid_for(M, 256), 256, 0, st>>>(ids, M, plan.expert_begin, n_loc, B > 1 ? k0 : nullptr, cnt,
                                                        vorder && n_bands == 1 ? plan.task_pair : nullptr);
     OMNI_CHECK_LAUNCH("hist_keys_kernel");
   }
@@ -450,12 +605,14 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
       token_offsets_kernel<<<grid_for(M + 1, 256), 256, 0, st>>>(M, token, hk, n_tok, plan.token_offsets, 2);
       OMNI_CHECK_LAUNCH("token_offsets_kernel");
     } else {
-      token_offsets_kernel<<<grid_for(M + 1, 256), 256, 0, st>>>(M, token, hk, n_tok, tok_off, 1);
-      OMNI_CHECK_LAUNCH("token_offsets_kernel");
+      if (token) {
+        token_offsets_kernel<<<grid_for(M + 1, 256), 256, 0, st>>>(M, token, hk, n_tok, tok_off, 1);
+        OMNI_CHECK_LAUNCH("token_offsets_kernel");
+      }
       const int64_t band_size = (n_loc + n_bands - 1) / n_bands;
       band_partition_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((n_tok + 7) / 8, kSMs * 16)), 256, 0,
-                              st>>>(ids, plan.expert_begin, n_loc, tok_off, n_tok, (int)n_bands, band_size, dest,
-                                    plan.task_pair, plan.token_offsets);
+                              st>>>(ids, plan.expert_begin, n_loc, token ? tok_off : nullptr, hk, M, n_tok,
+                                    (int)n_bands, band_size, dest, plan.task_pair, plan.token_offsets);
       OMNI_CHECK_LAUNCH("band_partition_kernel");
     }
   }
@@ -464,6 +621,24 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
   // a4: active-expert compaction and |E_active|
   OMNI_TRY(scan<1>(cnt, n_loc, plan.active, plan.n_active, tiles, st));
   if (M == 0) return OMNIMOE_OK;
+  if (B == 1) {  // a5 as a counting sort + per-segment sort (see the top of this file)
+    int2* perm = reinterpret_cast<int2*>(k0);  // k0 and k1 are adjacent: M (task, gate) pairs
+    int32_t* big = v0;                 // queued long segments (<= n_active entries <= M)
+    int32_t* big_count = cnt + n_loc;  // cnt[n_loc] is 0 after the scans and free now
+    count_scatter_kernel<<<grid_for(M, 256), 256, 0, st>>>(ids, gate, M, plan.expert_begin, n_loc,
+                                                          plan.expert_offsets, cnt, perm);
+    OMNI_CHECK_LAUNCH("count_scatter_kernel");
+    const int32_t* dst = vorder && n_bands > 1 ? dest : nullptr;
+    int32_t* stask = vorder ? plan.sorted_task : nullptr;
+    segment_sort_kernel<<<kSMs * 4, 256, 0, st>>>(plan.active, plan.n_active, plan.expert_offsets, perm, token, hk,
+                                                  dst, plan.sorted_token, plan.sorted_gate, plan.sorted_expert, stask,
+                                                  big, big_count);
+    OMNI_CHECK_LAUNCH("segment_sort_kernel");
+    segment_sort_big_kernel<<<kSMs * 4, 256, 0, st>>>(big, big_count, plan.expert_offsets, perm, token, hk, dst,
+                                                 plan.sorted_token, plan.sorted_gate, plan.sorted_expert, stask);
+    OMNI_CHECK_LAUNCH("segment_sort_big_kernel");
+    return OMNIMOE_OK;
+  }
   // a4: group of each expert = rank among the active experts / B
   int64_t n_keys = n_loc;  // largest key value (the sentinel)
   if (B > 1) {
