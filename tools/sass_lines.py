@@ -1,14 +1,19 @@
 """Attribute ncu per-SASS samples/instructions to CUDA source lines.
-    python tools/sass_lines.py <nvdisasm --print-line-info output> <ncu --page source --csv> <kernel substr> <src file>"""
+    python tools/sass_lines.py <cubin> <ncu --page source --csv --print-source sass> <kernel substr> <src file> [top]
+The cubin is disassembled with nvdisasm --print-line-info; the kernel is the first
+.text section whose name contains <kernel substr> (and 'ILb1' / 'ILb0' etc. if given)."""
 import collections
 import csv
 import re
+import subprocess
 import sys
 
-sass, prof, kname, srcf = sys.argv[1:5]
-txt = open(sass).read().split('\n')
-start = [i for i, l in enumerate(txt) if l.startswith('//----') and kname in l][0]
-end = [i for i, l in enumerate(txt[start + 1:], start + 1) if l.startswith('//----')]
+cubin, prof, kname, srcf = sys.argv[1:5]
+top = int(sys.argv[5]) if len(sys.argv) > 5 else 30
+txt = subprocess.run(["/usr/local/cuda/bin/nvdisasm", "--print-line-info", cubin], capture_output=True,
+                     text=True).stdout.split('\n')
+start = [i for i, l in enumerate(txt) if '.section' in l and '.text.' in l and kname in l][0]
+end = [i for i, l in enumerate(txt[start + 1:], start + 1) if '.section' in l]
 end = end[0] if end else len(txt)
 addr2line, cur = {}, None
 for l in txt[start:end]:
@@ -26,7 +31,7 @@ samp, ins, base = collections.Counter(), collections.Counter(), None
 for r in rows[2:]:
     try:
         a = int(r[ai], 16)
-    except ValueError:
+    except (ValueError, IndexError):
         continue
     base = a if base is None else base
     ln = addr2line.get(a - base, -1)
@@ -34,6 +39,6 @@ for r in rows[2:]:
     ins[ln] += float(r[ii] or 0)
 tot, toti = sum(samp.values()), sum(ins.values())
 src = open(srcf).read().split('\n')
-print('samples', tot, 'instructions', toti)
-for ln, s_ in samp.most_common(int(sys.argv[5]) if len(sys.argv) > 5 else 30):
+print('samples', tot, 'warp instructions', toti)
+for ln, s_ in samp.most_common(top):
     print(f"{ln:5d} {100 * s_ / tot:5.1f}% samp {100 * ins[ln] / toti:5.1f}% ins | {src[ln - 1].strip()[:100] if ln > 0 else ''}")
