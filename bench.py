@@ -127,7 +127,7 @@ def ncu_traffic(config, kernel):
 
 
 # ---------------------------------------------------------------- CPU oracle
-def cpu_oracle_rate(w, target_s, max_tokens, nthreads, inp=None, gpu=None):
+def cpu_oracle_rate(w, target_s, max_tokens, nthreads, inp=None, gpu=None):  # noqa: C901
     """The oracle layer (as it stands) on a bounded token sample.  Expert rows are
     taken from the seeded generator (the device twin's tables when ``inp`` holds
     them -- bit-identical to the host generator, tests/test_gpu_parity.py -- else
@@ -145,12 +145,6 @@ def cpu_oracle_rate(w, target_s, max_tokens, nthreads, inp=None, gpu=None):
     sub = host_rows(dims, w.seed, "subkeys").reshape(dims.n_heads, R, dims.d)
     wgu = host_rows(dims, w.seed, "w_gate_up") if dims.d_ff else None
     wdn = host_rows(dims, w.seed, "w_down") if dims.d_ff else None
-
-    if inp is None and torch.cuda.is_available():
-        # the generator's device twin fills the expert tables fast; the rows the
-        # sample needs are copied to the host (inputs only -- the oracle computes)
-        from synth.workloads import make_inputs
-        inp = make_inputs(dims, 1, w.seed, skip=("x", "subkeys", "w_gate_up", "w_down"))
 
     def rows(name, used):
         if inp is not None and name in inp:
@@ -196,10 +190,7 @@ def run_reference(args):
     w = configs.get(args.config)
     nth = os.cpu_count() or 1
     per_step_s = max(2.0, args.ref_seconds / max(args.steps, 1))
-    tables = None
-    if torch.cuda.is_available():
-        from synth.workloads import make_inputs
-        tables = make_inputs(w.dims, 1, w.seed, skip=("x", "subkeys", "w_gate_up", "w_down"))
+    tables = None  # expert rows from the generator's host twin: nothing of this arm runs on the GPU
     cpu_oracle_rate(w, 0.5, 32, nth, tables)  # warm-up (page-in, thread pool)
     rates, toks = [], 0
     for _ in range(args.steps):
@@ -465,14 +456,21 @@ def bench_single(args, w, lr):
 
 
 # ---------------------------------------------------------------- N > 1
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md)
+
+
 def bench_multi(args, w, ws, rk, lr):
+    """configs[4] (expert-sharded scale-out): the GLOBAL batch of w.L tokens split over
+    the ranks (strong scaling), expert rows N/R per rank, NCCL all-to-all dispatch and
+    combine."""
     from paper_2602_05711_b200 import distributed as ep, omnimoe as om
     from synth.workloads import make_inputs
     dims, L = w.dims, w.L
-    if dims.N % ws:
-        raise SystemExit(f"N={dims.N} not divisible by {ws} ranks")
-    n_per = dims.N // ws
-    inp = make_inputs(dims, L, w.seed, token_begin=rk * L, expert_rows=(rk * n_per, (rk + 1) * n_per))
+    if dims.N % ws or L % ws:
+        raise SystemExit(f"N={dims.N} and L={L} must be divisible by {ws} ranks")
+    n_per, L_loc = dims.N // ws, L // ws
+    inp = make_inputs(dims, L_loc, w.seed, token_begin=rk * L_loc, expert_rows=(rk * n_per, (rk + 1) * n_per))
+    oinp = {"W": inp["W"], "V": inp["V"]} if rk == 0 else None  # rows [0, n_per) for the oracle sample
     if dims.v_layout == om.V_SLICED:  # one-time re-layout of this rank's V shard
         inp["V"] = om.pack_v(dims, inp["V"])
         torch.cuda.synchronize()
@@ -492,7 +490,7 @@ def bench_multi(args, w, ws, rk, lr):
     dist.barrier()
     launches0 = om.LAUNCHES
     phase = {}
-    with ClockSampler(lr) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         ms_steps = []
         for i in range(args.steps):
             flush.zero_()
@@ -515,6 +513,18 @@ def bench_multi(args, w, ws, rk, lr):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     phase_ms = {k: statistics.median(v) for k, v in phase.items()}
+    # message sizes of one more step: rows / records this rank sent to OTHER ranks (its own
+    # block stays local), the bf16 partial rows it sent back; the records it processed
+    y_out, rst = ep.ep_layer_fwd(ops, comm, inp["x"], inp["subkeys"], inp["W"], inp["V"], n_per, return_state=True)
+    torch.cuda.synchronize()
+    cnt = ops.last_route  # this rank's routing (that step)
+    eb = 2 if dims.dtype == 0 else 4
+    sent_rows = sum(c for s_, c in enumerate(rst.send_tok) if s_ != rk)
+    sent_recs = sum(c for s_, c in enumerate(rst.send_task) if s_ != rk)
+    back_rows = sum(c for s_, c in enumerate(rst.recv_tok) if s_ != rk)
+    nvl_bytes = sent_rows * dims.d * eb + sent_recs * 12 + back_rows * dims.d * 2
+    a2a_ms = phase_ms.get("all_to_all_dispatch", 0.0) + phase_ms.get("all_to_all_combine", 0.0)
+    m_loc, rows_loc = sum(rst.recv_task), sum(rst.recv_tok)
     e2e = None
     if not args.no_e2e:
         xh = inp["x"].cpu().pin_memory()
@@ -533,20 +543,48 @@ def bench_multi(args, w, ws, rk, lr):
             tot.append(a.elapsed_time(b))
         te = torch.tensor([statistics.mean(tot[1:])], dtype=torch.float64, device="cuda")
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        eb = 2 if dims.dtype == 0 else 4
-        e2e = {"value": ws * L / (float(te.item()) / 1000.0), "unit": "tokens/s", "ms_per_step": float(te.item()),
-               "h2d_bytes_per_step": ws * L * dims.d * eb, "d2h_bytes_per_step": ws * L * dims.d * eb}
+        e2e = {"value": L / (float(te.item()) / 1000.0), "unit": "tokens/s", "ms_per_step": float(te.item()),
+               "h2d_bytes_per_step": L * dims.d * eb, "d2h_bytes_per_step": L * dims.d * eb}
         del yh
     if rk == 0:
-        line = {"metric": METRIC, "value": ws * L / (ms / 1000.0), "unit": "tokens/s", "n_gpus": ws,
+        pk = peaks()
+        exp_ms = phase_ms.get("expert", 0.0)
+        import math
+        n_act_est = n_per * -math.expm1(-m_loc / n_per)  # E|active experts of the shard| (uniform routing)
+        # W and V rows of the active experts once, the received x rows, fp32 partial rows, 24 B per task
+        a6_bytes = 2 * n_act_est * dims.d * eb + rows_loc * dims.d * (eb + 4) + 24 * m_loc
+        roofline = {"bound": "hbm", "achieved": a6_bytes / (exp_ms / 1e3) / 1e9 if exp_ms else None,
+                    "peak": pk["hbm"], "unit": "GB/s",
+                    "frac": a6_bytes / (exp_ms / 1e3) / 1e9 / pk["hbm"] if exp_ms else None, "traffic": None,
+                    "kernel": "rank 0 expert phase (unpack + schedule + SLICED a6 + bf16 partials)",
+                    "algorithmic_bytes_per_launch": a6_bytes, "avg_launch_ms": exp_ms,
+                    "peak_source": pk["src"] + " hbm_gbs (copy)",
+                    "nvlink": {"bytes_per_step_rank0": nvl_bytes, "a2a_ms": a2a_ms,
+                               "achieved_gbs": nvl_bytes / (a2a_ms / 1e3) / 1e9 if a2a_ms else None,
+                               "peak_gbs": NVLINK_PEER_GBS,
+                               "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}}
+        cpu = parity = None
+        if not args.no_cpu_baseline:
+            nth = os.cpu_count() or 1
+            gpu = (y_out.float().cpu().numpy(), cnt[0].cpu().numpy(), cnt[1].cpu().numpy())
+            sub_w = dataclasses.replace(w, L=L_loc)
+            rate, done, tcpu, parity = cpu_oracle_rate(sub_w, args.cpu_seconds, 1 << 20, nth, None, gpu)
+            parity["note"] = "rank 0's tokens: EP layer output vs oracle.layer (reading Q10 / Q17)"
+            cpu = {"value": rate, "unit": "tokens/s", "cores": nth, "kind": "oracle",
+                   "sample": f"{done} tokens of {w.name} (rank 0's slice): {tcpu:.1f} s of oracle time on {nth} threads"}
+        line = {"metric": METRIC, "value": L / (ms / 1000.0), "unit": "tokens/s", "n_gpus": ws,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "latency_ms": ms,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded counter-based generator, DESIGN.md §3)",
                 "config": dict(_config_dict(w, f"ep{ws} (experts row-sharded, tokens data-parallel, "
-                                               f"NCCL all-to-all)"), global_tokens=ws * L),
-                "phase_ms_rank0": phase_ms, "roofline": None, "e2e": e2e, "cpu_baseline": None,
-                "gpu_launches": launches, "launches_per_step": launches / max(args.steps, 1),
+                                               f"{args.backend} all-to-all)"), global_tokens=L, tokens_per_gpu=L_loc,
+                               backend=args.backend),
+                "phase_ms_rank0": phase_ms, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
+                "parity": parity, "gpu_launches": launches, "launches_per_step": launches / max(args.steps, 1),
                 "clocks": clk.summary()}
+        if args.backend == "gloo":
+            line["dry_run"] = ("gloo with host-staged all-to-alls (ranks may share a GPU): a protocol run, "
+                               "not an NVLink measurement")
         print(json.dumps(line), flush=True)
     dist.barrier()
     return 0
@@ -557,7 +595,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C3a")
+    ap.add_argument("--config", default=None,
+                    help="workload (default: C3a on one GPU -- configs[2]; C5 over N > 1 GPUs -- configs[4], "
+                         "the expert-sharded scale-out, strong scaling)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N > 1 process group: nccl (the product), or gloo with host-staged all-to-alls (dry run)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle time of the cpu_baseline sample")
     ap.add_argument("--ref-seconds", type=float, default=60.0, help="total oracle time of --impl reference")
@@ -578,12 +620,18 @@ def main():
                     help="SLICED pass V: L2 budget of one band step (dims.v_band_bytes; 0 = library choice)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
+    if args.config is None:
+        args.config = "C5" if rank_info()[0] > 1 else "C3a"
     if args.impl == "reference":
         return run_reference(args)
     ws, rk, lr = rank_info()
-    torch.cuda.set_device(lr)
+    dev = lr % max(torch.cuda.device_count(), 1)  # (the gloo dry run may put several ranks on one GPU)
+    torch.cuda.set_device(dev)
     if ws > 1:
-        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", lr))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo", init_method="env://")
     from paper_2602_05711_b200 import build, configs
     if rk == 0:
         build.build()

@@ -320,6 +320,16 @@ omnimoe_status omnimoe_shared_mlp(const omnimoe_dims* dims, int64_t L, const voi
                                   const void* w_gate_up, const void* w_down, const float* y_routed,
                                   void* y, void* ws, size_t ws_bytes, omnimoe_stream_t stream);
 /*   ws: omnimoe_workspace_size(dims, L, OMNIMOE_WS_MLP) bytes (holds H). */
+/* The same two GEMMs as separate calls, so that GEMM-1 (which needs only x) can run
+ * while the routed branch is still in flight (the expert-parallel driver overlaps it
+ * with the dispatch all-to-all):
+ *   omnimoe_shared_mlp_hidden: H = silu(x W_gate^T) * (x W_up^T) into H (H_bytes >=
+ *     omnimoe_workspace_size(dims, L, OMNIMOE_WS_MLP); layout opaque);
+ *   omnimoe_shared_mlp_out:    y = H W_down^T + y_routed (y_routed nullable). */
+omnimoe_status omnimoe_shared_mlp_hidden(const omnimoe_dims* dims, int64_t L, const void* x, const void* w_gate_up,
+                                         void* H, size_t H_bytes, omnimoe_stream_t stream);
+omnimoe_status omnimoe_shared_mlp_out(const omnimoe_dims* dims, int64_t L, const void* H, size_t H_bytes,
+                                      const void* w_down, const float* y_routed, void* y, omnimoe_stream_t stream);
 
 /* The paper's ablation "w/o Expert-Centric Scheduling": the routed
  * branch token by token straight from the routing decision (idx, gate [L][h*K],
@@ -407,11 +417,15 @@ omnimoe_status omnimoe_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A,
  *   inv      int32 [R][L]    slot of token l in s's block, -1 if none
  *   offsets  int32 [2R+2]    token block starts [0..R] (R+1 entries), then task
  *                            block starts [0..R]
+ *   counts   int64 [R][2]    (nullable) rows and records per destination -- the
+ *                            split sizes of the all-to-alls, ready to be exchanged
+ *                            device to device (one host read per forward for both
+ *                            directions)
  * Sizes are bounded by R*L rows and L*h*K records.  ws: omnimoe_ep_pack_workspace_size. */
 omnimoe_status omnimoe_ep_pack_workspace_size(int64_t L, int32_t R, size_t* bytes);
 omnimoe_status omnimoe_ep_pack(const omnimoe_dims* dims, int64_t L, int32_t R, const void* x,
                                const int32_t* idx, const float* gate, void* x_send, int32_t* rec_send,
-                               int32_t* inv, int32_t* offsets, void* ws, size_t ws_bytes,
+                               int32_t* inv, int32_t* offsets, int64_t* counts, void* ws, size_t ws_bytes,
                                omnimoe_stream_t stream);
 /* Received records (concatenated by source rank; task_off/tok_off int64 [R+1] are
  * the per-source block starts of the received records / x rows, device memory)
@@ -420,10 +434,15 @@ omnimoe_status omnimoe_ep_pack(const omnimoe_dims* dims, int64_t L, int32_t R, c
 omnimoe_status omnimoe_ep_unpack(int64_t M, int32_t R, const int32_t* rec, const int64_t* task_off,
                                  const int64_t* tok_off, int32_t* ids, float* gate, int32_t* token,
                                  omnimoe_stream_t stream);
+/* The partial output rows of a shard, fp32 [rows][d] -> bf16 [rows][d] (round to
+ * nearest even) for the return all-to-all: half the bytes of fp32. */
+omnimoe_status omnimoe_ep_partials(int64_t rows, const omnimoe_dims* dims, const float* y_part, void* y_bf16,
+                                   omnimoe_stream_t stream);
 /* y_routed[l] = sum over s = 0..R-1 (in that order) of y_ret[tok_off[s] + inv[s][l]]
- * (skipped where inv = -1): the returned partial rows, fp32 [rows][d]. */
-omnimoe_status omnimoe_ep_combine(const omnimoe_dims* dims, int64_t L, int32_t R, const float* y_ret,
-                                  const int32_t* inv, const int64_t* tok_off, float* y_routed,
+ * (skipped where inv = -1), accumulated in fp32: the returned partial rows [rows][d],
+ * bf16 (y_ret_bf16 != 0, from omnimoe_ep_partials) or fp32. */
+omnimoe_status omnimoe_ep_combine(const omnimoe_dims* dims, int64_t L, int32_t R, const void* y_ret,
+                                  int32_t y_ret_bf16, const int32_t* inv, const int64_t* tok_off, float* y_routed,
                                   omnimoe_stream_t stream);
 
 /* Load metrics of a plan's routing (after PKM / PEER): with c_e the

@@ -274,14 +274,21 @@ omnimoe_status route_impl(const omnimoe_dims& d, int64_t L, const void* x, const
   return launch_select(sp, smem, logits, idx, gate, score, cand, st);
 }
 
-omnimoe_status mlp_impl(const omnimoe_dims& d, int64_t L, const void* x, const void* wgu,
-                        const void* wdown, const float* y_routed, void* y, void* H, cudaStream_t st) {
+// shared MLP GEMM-1: H = SiLU(x W_gate^T) * (x W_up^T) (the bf16 pair [hi | lo] when split)
+omnimoe_status mlp_hidden(const omnimoe_dims& d, int64_t L, const void* x, const void* wgu, void* H,
+                          cudaStream_t st) {
   GemmArgs g1;
   g1.M = (int)L;
   g1.N = (int)d.d_ff;
   g1.K = (int)d.d;
   g1.out = H;
   g1.h_split = h_split(d);
+  if (d.dtype == OMNIMOE_BF16) return gemm_bf16(EPI_SWIGLU, x, wgu, g1, st);
+  return gemm_f32(EPI_SWIGLU, static_cast<const float*>(x), static_cast<const float*>(wgu), g1, st);
+}
+// shared MLP GEMM-2 + combine: y = H W_down^T + y_routed
+omnimoe_status mlp_out(const omnimoe_dims& d, int64_t L, const void* H, const void* wdown, const float* y_routed,
+                       void* y, cudaStream_t st) {
   GemmArgs g2;
   g2.M = (int)L;
   g2.N = (int)d.d;
@@ -289,12 +296,13 @@ omnimoe_status mlp_impl(const omnimoe_dims& d, int64_t L, const void* x, const v
   g2.b_kwrap = h_split(d) ? (int)d.d_ff : 0;
   g2.out = y;
   g2.addend = y_routed;
-  if (d.dtype == OMNIMOE_BF16) {
-    OMNI_TRY(gemm_bf16(EPI_SWIGLU, x, wgu, g1, st));
-    return gemm_bf16(EPI_ADD, H, wdown, g2, st);
-  }
-  OMNI_TRY(gemm_f32(EPI_SWIGLU, static_cast<const float*>(x), static_cast<const float*>(wgu), g1, st));
+  if (d.dtype == OMNIMOE_BF16) return gemm_bf16(EPI_ADD, H, wdown, g2, st);
   return gemm_f32(EPI_ADD, static_cast<const float*>(H), static_cast<const float*>(wdown), g2, st);
+}
+omnimoe_status mlp_impl(const omnimoe_dims& d, int64_t L, const void* x, const void* wgu,
+                        const void* wdown, const float* y_routed, void* y, void* H, cudaStream_t st) {
+  OMNI_TRY(mlp_hidden(d, L, x, wgu, H, st));
+  return mlp_out(d, L, H, wdown, y_routed, y, st);
 }
 
 __global__ void cast_out_kernel(const float* __restrict__ in, void* __restrict__ out, int64_t n, int bf16) {
@@ -496,6 +504,40 @@ omnimoe_status omnimoe_shared_mlp(const omnimoe_dims* dims, int64_t L, const voi
   OMNI_TRY(check_ws(ws_bytes, need, "shared_mlp"));
   OMNI_TRY(check_device());
   return mlp_impl(*dims, L, x, w_gate_up, w_down, y_routed, y, ws, (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_shared_mlp_hidden(const omnimoe_dims* dims, int64_t L, const void* x, const void* w_gate_up,
+                                         void* H, size_t H_bytes, omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  if (dims->d_ff < 1) {
+    set_error("shared_mlp_hidden needs d_ff >= 1");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (L == 0) return OMNIMOE_OK;
+  OMNI_NONNULL(x, "x");
+  OMNI_NONNULL(w_gate_up, "w_gate_up");
+  OMNI_NONNULL(H, "H");
+  OMNI_TRY(check_ws(H_bytes, h_bytes(*dims, L), "shared_mlp_hidden (H)"));
+  OMNI_TRY(check_device());
+  return mlp_hidden(*dims, L, x, w_gate_up, H, (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_shared_mlp_out(const omnimoe_dims* dims, int64_t L, const void* H, size_t H_bytes,
+                                      const void* w_down, const float* y_routed, void* y, omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  if (dims->d_ff < 1) {
+    set_error("shared_mlp_out needs d_ff >= 1");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (L == 0) return OMNIMOE_OK;
+  OMNI_NONNULL(H, "H");
+  OMNI_NONNULL(w_down, "w_down");
+  OMNI_NONNULL(y, "y");
+  OMNI_TRY(check_ws(H_bytes, h_bytes(*dims, L), "shared_mlp_out (H)"));
+  OMNI_TRY(check_device());
+  return mlp_out(*dims, L, H, w_down, y_routed, y, (cudaStream_t)stream);
 }
 
 omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* subkeys,
@@ -911,7 +953,7 @@ omnimoe_status omnimoe_ep_pack_workspace_size(int64_t L, int32_t R, size_t* byte
 
 omnimoe_status omnimoe_ep_pack(const omnimoe_dims* dims, int64_t L, int32_t R, const void* x, const int32_t* idx,
                                const float* gate, void* x_send, int32_t* rec_send, int32_t* inv, int32_t* offsets,
-                               void* ws, size_t ws_bytes, omnimoe_stream_t stream) {
+                               int64_t* counts, void* ws, size_t ws_bytes, omnimoe_stream_t stream) {
   reset_launch_count();
   OMNI_TRY(validate_dims(dims));
   const omnimoe_dims& d = *dims;
@@ -938,7 +980,7 @@ omnimoe_status omnimoe_ep_pack(const omnimoe_dims* dims, int64_t L, int32_t R, c
   OMNI_TRY(check_ws(ws_bytes, ep_pack_ws_bytes(L, R), "ep_pack"));
   OMNI_TRY(check_device());
   return ep_pack(d.dtype, L, (int)d.d, (int)(d.n_heads * d.top_k), R, N / R, x, idx, gate, x_send, rec_send, inv,
-                 offsets, ws, (cudaStream_t)stream);
+                 offsets, counts, ws, (cudaStream_t)stream);
 }
 
 omnimoe_status omnimoe_ep_unpack(int64_t M, int32_t R, const int32_t* rec, const int64_t* task_off,
@@ -960,8 +1002,23 @@ omnimoe_status omnimoe_ep_unpack(int64_t M, int32_t R, const int32_t* rec, const
   return ep_unpack(rec, M, R, task_off, tok_off, ids, gate, token, (cudaStream_t)stream);
 }
 
-omnimoe_status omnimoe_ep_combine(const omnimoe_dims* dims, int64_t L, int32_t R, const float* y_ret,
-                                  const int32_t* inv, const int64_t* tok_off, float* y_routed,
+omnimoe_status omnimoe_ep_partials(int64_t rows, const omnimoe_dims* dims, const float* y_part, void* y_bf16,
+                                   omnimoe_stream_t stream) {
+  reset_launch_count();
+  OMNI_TRY(validate_dims(dims));
+  if (rows < 0 || dims->d % 4 != 0) {
+    set_error("ep_partials: rows >= 0 and d % 4 == 0");
+    return OMNIMOE_ERR_INVALID_ARGUMENT;
+  }
+  if (rows == 0) return OMNIMOE_OK;
+  OMNI_NONNULL(y_part, "y_part");
+  OMNI_NONNULL(y_bf16, "y_bf16");
+  OMNI_TRY(check_device());
+  return ep_partials_bf16(y_part, rows * dims->d, y_bf16, (cudaStream_t)stream);
+}
+
+omnimoe_status omnimoe_ep_combine(const omnimoe_dims* dims, int64_t L, int32_t R, const void* y_ret,
+                                  int32_t y_ret_bf16, const int32_t* inv, const int64_t* tok_off, float* y_routed,
                                   omnimoe_stream_t stream) {
   reset_launch_count();
   OMNI_TRY(validate_dims(dims));
@@ -974,7 +1031,7 @@ omnimoe_status omnimoe_ep_combine(const omnimoe_dims* dims, int64_t L, int32_t R
   OMNI_NONNULL(tok_off, "tok_off");
   OMNI_NONNULL(y_routed, "y_routed");
   OMNI_TRY(check_device());
-  return ep_combine(y_ret, inv, tok_off, L, (int)dims->d, R, y_routed, (cudaStream_t)stream);
+  return ep_combine(y_ret, y_ret_bf16 != 0, inv, tok_off, L, (int)dims->d, R, y_routed, (cudaStream_t)stream);
 }
 
 omnimoe_status omnimoe_load_stats(const omnimoe_plan* plan, double* stats, void* ws, size_t ws_bytes,

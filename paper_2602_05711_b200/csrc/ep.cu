@@ -17,6 +17,7 @@
 //  ep_pack_kernel     per token (one warp): x rows to x_send, records to rec_send,
 //                     inv[s][l] = slot of token l in the message to s (or -1)
 //  ep_unpack_kernel   records -> (local id, gate, virtual token) task arrays
+//  ep_partials_kernel the partial rows of a shard, fp32 -> bf16 for the return trip
 //  ep_combine_kernel  y_routed[l] = sum over s = 0..R-1 of y_ret[s][inv[s][l]]
 #include "ep.cuh"
 
@@ -128,11 +129,15 @@ __global__ void ep_pack_kernel(const T* __restrict__ x, const int32_t* __restric
 }
 
 __global__ void ep_offsets_kernel(const int32_t* __restrict__ tok_pos, const int32_t* __restrict__ task_pos,
-                                  int64_t L, int R, int32_t* __restrict__ offsets) {
+                                  int64_t L, int R, int32_t* __restrict__ offsets, int64_t* __restrict__ counts) {
   const int s = threadIdx.x;
   if (s <= R) {
     offsets[s] = tok_pos[(int64_t)s * L];
     offsets[R + 1 + s] = task_pos[(int64_t)s * L];
+  }
+  if (counts && s < R) {  // (rows, records) per destination: the all-to-all split sizes
+    counts[2 * s] = tok_pos[(int64_t)(s + 1) * L] - tok_pos[(int64_t)s * L];
+    counts[2 * s + 1] = task_pos[(int64_t)(s + 1) * L] - task_pos[(int64_t)s * L];
   }
 }
 
@@ -148,7 +153,8 @@ __global__ void ep_unpack_kernel(const int32_t* __restrict__ rec, int64_t M, int
   }
 }
 
-__global__ void ep_combine_kernel(const float* __restrict__ y_ret, const int32_t* __restrict__ inv,
+template <bool BF16>
+__global__ void ep_combine_kernel(const void* __restrict__ y_ret, const int32_t* __restrict__ inv,
                                   const int64_t* __restrict__ tok_off, int64_t L, int d, int R,
                                   float* __restrict__ y) {
   const int64_t n4 = (int64_t)L * d / 4;
@@ -159,13 +165,26 @@ __global__ void ep_combine_kernel(const float* __restrict__ y_ret, const int32_t
     for (int s = 0; s < R; ++s) {  // fixed rank order
       const int slot = inv[(int64_t)s * L + l];
       if (slot < 0) continue;
-      const float4 v = *reinterpret_cast<const float4*>(y_ret + (tok_off[s] + slot) * d + c);
+      float4 v;
+      if (BF16) {
+        const uint2 u = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(y_ret) + (tok_off[s] + slot) * d + c);
+        v = make_float4(bf16_lo(u.x), bf16_hi(u.x), bf16_lo(u.y), bf16_hi(u.y));
+      } else {
+        v = *reinterpret_cast<const float4*>(static_cast<const float*>(y_ret) + (tok_off[s] + slot) * d + c);
+      }
       acc.x += v.x;
       acc.y += v.y;
       acc.z += v.z;
       acc.w += v.w;
     }
     reinterpret_cast<float4*>(y)[i] = acc;
+  }
+}
+
+__global__ void ep_partials_kernel(const float4* __restrict__ y, int64_t n4, uint2* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = y[i];
+    out[i] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
   }
 }
 
@@ -186,7 +205,7 @@ size_t ep_pack_ws_bytes(int64_t L, int R) {
 
 omnimoe_status ep_pack(int dtype, int64_t L, int d, int hk, int R, int64_t n_per, const void* x, const int32_t* idx,
                        const float* gate, void* x_send, int32_t* rec_send, int32_t* inv, int32_t* offsets,
-                       void* ws, cudaStream_t st) {
+                       int64_t* counts, void* ws, cudaStream_t st) {
   Carver c(ws);
   int32_t* cnt = c.take<int32_t>((size_t)R * L);
   int32_t* has = c.take<int32_t>((size_t)R * L);
@@ -208,7 +227,7 @@ omnimoe_status ep_pack(int dtype, int64_t L, int d, int hk, int R, int64_t n_per
                                                                 static_cast<float*>(x_send), rec_send, inv);
   OMNI_CHECK_LAUNCH("ep_pack_kernel");
   // offsets[0..R]: first send row (token) per destination; offsets[R+1..2R+1]: first record
-  ep_offsets_kernel<<<1, 32, 0, st>>>(tok_pos, task_pos, L, R, offsets);
+  ep_offsets_kernel<<<1, 32, 0, st>>>(tok_pos, task_pos, L, R, offsets, counts);
   OMNI_CHECK_LAUNCH("ep_offsets_kernel");
   return OMNIMOE_OK;
 }
@@ -221,11 +240,20 @@ omnimoe_status ep_unpack(const int32_t* rec, int64_t M, int R, const int64_t* ta
   return OMNIMOE_OK;
 }
 
-omnimoe_status ep_combine(const float* y_ret, const int32_t* inv, const int64_t* tok_off, int64_t L, int d, int R,
-                          float* y, cudaStream_t st) {
+omnimoe_status ep_combine(const void* y_ret, int bf16, const int32_t* inv, const int64_t* tok_off, int64_t L, int d,
+                          int R, float* y, cudaStream_t st) {
   if (L == 0) return OMNIMOE_OK;
-  ep_combine_kernel<<<grid_of(L * d / 4, 256), 256, 0, st>>>(y_ret, inv, tok_off, L, d, R, y);
+  if (bf16) ep_combine_kernel<true><<<grid_of(L * d / 4, 256), 256, 0, st>>>(y_ret, inv, tok_off, L, d, R, y);
+  else ep_combine_kernel<false><<<grid_of(L * d / 4, 256), 256, 0, st>>>(y_ret, inv, tok_off, L, d, R, y);
   OMNI_CHECK_LAUNCH("ep_combine_kernel");
+  return OMNIMOE_OK;
+}
+
+omnimoe_status ep_partials_bf16(const float* y, int64_t n, void* out, cudaStream_t st) {
+  if (n == 0) return OMNIMOE_OK;
+  ep_partials_kernel<<<grid_of(n / 4, 256), 256, 0, st>>>(reinterpret_cast<const float4*>(y), n / 4,
+                                                          static_cast<uint2*>(out));
+  OMNI_CHECK_LAUNCH("ep_partials_kernel");
   return OMNIMOE_OK;
 }
 

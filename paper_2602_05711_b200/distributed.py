@@ -7,14 +7,18 @@ replicated.  One forward, per rank:
 
   1. route the local tokens (omnimoe_route: exact, batch-independent, so ids are
      bit-identical to a single-GPU run) and pack the dispatch buffers
-     (omnimoe_ep_pack: each token once per destination + one record per task);
-  2. all-to-all of the per-destination counts, then of the x rows and records
-     (NCCL all_to_all_single over NVLink / NVSwitch);
+     (omnimoe_ep_pack: each token once per destination + one record per task, and
+     the per-destination counts on the device);
+  2. all-to-all of the counts (device to device; ONE host read of the send and
+     receive counts per forward sizes the exchanges), then of the x rows and the
+     records (NCCL all_to_all_single over NVLink / NVSwitch); the shared MLP's
+     first GEMM (it needs x only) runs meanwhile on a side stream;
   3. unpack (omnimoe_ep_unpack), schedule + grouped expert compute on the local
      shard (omnimoe_schedule + omnimoe_expert_fwd over the received rows);
-  4. all-to-all of the partial y rows back to the home ranks;
-  5. combine in fixed rank order (omnimoe_ep_combine) and add the shared MLP
-     (omnimoe_shared_mlp, bf16 output).
+  4. all-to-all of the partial y rows back to the home ranks, in bf16
+     (omnimoe_ep_partials: half the bytes of fp32);
+  5. combine in fixed rank order with fp32 accumulation (omnimoe_ep_combine) and
+     the shared MLP's second GEMM + combine (omnimoe_shared_mlp_out, bf16 output).
 
 The exchange is written against a small communicator interface so the same
 phases run over torch.distributed (NCCL on B200, gloo in the CPU tests) and
@@ -24,6 +28,7 @@ CPU tests inject the oracle -- there is no CPU path in the product.
 """
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass, field
 from typing import List, Optional
 
@@ -39,11 +44,16 @@ class LibOps:
 
     def __init__(self, dims: om.LayerDims):
         self.dims = dims
+        # the layer's routing: candidate order (same ids and gates as key order; the
+        # schedule re-sorts the tasks anyway)
+        self._rdims = dataclasses.replace(dims, route_order=om.ORDER_CANDIDATE)
+        self.last_route = None
 
     def route(self, x, subkeys):
-        idx, gate, _ = om.route(self.dims, x, subkeys, want_score=False)
+        idx, gate, _ = om.route(self._rdims, x, subkeys, want_score=False)
         hk = self.dims.n_heads * self.dims.top_k
-        return idx.reshape(-1, hk), gate.reshape(-1, hk)
+        self.last_route = (idx.reshape(-1, hk), gate.reshape(-1, hk))
+        return self.last_route
 
     def pack(self, x, idx, gate, R):
         return om.ep_pack(self.dims, x, idx.contiguous(), gate.contiguous(), R)
@@ -53,21 +63,26 @@ class LibOps:
 
     def expert(self, x_recv, W_loc, V_loc, ids, gate, tok, n_loc):
         """V_loc is [n_loc][d], or [d/64][n_loc][64] when dims.v_layout is V_SLICED
-        (om.pack_v of the shard); the SLICED executor writes every row of y."""
+        (om.pack_v of the shard); the SLICED executor writes every row of y.  Returns
+        the partial rows in bf16 (the return trip's payload)."""
         sliced = self.dims.v_layout == om.V_SLICED
         rows = x_recv.shape[0]
         if ids.numel() == 0 or rows == 0:
-            return torch.zeros((rows, self.dims.d), dtype=torch.float32, device=x_recv.device)
+            return torch.zeros((rows, self.dims.d), dtype=torch.bfloat16, device=x_recv.device)
         y = (torch.empty if sliced else torch.zeros)((rows, self.dims.d), dtype=torch.float32, device=x_recv.device)
         plan = om.schedule(self.dims, ids, gate, token=tok, expert_begin=0, expert_end=n_loc, n_tokens=rows)
-        return om.expert_fwd(self.dims, x_recv, W_loc, V_loc, plan, y_routed=y, accumulate=not sliced)
+        y = om.expert_fwd(self.dims, x_recv, W_loc, V_loc, plan, y_routed=y, accumulate=not sliced)
+        return om.ep_partials(self.dims, y)
 
     def combine(self, y_ret, inv, tok_off, L):
         return om.ep_combine(self.dims, y_ret, inv, tok_off, L)
 
-    def mlp(self, x, y_routed):
+    def mlp_hidden(self, x):
+        return om.shared_mlp_hidden(self.dims, x, self._wgu) if self.dims.d_ff else None
+
+    def mlp_out(self, x, H, y_routed):
         if self.dims.d_ff:
-            return om.shared_mlp(self.dims, x, self._wgu, self._wdn, y_routed=y_routed)
+            return om.shared_mlp_out(self.dims, x.shape[0], H, self._wdn, y_routed=y_routed)
         return y_routed.to(self.dims.torch_dtype)
 
     def set_mlp(self, w_gate_up, w_down):
@@ -76,24 +91,37 @@ class LibOps:
 
 # ---------------------------------------------------------------- communicators
 class TorchComm:
-    """all_to_all over a torch.distributed process group (NCCL or gloo)."""
+    """all_to_all over a torch.distributed process group: NCCL (device to device), or
+    gloo -- with CPU tensors as they are, with CUDA tensors staged through host memory
+    (the CPU tests, and the 2-process dry run on one GPU)."""
 
     def __init__(self, group=None):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.staged = dist.get_backend(group) == "gloo"
 
-    def exchange_counts(self, counts: List[int], device) -> List[int]:
-        t = torch.tensor(counts, dtype=torch.int64, device=device)
-        out = torch.empty_like(t)
-        dist.all_to_all_single(out, t, group=self.group)
-        return out.cpu().tolist()
+    def _a2a(self, out, inp, out_splits=None, in_splits=None):
+        if self.staged and inp.is_cuda:
+            o = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_to_all_single(o, inp.cpu(), output_split_sizes=out_splits, input_split_sizes=in_splits,
+                                   group=self.group)
+            out.copy_(o)
+        else:
+            dist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits,
+                                   group=self.group)
+        return out
+
+    def exchange_counts(self, counts):
+        """counts: int64 [R][2] (rows, records) for each destination -> the same for each
+        source, as host lists (sent, received): the forward's one host synchronisation."""
+        recv = self._a2a(torch.empty_like(counts), counts.contiguous())
+        both = torch.stack([counts, recv]).cpu()
+        return both[0].tolist(), both[1].tolist()
 
     def exchange(self, send, send_splits, recv_splits):
         out = torch.empty((sum(recv_splits),) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
-        dist.all_to_all_single(out, send.contiguous(), output_split_sizes=recv_splits,
-                               input_split_sizes=send_splits, group=self.group)
-        return out
+        return self._a2a(out, send[:sum(send_splits)].contiguous(), recv_splits, send_splits)
 
 
 # ---------------------------------------------------------------- per-rank state
@@ -104,6 +132,7 @@ class RankState:
     V_loc: torch.Tensor
     L: int = 0
     inv: Optional[torch.Tensor] = None
+    counts: Optional[torch.Tensor] = None              # int64 [R][2] (rows, records) per destination
     send_tok: List[int] = field(default_factory=list)    # rows sent to each rank
     send_task: List[int] = field(default_factory=list)   # records sent to each rank
     x_send: Optional[torch.Tensor] = None
@@ -128,9 +157,7 @@ def phase_dispatch(ops, st: RankState, subkeys, R: int):
     """Route the local tokens and pack one message per destination rank."""
     st.L = st.x.shape[0]
     idx, gate = ops.route(st.x, subkeys)
-    st.x_send, st.rec_send, st.inv, offs = ops.pack(st.x, idx, gate, R)
-    st.send_tok = [offs[s + 1] - offs[s] for s in range(R)]
-    st.send_task = [offs[R + 2 + s] - offs[R + 1 + s] for s in range(R)]
+    st.x_send, st.rec_send, st.inv, st.counts = ops.pack(st.x, idx, gate, R)
 
 
 def phase_expert(ops, st: RankState, R: int, n_loc: int):
@@ -140,24 +167,55 @@ def phase_expert(ops, st: RankState, R: int, n_loc: int):
     st.y_part = ops.expert(st.x_recv.contiguous(), st.W_loc, st.V_loc, ids, gate, tok, n_loc)
 
 
-def phase_combine(ops, st: RankState):
-    """Add the returned partial rows in rank order, then the shared MLP (a7 + a8)."""
+def phase_combine(ops, st: RankState, H):
+    """Add the returned partial rows in rank order, then the shared MLP's second GEMM
+    (a7 + a8)."""
     y_routed = ops.combine(st.y_ret.contiguous(), st.inv.contiguous(), _offsets(st.send_tok, st.x.device), st.L)
-    st.y = ops.mlp(st.x, y_routed)
+    st.y = ops.mlp_out(st.x, H, y_routed)
+
+
+class _Side:
+    """The shared MLP's first GEMM on a side stream (CUDA), joined before its second."""
+
+    def __init__(self, x):
+        self.cuda = x.is_cuda
+        if self.cuda:
+            self.stream = torch.cuda.Stream(device=x.device)
+            self.stream.wait_stream(torch.cuda.current_stream(x.device))
+
+    def run(self, fn, *args):
+        if not self.cuda:
+            return fn(*args)
+        with torch.cuda.stream(self.stream):
+            out = fn(*args)
+        self.event = torch.cuda.Event()
+        self.event.record(self.stream)
+        return out
+
+    def join(self, x, *tensors):
+        if self.cuda:
+            torch.cuda.current_stream(x.device).wait_event(self.event)
+            for t in tensors:  # allocated on the side stream, consumed on the main one
+                if t is not None:
+                    t.record_stream(torch.cuda.current_stream(x.device))
 
 
 # ---------------------------------------------------------------- drivers
-def ep_layer_fwd(ops, comm: TorchComm, x_loc, subkeys, W_loc, V_loc, n_per: int, marks=None):
+def ep_layer_fwd(ops, comm: TorchComm, x_loc, subkeys, W_loc, V_loc, n_per: int, marks=None, return_state=False):
     """One expert-parallel layer forward on this rank (torch.distributed).
-    marks: optional callable(name) invoked between phases (bench timing)."""
+    marks: optional callable(name) invoked between phases (bench timing);
+    return_state: also return the RankState (message sizes, for the bench)."""
     mark = marks or (lambda name: None)
     R = comm.world
     st = RankState(x=x_loc, W_loc=W_loc, V_loc=V_loc)
     mark("start")
     phase_dispatch(ops, st, subkeys, R)
+    side = _Side(x_loc)
+    H = side.run(ops.mlp_hidden, x_loc)  # overlaps the exchanges below
     mark("dispatch")
-    pairs = [v for s in range(R) for v in (st.send_tok[s], st.send_task[s])]  # block s -> rank s
-    st.recv_tok, st.recv_task = _split_counts(comm.exchange_counts(pairs, x_loc.device), R)
+    sent, recv = comm.exchange_counts(st.counts)
+    st.send_tok, st.send_task = [c[0] for c in sent], [c[1] for c in sent]
+    st.recv_tok, st.recv_task = [c[0] for c in recv], [c[1] for c in recv]
     st.x_recv = comm.exchange(st.x_send, st.send_tok, st.recv_tok)
     st.rec_recv = comm.exchange(st.rec_send, st.send_task, st.recv_task)
     mark("all_to_all_dispatch")
@@ -165,16 +223,10 @@ def ep_layer_fwd(ops, comm: TorchComm, x_loc, subkeys, W_loc, V_loc, n_per: int,
     mark("expert")
     st.y_ret = comm.exchange(st.y_part, st.recv_tok, st.send_tok)
     mark("all_to_all_combine")
-    phase_combine(ops, st)
+    side.join(x_loc, H)
+    phase_combine(ops, st, H)
     mark("combine_mlp")
-    return st.y
-
-
-def _split_counts(received, R):
-    """The counts travel as pairs (rows, records): element block s of the send
-    tensor goes to rank s, and ``received`` is the concatenation of the pairs
-    from every source rank."""
-    return [received[2 * s] for s in range(R)], [received[2 * s + 1] for s in range(R)]
+    return (st.y, st) if return_state else st.y
 
 
 def ep_layer_fwd_loopback(ops, xs, subkeys, W_locs, V_locs, n_per: int):
@@ -184,6 +236,8 @@ def ep_layer_fwd_loopback(ops, xs, subkeys, W_locs, V_locs, n_per: int):
     sts = [RankState(x=xs[r], W_loc=W_locs[r], V_loc=V_locs[r]) for r in range(R)]
     for st in sts:
         phase_dispatch(ops, st, subkeys, R)
+        sent = st.counts.cpu().tolist()
+        st.send_tok, st.send_task = [c[0] for c in sent], [c[1] for c in sent]
 
     def blocks(t, counts):
         out, o = [], 0
@@ -202,7 +256,7 @@ def ep_layer_fwd_loopback(ops, xs, subkeys, W_locs, V_locs, n_per: int):
     for r, st in enumerate(sts):
         st.y_ret = torch.cat([blocks(sts[s].y_part, sts[s].recv_tok)[r] for s in range(R)])
     for st in sts:
-        phase_combine(ops, st)
+        phase_combine(ops, st, ops.mlp_hidden(st.x))
     return [st.y for st in sts]
 
 

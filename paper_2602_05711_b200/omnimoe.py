@@ -57,7 +57,8 @@ EXPORTS = ["omnimoe_workspace_size", "omnimoe_route", "omnimoe_schedule", "omnim
            "omnimoe_v_bands", "omnimoe_expert_fwd_pass", "omnimoe_load_stats",
            "omnimoe_load_stats_workspace_size", "omnimoe_expert_fwd_tokens", "omnimoe_layer_executor",
            "omnimoe_expert_bwd", "omnimoe_router_bwd", "omnimoe_shared_mlp_bwd", "omnimoe_layer_fwd_host",
-           "omnimoe_expert_fwd_dense", "omnimoe_dense_workspace_size"]
+           "omnimoe_expert_fwd_dense", "omnimoe_dense_workspace_size", "omnimoe_ep_partials",
+           "omnimoe_shared_mlp_hidden", "omnimoe_shared_mlp_out"]
 
 _lib = None
 
@@ -83,9 +84,12 @@ def load(path: str = LIB_PATH):
         "omnimoe_router_logits": [PD, I64, V, V, V, I32, V, SZ, V],
         "omnimoe_gemm_bf16": [I64, I64, I64, V, V, V, V],
         "omnimoe_ep_pack_workspace_size": [I64, I32, ctypes.POINTER(ctypes.c_size_t)],
-        "omnimoe_ep_pack": [PD, I64, I32, V, V, V, V, V, V, V, V, SZ, V],
+        "omnimoe_ep_pack": [PD, I64, I32, V, V, V, V, V, V, V, V, V, SZ, V],
         "omnimoe_ep_unpack": [I64, I32, V, V, V, V, V, V, V],
-        "omnimoe_ep_combine": [PD, I64, I32, V, V, V, V, V],
+        "omnimoe_ep_partials": [I64, PD, V, V, V],
+        "omnimoe_ep_combine": [PD, I64, I32, V, I32, V, V, V, V],
+        "omnimoe_shared_mlp_hidden": [PD, I64, V, V, V, SZ, V],
+        "omnimoe_shared_mlp_out": [PD, I64, V, SZ, V, V, V, V],
         "omnimoe_pack_v": [PD, I64, V, V, V],
         "omnimoe_load_stats": [PP, V, V, SZ, V],
         "omnimoe_expert_fwd_tokens": [PD, I64, V, V, V, V, V, V, I32, V],
@@ -541,8 +545,9 @@ def gemm_bf16(A, B):
 # ---------------------------------------------------------------- expert parallelism
 def ep_pack(dims: LayerDims, x, idx, gate, R: int):
     """Dispatch buffers for R expert shards (include/omnimoe.h omnimoe_ep_pack).
-    Returns (x_send, rec_send, inv, offsets_host) with offsets_host a list of
-    2R+2 ints (token block starts, then record block starts), read after a sync."""
+    Returns (x_send, rec_send, inv, counts) with counts a device int64 [R][2] tensor
+    (rows, records per destination); x_send / rec_send are capacity-sized (R*L rows,
+    L*h*K records): the first sum of each column of counts are valid."""
     L = x.shape[0]
     hk = dims.n_heads * dims.top_k
     _req(x, "x", dims.torch_dtype, L * dims.d)
@@ -552,14 +557,24 @@ def ep_pack(dims: LayerDims, x, idx, gate, R: int):
     rec = torch.empty((max(L * hk, 1), 3), dtype=torch.int32, device=x.device)
     inv = torch.empty((R, max(L, 1)), dtype=torch.int32, device=x.device)
     off = torch.empty(2 * R + 2, dtype=torch.int32, device=x.device)
+    counts = torch.empty((R, 2), dtype=torch.int64, device=x.device)
     nb = ctypes.c_size_t(0)
     _check(load().omnimoe_ep_pack_workspace_size(L, R, ctypes.byref(nb)), "ep_pack_workspace_size")
     ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=x.device)
     dc = dims.c()
     _check(load().omnimoe_ep_pack(ctypes.byref(dc), L, R, _ptr(x), _ptr(idx), _ptr(gate), _ptr(x_send), _ptr(rec),
-                                  _ptr(inv), _ptr(off), _ptr(ws), ws.numel(), _stream()), "ep_pack")
-    offs = off.cpu().tolist()  # the split sizes of the all-to-all (host-visible counts)
-    return x_send[:offs[R]], rec[:offs[2 * R + 1]], inv[:, :L], offs
+                                  _ptr(inv), _ptr(off), _ptr(counts), _ptr(ws), ws.numel(), _stream()), "ep_pack")
+    return x_send, rec, inv[:, :L], counts
+
+
+def ep_partials(dims: LayerDims, y_part):
+    """fp32 partial rows -> bf16 for the return all-to-all (omnimoe_ep_partials)."""
+    rows = y_part.shape[0]
+    _req(y_part, "y_part", torch.float32, rows * dims.d)
+    out = torch.empty((rows, dims.d), dtype=torch.bfloat16, device=y_part.device)
+    dc = dims.c()
+    _check(load().omnimoe_ep_partials(rows, ctypes.byref(dc), _ptr(y_part), _ptr(out), _stream()), "ep_partials")
+    return out
 
 
 def ep_unpack(rec, R: int, task_off, tok_off):
@@ -577,14 +592,40 @@ def ep_unpack(rec, R: int, task_off, tok_off):
 
 
 def ep_combine(dims: LayerDims, y_ret, inv, tok_off, L: int):
-    """y_routed[l] = sum_s y_ret[tok_off[s] + inv[s][l]] in rank order (fp32)."""
+    """y_routed[l] = sum_s y_ret[tok_off[s] + inv[s][l]] in rank order (fp32 accumulation;
+    y_ret bf16 from ep_partials, or fp32)."""
     R = inv.shape[0]
     _req(inv, "inv", torch.int32, R * L)
     _req(tok_off, "tok_off", torch.int64, R + 1)
+    bf = y_ret.dtype == torch.bfloat16
     if y_ret.numel():
-        _req(y_ret, "y_ret", torch.float32)
+        _req(y_ret, "y_ret", torch.bfloat16 if bf else torch.float32)
     y = torch.empty((L, dims.d), dtype=torch.float32, device=inv.device)
     dc = dims.c()
-    _check(load().omnimoe_ep_combine(ctypes.byref(dc), L, R, _ptr(y_ret) if y_ret.numel() else None, _ptr(inv),
-                                     _ptr(tok_off), _ptr(y), _stream()), "ep_combine")
+    _check(load().omnimoe_ep_combine(ctypes.byref(dc), L, R, _ptr(y_ret) if y_ret.numel() else None, int(bf),
+                                     _ptr(inv), _ptr(tok_off), _ptr(y), _stream()), "ep_combine")
+    return y
+
+
+def shared_mlp_hidden(dims: LayerDims, x, w_gate_up, H=None):
+    """Shared-MLP GEMM-1 into an opaque H buffer (omnimoe_shared_mlp_hidden)."""
+    L = x.shape[0]
+    _req(x, "x", dims.torch_dtype, L * dims.d)
+    _req(w_gate_up, "w_gate_up", dims.torch_dtype, 2 * dims.d_ff * dims.d)
+    H = H if H is not None else workspace(dims, L, WS_MLP, x.device)
+    dc = dims.c()
+    _check(load().omnimoe_shared_mlp_hidden(ctypes.byref(dc), L, _ptr(x), _ptr(w_gate_up), _ptr(H), H.numel(),
+                                            _stream()), "shared_mlp_hidden")
+    return H
+
+
+def shared_mlp_out(dims: LayerDims, L: int, H, w_down, y_routed=None, y=None):
+    """Shared-MLP GEMM-2 + combine: y = H W_down^T + y_routed (omnimoe_shared_mlp_out)."""
+    _req(w_down, "w_down", dims.torch_dtype, dims.d * dims.d_ff)
+    if y_routed is not None:
+        _req(y_routed, "y_routed", torch.float32, L * dims.d)
+    y = y if y is not None else torch.empty((L, dims.d), dtype=dims.torch_dtype, device=H.device)
+    dc = dims.c()
+    _check(load().omnimoe_shared_mlp_out(ctypes.byref(dc), L, _ptr(H), H.numel(), _ptr(w_down), _ptr(y_routed),
+                                         _ptr(y), _stream()), "shared_mlp_out")
     return y

@@ -45,7 +45,9 @@ class RefOps:
             task_off.append(len(recs))
         x_send = torch.stack(rows) if rows else x[:0]
         rec = torch.tensor([[e, g, sl] for e, g, sl in recs], dtype=torch.float64).reshape(-1, 3)
-        return x_send, rec, torch.from_numpy(inv), tok_off + task_off
+        counts = torch.tensor([[tok_off[s + 1] - tok_off[s], task_off[s + 1] - task_off[s]] for s in range(R)],
+                              dtype=torch.int64)
+        return x_send, rec, torch.from_numpy(inv), counts
 
     def unpack(self, rec, R, task_off, tok_off):
         M = rec.shape[0]
@@ -72,7 +74,10 @@ class RefOps:
                     y[l] += y_ret[tok_off[s] + inv[s, l]]
         return y
 
-    def mlp(self, x, y_routed):
+    def mlp_hidden(self, x):
+        return None
+
+    def mlp_out(self, x, H, y_routed):
         if self.wgu is None:
             return y_routed
         return y_routed + torch.from_numpy(oracle.shared_mlp(x.numpy(), self.wgu.numpy(), self.wdn.numpy(), nthreads=1))

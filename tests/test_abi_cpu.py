@@ -60,7 +60,7 @@ def test_host_side_validation_without_gpu(lib):
     assert lib.omnimoe_status_string  # symbol resolves
     sl = om.LayerDims(d=64, n_rows=32, n_cols=32, top_k=8, d_ff=128, v_layout=om.V_SLICED)
     assert om.workspace_size(sl, 256, om.WS_LAYER) > om.workspace_size(ok, 256, om.WS_LAYER)
-    with pytest.raises(om.OmniMoEError, match="UNSUPPORTED"):  # SLICED layout needs d % 32 == 0
+    with pytest.raises(om.OmniMoEError, match="UNSUPPORTED"):  # SLICED layout needs d % 64 == 0
         om.workspace_size(om.LayerDims(d=72, n_rows=4, n_cols=4, top_k=2, v_layout=om.V_SLICED), 8, om.WS_LAYER)
     with pytest.raises(om.OmniMoEError, match="INVALID_ARGUMENT"):  # and runs the SLICED executor only
         om.workspace_size(om.LayerDims(d=64, n_rows=4, n_cols=4, top_k=2, expert_kernel=om.EXPERT_GROUP,

@@ -112,3 +112,57 @@ dist.destroy_process_group()
     line = [l for l in out.stdout.splitlines() if l.startswith("ERR")][0]
     e_tok, e_elt = map(float, line.split()[1:])
     assert e_tok <= 1e-2 and e_elt <= 1e-2
+
+
+def test_bench_multi_two_process_gloo_dry_run():
+    """bench.py's N > 1 path launched as the driver does (torchrun, 2 ranks), over gloo
+    with host-staged all-to-alls so that both ranks can share this box's one GPU: the
+    protocol runs end to end and rank 0 prints one well-formed JSON line."""
+    import json
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2", "--steps", "2", "--warmup",
+           "1", "--config", "C1", "--backend", "gloo", "--no-e2e", "--cpu-seconds", "2"]
+    out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["scaling"] == "strong" and j["config"]["global_tokens"] == 256
+    assert j["parity"]["mismatch"] == 0 and j["parity"]["e_tok"] <= 1e-2 and j["parity"]["e_elt"] <= 1e-2
+    assert j["roofline"]["nvlink"]["bytes_per_step_rank0"] > 0 and j["cpu_baseline"]["cores"] >= 1
+
+
+@pytest.mark.parametrize("vl", [om.V_SLICED])
+def test_ep_loopback_c5_per_rank_shape(vl):
+    """configs[4] at R = 8 in loopback: N = 2^22 experts (2^19 per virtual rank),
+    65,536 tokens (8,192 per rank), K = 512; sampled tokens against the oracle."""
+    w = configs.get("C5", v_layout=vl)
+    dims, L, R = w.dims, w.L, 8
+    full = make_inputs(dims, L, w.seed, skip=("W", "V"))
+    ops = ep.LibOps(dims)
+    ops.set_mlp(full["w_gate_up"], full["w_down"])
+    lpr, n_per = L // R, dims.N // R
+    xs = [full["x"][r * lpr:(r + 1) * lpr] for r in range(R)]
+    Ws, Vs = [], []
+    for r in range(R):
+        sh = make_inputs(dims, 1, w.seed, skip=("x", "subkeys", "w_gate_up", "w_down"),
+                         expert_rows=(r * n_per, (r + 1) * n_per))
+        Ws.append(sh["W"])
+        Vs.append(om.pack_v(dims, sh["V"]))
+        del sh
+    ys = ep.ep_layer_fwd_loopback(ops, xs, full["subkeys"], Ws, Vs, n_per)
+    y = torch.cat(ys)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(8)
+    toks = np.unique(np.concatenate([[0, lpr - 1, lpr, L - 1], rng.choice(L, 60, replace=False)]))
+    hr = lambda n, r=None: host_rows(dims, w.seed, n, r)
+    x = hr("x", toks)
+    sub = hr("subkeys").reshape(1, -1, dims.d)
+    lg = oracle.logits(x, sub)
+    rt = oracle.route(lg.reshape(len(toks), -1), dims.n_rows, dims.n_cols, dims.top_k)
+    used = np.unique(rt["idx"])
+    ref = oracle.layer(x, sub, hr("W", used), hr("V", used), dims.n_rows, dims.n_cols, dims.top_k,
+                       hr("w_gate_up"), hr("w_down"), id_map=np.stack([used, np.arange(len(used))], 1))
+    e_tok, e_elt = rel_errors(y[torch.from_numpy(toks).cuda()].float().cpu().numpy(), ref["y"])
+    assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
