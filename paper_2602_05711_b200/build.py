@@ -26,20 +26,26 @@ def _stale(target, sources):
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+LIB_MEASURE = os.path.join(PKG, "libomnimoe_measure.so")
+
+
+def build(force: bool = False, verbose: bool = False, measure: bool = False) -> str:
+    """measure: the measurement build (-DOMNIMOE_MEASURE, csrc/tuning.cuh) into
+    libomnimoe_measure.so -- tools/ sweeps load it with OMNIMOE_LIB=<path>; the product
+    library never reads the environment."""
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     deps = srcs + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "omnimoe.h")]
-    if force or _stale(LIB, deps):
-        cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB, *srcs]
+    lib = LIB_MEASURE if measure else LIB
+    if force or _stale(lib, deps):
+        cmd = [NVCC, *ARCH, *FLAGS, *(["-DOMNIMOE_MEASURE"] if measure else []), "-o", lib, *srcs]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
     if force or _stale(SYNTH_LIB, [SYNTH_SRC]):
         subprocess.check_call([NVCC, *ARCH, *FLAGS, "-o", SYNTH_LIB, SYNTH_SRC])
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, measure="--measure" in sys.argv))

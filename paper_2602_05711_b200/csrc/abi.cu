@@ -4,6 +4,8 @@
 #include <mutex>
 #include <string>
 #include <map>
+#include <set>
+#include <tuple>
 #include <vector>
 
 #include "backward.cuh"
@@ -24,30 +26,61 @@ void count_launch(int n) { g_launches += n; }
 void reset_launch_count() { g_launches = 0; }
 
 namespace {
+// per-device facts, queried once per device under a lock
+struct DeviceInfo {
+  int major = 0, minor = 0, sms = 0;
+};
+std::mutex g_dev_mu;
+std::map<int, DeviceInfo> g_dev;
+std::set<std::tuple<const void*, int, int>> g_smem_attr;  // (kernel, device, bytes) already applied
+
+int current_device() {
+  int dev = 0;
+  return cudaGetDevice(&dev) == cudaSuccess ? dev : -1;
+}
+DeviceInfo device_info(int dev) {
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  auto it = g_dev.find(dev);
+  if (it != g_dev.end()) return it->second;
+  DeviceInfo di;
+  cudaDeviceGetAttribute(&di.major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&di.minor, cudaDevAttrComputeCapabilityMinor, dev);
+  cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
+  g_dev[dev] = di;
+  return di;
+}
+}  // namespace
+
+int num_sms() {
+  const int dev = current_device();
+  const int n = dev < 0 ? 0 : device_info(dev).sms;
+  return n > 0 ? n : 148;
+}
+
+bool set_smem_attr(const void* func, int bytes) {
+  const int dev = current_device();
+  {
+    std::lock_guard<std::mutex> g(g_dev_mu);
+    if (g_smem_attr.count(std::make_tuple(func, dev, bytes))) return true;
+  }
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  g_smem_attr.insert(std::make_tuple(func, dev, bytes));
+  return true;
+}
+
+namespace {
 
 omnimoe_status check_device() {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) {
+  const int dev = current_device();
+  if (dev < 0) {
     set_error("no CUDA device");
     return OMNIMOE_ERR_UNSUPPORTED;
   }
-  static int cached_dev = -1, cached_ok = 0;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> g(mu);
-  if (cached_dev != dev) {
-    int major = 0, minor = 0;
-    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
-    cached_ok = (major == 10 && minor == 0);
-    cached_dev = dev;
-    if (!cached_ok) {
-      set_error("device " + std::to_string(dev) + " is sm_" + std::to_string(major) +
-                std::to_string(minor) + "; libomnimoe is built for sm_100a only");
-      return OMNIMOE_ERR_UNSUPPORTED;
-    }
-  }
-  if (!cached_ok) {
-    set_error("device is not sm_100a");
+  const DeviceInfo di = device_info(dev);
+  if (!(di.major == 10 && di.minor == 0)) {
+    set_error("device " + std::to_string(dev) + " is sm_" + std::to_string(di.major) + std::to_string(di.minor) +
+              "; libomnimoe is built for sm_100a only");
     return OMNIMOE_ERR_UNSUPPORTED;
   }
   return OMNIMOE_OK;
@@ -211,7 +244,7 @@ size_t layer_ws(const omnimoe_dims& d, int64_t L, void* ws, LayerWs* o) {
   void* sw = c.take<char>(sb);
   float* yr = c.take<float>((size_t)L * d.d);
   // measurement override: pad before the executor's work counters (placement study)
-  if (const char* pad = getenv("OMNIMOE_WS_PAD_COUNTERS")) c.take<char>((size_t)atoll(pad));
+  if (tuning().ws_pad_counters) c.take<char>((size_t)tuning().ws_pad_counters);
   void* ew = c.take<char>(layer_uses_dense_executor(d, L) ? dense_expert_ws_bytes(d, L) : expert_ws_bytes(d, L));
   void* H = c.take<char>(h_bytes(d, L));
   uint32_t* cand = c.take<uint32_t>(dense_router(d) ? 0 : select_cand_ws_bytes(d) / 4);
@@ -586,7 +619,7 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
   if (d.d_ff > 0) {
     OMNI_TRY(mlp_impl(d, L, x, w_gate_up, w_down, w.y_routed, y, w.H, st));
   } else {
-    cast_out_kernel<<<kSMs * 4, 256, 0, st>>>(w.y_routed, y, L * d.d, d.dtype == OMNIMOE_BF16);
+    cast_out_kernel<<<num_sms() * 4, 256, 0, st>>>(w.y_routed, y, L * d.d, d.dtype == OMNIMOE_BF16);
     OMNI_CHECK_LAUNCH("cast_out_kernel");
   }
   (void)r_launch;
@@ -868,7 +901,7 @@ omnimoe_status omnimoe_layer_fwd_host(const omnimoe_dims* dims, int64_t L, const
       if (d.dtype == OMNIMOE_BF16) OMNI_TRY(gemm_bf16(EPI_ADD, Hc, w_down, g2, st));
       else OMNI_TRY(gemm_f32(EPI_ADD, static_cast<const float*>(Hc), static_cast<const float*>(w_down), g2, st));
     } else {
-      cast_out_kernel<<<kSMs * 4, 256, 0, st>>>(w.y_routed + l0 * d.d, yc, n * d.d, d.dtype == OMNIMOE_BF16);
+      cast_out_kernel<<<num_sms() * 4, 256, 0, st>>>(w.y_routed + l0 * d.d, yc, n * d.d, d.dtype == OMNIMOE_BF16);
       OMNI_CHECK_LAUNCH("cast_out_kernel");
     }
     if (cudaEventRecord(evs[n_ch + c], st) != cudaSuccess || cudaStreamWaitEvent(cs, evs[n_ch + c], 0) != cudaSuccess ||

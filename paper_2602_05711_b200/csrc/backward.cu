@@ -44,7 +44,7 @@ omnimoe_status transpose16(const void* in, void* out, int64_t R, int64_t C, cuda
   if (ld == 0) ld = R;
   if (R == 0 || C == 0) return OMNIMOE_OK;
   const int64_t tiles = ((ld + 31) / 32) * ((C + 31) / 32);
-  transpose16_kernel<<<(int)std::min<int64_t>(tiles, kSMs * 16), dim3(32, 8), 0, st>>>(
+  transpose16_kernel<<<(int)std::min<int64_t>(tiles, num_sms() * 16), dim3(32, 8), 0, st>>>(
       static_cast<const uint16_t*>(in), static_cast<uint16_t*>(out), R, C, ld);
   OMNI_CHECK_LAUNCH("transpose16_kernel");
   return OMNIMOE_OK;
@@ -66,7 +66,7 @@ omnimoe_status add_f32(float* dst, const float* src, int64_t n, int accumulate, 
     }
     return OMNIMOE_OK;
   }
-  add_f32_kernel<<<kSMs * 4, 256, 0, st>>>(dst, src, n);
+  add_f32_kernel<<<num_sms() * 4, 256, 0, st>>>(dst, src, n);
   OMNI_CHECK_LAUNCH("add_f32_kernel");
   return OMNIMOE_OK;
 }
@@ -202,7 +202,7 @@ omnimoe_status router_bwd_run(const omnimoe_dims& d, int64_t L, const void* x, c
     set_error("router_bwd: cannot set shared memory");
     return OMNIMOE_ERR_CUDA;
   }
-  router_ds_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((T + 7) / 8, kSMs * 2)), 256, smem, st>>>(
+  router_ds_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((T + 7) / 8, num_sms() * 2)), 256, smem, st>>>(
       T, R, (int)d.n_rows, (int)d.n_cols, (int)d.top_k, idx, gate, dgate, w.ds, hR, (int)d.n_heads);
   OMNI_CHECK_LAUNCH("router_ds_kernel");
   // dsub [hR][d] = hi^T x + lo^T x :  A = [hi^T ; lo^T] halves [hR][L], B = x^T [d][L]
@@ -234,7 +234,7 @@ omnimoe_status mlp_bwd_run(const omnimoe_dims& d, int64_t L, const void* x, cons
   OMNI_TRY(gemm_f32out(x, wgu, L, 2 * F, D, w.gu, st));       // G|U = x W_gu^T
   OMNI_TRY(transpose16(wdn, w.wdT, D, F, st));                 // W_down^T [F][D]
   OMNI_TRY(gemm_f32out(dy, w.wdT, L, F, D, w.dh, st));        // dH = dy W_down
-  swiglu_bwd_kernel<<<kSMs * 8, 256, 0, st>>>(w.gu, w.dh, L, (int)F, w.H2, w.dgu2);
+  swiglu_bwd_kernel<<<num_sms() * 8, 256, 0, st>>>(w.gu, w.dh, L, (int)F, w.H2, w.dgu2);
   OMNI_CHECK_LAUNCH("swiglu_bwd_kernel");
   // dW_down = dy^T (H_hi + H_lo)
   OMNI_TRY(transpose16(dy, w.dyT, L, D, st, Lp));

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "../../include/omnimoe.h"
+#include "tuning.cuh"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "libomnimoe targets sm_100a only"
@@ -14,7 +15,12 @@
 
 namespace omni {
 
-constexpr int kSMs = 148;
+// SM count of the current device, queried once per device (148 on B200): grids are
+// sized in multiples of it (persistent kernels: one wave of resident CTAs)
+int num_sms();
+// cudaFuncSetAttribute(func, MaxDynamicSharedMemorySize, bytes), applied once per
+// (kernel, device, size) behind a lock: safe for several devices and host threads
+bool set_smem_attr(const void* func, int bytes);
 
 // ---- host-side error state (thread-local, see omnimoe_last_error) ----------
 void set_error(const std::string& msg);

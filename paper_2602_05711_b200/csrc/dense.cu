@@ -130,10 +130,6 @@ __global__ void __launch_bounds__(256) dense_prep_kernel(int k, int words, const
   }
 }
 
-int env_int_d(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
 
 }  // namespace
 
@@ -145,7 +141,7 @@ bool layer_uses_dense_executor(const omnimoe_dims& d, int64_t L) {
   // 0.5%: 2.9 vs 1.4 ms), so the rule asks for K >= N / 40 and eta >= 32 (every expert
   // shared by many tokens).  One head: a token's K ids are distinct, A needs no sums.
   return d.expert_kernel == OMNIMOE_EXPERT_AUTO && d.v_layout == OMNIMOE_V_ROWS && d.dtype == OMNIMOE_BF16 &&
-         d.n_heads == 1 && d.top_k * env_int_d("OMNIMOE_DENSE_RATIO", 40) >= N &&
+         d.n_heads == 1 && d.top_k * tuning().dense_ratio >= N &&
          expected_eta(d, L) >= 32.0 && (double)L * pad8(N) * 6.0 <= 32.0 * (1 << 30);
 }
 
@@ -186,11 +182,11 @@ omnimoe_status dense_expert_run(const omnimoe_dims& d, int64_t L, const void* x,
       set_error("dense executor: memset failed");
       return OMNIMOE_ERR_CUDA;
     }
-    dense_mask_kernel<<<kSMs * 8, 256, 0, st>>>(M, k, words, idx, w.mask);
+    dense_mask_kernel<<<num_sms() * 8, 256, 0, st>>>(M, k, words, idx, w.mask);
     OMNI_CHECK_LAUNCH("dense_mask_kernel");
     dense_prefix_kernel<<<(unsigned)((L * 32 + 255) / 256), 256, 0, st>>>(L, words, w.mask, w.prefix);
     OMNI_CHECK_LAUNCH("dense_prefix_kernel");
-    dense_gate_kernel<<<kSMs * 8, 256, 0, st>>>(M, k, words, idx, gate, w.mask, w.prefix, w.gate_c);
+    dense_gate_kernel<<<num_sms() * 8, 256, 0, st>>>(M, k, words, idx, gate, w.mask, w.prefix, w.gate_c);
     OMNI_CHECK_LAUNCH("dense_gate_kernel");
   }
   GemmArgs g1;  // A = mask (.) g act(x W^T), written once in bf16 by the GEMM epilogue

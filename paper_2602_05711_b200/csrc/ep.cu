@@ -189,7 +189,7 @@ __global__ void ep_partials_kernel(const float4* __restrict__ y, int64_t n4, uin
 }
 
 int grid_of(int64_t n, int threads) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, kSMs * 16));
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, num_sms() * 16));
 }
 
 }  // namespace

@@ -25,10 +25,6 @@
 namespace omni {
 namespace {
 
-int env_int(const char* name, int dflt) {  // measurement overrides (tools/ sweeps)
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
 
 template <typename T>
 struct VecT;
@@ -503,10 +499,10 @@ omnimoe_status launch_group_tma(int d, const void* x, const void* W, const void*
     set_error("expert_fwd: cannot set shared memory of the TMA group kernel");
     return OMNIMOE_ERR_CUDA;
   }
-  kern<<<kSMs, warps * 32, smem, st>>>(d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W),
+  kern<<<num_sms(), warps * 32, smem, st>>>(d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W),
                                        static_cast<const __nv_bfloat16*>(V), plan.run_offsets, plan.n_runs, m_loc,
                                        plan.sorted_token, plan.sorted_expert, plan.sorted_gate, y, act, work,
-                                       getenv("OMNIMOE_L2_HINTS") ? atoi(getenv("OMNIMOE_L2_HINTS")) : 0);
+                                       tuning().l2_hints);
   OMNI_CHECK_LAUNCH("expert_group_tma_kernel");
   return OMNIMOE_OK;
 }
@@ -689,7 +685,7 @@ omnimoe_status launch_run_reg(int d, const void* x, const void* W, const void* V
                               const int32_t* m_loc, float* y, int act, int* work, cudaStream_t st) {
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_run_reg_kernel<NV>, 256, 0);
-  expert_run_reg_kernel<NV><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(
+  expert_run_reg_kernel<NV><<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(
       d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W),
       static_cast<const __nv_bfloat16*>(V), plan.run_offsets, plan.n_runs, m_loc, plan.sorted_token,
       plan.sorted_expert, plan.sorted_gate, y, act, work);
@@ -708,8 +704,7 @@ omnimoe_status launch_group(int d, const void* x, const void* W, const void* V, 
   const int32_t* m_loc = plan.expert_offsets + n_loc;
   // register-load run kernel for d <= 1024 (enough warps resident to hide L2 latency);
   // TMA-staged kernel above that (profiles/r1/sweep_executors.log)
-  const char* force = getenv("OMNIMOE_GROUP_KERNEL");  // "reg" | "tma" (measurement override)
-  const bool reg = force ? force[0] == 'r' : d <= 1024;
+  const bool reg = tuning().group_kernel >= 0 ? tuning().group_kernel == 1 : d <= 1024;
   if (sizeof(T) == 2 && d % 256 == 0 && d <= 2048 && reg) {
     switch (d / 256) {
       case 1: return launch_run_reg<1>(d, x, W, V, plan, m_loc, y, act, work, st);
@@ -738,7 +733,7 @@ omnimoe_status launch_group(int d, const void* x, const void* W, const void* V, 
   case NVC: {                                                                                         \
     int per_sm = 1;                                                                                   \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_group_kernel<T, NVC>, 256, 0);      \
-    expert_group_kernel<T, NVC><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(                          \
+    expert_group_kernel<T, NVC><<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(                          \
         d, X, Wp, Vp, plan.run_offsets, plan.n_runs, m_loc, plan.sorted_token, plan.sorted_expert,    \
         plan.sorted_gate, y, act, work);                                                              \
     break;                                                                                            \
@@ -751,13 +746,13 @@ omnimoe_status launch_group(int d, const void* x, const void* W, const void* V, 
     OMNI_GROUP_CASE(16)  // fp32 at d = 2048 (all-fp32 mode at the paper's width)
     default:
       if (nv == 3) {
-        expert_group_kernel<T, 4><<<kSMs * 4, 256, 0, st>>>(d, X, Wp, Vp, plan.run_offsets, plan.n_runs, m_loc,
+        expert_group_kernel<T, 4><<<num_sms() * 4, 256, 0, st>>>(d, X, Wp, Vp, plan.run_offsets, plan.n_runs, m_loc,
                                                              plan.sorted_token, plan.sorted_expert,
                                                              plan.sorted_gate, y, act, work);
         break;
       }
       if (nv <= 8) {
-        expert_group_kernel<T, 8><<<kSMs * 4, 256, 0, st>>>(d, X, Wp, Vp, plan.run_offsets, plan.n_runs, m_loc,
+        expert_group_kernel<T, 8><<<num_sms() * 4, 256, 0, st>>>(d, X, Wp, Vp, plan.run_offsets, plan.n_runs, m_loc,
                                                              plan.sorted_token, plan.sorted_expert,
                                                              plan.sorted_gate, y, act, work);
         break;
@@ -775,7 +770,7 @@ omnimoe_status launch_warp(int d, const void* x, const void* W, const void* V,
                            const omnimoe_plan& plan, float* y, int act, cudaStream_t st) {
   constexpr int E = VecT<T>::E;
   const int nv = (d + 32 * E - 1) / (32 * E);
-  const int grid = kSMs * 8;
+  const int grid = num_sms() * 8;
   auto X = static_cast<const T*>(x);
   auto Wp = static_cast<const T*>(W);
   auto Vp = static_cast<const T*>(V);
@@ -1305,10 +1300,10 @@ omnimoe_status launch_zdot(int d, const void* x, const void* W, const omnimoe_pl
   auto go = [&](auto kern) {
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
-    kern<<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(
+    kern<<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(
         d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W), plan.expert_offsets,
         plan.active, plan.n_active, plan.sorted_token, plan.sorted_gate, plan.sorted_task, plan.task_pair, act, work,
-        env_int("OMNIMOE_W_HINT", 1), env_int("OMNIMOE_X_HINT", 0));
+        tuning().w_hint, tuning().x_hint);
   };
   // 80 registers (3 CTAs per SM) with two x rows in flight per warp: pass Z 3.27 -> 2.25 ms at
   // C3a against 64 registers / 4 CTAs (profiles/r2/occupancy/); 2 CTAs or 4 rows in flight: no gain
@@ -1322,7 +1317,7 @@ omnimoe_status launch_dot(int d, const void* x, const void* W, const omnimoe_pla
                           int act, int* work, cudaStream_t st) {
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_dot_kernel<NV>, 256, 0);
-  expert_dot_kernel<NV><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(
+  expert_dot_kernel<NV><<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(
       d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W), plan.run_offsets, plan.n_runs,
       m_loc, plan.sorted_token, plan.sorted_expert, plan.sorted_gate, plan.sorted_task, plan.task_pair, act, work);
   OMNI_CHECK_LAUNCH("expert_dot_kernel");
@@ -1476,7 +1471,7 @@ omnimoe_status expert_token_run(const omnimoe_dims& dm, int64_t L, const void* x
   }
   if (L == 0) return OMNIMOE_OK;
   const int hk = (int)(dm.n_heads * dm.top_k);
-  const int grid = (int)std::min<int64_t>((L + 7) / 8, kSMs * 16);
+  const int grid = (int)std::min<int64_t>((L + 7) / 8, num_sms() * 16);
   auto X = static_cast<const __nv_bfloat16*>(x);
   auto Wp = static_cast<const __nv_bfloat16*>(W);
   auto Vp = static_cast<const __nv_bfloat16*>(V);
@@ -1521,7 +1516,7 @@ bool layer_uses_token_executor(const omnimoe_dims& d, int64_t L) {
   // measured (profiles/r1/README.md, C3b / C5s at eta ~ 1.1): with no expert shared by two
   // tasks, scheduling and two passes cost more than they save; full-row gathers win
   return d.expert_kernel == OMNIMOE_EXPERT_AUTO && d.v_layout == OMNIMOE_V_ROWS && d.dtype == OMNIMOE_BF16 &&
-         d.d % 256 == 0 && d.d <= 2048 && expected_eta(d, L) < env_int("OMNIMOE_TOKEN_ETA_X100", 200) / 100.0;
+         d.d % 256 == 0 && d.d <= 2048 && expected_eta(d, L) < tuning().token_eta_x100 / 100.0;
 }
 
 // pass V geometry: pass V sweeps the 64-column slices of V one band of
@@ -1573,7 +1568,7 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
     auto go = [&](auto kern) {
       int per_sm = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
-      kern<<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(
+      kern<<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(
           d, static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(W), plan.expert_offsets,
           plan.active, plan.n_active, plan.sorted_token, plan.sorted_gate, plan.sorted_task, plan.task_pair, dm.act,
           work);
@@ -1619,17 +1614,17 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
   // use them; band b > 0 adds to the slices band b - 1 wrote (stream order: the
   // summation order is fixed, the result bitwise deterministic)
   // few tasks per token: 8 tokens per warp (lane groups), else one token per warp
-  const bool grouped = dm.n_heads * dm.top_k <= env_int("OMNIMOE_V_GROUP_MAX_TASKS", 64);
+  const bool grouped = dm.n_heads * dm.top_k <= tuning().v_group_max_tasks;
   int gper_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gper_sm, expert_vslice_group_kernel, 256, 0);
   for (int b = 0; b < nb; ++b) {
     if (grouped) {
-      expert_vslice_group_kernel<<<kSMs * std::max(gper_sm, 1), 256, 0, st>>>(
+      expert_vslice_group_kernel<<<num_sms() * std::max(gper_sm, 1), 256, 0, st>>>(
           d, L, n_loc, plan.token_offsets, nb + 1, b, n_tok, plan.task_pair, static_cast<const __nv_bfloat16*>(Vs),
           y, b > 0 ? 1 : accumulate, work + 1 + b);
       OMNI_CHECK_LAUNCH("expert_vslice_group_kernel");
     } else {
-      vkern<<<kSMs * per_sm, 256, 0, st>>>(
+      vkern<<<num_sms() * per_sm, 256, 0, st>>>(
           d, L, n_loc, plan.token_offsets, nb + 1, b, n_tok, plan.task_pair, static_cast<const __nv_bfloat16*>(Vs),
           y, b > 0 ? 1 : accumulate, work + 1 + b);
       OMNI_CHECK_LAUNCH("expert_vslice_kernel");
@@ -1640,7 +1635,7 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
 
 omnimoe_status pack_v(int64_t n, int d, const void* V, void* Vs, cudaStream_t st) {
   if (n == 0) return OMNIMOE_OK;
-  pack_v_kernel<<<kSMs * 8, 256, 0, st>>>(static_cast<const uint4*>(V), static_cast<uint4*>(Vs), n, d);
+  pack_v_kernel<<<num_sms() * 8, 256, 0, st>>>(static_cast<const uint4*>(V), static_cast<uint4*>(Vs), n, d);
   OMNI_CHECK_LAUNCH("pack_v_kernel");
   return OMNIMOE_OK;
 }
@@ -1661,7 +1656,7 @@ omnimoe_status expert_bwd_run(const omnimoe_dims& dm, int64_t L, const void* x, 
 #define OMNI_BWD_CASE(N, G)                                                                                     \
   {                                                                                                            \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expert_bwd_kernel<N, G>, 256, 0);                   \
-    expert_bwd_kernel<N, G><<<kSMs * std::max(per_sm, 1), 256, 0, st>>>(                                       \
+    expert_bwd_kernel<N, G><<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(                                       \
         d, X, Wp, Vp, D, plan.expert_offsets, plan.active, plan.n_active, plan.sorted_token, plan.sorted_gate, \
         plan.sorted_task, plan.task_pair, dgate, dW_act, dV_act, dm.act);                                      \
   }

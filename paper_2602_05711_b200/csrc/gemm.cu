@@ -330,14 +330,10 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t k, uint32
 
 template <int EPI, bool BMN = false>
 omnimoe_status launch_tc(const void* A, const void* B, const GemmArgs& a, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_tc_kernel<EPI, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             EPI == EPI_GATED ? kSmemGated : kSmemBytes) != cudaSuccess) {
-      set_error("gemm: cannot set dynamic shared memory size");
-      return OMNIMOE_ERR_CUDA;
-    }
-    attr_set = true;
+  if (!set_smem_attr(reinterpret_cast<const void*>(gemm_tc_kernel<EPI, BMN>),
+                     EPI == EPI_GATED ? kSmemGated : kSmemBytes)) {
+    set_error("gemm: cannot set dynamic shared memory size");
+    return OMNIMOE_ERR_CUDA;
   }
   CUtensorMap mA, mB, mB2;
   bool ok = make_map(&mA, A, a.M, a.K, BM);
@@ -368,8 +364,8 @@ omnimoe_status launch_tc(const void* A, const void* B, const GemmArgs& a, cudaSt
     const double a_bytes = (double)a.M * a.K * 2, b_bytes = (double)a.N * a.K * 2 * (EPI == EPI_SWIGLU ? 2 : 1);
     ka.m_fast = (a_bytes < b_bytes && a_bytes <= 48.0 * (1 << 20)) ? 1 : 0;
   }
-  if (const char* e = getenv("OMNIMOE_GEMM_MFAST")) ka.m_fast = atoi(e);
-  gemm_tc_kernel<EPI, BMN><<<(int)std::min<int64_t>(tiles, kSMs), 128 + 32 * kEpiWarps,
+  if (tuning().gemm_mfast >= 0) ka.m_fast = tuning().gemm_mfast;
+  gemm_tc_kernel<EPI, BMN><<<(int)std::min<int64_t>(tiles, num_sms()), 128 + 32 * kEpiWarps,
                         EPI == EPI_GATED ? kSmemGated : kSmemBytes, st>>>(
       mA, mB, mB2, ka);
   OMNI_CHECK_LAUNCH("gemm_tc_kernel");

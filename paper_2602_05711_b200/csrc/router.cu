@@ -984,7 +984,7 @@ omnimoe_status select_params(const omnimoe_dims& d, int64_t T, SelectParams* p, 
   // small K uses select_warp_kernel instead (launch_select)
   // one CTA per token-head (1024 threads when K is in the thousands: the key buffers then
   // allow only one CTA per SM, and more threads hide more latency)
-  p->group = getenv("OMNIMOE_SELECT_WARP_GROUP") && p->pkeep <= 1024 ? 32 : (p->pkeep >= 2048 ? 1024 : 256);
+  p->group = tuning().select_warp_group && p->pkeep <= 1024 ? 32 : (p->pkeep >= 2048 ? 1024 : 256);
   const size_t gb = p->group == 32 ? group_bytes<32>(*p) : p->group == 256 ? group_bytes<256>(*p) : group_bytes<1024>(*p);
   p->groups_per_cta = p->group == 32 ? (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024 - cand_bytes) / gb)) : 1;
   *smem = cand_bytes + gb * p->groups_per_cta;
@@ -1013,7 +1013,7 @@ omnimoe_status launch_dense_select(const omnimoe_dims& d, int64_t T, const float
   }
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dense_select_kernel, 1024, sm);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(T, (int64_t)kSMs * std::max(per_sm, 1)));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(T, (int64_t)num_sms() * std::max(per_sm, 1)));
   dense_select_kernel<<<grid, 1024, sm, st>>>((int)T, (int)N, K, plen, logits, idx, gate, score);
   OMNI_CHECK_LAUNCH("dense_select_kernel");
   return OMNIMOE_OK;
@@ -1035,14 +1035,14 @@ size_t select_cand_ws_bytes(const omnimoe_dims& d) {
 omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* logits, int32_t* idx,
                              float* gate, float* score, uint32_t* cand_ws, cudaStream_t st) {
   if (p.top_k + 1 <= 32 && p.C <= 160) {  // small K: warp per token-head, repeated arg-max
-    const int grid = std::max(1, std::min((p.T + 7) / 8, kSMs * 8));
+    const int grid = std::max(1, std::min((p.T + 7) / 8, num_sms() * 8));
     select_warp_kernel<<<grid, 256, 0, st>>>(p, logits, idx, gate, score);
     OMNI_CHECK_LAUNCH("select_warp_kernel");
     return OMNIMOE_OK;
   }
   if (!p.sorted && p.top_k >= 32 && std::min(p.top_k, p.n_rows) <= 1024 && std::min(p.top_k, p.n_cols) <= 1024 &&
       cand_ws &&
-      !getenv("OMNIMOE_SELECT_CTA")) {
+      !tuning().select_cta) {
     // candidate-order output (the layer path): warp per token-head, bucket selection
     const int K = p.top_k, kr = std::min(K, p.n_rows), kc = std::min(K, p.n_cols);
     const int C = bucket_cand_count(K, p.n_rows, p.n_cols);
@@ -1058,7 +1058,7 @@ omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* lo
     // in global memory, read through L1, for twice the resident warps (C4: 1.17 vs 1.49 ms)
     const bool fits = cand_bytes + warps * per_warp <= 200 * 1024;
     const bool in_smem =
-        fits && (2 * (cand_bytes + warps * per_warp) <= 220 * 1024 || (int64_t)p.T <= (int64_t)warps * kSMs);
+        fits && (2 * (cand_bytes + warps * per_warp) <= 220 * 1024 || (int64_t)p.T <= (int64_t)warps * num_sms());
     const size_t sm = (in_smem ? cand_bytes : 0) + warps * per_warp;
     if (sm <= 200 * 1024) {
       cand_table_kernel<<<1, 1024, 0, st>>>(K, kr, kc, cand_ws);
@@ -1070,7 +1070,7 @@ omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* lo
       }
       int per_sm = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, sm);
-      const int grid = std::max(1, std::min((p.T + warps - 1) / warps, kSMs * std::max(per_sm, 1)));
+      const int grid = std::max(1, std::min((p.T + warps - 1) / warps, num_sms() * std::max(per_sm, 1)));
       kern<<<grid, warps * 32, sm, st>>>(p, C, Pr, Pc, cand_ws, logits, idx, gate, score);
       OMNI_CHECK_LAUNCH("select_bucket_kernel");
       return OMNIMOE_OK;
@@ -1085,7 +1085,7 @@ omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* lo
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   const int per_cta = threads / p.group;
-  const int grid = std::max(1, std::min((p.T + per_cta - 1) / per_cta, kSMs * std::max(per_sm, 1)));
+  const int grid = std::max(1, std::min((p.T + per_cta - 1) / per_cta, num_sms() * std::max(per_sm, 1)));
   kern<<<grid, threads, smem, st>>>(p, logits, idx, gate, score);
   OMNI_CHECK_LAUNCH("select_kernel");
   return OMNIMOE_OK;

@@ -29,10 +29,6 @@ namespace omni {
 namespace {
 using namespace tc;
 
-int env_int(const char* name, int dflt) {  // measurement overrides (tools/ sweeps)
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
 
 constexpr int kMaxBits = 22;  // |X| < 2^22 => three balanced base-256 digits fit int8
 
@@ -573,7 +569,7 @@ omnimoe_status launch_exact_dd(int dtype, const void* x, const void* sub, int d,
                                cudaStream_t st) {
   int grid;
   if (mode == 0) grid = (int)std::min<int64_t>((int64_t)L * ((NC + 127) / 128), 1 << 30);
-  else grid = kSMs * 8;
+  else grid = num_sms() * 8;
   if (grid <= 0) return OMNIMOE_OK;
   if (dtype == OMNIMOE_BF16)
     exact_dd_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(x),
@@ -597,7 +593,7 @@ omnimoe_status exact_logits(const omnimoe_dims& d, int64_t L, const void* x, con
     set_error("route: memset failed");
     return OMNIMOE_ERR_CUDA;
   }
-  const int grid_x = (int)std::min<int64_t>((L + 7) / 8, kSMs * 16);
+  const int grid_x = (int)std::min<int64_t>((L + 7) / 8, num_sms() * 16);
   limb_split_kernel<<<std::max(grid_x, 1), 256, 0, st>>>(static_cast<const uint16_t*>(x), L, (int)d.d, w.limbs_x,
                                                          w.ex, w.bad_x, w.counts);
   OMNI_CHECK_LAUNCH("limb_split_kernel(x)");
@@ -605,18 +601,14 @@ omnimoe_status exact_logits(const omnimoe_dims& d, int64_t L, const void* x, con
                                                   w.ew, w.bad_w, w.counts + 1);
   OMNI_CHECK_LAUNCH("limb_split_kernel(subkeys)");
 
-  static bool attr_set = false;
-  if (!attr_set) {
-    for (auto k : {gemm_i8_exact_kernel<1>, gemm_i8_exact_kernel<2>, gemm_i8_exact_kernel<4>, gemm_i8_persist_kernel})
-      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kISmemBytes) != cudaSuccess) {
-        set_error("route: cannot set dynamic shared memory size of the i8 GEMM");
-        return OMNIMOE_ERR_CUDA;
-      }
-    attr_set = true;
-  }
+  for (auto k : {gemm_i8_exact_kernel<1>, gemm_i8_exact_kernel<2>, gemm_i8_exact_kernel<4>, gemm_i8_persist_kernel})
+    if (!set_smem_attr(reinterpret_cast<const void*>(k), kISmemBytes)) {
+      set_error("route: cannot set dynamic shared memory size of the i8 GEMM");
+      return OMNIMOE_ERR_CUDA;
+    }
   // clusters of CN CTAs along N multicast the A limbs (CN | number of N tiles)
   const int n_tiles = (NC + IBN - 1) / IBN;
-  int CN = std::max(1, std::min(4, env_int("OMNIMOE_I8_CLUSTER", 1)));
+  int CN = std::max(1, std::min(4, tuning().i8_cluster));
   while (CN > 1 && n_tiles % CN) CN >>= 1;
   CUtensorMap mA, mB;
   const bool ok =
@@ -628,9 +620,9 @@ omnimoe_status exact_logits(const omnimoe_dims& d, int64_t L, const void* x, con
   }
   I8Args a{(int)L, NC, (int)d.d, w.ex, w.ew, logits};
   dim3 grid(n_tiles, (unsigned)((L + IBM - 1) / IBM));
-  if (CN == 1 && env_int("OMNIMOE_I8_PERSIST", 1)) {
+  if (CN == 1 && tuning().i8_persist) {
     const int64_t tiles = (int64_t)grid.x * grid.y;
-    gemm_i8_persist_kernel<<<(int)std::min<int64_t>(tiles, kSMs), 128 + 32 * kIEpiWarps, kISmemBytes, st>>>(mA, mB,
+    gemm_i8_persist_kernel<<<(int)std::min<int64_t>(tiles, num_sms()), 128 + 32 * kIEpiWarps, kISmemBytes, st>>>(mA, mB,
                                                                                                          a);
   } else if (CN == 1) {
     gemm_i8_exact_kernel<1><<<grid, 256, kISmemBytes, st>>>(mA, mB, a);

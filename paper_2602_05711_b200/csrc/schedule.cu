@@ -524,16 +524,16 @@ __global__ void load_stats_final_kernel(const double* __restrict__ partial, int 
 
 int grid_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
-  return (int)std::min<int64_t>(std::max<int64_t>(b, 1), kSMs * 16);
+  return (int)std::min<int64_t>(std::max<int64_t>(b, 1), num_sms() * 16);
 }
 
 }  // namespace
 
-size_t load_stats_ws_bytes() { return 2 * kSMs * 2 * sizeof(double); }
+size_t load_stats_ws_bytes() { return 2 * num_sms() * 2 * sizeof(double); }
 
 omnimoe_status load_stats_run(const omnimoe_plan& plan, double* out, void* ws, cudaStream_t st) {
   const int64_t n_loc = plan.expert_end - plan.expert_begin;
-  const int nblk = kSMs * 2;
+  const int nblk = num_sms() * 2;
   load_stats_kernel<<<nblk, 256, 0, st>>>(plan.expert_offsets, n_loc, static_cast<double*>(ws));
   OMNI_CHECK_LAUNCH("load_stats_kernel");
   load_stats_final_kernel<<<1, 1, 0, st>>>(static_cast<const double*>(ws), nblk, n_loc, plan.expert_offsets, out);
@@ -610,7 +610,7 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
         OMNI_CHECK_LAUNCH("token_offsets_kernel");
       }
       const int64_t band_size = (n_loc + n_bands - 1) / n_bands;
-      band_partition_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((n_tok + 7) / 8, kSMs * 16)), 256, 0,
+      band_partition_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((n_tok + 7) / 8, num_sms() * 16)), 256, 0,
                               st>>>(ids, plan.expert_begin, n_loc, token ? tok_off : nullptr, hk, M, n_tok,
                                     (int)n_bands, band_size, dest, plan.task_pair, plan.token_offsets);
       OMNI_CHECK_LAUNCH("band_partition_kernel");
@@ -630,11 +630,11 @@ omnimoe_status schedule_run(int64_t M, const int32_t* ids, const float* gate, co
     OMNI_CHECK_LAUNCH("count_scatter_kernel");
     const int32_t* dst = vorder && n_bands > 1 ? dest : nullptr;
     int32_t* stask = vorder ? plan.sorted_task : nullptr;
-    segment_sort_kernel<<<kSMs * 4, 256, 0, st>>>(plan.active, plan.n_active, plan.expert_offsets, perm, token, hk,
+    segment_sort_kernel<<<num_sms() * 4, 256, 0, st>>>(plan.active, plan.n_active, plan.expert_offsets, perm, token, hk,
                                                   dst, plan.sorted_token, plan.sorted_gate, plan.sorted_expert, stask,
                                                   big, big_count);
     OMNI_CHECK_LAUNCH("segment_sort_kernel");
-    segment_sort_big_kernel<<<kSMs * 4, 256, 0, st>>>(big, big_count, plan.expert_offsets, perm, token, hk, dst,
+    segment_sort_big_kernel<<<num_sms() * 4, 256, 0, st>>>(big, big_count, plan.expert_offsets, perm, token, hk, dst,
                                                  plan.sorted_token, plan.sorted_gate, plan.sorted_expert, stask);
     OMNI_CHECK_LAUNCH("segment_sort_big_kernel");
     return OMNIMOE_OK;

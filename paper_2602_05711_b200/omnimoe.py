@@ -14,7 +14,8 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libomnimoe.so")
+# OMNIMOE_LIB: another build of the same library (the measurement build of tools/ sweeps)
+LIB_PATH = os.environ.get("OMNIMOE_LIB") or os.path.join(_PKG, "libomnimoe.so")
 
 BF16, F32 = 0, 1
 SILU, IDENTITY = 0, 1

@@ -414,27 +414,19 @@ def v_geom(request):
     return request.param
 
 
-@pytest.fixture(params=["auto", "warp"])
-def v_mode(request, monkeypatch):
-    """pass V kernel for one slice per item: auto (8 tokens per warp for h*K <= 64) or
-    forced one token per warp."""
-    if request.param == "warp":
-        monkeypatch.setenv("OMNIMOE_V_GROUP_MAX_TASKS", "0")
-    return request.param
-
-
 @pytest.mark.parametrize("B", [0, 2, 512])
 @pytest.mark.parametrize("d,act", [(64, om.SILU), (192, om.SILU), (1024, om.SILU), (2048, om.SILU),
                                    (64, om.IDENTITY)])
 @pytest.mark.parametrize("accumulate", [False, True])
-def test_expert_fwd_sliced_given_plan(d, act, B, accumulate, v_geom, v_mode):
+@pytest.mark.parametrize("HK", [12, 96])  # pass V: 8 tokens per warp (h*K <= 64) / one token per warp
+def test_expert_fwd_sliced_given_plan(d, act, B, accumulate, v_geom, HK):
     rng = np.random.default_rng(d + B)
-    L, N, HK = 200, 3000, 12
+    L, N = 200, 3000
     dims = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, act=act, group_size=B, v_layout=om.V_SLICED,
                         **v_geom)
     inp = make_inputs(dims, L, 9, skip=("subkeys",))
-    base = rng.integers(0, N - 64, L)
-    ids = np.stack([b0 + rng.choice(64, HK, replace=False) for b0 in base]).astype(np.int32)
+    base = rng.integers(0, N - 128, L)
+    ids = np.stack([b0 + rng.choice(128, HK, replace=False) for b0 in base]).astype(np.int32)
     ids[7] = ids[3]  # two tokens with identical expert lists
     gates = rng.random((L, HK)).astype(np.float32)
     plan = om.schedule(dims, torch.from_numpy(ids).cuda().reshape(-1), torch.from_numpy(gates).cuda().reshape(-1))
@@ -456,7 +448,7 @@ def test_expert_fwd_sliced_given_plan(d, act, B, accumulate, v_geom, v_mode):
     assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
 
 
-def test_expert_fwd_sliced_shard_and_empty_tokens(v_geom, v_mode):
+def test_expert_fwd_sliced_shard_and_empty_tokens(v_geom):
     """Expert range of a shard (tasks outside it are skipped) and tokens with no
     tasks in range (their y_routed rows are written as zeros)."""
     rng = np.random.default_rng(3)
@@ -484,7 +476,7 @@ def test_expert_fwd_sliced_shard_and_empty_tokens(v_geom, v_mode):
 
 @pytest.mark.parametrize("mode", [synth.NORMAL, synth.DYADIC])
 @pytest.mark.parametrize("B", [0, 5])
-def test_layer_c1_sliced(mode, B, v_geom, v_mode):
+def test_layer_c1_sliced(mode, B, v_geom):
     w = _dims("C1", group_size=B, v_layout=om.V_SLICED, **v_geom)
     dims = w.dims
     inp = make_inputs(dims, w.L, w.seed, mode)

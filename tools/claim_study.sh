@@ -2,6 +2,9 @@
 # pass-V claim pipeline: parity of the executors, then C5/C3a per-kernel times with the
 # executor's work counters at the committed offset and shifted by 4 KB / 14 KB
 cd "$(dirname "$0")/.."
+# OMNIMOE_* knobs are read only by the measurement build (csrc/tuning.cuh)
+python -m paper_2602_05711_b200.build --measure > /dev/null
+export OMNIMOE_LIB=$(pwd)/paper_2602_05711_b200/libomnimoe_measure.so
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 OUT=gpurun_out/${TAG:-claim}
 mkdir -p $OUT
