@@ -141,3 +141,22 @@ def test_layer_f32_reduced_c3(c3_f32, ek, B):
                                   np.sort(idx_ref.reshape(w.L, -1), -1))
     e_tok, e_elt = rel_errors(y.cpu().numpy(), y_ref)
     assert e_tok <= 1e-5 and e_elt <= 1e-5, (e_tok, e_elt)
+
+
+@pytest.mark.parametrize("K", [1, 4, 16, 64])
+@pytest.mark.parametrize("L", [1024, 2048, 4096, 8192, 16384])
+def test_c2_sweep_brute_force(L, K):
+    """configs[1]'s router-only sweep (tools/c2_sweep.py times it): at every (L, K) point
+    the key-ordered ids of a 24-token subsample equal brute force over all N cells
+    (Eq.TopK by definition), and the whole batch's sets equal the product path."""
+    w = configs.get("C2", top_k=K)
+    dims = w.dims
+    inp = make_inputs(dims, L, w.seed, skip=("W", "V", "w_gate_up", "w_down"))
+    idx, gate, _ = om.route(dims, inp["x"], inp["subkeys"], want_score=False)
+    torch.cuda.synchronize()
+    idx = idx.cpu().numpy().reshape(L, dims.n_heads, K)
+    toks = np.unique(np.concatenate([[0, L - 1], np.random.default_rng(L + K).choice(L, 22, replace=False)]))
+    lg, _ = _oracle_logits(dims, w.seed, toks)
+    rows = lg.reshape(-1, dims.n_rows + dims.n_cols)
+    bf = oracle.route(rows, dims.n_rows, dims.n_cols, K, method=oracle.BRUTE)
+    np.testing.assert_array_equal(idx[toks].reshape(-1, K), bf["idx"])
