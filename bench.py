@@ -103,7 +103,9 @@ def expected_eta(dims, L):
     return M / (N * -math.expm1(-M / N))
 
 
-L2_GATHER_GBS = 14404.1  # measured: random 4 KB row gathers from an L2-resident table (tools/microbench.cu)
+# measured L2 -> SM gather ceilings of this B200 (tools/l2_ceiling.cu, profiles/r2/l2_ceiling/):
+# random pieces from a 64 MB L2-resident table with 256-bit loads
+L2_GATHER_GBS = {"piece128": 18757.0, "row4k": 19414.0}
 
 
 def a6_algorithmic_bytes(dims, L, n_active, M):
@@ -116,7 +118,7 @@ def a6_algorithmic_bytes(dims, L, n_active, M):
 
 def ncu_traffic(config, kernel):
     """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
-    p = os.path.join(ROOT, "profiles", "r1", "ncu_summary.json")
+    p = os.path.join(ROOT, "profiles", "r2", "ncu_summary.json")
     if not os.path.exists(p):
         return None, None
     j = json.load(open(p))
@@ -367,37 +369,46 @@ def bench_single(args, w, lr):
         zb = n_active * dims.d * eb + L * dims.d * eb + 12 * M + 4 * M              # W rows once, x, plan, a
         vb = n_active * dims.d * eb + 8 * M + 4 * L * dims.d                       # V rows once, pairs, y write
         zl2 = M * dims.d * eb + n_active * dims.d * eb + 12 * M                    # x per task + W + plan
-        vl2 = M * dims.d * eb + 8 * M * (dims.d // 64)                             # v slices per task + pairs per slice
-        cand = {"expert_zdot_kernel": (zb, zl2, stage_ms["a6_pass_z"]),
-                "expert_vslice_kernel": (vb, vl2, stage_ms["a6_pass_v"])}
+        nbv = om.v_bands(dims, dims.N, L)
+        vl2 = M * dims.d * eb + 8 * M * (dims.d // 64) + 4 * L * dims.d * (2 * nbv - 1)  # v pieces + pairs + y
+        zk = "expert_zdot256_kernel" if dims.d % 512 == 0 else "expert_zdot_kernel"
+        cand = {zk: (zb, zl2, stage_ms["a6_pass_z"], L2_GATHER_GBS["row4k"], 1),
+                "expert_vslice_kernel": (vb, vl2, stage_ms["a6_pass_v"], L2_GATHER_GBS["piece128"], nbv)}
         kern = max(cand, key=lambda k: cand[k][2])
-        for k, (hb, l2b, kms) in cand.items():
-            other[k] = {"algorithmic_hbm_bytes": hb, "ms": kms, "hbm_gbs": hb / kms / 1e6,
+        for k, (hb, l2b, kms, l2pk, nl) in cand.items():
+            other[k] = {"algorithmic_hbm_bytes": hb, "ms": kms, "launches": nl, "hbm_gbs": hb / kms / 1e6,
                         "hbm_frac": hb / kms / 1e6 / pk["hbm"], "l2_bytes_dataflow": l2b,
-                        "l2_gbs": l2b / kms / 1e6, "l2_frac": l2b / kms / 1e6 / L2_GATHER_GBS}
-        a6_bytes, l2_bytes, a6_ms = cand[kern]
+                        "l2_gbs": l2b / kms / 1e6, "l2_peak_gbs": l2pk, "l2_frac": l2b / kms / 1e6 / l2pk}
+        a6_bytes, l2_bytes, a6_ms, l2_peak, n_launch = cand[kern]
     else:
         kern = "expert_token_kernel" if token else ("expert_group_tma_kernel" if B > 1 else "expert_warp_kernel")
         if dense:
             kern = "gemm_tc_kernel (dense routed branch)"
         a6_bytes, a6_ms = a6_algorithmic_bytes(dims, L, n_active, M), stage_ms["expert_a6"]
-        l2_bytes = 2 * M * dims.d * 2
+        l2_bytes, l2_peak, n_launch = 2 * M * dims.d * 2, L2_GATHER_GBS["row4k"], 1
     a6_gbs = a6_bytes / (a6_ms / 1000.0) / 1e9
     traffic, tsrc = ncu_traffic(w.name, kern)
+    if traffic is not None:  # ncu captures one launch; a pass of n_launch band launches moves n_launch x that
+        traffic *= n_launch
     if dense:  # two dense GEMMs: the tensor roofline (L x N x d MACs each)
         tf = 2 * 2.0 * L * dims.N * dims.d / (a6_ms / 1000.0) / 1e12
         roofline = {"bound": "tensor", "achieved": tf, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
                     "frac": tf / pk["bf16_sus"], "traffic": None, "kernel": "gemm_tc_kernel x2 (dense routed branch)",
                     "avg_launch_ms": a6_ms, "peak_source": pk["src"] + " bf16 sustained",
-                    "note": f"eta = {eta:.0f}: Z = x W^T and y = A V on tcgen05 (DESIGN.md §4.4)"}
+                    "note": f"eta = {eta:.0f}: Z = x W^T and y = A V on tcgen05 (DESIGN.md §4.4)",
+                    # the method's own work: 2 FLOP per task for z = x.w_e and 2 for y += a v_e, per column
+                    "method_work": {"flop": 4.0 * dims.d * M,
+                                    "achieved_tflops": 4.0 * dims.d * M / (a6_ms / 1000.0) / 1e12,
+                                    "dense_equivalent_flop": 2 * 2.0 * L * dims.N * dims.d,
+                                    "note": "the dense GEMMs do L N d MACs each; the method needs 2 d per task"}}
     if not dense:
       roofline = {"bound": "hbm", "achieved": a6_gbs, "peak": pk["hbm"], "unit": "GB/s", "frac": a6_gbs / pk["hbm"],
                 "traffic": traffic, "kernel": f"{kern} (a6)", "algorithmic_bytes_per_launch": a6_bytes,
                 "avg_launch_ms": a6_ms, "peak_source": pk["src"] + " hbm_gbs (copy)",
                 "traffic_source": tsrc,
                 "l2": {"bytes_per_launch": l2_bytes, "achieved_gbs": l2_bytes / (a6_ms / 1000.0) / 1e9,
-                       "peak_gbs": L2_GATHER_GBS, "frac": l2_bytes / (a6_ms / 1000.0) / 1e9 / L2_GATHER_GBS,
-                       "peak_source": "tools/microbench.cu l2_gather_4KB_rows_gbs (profiles/r1/microbench.json)"},
+                       "peak_gbs": l2_peak, "frac": l2_bytes / (a6_ms / 1000.0) / 1e9 / l2_peak,
+                       "peak_source": "tools/l2_ceiling.cu (profiles/r2/l2_ceiling/l2_ceiling.json)"},
                 "note": f"every task moves a d-row of x (pass Z) and of V (pass V) through L2 whatever the loop "
                         f"order (eta = M/|E_active| = {eta:.1f} tasks share an expert, the only reuse); the binding "
                         "roofline is L2 -> SM throughput, not HBM -- DESIGN.md §4.4, profiles/r1/README.md"}

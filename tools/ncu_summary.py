@@ -1,4 +1,4 @@
-"""Summarise ncu captures into profiles/r1/ncu_summary.json (read by bench.py for
+"""Summarise ncu captures into profiles/r2/ncu_summary.json (read by bench.py for
 roofline.traffic) and print a short table.
 
     python tools/ncu_summary.py CONFIG report.ncu-rep [report2.ncu-rep ...]
@@ -12,7 +12,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OUT = os.path.join(ROOT, "profiles", "r1", "ncu_summary.json")
+OUT = os.path.join(ROOT, "profiles", "r2", "ncu_summary.json")
 WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
         "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
