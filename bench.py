@@ -490,8 +490,15 @@ def bench_multi(args, w, ws, rk, lr):
     comm = ep.TorchComm()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream()
+    dx = None
+    if args.exchange == "device":  # N3: the fused exchange on the NCCL device API
+        hk = dims.n_heads * dims.top_k
+        dx = ep.DevExchange(dims, row_cap=L, rec_cap=int(1.5 * L * hk / ws) + 4096)
 
     def step(x=None, marks=None):
+        if dx is not None:
+            return ep.ep_layer_fwd_dev(ops, dx, inp["x"] if x is None else x, inp["subkeys"], inp["W"], inp["V"],
+                                       n_per, marks=marks)
         return ep.ep_layer_fwd(ops, comm, inp["x"] if x is None else x, inp["subkeys"], inp["W"], inp["V"], n_per,
                                marks=marks)
 
@@ -527,6 +534,8 @@ def bench_multi(args, w, ws, rk, lr):
     # message sizes of one more step: rows / records this rank sent to OTHER ranks (its own
     # block stays local), the bf16 partial rows it sent back; the records it processed
     y_out, rst = ep.ep_layer_fwd(ops, comm, inp["x"], inp["subkeys"], inp["W"], inp["V"], n_per, return_state=True)
+    if dx is not None:
+        y_out = step()
     torch.cuda.synchronize()
     cnt = ops.last_route  # this rank's routing (that step)
     eb = 2 if dims.dtype == 0 else 4
@@ -589,7 +598,7 @@ def bench_multi(args, w, ws, rk, lr):
                 "data": "synthetic (seeded counter-based generator, DESIGN.md §3)",
                 "config": dict(_config_dict(w, f"ep{ws} (experts row-sharded, tokens data-parallel, "
                                                f"{args.backend} all-to-all)"), global_tokens=L, tokens_per_gpu=L_loc,
-                               backend=args.backend),
+                               backend=args.backend, exchange=args.exchange),
                 "phase_ms_rank0": phase_ms, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
                 "parity": parity, "gpu_launches": launches, "launches_per_step": launches / max(args.steps, 1),
                 "clocks": clk.summary()}
@@ -609,6 +618,8 @@ def main():
     ap.add_argument("--config", default=None,
                     help="workload (default: C3a on one GPU -- configs[2]; C5 over N > 1 GPUs -- configs[4], "
                          "the expert-sharded scale-out, strong scaling)")
+    ap.add_argument("--exchange", default="host", choices=["host", "device"],
+                    help="N > 1: host (NCCL all_to_all) or device (fused peer stores on the NCCL device API, N3)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="N > 1 process group: nccl (the product), or gloo with host-staged all-to-alls (dry run)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

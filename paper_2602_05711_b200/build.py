@@ -42,9 +42,32 @@ def build(force: bool = False, verbose: bool = False, measure: bool = False) -> 
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
+    build_ep(force)
     if force or _stale(SYNTH_LIB, [SYNTH_SRC]):
         subprocess.check_call([NVCC, *ARCH, *FLAGS, "-o", SYNTH_LIB, SYNTH_SRC])
     return lib
+
+
+EP_SRC = os.path.join(CSRC, "nccl", "ep_dev.cu")
+EP_LIB = os.path.join(PKG, "libomnimoe_ep.so")
+
+
+def nccl_dirs():
+    """The NCCL 2.28 headers (with the device API) and library torch uses."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    base = list(spec.submodule_search_locations)[0] if spec else ""
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
+def build_ep(force: bool = False) -> str:
+    """libomnimoe_ep.so: the fused expert-parallel exchange on the NCCL device API
+    (include/omnimoe_ep.h), linked against torch's libnccl.so.2."""
+    inc, lib = nccl_dirs()
+    if force or _stale(EP_LIB, [EP_SRC, os.path.join(ROOT, "include", "omnimoe_ep.h")]):
+        subprocess.check_call([NVCC, *ARCH, *FLAGS, "-I" + inc, "-o", EP_LIB, EP_SRC, "-L" + lib, "-l:libnccl.so.2",
+                               "-Xlinker", "-rpath=" + lib])
+    return EP_LIB
 
 
 if __name__ == "__main__":

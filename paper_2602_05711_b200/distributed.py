@@ -263,3 +263,122 @@ def ep_layer_fwd_loopback(ops, xs, subkeys, W_locs, V_locs, n_per: int):
 def shard_rows(t, R: int, r: int):
     n = t.shape[0] // R
     return t[r * n:(r + 1) * n]
+
+
+# ---------------------------------------------------------------- fused device-API exchange (N3)
+class _DevPtr:
+    """A device buffer exposed to torch.as_tensor through __cuda_array_interface__."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class DevExchange:
+    """The dispatch / return exchange on the NCCL device API (libomnimoe_ep.so,
+    include/omnimoe_ep.h): symmetric windows, peer stores over NVLink from the GPU's own
+    kernels, in-kernel LSA barriers -- no NCCL collective in the forward.  row_cap / rec_cap:
+    capacities of the receive windows (rows and task records any rank can receive)."""
+
+    def __init__(self, dims: om.LayerDims, row_cap: int, rec_cap: int, group=None):
+        import ctypes
+        import os
+        from . import build
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libomnimoe_ep.so")
+        if not os.path.exists(path):
+            raise om.OmniMoEError(f"{path} not built (build.build_ep())")
+        self.lib = lib = ctypes.CDLL(path)
+        V, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+        lib.omnimoe_ep_dev_unique_id_bytes.restype = ctypes.c_size_t
+        lib.omnimoe_ep_dev_unique_id.argtypes = [V]
+        lib.omnimoe_ep_dev_create.argtypes = [V, I32, I32, I64, I64, I64, ctypes.POINTER(V)]
+        lib.omnimoe_ep_dev_destroy.argtypes = [V]
+        lib.omnimoe_ep_dev_buffers.argtypes = [V, ctypes.POINTER(V), ctypes.POINTER(V), ctypes.POINTER(V),
+                                               ctypes.POINTER(V)]
+        lib.omnimoe_ep_dev_dispatch.argtypes = [V, V, V, V, V]
+        lib.omnimoe_ep_dev_return.argtypes = [V, V, I64, V]
+        lib.omnimoe_ep_last_error.restype = ctypes.c_char_p
+        for f in ("omnimoe_ep_dev_unique_id", "omnimoe_ep_dev_create", "omnimoe_ep_dev_destroy",
+                  "omnimoe_ep_dev_buffers", "omnimoe_ep_dev_dispatch", "omnimoe_ep_dev_return"):
+            getattr(lib, f).restype = ctypes.c_int
+        self.dims, self.row_cap, self.rec_cap = dims, row_cap, rec_cap
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        nb = lib.omnimoe_ep_dev_unique_id_bytes()
+        uid = (ctypes.c_uint8 * nb)()
+        if self.rank == 0:
+            self._check(lib.omnimoe_ep_dev_unique_id(ctypes.cast(uid, V)), "unique_id")
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0, group=group)
+        ctypes.memmove(uid, box[0], nb)
+        self.handle = V()
+        self._check(lib.omnimoe_ep_dev_create(ctypes.cast(uid, V), self.rank, self.world, dims.d, row_cap, rec_cap,
+                                              ctypes.byref(self.handle)), "create")
+        px, pr, py, pc = V(), V(), V(), V()
+        self._check(lib.omnimoe_ep_dev_buffers(self.handle, ctypes.byref(px), ctypes.byref(pr), ctypes.byref(py),
+                                               ctypes.byref(pc)), "buffers")
+        R = self.world
+        self.x_recv = torch.as_tensor(_DevPtr(px.value, (row_cap, dims.d), "<i2"), device="cuda").view(torch.bfloat16)
+        self.rec = torch.as_tensor(_DevPtr(pr.value, (rec_cap, 3), "<i4"), device="cuda")
+        self.y_ret = torch.as_tensor(_DevPtr(py.value, (row_cap, dims.d), "<i2"), device="cuda").view(torch.bfloat16)
+        self.counts = torch.as_tensor(_DevPtr(pc.value, (R, R, 2), "<i8"), device="cuda")
+
+    def _check(self, rc, what):
+        if rc != 0:
+            raise om.OmniMoEError(f"ep_dev {what}: status {rc}: {self.lib.omnimoe_ep_last_error().decode()}")
+
+    def _stream(self):
+        import ctypes
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def dispatch(self, x_send, rec_send, counts):
+        import ctypes
+        self._check(self.lib.omnimoe_ep_dev_dispatch(self.handle, ctypes.c_void_p(x_send.data_ptr()),
+                                                     ctypes.c_void_p(rec_send.data_ptr()),
+                                                     ctypes.c_void_p(counts.contiguous().data_ptr()),
+                                                     self._stream()), "dispatch")
+
+    def return_(self, y_part):
+        import ctypes
+        self._check(self.lib.omnimoe_ep_dev_return(self.handle, ctypes.c_void_p(y_part.data_ptr()),
+                                                   y_part.shape[0], self._stream()), "return")
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self.lib.omnimoe_ep_dev_destroy(self.handle)
+            self.handle = None
+
+
+def ep_layer_fwd_dev(ops: LibOps, dx: DevExchange, x_loc, subkeys, W_loc, V_loc, n_per: int, marks=None):
+    """One expert-parallel layer forward with the fused device-API exchange (N3): same
+    pack / unpack / schedule / expert / combine kernels as ep_layer_fwd, the messages moved by
+    the GPU's own peer stores into the symmetric windows.  One 8 R^2-byte read of the counts
+    matrix per forward sizes the receiver's schedule (its sizes are host values)."""
+    mark = marks or (lambda name: None)
+    R = dx.world
+    st = RankState(x=x_loc, W_loc=W_loc, V_loc=V_loc)
+    mark("start")
+    phase_dispatch(ops, st, subkeys, R)
+    side = _Side(x_loc)
+    H = side.run(ops.mlp_hidden, x_loc)
+    mark("dispatch")
+    dx.dispatch(st.x_send, st.rec_send, st.counts)
+    cm = dx.counts.cpu()  # [src][dst][rows, records]
+    me = dx.rank
+    rows = int(cm[:, me, 0].sum())
+    M = int(cm[:, me, 1].sum())
+    st.send_tok = cm[me, :, 0].tolist()
+    if rows > dx.row_cap or M > dx.rec_cap or sum(st.send_tok) > dx.row_cap:
+        raise om.OmniMoEError(f"ep_dev: capacities exceeded (rows {rows}, records {M}, caps {dx.row_cap}, {dx.rec_cap})")
+    mark("all_to_all_dispatch")
+    dev = x_loc.device
+    z = torch.zeros(2, dtype=torch.int64, device=dev)
+    ids, gate, tok = ops.unpack(dx.rec[:M], 1, torch.tensor([0, M], dtype=torch.int64, device=dev), z)
+    st.y_part = ops.expert(dx.x_recv[:rows], W_loc, V_loc, ids, gate, tok, n_per)
+    mark("expert")
+    dx.return_(st.y_part)
+    st.y_ret = dx.y_ret[:sum(st.send_tok)]
+    mark("all_to_all_combine")
+    side.join(x_loc, H)
+    phase_combine(ops, st, H)
+    mark("combine_mlp")
+    return st.y

@@ -81,3 +81,19 @@ def test_oracle_includes_no_cuda():
     src = open(os.path.join(ROOT, "oracle", "oracle.cpp")).read()
     incs = re.findall(r"^\s*#\s*include\s*[<\"]([^>\"]+)", src, re.M)
     assert incs and not any("cuda" in i.lower() or "omnimoe" in i or "csrc" in i for i in incs), incs
+
+
+def test_ep_device_library_exports():
+    """libomnimoe_ep.so (the NCCL device-API exchange, N3) builds and exports what
+    include/omnimoe_ep.h declares; it is a separate library (libomnimoe.so has no NCCL)."""
+    from paper_2602_05711_b200 import build
+    path = build.build_ep()
+    ep = ctypes.CDLL(path)
+    hdr = open(os.path.join(ROOT, "include", "omnimoe_ep.h")).read()
+    names = sorted(set(re.findall(r"\b(omnimoe_ep_[a-z_0-9]+)\s*\(", hdr)))
+    assert "omnimoe_ep_dev_dispatch" in names and "omnimoe_ep_dev_return" in names
+    for n in names:
+        assert hasattr(ep, n), n
+    assert ep.omnimoe_ep_dev_unique_id_bytes() == 128
+    out = subprocess.run(["ldd", build.LIB], capture_output=True, text=True).stdout
+    assert "nccl" not in out

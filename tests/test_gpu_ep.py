@@ -166,3 +166,44 @@ def test_ep_loopback_c5_per_rank_shape(vl):
                        hr("w_gate_up"), hr("w_down"), id_map=np.stack([used, np.arange(len(used))], 1))
     e_tok, e_elt = rel_errors(y[torch.from_numpy(toks).cuda()].float().cpu().numpy(), ref["y"])
     assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
+
+
+def test_ep_device_api_one_rank():
+    """The fused exchange on the NCCL device API (N3: symmetric windows, peer stores,
+    in-kernel LSA barriers) over a real one-rank NCCL communicator -- the only size this
+    box has: the layer output equals the host-API expert-parallel path bit for bit (same
+    kernels, same message layouts) and the single-GPU layer within 1e-2."""
+    script = r'''
+import os, sys, torch, torch.distributed as dist
+sys.path.insert(0, os.getcwd())
+from paper_2602_05711_b200 import build, distributed as ep, omnimoe as om
+from synth.workloads import make_inputs
+from tests.helpers import rel_errors
+build.build_ep()
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+dims = om.LayerDims(d=256, n_rows=64, n_cols=64, top_k=32, n_heads=2, d_ff=256, v_layout=om.V_SLICED)
+full = make_inputs(dims, 384, 7)
+Vs = om.pack_v(dims, full["V"])
+ops = ep.LibOps(dims); ops.set_mlp(full["w_gate_up"], full["w_down"])
+dx = ep.DevExchange(dims, row_cap=384, rec_cap=384 * 64)
+y_dev = ep.ep_layer_fwd_dev(ops, dx, full["x"], full["subkeys"], full["W"], Vs, dims.N)
+y_host = ep.ep_layer_fwd(ops, ep.TorchComm(), full["x"], full["subkeys"], full["W"], Vs, dims.N)
+torch.cuda.synchronize()
+print("EQUAL", bool(torch.equal(y_dev, y_host)))
+y1 = om.layer_fwd(dims, full["x"], full["subkeys"], full["W"], Vs, full["w_gate_up"], full["w_down"])
+torch.cuda.synchronize()
+e = rel_errors(y_dev.float().cpu().numpy(), y1.float().cpu().numpy())
+print("ERR", e[0], e[1])
+dx.close()
+dist.destroy_process_group()
+'''
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", script], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, (out.stdout[-2000:], out.stderr[-3000:])
+    assert "EQUAL True" in out.stdout, out.stdout[-2000:]
+    line = [l for l in out.stdout.splitlines() if l.startswith("ERR")][0]
+    e_tok, e_elt = map(float, line.split()[1:])
+    assert e_tok <= 1e-2 and e_elt <= 1e-2
