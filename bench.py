@@ -183,13 +183,12 @@ def cpu_oracle_rate(w, target_s, max_tokens, nthreads, inp=None, gpu=None):  # n
     return done / total_t, done, total_t, par
 
 
-def run_reference(args):
-    """--impl reference: the oracle on the host cores, bounded sample per step."""
+def run_reference(args, w):
+    """--impl reference: the oracle on the host cores, bounded sample per step, on the
+    workload the other arm times (same config dict)."""
     ws, rk, _ = rank_info()
     if rk != 0:
         return 0
-    from paper_2602_05711_b200 import configs
-    w = configs.get(args.config)
     nth = os.cpu_count() or 1
     per_step_s = max(2.0, args.ref_seconds / max(args.steps, 1))
     tables = None  # expert rows from the generator's host twin: nothing of this arm runs on the GPU
@@ -203,7 +202,9 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * w.L / rate,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config_dict(w, "cpu-oracle"),
+            "config": _arm_config(w, args, ws),
+            "timing_note": ("each step times a bounded token sample of the batch on the host cores; value = "
+                            "sampled tokens / oracle seconds, ms_per_step extrapolates it to the whole batch"),
             "cpu_baseline": {"value": rate, "unit": "tokens/s", "cores": nth, "kind": "oracle",
                              "sample": f"{toks} tokens of {w.name} over {args.steps} steps (~{per_step_s:.0f} s of "
                                        f"oracle time each): exact logits, product top-K, token-centric routed "
@@ -211,6 +212,24 @@ def run_reference(args):
             "e2e": {"value": rate, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _arm_config(w, args, ws):
+    """The config dict both arms print (the driver compares them): the workload, and for one
+    GPU the executor the layer runs, for N > 1 the expert-parallel layout."""
+    from paper_2602_05711_b200 import omnimoe as om
+    dims = w.dims
+    if ws > 1:
+        return dict(_config_dict(w, f"ep{ws} (experts row-sharded, tokens data-parallel, {args.backend} all-to-all)"),
+                    global_tokens=w.L, tokens_per_gpu=w.L // ws, backend=args.backend, exchange=args.exchange)
+    return dict(_config_dict(w, "single-gpu"), group_size=om.group_size(dims), expert_kernel=args.expert_kernel,
+                v_layout="sliced" if dims.v_layout == om.V_SLICED else "rows",
+                executor={om.EXPERT_TOKEN: "token-centric (eta < 2: no expert reuse; ECS skipped)",
+                          om.EXPERT_DENSE: "dense tcgen05 GEMMs (K >= N/40; ECS skipped)",
+                          om.EXPERT_SLICED: "SLICED (ECS pass Z + slice-major pass V)",
+                          om.EXPERT_GROUP: "grouped ECS (rows)",
+                          om.EXPERT_WARP: "expert-major ECS (rows)"}[om.layer_executor(dims, w.L)],
+                eta=expected_eta(dims, w.L))
 
 
 def _config_dict(w, parallelism):
@@ -435,14 +454,7 @@ def bench_single(args, w, lr):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "latency_ms": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded counter-based generator, DESIGN.md §3)",
-        "config": dict(_config_dict(w, "single-gpu"), group_size=B, expert_kernel=args.expert_kernel,
-                       v_layout="sliced" if dims.v_layout == om.V_SLICED else "rows",
-                       executor={om.EXPERT_TOKEN: "token-centric (eta < 2: no expert reuse; ECS skipped)",
-                                 om.EXPERT_DENSE: "dense tcgen05 GEMMs (K >= N/40; ECS skipped)",
-                                 om.EXPERT_SLICED: "SLICED (ECS pass Z + slice-major pass V)",
-                                 om.EXPERT_GROUP: "grouped ECS (rows)",
-                                 om.EXPERT_WARP: "expert-major ECS (rows)"}[om.layer_executor(dims, L)],
-                       eta=expected_eta(dims, L)),
+        "config": _arm_config(w, args, 1),
         "stage_ms": stage_ms, "n_active": n_active, "tasks": M,
         "load": {"expert_usage": usage, "unevenness": uneven,
                  "note": "PAPER:405-410 (paper's full model: usage 100%, unevenness 0.24 with trained routers; "
@@ -596,9 +608,7 @@ def bench_multi(args, w, ws, rk, lr):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "latency_ms": ms,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded counter-based generator, DESIGN.md §3)",
-                "config": dict(_config_dict(w, f"ep{ws} (experts row-sharded, tokens data-parallel, "
-                                               f"{args.backend} all-to-all)"), global_tokens=L, tokens_per_gpu=L_loc,
-                               backend=args.backend, exchange=args.exchange),
+                "config": _arm_config(w, args, ws),
                 "phase_ms_rank0": phase_ms, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
                 "parity": parity, "gpu_launches": launches, "launches_per_step": launches / max(args.steps, 1),
                 "clocks": clk.summary()}
@@ -608,6 +618,31 @@ def bench_multi(args, w, ws, rk, lr):
         print(json.dumps(line), flush=True)
     dist.barrier()
     return 0
+
+
+def _workload(args):
+    """The workload of this run: config, V layout (auto: the executor the measurements favour,
+    DESIGN.md §4.4), ablation switches."""
+    from paper_2602_05711_b200 import configs, omnimoe as om
+    w = configs.get(args.config)
+    eta = expected_eta(w.dims, w.L)
+    # auto: the V layout whose executor the measurements favour (DESIGN.md §4.4) -- rows for
+    # the token-centric (eta < 2) and dense (K >= N/40) executors, SLICED for 2 <= eta <= 32
+    dense_rows = om.layer_executor(w.dims, w.L) == om.EXPERT_DENSE
+    sliced = args.expert_kernel == "auto" and (args.v_layout == "sliced" or
+                                               (args.v_layout == "auto" and 2.0 <= eta <= 32.0 and not dense_rows))
+    w = configs.get(args.config, v_layout=om.V_SLICED if sliced else om.V_ROWS,
+                    v_band_bytes=int(args.v_band_mb * (1 << 20)))
+    if args.expert_kernel != "auto":
+        ek = {"token": om.EXPERT_TOKEN, "warp": om.EXPERT_WARP}[args.expert_kernel]
+        w = configs.get(args.config, expert_kernel=ek, group_size=1 if ek == om.EXPERT_WARP else 0)
+    if args.router == "dense":
+        w = configs.get(w.name, **{k: getattr(w.dims, k) for k in ("v_layout", "expert_kernel", "group_size")},
+                        router=om.ROUTER_DENSE)
+    if args.no_shared_mlp:
+        w = configs.get(w.name, **{k: getattr(w.dims, k) for k in ("v_layout", "expert_kernel", "group_size",
+                                                                   "router")}, d_ff=0)
+    return w
 
 
 def main():
@@ -644,9 +679,11 @@ def main():
     args.warmup = max(args.warmup, 1)
     if args.config is None:
         args.config = "C5" if rank_info()[0] > 1 else "C3a"
-    if args.impl == "reference":
-        return run_reference(args)
     ws, rk, lr = rank_info()
+    if args.impl == "reference":  # the oracle arm: the same workload object, nothing on the GPU
+        from paper_2602_05711_b200 import build as _b
+        _b.build()
+        return run_reference(args, _workload(args))
     dev = lr % max(torch.cuda.device_count(), 1)  # (the gloo dry run may put several ranks on one GPU)
     torch.cuda.set_device(dev)
     if ws > 1:
@@ -659,25 +696,7 @@ def main():
         build.build()
     if ws > 1:
         dist.barrier()
-    from paper_2602_05711_b200 import omnimoe as om
-    w = configs.get(args.config)
-    eta = expected_eta(w.dims, w.L)
-    # auto: the V layout whose executor the measurements favour -- rows for
-    # the token-centric (eta < 2) and dense (K >= N/40) executors, SLICED for 2 <= eta <= 32
-    dense_rows = om.layer_executor(w.dims, w.L) == om.EXPERT_DENSE
-    sliced = args.expert_kernel == "auto" and (args.v_layout == "sliced" or
-                                               (args.v_layout == "auto" and 2.0 <= eta <= 32.0 and not dense_rows))
-    w = configs.get(args.config, v_layout=om.V_SLICED if sliced else om.V_ROWS,
-                    v_band_bytes=int(args.v_band_mb * (1 << 20)))
-    if args.expert_kernel != "auto":
-        ek = {"token": om.EXPERT_TOKEN, "warp": om.EXPERT_WARP}[args.expert_kernel]
-        w = configs.get(args.config, expert_kernel=ek, group_size=1 if ek == om.EXPERT_WARP else 0)
-    if args.router == "dense":
-        w = configs.get(w.name, **{k: getattr(w.dims, k) for k in ("v_layout", "expert_kernel", "group_size")},
-                        router=om.ROUTER_DENSE)
-    if args.no_shared_mlp:
-        w = configs.get(w.name, **{k: getattr(w.dims, k) for k in ("v_layout", "expert_kernel", "group_size",
-                                                                   "router")}, d_ff=0)
+    w = _workload(args)
     try:
         if ws > 1:
             return bench_multi(args, w, ws, rk, lr)
