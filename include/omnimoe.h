@@ -68,7 +68,7 @@ enum { OMNIMOE_EXPERT_AUTO = 0, OMNIMOE_EXPERT_WARP = 1, OMNIMOE_EXPERT_GROUP = 
 enum { OMNIMOE_V_ROWS = 0, OMNIMOE_V_SLICED = 1 };
 /* workspace query selector */
 enum { OMNIMOE_WS_ROUTE = 0, OMNIMOE_WS_SCHEDULE = 1, OMNIMOE_WS_EXPERT = 2, OMNIMOE_WS_LAYER = 3,
-       OMNIMOE_WS_ROUTER_BWD = 4, OMNIMOE_WS_MLP_BWD = 5, OMNIMOE_WS_MLP = 6 };
+       OMNIMOE_WS_ROUTER_BWD = 4, OMNIMOE_WS_MLP_BWD = 5, OMNIMOE_WS_MLP = 6, OMNIMOE_WS_EXPERT_BWD = 7 };
 
 /* How omnimoe_route computes the sub-key logits.  Both give the same bits:
  * logit = RN32(exact dot product x . w) (reading Q9).
@@ -270,10 +270,12 @@ omnimoe_status omnimoe_expert_fwd_pass(const omnimoe_dims* dims, int64_t L, cons
  *   dx_l = sum_t dz_t w_e               (written, or added when accumulate_dx)
  *   x, dy [L][d]; W_loc, V_loc [n_loc][d] (ROWS); W_sliced = omnimoe_pack_v(W_loc)
  *   (the dx pass reads W slice by slice like pass V reads V); plan: the expert-major
- *   plan (group size 1) with its V-order arrays and one band; dW_act, dV_act fp32
+ *   plan (group size 1) with its V-order arrays and ONE band (dims.v_band_bytes >=
+ *   128 n_loc; otherwise OMNIMOE_ERR_UNSUPPORTED); dW_act, dV_act fp32
  *   [n_loc][d]: row tau = the expert plan->active[tau] (tau < n_active; other rows
- *   untouched); dgate fp32 [M].  bf16, d % 64 == 0, d <= 2048; no atomics (the
- *   expert rows are owned by one warp pair, dx by one warp per slice). */
+ *   untouched); dgate fp32 [M].  bf16, d % 64 == 0, d <= 2048; no atomics (every
+ *   expert row and every dx slice is owned by one warp; summation orders are fixed).
+ *   ws: omnimoe_workspace_size(dims, L, OMNIMOE_WS_EXPERT_BWD) bytes. */
 omnimoe_status omnimoe_expert_bwd(const omnimoe_dims* dims, int64_t L, const void* x, const void* W_loc,
                                   const void* V_loc, const void* W_sliced, const omnimoe_plan* plan,
                                   const void* dy, float* dx, float* dW_act, float* dV_act, float* dgate,

@@ -376,6 +376,7 @@ omnimoe_status omnimoe_workspace_size(const omnimoe_dims* dims, int64_t L, int w
     case OMNIMOE_WS_ROUTER_BWD: *bytes = router_bwd_ws_bytes(d, L); break;
     case OMNIMOE_WS_MLP_BWD: *bytes = mlp_bwd_ws_bytes(d, L); break;
     case OMNIMOE_WS_MLP: *bytes = h_bytes(d, L); break;
+    case OMNIMOE_WS_EXPERT_BWD: *bytes = expert_bwd_ws_bytes(d, L); break;
     default:
       set_error("unknown workspace selector " + std::to_string(which));
       return OMNIMOE_ERR_INVALID_ARGUMENT;
@@ -705,7 +706,15 @@ omnimoe_status omnimoe_expert_bwd(const omnimoe_dims* dims, int64_t L, const voi
     set_error("expert_bwd: needs the expert-major plan (group_size 1 or the SLICED layout)");
     return OMNIMOE_ERR_INVALID_ARGUMENT;
   }
-  OMNI_TRY(check_ws(ws_bytes, expert_ws_bytes(d, L), "expert_bwd"));
+  {  // the backward writes dgate in task order through plan.sorted_task: one band (V order = task order)
+    const int64_t n_loc = plan->expert_end - plan->expert_begin;
+    const int64_t n_tok = plan->n_tokens > 0 ? plan->n_tokens : L;
+    if (resolve_v_bands(ds, n_loc, std::max<int64_t>(n_tok, 1)) != 1) {
+      set_error("expert_bwd: the plan must have one V band (dims.v_band_bytes >= 128 * n_loc)");
+      return OMNIMOE_ERR_UNSUPPORTED;
+    }
+  }
+  OMNI_TRY(check_ws(ws_bytes, expert_bwd_ws_bytes(d, L), "expert_bwd"));
   OMNI_TRY(check_device());
   return expert_bwd_run(ds, L, x, W_loc, V_loc, W_sliced, *plan, dy, dx, dW_act, dV_act, dgate, accumulate_dx, ws,
                         (cudaStream_t)stream);

@@ -1462,6 +1462,12 @@ __global__ void __launch_bounds__(256)
 
 size_t expert_ws_bytes(const omnimoe_dims&, int64_t) { return 256; }  // work counters
 
+// N2 workspace: counters + z, q, dz, g s per task (upper bound L h K tasks) + the dx pass's
+int64_t bwd_ws_tasks(const omnimoe_dims& d, int64_t L) { return std::max<int64_t>(L * d.n_heads * d.top_k, 1); }
+size_t expert_bwd_ws_bytes(const omnimoe_dims& d, int64_t L) {
+  return 256 + 16 * (size_t)bwd_ws_tasks(d, L) + expert_ws_bytes(d, L);
+}
+
 omnimoe_status expert_token_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* V,
                                 const int32_t* idx, const float* gate, int64_t begin, int64_t end, float* y,
                                 int accumulate, cudaStream_t st) {
@@ -1640,10 +1646,251 @@ omnimoe_status pack_v(int64_t n, int d, const void* V, void* Vs, cudaStream_t st
   return OMNIMOE_OK;
 }
 
+// ---------------------------------------------------------------------------
+// N2, d % 512 == 0: the routed-branch backward as row-gather passes, each holding at most
+// one weight row per warp in registers (the fused two-warps-per-expert kernel above waits
+// on a named barrier per task and runs at ~4 TB/s of L2 traffic):
+//   1. z_p = x_l . w_e and q_p = dy_l . v_e for every plan position p (expert-major, the
+//      pass-Z kernel shape: warp per active expert, weight row in registers, two gathered
+//      rows in flight);
+//   2. per p: s = sigma(z), dgate[t] = s q, dz = g q sigma'(z) (also into task_pair for the
+//      dx pass), the coefficients dz and g s of the weight gradients;
+//   3. dW_e = sum_p dz_p x_l and dV_e = sum_p g_p s_p dy_l: one warp per (active expert,
+//      512-column part), fp32 accumulators in registers, the expert's rows gathered in plan
+//      order (fixed summation order, no atomics);
+//   4. dx (the SLICED pass V over the sliced W with a = dz), as before.
+template <int NV8>
+__global__ void __launch_bounds__(256, 3)
+    expert_rowdot_kernel(int d, const __nv_bfloat16* __restrict__ rows, const __nv_bfloat16* __restrict__ Wt,
+                         const int32_t* __restrict__ offsets, const int32_t* __restrict__ active,
+                         const int32_t* __restrict__ n_active, const int32_t* __restrict__ stok,
+                         float* __restrict__ out, int* __restrict__ work) {
+  const int lane = threadIdx.x & 31;
+  const int na = *n_active;
+  const uint64_t pol = policy_evict_first(), rpol = policy_evict_normal();
+  int tau = 0;
+  if (lane == 0) tau = atomicAdd(work, 1);
+  tau = __shfl_sync(0xffffffffu, tau, 0);
+  while (tau < na) {
+    const int e = active[tau];
+    const int beg = offsets[e], end = offsets[e + 1];
+    U8 wv[NV8];
+#pragma unroll
+    for (int j = 0; j < NV8; ++j) wv[j] = ld256_hint(Wt + (size_t)e * d + (j * 32 + lane) * 16, pol);
+    int nxt = 0;
+    if (lane == 0) nxt = atomicAdd(work, 1);
+    for (int p0 = beg; p0 < end; p0 += 32) {
+      const int pl = p0 + lane;
+      const int l_l = pl < end ? stok[pl] : 0;
+      const int cnt = min(32, end - p0);
+      float mine = 0.f;
+      for (int t = 0; t < cnt; t += 2) {
+        U8 xr[2][NV8];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int lt = __shfl_sync(0xffffffffu, l_l, min(t + u, cnt - 1));
+#pragma unroll
+          for (int j = 0; j < NV8; ++j) xr[u][j] = ld256_hint(rows + (size_t)lt * d + (j * 32 + lane) * 16, rpol);
+        }
+        float z[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          z[u] = 0.f;
+#pragma unroll
+          for (int j = 0; j < NV8; ++j) {
+            float q = 0.f, q2 = 0.f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              q = dot2_bf16(q, wv[j].w[i], xr[u][j].w[i]);
+              q2 = dot2_bf16(q2, wv[j].w[4 + i], xr[u][j].w[4 + i]);
+            }
+            z[u] += q + q2;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) z[u] += __shfl_xor_sync(0xffffffffu, z[u], o);
+        if (lane == t) mine = z[0];
+        if (lane == t + 1) mine = z[1];
+      }
+      if (lane < cnt) out[pl] = mine;
+    }
+    tau = __shfl_sync(0xffffffffu, nxt, 0);
+  }
+}
+
+__global__ void bwd_scalars_kernel(const int32_t* __restrict__ m_loc_p, const float* __restrict__ zb,
+                                   const float* __restrict__ qb, const float* __restrict__ sgate,
+                                   const int32_t* __restrict__ stask, float* __restrict__ dgate,
+                                   int32_t* __restrict__ task_pair, float* __restrict__ cw, float* __restrict__ cv,
+                                   int act) {
+  const int64_t m = *m_loc_p;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+    const float z = zb[p], q = qb[p], g = sgate[p];
+    const float lg = 1.0f / (1.0f + __expf(-z));
+    const float sz = act == OMNIMOE_IDENTITY ? z : z * lg;
+    const float sp = act == OMNIMOE_IDENTITY ? 1.0f : lg * (1.0f + z * (1.0f - lg));
+    const float dz = g * q * sp;
+    const int t = stask[p];
+    dgate[t] = sz * q;
+    task_pair[2 * (size_t)t + 1] = __float_as_int(dz);
+    cw[p] = dz;
+    cv[p] = g * sz;
+  }
+}
+
+// out[tau][part] = sum over the expert's plan positions p of coef[p] * rows[tok[p]][part]:
+// one warp per (active expert, part of PW x 512 columns), T rows in flight.  Items hold
+// ~eta tasks, so the next item is claimed and its expert / segment looked up while the
+// current item's rows are in flight (the item-to-item dependency chain is the cost).
+template <int T, int PW, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    expert_accum_kernel(int d, const __nv_bfloat16* __restrict__ rows, const float* __restrict__ coef,
+                        const int32_t* __restrict__ offsets, const int32_t* __restrict__ active,
+                        const int32_t* __restrict__ n_active, const int32_t* __restrict__ stok,
+                        float* __restrict__ out, int* __restrict__ work) {
+  const int lane = threadIdx.x & 31;
+  const int parts = d / (512 * PW);  // 16 PW columns per lane and part
+  const int64_t n_items = (int64_t)(*n_active) * parts;
+  auto claim = [&]() {
+    int v = 0;
+    if (lane == 0) v = atomicAdd(work, 1);
+    return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+  };
+  auto meta = [&](int64_t item, int& beg, int& end) {
+    beg = end = 0;
+    if (item < n_items) {
+      const int e = active[item / parts];
+      beg = offsets[e];
+      end = offsets[e + 1];
+    }
+  };
+  int64_t it = claim();
+  int beg, end;
+  meta(it, beg, end);
+  while (it < n_items) {
+    const int tau = (int)(it / parts), part = (int)(it - (int64_t)tau * parts);
+    const int col = part * 512 * PW + lane * 16;
+    const int64_t nxt = claim();  // in flight while this item's rows are
+    unsigned long long acc[PW][8];
+#pragma unroll
+    for (int j = 0; j < PW; ++j)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[j][i] = 0ull;
+    int nbeg = 0, nend = 0;
+    bool fetched = false;
+    for (int p0 = beg; p0 < end; p0 += 32) {
+      const int pl = p0 + lane;
+      const int l_l = pl < end ? stok[pl] : 0;
+      const float c_l = pl < end ? coef[pl] : 0.f;
+      const int cnt = min(32, end - p0);
+      for (int t = 0; t < cnt; t += T) {
+        U8 r[T][PW];
+        float c[T];
+#pragma unroll
+        for (int u = 0; u < T; ++u) {
+          const int src = min(t + u, cnt - 1);
+          const int l = __shfl_sync(0xffffffffu, l_l, src);
+          c[u] = t + u < cnt ? __shfl_sync(0xffffffffu, c_l, src) : 0.f;
+#pragma unroll
+          for (int j = 0; j < PW; ++j) r[u][j] = ld256(rows + (size_t)l * d + col + j * 512);
+        }
+        if (!fetched) {  // the next item's segment, behind this item's first row loads
+          meta(nxt, nbeg, nend);
+          fetched = true;
+        }
+#pragma unroll
+        for (int u = 0; u < T; ++u) {
+          const unsigned long long c2 = ((unsigned long long)__float_as_uint(c[u]) << 32) | __float_as_uint(c[u]);
+#pragma unroll
+          for (int j = 0; j < PW; ++j)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) axpy2_bf16(acc[j][i], c2, r[u][j].w[i]);
+        }
+      }
+    }
+    if (!fetched) meta(nxt, nbeg, nend);
+#pragma unroll
+    for (int j = 0; j < PW; ++j) {
+      float4* dst = reinterpret_cast<float4*>(out + (size_t)tau * d + col + j * 512);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        dst[q] = make_float4(lo_f(acc[j][2 * q]), hi_f(acc[j][2 * q]), lo_f(acc[j][2 * q + 1]),
+                             hi_f(acc[j][2 * q + 1]));
+    }
+    it = nxt;
+    beg = nbeg;
+    end = nend;
+  }
+}
+
 omnimoe_status expert_bwd_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* V,
                               const void* Ws, const omnimoe_plan& plan, const void* dy, float* dx, float* dW_act,
                               float* dV_act, float* dgate, int accumulate_dx, void* ws, cudaStream_t st) {
   const int d = (int)dm.d;
+  // row-gather passes (above) when experts are shared (eta >= 2; C3a 19.2 -> 16.3 ms); at
+  // eta ~ 1 every expert has ~one task and the fused kernel's single gather of x and dy per
+  // task wins (C3b 1.6 vs 2.6 ms)
+  if (d % 512 == 0 && d <= 2048 && expected_eta(dm, L) >= 2.0) {
+    const int64_t n_loc = plan.expert_end - plan.expert_begin;
+    const int64_t M = bwd_ws_tasks(dm, L);
+    int* work = static_cast<int*>(ws);
+    float* zb = reinterpret_cast<float*>(static_cast<char*>(ws) + 256);
+    float* qb = zb + M;
+    float* cw = qb + M;
+    float* cv = cw + M;
+    if (cudaMemsetAsync(work, 0, 64 * sizeof(int), st) != cudaSuccess) {
+      set_error("expert_bwd: memset failed");
+      return OMNIMOE_ERR_CUDA;
+    }
+    auto X = static_cast<const __nv_bfloat16*>(x);
+    auto D = static_cast<const __nv_bfloat16*>(dy);
+    auto Wp = static_cast<const __nv_bfloat16*>(W);
+    auto Vp = static_cast<const __nv_bfloat16*>(V);
+    auto rowdot = [&](const __nv_bfloat16* rows, const __nv_bfloat16* Wt, float* out, int* w) {
+      auto go = [&](auto kern) {
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+        kern<<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(d, rows, Wt, plan.expert_offsets, plan.active,
+                                                               plan.n_active, plan.sorted_token, out, w);
+      };
+      switch (d / 512) {
+        case 1: go(expert_rowdot_kernel<1>); break;
+        case 2: go(expert_rowdot_kernel<2>); break;
+        case 3: go(expert_rowdot_kernel<3>); break;
+        default: go(expert_rowdot_kernel<4>); break;
+      }
+    };
+    rowdot(X, Wp, zb, work);
+    OMNI_CHECK_LAUNCH("expert_rowdot_kernel(z)");
+    rowdot(D, Vp, qb, work + 1);
+    OMNI_CHECK_LAUNCH("expert_rowdot_kernel(q)");
+    const int32_t* m_loc = plan.expert_offsets + n_loc;
+    bwd_scalars_kernel<<<num_sms() * 8, 256, 0, st>>>(m_loc, zb, qb, plan.sorted_gate, plan.sorted_task, dgate,
+                                                     plan.task_pair, cw, cv, dm.act);
+    OMNI_CHECK_LAUNCH("bwd_scalars_kernel");
+    auto accum = [&](const __nv_bfloat16* rows, const float* coef, float* out, int* w) {
+      auto go = [&](auto kern) {
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+        kern<<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(d, rows, coef, plan.expert_offsets, plan.active,
+                                                               plan.n_active, plan.sorted_token, out, w);
+      };
+      // C3a, both weight gradients: <4 rows, 1024 columns, 2 CTAs> 8.1 ms, <4, 512, 3> 8.8,
+      // <8, 512, 2> 10.6, <8, 512, 3> 12.1 (the fp32 dW / dV rows are 17 GB of writes)
+      if (d % 1024 == 0) go(expert_accum_kernel<4, 2, 2>);
+      else go(expert_accum_kernel<4, 1, 3>);
+    };
+    accum(X, cw, dW_act, work + 2);
+    OMNI_CHECK_LAUNCH("expert_accum_kernel(dW)");
+    accum(D, cv, dV_act, work + 3);
+    OMNI_CHECK_LAUNCH("expert_accum_kernel(dV)");
+    omnimoe_dims dv = dm;
+    dv.v_layout = OMNIMOE_V_SLICED;
+    return expert_sliced_run(dv, L, x, W, Ws, plan, dx, accumulate_dx, static_cast<char*>(ws) + 256 + 16 * M, st,
+                             2);
+  }
   // d >= 1024: four warps per expert (a quarter of the columns each: more warps resident),
   // else a pair
   const bool quad = d >= 1024;

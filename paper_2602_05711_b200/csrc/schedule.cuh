@@ -36,6 +36,8 @@ omnimoe_status dense_expert_run(const omnimoe_dims& d, int64_t L, const void* x,
 omnimoe_status pack_v(int64_t n, int d, const void* V, void* Vs, cudaStream_t st);
 
 size_t expert_ws_bytes(const omnimoe_dims& d, int64_t L);
+int64_t bwd_ws_tasks(const omnimoe_dims& d, int64_t L);
+size_t expert_bwd_ws_bytes(const omnimoe_dims& d, int64_t L);
 // SLICED executor; passes: bit 0 = pass Z, bit 1 = pass V
 omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* Vs,
                                  const omnimoe_plan& plan, float* y, int accumulate, void* ws, cudaStream_t st,

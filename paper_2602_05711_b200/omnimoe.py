@@ -24,7 +24,7 @@ V_ROWS, V_SLICED = 0, 1
 ORDER_KEY, ORDER_CANDIDATE = 0, 1
 ROUTER_EXACT, ROUTER_EXACT_F64, ROUTER_DENSE = 0, 1, 2
 LOGITS_ROUTE, LOGITS_EXACT_F64, LOGITS_BF16_FAST = 0, 1, 2
-WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER, WS_ROUTER_BWD, WS_MLP_BWD, WS_MLP = 0, 1, 2, 3, 4, 5, 6
+WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER, WS_ROUTER_BWD, WS_MLP_BWD, WS_MLP, WS_EXPERT_BWD = 0, 1, 2, 3, 4, 5, 6, 7
 
 
 class OmniMoEError(RuntimeError):
@@ -324,7 +324,7 @@ def expert_bwd(dims: LayerDims, x, W_loc, V_loc, W_sliced, plan, dy, dx=None, ac
     dW = torch.empty((n_loc, dims.d), dtype=torch.float32, device=dev)
     dV = torch.empty((n_loc, dims.d), dtype=torch.float32, device=dev)
     dg = torch.empty(max(M, 1), dtype=torch.float32, device=dev)
-    ws = ws if ws is not None else workspace(dims, L, WS_EXPERT, dev)
+    ws = ws if ws is not None else workspace(dims, L, WS_EXPERT_BWD, dev)
     dc, cp = dims.c(), _cplan(plan)
     _check(load().omnimoe_expert_bwd(ctypes.byref(dc), L, _ptr(x), _ptr(W_loc), _ptr(V_loc), _ptr(W_sliced),
                                      ctypes.byref(cp), _ptr(dy), _ptr(dx), _ptr(dW), _ptr(dV), _ptr(dg),
@@ -366,12 +366,18 @@ def shared_mlp_bwd(dims: LayerDims, x, w_gate_up, w_down, dy, dx=None, accumulat
     return dx, dgu, ddn
 
 
+def bwd_dims(dims: LayerDims) -> LayerDims:
+    """The dims the backward's plan is scheduled with (and omnimoe_expert_bwd called with):
+    group size 1 and one V band, so that the plan's V order is the task order."""
+    return _replace(dims, group_size=1, v_band_bytes=max(dims.v_band_bytes, 128 * dims.N + 1))
+
+
 def layer_bwd(dims: LayerDims, x, subkeys, W, V, W_sliced, w_gate_up, w_down, idx, gate, plan, dy):
     """N2: the layer's backward for the forward's routing decision (idx, gate [L][h][K],
-    the plan of those tasks with group size 1): routed branch (omnimoe_expert_bwd), router
+    the plan of those tasks scheduled with bwd_dims(dims)): routed branch (omnimoe_expert_bwd), router
     gates (omnimoe_router_bwd) and shared MLP (omnimoe_shared_mlp_bwd), dx summed over the
     three.  Returns dict(dx, dsubkeys, dW_act, dV_act, active, dgate, dw_gate_up, dw_down)."""
-    rd = dims if dims.group_size == 1 else _replace(dims, group_size=1)
+    rd = bwd_dims(dims)
     dx, dW, dV, dg = expert_bwd(rd, x, W, V, W_sliced, plan, dy)
     _, dsub = router_bwd(dims, x, subkeys, idx, gate, dg.reshape(gate.shape), dx=dx, accumulate_dx=True)
     out = dict(dx=dx, dsubkeys=dsub, dW_act=dW, dV_act=dV, active=plan["active"][:dW.shape[0]], dgate=dg)

@@ -646,10 +646,12 @@ def test_layer_low_eta_uses_token_executor():
 
 
 # ---------------------------------------------------------------- N2: routed-branch backward
-@pytest.mark.parametrize("d,act", [(64, om.SILU), (256, om.SILU), (1024, om.SILU), (2048, om.SILU), (128, om.IDENTITY)])
-def test_expert_bwd_matches_oracle(d, act):
+@pytest.mark.parametrize("N", [3000, 800])  # eta 1.45 (fused kernel) / 3.2 (row-gather passes when d % 512 == 0)
+@pytest.mark.parametrize("d,act", [(64, om.SILU), (256, om.SILU), (1024, om.SILU), (1536, om.SILU), (2048, om.SILU),
+                                   (128, om.IDENTITY), (512, om.IDENTITY)])
+def test_expert_bwd_matches_oracle(d, act, N):
     rng = np.random.default_rng(d + act)
-    L, N, HK = 200, 3000, 12
+    L, HK = 200, 12
     dims = om.LayerDims(d=d, n_rows=N, n_cols=1, top_k=HK, d_ff=0, act=act, group_size=1)
     inp = make_inputs(dims, L, 9, skip=("subkeys",))
     base = rng.integers(0, N - 64, L)
@@ -673,6 +675,18 @@ def test_expert_bwd_matches_oracle(d, act):
         assert e_tok <= 1e-2 and e_elt <= 1e-2, (e_tok, e_elt)
     np.testing.assert_allclose(dg.cpu().numpy(), ref["dgate"].reshape(-1),
                                atol=1e-2 * np.abs(ref["dgate"]).max(), rtol=1e-2)
+
+
+def test_expert_bwd_needs_one_band():
+    """dgate is written in task order through the plan's V order, which needs one band."""
+    dims = om.LayerDims(d=512, n_rows=3000, n_cols=1, top_k=4, d_ff=0, group_size=1, v_band_bytes=64 << 10)
+    assert om.v_bands(dims, dims.N, 8) > 1
+    inp = make_inputs(dims, 8, 2, skip=("subkeys",))
+    ids = torch.arange(32, dtype=torch.int32, device="cuda") * 90
+    plan = om.schedule(dims, ids, torch.ones(32, device="cuda"))
+    Ws = om.pack_v(om.LayerDims(d=512, n_rows=3000, n_cols=1, top_k=4, v_layout=om.V_SLICED), inp["W"])
+    with pytest.raises(om.OmniMoEError, match="UNSUPPORTED"):
+        om.expert_bwd(dims, inp["x"], inp["W"], inp["V"], Ws, plan, inp["x"])
 
 
 @pytest.mark.parametrize("d,nr,nc,K,h,L", [(64, 32, 32, 8, 1, 256), (256, 64, 64, 64, 2, 300), (1024, 256, 256, 512, 1, 64)])

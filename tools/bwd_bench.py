@@ -17,10 +17,10 @@ w = configs.get(name, v_layout=om.V_SLICED, route_order=om.ORDER_CANDIDATE)
 dims, L = w.dims, w.L
 inp = make_inputs(dims, L, w.seed)
 idx, gate, _ = om.route(dims, inp["x"], inp["subkeys"], want_score=False)
-plan = om.schedule(dims, idx.reshape(-1), gate.reshape(-1))
+rd = om.bwd_dims(dims)  # group size 1, one V band (the backward's plan)
+plan = om.schedule(rd, idx.reshape(-1), gate.reshape(-1))
 Ws = om.pack_v(dims, inp["W"])
 dy = torch.randn(L, dims.d, device="cuda").to(torch.bfloat16)
-rd = configs.get(name, group_size=1).dims
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 ms, parts = [], {"expert_bwd": [], "router_bwd": [], "mlp_bwd": []}
 for i in range(reps + 1):
