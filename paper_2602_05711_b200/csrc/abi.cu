@@ -32,7 +32,9 @@ struct DeviceInfo {
 };
 std::mutex g_dev_mu;
 std::map<int, DeviceInfo> g_dev;
-std::set<std::tuple<const void*, int, int>> g_smem_attr;  // (kernel, device, bytes) already applied
+// (kernel, device) -> the largest dynamic shared memory size applied so far: the attribute
+// only ever rises, so every smaller launch stays valid
+std::map<std::pair<const void*, int>, int> g_smem_attr;
 
 int current_device() {
   int dev = 0;
@@ -59,13 +61,11 @@ int num_sms() {
 
 bool set_smem_attr(const void* func, int bytes) {
   const int dev = current_device();
-  {
-    std::lock_guard<std::mutex> g(g_dev_mu);
-    if (g_smem_attr.count(std::make_tuple(func, dev, bytes))) return true;
-  }
-  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
   std::lock_guard<std::mutex> g(g_dev_mu);
-  g_smem_attr.insert(std::make_tuple(func, dev, bytes));
+  auto it = g_smem_attr.find(std::make_pair(func, dev));
+  if (it != g_smem_attr.end() && it->second >= bytes) return true;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  g_smem_attr[std::make_pair(func, dev)] = bytes;
   return true;
 }
 

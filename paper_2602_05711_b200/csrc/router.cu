@@ -1155,7 +1155,7 @@ omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* lo
       cand_table_kernel<<<1, 1024, 0, st>>>(K, kr, kc, cand_ws);
       OMNI_CHECK_LAUNCH("cand_table_kernel");
       auto kern = in_smem ? select_bucket_kernel<true> : select_bucket_kernel<false>;
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
+      if (!set_smem_attr((const void*)kern, (int)sm)) {
         set_error("route: cannot set select_bucket_kernel shared memory");
         return OMNIMOE_ERR_CUDA;
       }

@@ -19,7 +19,8 @@ addr2line, cur = {}, None
 for l in txt[start:end]:
     m = re.search(r'line (\d+)', l)
     if l.strip().startswith('//##') and m:
-        cur = int(m.group(1))
+        f = re.search(r'File "([^"]+)"', l)
+        cur = (f.group(1) if f else srcf, int(m.group(1)))
         continue
     m = re.match(r'\s*/\*([0-9a-f]+)\*/', l)
     if m and cur is not None:
@@ -34,11 +35,25 @@ for r in rows[2:]:
     except (ValueError, IndexError):
         continue
     base = a if base is None else base
-    ln = addr2line.get(a - base, -1)
+    ln = addr2line.get(a - base, ('', -1))
     samp[ln] += float(r[si] or 0)
     ins[ln] += float(r[ii] or 0)
 tot, toti = sum(samp.values()), sum(ins.values())
-src = open(srcf).read().split('\n')
+srcs = {}
+
+
+def line_of(f, ln):
+    if ln <= 0:
+        return ''
+    if f not in srcs:
+        try:
+            srcs[f] = open(f).read().split('\n')
+        except OSError:
+            srcs[f] = []
+    return srcs[f][ln - 1].strip()[:90] if ln <= len(srcs[f]) else ''
+
+
 print('samples', tot, 'warp instructions', toti)
-for ln, s_ in samp.most_common(top):
-    print(f"{ln:5d} {100 * s_ / tot:5.1f}% samp {100 * ins[ln] / toti:5.1f}% ins | {src[ln - 1].strip()[:100] if ln > 0 else ''}")
+for (f, ln), s_ in samp.most_common(top):
+    name = f.split('/')[-1] if f else '?'
+    print(f"{name[:14]:>14}:{ln:<5d} {100 * s_ / tot:5.1f}% samp {100 * ins[(f, ln)] / toti:5.1f}% ins | {line_of(f, ln)}")
