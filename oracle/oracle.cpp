@@ -12,10 +12,11 @@
 // named alongside); "Q#" = a reading listed in DESIGN.md "Readings".
 //
 // Pins: every function below is pinned by tests/test_oracle.py (-m "not gpu")
-// against closed forms, brute force, invariants and SPEC worked examples,
-// EXCEPT absolute layer outputs at paper scale, which the paper never prints:
-// "parity unpinned" for absolute values (P12) -- only the
-// composition of individually pinned steps vouches for them.
+// against closed forms, brute force, invariants and SPEC worked examples.
+// Absolute layer outputs at paper scale (the paper prints none, P12)
+// are pinned by closed forms at d = 2048, K = 512 (constant expert rows:
+// y = h silu(x.w) u for any routing; one-hot expert rows: the gate-weighted
+// scatter of the selected ids) -- test_layer_closed_forms_paper_width.
 // ============================================================================
 #include <algorithm>
 #include <cmath>

@@ -473,6 +473,42 @@ def test_layer_composition_equals_steps():
     np.testing.assert_array_equal(out2["y"], out["y"])
 
 
+# ---- P12: absolute layer values at the paper's width, from closed forms -------------
+def test_layer_closed_forms_paper_width():
+    """Eq.MoE at d = 2048, K = 512 (C3a's width and top-k) on a 64 x 64 grid, with expert
+    tables built so that the routed branch has a closed form whatever the routing: with every
+    w_e = w and v_e = u, Eq.Assemble gives y_routed = sum_heads sum_k g_k silu(x.w) u =
+    h silu(x.w) u (Eq.Gate: the gates of a head sum to 1); with v_e = (e mod d)-th unit vector
+    scaled by (e + 1), y_routed[j] = sum over the selected e with e mod d = j of
+    g_e silu(x.w_e) (e + 1).  The shared branch is switched off (w_down = 0) or
+    checked against numpy's matrix form."""
+    rng = np.random.default_rng(12)
+    L, d, Nr, Nc, K, h, dff = 3, 2048, 64, 64, 512, 2, 64
+    N = Nr * Nc
+    x = rng.standard_normal((L, d)).astype(np.float32).astype(np.float64)
+    sub = rng.standard_normal((h, Nr + Nc, d)).astype(np.float32).astype(np.float64) / 32
+    w = rng.standard_normal(d) / 64
+    u = rng.standard_normal(d)
+    silu = lambda z: z / (1 + np.exp(-z))
+    wgu = rng.standard_normal((2 * dff, d)) / 64
+    out = oracle.layer(x, sub, np.tile(w, (N, 1)), np.tile(u, (N, 1)), Nr, Nc, K, wgu, np.zeros((d, dff)))
+    np.testing.assert_allclose(out["y"], h * silu(x @ w)[:, None] * u[None, :], rtol=1e-10, atol=1e-12)
+    # one-hot expert rows: the assembled output is the gate-weighted scatter of the selected ids
+    W = rng.standard_normal((N, d)) / 64
+    V = np.zeros((N, d))
+    V[np.arange(N), np.arange(N) % d] = np.arange(N) + 1.0
+    wd = rng.standard_normal((d, dff)) / 8
+    out = oracle.layer(x, sub, W, V, Nr, Nc, K, wgu, wd)
+    ref = np.zeros((L, d))
+    for l in range(L):
+        for head in range(h):
+            for e, g in zip(out["idx"][l, head], out["gate"][l, head]):
+                ref[l, e % d] += g * silu(x[l] @ W[e]) * (e + 1)
+    hmid = silu(x @ wgu[:dff].T) * (x @ wgu[dff:].T)
+    np.testing.assert_allclose(out["y"], ref + hmid @ wd.T, rtol=1e-9, atol=1e-9)
+    assert np.allclose(out["gate"].sum(-1), 1.0) and len(set(out["idx"][0, 0])) == K
+
+
 # ---- P11 generator sanity: |E_active| under near-uniform routing ---------------------
 def test_active_expert_count_uniform_model():
     d, Nr, Nc, K, L = 64, 32, 32, 8, 256
