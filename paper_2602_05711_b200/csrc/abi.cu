@@ -183,15 +183,18 @@ bool dense_router(const omnimoe_dims& d) { return d.router == OMNIMOE_ROUTER_DEN
 int64_t logit_cols(const omnimoe_dims& d) { return dense_router(d) ? d.n_rows * d.n_cols : d.n_rows + d.n_cols; }
 
 size_t route_ws(const omnimoe_dims& d, int64_t L, void* ws, float** logits, void** sub_ws,
-                uint32_t** cand = nullptr, bool with_cand = true) {
+                uint32_t** cand = nullptr, bool with_cand = true, void** fused_ws = nullptr) {
   Carver c(ws);
   const int64_t T = L * d.n_heads;
   float* lg = c.take<float>((size_t)std::max<int64_t>(T, 1) * logit_cols(d));
   void* sw = c.take<char>(dense_router(d) ? 0 : exact_logits_ws_bytes(d, L));
   uint32_t* ct = c.take<uint32_t>(dense_router(d) || !with_cand ? 0 : select_cand_ws_bytes(d) / 4);
+  // N4 (small K): the epilogue's per-half lists; zero bytes where the fused path does not apply
+  void* fw = c.take<char>(dense_router(d) ? 0 : fused_route_bytes(d, L));
   if (logits) *logits = lg;
   if (sub_ws) *sub_ws = sw;
   if (cand) *cand = ct;
+  if (fused_ws) *fused_ws = fw;
   return c.bytes();
 }
 
@@ -293,8 +296,9 @@ omnimoe_status route_impl(const omnimoe_dims& d, int64_t L, const void* x, const
                           uint32_t* cand_ws = nullptr) {
   float* logits;
   void* sub_ws;
+  void* fused_ws = nullptr;
   uint32_t* cand = cand_ws;
-  route_ws(d, L, ws, &logits, &sub_ws, cand_ws ? nullptr : &cand, cand_ws == nullptr);
+  route_ws(d, L, ws, &logits, &sub_ws, cand_ws ? nullptr : &cand, cand_ws == nullptr, &fused_ws);
   if (dense_router(d)) {
     OMNI_TRY(logits_impl(d, L, x, subkeys, logits, sub_ws, st));
     return launch_dense_select(d, L * d.n_heads, logits, idx, gate, score, st);
@@ -303,6 +307,11 @@ omnimoe_status route_impl(const omnimoe_dims& d, int64_t L, const void* x, const
   size_t smem;
   OMNI_TRY(select_params(d, L * d.n_heads, &sp, &smem));
   sp.sorted = sorted;
+  if (i8_logits(d) && fused_kp(d) > 0) {  // N4: per-half top-k' in the GEMM epilogue
+    FusedRoute fr;
+    OMNI_TRY(exact_logits_fused(d, L, x, subkeys, logits, sub_ws, fused_ws, score != nullptr, &fr, st));
+    return launch_select(sp, smem, logits, idx, gate, score, cand, st, &fr);
+  }
   OMNI_TRY(logits_impl(d, L, x, subkeys, logits, sub_ws, st));
   return launch_select(sp, smem, logits, idx, gate, score, cand, st);
 }

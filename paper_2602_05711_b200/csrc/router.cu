@@ -724,9 +724,36 @@ __device__ uint64_t warp_half_topk_any(const float* __restrict__ lg, int n, int 
   return mine;
 }
 
+// N4 fused path: lane t (< k1) returns the t-th largest key of the half's two epilogue
+// lists (the top kp of each 48-column half of the GEMM's tiles, gemm_i8_topk_kernel); the
+// half's logsumexp from their (max, sum exp) pairs
+__device__ uint64_t warp_half_topk_fused(const uint64_t* __restrict__ c2, int kp, int k1,
+                                         const float2* __restrict__ pp, float* lse) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t a = lane < 2 * kp ? c2[lane] : 0ull;
+  const uint64_t b = lane + 32 < 2 * kp ? c2[lane + 32] : 0ull;
+  uint64_t prev = ~0ull, mine = 0ull;
+  for (int t = 0; t < k1; ++t) {
+    uint64_t best = a < prev ? a : 0ull;
+    if (b < prev && b > best) best = b;
+    best = warp_max_u64(best);
+    if (lane == t) mine = best;
+    prev = best;
+  }
+  if (pp) {
+    const float2 p0 = pp[0], p1 = pp[1];
+    const float M = fmaxf(p0.x, p1.x);
+    const float sum = (p0.x == -INFINITY ? 0.f : p0.y * __expf(p0.x - M)) + (p1.x == -INFINITY ? 0.f : p1.y * __expf(p1.x - M));
+    *lse = M + __logf(sum);
+  }
+  return mine;
+}
+
 __global__ void __launch_bounds__(256)
     select_warp_kernel(SelectParams p, const float* __restrict__ logits, int32_t* __restrict__ idx,
-                       float* __restrict__ gate, float* __restrict__ score) {
+                       float* __restrict__ gate, float* __restrict__ score, const uint64_t* __restrict__ fcand,
+                       const float2* __restrict__ fpart, int kp, int n_heads, const int32_t* __restrict__ fcounts,
+                       const int32_t* __restrict__ fbad) {
   __shared__ uint32_t cand[1024];
   __shared__ int hist_all[8][256];      // per-warp bucket histograms (long halves)
   __shared__ uint64_t sorted_all[8][32];  // per-warp top-k1 keys of a half
@@ -747,11 +774,26 @@ __global__ void __launch_bounds__(256)
   const uint32_t Nc = (uint32_t)p.n_cols;
   for (int th = gw; th < p.T; th += nw) {
     const float* lg = logits + (size_t)th * R;
-    float lse_r, lse_c;
+    float lse_r = 0.f, lse_c = 0.f;
     int* hist = hist_all[(threadIdx.x >> 5) & 7];
     uint64_t* srt = sorted_all[(threadIdx.x >> 5) & 7];
-    const uint64_t kr = warp_half_topk_any(lg, p.n_rows, p.kr1, &lse_r, hist, srt);
-    const uint64_t kc = warp_half_topk_any(lg + p.n_rows, p.n_cols, p.kc1, &lse_c, hist, srt);
+    // the fused lists, unless a flag sent this token's logits (or every token's) through the
+    // fp64 kernel
+    bool fused = fcand != nullptr && fcounts[1] == 0;
+    if (fused) {
+      const int l = th / n_heads, nbad = fcounts[0];
+      for (int j = 0; j < nbad; ++j) fused = fused && fbad[j] != l;
+    }
+    uint64_t kr, kc;
+    if (fused) {
+      const size_t base = (size_t)th * 2;  // (token, head) -> halves 2 * head, 2 * head + 1
+      kr = warp_half_topk_fused(fcand + base * 2 * kp, kp, p.kr1, fpart ? fpart + base * 2 : nullptr, &lse_r);
+      kc = warp_half_topk_fused(fcand + (base + 1) * 2 * kp, kp, p.kc1, fpart ? fpart + (base + 1) * 2 : nullptr,
+                                &lse_c);
+    } else {
+      kr = warp_half_topk_any(lg, p.n_rows, p.kr1, &lse_r, hist, srt);
+      kc = warp_half_topk_any(lg + p.n_rows, p.n_cols, p.kc1, &lse_c, hist, srt);
+    }
     // candidate keys, at most ceil(C / 32) per lane (C <= 32 * (ln 32 + 1) < 160)
     U128 ck[5];
     const int per = (C + 31) / 32;
@@ -1052,6 +1094,7 @@ omnimoe_status select_params(const omnimoe_dims& d, int64_t T, SelectParams* p, 
   p->n_rows = (int)d.n_rows;
   p->n_cols = (int)d.n_cols;
   p->top_k = (int)d.top_k;
+  p->n_heads = (int)d.n_heads;
   const int64_t K1 = d.top_k + 1;
   p->kr1 = (int)std::min<int64_t>(K1, d.n_rows);
   p->kc1 = (int)std::min<int64_t>(K1, d.n_cols);
@@ -1124,10 +1167,14 @@ size_t select_cand_ws_bytes(const omnimoe_dims& d) {
 }
 
 omnimoe_status launch_select(const SelectParams& p, size_t smem, const float* logits, int32_t* idx,
-                             float* gate, float* score, uint32_t* cand_ws, cudaStream_t st) {
+                             float* gate, float* score, uint32_t* cand_ws, cudaStream_t st, const FusedRoute* fused) {
   if (p.top_k + 1 <= 32 && p.C <= 160) {  // small K: warp per token-head, repeated arg-max
     const int grid = std::max(1, std::min((p.T + 7) / 8, num_sms() * 8));
-    select_warp_kernel<<<grid, 256, 0, st>>>(p, logits, idx, gate, score);
+    const bool fz = fused && fused->kp > 0;
+    select_warp_kernel<<<grid, 256, 0, st>>>(p, logits, idx, gate, score, fz ? fused->cand : nullptr,
+                                             fz ? fused->part : nullptr, fz ? fused->kp : 0,
+                                             std::max(1, p.n_heads), fz ? fused->counts : nullptr,
+                                             fz ? fused->bad_x : nullptr);
     OMNI_CHECK_LAUNCH("select_warp_kernel");
     return OMNIMOE_OK;
   }

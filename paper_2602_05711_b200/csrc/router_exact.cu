@@ -442,6 +442,217 @@ __global__ void __launch_bounds__(128 + 32 * kIEpiWarps, 1)
 }
 
 // ---------------------------------------------------------------------------
+// N4 (the selection never materialises the full
+// score matrix): the persistent exact-logit GEMM with the per-half top-k' taken in its
+// epilogue.  Work units are (128-token block, half of a head): a CTA walks the unit's
+// column tiles in order, so each epilogue thread (one token row, one 48-column half of every
+// tile) sees its half's columns one after another and keeps their top kp half keys
+// (value desc, index asc -- the selection's key) in a sorted register list, plus the running
+// (max, sum exp) of the logsumexp; at the unit's end it writes kp keys (+ one float2)
+// instead of the half's logits.  Tiles past the half's end are computed and masked (the B
+// rows beyond it belong to the next half or are TMA zero fill).
+// + the epilogue scratch: 256 threads x 48 floats after the barriers (which take < 256 bytes)
+constexpr int kISmemTopk = kIStages * kIStageBytes + 1024 + 256 + 256 * (IBN / 2) * 4;
+static_assert(kISmemTopk <= 227 * 1024, "fused i8 GEMM shared memory");
+struct I8TopArgs {
+  int kp, R, n_rows, n_cols, n_heads;
+  uint64_t* cand;         // [M][2h][2][kp]
+  float2* part;           // [M][2h][2] or null
+  const int32_t* counts;  // counts[1] > 0: flagged sub-key rows -> the logits are written too
+};
+__device__ __forceinline__ uint64_t fused_half_key(float v, uint32_t i) {
+  v = v + 0.0f;  // -0.0 -> +0.0: equal values compare equal (the selection's half_key)
+  return ((uint64_t)ord32(v) << 32) | (uint64_t)(0xFFFFFFFFu - i);
+}
+template <int KP>
+__global__ void __launch_bounds__(128 + 32 * kIEpiWarps, 1)
+    gemm_i8_topk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        I8Args args, I8TopArgs ta) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kIStages * 3 * kIABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kIStages * kIStageBytes);
+  uint64_t* empty = full + kIStages;
+  uint64_t* tfull = empty + kIStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_kb = (args.K + IBK - 1) / IBK;
+  const int G = 2 * ta.n_heads;  // halves per token
+  const int n_units = ((args.M + IBM - 1) / IBM) * G;
+  auto unit = [&](int u, int& m0, int& c0, int& len) {
+    const int g = u % G;
+    m0 = (u / G) * IBM;
+    c0 = (g >> 1) * ta.R + ((g & 1) ? ta.n_rows : 0);
+    len = (g & 1) ? ta.n_cols : ta.n_rows;
+  };
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int s = 0; s < kIStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, kIEpiWarps);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kITmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    int g = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int m0, c0, len;
+      unit(u, m0, c0, len);
+      for (int n0 = c0; n0 < c0 + len; n0 += IBN)
+        for (int kb = 0; kb < num_kb; ++kb, ++g) {
+          const int s = g % kIStages;
+          mbar_wait(&empty[s], ((g / kIStages) & 1) ^ 1);
+          mbar_expect_tx(&full[s], kIStageBytes);
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            tma_load_2d(&tmA, &full[s], sA + (s * 3 + p) * kIABytes, kb * IBK, p * args.M + m0);
+            tma_load_2d(&tmB, &full[s], sB + (s * 3 + p) * kIBBytes, kb * IBK, p * args.N + n0);
+          }
+        }
+    }
+  } else if (warp == 1 && lane == 0) {
+    int g = 0, it = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int m0, c0, len;
+      unit(u, m0, c0, len);
+      for (int n0 = c0; n0 < c0 + len; n0 += IBN, ++it) {
+        mbar_wait(tempty, (it & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int kb = 0; kb < num_kb; ++kb, ++g) {
+          const int s = g % kIStages;
+          mbar_wait(&full[s], (g / kIStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+          for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              const uint32_t a0 = smem_u32(sA + (s * 3 + p) * kIABytes);
+              const uint32_t b0 = smem_u32(sB + (s * 3 + q) * kIBBytes);
+              const bool first_pair = (p == 0 || q == 2);
+#pragma unroll
+              for (int k = 0; k < IBK / 32; ++k)
+                umma_i8(tmem + (uint32_t)((p + q) * IBN), sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32),
+                        kIdescI8, !(kb == 0 && k == 0 && first_pair));
+            }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(tfull);
+      }
+    }
+  } else if (warp >= 4) {
+    // the tile's values go through a per-thread shared-memory scratch (48 floats, thread-
+    // contiguous words): the accumulators are released right after the TMEM reads, and the
+    // list updates run while the MMAs of the next tile proceed
+    const int e = warp - 4, qd = e & 3, h = e >> 2;
+    constexpr int kChunks = IBN / 16, kCols = IBN / 2;
+    const int c_lo = h * kChunks / 2, c_hi = (h + 1) * kChunks / 2;
+    const int et = threadIdx.x - 128;
+    float* scr = reinterpret_cast<float*>(smem + kIStages * kIStageBytes + 256) + et;
+    const bool wlog = ta.counts[1] > 0;
+    int it = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int m0, c0, len;
+      unit(u, m0, c0, len);
+      const int row = m0 + qd * 32 + lane;
+      const bool row_ok = row < args.M;
+      const int exr = row_ok ? args.ex[row] : 0;
+      uint64_t lst[KP];
+#pragma unroll
+      for (int i = 0; i < KP; ++i) lst[i] = 0ull;
+      float mx = -INFINITY, se = 0.f;
+      for (int n0 = c0; n0 < c0 + len; n0 += IBN, ++it) {
+        mbar_wait(tfull, it & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16);
+#pragma unroll 1
+        for (int c = c_lo; c < c_hi; ++c) {
+          uint32_t D[5][16];
+#pragma unroll
+          for (int s = 0; s < 5; ++s) tmem_ld16(tbase + s * IBN + c * 16, D[s]);
+          tmem_wait_ld();
+          if (c == c_hi - 1) {
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty)) : "memory");
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int64_t S = (int64_t)(int32_t)D[0][j] + ((int64_t)(int32_t)D[1][j] << 8) +
+                              ((int64_t)(int32_t)D[2][j] << 16) + ((int64_t)(int32_t)D[3][j] << 24) +
+                              ((int64_t)(int32_t)D[4][j] << 32);
+            const int col = min(n0 + c * 16 + j, args.N - 1);
+            scr[((c - c_lo) * 16 + j) * 256] = ldexpf(__ll2float_rn(S), exr + args.ew[col]);
+          }
+        }
+        const int col0 = n0 + c_lo * 16;
+        const int nv = row_ok ? max(0, min(kCols, c0 + len - col0)) : 0;  // this thread's columns in the half
+        if (wlog && nv > 0) {
+          float* dst = args.out + (size_t)row * args.N + col0;
+          for (int j = 0; j < nv; ++j) dst[j] = scr[j * 256];
+        }
+        if (ta.part && nv > 0) {
+          float cm = mx;
+          for (int j = 0; j < nv; ++j) cm = fmaxf(cm, scr[j * 256]);
+          float add = 0.f;
+          for (int j = 0; j < nv; ++j) add += __expf(scr[j * 256] - cm);
+          se = (mx == -INFINITY ? 0.f : se * __expf(mx - cm)) + add;
+          mx = cm;
+        }
+        // the columns above the list's current threshold, then one insertion round per
+        // pending column: the warp runs max over its lanes of the insertions, not one
+        // round per column in which any lane inserts
+        uint64_t pend = 0;
+        for (int j = 0; j < nv; ++j)
+          if (fused_half_key(scr[j * 256], (uint32_t)(col0 + j - c0)) > lst[KP - 1]) pend |= 1ull << j;
+        while (__any_sync(0xffffffffu, pend != 0)) {
+          if (pend) {
+            const int j = __ffsll((long long)pend) - 1;
+            pend &= pend - 1;
+            const uint64_t key = fused_half_key(scr[j * 256], (uint32_t)(col0 + j - c0));
+            if (key > lst[KP - 1]) {
+#pragma unroll
+              for (int i = KP - 1; i > 0; --i) lst[i] = key > lst[i - 1] ? lst[i - 1] : (key > lst[i] ? key : lst[i]);
+              lst[0] = key > lst[0] ? key : lst[0];
+            }
+          }
+        }
+      }
+      if (row_ok) {
+        const int g = u % G;
+        uint64_t* dst = ta.cand + (((size_t)row * G + g) * 2 + h) * ta.kp;
+#pragma unroll
+        for (int i = 0; i < KP; ++i)
+          if (i < ta.kp) dst[i] = lst[i];
+        if (ta.part) ta.part[((size_t)row * G + g) * 2 + h] = make_float2(mx, se);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kITmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // exact fp64 double-double dot + correct RN32
 template <typename T>
 __device__ __forceinline__ double to_d(T v);
@@ -582,8 +793,34 @@ omnimoe_status launch_exact_dd(int dtype, const void* x, const void* sub, int d,
   return OMNIMOE_OK;
 }
 
+int fused_kp(const omnimoe_dims& d) {
+  // small K only: the per-half lists (K+1 keys) are what the warp selection kernel takes
+  // (launch_select: K+1 <= 32 and <= 160 product candidates); at large K a 48-column
+  // segment would keep all its keys
+  if (d.dtype != OMNIMOE_BF16 || d.router != OMNIMOE_ROUTER_EXACT || d.d >= 65536) return 0;
+  const int64_t K1 = d.top_k + 1;
+  if (K1 > 32 || tuning().i8_cluster > 1 || !tuning().i8_persist || !tuning().route_fused) return 0;
+  const int64_t kr1 = std::min<int64_t>(K1, d.n_rows), kc1 = std::min<int64_t>(K1, d.n_cols);
+  int64_t C = 0;
+  for (int64_t a = 1; a <= kr1; ++a) C += std::min<int64_t>(kc1, K1 / a);
+  return C <= 160 ? (int)K1 : 0;
+}
+size_t fused_route_bytes(const omnimoe_dims& d, int64_t L) {
+  const int kp = fused_kp(d);
+  if (!kp) return 0;
+  Carver c(nullptr);
+  c.take<uint64_t>((size_t)std::max<int64_t>(L, 1) * 2 * d.n_heads * 2 * kp);
+  c.take<float2>((size_t)std::max<int64_t>(L, 1) * 2 * d.n_heads * 2);
+  return c.bytes();
+}
+
 omnimoe_status exact_logits(const omnimoe_dims& d, int64_t L, const void* x, const void* sub, float* logits,
                             void* ws, cudaStream_t st) {
+  return exact_logits_fused(d, L, x, sub, logits, ws, nullptr, false, nullptr, st);
+}
+
+omnimoe_status exact_logits_fused(const omnimoe_dims& d, int64_t L, const void* x, const void* sub, float* logits,
+                                  void* ws, void* fused_ws, bool want_part, FusedRoute* fr, cudaStream_t st) {
   const int NC = (int)(d.n_heads * (d.n_rows + d.n_cols));
   if (d.dtype != OMNIMOE_BF16)
     return launch_exact_dd(d.dtype, x, sub, (int)d.d, NC, (int)L, logits, 0, nullptr, nullptr, st);
@@ -620,6 +857,44 @@ omnimoe_status exact_logits(const omnimoe_dims& d, int64_t L, const void* x, con
   }
   I8Args a{(int)L, NC, (int)d.d, w.ex, w.ew, logits};
   dim3 grid(n_tiles, (unsigned)((L + IBM - 1) / IBM));
+  const int kp = fused_ws ? fused_kp(d) : 0;
+  if (kp && CN == 1) {
+    Carver c(fused_ws);
+    I8TopArgs ta;
+    ta.kp = kp;
+    ta.R = (int)(d.n_rows + d.n_cols);
+    ta.n_rows = (int)d.n_rows;
+    ta.n_cols = (int)d.n_cols;
+    ta.n_heads = (int)d.n_heads;
+    ta.cand = c.take<uint64_t>((size_t)std::max<int64_t>(L, 1) * 2 * d.n_heads * 2 * kp);
+    float2* part = c.take<float2>((size_t)std::max<int64_t>(L, 1) * 2 * d.n_heads * 2);
+    ta.part = want_part ? part : nullptr;
+    ta.counts = w.counts;
+    const int64_t units = ((L + IBM - 1) / IBM) * 2 * d.n_heads;
+    const int g = (int)std::min<int64_t>(units, num_sms());
+    // list length = kp for the common K = 16 (kp = 17), else the next multiple of 8
+    auto k = kp <= 8 ? gemm_i8_topk_kernel<8> : kp <= 16 ? gemm_i8_topk_kernel<16> : kp == 17 ? gemm_i8_topk_kernel<17>
+             : kp <= 24 ? gemm_i8_topk_kernel<24> : gemm_i8_topk_kernel<32>;
+    if (!set_smem_attr(reinterpret_cast<const void*>(k), kISmemTopk)) {
+      set_error("route: cannot set dynamic shared memory size of the fused i8 GEMM");
+      return OMNIMOE_ERR_CUDA;
+    }
+    k<<<g, 128 + 32 * kIEpiWarps, kISmemTopk, st>>>(mA, mB, a, ta);
+    OMNI_CHECK_LAUNCH("gemm_i8_topk_kernel");
+    if (fr) {
+      fr->cand = ta.cand;
+      fr->part = ta.part;
+      fr->kp = kp;
+      fr->counts = w.counts;
+      fr->bad_x = w.bad_x;
+    }
+    // flagged rows: the fp64 kernel rewrites those tokens' logits (all columns), flagged
+    // sub-key rows those columns (the epilogue then wrote every logit too); the selection
+    // reads the logits wherever a flag applies
+    OMNI_TRY(launch_exact_dd(d.dtype, x, sub, (int)d.d, NC, (int)L, logits, 1, w.bad_x, w.counts, st));
+    return launch_exact_dd(d.dtype, x, sub, (int)d.d, NC, (int)L, logits, 2, w.bad_w, w.counts + 1, st);
+  }
+  if (fr) fr->kp = 0;
   if (CN == 1 && tuning().i8_persist) {
     const int64_t tiles = (int64_t)grid.x * grid.y;
     gemm_i8_persist_kernel<<<(int)std::min<int64_t>(tiles, num_sms()), 128 + 32 * kIEpiWarps, kISmemBytes, st>>>(mA, mB,

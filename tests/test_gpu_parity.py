@@ -114,6 +114,28 @@ def test_logits_fallback_rows_bitwise():
     np.testing.assert_array_equal(idx.cpu().numpy().reshape(L, 4), r["idx"])
 
 
+@pytest.mark.parametrize("h", [1, 2])
+def test_route_fused_token_flags(h):
+    """N4 (small K: per-half top-k' in the exact-logit GEMM epilogue): tokens whose rows take
+    the fp64 path are routed from their recomputed logits, every other token from the
+    epilogue's lists -- ids, gates and scores equal the oracle either way."""
+    d = om.LayerDims(d=64, n_rows=16, n_cols=24, top_k=4, n_heads=h)
+    L = 300
+    inp = make_inputs(d, L, 11, skip=("W", "V"))
+    x = inp["x"].clone()
+    x[3, 5] = 2.0 ** 12   # token 3 spans 2^12 .. 2^-15: fp64 path
+    x[17, 0] = 2.0 ** -40
+    x[299, 2] = 2.0 ** 13
+    idx, gate, score = om.route(d, x, inp["subkeys"])
+    torch.cuda.synchronize()
+    dec = lambda t: t.float().cpu().numpy().astype(np.float64)
+    lg = oracle.logits(dec(x), dec(inp["subkeys"])).reshape(L * h, -1)
+    r = oracle.route(lg, 16, 24, 4, method=oracle.BRUTE)
+    np.testing.assert_array_equal(idx.cpu().numpy().reshape(L * h, 4), r["idx"])
+    np.testing.assert_allclose(gate.cpu().numpy().reshape(L * h, 4), r["gate"], atol=1e-5, rtol=0)
+    np.testing.assert_allclose(score.cpu().numpy().reshape(L * h, 4), r["score"], atol=1e-4, rtol=0)
+
+
 def test_bf16_fast_logits_are_not_exact():
     """Why Q9 needs the exact path: fp32-accumulated tcgen05 logits differ from the
     exact ones."""
@@ -143,7 +165,7 @@ def test_route_c2_multihead(router):
     np.testing.assert_array_equal(orc["idx"][:64], bf["idx"])
 
 
-@pytest.mark.parametrize("name,L", [("C3a", 96), ("C3b", 256), ("C4", 24), ("C4pp", 64), ("C5", 32)])
+@pytest.mark.parametrize("name,L", [("C3a", 96), ("C3b", 256), ("C4", 24), ("C4pp", 64), ("C5", 32), ("C5s", 64)])
 def test_route_large_configs_sampled(name, L):
     """Full-size router shapes (large K, candidates in the thousands) on a token sample."""
     w = _dims(name)
