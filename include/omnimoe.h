@@ -74,6 +74,10 @@ enum { OMNIMOE_WS_ROUTE = 0, OMNIMOE_WS_SCHEDULE = 1, OMNIMOE_WS_EXPERT = 2, OMN
  * logit = RN32(exact dot product x . w) (reading Q9).
  *   EXACT      tcgen05 kind::i8 products of 3 int8 digits per operand (fast);
  *              rows whose exponents span > 22 bits fall back to EXACT_F64.
+ *              For K + 1 <= 32 (bf16) the per-half top K+1 is taken inside the
+ *              GEMM's epilogue and the logits are not written (N4, PAPER:226-229:
+ *              the selection never materialises the score matrix);
+ *              the routing result is the same.
  *   EXACT_F64  fp64 double-double dot products on CUDA cores (slow reference). */
 enum { OMNIMOE_ROUTER_EXACT = 0, OMNIMOE_ROUTER_EXACT_F64 = 1, OMNIMOE_ROUTER_DENSE = 2 };
 /* OMNIMOE_ROUTER_DENSE is the paper's ablation "w/o Cartesian Product Router"
