@@ -259,8 +259,9 @@ omnimoe_status omnimoe_expert_fwd(const omnimoe_dims* dims, int64_t L, const voi
                                   omnimoe_stream_t stream);
 
 /* One pass of the SLICED executor, for measurement (pass 1: Z, writes
- * plan->task_pair a-values; pass 2: V, reads them and writes y_routed); pass 3 =
- * omnimoe_expert_fwd.  Arguments as omnimoe_expert_fwd. */
+ * plan->task_pair a-values; pass 2: V, reads them and writes y_routed), run as
+ * omnimoe_layer_fwd runs them (pass V takes the a-values in bf16, reading Q21);
+ * pass 3 = omnimoe_expert_fwd.  Arguments as omnimoe_expert_fwd. */
 omnimoe_status omnimoe_expert_fwd_pass(const omnimoe_dims* dims, int64_t L, const void* x,
                                        const void* W_loc, const void* V_loc, const omnimoe_plan* plan,
                                        float* y_routed, int accumulate, int pass, void* ws,
@@ -372,7 +373,10 @@ int32_t omnimoe_layer_executor(const omnimoe_dims* dims, int64_t L);
  *   idx_out, gate_out  nullable copies of the routing decision [L][h][K]; the same
  *              set and gates as omnimoe_route, but (for K + 1 > 32) in the order of the
  *              Cartesian candidates (row rank, then column rank) instead of by key --
- *              the layer never needs the sort */
+ *              the layer never needs the sort
+ * Precision: the routed activations a_t = g_t sigma(z_t) enter the SLICED executor's
+ * slice accumulation in bf16 (fp32 accumulation; reading Q21 -- the output is bf16);
+ * omnimoe_expert_fwd keeps them in fp32. */
 omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void* x,
                                  const void* subkeys, const void* W, const void* V,
                                  const void* w_gate_up, const void* w_down, void* y,

@@ -506,8 +506,9 @@ omnimoe_status expert_fwd_impl(const omnimoe_dims* dims, int64_t L, const void* 
       set_error("expert_fwd_pass: pass 1 (Z) or 2 (V) of the SLICED executor only");
       return OMNIMOE_ERR_INVALID_ARGUMENT;
     }
+    // the measurement entry point times the passes as omnimoe_layer_fwd runs them
     return expert_sliced_run(*dims, L, x, W_loc, V_loc, *plan, y_routed, accumulate, ws, (cudaStream_t)stream,
-                             passes);
+                             passes, /*act_bf16=*/1);
   }
   return expert_run(*dims, L, x, W_loc, V_loc, *plan, y_routed, accumulate, ws, (cudaStream_t)stream);
 }
@@ -624,7 +625,7 @@ omnimoe_status omnimoe_layer_fwd(const omnimoe_dims* dims, int64_t L, const void
   } else {
     OMNI_TRY(schedule_run(M, idx, gate, nullptr, d.n_heads * d.top_k, w.plan, resolve_group_size(d),
                           resolve_token_blocks(d, L), resolve_v_bands(d, d.n_rows * d.n_cols, L), w.sched_ws, st));
-    OMNI_TRY(expert_run(d, L, x, W, V, w.plan, w.y_routed, 0, w.expert_ws, st));
+    OMNI_TRY(expert_run(d, L, x, W, V, w.plan, w.y_routed, 0, w.expert_ws, st, /*act_bf16=*/1));
   }
   if (d.d_ff > 0) {
     OMNI_TRY(mlp_impl(d, L, x, w_gate_up, w_down, w.y_routed, y, w.H, st));
@@ -895,7 +896,7 @@ omnimoe_status omnimoe_layer_fwd_host(const omnimoe_dims* dims, int64_t L, const
   } else {
     OMNI_TRY(schedule_run(M, w.idx, w.gate, nullptr, hk, w.plan, resolve_group_size(d), resolve_token_blocks(d, L),
                           resolve_v_bands(d, d.n_rows * d.n_cols, L), w.sched_ws, st));
-    OMNI_TRY(expert_run(d, L, x_dev, W, V, w.plan, w.y_routed, 0, w.expert_ws, st));
+    OMNI_TRY(expert_run(d, L, x_dev, W, V, w.plan, w.y_routed, 0, w.expert_ws, st, /*act_bf16=*/1));
   }
   // 3. shared MLP GEMM-2 (+ combine) chunk by chunk (GEMM-1 ran per chunk above), each chunk
   //    of y copied back on the copy stream while the next is computed

@@ -227,6 +227,15 @@ __device__ __forceinline__ void axpy2_bf16(unsigned long long& acc, unsigned lon
   const unsigned long long v2 = ((unsigned long long)(vp & 0xFFFF0000u) << 32) | (unsigned long long)(vp << 16);
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a2), "l"(v2));
 }
+// lo += a * bf16(vp.lo), hi += a * bf16(vp.hi): fma.rn.f32.bf16 on the halves of vp (FHFMA)
+__device__ __forceinline__ void fma_bf16_pair(float& lo, float& hi, unsigned short a, uint32_t vp) {
+  asm("{ .reg .b16 vl, vh;\n\t"
+      "mov.b32 {vl, vh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, %3, vl, %0;\n\t"
+      "fma.rn.f32.bf16 %1, %3, vh, %1; }"
+      : "+f"(lo), "+f"(hi)
+      : "r"(vp), "h"(a));
+}
 __device__ __forceinline__ float lo_f(unsigned long long p) { return __uint_as_float((uint32_t)p); }
 __device__ __forceinline__ float hi_f(unsigned long long p) { return __uint_as_float((uint32_t)(p >> 32)); }
 
@@ -930,7 +939,13 @@ __device__ __forceinline__ U8 ld256(const void* p) {
 // processed.  Items (slice, token) are claimed in order from one counter so that the
 // warps in flight stay within ~one slice (a static round-robin lets warps drift over
 // many slices: C3a pass V 3.45 -> 13.6 ms in round 1).
-template <int MINB, int W>
+// BF16A: the task's coefficient a_t is rounded to bf16 and multiplied with the bf16 slice
+// elements by fma.rn.f32.bf16 (FHFMA, one instruction per element, fp32 accumulation),
+// instead of unpacking the pieces to fp32 for FFMA2 (three instructions per two elements;
+// the unpack was 30 % of the kernel's instructions).  Reading Q21: the
+// forward's activations a_t = g_t SiLU(z_t) enter the scatter-accumulate in bf16, as the
+// paper's bf16 kernels hold them; the backward's dz keeps fp32 (BF16A = false).
+template <int MINB, int W, bool BF16A>
 __global__ void __launch_bounds__(256, MINB)
     expert_vslice_kernel(int d, int64_t L, int64_t n_loc, const int32_t* __restrict__ seg, int seg_stride,
                          int band, int64_t n_tok, const int32_t* __restrict__ task_pair,
@@ -990,8 +1005,11 @@ __global__ void __launch_bounds__(256, MINB)
     }
     const __nv_bfloat16* vs = Vs + (size_t)s * n_loc * 64 + c4 * 16;
     unsigned long long acc[8];
+    float fa[16];
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = 0ull;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) fa[i] = 0.f;
     for (int p0 = beg; p0 < end; p0 += WT) {
       int2 cp[NP];
 #pragma unroll
@@ -1016,17 +1034,23 @@ __global__ void __launch_bounds__(256, MINB)
       }
 #pragma unroll
       for (int r = 0; r < W; ++r) {
-        const unsigned long long a2 = ((unsigned long long)__float_as_uint(a[r]) << 32) | __float_as_uint(a[r]);
+        if (BF16A) {
+          const unsigned short ab = __bfloat16_as_ushort(__float2bfloat16_rn(a[r]));
 #pragma unroll
-        for (int i = 0; i < 8; ++i) axpy2_bf16(acc[i], a2, v[r].w[i]);
+          for (int i = 0; i < 8; ++i) fma_bf16_pair(fa[2 * i], fa[2 * i + 1], ab, v[r].w[i]);
+        } else {
+          const unsigned long long a2 = ((unsigned long long)__float_as_uint(a[r]) << 32) | __float_as_uint(a[r]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) axpy2_bf16(acc[i], a2, v[r].w[i]);
+        }
       }
     }
     if (beg == end) fetch(nbeg, nend, np_);
     float f[16];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      f[2 * i] = lo_f(acc[i]);
-      f[2 * i + 1] = hi_f(acc[i]);
+      f[2 * i] = BF16A ? fa[2 * i] : lo_f(acc[i]);
+      f[2 * i + 1] = BF16A ? fa[2 * i + 1] : hi_f(acc[i]);
     }
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1)
@@ -1557,7 +1581,7 @@ int64_t resolve_token_blocks(const omnimoe_dims& d, int64_t L) {
 
 omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* Vs,
                                  const omnimoe_plan& plan, float* y, int accumulate, void* ws, cudaStream_t st,
-                                 int passes) {
+                                 int passes, int act_bf16) {
   const int64_t n_loc = plan.expert_end - plan.expert_begin;
   int* work = static_cast<int*>(ws);
   if (cudaMemsetAsync(work, 0, 64 * sizeof(int), st) != cudaSuccess) {
@@ -1611,7 +1635,7 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
   if (!(passes & 2)) return OMNIMOE_OK;
   // 80 registers (3 CTAs per SM), 4 rounds of 8 tasks per window (C3a pass V: <3,4> 2.82 ms,
   // <4,4> 2.92, <3,6> 2.96, <2,8> 3.12; profiles/r2/slices128/)
-  auto vkern = expert_vslice_kernel<3, 4>;
+  auto vkern = act_bf16 ? expert_vslice_kernel<3, 4, true> : expert_vslice_kernel<3, 4, false>;
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vkern, 256, 0);
   const int64_t n_tok = plan.n_tokens > 0 ? plan.n_tokens : L;
@@ -1889,7 +1913,7 @@ omnimoe_status expert_bwd_run(const omnimoe_dims& dm, int64_t L, const void* x, 
     omnimoe_dims dv = dm;
     dv.v_layout = OMNIMOE_V_SLICED;
     return expert_sliced_run(dv, L, x, W, Ws, plan, dx, accumulate_dx, static_cast<char*>(ws) + 256 + 16 * M, st,
-                             2);
+                             2, /*act_bf16=*/0);
   }
   // d >= 1024: four warps per expert (a quarter of the columns each: more warps resident),
   // else a pair
@@ -1917,13 +1941,14 @@ omnimoe_status expert_bwd_run(const omnimoe_dims& dm, int64_t L, const void* x, 
   // dx_l = sum_t dz_t w_e: the token-stationary slice pass over the sliced W
   omnimoe_dims dv = dm;
   dv.v_layout = OMNIMOE_V_SLICED;
-  return expert_sliced_run(dv, L, x, W, Ws, plan, dx, accumulate_dx, ws, st, 2);
+  return expert_sliced_run(dv, L, x, W, Ws, plan, dx, accumulate_dx, ws, st, 2, /*act_bf16=*/0);
 }
 
 omnimoe_status expert_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W,
                           const void* V, const omnimoe_plan& plan, float* y, int accumulate,
-                          void* ws, cudaStream_t st) {
-  if (dm.v_layout == OMNIMOE_V_SLICED) return expert_sliced_run(dm, L, x, W, V, plan, y, accumulate, ws, st, 3);
+                          void* ws, cudaStream_t st, int act_bf16) {
+  if (dm.v_layout == OMNIMOE_V_SLICED)
+    return expert_sliced_run(dm, L, x, W, V, plan, y, accumulate, ws, st, 3, act_bf16);
   if (!accumulate) {
     if (cudaMemsetAsync(y, 0, (size_t)L * dm.d * sizeof(float), st) != cudaSuccess) {
       set_error("expert_fwd: memset failed");

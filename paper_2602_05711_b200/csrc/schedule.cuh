@@ -41,13 +41,15 @@ size_t expert_bwd_ws_bytes(const omnimoe_dims& d, int64_t L);
 // SLICED executor; passes: bit 0 = pass Z, bit 1 = pass V
 omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* Vs,
                                  const omnimoe_plan& plan, float* y, int accumulate, void* ws, cudaStream_t st,
-                                 int passes);
+                                 int passes, int act_bf16 = 0);
 // N2: routed-branch backward (expert-major plan)
 omnimoe_status expert_bwd_run(const omnimoe_dims& dm, int64_t L, const void* x, const void* W, const void* V,
                               const void* Ws, const omnimoe_plan& plan, const void* dy, float* dx, float* dW_act,
                               float* dV_act, float* dgate, int accumulate_dx, void* ws, cudaStream_t st);
+// act_bf16 (SLICED pass V): the activations a_t enter the slice accumulation in bf16 (the
+// layer, whose output is bf16; reading Q21) or fp32 (omnimoe_expert_fwd's fp32 y_routed)
 omnimoe_status expert_run(const omnimoe_dims& d, int64_t L, const void* x, const void* W,
                           const void* V, const omnimoe_plan& plan, float* y, int accumulate,
-                          void* ws, cudaStream_t st);
+                          void* ws, cudaStream_t st, int act_bf16 = 0);
 
 }  // namespace omni
