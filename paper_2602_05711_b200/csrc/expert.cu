@@ -1633,9 +1633,21 @@ omnimoe_status expert_sliced_run(const omnimoe_dims& dm, int64_t L, const void* 
   }
   OMNI_TRY(s);
   if (!(passes & 2)) return OMNIMOE_OK;
-  // 80 registers (3 CTAs per SM), 4 rounds of 8 tasks per window (C3a pass V: <3,4> 2.82 ms,
-  // <4,4> 2.92, <3,6> 2.96, <2,8> 3.12; profiles/r2/slices128/)
-  auto vkern = act_bf16 ? expert_vslice_kernel<3, 4, true> : expert_vslice_kernel<3, 4, false>;
+  // 3 CTAs per SM; rounds of 8 tasks per window: 5 for the FHFMA (bf16 a) variant (C3a layer
+  // 7.32 -> 7.18 ms, C5 42.0 -> 41.4 vs 4 rounds; profiles/r2/vconfig/), 4 for the FFMA2
+  // variant (C3a pass V: <3,4> 2.82 ms, <4,4> 2.92, <3,6> 2.96, <2,8> 3.12; profiles/r2/slices128/)
+  auto vkern = act_bf16 ? expert_vslice_kernel<3, 5, true> : expert_vslice_kernel<3, 4, false>;
+#ifdef OMNIMOE_MEASURE
+  switch (tuning().v_config) {  // (CTAs per SM, rounds of 8 tasks per window) sweep
+    case 1: vkern = act_bf16 ? expert_vslice_kernel<4, 4, true> : expert_vslice_kernel<4, 4, false>; break;
+    case 2: vkern = act_bf16 ? expert_vslice_kernel<3, 6, true> : expert_vslice_kernel<3, 6, false>; break;
+    case 3: vkern = act_bf16 ? expert_vslice_kernel<2, 8, true> : expert_vslice_kernel<2, 8, false>; break;
+    case 4: vkern = act_bf16 ? expert_vslice_kernel<4, 3, true> : expert_vslice_kernel<4, 3, false>; break;
+    case 5: vkern = act_bf16 ? expert_vslice_kernel<3, 4, true> : expert_vslice_kernel<3, 5, false>; break;
+    case 6: vkern = act_bf16 ? expert_vslice_kernel<4, 5, true> : expert_vslice_kernel<4, 5, false>; break;
+    default: break;
+  }
+#endif
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vkern, 256, 0);
   const int64_t n_tok = plan.n_tokens > 0 ? plan.n_tokens : L;

@@ -25,6 +25,7 @@ struct Tuning {
   int i8_cluster = 1;           // exact router GEMM: CTAs per cluster multicasting the token limbs
   int i8_persist = 1;           // exact router GEMM: persistent kernel
   int route_fused = 1;          // N4: per-half top-k' in the exact-logit GEMM epilogue (small K)
+  int v_config = 0;             // pass V (CTAs per SM, window) variant, measurement build only
   int64_t ws_pad_counters = 0;  // bytes (<= 16 MB) padded before the layer's work counters
 };
 
@@ -52,6 +53,7 @@ inline const Tuning& tuning() {
     x.i8_cluster = (int)get("OMNIMOE_I8_CLUSTER", 1, 4, x.i8_cluster);
     x.i8_persist = (int)get("OMNIMOE_I8_PERSIST", 0, 1, x.i8_persist);
     x.route_fused = (int)get("OMNIMOE_ROUTE_FUSED", 0, 1, x.route_fused);
+    x.v_config = (int)get("OMNIMOE_V_CONFIG", 0, 6, x.v_config);
     x.ws_pad_counters = get("OMNIMOE_WS_PAD_COUNTERS", 0, 16ll << 20, x.ws_pad_counters);
 #endif
     return x;
