@@ -983,6 +983,7 @@ __global__ void __launch_bounds__(256, MINB)
   // memory by cp.async when the item starts and read when it ends: no dependent round
   // trip at the end of the item and no registers held across it
   __shared__ __align__(16) float ysm[8][4][16];
+  __shared__ __align__(16) float rsm[8][8 * 68];
   float* my_y = ysm[threadIdx.x >> 5][c4];
   int64_t it = claim();
   int beg, end;
@@ -1046,29 +1047,37 @@ __global__ void __launch_bounds__(256, MINB)
       }
     }
     if (beg == end) fetch(nbeg, nend, np_);
-    float f[16];
+    // the 8 task groups' partial sums of the slice's 64 columns go through shared memory
+    // (rows padded to 68 floats): lane j then adds columns 2j, 2j+1 over the 8 rows and
+    // writes them with one coalesced 256-byte store per warp -- instead of 48 shuffles
+    // + 48 adds per lane and 4 writing lanes
+    float* red = rsm[threadIdx.x >> 5];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      f[2 * i] = BF16A ? fa[2 * i] : lo_f(acc[i]);
-      f[2 * i + 1] = BF16A ? fa[2 * i + 1] : hi_f(acc[i]);
-    }
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1)
-#pragma unroll
-      for (int i = 0; i < 16; ++i) f[i] += __shfl_xor_sync(0xffffffffu, f[i], o);
-    if (g8 == 0) {
-      float4* dst = reinterpret_cast<float4*>(yq);
-      if (accumulate) asm volatile("cp.async.wait_all;" ::: "memory");
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float4 u = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
-        if (accumulate) {
-          const float4 p = reinterpret_cast<const float4*>(my_y)[q];
-          u.x += p.x; u.y += p.y; u.z += p.z; u.w += p.w;
-        }
-        dst[q] = u;
+    for (int q = 0; q < 4; ++q) {
+      float4 u;
+      if (BF16A) {
+        u = make_float4(fa[4 * q], fa[4 * q + 1], fa[4 * q + 2], fa[4 * q + 3]);
+      } else {
+        u = make_float4(lo_f(acc[2 * q]), hi_f(acc[2 * q]), lo_f(acc[2 * q + 1]), hi_f(acc[2 * q + 1]));
       }
+      *reinterpret_cast<float4*>(red + g8 * 68 + c4 * 16 + 4 * q) = u;
     }
+    if (accumulate && g8 == 0) asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    float2 sum = *reinterpret_cast<const float2*>(red + 2 * lane);
+#pragma unroll
+    for (int g = 1; g < 8; ++g) {
+      const float2 t = *reinterpret_cast<const float2*>(red + g * 68 + 2 * lane);
+      sum.x += t.x;
+      sum.y += t.y;
+    }
+    if (accumulate) {
+      const float2 p = reinterpret_cast<const float2*>(ysm[threadIdx.x >> 5])[lane];
+      sum.x += p.x;
+      sum.y += p.y;
+    }
+    *reinterpret_cast<float2*>(y + (size_t)l * d + s * 64 + 2 * lane) = sum;
+    __syncwarp();  // red and the prefetched output slice are reused by the next item
     it = nxt;
     beg = nbeg;
     end = nend;
