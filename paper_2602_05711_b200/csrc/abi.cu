@@ -307,7 +307,7 @@ omnimoe_status route_impl(const omnimoe_dims& d, int64_t L, const void* x, const
   size_t smem;
   OMNI_TRY(select_params(d, L * d.n_heads, &sp, &smem));
   sp.sorted = sorted;
-  if (i8_logits(d) && fused_kp(d) > 0) {  // N4: per-half top-k' in the GEMM epilogue
+  if (i8_logits(d) && fused_kp(d, L) > 0) {  // N4: per-half top-k' in the GEMM epilogue
     FusedRoute fr;
     OMNI_TRY(exact_logits_fused(d, L, x, subkeys, logits, sub_ws, fused_ws, score != nullptr, &fr, st));
     return launch_select(sp, smem, logits, idx, gate, score, cand, st, &fr);

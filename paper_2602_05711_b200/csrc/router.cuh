@@ -49,7 +49,7 @@ struct FusedRoute {
   const int32_t* counts = nullptr;  // [2]: flagged token rows, flagged sub-key rows (device)
   const int32_t* bad_x = nullptr;   // flagged token rows (device list)
 };
-int fused_kp(const omnimoe_dims& d);  // 0: no fused path for these dims
+int fused_kp(const omnimoe_dims& d, int64_t L);  // 0: no fused path for these dims and L
 size_t fused_route_bytes(const omnimoe_dims& d, int64_t L);
 omnimoe_status exact_logits_fused(const omnimoe_dims& d, int64_t L, const void* x, const void* sub, float* logits,
                                   void* ws, void* fused_ws, bool want_part, FusedRoute* fr, cudaStream_t st);

@@ -114,26 +114,48 @@ def test_logits_fallback_rows_bitwise():
     np.testing.assert_array_equal(idx.cpu().numpy().reshape(L, 4), r["idx"])
 
 
-@pytest.mark.parametrize("h", [1, 2])
-def test_route_fused_token_flags(h):
-    """N4 (small K: per-half top-k' in the exact-logit GEMM epilogue): tokens whose rows take
-    the fp64 path are routed from their recomputed logits, every other token from the
-    epilogue's lists -- ids, gates and scores equal the oracle either way."""
-    d = om.LayerDims(d=64, n_rows=16, n_cols=24, top_k=4, n_heads=h)
-    L = 300
+@pytest.mark.parametrize("h,flag_sub", [(1, False), (2, False), (2, True)])
+def test_route_fused_flags(h, flag_sub):
+    """N4 (small K: per-half top-k' in the exact-logit GEMM epilogue; K >= 8 and enough
+    (token block, half) units): tokens whose rows take the fp64 path are routed from their
+    recomputed logits, every other token from the epilogue's lists; a flagged sub-key row
+    sends every token through the logits -- ids, gates and scores equal the oracle."""
+    d = om.LayerDims(d=64, n_rows=16, n_cols=24, top_k=8, n_heads=h)
+    L = 6400
     inp = make_inputs(d, L, 11, skip=("W", "V"))
-    x = inp["x"].clone()
+    x, sub = inp["x"].clone(), inp["subkeys"].clone()
     x[3, 5] = 2.0 ** 12   # token 3 spans 2^12 .. 2^-15: fp64 path
     x[17, 0] = 2.0 ** -40
-    x[299, 2] = 2.0 ** 13
-    idx, gate, score = om.route(d, x, inp["subkeys"])
+    x[L - 1, 2] = 2.0 ** 13
+    if flag_sub:
+        sub[h - 1, 9, 1] = 2.0 ** 9
+    idx, gate, score = om.route(d, x, sub)
     torch.cuda.synchronize()
     dec = lambda t: t.float().cpu().numpy().astype(np.float64)
-    lg = oracle.logits(dec(x), dec(inp["subkeys"])).reshape(L * h, -1)
-    r = oracle.route(lg, 16, 24, 4, method=oracle.BRUTE)
-    np.testing.assert_array_equal(idx.cpu().numpy().reshape(L * h, 4), r["idx"])
-    np.testing.assert_allclose(gate.cpu().numpy().reshape(L * h, 4), r["gate"], atol=1e-5, rtol=0)
-    np.testing.assert_allclose(score.cpu().numpy().reshape(L * h, 4), r["score"], atol=1e-4, rtol=0)
+    lg = oracle.logits(dec(x), dec(sub)).reshape(L * h, -1)
+    r = oracle.route(lg, 16, 24, 8, method=oracle.PRODUCT)
+    np.testing.assert_array_equal(idx.cpu().numpy().reshape(L * h, 8), r["idx"])
+    np.testing.assert_allclose(gate.cpu().numpy().reshape(L * h, 8), r["gate"], atol=1e-5, rtol=0)
+    np.testing.assert_allclose(score.cpu().numpy().reshape(L * h, 8), r["score"], atol=1e-4, rtol=0)
+    bf = oracle.route(lg[:300], 16, 24, 8, method=oracle.BRUTE)
+    np.testing.assert_array_equal(r["idx"][:300], bf["idx"])
+
+
+@pytest.mark.parametrize("name,L,n_check", [("C3b", 8192, 192), ("C5s", 6656, 96), ("C2", 8192, 256)])
+def test_route_fused_full_configs(name, L, n_check):
+    """N4 at the small-K workloads' shapes with the fused path on (enough tokens): the ids,
+    gates and scores of tokens spread over the batch equal the oracle's."""
+    w = _dims(name)
+    inp = make_inputs(w.dims, L, w.seed, skip=("W", "V", "w_gate_up", "w_down"))
+    idx, gate, score = om.route(w.dims, inp["x"], inp["subkeys"])
+    torch.cuda.synchronize()
+    toks = np.linspace(0, L - 1, n_check).astype(np.int64)
+    orc, rows = _oracle_route(w.dims, w.seed, toks, method=oracle.PRODUCT)
+    h, K = w.dims.n_heads, w.dims.top_k
+    th = (toks[:, None] * h + np.arange(h)[None, :]).reshape(-1)
+    np.testing.assert_array_equal(idx.cpu().numpy().reshape(-1, K)[th], orc["idx"])
+    np.testing.assert_allclose(gate.cpu().numpy().reshape(-1, K)[th], orc["gate"], atol=1e-5, rtol=0)
+    np.testing.assert_allclose(score.cpu().numpy().reshape(-1, K)[th], orc["score"], atol=1e-4, rtol=0)
 
 
 def test_bf16_fast_logits_are_not_exact():
