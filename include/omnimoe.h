@@ -128,8 +128,15 @@ typedef struct {
   int32_t v_layout;      /* OMNIMOE_V_ROWS | OMNIMOE_V_SLICED */
   int32_t route_order;   /* omnimoe_route output order: OMNIMOE_ORDER_KEY | OMNIMOE_ORDER_CANDIDATE */
   int64_t v_band_bytes;  /* >= 0 */
-  int64_t reserved;      /* must be 0 */
+  int64_t flags;         /* OMNIMOE_FLAG_* (other bits must be 0) */
 } omnimoe_dims;
+/* flags
+ *   OMNIMOE_FLAG_ACT_BF16  omnimoe_expert_fwd (SLICED layout): the routed activations
+ *              a_t = g_t sigma(z_t) enter pass V's slice accumulation in bf16 (fp32
+ *              accumulation), as omnimoe_layer_fwd always runs it (reading Q21) -- for
+ *              callers that round the routed output to bf16 anyway (the expert-parallel
+ *              layer's bf16 partials); without it a_t stays fp32. */
+enum { OMNIMOE_FLAG_ACT_BF16 = 1 };
 
 /* Expert-centric plan for the local expert range [expert_begin, expert_end)
  * (Eq.Tasks + active compression + Eq.Sort).  n_loc =

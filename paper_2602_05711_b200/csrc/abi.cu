@@ -123,8 +123,8 @@ omnimoe_status validate_dims(const omnimoe_dims* dp) {
     set_error("group_size and token_blocks must be >= 0");
     return OMNIMOE_ERR_INVALID_ARGUMENT;
   }
-  if (d.v_band_bytes < 0 || d.reserved != 0) {
-    set_error("v_band_bytes must be >= 0 and reserved 0 " + dims_str(d));
+  if (d.v_band_bytes < 0 || (d.flags & ~(int64_t)OMNIMOE_FLAG_ACT_BF16) != 0) {
+    set_error("v_band_bytes must be >= 0 and flags a set of OMNIMOE_FLAG_* " + dims_str(d));
     return OMNIMOE_ERR_INVALID_ARGUMENT;
   }
   if (d.route_order != OMNIMOE_ORDER_KEY && d.route_order != OMNIMOE_ORDER_CANDIDATE) {
@@ -510,7 +510,8 @@ omnimoe_status expert_fwd_impl(const omnimoe_dims* dims, int64_t L, const void* 
     return expert_sliced_run(*dims, L, x, W_loc, V_loc, *plan, y_routed, accumulate, ws, (cudaStream_t)stream,
                              passes, /*act_bf16=*/1);
   }
-  return expert_run(*dims, L, x, W_loc, V_loc, *plan, y_routed, accumulate, ws, (cudaStream_t)stream);
+  return expert_run(*dims, L, x, W_loc, V_loc, *plan, y_routed, accumulate, ws, (cudaStream_t)stream,
+                    (dims->flags & OMNIMOE_FLAG_ACT_BF16) ? 1 : 0);
 }
 }  // namespace
 }  // namespace omni

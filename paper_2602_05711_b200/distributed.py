@@ -71,7 +71,10 @@ class LibOps:
             return torch.zeros((rows, self.dims.d), dtype=torch.bfloat16, device=x_recv.device)
         y = (torch.empty if sliced else torch.zeros)((rows, self.dims.d), dtype=torch.float32, device=x_recv.device)
         plan = om.schedule(self.dims, ids, gate, token=tok, expert_begin=0, expert_end=n_loc, n_tokens=rows)
-        y = om.expert_fwd(self.dims, x_recv, W_loc, V_loc, plan, y_routed=y, accumulate=not sliced)
+        # the partials go back in bf16, so pass V may take the activations in bf16 as
+        # omnimoe_layer_fwd does (reading Q21)
+        ed = dataclasses.replace(self.dims, flags=self.dims.flags | om.FLAG_ACT_BF16)
+        y = om.expert_fwd(ed, x_recv, W_loc, V_loc, plan, y_routed=y, accumulate=not sliced)
         return om.ep_partials(self.dims, y)
 
     def combine(self, y_ret, inv, tok_off, L):

@@ -22,6 +22,7 @@ SILU, IDENTITY = 0, 1
 EXPERT_AUTO, EXPERT_WARP, EXPERT_GROUP, EXPERT_TOKEN, EXPERT_SLICED, EXPERT_DENSE = 0, 1, 2, 3, 4, 5
 V_ROWS, V_SLICED = 0, 1
 ORDER_KEY, ORDER_CANDIDATE = 0, 1
+FLAG_ACT_BF16 = 1
 ROUTER_EXACT, ROUTER_EXACT_F64, ROUTER_DENSE = 0, 1, 2
 LOGITS_ROUTE, LOGITS_EXACT_F64, LOGITS_BF16_FAST = 0, 1, 2
 WS_ROUTE, WS_SCHEDULE, WS_EXPERT, WS_LAYER, WS_ROUTER_BWD, WS_MLP_BWD, WS_MLP, WS_EXPERT_BWD = 0, 1, 2, 3, 4, 5, 6, 7
@@ -37,7 +38,7 @@ class Dims(ctypes.Structure):
                 ("dtype", ctypes.c_int32), ("act", ctypes.c_int32), ("router", ctypes.c_int32),
                 ("expert_kernel", ctypes.c_int32), ("group_size", ctypes.c_int64),
                 ("token_blocks", ctypes.c_int64), ("v_layout", ctypes.c_int32), ("route_order", ctypes.c_int32),
-                ("v_band_bytes", ctypes.c_int64), ("reserved", ctypes.c_int64)]
+                ("v_band_bytes", ctypes.c_int64), ("flags", ctypes.c_int64)]
 
 
 class Plan(ctypes.Structure):
@@ -157,6 +158,7 @@ class LayerDims:
     v_layout: int = V_ROWS
     route_order: int = ORDER_KEY
     v_band_bytes: int = 0
+    flags: int = 0  # FLAG_ACT_BF16: omnimoe_expert_fwd takes the activations in bf16 (reading Q21)
 
     @property
     def N(self) -> int:
@@ -175,7 +177,7 @@ class LayerDims:
     def c(self) -> Dims:
         return Dims(self.d, self.n_rows, self.n_cols, self.top_k, self.n_heads, self.d_ff,
                     self.dtype, self.act, self.router, self.expert_kernel, self.group_size,
-                    self.token_blocks, self.v_layout, self.route_order, self.v_band_bytes, 0)
+                    self.token_blocks, self.v_layout, self.route_order, self.v_band_bytes, self.flags)
 
 
 def _ptr(t):
