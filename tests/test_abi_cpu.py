@@ -65,6 +65,11 @@ def test_host_side_validation_without_gpu(lib):
     with pytest.raises(om.OmniMoEError, match="INVALID_ARGUMENT"):  # and runs the SLICED executor only
         om.workspace_size(om.LayerDims(d=64, n_rows=4, n_cols=4, top_k=2, expert_kernel=om.EXPERT_GROUP,
                                        v_layout=om.V_SLICED), 8, om.WS_LAYER)
+    # dims.flags: OMNIMOE_FLAG_ACT_BF16 is the only defined bit
+    assert om.workspace_size(om.LayerDims(d=64, n_rows=4, n_cols=4, top_k=2, flags=om.FLAG_ACT_BF16), 8,
+                             om.WS_EXPERT) > 0
+    with pytest.raises(om.OmniMoEError, match="INVALID_ARGUMENT"):
+        om.workspace_size(om.LayerDims(d=64, n_rows=4, n_cols=4, top_k=2, flags=2), 8, om.WS_EXPERT)
 
 
 def test_product_never_imports_oracle():
