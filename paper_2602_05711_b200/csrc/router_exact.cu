@@ -793,23 +793,29 @@ omnimoe_status launch_exact_dd(int dtype, const void* x, const void* sub, int d,
   return OMNIMOE_OK;
 }
 
+// K-only part of the rule (the workspace size must not depend on the device's SM count)
+static int fused_kp_dims(const omnimoe_dims& d) {
+  if (d.dtype != OMNIMOE_BF16 || d.router != OMNIMOE_ROUTER_EXACT || d.d >= 65536) return 0;
+  const int64_t K1 = d.top_k + 1;
+  if (K1 > 32 || K1 < 9) return 0;
+  const int64_t kr1 = std::min<int64_t>(K1, d.n_rows), kc1 = std::min<int64_t>(K1, d.n_cols);
+  int64_t C = 0;
+  for (int64_t a = 1; a <= kr1; ++a) C += std::min<int64_t>(kc1, K1 / a);
+  return C <= 160 ? (int)K1 : 0;
+}
 int fused_kp(const omnimoe_dims& d, int64_t L) {
   // small K only: the per-half lists (K+1 keys) are what the warp selection kernel takes
   // (launch_select: K+1 <= 32 and <= 160 product candidates); at large K a 48-column
   // segment would keep all its keys.  And only where it pays (the C2
   // sweep, profiles/r2/n4/): K >= 8 (below, the selection it saves is cheaper than the
   // list updates) and at least ~2/3 of the SMs' worth of (128-token block, half) units
-  if (d.dtype != OMNIMOE_BF16 || d.router != OMNIMOE_ROUTER_EXACT || d.d >= 65536) return 0;
-  const int64_t K1 = d.top_k + 1;
-  if (K1 > 32 || K1 < 9 || tuning().i8_cluster > 1 || !tuning().i8_persist || !tuning().route_fused) return 0;
+  const int kp = fused_kp_dims(d);
+  if (!kp || tuning().i8_cluster > 1 || !tuning().i8_persist || !tuning().route_fused) return 0;
   if (((L + IBM - 1) / IBM) * 2 * d.n_heads * 3 < 2 * (int64_t)num_sms()) return 0;
-  const int64_t kr1 = std::min<int64_t>(K1, d.n_rows), kc1 = std::min<int64_t>(K1, d.n_cols);
-  int64_t C = 0;
-  for (int64_t a = 1; a <= kr1; ++a) C += std::min<int64_t>(kc1, K1 / a);
-  return C <= 160 ? (int)K1 : 0;
+  return kp;
 }
 size_t fused_route_bytes(const omnimoe_dims& d, int64_t L) {
-  const int kp = fused_kp(d, L);
+  const int kp = fused_kp_dims(d);  // reserved whenever K qualifies, whatever the device
   if (!kp) return 0;
   Carver c(nullptr);
   c.take<uint64_t>((size_t)std::max<int64_t>(L, 1) * 2 * d.n_heads * 2 * kp);
