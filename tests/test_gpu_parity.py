@@ -121,7 +121,7 @@ def test_route_fused_flags(h, flag_sub):
     recomputed logits, every other token from the epilogue's lists; a flagged sub-key row
     sends every token through the logits -- ids, gates and scores equal the oracle."""
     d = om.LayerDims(d=64, n_rows=16, n_cols=24, top_k=8, n_heads=h)
-    L = 6400
+    L = 6477  # a partial last 128-token block
     inp = make_inputs(d, L, 11, skip=("W", "V"))
     x, sub = inp["x"].clone(), inp["subkeys"].clone()
     x[3, 5] = 2.0 ** 12   # token 3 spans 2^12 .. 2^-15: fp64 path
