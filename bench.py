@@ -201,8 +201,8 @@ def run_reference(args, w):
     rate = statistics.mean(rates)
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * w.L / rate,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _arm_config(w, args, ws),
+            "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _arm_config(w, args, ws),
             "timing_note": ("each step times a bounded token sample of the batch on the host cores; value = "
                             "sampled tokens / oracle seconds, ms_per_step extrapolates it to the whole batch"),
             "cpu_baseline": {"value": rate, "unit": "tokens/s", "cores": nth, "kind": "oracle",
